@@ -1,0 +1,143 @@
+/* flashbutterfly.h — C ABI of the B200-native FlashButterfly long convolution
+ * (libflashbutterfly.so, built from paper_2302_06646_b200/csrc for sm_100a).
+ *
+ * This is the drop-in boundary for the reference `longconv` hot path
+ * (/root/reference/proj/include/longconv).  Each entry point names the
+ * reference interface it replaces.  Plain C: pointers, sizes, a cudaStream_t
+ * passed as void*.  No torch types.  All device pointers are caller-owned,
+ * row-major with the length dimension innermost, exactly like the
+ * reference's containers:
+ *   signals  [B][H][N]   (SignalBatch, types.hpp:37-57)
+ *   kernels  [H][N] f32, skip gains D[H] f32   (KernelBank, types.hpp:60-75)
+ *
+ * Errors: every function returns FB_OK (0) or an FB_ERR_* code and sets a
+ * thread-local message readable through fb_last_error().  The codes map to
+ * the reference exception types: FB_ERR_DIM <-> DimensionError, FB_ERR_PLAN
+ * <-> PlanError (errors.hpp:9-26).  There is no CPU fallback: a missing or
+ * failing device returns FB_ERR_CUDA.
+ *
+ * Streams: every launch is asynchronous on the given stream.  A plan may be
+ * used by one stream at a time; results are deterministic for a fixed plan
+ * (no atomics: the dK batch reduction runs in a fixed order).
+ */
+#ifndef FLASHBUTTERFLY_H
+#define FLASHBUTTERFLY_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define FB_VERSION 100
+
+enum fb_status {
+  FB_OK = 0,
+  FB_ERR_DIM = 1,   /* DimensionError (errors.hpp:10-12)                 */
+  FB_ERR_PLAN = 2,  /* PlanError (errors.hpp:15-17)                      */
+  FB_ERR_CUDA = 3,  /* device / launch failure                           */
+  FB_ERR_NCCL = 4,  /* collective failure (sequence-sharded path)        */
+  FB_ERR_ARG = 5,   /* invalid argument (null pointer, bad enum, ...)    */
+  FB_ERR_UNSUPPORTED = 6
+};
+
+/* ConvMode (butterfly.hpp:69): same numeric order as the reference enum. */
+enum fb_mode { FB_MODE_CIRCULAR = 0, FB_MODE_CAUSAL = 1 };
+
+/* Engine (regularize.hpp:17) minus kNaive (the O(N^2) oracle stays in
+ * oracle/): AUTO picks single-pass when the transform fits in shared memory. */
+enum fb_engine { FB_ENGINE_AUTO = 0, FB_ENGINE_SINGLE = 1, FB_ENGINE_THREE = 2 };
+
+/* I/O element type of u, y, dy, du. K, D, dK, dD are always f32. */
+enum fb_dtype { FB_F32 = 0, FB_BF16 = 1, FB_F16 = 2 };
+
+/* SmoothDomain (regularize.hpp:16). */
+enum fb_smooth { FB_SMOOTH_TIME = 0, FB_SMOOTH_FREQUENCY = 1 };
+
+/* RegularizationConfig (regularize.hpp:19-25). */
+typedef struct fb_reg_config {
+  double lambda;        /* soft threshold >= 0                     */
+  int64_t smooth_width; /* p; window 2p+1                          */
+  double dropout_rate;  /* in [0,1)                                */
+  int smooth_domain;    /* fb_smooth                               */
+  uint64_t seed;        /* dropout stream (SeededRng(seed).child(h)) */
+} fb_reg_config;
+
+typedef struct fb_plan fb_plan;
+
+typedef struct fb_plan_info {
+  int64_t N, H;
+  int64_t n;       /* transform length (2N causal, N circular; >= 256)  */
+  int64_t l, m;    /* three-pass split n = l*m (l = n, m = 1 single)    */
+  int engine;      /* resolved fb_engine                                */
+  int dtype, mode;
+} fb_plan_info;
+
+/* Plan for a bank of H kernels of length N.  Replaces the per-call
+ * build_plan(2N, 16) / build_three_pass(...) of regularized_long_conv
+ * (regularize.cpp:161-174, butterfly.cpp:72-118, three_pass.cpp:183-205).
+ * Allocates the per-head kernel spectrum and twiddle tables on `device`. */
+int fb_plan_create(fb_plan** plan, int64_t N, int64_t H, int mode, int dtype, int engine,
+                   int device);
+int fb_plan_destroy(fb_plan* plan);
+int fb_plan_get_info(const fb_plan* plan, fb_plan_info* info);
+
+/* Kernel preparation (K1).  Replaces regularize_bank (regularize.hpp:62-63,
+ * regularize.cpp:93-107: dropout -> smooth -> squash) fused with the kernel
+ * transform that conv_butterfly recomputes per channel (butterfly.cpp:205)
+ * and build_three_pass precomputes per head (three_pass.cpp:197-203).
+ * K: [H][N] f32 device, D: [H] f32 device.  The regularized bank Kbar is kept
+ * in the plan (fb_plan_kbar) for the backward. */
+int fb_kernel_prep(fb_plan* plan, const float* K, const float* D, const fb_reg_config* cfg,
+                   int training, void* stream);
+
+/* Device pointer to the plan's regularized kernels Kbar [H][N] f32. */
+const float* fb_plan_kbar(const fb_plan* plan);
+
+/* Scratch bytes fb_fwd / fb_bwd need for a batch of B (caller allocates). */
+size_t fb_workspace_size(const fb_plan* plan, int64_t B);
+
+/* Forward (K2 single-pass / K3 three-pass).  Replaces regularized_long_conv
+ * (regularize.hpp:67-70, regularize.cpp:149-190) after fb_kernel_prep:
+ *   y[b,h] = conv(u[b,h], Kbar[h]) + D[h] u[b,h].
+ * u, y: [B][H][N] in the plan dtype (device). */
+int fb_fwd(fb_plan* plan, const void* u, void* y, int64_t B, void* workspace, void* stream);
+
+/* Backward (K4a / K4b).  No reference counterpart (the reference is
+ * forward-only); restates the composed oracle of SURVEY.md §8c:
+ *   du = corr(dy, Kbar) + D dy,  dKbar = sum_b corr(dy, u),  dD = sum dy u,
+ *   dK = dropout'(K) * smooth(1[Kbar != 0] * dKbar)   (chain through K1).
+ * dK: [H][N] f32 (gradient w.r.t. the RAW K passed to fb_kernel_prep);
+ * dKbar (optional, may be NULL): [H][N] f32; dD: [H] f32. */
+int fb_bwd(fb_plan* plan, const void* dy, const void* u, void* du, float* dK, float* dKbar,
+           float* dD, int64_t B, void* workspace, void* stream);
+
+/* Learned butterfly (K5).  Replaces learned_forward / learned_gradients
+ * (butterfly.hpp:88-108, butterfly.cpp:221-307) batched over rows: rows
+ * [B][H] of complex length n, with per-head block parameters (one factor x
+ * factor complex matrix per stage of build_plan(n, r), concatenated; P =
+ * sum_s f_s^2 complex values per head).  Complex data is interleaved f32
+ * (re, im).  x, y, g, dx: [B][H][n] complex in the plan dtype;
+ * blocks, dblocks: [H][P] complex f32.  dblocks = sum over b (per head). */
+typedef struct fb_learned_plan fb_learned_plan;
+int fb_learned_plan_create(fb_learned_plan** plan, int64_t n, int64_t r, int64_t H, int dtype,
+                           int device);
+int fb_learned_plan_destroy(fb_learned_plan* plan);
+/* Number of stages and their factors (build_plan greedy chain,
+ * butterfly.cpp:83-100); returns P through *param_count. */
+int fb_learned_plan_factors(const fb_learned_plan* plan, int64_t* factors, int64_t* count,
+                            int64_t* param_count);
+size_t fb_learned_workspace_size(const fb_learned_plan* plan, int64_t B);
+int fb_learned_fwd(fb_learned_plan* plan, const float* blocks, const void* x, void* y, int64_t B,
+                   void* workspace, void* stream);
+int fb_learned_bwd(fb_learned_plan* plan, const float* blocks, const void* x, const void* g,
+                   void* dx, float* dblocks, int64_t B, void* workspace, void* stream);
+
+const char* fb_last_error(void);
+int fb_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* FLASHBUTTERFLY_H */

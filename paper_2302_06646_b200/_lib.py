@@ -1,0 +1,91 @@
+"""ctypes binding of the C ABI in include/flashbutterfly.h.
+
+Loads the in-tree ``libflashbutterfly.so``.  There is no fallback: if the
+library is missing or no CUDA device is present, every call raises.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from pathlib import Path
+
+LIB_PATH = Path(__file__).resolve().parent / "libflashbutterfly.so"
+
+FB_OK, FB_ERR_DIM, FB_ERR_PLAN, FB_ERR_CUDA, FB_ERR_NCCL, FB_ERR_ARG, FB_ERR_UNSUPPORTED = range(7)
+FB_MODE_CIRCULAR, FB_MODE_CAUSAL = 0, 1
+FB_ENGINE_AUTO, FB_ENGINE_SINGLE, FB_ENGINE_THREE = 0, 1, 2
+FB_F32, FB_BF16, FB_F16 = 0, 1, 2
+FB_SMOOTH_TIME, FB_SMOOTH_FREQUENCY = 0, 1
+
+# Every symbol include/flashbutterfly.h declares (tests check the export list).
+EXPORTED = [
+    "fb_plan_create", "fb_plan_destroy", "fb_plan_get_info", "fb_kernel_prep", "fb_plan_kbar",
+    "fb_workspace_size", "fb_fwd", "fb_bwd", "fb_learned_plan_create", "fb_learned_plan_destroy",
+    "fb_learned_plan_factors", "fb_learned_workspace_size", "fb_learned_fwd", "fb_learned_bwd",
+    "fb_last_error", "fb_version",
+]
+
+
+class FBError(RuntimeError):
+    def __init__(self, code: int, msg: str):
+        super().__init__(f"[fb error {code}] {msg}")
+        self.code = code
+
+
+class DimensionError(FBError, ValueError):
+    """FB_ERR_DIM — mirrors longconv::DimensionError (errors.hpp:10-12)."""
+
+
+class PlanError(FBError, ValueError):
+    """FB_ERR_PLAN — mirrors longconv::PlanError (errors.hpp:15-17)."""
+
+
+class RegConfig(C.Structure):
+    _fields_ = [("lambda_", C.c_double), ("smooth_width", C.c_int64),
+                ("dropout_rate", C.c_double), ("smooth_domain", C.c_int), ("seed", C.c_uint64)]
+
+
+class PlanInfo(C.Structure):
+    _fields_ = [("N", C.c_int64), ("H", C.c_int64), ("n", C.c_int64), ("l", C.c_int64),
+                ("m", C.c_int64), ("engine", C.c_int), ("dtype", C.c_int), ("mode", C.c_int)]
+
+
+_lib = None
+
+
+def lib() -> C.CDLL:
+    global _lib
+    if _lib is None:
+        if not LIB_PATH.exists():
+            raise FileNotFoundError(
+                f"{LIB_PATH} is missing — build it with `python -m paper_2302_06646_b200.build` "
+                "(there is no CPU fallback)")
+        L = C.CDLL(str(LIB_PATH))
+        vp, i64, sz = C.c_void_p, C.c_int64, C.c_size_t
+        L.fb_plan_create.argtypes = [C.POINTER(vp), i64, i64, C.c_int, C.c_int, C.c_int, C.c_int]
+        L.fb_plan_destroy.argtypes = [vp]
+        L.fb_plan_get_info.argtypes = [vp, C.POINTER(PlanInfo)]
+        L.fb_kernel_prep.argtypes = [vp, vp, vp, C.POINTER(RegConfig), C.c_int, vp]
+        L.fb_plan_kbar.argtypes = [vp]
+        L.fb_plan_kbar.restype = vp
+        L.fb_workspace_size.argtypes = [vp, i64]
+        L.fb_workspace_size.restype = sz
+        L.fb_fwd.argtypes = [vp, vp, vp, i64, vp, vp]
+        L.fb_bwd.argtypes = [vp, vp, vp, vp, vp, vp, vp, i64, vp, vp]
+        L.fb_learned_plan_create.argtypes = [C.POINTER(vp), i64, i64, i64, C.c_int, C.c_int]
+        L.fb_learned_plan_destroy.argtypes = [vp]
+        L.fb_learned_plan_factors.argtypes = [vp, C.POINTER(i64), C.POINTER(i64), C.POINTER(i64)]
+        L.fb_learned_workspace_size.argtypes = [vp, i64]
+        L.fb_learned_workspace_size.restype = sz
+        L.fb_learned_fwd.argtypes = [vp, vp, vp, vp, i64, vp, vp]
+        L.fb_learned_bwd.argtypes = [vp, vp, vp, vp, vp, vp, i64, vp, vp]
+        L.fb_last_error.restype = C.c_char_p
+        _lib = L
+    return _lib
+
+
+def check(rc: int) -> None:
+    if rc == FB_OK:
+        return
+    msg = lib().fb_last_error().decode()
+    cls = {FB_ERR_DIM: DimensionError, FB_ERR_PLAN: PlanError}.get(rc, FBError)
+    raise cls(rc, msg)

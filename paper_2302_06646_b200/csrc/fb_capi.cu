@@ -1,0 +1,209 @@
+// FlashButterfly-B200 C ABI (include/flashbutterfly.h): plan lifetime, engine
+// resolution, argument checking and dispatch.  No CPU compute path exists:
+// every entry point either launches sm_100a kernels or returns an error.
+#include <cmath>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "fb_internal.h"
+
+namespace fb {
+
+static thread_local std::string g_last_error;
+
+void set_error(const std::string& msg) { g_last_error = msg; }
+
+int cuda_status(cudaError_t e, const char* where) {
+  if (e == cudaSuccess) return FB_OK;
+  set_error(std::string(where) + ": " + cudaGetErrorString(e));
+  return FB_ERR_CUDA;
+}
+
+static int fail(int code, const std::string& msg) {
+  set_error(msg);
+  return code;
+}
+
+static bool is_pow2(int64_t x) { return x > 0 && (x & (x - 1)) == 0; }
+static int64_t next_pow2(int64_t x) {
+  int64_t p = 1;
+  while (p < x) p <<= 1;
+  return p;
+}
+
+// Host-side twiddle table exp(-2 pi i t / n), computed in fp64 then rounded.
+static int upload_twiddles(float2** dst, int64_t n) {
+  std::vector<float2> h((size_t)n);
+  for (int64_t t = 0; t < n; ++t) {
+    const double a = -2.0 * M_PI * (double)t / (double)n;
+    h[(size_t)t] = make_float2((float)std::cos(a), (float)std::sin(a));
+  }
+  int rc = cuda_status(cudaMalloc(dst, sizeof(float2) * n), "cudaMalloc(twiddles)");
+  if (rc) return rc;
+  return cuda_status(cudaMemcpy(*dst, h.data(), sizeof(float2) * n, cudaMemcpyHostToDevice),
+                     "cudaMemcpy(twiddles)");
+}
+
+constexpr int64_t kSinglePassMax = 8192;   // fp32 complex transform in smem
+constexpr int64_t kThreePassRow = 8192;    // l: row length of pass 2
+constexpr int64_t kMinTransform = 256;
+
+}  // namespace fb
+
+using namespace fb;
+
+extern "C" {
+
+const char* fb_last_error(void) { return g_last_error.c_str(); }
+int fb_version(void) { return FB_VERSION; }
+
+int fb_plan_create(fb_plan** out, int64_t N, int64_t H, int mode, int dtype, int engine,
+                   int device) {
+  if (!out) return fail(FB_ERR_ARG, "fb_plan_create: null output pointer");
+  *out = nullptr;
+  if (N < 1 || H < 1) return fail(FB_ERR_DIM, "fb_plan_create: N and H must be >= 1");
+  if (mode != FB_MODE_CAUSAL && mode != FB_MODE_CIRCULAR)
+    return fail(FB_ERR_ARG, "fb_plan_create: bad mode");
+  if (dtype < FB_F32 || dtype > FB_F16) return fail(FB_ERR_ARG, "fb_plan_create: bad dtype");
+  if (engine < FB_ENGINE_AUTO || engine > FB_ENGINE_THREE)
+    return fail(FB_ERR_ARG, "fb_plan_create: bad engine");
+  if (mode == FB_MODE_CIRCULAR && !is_pow2(N))
+    return fail(FB_ERR_PLAN, "fb_plan_create: circular mode needs a power-of-two N "
+                             "(causal mode accepts any N; pad the input)");
+  int rc = cuda_status(cudaSetDevice(device), "cudaSetDevice");
+  if (rc) return rc;
+  fb_plan* p = new fb_plan();
+  p->N = N;
+  p->H = H;
+  p->mode = mode;
+  p->dtype = dtype;
+  p->device = device;
+  int64_t n = mode == FB_MODE_CAUSAL ? next_pow2(2 * N) : N;
+  if (n < kMinTransform) n = kMinTransform;
+  p->n = n;
+  p->periodic = (mode == FB_MODE_CIRCULAR) && n > N;
+  if (engine == FB_ENGINE_AUTO) engine = n <= kSinglePassMax ? FB_ENGINE_SINGLE : FB_ENGINE_THREE;
+  if (engine == FB_ENGINE_SINGLE && n > kSinglePassMax) {
+    delete p;
+    return fail(FB_ERR_PLAN, "fb_plan_create: single-pass engine supports transforms up to " +
+                                 std::to_string(kSinglePassMax) + " points; use three-pass");
+  }
+  p->engine = engine;
+  if (engine == FB_ENGINE_THREE) {
+    p->l = std::min<int64_t>(n, kThreePassRow);
+    p->m = n / p->l;
+  } else {
+    p->l = n;
+    p->m = 1;
+  }
+  cudaDeviceGetAttribute(&p->num_sms, cudaDevAttrMultiProcessorCount, device);
+  rc = upload_twiddles(&p->tw_n, n);
+  if (!rc && engine == FB_ENGINE_THREE) rc = upload_twiddles(&p->tw_l, p->l);
+  if (!rc && engine == FB_ENGINE_THREE) rc = upload_twiddles(&p->tw_m, std::max<int64_t>(p->m, 2));
+  if (!rc) rc = cuda_status(cudaMalloc(&p->kf, sizeof(float2) * H * n), "cudaMalloc(kf)");
+  if (!rc) rc = cuda_status(cudaMalloc(&p->kbar, sizeof(float) * H * N), "cudaMalloc(kbar)");
+  if (!rc) rc = cuda_status(cudaMalloc(&p->d, sizeof(float) * H), "cudaMalloc(D)");
+  if (rc) {
+    fb_plan_destroy(p);
+    return rc;
+  }
+  *out = p;
+  return FB_OK;
+}
+
+int fb_plan_destroy(fb_plan* p) {
+  if (!p) return FB_OK;
+  cudaFree(p->tw_n);
+  cudaFree(p->tw_l);
+  cudaFree(p->tw_m);
+  cudaFree(p->kf);
+  cudaFree(p->kbar);
+  cudaFree(p->keep);
+  cudaFree(p->d);
+  delete p;
+  return FB_OK;
+}
+
+int fb_plan_get_info(const fb_plan* p, fb_plan_info* info) {
+  if (!p || !info) return fail(FB_ERR_ARG, "fb_plan_get_info: null argument");
+  info->N = p->N;
+  info->H = p->H;
+  info->n = p->n;
+  info->l = p->l;
+  info->m = p->m;
+  info->engine = p->engine;
+  info->dtype = p->dtype;
+  info->mode = p->mode;
+  return FB_OK;
+}
+
+const float* fb_plan_kbar(const fb_plan* p) { return p ? p->kbar : nullptr; }
+
+int fb_kernel_prep(fb_plan* p, const float* K, const float* D, const fb_reg_config* cfg,
+                   int training, void* stream) {
+  if (!p || !K || !D || !cfg) return fail(FB_ERR_ARG, "fb_kernel_prep: null argument");
+  if (cfg->lambda < 0.0) return fail(FB_ERR_DIM, "squash: lambda must be >= 0");
+  if (cfg->dropout_rate < 0.0 || cfg->dropout_rate >= 1.0)
+    return fail(FB_ERR_DIM, "kernel_dropout: rate must be in [0, 1)");
+  if (cfg->smooth_width < 0) return fail(FB_ERR_DIM, "smooth: width must be >= 0");
+  if (cfg->smooth_domain != FB_SMOOTH_TIME && cfg->smooth_domain != FB_SMOOTH_FREQUENCY)
+    return fail(FB_ERR_ARG, "fb_kernel_prep: bad smooth domain");
+  cudaStream_t s = (cudaStream_t)stream;
+  int rc = cuda_status(cudaSetDevice(p->device), "cudaSetDevice");
+  if (rc) return rc;
+  p->lambda = cfg->lambda;
+  p->p = cfg->smooth_width;
+  p->smooth_domain = cfg->smooth_domain;
+  p->use_keep = training && cfg->dropout_rate > 0.0;
+  p->keep_scale = 1.0 / (1.0 - cfg->dropout_rate);
+  if (p->use_keep) {
+    if (!p->keep) {
+      rc = cuda_status(cudaMalloc(&p->keep, (size_t)p->H * p->N), "cudaMalloc(keep)");
+      if (rc) return rc;
+    }
+    rc = dropout_keep_dev(p, cfg->dropout_rate, cfg->seed, s);
+    if (rc) return rc;
+  }
+  rc = cuda_status(cudaMemcpyAsync(p->d, D, sizeof(float) * p->H, cudaMemcpyDeviceToDevice, s),
+                   "copy D");
+  if (rc) return rc;
+  rc = p->engine == FB_ENGINE_SINGLE ? sp_prep(p, K, s) : tp_prep(p, K, s);
+  if (rc) return rc;
+  p->prepared = true;
+  return FB_OK;
+}
+
+size_t fb_workspace_size(const fb_plan* p, int64_t B) {
+  if (!p || B < 1) return 0;
+  return p->engine == FB_ENGINE_SINGLE ? sp_workspace(p, B) : tp_workspace(p, B);
+}
+
+static int check_run(const fb_plan* p, int64_t B, const char* who) {
+  if (!p) return fail(FB_ERR_ARG, std::string(who) + ": null plan");
+  if (!p->prepared) return fail(FB_ERR_ARG, std::string(who) + ": call fb_kernel_prep first");
+  if (B < 1) return fail(FB_ERR_DIM, std::string(who) + ": batch must be >= 1");
+  if (B > 65535 * 2) return fail(FB_ERR_DIM, std::string(who) + ": batch too large");
+  return cuda_status(cudaSetDevice(p->device), "cudaSetDevice");
+}
+
+int fb_fwd(fb_plan* p, const void* u, void* y, int64_t B, void* ws, void* stream) {
+  int rc = check_run(p, B, "fb_fwd");
+  if (rc) return rc;
+  if (!u || !y) return fail(FB_ERR_ARG, "fb_fwd: null tensor");
+  if (p->engine == FB_ENGINE_THREE && !ws) return fail(FB_ERR_ARG, "fb_fwd: workspace required");
+  cudaStream_t s = (cudaStream_t)stream;
+  return p->engine == FB_ENGINE_SINGLE ? sp_fwd(p, u, y, B, s) : tp_fwd(p, u, y, B, ws, s);
+}
+
+int fb_bwd(fb_plan* p, const void* dy, const void* u, void* du, float* dK, float* dKbar,
+           float* dD, int64_t B, void* ws, void* stream) {
+  int rc = check_run(p, B, "fb_bwd");
+  if (rc) return rc;
+  if (!dy || !u || !du || !dK || !dD || !ws) return fail(FB_ERR_ARG, "fb_bwd: null argument");
+  cudaStream_t s = (cudaStream_t)stream;
+  return p->engine == FB_ENGINE_SINGLE ? sp_bwd(p, dy, u, du, dK, dKbar, dD, B, ws, s)
+                                       : tp_bwd(p, dy, u, du, dK, dKbar, dD, B, ws, s);
+}
+
+}  // extern "C"

@@ -1,0 +1,69 @@
+// FlashButterfly-B200: host-side plan object and internal launcher API.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+
+#include "../../include/flashbutterfly.h"
+
+struct fb_plan {
+  int64_t N = 0, H = 0;
+  int64_t n = 0;       // transform length
+  int64_t l = 0, m = 1;  // three-pass split (single: l = n, m = 1)
+  int mode = FB_MODE_CAUSAL, dtype = FB_F32, engine = FB_ENGINE_SINGLE, device = 0;
+  bool periodic = false;  // circular with n > N: u periodically extended
+  float2* tw_n = nullptr;  // exp(-2 pi i t / n), t < n
+  float2* tw_l = nullptr;  // exp(-2 pi i t / l), t < l   (three-pass)
+  float2* tw_m = nullptr;  // exp(-2 pi i t / m), t < m   (three-pass)
+  float2* kf = nullptr;    // per-head spectrum / n: single [H][n]; three [H][m][l]
+  float* kbar = nullptr;   // [H][N] regularized kernels
+  uint8_t* keep = nullptr; // [H][N] dropout keep flags (training only)
+  float* d = nullptr;      // [H] skip gains
+  bool prepared = false;
+  bool use_keep = false;
+  double lambda = 0.0, keep_scale = 1.0;
+  int64_t p = 0;
+  int smooth_domain = FB_SMOOTH_TIME;
+  int num_sms = 148;
+};
+
+struct fb_learned_plan {
+  int64_t n = 0, r = 0, H = 0;
+  int dtype = FB_F32, device = 0;
+  int nstages = 0;
+  int64_t factors[32] = {0};
+  int64_t param_count = 0;
+};
+
+namespace fb {
+void set_error(const std::string& msg);
+int cuda_status(cudaError_t e, const char* where);
+
+// single-pass (fb_single.cu)
+int sp_prep(fb_plan* p, const float* K, cudaStream_t s);
+int sp_fwd(fb_plan* p, const void* u, void* y, int64_t B, cudaStream_t s);
+size_t sp_workspace(const fb_plan* p, int64_t B);
+int sp_bwd(fb_plan* p, const void* dy, const void* u, void* du, float* dK, float* dKbar, float* dD,
+           int64_t B, void* ws, cudaStream_t s);
+
+// three-pass (fb_three.cu)
+int tp_prep(fb_plan* p, const float* K, cudaStream_t s);
+int tp_fwd(fb_plan* p, const void* u, void* y, int64_t B, void* ws, cudaStream_t s);
+size_t tp_workspace(const fb_plan* p, int64_t B);
+int tp_bwd(fb_plan* p, const void* dy, const void* u, void* du, float* dK, float* dKbar, float* dD,
+           int64_t B, void* ws, cudaStream_t s);
+
+// shared K1 pieces (fb_prep.cu)
+int regularize_bank_dev(fb_plan* p, const float* K, cudaStream_t s);
+int dropout_keep_dev(fb_plan* p, double rate, uint64_t seed, cudaStream_t s);
+// dK = chain(dKbar) through dropout/smooth/squash, per head; dkbar_in [H][N]
+int regularizer_backward_dev(fb_plan* p, const float* dkbar, float* dK, cudaStream_t s);
+
+// learned (fb_learned.cu)
+size_t lb_workspace(const fb_learned_plan* p, int64_t B);
+int lb_fwd(fb_learned_plan* p, const float* blocks, const void* x, void* y, int64_t B, void* ws,
+           cudaStream_t s);
+int lb_bwd(fb_learned_plan* p, const float* blocks, const void* x, const void* g, void* dx,
+           float* dblocks, int64_t B, void* ws, cudaStream_t s);
+}  // namespace fb

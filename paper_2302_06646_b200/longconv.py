@@ -1,0 +1,240 @@
+"""Host-side mirror of the reference ``longconv`` layer API on top of the C ABI.
+
+Names, argument meaning and error behaviour follow
+/root/reference/proj/include/longconv/regularize.hpp and butterfly.hpp:
+
+* :class:`RegularizationConfig`  <- ``RegularizationConfig`` (regularize.hpp:19-25)
+* :class:`Engine`, :class:`ConvMode`, :class:`SmoothDomain` <- the reference enums
+* :func:`regularized_long_conv`  <- ``regularized_long_conv`` (regularize.hpp:67-70)
+* :func:`regularized_long_conv_backward` — the backward the reference lacks
+* :func:`long_conv`              — differentiable (torch.autograd) form
+* :class:`LongConvPlan`          — explicit plan handle (``fb_plan``)
+
+Tensors are torch CUDA tensors laid out like ``SignalBatch`` [B, H, N] and
+``KernelBank`` ([H, N] kernels + [H] skip gains).  All compute happens in
+libflashbutterfly.so on the current CUDA stream; there is no CPU path.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import enum
+from dataclasses import dataclass
+
+import torch
+
+from . import _lib
+from ._lib import DimensionError, FBError, PlanError, check  # noqa: F401 (re-export)
+
+
+class Engine(enum.IntEnum):
+    """Execution path (regularize.hpp:17).  kNaive stays in the CPU oracle;
+    AUTO picks single-pass when the transform fits in shared memory."""
+
+    AUTO = _lib.FB_ENGINE_AUTO
+    BUTTERFLY = _lib.FB_ENGINE_SINGLE  # single-pass fused kernel
+    THREE_PASS = _lib.FB_ENGINE_THREE
+
+
+class ConvMode(enum.IntEnum):  # butterfly.hpp:69
+    CIRCULAR = _lib.FB_MODE_CIRCULAR
+    CAUSAL = _lib.FB_MODE_CAUSAL
+
+
+class SmoothDomain(enum.IntEnum):  # regularize.hpp:16
+    TIME = _lib.FB_SMOOTH_TIME
+    FREQUENCY = _lib.FB_SMOOTH_FREQUENCY
+
+
+@dataclass(frozen=True)
+class RegularizationConfig:  # regularize.hpp:19-25
+    lambda_: float = 0.0
+    smooth_width: int = 0
+    dropout_rate: float = 0.0
+    smooth_domain: SmoothDomain = SmoothDomain.TIME
+    seed: int = 0
+
+    def to_c(self) -> _lib.RegConfig:
+        return _lib.RegConfig(float(self.lambda_), int(self.smooth_width), float(self.dropout_rate),
+                              int(self.smooth_domain), int(self.seed) & (2**64 - 1))
+
+
+_DT = {torch.float32: _lib.FB_F32, torch.bfloat16: _lib.FB_BF16, torch.float16: _lib.FB_F16}
+
+
+def _stream() -> C.c_void_p:
+    return C.c_void_p(torch.cuda.current_stream().cuda_stream)
+
+
+def _ptr(t: torch.Tensor | None):
+    return C.c_void_p(t.data_ptr()) if t is not None else C.c_void_p(0)
+
+
+class LongConvPlan:
+    """Owns an ``fb_plan``: per-head spectra, twiddles and the regularized bank."""
+
+    def __init__(self, N: int, H: int, mode: ConvMode = ConvMode.CAUSAL,
+                 dtype: torch.dtype = torch.float32, engine: Engine = Engine.AUTO,
+                 device: int | torch.device | None = None):
+        if dtype not in _DT:
+            raise TypeError(f"unsupported I/O dtype {dtype}")
+        dev = torch.device("cuda", torch.cuda.current_device()) if device is None else torch.device(device)
+        if dev.type != "cuda":
+            raise RuntimeError("LongConvPlan needs a CUDA device (no CPU fallback)")
+        self.N, self.H, self.mode, self.dtype = int(N), int(H), ConvMode(mode), dtype
+        self.device = dev
+        h = C.c_void_p()
+        with torch.cuda.device(dev):
+            check(_lib.lib().fb_plan_create(C.byref(h), self.N, self.H, int(mode), _DT[dtype],
+                                            int(engine), dev.index or 0))
+        self._h = h
+        info = _lib.PlanInfo()
+        check(_lib.lib().fb_plan_get_info(h, C.byref(info)))
+        self.n, self.l, self.m, self.engine = info.n, info.l, info.m, Engine(info.engine)
+        self._token = None
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h is not None and h.value:
+            try:
+                _lib.lib().fb_plan_destroy(h)
+            except Exception:
+                pass
+            self._h = None
+
+    # -- K1 ------------------------------------------------------------------
+    def prep(self, K: torch.Tensor, D: torch.Tensor, cfg: RegularizationConfig,
+             training: bool = False) -> None:
+        """regularize_bank + kernel spectrum (fb_kernel_prep)."""
+        if K.shape != (self.H, self.N) or D.shape != (self.H,):
+            raise DimensionError(_lib.FB_ERR_DIM, "regularized_long_conv: bank dimensions must "
+                                                  "match the batch")
+        K = K.detach().to(self.device, torch.float32).contiguous()
+        D = D.detach().to(self.device, torch.float32).contiguous()
+        c = cfg.to_c()
+        check(_lib.lib().fb_kernel_prep(self._h, _ptr(K), _ptr(D), C.byref(c), int(training),
+                                        _stream()))
+        self._token = (K.data_ptr(), K._version, cfg, bool(training))
+        self._keep = (K, D)
+
+    def kbar(self) -> torch.Tensor:
+        """Copy of the plan's regularized bank Kbar [H, N] (fp32)."""
+        ptr = _lib.lib().fb_plan_kbar(self._h)
+        out = torch.empty(self.H, self.N, dtype=torch.float32, device=self.device)
+        torch.cuda.synchronize(self.device)
+        _copy_from_ptr(out, ptr)
+        return out
+
+    def workspace(self, B: int) -> torch.Tensor:
+        nbytes = _lib.lib().fb_workspace_size(self._h, int(B))
+        return torch.empty(max(int(nbytes), 1), dtype=torch.uint8, device=self.device)
+
+    def _check_signal(self, x: torch.Tensor, name: str) -> int:
+        if x.dim() != 3 or x.shape[1] != self.H or x.shape[2] != self.N:
+            raise DimensionError(_lib.FB_ERR_DIM, f"{name}: expected [B, {self.H}, {self.N}], "
+                                                  f"got {list(x.shape)}")
+        if x.dtype != self.dtype or x.device != self.device or not x.is_contiguous():
+            raise TypeError(f"{name}: expected contiguous {self.dtype} on {self.device}")
+        return x.shape[0]
+
+    # -- K2/K3 ------------------------------------------------------------------
+    def forward(self, u: torch.Tensor, out: torch.Tensor | None = None,
+                workspace: torch.Tensor | None = None) -> torch.Tensor:
+        B = self._check_signal(u, "u")
+        y = torch.empty_like(u) if out is None else out
+        ws = self.workspace(B) if workspace is None else workspace
+        check(_lib.lib().fb_fwd(self._h, _ptr(u), _ptr(y), B, _ptr(ws), _stream()))
+        return y
+
+    # -- K4 ------------------------------------------------------------------
+    def backward(self, dy: torch.Tensor, u: torch.Tensor, want_dkbar: bool = False,
+                 workspace: torch.Tensor | None = None):
+        """-> (du, dK, dD[, dKbar]); dK w.r.t. the raw K given to prep()."""
+        B = self._check_signal(dy, "dy")
+        if self._check_signal(u, "u") != B:
+            raise DimensionError(_lib.FB_ERR_DIM, "backward: dy and u batch mismatch")
+        du = torch.empty_like(u)
+        dK = torch.empty(self.H, self.N, dtype=torch.float32, device=self.device)
+        dD = torch.empty(self.H, dtype=torch.float32, device=self.device)
+        dKbar = torch.empty_like(dK) if want_dkbar else None
+        ws = self.workspace(B) if workspace is None else workspace
+        check(_lib.lib().fb_bwd(self._h, _ptr(dy), _ptr(u), _ptr(du), _ptr(dK), _ptr(dKbar),
+                                _ptr(dD), B, _ptr(ws), _stream()))
+        return (du, dK, dD, dKbar) if want_dkbar else (du, dK, dD)
+
+
+def _copy_from_ptr(out: torch.Tensor, ptr: int) -> None:
+    """Device-to-device copy from a raw device pointer into ``out``."""
+    cudart = torch.cuda.cudart()
+    nbytes = out.numel() * out.element_size()
+    res = cudart.cudaMemcpy(out.data_ptr(), ptr, nbytes, 3)  # cudaMemcpyDeviceToDevice
+    if int(res) != 0:
+        raise FBError(_lib.FB_ERR_CUDA, f"cudaMemcpy failed ({res})")
+
+
+_PLANS: dict = {}
+
+
+def get_plan(N: int, H: int, mode: ConvMode, dtype: torch.dtype, engine: Engine,
+             device: torch.device) -> LongConvPlan:
+    key = (N, H, int(mode), dtype, int(engine), str(device))
+    p = _PLANS.get(key)
+    if p is None:
+        p = LongConvPlan(N, H, mode, dtype, engine, device)
+        _PLANS[key] = p
+    return p
+
+
+def regularized_long_conv(u: torch.Tensor, K: torch.Tensor, D: torch.Tensor,
+                          cfg: RegularizationConfig = RegularizationConfig(),
+                          engine: Engine = Engine.AUTO, mode: ConvMode = ConvMode.CAUSAL,
+                          training: bool = False) -> torch.Tensor:
+    """y[b,h] = conv(u[b,h], regularize(K)[h]) + D[h] u[b,h] (regularize.hpp:67-70).
+    ``threads`` of the reference has no meaning here (the grid is the parallelism)."""
+    if u.dim() != 3:
+        raise DimensionError(_lib.FB_ERR_DIM, "regularized_long_conv: u must be [B, H, N]")
+    B, H, N = u.shape
+    plan = get_plan(N, H, mode, u.dtype, engine, u.device)
+    plan.prep(K, D, cfg, training)
+    return plan.forward(u.contiguous())
+
+
+def regularized_long_conv_backward(dy: torch.Tensor, u: torch.Tensor, K: torch.Tensor,
+                                   D: torch.Tensor,
+                                   cfg: RegularizationConfig = RegularizationConfig(),
+                                   engine: Engine = Engine.AUTO,
+                                   mode: ConvMode = ConvMode.CAUSAL, training: bool = False,
+                                   want_dkbar: bool = False):
+    """(du, dK, dD[, dKbar]) for the layer above (SURVEY.md §8c formulas)."""
+    B, H, N = u.shape
+    plan = get_plan(N, H, mode, u.dtype, engine, u.device)
+    plan.prep(K, D, cfg, training)
+    return plan.backward(dy.contiguous(), u.contiguous(), want_dkbar)
+
+
+class _LongConvFn(torch.autograd.Function):
+    @staticmethod
+    def forward(ctx, u, K, D, cfg, engine, mode, training):
+        B, H, N = u.shape
+        plan = get_plan(N, H, mode, u.dtype, engine, u.device)
+        plan.prep(K, D, cfg, training)
+        y = plan.forward(u.contiguous())
+        ctx.save_for_backward(u, K, D)
+        ctx.cfg, ctx.plan, ctx.training = cfg, plan, training
+        ctx.token = plan._token
+        return y
+
+    @staticmethod
+    def backward(ctx, dy):
+        u, K, D = ctx.saved_tensors
+        plan = ctx.plan
+        if plan._token != ctx.token:  # plan re-prepared by another call meanwhile
+            plan.prep(K, D, ctx.cfg, ctx.training)
+        du, dK, dD = plan.backward(dy.contiguous().to(u.dtype), u.contiguous())
+        return du, dK.to(K.dtype), dD.to(D.dtype), None, None, None, None
+
+
+def long_conv(u: torch.Tensor, K: torch.Tensor, D: torch.Tensor,
+              cfg: RegularizationConfig = RegularizationConfig(), engine: Engine = Engine.AUTO,
+              mode: ConvMode = ConvMode.CAUSAL, training: bool = False) -> torch.Tensor:
+    """Differentiable regularized long convolution (Algorithm 1)."""
+    return _LongConvFn.apply(u, K, D, cfg, engine, mode, training)

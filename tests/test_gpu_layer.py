@@ -1,0 +1,163 @@
+"""GPU parity of the layer (K1 + K2/K3 forward, K4 backward) through the C ABI
+against the fp64 oracle (oracle/lc_oracle.c, pinned to the reference) and
+the reference-generated golden fixtures.
+
+Bars (BASELINE.json north_star): relative L2 <= 1e-5 in fp32 mode,
+<= 2e-2 in bf16/fp16 tensor mode, for y, du, dK (and dD)."""
+import numpy as np
+import pytest
+import torch
+
+from conftest import golden
+from helpers import TOL, layer_inputs, rounded, to_np
+from oracle.oracle import rel_l2
+
+pytestmark = pytest.mark.gpu
+
+fb = pytest.importorskip("paper_2302_06646_b200")
+
+
+def run_layer(inp, N, H, dtype, cfg, mode=1, engine=0, training=False):
+    plan = fb.LongConvPlan(N, H, fb.ConvMode(mode), dtype, fb.Engine(engine))
+    plan.prep(inp["tK"], inp["tD"], cfg, training)
+    y = plan.forward(inp["tu"])
+    du, dK, dD, dKbar = plan.backward(inp["tdy"], inp["tu"], want_dkbar=True)
+    torch.cuda.synchronize()
+    return plan, dict(y=to_np(y), du=to_np(du), dK=to_np(dK), dD=to_np(dD), dKbar=to_np(dKbar),
+                      kbar=to_np(plan.kbar()))
+
+
+def oracle_layer(lc, inp, cfg, causal=True, training=False):
+    lam, p = cfg.lambda_, cfg.smooth_width
+    Kbar = lc.regularize_bank(inp["K"], lam, p, cfg.dropout_rate, int(cfg.smooth_domain), cfg.seed,
+                              training)
+    y = lc.long_conv_forward(inp["u"], Kbar, inp["D"], causal)
+    du, dKbar, dD = lc.long_conv_backward(inp["u"], inp["dy"], Kbar, inp["D"], causal)
+    if cfg.smooth_domain == 0:
+        dK = lc.regularizer_backward(inp["K"], lam, p, dKbar, cfg.dropout_rate, cfg.seed, training)
+    else:
+        dK = None
+    return dict(y=y, du=du, dK=dK, dD=dD, dKbar=dKbar, kbar=Kbar)
+
+
+def assert_parity(got, want, tol, keys=("y", "du", "dK", "dD", "dKbar", "kbar")):
+    errs = {k: rel_l2(got[k], want[k]) for k in keys if want.get(k) is not None}
+    assert all(e <= tol for e in errs.values()), errs
+    return errs
+
+
+CFG = dict(lambda_=0.003, smooth_width=1)
+
+
+@pytest.mark.parametrize("dtype", [torch.float32, torch.bfloat16, torch.float16])
+def test_config1_single_channel(lc, dtype):
+    # BASELINE config 1: B=1 H=1 N=1024 causal fwd+bwd vs the CPU oracle
+    inp = layer_inputs(lc, 1, 1, 1024, dtype)
+    cfg = fb.RegularizationConfig(**CFG)
+    _, got = run_layer(inp, 1024, 1, dtype, cfg)
+    assert_parity(got, oracle_layer(lc, inp, cfg), TOL[dtype])
+
+
+@pytest.mark.parametrize("B,H,N", [(2, 3, 128), (3, 4, 256), (4, 2, 1000), (2, 2, 4096),
+                                   (5, 3, 64), (1, 2, 4), (2, 1, 1)])
+def test_single_pass_shapes_fp32(lc, B, H, N):
+    inp = layer_inputs(lc, B, H, N, torch.float32)
+    cfg = fb.RegularizationConfig(**CFG)
+    _, got = run_layer(inp, N, H, torch.float32, cfg, engine=1)
+    assert_parity(got, oracle_layer(lc, inp, cfg), 1e-5)
+
+
+@pytest.mark.parametrize("N", [8, 64, 256, 1024])
+def test_circular_mode_fp32(lc, N):
+    inp = layer_inputs(lc, 3, 2, N, torch.float32)
+    cfg = fb.RegularizationConfig(**CFG)
+    _, got = run_layer(inp, N, 2, torch.float32, cfg, mode=0)
+    assert_parity(got, oracle_layer(lc, inp, cfg, causal=False), 1e-5)
+
+
+def test_dropout_training_mode(lc):
+    # on-device xoshiro256++ stream must reproduce the reference mask exactly
+    inp = layer_inputs(lc, 2, 3, 512, torch.float32)
+    cfg = fb.RegularizationConfig(lambda_=0.003, smooth_width=1, dropout_rate=0.2, seed=7)
+    _, got = run_layer(inp, 512, 3, torch.float32, cfg, training=True)
+    want = oracle_layer(lc, inp, cfg, training=True)
+    assert np.array_equal(got["kbar"] == 0, want["kbar"] == 0)
+    assert_parity(got, want, 1e-5)
+
+
+def test_smooth_frequency(lc):
+    inp = layer_inputs(lc, 2, 2, 256, torch.float32)
+    cfg = fb.RegularizationConfig(lambda_=0.01, smooth_width=2,
+                                  smooth_domain=fb.SmoothDomain.FREQUENCY)
+    _, got = run_layer(inp, 256, 2, torch.float32, cfg)
+    want = oracle_layer(lc, inp, cfg)
+    assert_parity(got, want, 1e-5, keys=("y", "du", "dD", "dKbar", "kbar"))
+    # chain rule: smooth_frequency(k) = k * w (Dirichlet window) is self-adjoint
+    t = np.arange(256)
+    w = (1 + 2 * sum(np.cos(2 * np.pi * d * t / 256) for d in (1, 2))) / 5
+    dK = (want["kbar"] != 0) * want["dKbar"] * w
+    assert rel_l2(got["dK"], dK) < 1e-5
+
+
+@pytest.mark.parametrize("name", ["layer_b1h1n1024", "layer_b3h4n256", "layer_b2h2n128_circ",
+                                  "layer_b2h3n64_drop"])
+def test_against_reference_golden(name):
+    """Directly against outputs of the unmodified reference (tests/golden)."""
+    g = golden(name)
+    causal, training = bool(g["causal"]), bool(g["training"])
+    B, H, N = g["u"].shape
+    cfg = fb.RegularizationConfig(lambda_=float(g["lam"]), smooth_width=int(g["p"]),
+                                  dropout_rate=float(g["rate"]), seed=int(g["seed"]))
+    # fp32 inputs: compare against the reference evaluated on fp64 inputs,
+    # so the bar absorbs the input rounding (rel ~6e-8)
+    inp = dict(tu=torch.tensor(g["u"], dtype=torch.float32).cuda(),
+               tdy=torch.tensor(g["dy"], dtype=torch.float32).cuda(),
+               tK=torch.tensor(g["K"], dtype=torch.float32).cuda(),
+               tD=torch.tensor(g["D"], dtype=torch.float32).cuda())
+    _, got = run_layer(inp, N, H, torch.float32, cfg, mode=int(causal), training=training)
+    assert rel_l2(got["y"], g["y_engine1"]) < 1e-5
+    if causal:
+        for k in ("du", "dK", "dD"):
+            assert rel_l2(got[k], g[k]) < 1e-5, k
+
+
+@pytest.mark.parametrize("dtype", [torch.float32, torch.bfloat16])
+def test_deterministic(lc, dtype):
+    inp = layer_inputs(lc, 6, 4, 2048, dtype)
+    cfg = fb.RegularizationConfig(**CFG)
+    _, a = run_layer(inp, 2048, 4, dtype, cfg)
+    _, b = run_layer(inp, 2048, 4, dtype, cfg)
+    for k in a:
+        assert np.array_equal(a[k], b[k]), k
+
+
+def test_autograd_long_conv(lc):
+    B, H, N = 2, 3, 512
+    inp = layer_inputs(lc, B, H, N, torch.float32)
+    u = inp["tu"].clone().requires_grad_(True)
+    K = inp["tK"].clone().requires_grad_(True)
+    D = inp["tD"].clone().requires_grad_(True)
+    cfg = fb.RegularizationConfig(**CFG)
+    y = fb.long_conv(u, K, D, cfg)
+    y.backward(inp["tdy"])
+    want = oracle_layer(lc, inp, cfg)
+    assert rel_l2(to_np(y), want["y"]) < 1e-5
+    assert rel_l2(to_np(u.grad), want["du"]) < 1e-5
+    assert rel_l2(to_np(K.grad), want["dK"]) < 1e-5
+    assert rel_l2(to_np(D.grad), want["dD"]) < 1e-5
+
+
+def test_dimension_errors():
+    with pytest.raises(fb.DimensionError):
+        plan = fb.LongConvPlan(64, 2)
+        plan.prep(torch.zeros(3, 64, device="cuda"), torch.zeros(3, device="cuda"),
+                  fb.RegularizationConfig())
+    plan = fb.LongConvPlan(64, 2)
+    plan.prep(torch.zeros(2, 64, device="cuda"), torch.zeros(2, device="cuda"),
+              fb.RegularizationConfig())
+    with pytest.raises(fb.DimensionError):
+        plan.forward(torch.zeros(1, 3, 64, device="cuda"))
+    with pytest.raises(fb.DimensionError):
+        fb.LongConvPlan(64, 2).prep(torch.zeros(2, 64, device="cuda"),
+                                    torch.zeros(2, device="cuda"),
+                                    fb.RegularizationConfig(lambda_=-1.0))
