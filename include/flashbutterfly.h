@@ -88,12 +88,13 @@ int fb_plan_get_info(const fb_plan* plan, fb_plan_info* info);
  * transform that conv_butterfly recomputes per channel (butterfly.cpp:205)
  * and build_three_pass precomputes per head (three_pass.cpp:197-203).
  * K: [H][N] f32 device, D: [H] f32 device.  The regularized bank Kbar is kept
- * in the plan (fb_plan_kbar) for the backward. */
+ * in the plan (fb_plan_copy_kbar) for the backward. */
 int fb_kernel_prep(fb_plan* plan, const float* K, const float* D, const fb_reg_config* cfg,
                    int training, void* stream);
 
-/* Device pointer to the plan's regularized kernels Kbar [H][N] f32. */
-const float* fb_plan_kbar(const fb_plan* plan);
+/* Copy the plan's regularized kernels Kbar [H][N] f32 into dst (device),
+ * stream-ordered after fb_kernel_prep. */
+int fb_plan_copy_kbar(const fb_plan* plan, float* dst, void* stream);
 
 /* Scratch bytes fb_fwd / fb_bwd need for a batch of B (caller allocates). */
 size_t fb_workspace_size(const fb_plan* plan, int64_t B);

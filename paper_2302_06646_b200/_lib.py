@@ -18,7 +18,7 @@ FB_SMOOTH_TIME, FB_SMOOTH_FREQUENCY = 0, 1
 
 # Every symbol include/flashbutterfly.h declares (tests check the export list).
 EXPORTED = [
-    "fb_plan_create", "fb_plan_destroy", "fb_plan_get_info", "fb_kernel_prep", "fb_plan_kbar",
+    "fb_plan_create", "fb_plan_destroy", "fb_plan_get_info", "fb_kernel_prep", "fb_plan_copy_kbar",
     "fb_workspace_size", "fb_fwd", "fb_bwd", "fb_learned_plan_create", "fb_learned_plan_destroy",
     "fb_learned_plan_factors", "fb_learned_workspace_size", "fb_learned_fwd", "fb_learned_bwd",
     "fb_last_error", "fb_version",
@@ -65,8 +65,7 @@ def lib() -> C.CDLL:
         L.fb_plan_destroy.argtypes = [vp]
         L.fb_plan_get_info.argtypes = [vp, C.POINTER(PlanInfo)]
         L.fb_kernel_prep.argtypes = [vp, vp, vp, C.POINTER(RegConfig), C.c_int, vp]
-        L.fb_plan_kbar.argtypes = [vp]
-        L.fb_plan_kbar.restype = vp
+        L.fb_plan_copy_kbar.argtypes = [vp, vp, vp]
         L.fb_workspace_size.argtypes = [vp, i64]
         L.fb_workspace_size.restype = sz
         L.fb_fwd.argtypes = [vp, vp, vp, i64, vp, vp]

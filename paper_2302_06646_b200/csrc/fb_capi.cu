@@ -138,7 +138,12 @@ int fb_plan_get_info(const fb_plan* p, fb_plan_info* info) {
   return FB_OK;
 }
 
-const float* fb_plan_kbar(const fb_plan* p) { return p ? p->kbar : nullptr; }
+int fb_plan_copy_kbar(const fb_plan* p, float* dst, void* stream) {
+  if (!p || !dst) return fail(FB_ERR_ARG, "fb_plan_copy_kbar: null argument");
+  return cuda_status(cudaMemcpyAsync(dst, p->kbar, sizeof(float) * p->H * p->N,
+                                     cudaMemcpyDeviceToDevice, (cudaStream_t)stream),
+                     "fb_plan_copy_kbar");
+}
 
 int fb_kernel_prep(fb_plan* p, const float* K, const float* D, const fb_reg_config* cfg,
                    int training, void* stream) {

@@ -118,10 +118,8 @@ class LongConvPlan:
 
     def kbar(self) -> torch.Tensor:
         """Copy of the plan's regularized bank Kbar [H, N] (fp32)."""
-        ptr = _lib.lib().fb_plan_kbar(self._h)
         out = torch.empty(self.H, self.N, dtype=torch.float32, device=self.device)
-        torch.cuda.synchronize(self.device)
-        _copy_from_ptr(out, ptr)
+        check(_lib.lib().fb_plan_copy_kbar(self._h, _ptr(out), _stream()))
         return out
 
     def workspace(self, B: int) -> torch.Tensor:
@@ -160,15 +158,6 @@ class LongConvPlan:
         check(_lib.lib().fb_bwd(self._h, _ptr(dy), _ptr(u), _ptr(du), _ptr(dK), _ptr(dKbar),
                                 _ptr(dD), B, _ptr(ws), _stream()))
         return (du, dK, dD, dKbar) if want_dkbar else (du, dK, dD)
-
-
-def _copy_from_ptr(out: torch.Tensor, ptr: int) -> None:
-    """Device-to-device copy from a raw device pointer into ``out``."""
-    cudart = torch.cuda.cudart()
-    nbytes = out.numel() * out.element_size()
-    res = cudart.cudaMemcpy(out.data_ptr(), ptr, nbytes, 3)  # cudaMemcpyDeviceToDevice
-    if int(res) != 0:
-        raise FBError(_lib.FB_ERR_CUDA, f"cudaMemcpy failed ({res})")
 
 
 _PLANS: dict = {}
