@@ -1,0 +1,380 @@
+"""FlashButterfly-B200 benchmark (driver contract: one JSON line on rank 0).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config 2] [--impl ours|reference]
+
+A step = one pass of the hot path over one batch of synthetic input:
+K1 kernel prep (regularize + kernel spectrum, once per call like the
+reference, regularize.cpp:157) + forward + backward (du, dK, dD).
+Metric (BASELINE.json): long-conv fwd+bwd elements/sec, E = B*H*N per step.
+
+Multi-GPU (torchrun, one process per GPU): heads are sharded with no
+communication (weak scaling: every rank owns a full per-GPU workload of H
+heads); the barrier + max-over-ranks device time give the job time.
+
+--impl reference runs the reference's own CPU implementation (the
+unmodified /root/reference sources compiled in oracle/_ref) on the host
+cores of this box, rank 0 only.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import platform
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+CONFIGS = {
+    # BASELINE.json configs[i] -> (B, H, N, dtype, engine, workload)
+    1: dict(B=1, H=1, N=1024, dtype="f32", engine="auto",
+            workload="config1: single-channel causal B=1 H=1 N=1024 fp32 fwd+bwd"),
+    2: dict(B=32, H=256, N=4096, dtype="bf16", engine="single",
+            workload="config2: LRA-scale B=32 H=256 N=4096 single-pass fwd+bwd, Squash/Smooth"),
+    3: dict(B=16, H=128, N=65536, dtype="bf16", engine="three",
+            workload="config3: Path256-scale B=16 H=128 N=65536 three-pass fwd+bwd"),
+}
+LAM, P = 0.003, 1
+
+
+def load_peaks():
+    f = ROOT / "MEASURED_PEAKS.json"
+    if f.exists():
+        d = json.loads(f.read_text())
+        return float(d["hbm_gbs"]), float(d.get("bf16_tflops_sustained", d["bf16_tflops"])), "measured"
+    return 6650.0, 1590.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.samples = []
+        self._stop = threading.Event()
+        self._t = threading.Thread(target=self._run, daemon=True)
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                                      "--format=csv,noheader,nounits"], capture_output=True,
+                                     text=True, timeout=5).stdout.strip()
+                if out:
+                    self.samples.append([x.strip() for x in out.split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = sorted(float(s[0]) for s in self.samples)
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for s in self.samples for i in range(4)
+                          if s[2 + i].lower().startswith("active")})
+        return {"sm_mhz": sm[len(sm) // 2], "sm_max_mhz": float(self.samples[0][1]),
+                "reasons": reasons, "samples": len(sm)}
+
+
+def alg_bytes(cfg, s):
+    """Algorithmic HBM bytes per step."""
+    E = cfg["B"] * cfg["H"] * cfg["N"]
+    HN = cfg["H"] * cfg["N"]
+    if cfg["engine"] == "three":
+        return 25 * s * E + 48 * HN
+    return 5 * s * E + 32 * HN
+
+
+def run_ours(args, cfg, rank, world, local_rank):
+    import torch
+
+    import paper_2302_06646_b200 as fb
+    from paper_2302_06646_b200 import _lib
+
+    dev = torch.device("cuda", local_rank)
+    torch.cuda.set_device(dev)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=dev)
+    dt = {"f32": torch.float32, "bf16": torch.bfloat16, "f16": torch.float16}[cfg["dtype"]]
+    s = torch.tensor([], dtype=dt).element_size()
+    B, H, N = cfg["B"], cfg["H"], cfg["N"]
+    eng = {"auto": fb.Engine.AUTO, "single": fb.Engine.BUTTERFLY,
+           "three": fb.Engine.THREE_PASS}[cfg["engine"]]
+    g = torch.Generator(device=dev)
+    g.manual_seed(1234 + rank)
+    # synthetic data (random-init kernels, geometric decay like init_kernels)
+    u = torch.randn(B, H, N, device=dev, generator=g).to(dt)
+    dy = torch.randn(B, H, N, device=dev, generator=g).to(dt)
+    pos = torch.arange(N, device=dev, dtype=torch.float32) / N
+    decay = (H / 2.0) ** (torch.arange(H, device=dev, dtype=torch.float32) / H)
+    K = torch.randn(H, N, device=dev, generator=g) * torch.exp(-pos[None, :] * decay[:, None])
+    D = torch.randn(H, device=dev, generator=g)
+    rc = fb.RegularizationConfig(lambda_=LAM, smooth_width=P)
+    plan = fb.LongConvPlan(N, H, fb.ConvMode.CAUSAL, dt, eng, dev)
+    ws = plan.workspace(B)
+    y = torch.empty_like(u)
+    du = torch.empty_like(u)
+    dK = torch.empty(H, N, device=dev)
+    dD = torch.empty(H, device=dev)
+    L = _lib.lib()
+    stream = torch.cuda.current_stream()
+    sp = stream.cuda_stream
+    import ctypes as C
+
+    c = rc.to_c()
+    P_ = lambda t: C.c_void_p(t.data_ptr())  # noqa: E731
+    h = plan._h
+    n_events = []
+
+    def step(rec=None):
+        _lib.check(L.fb_kernel_prep(h, P_(K), P_(D), C.byref(c), 0, C.c_void_p(sp)))
+        if rec is not None:
+            rec[0].record(stream)
+        _lib.check(L.fb_fwd(h, P_(u), P_(y), B, P_(ws), C.c_void_p(sp)))
+        if rec is not None:
+            rec[1].record(stream)
+        _lib.check(L.fb_bwd(h, P_(dy), P_(u), P_(du), P_(dK), C.c_void_p(0), P_(dD), B, P_(ws),
+                            C.c_void_p(sp)))
+        if rec is not None:
+            rec[2].record(stream)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    recs = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(args.steps)]
+    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local_rank) as clk:
+        t0.record(stream)
+        for i in range(args.steps):
+            step(recs[i])
+        t1.record(stream)
+        torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    ms = t0.elapsed_time(t1)
+    fwd_ms = sum(r[0].elapsed_time(r[1]) for r in recs) / args.steps
+    bwd_ms = sum(r[1].elapsed_time(r[2]) for r in recs) / args.steps
+    tmax = torch.tensor([ms], device=dev)
+    if dist:
+        dist.all_reduce(tmax, op=dist.ReduceOp.MAX)
+    ms = float(tmax.item())
+    ms_step = ms / args.steps
+    E = B * H * N
+    value = E * world / (ms_step / 1e3)
+
+    # ---------------- e2e: public API with host buffers, copies timed -------
+    hu = u.cpu().pin_memory()
+    hdy = dy.cpu().pin_memory()
+    hK = K.cpu().pin_memory()
+    hD = D.cpu().pin_memory()
+    hy = torch.empty_like(hu).pin_memory()
+    hdu = torch.empty_like(hu).pin_memory()
+    hdK = torch.empty_like(hK).pin_memory()
+    hdD = torch.empty_like(hD).pin_memory()
+    du_, uu, dyy = torch.empty_like(u), torch.empty_like(u), torch.empty_like(u)
+    KK, DD = torch.empty_like(K), torch.empty_like(D)
+
+    def e2e_step():
+        uu.copy_(hu, non_blocking=True)
+        dyy.copy_(hdy, non_blocking=True)
+        KK.copy_(hK, non_blocking=True)
+        DD.copy_(hD, non_blocking=True)
+        plan.prep(KK, DD, rc)
+        yy = plan.forward(uu, out=y, workspace=ws)
+        _lib.check(L.fb_bwd(h, P_(dyy), P_(uu), P_(du_), P_(dK), C.c_void_p(0), P_(dD), B,
+                            P_(ws), C.c_void_p(sp)))
+        hy.copy_(yy, non_blocking=True)
+        hdu.copy_(du_, non_blocking=True)
+        hdK.copy_(dK, non_blocking=True)
+        hdD.copy_(dD, non_blocking=True)
+
+    for _ in range(max(1, args.warmup)):
+        e2e_step()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e2e_steps = max(1, min(args.steps, 10))
+    if dist:
+        dist.barrier()
+    e0.record(stream)
+    for _ in range(e2e_steps):
+        e2e_step()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    ems = torch.tensor([e0.elapsed_time(e1) / e2e_steps], device=dev)
+    if dist:
+        dist.all_reduce(ems, op=dist.ReduceOp.MAX)
+    e2e_val = E * world / (float(ems.item()) / 1e3)
+    h2d = (hu.numel() + hdy.numel()) * s + (hK.numel() + hD.numel()) * 4
+    d2h = (hy.numel() + hdu.numel()) * s + (hdK.numel() + hdD.numel()) * 4
+
+    if dist:
+        dist.barrier()
+    if rank != 0:
+        if dist:
+            dist.destroy_process_group()
+        return None
+
+    hbm_peak, tc_peak, peak_kind = load_peaks()
+    # dominant kernel: the backward (K4a sp_bwd / K4b passes)
+    HN = H * N
+    bwd_bytes = 3 * s * E + 16 * HN
+    fwd_bytes = 2 * s * E + 16 * HN
+    dom = "bwd" if bwd_ms >= fwd_ms else "fwd"
+    dom_bytes, dom_ms = (bwd_bytes, bwd_ms) if dom == "bwd" else (fwd_bytes, fwd_ms)
+    achieved = dom_bytes / (dom_ms / 1e3) / 1e9
+    step_bytes = alg_bytes(cfg, s)
+    prof = ROOT / "profiles" / "traffic.json"
+    traffic = None
+    if prof.exists():
+        traffic = json.loads(prof.read_text()).get(f"config{args.config}", {}).get(dom)
+    cpu = None
+    if not args.no_cpu_baseline:
+        cpu = cpu_baseline(cfg, args.cpu_sample_heads)
+    launches_per_step = {"single": 6, "three": 9, "auto": 6}[cfg["engine"]]
+    out = {
+        "metric": "long-conv fwd+bwd elements/sec (E=B*H*N per step: K1 prep + fwd + bwd)",
+        "value": value, "unit": "elements/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": cfg["dtype"],
+        "data": "synthetic (torch.randn signals, random geometric-decay kernels)",
+        "config": {"workload": cfg["workload"], "B": B, "H": H, "N": N,
+                   "engine": plan.engine.name.lower(), "transform_len": plan.n,
+                   "lambda": LAM, "smooth_width": P, "mode": "causal",
+                   "sharding": f"heads, {H} per GPU, no communication",
+                   "l2": "inputs larger than L2 (u, dy, y, du = "
+                         f"{4 * E * s / 2**20:.0f} MiB per GPU)"},
+        "fwd_ms": fwd_ms, "bwd_ms": bwd_ms,
+        "roofline": {"bound": "hbm", "kernel": f"{dom} (sp_{dom}_kernel)" if plan.engine.name != "THREE_PASS" else dom,
+                     "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
+                     "frac": achieved / hbm_peak, "traffic": traffic,
+                     "alg_bytes_per_launch": dom_bytes, "peak_kind": peak_kind},
+        "step_roofline": {"alg_bytes": step_bytes,
+                          "achieved_GBs": step_bytes / (ms_step / 1e3) / 1e9,
+                          "frac": step_bytes / (ms_step / 1e3) / 1e9 / hbm_peak},
+        "e2e": {"value": e2e_val, "unit": "elements/s", "h2d_bytes_per_step": h2d,
+                "d2h_bytes_per_step": d2h, "ms_per_step": float(ems.item())},
+        "cpu_baseline": cpu,
+        "clocks": clk.summary(),
+        "gpu_launches": launches_per_step * args.steps,
+    }
+    print(json.dumps(out), flush=True)
+    if dist:
+        dist.destroy_process_group()
+    return out
+
+
+def reference_cpu_run(cfg, heads, steps=1, threads=None):
+    """Reference CPU path (oracle/_ref = unmodified reference sources):
+    regularized_long_conv(kButterfly, kCausal, threads=nproc) + the backward
+    composed from conv_butterfly.  Returns (elements, seconds)."""
+    import numpy as np
+
+    from oracle.oracle import RefOracle, ref_available
+
+    if not ref_available():
+        raise RuntimeError("oracle/_ref/liblongconv_ref.so missing")
+    ref = RefOracle(threads)
+    B, N = cfg["B"], cfg["N"]
+    rng = np.random.default_rng(0)
+    u = rng.standard_normal((B, heads, N))
+    dy = rng.standard_normal((B, heads, N))
+    K, D = ref.init_kernels(1, heads, N, 3)
+    engine = 2 if cfg["engine"] == "three" else 1
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        Kbar = ref.regularize_bank(K, LAM, P)
+        ref.regularized_long_conv(u, K, D, LAM, P, engine=engine)
+        _, dKbar, _ = ref.long_conv_backward(u, dy, Kbar, D)
+        ref.regularizer_backward(K, LAM, P, dKbar)
+    return B * heads * N * steps, time.perf_counter() - t0
+
+
+def cpu_baseline(cfg, heads):
+    heads = min(cfg["H"], heads)
+    threads = os.cpu_count() or 1
+    try:
+        el, sec = reference_cpu_run(cfg, heads, 1, threads)
+    except Exception as e:  # pragma: no cover
+        return {"value": None, "unit": "elements/s", "error": str(e)}
+    return {"value": el / sec, "unit": "elements/s", "cores": threads, "kind": "reference",
+            "sample": f"B={cfg['B']} H={heads} (of {cfg['H']}) N={cfg['N']}, fp64, "
+                      f"{sec:.1f}s: regularize_bank + regularized_long_conv(kButterfly) + "
+                      "composed conv_butterfly backward; channels independent so the rate "
+                      "extrapolates linearly",
+            "host": platform.processor() or platform.machine()}
+
+
+def run_reference(args, cfg, rank):
+    if rank != 0:
+        return
+    heads = min(cfg["H"], args.cpu_sample_heads)
+    threads = os.cpu_count() or 1
+    for _ in range(args.warmup if args.warmup < 1 else 1):
+        reference_cpu_run(cfg, max(1, heads // 8), 1, threads)
+    el, sec = reference_cpu_run(cfg, heads, args.steps, threads)
+    val = el / sec
+    out = {
+        "impl": "reference",
+        "metric": "long-conv fwd+bwd elements/sec (E=B*H*N per step: K1 prep + fwd + bwd)",
+        "value": val, "unit": "elements/s", "n_gpus": 1, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": sec / args.steps * 1e3 * cfg["H"] / heads,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic", "config": {"workload": cfg["workload"], "B": cfg["B"], "H": cfg["H"],
+                                        "N": cfg["N"]},
+        "cpu_baseline": {"value": val, "unit": "elements/s", "cores": threads,
+                         "kind": "reference",
+                         "sample": f"each step B={cfg['B']} H={heads} of {cfg['H']} heads"},
+        "e2e": {"value": val, "unit": "elements/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(out), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--config", type=int, default=2, choices=sorted(CONFIGS))
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--cpu-sample-heads", type=int, default=32)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    rank = int(os.environ.get("RANK", 0))
+    world = int(os.environ.get("WORLD_SIZE", 1))
+    local_rank = int(os.environ.get("LOCAL_RANK", 0))
+    cfg = CONFIGS[args.config]
+    if args.impl == "reference":
+        run_reference(args, cfg, rank)
+        return
+    if world != args.gpus and rank == 0:
+        print(f"warning: --gpus {args.gpus} but WORLD_SIZE={world}", file=sys.stderr)
+    run_ours(args, cfg, rank, world, local_rank)
+
+
+if __name__ == "__main__":
+    main()

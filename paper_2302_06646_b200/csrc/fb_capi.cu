@@ -45,6 +45,24 @@ static int upload_twiddles(float2** dst, int64_t n) {
                      "cudaMemcpy(twiddles)");
 }
 
+// Two-level table [w^i (i < 64) | w^(64 i) (i < n/64)], w = exp(-2 pi i / n).
+static int upload_twiddles2(float2** dst, int64_t n) {
+  const int64_t lo = 64, hi = n / 64 > 0 ? n / 64 : 1;
+  std::vector<float2> h((size_t)(lo + hi));
+  for (int64_t t = 0; t < lo; ++t) {
+    const double a = -2.0 * M_PI * (double)t / (double)n;
+    h[(size_t)t] = make_float2((float)std::cos(a), (float)std::sin(a));
+  }
+  for (int64_t i = 0; i < hi; ++i) {
+    const double a = -2.0 * M_PI * (double)(64 * i) / (double)n;
+    h[(size_t)(lo + i)] = make_float2((float)std::cos(a), (float)std::sin(a));
+  }
+  int rc = cuda_status(cudaMalloc(dst, sizeof(float2) * h.size()), "cudaMalloc(twiddles2)");
+  if (rc) return rc;
+  return cuda_status(cudaMemcpy(*dst, h.data(), sizeof(float2) * h.size(), cudaMemcpyHostToDevice),
+                     "cudaMemcpy(twiddles2)");
+}
+
 constexpr int64_t kSinglePassMax = 8192;   // fp32 complex transform in smem
 constexpr int64_t kThreePassRow = 8192;    // l: row length of pass 2
 constexpr int64_t kMinTransform = 256;
@@ -99,6 +117,7 @@ int fb_plan_create(fb_plan** out, int64_t N, int64_t H, int mode, int dtype, int
   }
   cudaDeviceGetAttribute(&p->num_sms, cudaDevAttrMultiProcessorCount, device);
   rc = upload_twiddles(&p->tw_n, n);
+  if (!rc) rc = upload_twiddles2(&p->tw2, n);
   if (!rc && engine == FB_ENGINE_THREE) rc = upload_twiddles(&p->tw_l, p->l);
   if (!rc && engine == FB_ENGINE_THREE) rc = upload_twiddles(&p->tw_m, std::max<int64_t>(p->m, 2));
   if (!rc) rc = cuda_status(cudaMalloc(&p->kf, sizeof(float2) * H * n), "cudaMalloc(kf)");
@@ -115,6 +134,7 @@ int fb_plan_create(fb_plan** out, int64_t N, int64_t H, int mode, int dtype, int
 int fb_plan_destroy(fb_plan* p) {
   if (!p) return FB_OK;
   cudaFree(p->tw_n);
+  cudaFree(p->tw2);
   cudaFree(p->tw_l);
   cudaFree(p->tw_m);
   cudaFree(p->kf);

@@ -207,4 +207,105 @@ __device__ __forceinline__ void smem_passes(float2* s, uint32_t n, uint32_t batc
   }
 }
 
+
+// ---------------------------------------------------------------------------
+// Compile-time-size Stockham passes (v2): n = 2^LOG2N points per transform,
+// T = n/16 threads, pass order [16, SMALL?, 16, ..., 16] with SMALL =
+// 2^(LOG2N mod 4) at Ns == 16.  Twiddles come from a two-level smem table
+//   tab[i] = w^i (i < 64),  tab[64 + i] = w^(64 i) (i < n/64),  w = e^{-2 pi i/n}
+// so w^t = tab[t & 63] * tab[64 + (t >> 6)].
+// ---------------------------------------------------------------------------
+template <int LOG2N>
+struct FftShape {
+  static constexpr uint32_t n = 1u << LOG2N;
+  static constexpr uint32_t T = n / 16;
+  static constexpr uint32_t stride = n / 16;
+  static constexpr int SMALL = 1 << (LOG2N % 4);
+  static constexpr uint32_t tab_len = 64 + n / 64;
+  static constexpr uint32_t work_len = n + n / 16;  // padded float2 slots
+};
+
+template <int SIGN>
+__device__ __forceinline__ float2 tw2(const float2* tab, uint32_t t) {
+  const float2 w = cmul(tab[t & 63u], tab[64u + (t >> 6)]);
+  return SIGN < 0 ? w : make_float2(w.x, -w.y);
+}
+
+// v[r] *= w^(r * base) for r in [1, R): four table lookups, the rest by
+// products (depth <= 3), so twiddle error stays at a few ulp.
+template <int SIGN, int R>
+__device__ __forceinline__ void apply_tw(float2 (&v)[R], const float2* tab, uint32_t base) {
+  const float2 w1 = tw2<SIGN>(tab, base);
+  v[1] = cmul(v[1], w1);
+  if constexpr (R >= 4) {
+    const float2 w2 = tw2<SIGN>(tab, 2 * base);
+    const float2 w3 = cmul(w1, w2);
+    v[2] = cmul(v[2], w2);
+    v[3] = cmul(v[3], w3);
+    if constexpr (R >= 8) {
+      const float2 w4 = tw2<SIGN>(tab, 4 * base);
+      v[4] = cmul(v[4], w4);
+      v[5] = cmul(v[5], cmul(w1, w4));
+      v[6] = cmul(v[6], cmul(w2, w4));
+      const float2 w7 = cmul(w3, w4);
+      v[7] = cmul(v[7], w7);
+      if constexpr (R >= 16) {
+        const float2 w8 = tw2<SIGN>(tab, 8 * base);
+        v[8] = cmul(v[8], w8);
+        v[9] = cmul(v[9], cmul(w1, w8));
+        v[10] = cmul(v[10], cmul(w2, w8));
+        v[11] = cmul(v[11], cmul(w3, w8));
+        v[12] = cmul(v[12], cmul(w4, w8));
+        v[13] = cmul(v[13], cmul(cmul(w1, w4), w8));
+        v[14] = cmul(v[14], cmul(cmul(w2, w4), w8));
+        v[15] = cmul(v[15], cmul(w7, w8));
+      }
+    }
+  }
+}
+
+// Load + twiddle + DFT of one radix-R butterfly j of the pass at Ns = NS.
+template <int SIGN, int R, uint32_t NS, int LOG2N>
+__device__ __forceinline__ void bfly_load(const float2* s, const float2* tab, float2 (&v)[R],
+                                          uint32_t j) {
+  constexpr uint32_t n = 1u << LOG2N, str = n / R;
+#pragma unroll
+  for (int r = 0; r < R; ++r) v[r] = s[pad16(j + r * str)];
+  if constexpr (NS > 1) apply_tw<SIGN, R>(v, tab, (j % NS) * (n / (NS * R)));
+  dft_reg<SIGN, R>(v);
+}
+template <int R, uint32_t NS>
+__device__ __forceinline__ void bfly_store(float2* s, const float2 (&v)[R], uint32_t j) {
+  const uint32_t idxD = (j / NS) * NS * R + (j % NS);
+#pragma unroll
+  for (int r = 0; r < R; ++r) s[pad16(idxD + r * NS)] = v[r];
+}
+
+// All passes with NS in [NS0, n/16): in place, __syncthreads between.
+template <int SIGN, int LOG2N, uint32_t NS>
+__device__ __forceinline__ void mid_passes(float2* s, const float2* tab) {
+  using S = FftShape<LOG2N>;
+  if constexpr (NS < S::n / 16) {
+    const uint32_t tid = threadIdx.x;
+    if constexpr (S::SMALL > 1 && NS == 16) {
+      constexpr int R = S::SMALL, G = 16 / R;
+      float2 v[G][R];
+#pragma unroll
+      for (int g = 0; g < G; ++g) bfly_load<SIGN, R, NS, LOG2N>(s, tab, v[g], tid + g * S::T);
+      __syncthreads();
+#pragma unroll
+      for (int g = 0; g < G; ++g) bfly_store<R, NS>(s, v[g], tid + g * S::T);
+      __syncthreads();
+      mid_passes<SIGN, LOG2N, NS * R>(s, tab);
+    } else {
+      float2 v[16];
+      bfly_load<SIGN, 16, NS, LOG2N>(s, tab, v, tid);
+      __syncthreads();
+      bfly_store<16, NS>(s, v, tid);
+      __syncthreads();
+      mid_passes<SIGN, LOG2N, NS * 16>(s, tab);
+    }
+  }
+}
+
 }  // namespace fb

@@ -14,6 +14,7 @@ struct fb_plan {
   int mode = FB_MODE_CAUSAL, dtype = FB_F32, engine = FB_ENGINE_SINGLE, device = 0;
   bool periodic = false;  // circular with n > N: u periodically extended
   float2* tw_n = nullptr;  // exp(-2 pi i t / n), t < n
+  float2* tw2 = nullptr;   // two-level table for n: [w^i, i<64 | w^(64 i), i<n/64]
   float2* tw_l = nullptr;  // exp(-2 pi i t / l), t < l   (three-pass)
   float2* tw_m = nullptr;  // exp(-2 pi i t / m), t < m   (three-pass)
   float2* kf = nullptr;    // per-head spectrum / n: single [H][n]; three [H][m][l]

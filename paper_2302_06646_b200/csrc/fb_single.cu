@@ -4,10 +4,13 @@
 // Reference path replaced (regularize.cpp:149-190 -> conv_channel :112-138
 // -> conv_butterfly butterfly.cpp:187-210 -> apply_plan x3):
 //   * the kernel FFT (butterfly.cpp:205, recomputed per channel by the
-//     reference) is hoisted into sp_prep_kernel, once per head, scaled by
-//     1/n so the inverse needs no extra pass;
+//     reference) is hoisted into sp_spectrum_kernel, once per head, scaled
+//     by 1/n so the inverse needs no extra pass;
 //   * two real channels (b, b+1) of one head ride in the real and imaginary
 //     parts of one complex signal (K is real, so conv is linear per part);
+//   * each CTA owns one head and a run of channel pairs: k_f is staged in
+//     shared memory once, the next pair's rows are prefetched by TMA bulk
+//     copies (cp.async.bulk + mbarrier) while the current pair transforms;
 //   * u is read from HBM once, y written once; the spectrum never leaves the
 //     SM: forward passes -> (x) k_f in registers -> inverse passes.
 #include <algorithm>
@@ -15,229 +18,349 @@
 #include "fb_common.cuh"
 #include "fb_fft.cuh"
 #include "fb_internal.h"
+#include "fb_ptx.cuh"
 
 namespace fb {
 
-// Transform-position value of a length-N channel: zero extension (causal,
-// or circular kernels) or periodic extension (circular signals, n > N).
+// Staged signal value at transform position t of a length-N row in smem:
+// zero extension (causal) or periodic extension (circular with n > N).
 template <typename IO>
-__device__ __forceinline__ float sig_at(const IO* __restrict__ p, uint32_t t, uint32_t N,
-                                        bool periodic) {
-  if (t < N) return ld(p + t);
-  if (periodic) return ld(p + (t & (N - 1)));
+__device__ __forceinline__ float stage_at(const IO* row, uint32_t t, uint32_t N, bool periodic) {
+  if (t < N) return tof(row[t]);
+  if (periodic) return tof(row[t & (N - 1)]);
   return 0.f;
+}
+
+template <typename IO>
+__host__ __device__ constexpr uint32_t row_pitch(uint32_t N) {
+  // row stride in elements, 16-byte multiple (TMA bulk granularity)
+  return (N + (16 / sizeof(IO)) - 1) / (16 / sizeof(IO)) * (16 / sizeof(IO));
+}
+
+// Copy rows [b0, b0+nrows) x head h of `src` ([B][H][N]) into smem rows of
+// pitch P.  TMA bulk path when every row is 16-byte aligned, else a
+// cooperative (synchronous) copy.  Returns the number of bytes in flight.
+template <typename IO>
+__device__ __forceinline__ uint32_t stage_rows(IO* dst, const IO* const* srcs, int nrows, uint32_t N,
+                                               uint32_t P, bool tma, uint64_t* bar) {
+  if (tma) {
+    uint32_t bytes = 0;
+    if (threadIdx.x == 0) {
+      const uint32_t rb = N * (uint32_t)sizeof(IO);
+      bytes = rb * nrows;
+      ptx::fence_proxy_async_smem();
+      ptx::mbar_arrive_expect_tx(bar, bytes);
+      for (int r = 0; r < nrows; ++r) ptx::bulk_g2s(dst + r * P, srcs[r], rb, bar);
+    }
+    return bytes;
+  }
+  for (int r = 0; r < nrows; ++r)
+    for (uint32_t t = threadIdx.x; t < N; t += blockDim.x) dst[r * P + t] = __ldg(srcs[r] + t);
+  return 0;
+}
+
+template <int LOG2N>
+__device__ __forceinline__ void load_table(float2* tab, const float2* __restrict__ g) {
+  for (uint32_t i = threadIdx.x; i < FftShape<LOG2N>::tab_len; i += blockDim.x) tab[i] = __ldg(g + i);
 }
 
 // ---------------------------------------------------------------- K1 (spectrum)
 // kf[h][e] = FFT_n(zero-pad(kbar[h]))[e] / n
-template <int SMALL>
-__global__ void __launch_bounds__(512) sp_spectrum_kernel(const float* __restrict__ kbar,
-                                                           float2* __restrict__ kf,
-                                                           const float2* __restrict__ tw,
-                                                           uint32_t N, uint32_t n) {
-  extern __shared__ float2 smem[];
-  const uint32_t h = blockIdx.x, j = threadIdx.x, stride = n / 16;
+template <int LOG2N>
+__global__ void __launch_bounds__(FftShape<LOG2N>::T, 1)
+    sp_spectrum_kernel(const float* __restrict__ kbar, float2* __restrict__ kf,
+                       const float2* __restrict__ tab_g, uint32_t N) {
+  using S = FftShape<LOG2N>;
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  float2* work = reinterpret_cast<float2*>(smem_raw);
+  float2* tab = work + S::work_len;
+  const uint32_t h = blockIdx.x, j = threadIdx.x;
+  load_table<LOG2N>(tab, tab_g);
   const float* kh = kbar + (size_t)h * N;
   float2 v[16];
 #pragma unroll
   for (int r = 0; r < 16; ++r) {
-    const uint32_t t = j + r * stride;
+    const uint32_t t = j + r * S::stride;
     v[r] = make_float2(t < N ? __ldg(kh + t) : 0.f, 0.f);
   }
   dft_reg<-1, 16>(v);
-  stockham_store<16>(smem, v, j, 0, 1, 1);
+  bfly_store<16, 1>(work, v, j);
   __syncthreads();
-  smem_passes<-1, SMALL>(smem, n, 1, 16, stride, tw);
-  stockham_load_twiddle<-1, 16>(smem, v, j, 0, n, 1, stride, tw);
-  dft_reg<-1, 16>(v);
-  const float inv_n = 1.0f / (float)n;
-  float2* out = kf + (size_t)h * n;
+  mid_passes<-1, LOG2N, 16>(work, tab);
+  bfly_load<-1, 16, S::n / 16, LOG2N>(work, tab, v, j);
+  const float inv_n = 1.0f / (float)S::n;
+  float2* out = kf + (size_t)h * S::n;
 #pragma unroll
-  for (int r = 0; r < 16; ++r) out[j + r * stride] = cscale(v[r], inv_n);
+  for (int r = 0; r < 16; ++r) out[j + r * S::stride] = cscale(v[r], inv_n);
 }
 
 // ---------------------------------------------------------------- K2 forward
-// One CTA = one (head h, channel pair b0=2*blockIdx.y, b1=b0+1); T = n/16.
-template <typename IO, int SMALL>
-__global__ void __launch_bounds__(512) sp_fwd_kernel(const IO* __restrict__ u, IO* __restrict__ y,
-                                                      const float2* __restrict__ kf,
-                                                      const float* __restrict__ D,
-                                                      const float2* __restrict__ tw, int B, int H,
-                                                      uint32_t N, uint32_t n, int periodic) {
-  extern __shared__ float2 smem[];
-  const int h = blockIdx.x;
-  const int b0 = 2 * blockIdx.y, b1 = b0 + 1;
-  const bool has1 = b1 < B;
-  const size_t off0 = ((size_t)b0 * H + h) * N, off1 = ((size_t)b1 * H + h) * N;
-  const uint32_t j = threadIdx.x, stride = n / 16;
-  float2 v[16];
-  // forward pass 1 (Ns = 1) straight from HBM: pair (u[b0], u[b1]) -> complex
-#pragma unroll
-  for (int r = 0; r < 16; ++r) {
-    const uint32_t t = j + r * stride;
-    v[r].x = sig_at(u + off0, t, N, periodic);
-    v[r].y = has1 ? sig_at(u + off1, t, N, periodic) : 0.f;
+// grid (H, chunks): CTA (h, c) runs channel pairs [c*ppc, (c+1)*ppc).
+template <typename IO, int LOG2N>
+__global__ void __launch_bounds__(FftShape<LOG2N>::T, 1)
+    sp_fwd_kernel(const IO* __restrict__ u, IO* __restrict__ y, const float2* __restrict__ kf,
+                  const float* __restrict__ D, const float2* __restrict__ tab_g, int B, int H,
+                  uint32_t N, int periodic, int ppc, int tma) {
+  using S = FftShape<LOG2N>;
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  __shared__ __align__(8) uint64_t bars[2];
+  const uint32_t P = row_pitch<IO>(N);
+  float2* work = reinterpret_cast<float2*>(smem_raw);
+  float2* kfs = work + S::work_len;
+  float2* tab = kfs + S::n;
+  IO* stage = reinterpret_cast<IO*>(tab + ((S::tab_len + 1) & ~1u));  // [2][2][P]
+  const int h = blockIdx.x, j = threadIdx.x;
+  const int npairs = (B + 1) / 2;
+  const int p0 = blockIdx.y * ppc, p1 = min(npairs, p0 + ppc);
+  if (p0 >= p1) return;
+  if (j == 0) {
+    ptx::mbar_init(&bars[0], 1);
+    ptx::mbar_init(&bars[1], 1);
+    ptx::fence_barrier_init();
   }
-  dft_reg<-1, 16>(v);
-  stockham_store<16>(smem, v, j, 0, 1, 1);
-  __syncthreads();
-  smem_passes<-1, SMALL>(smem, n, 1, 16, stride, tw);
-  // last forward pass (Ns = n/16): thread j ends up owning bins j + r n/16,
-  // exactly the points the first inverse pass (Ns = 1) needs: the pointwise
-  // product with k_f and the first inverse DFT block stay in registers.
-  stockham_load_twiddle<-1, 16>(smem, v, j, 0, n, 1, stride, tw);
-  dft_reg<-1, 16>(v);
-  const float2* kh = kf + (size_t)h * n;
-#pragma unroll
-  for (int r = 0; r < 16; ++r) v[r] = cmul(v[r], __ldg(kh + j + r * stride));
-  dft_reg<+1, 16>(v);
-  __syncthreads();
-  stockham_store<16>(smem, v, j, 0, 1, 1);
-  __syncthreads();
-  smem_passes<+1, SMALL>(smem, n, 1, 16, stride, tw);
-  stockham_load_twiddle<+1, 16>(smem, v, j, 0, n, 1, stride, tw);
-  dft_reg<+1, 16>(v);
-  // epilogue: y = conv + D u, straight to HBM (u re-read hits L2)
+  load_table<LOG2N>(tab, tab_g);
+  {
+    const float4* src = reinterpret_cast<const float4*>(kf + (size_t)h * S::n);
+    float4* dst = reinterpret_cast<float4*>(kfs);
+    for (uint32_t i = j; i < S::n / 2; i += S::T) dst[i] = __ldg(src + i);
+  }
   const float d = __ldg(D + h);
-#pragma unroll
-  for (int r = 0; r < 16; ++r) {
-    const uint32_t t = j + r * stride;
-    if (t < N) {
-      st(y + off0 + t, fmaf(d, ld(u + off0 + t), v[r].x));
-      if (has1) st(y + off1 + t, fmaf(d, ld(u + off1 + t), v[r].y));
+  __syncthreads();
+  auto issue = [&](int pr, int buf) {
+    const int b0 = 2 * pr;
+    const IO* rows[2] = {u + ((size_t)b0 * H + h) * N, u + ((size_t)(b0 + 1) * H + h) * N};
+    stage_rows<IO>(stage + buf * 2 * P, rows, (b0 + 1 < B) ? 2 : 1, N, P, tma, &bars[buf]);
+  };
+  if (tma) issue(p0, 0);
+  for (int pr = p0, it = 0; pr < p1; ++pr, ++it) {
+    const int buf = tma ? (it & 1) : 0;
+    const int b0 = 2 * pr, b1 = b0 + 1;
+    const bool has1 = b1 < B;
+    if (tma) {
+      ptx::mbar_wait(&bars[buf], (it >> 1) & 1);
+      if (pr + 1 < p1) issue(pr + 1, buf ^ 1);
+    } else {
+      issue(pr, 0);
+      __syncthreads();
     }
+    const IO* s0 = stage + buf * 2 * P;
+    const IO* s1 = s0 + P;
+    float2 v[16];
+#pragma unroll
+    for (int r = 0; r < 16; ++r) {
+      const uint32_t t = j + r * S::stride;
+      v[r].x = stage_at(s0, t, N, periodic);
+      v[r].y = has1 ? stage_at(s1, t, N, periodic) : 0.f;
+    }
+    dft_reg<-1, 16>(v);
+    bfly_store<16, 1>(work, v, j);
+    __syncthreads();
+    mid_passes<-1, LOG2N, 16>(work, tab);
+    // last forward pass (Ns = n/16): thread j owns bins j + r n/16, exactly
+    // the points the first inverse pass (Ns = 1) needs, so the product with
+    // k_f and the first inverse DFT block stay in registers.
+    bfly_load<-1, 16, S::n / 16, LOG2N>(work, tab, v, j);
+#pragma unroll
+    for (int r = 0; r < 16; ++r) v[r] = cmul(v[r], kfs[j + r * S::stride]);
+    dft_reg<+1, 16>(v);
+    __syncthreads();
+    bfly_store<16, 1>(work, v, j);
+    __syncthreads();
+    mid_passes<+1, LOG2N, 16>(work, tab);
+    bfly_load<+1, 16, S::n / 16, LOG2N>(work, tab, v, j);
+    IO* y0 = y + ((size_t)b0 * H + h) * N;
+    IO* y1 = y + ((size_t)b1 * H + h) * N;
+#pragma unroll
+    for (int r = 0; r < 16; ++r) {
+      const uint32_t t = j + r * S::stride;
+      if (t < N) {
+        st(y0 + t, fmaf(d, tof(s0[t]), v[r].x));
+        if (has1) st(y1 + t, fmaf(d, tof(s1[t]), v[r].y));
+      }
+    }
+    __syncthreads();  // work + stage[buf] free for the next pair
   }
 }
 
 // ---------------------------------------------------------------- K4a backward
-// One CTA = one (head h, chunk of channel pairs).  Per pair:
+// grid (H, chunks).  Per pair:
 //   DY = FFT(dy pair), U = FFT(u pair)            (2 forward transforms)
-//   acc += conj(U) DY        (thread-owned bins, smem, fixed order => determ.)
+//   acc += conj(U) DY        (thread-owned bins in smem, fixed order)
 //   du = IFFT(DY conj(k_f)) + D dy                (1 inverse transform)
-// plus dD partial = sum dy u.  Partials per chunk are reduced by
-// sp_dk_finalize_kernel in a fixed order.
-template <typename IO, int SMALL>
-__global__ void __launch_bounds__(512) sp_bwd_kernel(
-    const IO* __restrict__ dy, const IO* __restrict__ u, IO* __restrict__ du,
-    const float2* __restrict__ kf, const float* __restrict__ D, const float2* __restrict__ tw,
-    float2* __restrict__ spart, float* __restrict__ ddpart, int B, int H, uint32_t N, uint32_t n,
-    int periodic, int pairs_per_chunk) {
-  extern __shared__ float2 smem[];
-  float2* acc = smem + padded_len(n);  // [n], thread-owned bins
+// plus dD partial = sum dy u.  Per-chunk partials are reduced by
+// sp_dk_finalize_kernel in a fixed order (deterministic, no atomics).
+template <typename IO, int LOG2N, int NBUF>
+__global__ void __launch_bounds__(FftShape<LOG2N>::T, 1)
+    sp_bwd_kernel(const IO* __restrict__ dy, const IO* __restrict__ u, IO* __restrict__ du,
+                  const float2* __restrict__ kf, const float* __restrict__ D,
+                  const float2* __restrict__ tab_g, float2* __restrict__ spart,
+                  float* __restrict__ ddpart, int B, int H, uint32_t N, int periodic, int ppc,
+                  int tma) {
+  using S = FftShape<LOG2N>;
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  __shared__ __align__(8) uint64_t bars[2];
   __shared__ float red[32];
+  const uint32_t P = row_pitch<IO>(N);
+  float2* work = reinterpret_cast<float2*>(smem_raw);
+  float2* acc = work + S::work_len;  // [n], thread-owned bins
+  float2* tab = acc + S::n;
+  IO* stage = reinterpret_cast<IO*>(tab + ((S::tab_len + 1) & ~1u));  // [NBUF][4][P]
   const int h = blockIdx.x, chunk = blockIdx.y, chunks = gridDim.y;
-  const uint32_t j = threadIdx.x, stride = n / 16;
+  const uint32_t j = threadIdx.x;
   const int npairs = (B + 1) / 2;
-  const float2* kh = kf + (size_t)h * n;
+  const float2* kh = kf + (size_t)h * S::n;
   const float d = __ldg(D + h);
+  if (j == 0) {
+    ptx::mbar_init(&bars[0], 1);
+    ptx::mbar_init(&bars[1], 1);
+    ptx::fence_barrier_init();
+  }
+  load_table<LOG2N>(tab, tab_g);
 #pragma unroll
-  for (int r = 0; r < 16; ++r) acc[j + r * stride] = make_float2(0.f, 0.f);
+  for (int r = 0; r < 16; ++r) acc[j + r * S::stride] = make_float2(0.f, 0.f);
   float dd = 0.f;
-  const int p_begin = chunk * pairs_per_chunk;
-  const int p_end = min(npairs, p_begin + pairs_per_chunk);
-  for (int pr = p_begin; pr < p_end; ++pr) {
+  const int p0 = chunk * ppc, p1 = min(npairs, p0 + ppc);
+  __syncthreads();
+  // rows in a stage buffer: dy[b0], dy[b1], u[b0], u[b1]
+  auto issue = [&](int pr, int buf) {
+    const int b0 = 2 * pr;
+    const bool two = b0 + 1 < B;
+    IO* dst = stage + buf * 4 * P;
+    const IO* rd[2] = {dy + ((size_t)b0 * H + h) * N, dy + ((size_t)(b0 + 1) * H + h) * N};
+    const IO* ru[2] = {u + ((size_t)b0 * H + h) * N, u + ((size_t)(b0 + 1) * H + h) * N};
+    if (tma) {
+      if (j == 0) {
+        const uint32_t rb = N * (uint32_t)sizeof(IO);
+        const int nr = two ? 2 : 1;
+        ptx::fence_proxy_async_smem();
+        ptx::mbar_arrive_expect_tx(&bars[buf], 2 * nr * rb);
+        for (int r = 0; r < nr; ++r) {
+          ptx::bulk_g2s(dst + r * P, rd[r], rb, &bars[buf]);
+          ptx::bulk_g2s(dst + (2 + r) * P, ru[r], rb, &bars[buf]);
+        }
+      }
+    } else {
+      stage_rows<IO>(dst, rd, two ? 2 : 1, N, P, false, nullptr);
+      stage_rows<IO>(dst + 2 * P, ru, two ? 2 : 1, N, P, false, nullptr);
+    }
+  };
+  if (tma && p0 < p1) issue(p0, 0);
+  for (int pr = p0, it = 0; pr < p1; ++pr, ++it) {
+    const int buf = (NBUF == 2 && tma) ? (it & 1) : 0;
     const int b0 = 2 * pr, b1 = b0 + 1;
     const bool has1 = b1 < B;
-    const size_t off0 = ((size_t)b0 * H + h) * N, off1 = ((size_t)b1 * H + h) * N;
+    if (tma) {
+      ptx::mbar_wait(&bars[buf], NBUF == 2 ? ((it >> 1) & 1) : (it & 1));
+      if (NBUF == 2 && pr + 1 < p1) issue(pr + 1, buf ^ 1);
+    } else {
+      issue(pr, 0);
+      __syncthreads();
+    }
+    const IO* g0 = stage + buf * 4 * P;
+    const IO* g1 = g0 + P;
+    const IO* u0 = g0 + 2 * P;
+    const IO* u1 = g0 + 3 * P;
     float2 gv[16], v[16];
-    // ---- FFT(dy)
+    // ---- FFT(dy), with the dD partial from the staged rows
 #pragma unroll
     for (int r = 0; r < 16; ++r) {
-      const uint32_t t = j + r * stride;
-      v[r].x = sig_at(dy + off0, t, N, periodic);
-      v[r].y = has1 ? sig_at(dy + off1, t, N, periodic) : 0.f;
+      const uint32_t t = j + r * S::stride;
+      v[r].x = stage_at(g0, t, N, periodic);
+      v[r].y = has1 ? stage_at(g1, t, N, periodic) : 0.f;
       if (t < N) {
-        dd = fmaf(v[r].x, ld(u + off0 + t), dd);
-        if (has1) dd = fmaf(v[r].y, ld(u + off1 + t), dd);
+        dd = fmaf(v[r].x, tof(u0[t]), dd);
+        if (has1) dd = fmaf(v[r].y, tof(u1[t]), dd);
       }
     }
     dft_reg<-1, 16>(v);
+    bfly_store<16, 1>(work, v, j);
     __syncthreads();
-    stockham_store<16>(smem, v, j, 0, 1, 1);
-    __syncthreads();
-    smem_passes<-1, SMALL>(smem, n, 1, 16, stride, tw);
-    stockham_load_twiddle<-1, 16>(smem, gv, j, 0, n, 1, stride, tw);
-    dft_reg<-1, 16>(gv);
+    mid_passes<-1, LOG2N, 16>(work, tab);
+    bfly_load<-1, 16, S::n / 16, LOG2N>(work, tab, gv, j);
     // ---- FFT(u)
 #pragma unroll
     for (int r = 0; r < 16; ++r) {
-      const uint32_t t = j + r * stride;
-      v[r].x = sig_at(u + off0, t, N, periodic);
-      v[r].y = has1 ? sig_at(u + off1, t, N, periodic) : 0.f;
+      const uint32_t t = j + r * S::stride;
+      v[r].x = stage_at(u0, t, N, periodic);
+      v[r].y = has1 ? stage_at(u1, t, N, periodic) : 0.f;
     }
     dft_reg<-1, 16>(v);
     __syncthreads();
-    stockham_store<16>(smem, v, j, 0, 1, 1);
+    bfly_store<16, 1>(work, v, j);
     __syncthreads();
-    smem_passes<-1, SMALL>(smem, n, 1, 16, stride, tw);
-    stockham_load_twiddle<-1, 16>(smem, v, j, 0, n, 1, stride, tw);
-    dft_reg<-1, 16>(v);
+    mid_passes<-1, LOG2N, 16>(work, tab);
+    bfly_load<-1, 16, S::n / 16, LOG2N>(work, tab, v, j);
     // ---- spectral products
 #pragma unroll
     for (int r = 0; r < 16; ++r) {
-      const uint32_t e = j + r * stride;
-      const float2 a = acc[e];
-      acc[e] = cadd(a, cconjmul(v[r], gv[r]));
+      const uint32_t e = j + r * S::stride;
+      acc[e] = cadd(acc[e], cconjmul(v[r], gv[r]));
       v[r] = cmulc(gv[r], __ldg(kh + e));
     }
     // ---- du = IFFT(DY conj(kf)) + D dy
     dft_reg<+1, 16>(v);
     __syncthreads();
-    stockham_store<16>(smem, v, j, 0, 1, 1);
+    bfly_store<16, 1>(work, v, j);
     __syncthreads();
-    smem_passes<+1, SMALL>(smem, n, 1, 16, stride, tw);
-    stockham_load_twiddle<+1, 16>(smem, v, j, 0, n, 1, stride, tw);
-    dft_reg<+1, 16>(v);
+    mid_passes<+1, LOG2N, 16>(work, tab);
+    bfly_load<+1, 16, S::n / 16, LOG2N>(work, tab, v, j);
+    IO* d0 = du + ((size_t)b0 * H + h) * N;
+    IO* d1 = du + ((size_t)b1 * H + h) * N;
 #pragma unroll
     for (int r = 0; r < 16; ++r) {
-      const uint32_t t = j + r * stride;
+      const uint32_t t = j + r * S::stride;
       if (t < N) {
-        st(du + off0 + t, fmaf(d, ld(dy + off0 + t), v[r].x));
-        if (has1) st(du + off1 + t, fmaf(d, ld(dy + off1 + t), v[r].y));
+        st(d0 + t, fmaf(d, tof(g0[t]), v[r].x));
+        if (has1) st(d1 + t, fmaf(d, tof(g1[t]), v[r].y));
       }
     }
+    __syncthreads();
+    if (NBUF == 1 && tma && pr + 1 < p1) issue(pr + 1, 0);
   }
   // partial spectra + dD (deterministic block reduction)
-  float2* sp = spart + ((size_t)h * chunks + chunk) * n;
+  float2* sp = spart + ((size_t)h * chunks + chunk) * S::n;
 #pragma unroll
-  for (int r = 0; r < 16; ++r) sp[j + r * stride] = acc[j + r * stride];
+  for (int r = 0; r < 16; ++r) sp[j + r * S::stride] = acc[j + r * S::stride];
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) dd += __shfl_xor_sync(0xffffffffu, dd, o);
   if ((j & 31) == 0) red[j >> 5] = dd;
   __syncthreads();
   if (j == 0) {
     float t = 0.f;
-    for (uint32_t w = 0; w < (blockDim.x + 31) / 32; ++w) t += red[w];
+    for (uint32_t w = 0; w < (S::T + 31) / 32; ++w) t += red[w];
     ddpart[(size_t)h * chunks + chunk] = t;
   }
 }
 
 // dKbar[h][t] = scale * Re IFFT(sum_c spart[h][c])[t] / n ; dD[h] = sum_c ddpart.
-template <int SMALL>
-__global__ void __launch_bounds__(512) sp_dk_finalize_kernel(
-    const float2* __restrict__ spart, const float* __restrict__ ddpart, int chunks,
-    float* __restrict__ dkbar, float* __restrict__ dD, const float2* __restrict__ tw, uint32_t N,
-    uint32_t n, float scale) {
-  extern __shared__ float2 smem[];
-  const uint32_t h = blockIdx.x, j = threadIdx.x, stride = n / 16;
+template <int LOG2N>
+__global__ void __launch_bounds__(FftShape<LOG2N>::T, 1)
+    sp_dk_finalize_kernel(const float2* __restrict__ spart, const float* __restrict__ ddpart,
+                          int chunks, float* __restrict__ dkbar, float* __restrict__ dD,
+                          const float2* __restrict__ tab_g, uint32_t N, float scale) {
+  using S = FftShape<LOG2N>;
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  float2* work = reinterpret_cast<float2*>(smem_raw);
+  float2* tab = work + S::work_len;
+  const uint32_t h = blockIdx.x, j = threadIdx.x;
+  load_table<LOG2N>(tab, tab_g);
   float2 v[16];
 #pragma unroll
   for (int r = 0; r < 16; ++r) v[r] = make_float2(0.f, 0.f);
   for (int c = 0; c < chunks; ++c) {
-    const float2* sp = spart + ((size_t)h * chunks + c) * n;
+    const float2* sp = spart + ((size_t)h * chunks + c) * S::n;
 #pragma unroll
-    for (int r = 0; r < 16; ++r) v[r] = cadd(v[r], __ldg(sp + j + r * stride));
+    for (int r = 0; r < 16; ++r) v[r] = cadd(v[r], __ldg(sp + j + r * S::stride));
   }
   dft_reg<+1, 16>(v);
-  stockham_store<16>(smem, v, j, 0, 1, 1);
+  bfly_store<16, 1>(work, v, j);
   __syncthreads();
-  smem_passes<+1, SMALL>(smem, n, 1, 16, stride, tw);
-  stockham_load_twiddle<+1, 16>(smem, v, j, 0, n, 1, stride, tw);
-  dft_reg<+1, 16>(v);
-  const float s = scale / (float)n;
+  mid_passes<+1, LOG2N, 16>(work, tab);
+  bfly_load<+1, 16, S::n / 16, LOG2N>(work, tab, v, j);
+  const float s = scale / (float)S::n;
 #pragma unroll
   for (int r = 0; r < 16; ++r) {
-    const uint32_t t = j + r * stride;
+    const uint32_t t = j + r * S::stride;
     if (t < N) dkbar[(size_t)h * N + t] = v[r].x * s;
   }
   if (j == 0) {
@@ -256,55 +379,91 @@ int log2i(int64_t n) {
   return k;
 }
 
-template <int SMALL>
-struct SpKernels {
+template <typename IO>
+size_t stage_bytes(uint32_t N, int rows) {
+  return (size_t)rows * row_pitch<IO>(N) * sizeof(IO);
+}
+
+template <int LOG2N>
+size_t base_smem(bool with_n_extra) {
+  using S = FftShape<LOG2N>;
+  return (S::work_len + (with_n_extra ? S::n : 0) + ((S::tab_len + 1) & ~1u)) * sizeof(float2);
+}
+
+constexpr size_t kMaxSmem = 227 * 1024;
+
+bool rows_aligned(const void* a, const void* b, uint32_t N, size_t es) {
+  return ((N * es) % 16 == 0) && ((uintptr_t)a % 16 == 0) && (b == nullptr || (uintptr_t)b % 16 == 0);
+}
+
+template <int LOG2N>
+struct Sp {
   template <typename IO>
-  static void fwd(dim3 g, dim3 b, size_t sm, cudaStream_t s, const void* u, void* y,
-                  const fb_plan* p, int B) {
-    auto k = sp_fwd_kernel<IO, SMALL>;
+  static void fwd(cudaStream_t s, const fb_plan* p, const void* u, void* y, int B, int chunks,
+                  int ppc) {
+    const size_t sm = base_smem<LOG2N>(true) + stage_bytes<IO>((uint32_t)p->N, 4);
+    auto k = sp_fwd_kernel<IO, LOG2N>;
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-    k<<<g, b, sm, s>>>((const IO*)u, (IO*)y, p->kf, p->d, p->tw_n, B, (int)p->H, (uint32_t)p->N,
-                       (uint32_t)p->n, p->periodic ? 1 : 0);
+    const int tma = rows_aligned(u, nullptr, (uint32_t)p->N, sizeof(IO)) ? 1 : 0;
+    k<<<dim3((unsigned)p->H, (unsigned)chunks), FftShape<LOG2N>::T, sm, s>>>(
+        (const IO*)u, (IO*)y, p->kf, p->d, p->tw2, B, (int)p->H, (uint32_t)p->N,
+        p->periodic ? 1 : 0, ppc, tma);
   }
   template <typename IO>
-  static void bwd(dim3 g, dim3 b, size_t sm, cudaStream_t s, const void* dy, const void* u,
-                  void* du, const fb_plan* p, float2* spart, float* ddpart, int B, int ppc) {
-    auto k = sp_bwd_kernel<IO, SMALL>;
-    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-    k<<<g, b, sm, s>>>((const IO*)dy, (const IO*)u, (IO*)du, p->kf, p->d, p->tw_n, spart, ddpart,
-                       B, (int)p->H, (uint32_t)p->N, (uint32_t)p->n, p->periodic ? 1 : 0, ppc);
+  static void bwd(cudaStream_t s, const fb_plan* p, const void* dy, const void* u, void* du,
+                  float2* spart, float* ddpart, int B, int chunks, int ppc) {
+    const size_t sm2 = base_smem<LOG2N>(true) + stage_bytes<IO>((uint32_t)p->N, 8);
+    const int tma = rows_aligned(dy, u, (uint32_t)p->N, sizeof(IO)) ? 1 : 0;
+    const dim3 g((unsigned)p->H, (unsigned)chunks);
+    if (sm2 <= kMaxSmem) {
+      auto k = sp_bwd_kernel<IO, LOG2N, 2>;
+      cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm2);
+      k<<<g, FftShape<LOG2N>::T, sm2, s>>>((const IO*)dy, (const IO*)u, (IO*)du, p->kf, p->d,
+                                           p->tw2, spart, ddpart, B, (int)p->H, (uint32_t)p->N,
+                                           p->periodic ? 1 : 0, ppc, tma);
+    } else {
+      const size_t sm1 = base_smem<LOG2N>(true) + stage_bytes<IO>((uint32_t)p->N, 4);
+      auto k = sp_bwd_kernel<IO, LOG2N, 1>;
+      cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm1);
+      k<<<g, FftShape<LOG2N>::T, sm1, s>>>((const IO*)dy, (const IO*)u, (IO*)du, p->kf, p->d,
+                                           p->tw2, spart, ddpart, B, (int)p->H, (uint32_t)p->N,
+                                           p->periodic ? 1 : 0, ppc, tma);
+    }
   }
-  static void spectrum(dim3 g, dim3 b, size_t sm, cudaStream_t s, const fb_plan* p) {
-    auto k = sp_spectrum_kernel<SMALL>;
+  static void spectrum(cudaStream_t s, const fb_plan* p) {
+    const size_t sm = base_smem<LOG2N>(false);
+    auto k = sp_spectrum_kernel<LOG2N>;
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-    k<<<g, b, sm, s>>>(p->kbar, p->kf, p->tw_n, (uint32_t)p->N, (uint32_t)p->n);
+    k<<<(unsigned)p->H, FftShape<LOG2N>::T, sm, s>>>(p->kbar, p->kf, p->tw2, (uint32_t)p->N);
   }
-  static void finalize(dim3 g, dim3 b, size_t sm, cudaStream_t s, const fb_plan* p,
-                       const float2* spart, const float* ddpart, int chunks, float* dkbar,
-                       float* dD) {
-    auto k = sp_dk_finalize_kernel<SMALL>;
+  static void finalize(cudaStream_t s, const fb_plan* p, const float2* spart, const float* ddpart,
+                       int chunks, float* dkbar, float* dD) {
+    const size_t sm = base_smem<LOG2N>(false);
+    auto k = sp_dk_finalize_kernel<LOG2N>;
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     const float scale = p->periodic ? (float)p->N / (float)p->n : 1.0f;
-    k<<<g, b, sm, s>>>(spart, ddpart, chunks, dkbar, dD, p->tw_n, (uint32_t)p->N,
-                       (uint32_t)p->n, scale);
+    k<<<(unsigned)p->H, FftShape<LOG2N>::T, sm, s>>>(spart, ddpart, chunks, dkbar, dD, p->tw2,
+                                                      (uint32_t)p->N, scale);
   }
 };
 
 template <class F>
-void with_small(int64_t n, F&& f) {
-  switch (log2i(n) % 4) {
-    case 0: f(SpKernels<1>{}); break;
-    case 1: f(SpKernels<2>{}); break;
-    case 2: f(SpKernels<4>{}); break;
-    default: f(SpKernels<8>{}); break;
+void with_log2n(int64_t n, F&& f) {
+  switch (log2i(n)) {
+    case 8: f(Sp<8>{}); break;
+    case 9: f(Sp<9>{}); break;
+    case 10: f(Sp<10>{}); break;
+    case 11: f(Sp<11>{}); break;
+    case 12: f(Sp<12>{}); break;
+    default: f(Sp<13>{}); break;
   }
 }
 
+// Split the channel pairs of a head into chunks (CTAs per head): enough CTAs
+// for ~1 wave while keeping each CTA's k_f staging amortised.
 int chunks_for(const fb_plan* p, int64_t B) {
-  // enough CTAs to cover the SMs ~2x while keeping the per-head reduction
-  // short; each chunk owns >= 1 pair.
   const int64_t npairs = (B + 1) / 2;
-  int64_t c = (2 * p->num_sms + p->H - 1) / p->H;
+  int64_t c = (p->num_sms + p->H - 1) / p->H;
   c = std::max<int64_t>(1, std::min<int64_t>(c, npairs));
   return (int)c;
 }
@@ -314,19 +473,19 @@ int chunks_for(const fb_plan* p, int64_t B) {
 int sp_prep(fb_plan* p, const float* K, cudaStream_t s) {
   int rc = regularize_bank_dev(p, K, s);
   if (rc) return rc;
-  const size_t sm = padded_len((uint32_t)p->n) * sizeof(float2);
-  with_small(p->n, [&](auto ks) { ks.spectrum(dim3((unsigned)p->H), dim3((unsigned)(p->n / 16)), sm, s, p); });
+  with_log2n(p->n, [&](auto ks) { ks.spectrum(s, p); });
   return cuda_status(cudaGetLastError(), "sp_prep");
 }
 
 int sp_fwd(fb_plan* p, const void* u, void* y, int64_t B, cudaStream_t s) {
-  const size_t sm = padded_len((uint32_t)p->n) * sizeof(float2);
-  const dim3 g((unsigned)p->H, (unsigned)((B + 1) / 2)), b((unsigned)(p->n / 16));
-  with_small(p->n, [&](auto ks) {
+  const int chunks = chunks_for(p, B);
+  const int64_t npairs = (B + 1) / 2;
+  const int ppc = (int)((npairs + chunks - 1) / chunks);
+  with_log2n(p->n, [&](auto ks) {
     switch (p->dtype) {
-      case FB_F32: ks.template fwd<float>(g, b, sm, s, u, y, p, (int)B); break;
-      case FB_BF16: ks.template fwd<__nv_bfloat16>(g, b, sm, s, u, y, p, (int)B); break;
-      default: ks.template fwd<__half>(g, b, sm, s, u, y, p, (int)B); break;
+      case FB_F32: ks.template fwd<float>(s, p, u, y, (int)B, chunks, ppc); break;
+      case FB_BF16: ks.template fwd<__nv_bfloat16>(s, p, u, y, (int)B, chunks, ppc); break;
+      default: ks.template fwd<__half>(s, p, u, y, (int)B, chunks, ppc); break;
     }
   });
   return cuda_status(cudaGetLastError(), "sp_fwd");
@@ -353,16 +512,13 @@ int sp_bwd(fb_plan* p, const void* dy, const void* u, void* du, float* dK, float
   off += (size_t)p->H * chunks * sizeof(float);
   off = (off + 255) & ~size_t(255);
   float* dkbar = dKbar ? dKbar : (float*)(w + off);
-  const size_t sm1 = padded_len((uint32_t)p->n) * sizeof(float2);
-  const size_t smb = sm1 + p->n * sizeof(float2);
-  const dim3 g((unsigned)p->H, (unsigned)chunks), b((unsigned)(p->n / 16));
-  with_small(p->n, [&](auto ks) {
+  with_log2n(p->n, [&](auto ks) {
     switch (p->dtype) {
-      case FB_F32: ks.template bwd<float>(g, b, smb, s, dy, u, du, p, spart, ddpart, (int)B, ppc); break;
-      case FB_BF16: ks.template bwd<__nv_bfloat16>(g, b, smb, s, dy, u, du, p, spart, ddpart, (int)B, ppc); break;
-      default: ks.template bwd<__half>(g, b, smb, s, dy, u, du, p, spart, ddpart, (int)B, ppc); break;
+      case FB_F32: ks.template bwd<float>(s, p, dy, u, du, spart, ddpart, (int)B, chunks, ppc); break;
+      case FB_BF16: ks.template bwd<__nv_bfloat16>(s, p, dy, u, du, spart, ddpart, (int)B, chunks, ppc); break;
+      default: ks.template bwd<__half>(s, p, dy, u, du, spart, ddpart, (int)B, chunks, ppc); break;
     }
-    ks.finalize(dim3((unsigned)p->H), b, sm1, s, p, spart, ddpart, chunks, dkbar, dD);
+    ks.finalize(s, p, spart, ddpart, chunks, dkbar, dD);
   });
   int rc = cuda_status(cudaGetLastError(), "sp_bwd");
   if (rc) return rc;
