@@ -107,9 +107,16 @@ int fb_plan_create(fb_plan** out, int64_t N, int64_t H, int mode, int dtype, int
     return fail(FB_ERR_PLAN, "fb_plan_create: single-pass engine supports transforms up to " +
                                  std::to_string(kSinglePassMax) + " points; use three-pass");
   }
+  if (engine == FB_ENGINE_THREE && (n < 2 * kThreePassRow || n > 16 * kThreePassRow)) {
+    delete p;
+    return fail(FB_ERR_PLAN, "fb_plan_create: three-pass engine needs a transform of " +
+                                 std::to_string(2 * kThreePassRow) + ".." +
+                                 std::to_string(16 * kThreePassRow) + " points (l = " +
+                                 std::to_string(kThreePassRow) + ", m = 2..16)");
+  }
   p->engine = engine;
   if (engine == FB_ENGINE_THREE) {
-    p->l = std::min<int64_t>(n, kThreePassRow);
+    p->l = kThreePassRow;
     p->m = n / p->l;
   } else {
     p->l = n;
@@ -118,8 +125,7 @@ int fb_plan_create(fb_plan** out, int64_t N, int64_t H, int mode, int dtype, int
   cudaDeviceGetAttribute(&p->num_sms, cudaDevAttrMultiProcessorCount, device);
   rc = upload_twiddles(&p->tw_n, n);
   if (!rc) rc = upload_twiddles2(&p->tw2, n);
-  if (!rc && engine == FB_ENGINE_THREE) rc = upload_twiddles(&p->tw_l, p->l);
-  if (!rc && engine == FB_ENGINE_THREE) rc = upload_twiddles(&p->tw_m, std::max<int64_t>(p->m, 2));
+  if (!rc && engine == FB_ENGINE_THREE) rc = upload_twiddles2(&p->tw_l, p->l);
   if (!rc) rc = cuda_status(cudaMalloc(&p->kf, sizeof(float2) * H * n), "cudaMalloc(kf)");
   if (!rc) rc = cuda_status(cudaMalloc(&p->kbar, sizeof(float) * H * N), "cudaMalloc(kbar)");
   if (!rc) rc = cuda_status(cudaMalloc(&p->d, sizeof(float) * H), "cudaMalloc(D)");
@@ -136,7 +142,6 @@ int fb_plan_destroy(fb_plan* p) {
   cudaFree(p->tw_n);
   cudaFree(p->tw2);
   cudaFree(p->tw_l);
-  cudaFree(p->tw_m);
   cudaFree(p->kf);
   cudaFree(p->kbar);
   cudaFree(p->keep);

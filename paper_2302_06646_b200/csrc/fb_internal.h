@@ -15,8 +15,7 @@ struct fb_plan {
   bool periodic = false;  // circular with n > N: u periodically extended
   float2* tw_n = nullptr;  // exp(-2 pi i t / n), t < n
   float2* tw2 = nullptr;   // two-level table for n: [w^i, i<64 | w^(64 i), i<n/64]
-  float2* tw_l = nullptr;  // exp(-2 pi i t / l), t < l   (three-pass)
-  float2* tw_m = nullptr;  // exp(-2 pi i t / m), t < m   (three-pass)
+  float2* tw_l = nullptr;  // two-level table for l (three-pass pass 2)
   float2* kf = nullptr;    // per-head spectrum / n: single [H][n]; three [H][m][l]
   float* kbar = nullptr;   // [H][N] regularized kernels
   uint8_t* keep = nullptr; // [H][N] dropout keep flags (training only)

@@ -1,8 +1,509 @@
-// FlashButterfly-B200 three-pass engine (placeholder; implemented next).
+// FlashButterfly-B200 three-pass engine (K3 forward, K4b backward, K1
+// spectrum in the pass-2 layout) for transforms beyond shared memory:
+// n = l * m with l = 8192 (the row length the single-pass machinery runs
+// on-chip) and m in {2, 4, 8, 16} (n = 16K ... 128K, i.e. N = 8K ... 64K causal).
+//
+// Reference: conv_three_pass_ordered (proj/src/three_pass.cpp:225-254) with
+// BlockDiagonalButterfly::apply (:101-122) as passes 1/3, middle_block
+// (:211-221) as pass 2 and build_three_pass's d_k (:197-203) as the pass-2
+// kernel spectrum.  With t = c*l + tau and f = a + m*s:
+//   pass 1  X1[a][tau] = w_n^(-a tau) sum_c w_m^(-a c) x[c l + tau]
+//           (m-point DFT down each column tau, then the twiddle)
+//   pass 2  per row a: Z = FFT_l(X1[a]) = X[a + m s]; Z *= Kf2[a][s];
+//           W[a] = IFFT_l(Z)   (Kf2[h][a][s] = K_hat[a + m s] / n)
+//   pass 3  y[c l + tau] = sum_a w_m^(+a c) w_n^(+a tau) W[a][tau]
+// The reference's B^T / B^-1^T factors are exactly passes 1 and 3 (entry
+// exp(-2 pi i k (j l + tau)/n), three_pass.hpp:71-75); its d_k = l K_hat
+// permuted is Kf2 up to the 1/(l n) normalisation folded here.
+// Each pass streams the buffer once with coalesced, vectorised accesses:
+// passes 1/3 give one column tau per thread (consecutive threads =
+// consecutive tau), pass 2 moves whole rows by TMA bulk copies.
+#include <algorithm>
+
+#include "fb_common.cuh"
+#include "fb_fft.cuh"
 #include "fb_internal.h"
+#include "fb_ptx.cuh"
+
 namespace fb {
-int tp_prep(fb_plan*, const float*, cudaStream_t) { set_error("three-pass: not built yet"); return FB_ERR_UNSUPPORTED; }
-int tp_fwd(fb_plan*, const void*, void*, int64_t, void*, cudaStream_t) { set_error("three-pass: not built yet"); return FB_ERR_UNSUPPORTED; }
-size_t tp_workspace(const fb_plan*, int64_t) { return 256; }
-int tp_bwd(fb_plan*, const void*, const void*, void*, float*, float*, float*, int64_t, void*, cudaStream_t) { set_error("three-pass: not built yet"); return FB_ERR_UNSUPPORTED; }
+
+constexpr int kL2 = 13;  // log2(l)
+constexpr uint32_t kL = 1u << kL2;
+constexpr int kColThreads = 256;
+
+// complex storage element of the intermediates
+template <typename ST>
+struct CxT {
+  ST x, y;
+};
+
+// ---------------------------------------------------------------- pass 1
+// grid (l/256, H, npairs [or 1 for the kernel spectrum]).  SRC: 0 = signal
+// pairs (real channels b0, b1 -> re, im); 1 = two signals (dy, u) at once
+// with the dD partial; 2 = the regularized kernel bank (fp32, one channel).
+template <typename IO, typename ST, int M, int SRC>
+__global__ void __launch_bounds__(kColThreads)
+    tp_pass1_kernel(const IO* __restrict__ a_in, const IO* __restrict__ b_in,
+                    const float* __restrict__ kbar, CxT<ST>* __restrict__ out_a,
+                    CxT<ST>* __restrict__ out_b, float* __restrict__ ddpart,
+                    const float2* __restrict__ tab_g, int B, int H, uint32_t N, int causal) {
+  __shared__ float2 tab[64 + (kL * M) / 64];
+  __shared__ float red[kColThreads / 32];
+  for (uint32_t i = threadIdx.x; i < 64 + (kL * M) / 64; i += blockDim.x) tab[i] = __ldg(tab_g + i);
+  __syncthreads();
+  const uint32_t tau = blockIdx.x * kColThreads + threadIdx.x;
+  const int h = blockIdx.y, pr = blockIdx.z;
+  const int b0 = 2 * pr, b1 = b0 + 1;
+  const bool has1 = b1 < B;
+  constexpr int MH = M;  // rows that can hold data
+  const int cmax = causal ? M / 2 : M;
+  float dd = 0.f;
+  auto column = [&](const IO* src, float2 (&v)[M]) {
+    const IO* r0 = src + ((size_t)b0 * H + h) * N;
+    const IO* r1 = src + ((size_t)b1 * H + h) * N;
+#pragma unroll
+    for (int c = 0; c < MH; ++c) {
+      const uint32_t t = c * kL + tau;
+      const bool ok = c < cmax && t < N;
+      v[c].x = ok ? ld(r0 + t) : 0.f;
+      v[c].y = (ok && has1) ? ld(r1 + t) : 0.f;
+    }
+  };
+  float2 v[M];
+  if constexpr (SRC == 2) {
+    const float* kr = kbar + (size_t)h * N;
+#pragma unroll
+    for (int c = 0; c < M; ++c) {
+      const uint32_t t = c * kL + tau;
+      v[c] = make_float2((c < cmax && t < N) ? __ldg(kr + t) : 0.f, 0.f);
+    }
+  } else {
+    column(a_in, v);
+  }
+  if constexpr (SRC == 1) {
+    float2 w[M];
+    column(b_in, w);
+#pragma unroll
+    for (int c = 0; c < M; ++c) dd = fmaf(v[c].x, w[c].x, fmaf(v[c].y, w[c].y, dd));
+    dft_reg<-1, M>(w);
+    apply_tw<-1, M>(w, tab, tau);
+    CxT<ST>* ob = out_b + ((size_t)pr * H + h) * (size_t)M * kL;
+#pragma unroll
+    for (int a = 0; a < M; ++a) stc<ST>(&ob[a * kL + tau].x, w[a]);
+  }
+  dft_reg<-1, M>(v);
+  apply_tw<-1, M>(v, tab, tau);
+  CxT<ST>* oa = out_a + ((size_t)pr * H + h) * (size_t)M * kL;
+#pragma unroll
+  for (int a = 0; a < M; ++a) stc<ST>(&oa[a * kL + tau].x, v[a]);
+  if constexpr (SRC == 1) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) dd += __shfl_xor_sync(0xffffffffu, dd, o);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = dd;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      float t = 0.f;
+      for (int w = 0; w < kColThreads / 32; ++w) t += red[w];
+      ddpart[((size_t)h * gridDim.z + pr) * gridDim.x + blockIdx.x] = t;
+    }
+  }
 }
+
+// ---------------------------------------------------------------- pass 2
+template <typename ST>
+__device__ __forceinline__ void stage_row(CxT<ST>* dst, const CxT<ST>* src, uint64_t* bar) {
+  if (threadIdx.x == 0) {
+    constexpr uint32_t bytes = kL * sizeof(CxT<ST>);
+    ptx::fence_proxy_async_smem();
+    ptx::mbar_arrive_expect_tx(bar, bytes);
+    ptx::bulk_g2s(dst, src, bytes, bar);
+  }
+}
+
+__device__ __forceinline__ float2 cx_load(const CxT<float>* p) { return *reinterpret_cast<const float2*>(p); }
+__device__ __forceinline__ float2 cx_load(const CxT<__nv_bfloat16>* p) {
+  return __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(p));
+}
+__device__ __forceinline__ float2 cx_load(const CxT<__half>* p) {
+  return __half22float2(*reinterpret_cast<const __half2*>(p));
+}
+
+// MODE 0: forward rows  W = IFFT(FFT(X1 row) * Kf2[h][a])   (in place)
+// MODE 1: spectrum      Kf2[h][a] = FFT(X1k row) / n
+// grid (H*m, chunks); rows of pair pr: X1[((pr*H + h)*m + a)*l ...].
+template <typename ST, int MODE>
+__global__ void __launch_bounds__(kL / 16, 1)
+    tp_pass2_kernel(CxT<ST>* __restrict__ x1, const float2* __restrict__ kf2,
+                    float2* __restrict__ kf2_out, const float2* __restrict__ tab_g, int npairs,
+                    int H, int m, int ppc, float inv_n) {
+  using S = FftShape<kL2>;
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  __shared__ __align__(8) uint64_t bars[2];
+  // k_f row staged in smem for 16-bit storage; fp32 rows need the room for
+  // the double-buffered stage, so k_f is read through L2 there.
+  constexpr bool KF_SMEM = sizeof(ST) < 4;
+  float2* work = reinterpret_cast<float2*>(smem_raw);
+  float2* kfs = work + S::work_len;
+  float2* tab = kfs + (KF_SMEM ? S::n : 0);
+  CxT<ST>* stage = reinterpret_cast<CxT<ST>*>(tab + ((S::tab_len + 1) & ~1u));  // [2][l]
+  const int ha = blockIdx.x, h = ha / m, a = ha % m;
+  const uint32_t j = threadIdx.x;
+  const float2* kfg = kf2 + (size_t)ha * S::n;
+  const int p0 = blockIdx.y * ppc, p1 = min(npairs, p0 + ppc);
+  if (p0 >= p1) return;
+  if (j == 0) {
+    ptx::mbar_init(&bars[0], 1);
+    ptx::mbar_init(&bars[1], 1);
+    ptx::fence_barrier_init();
+  }
+  for (uint32_t i = j; i < S::tab_len; i += S::T) tab[i] = __ldg(tab_g + i);
+  if constexpr (MODE == 0 && KF_SMEM) {
+    const float4* src = reinterpret_cast<const float4*>(kfg);
+    float4* dst = reinterpret_cast<float4*>(kfs);
+    for (uint32_t i = j; i < S::n / 2; i += S::T) dst[i] = __ldg(src + i);
+  }
+  __syncthreads();
+  auto row_ptr = [&](int pr) { return x1 + ((size_t)pr * H + h) * (size_t)m * kL + (size_t)a * kL; };
+  stage_row<ST>(stage, row_ptr(p0), &bars[0]);
+  for (int pr = p0, it = 0; pr < p1; ++pr, ++it) {
+    const int buf = it & 1;
+    ptx::mbar_wait(&bars[buf], (it >> 1) & 1);
+    if (pr + 1 < p1) stage_row<ST>(stage + (buf ^ 1) * kL, row_ptr(pr + 1), &bars[buf ^ 1]);
+    const CxT<ST>* srow = stage + buf * kL;
+    float2 v[16];
+#pragma unroll
+    for (int r = 0; r < 16; ++r) v[r] = cx_load(srow + j + r * S::stride);
+    dft_reg<-1, 16>(v);
+    bfly_store<16, 1>(work, v, j);
+    __syncthreads();
+    mid_passes<-1, kL2, 16>(work, tab);
+    bfly_load<-1, 16, S::n / 16, kL2>(work, tab, v, j);
+    if constexpr (MODE == 1) {
+      float2* out = kf2_out + (size_t)ha * S::n;
+#pragma unroll
+      for (int r = 0; r < 16; ++r) out[j + r * S::stride] = cscale(v[r], inv_n);
+    } else {
+#pragma unroll
+      for (int r = 0; r < 16; ++r)
+        v[r] = cmul(v[r], KF_SMEM ? kfs[j + r * S::stride] : __ldg(kfg + j + r * S::stride));
+      dft_reg<+1, 16>(v);
+      __syncthreads();
+      bfly_store<16, 1>(work, v, j);
+      __syncthreads();
+      mid_passes<+1, kL2, 16>(work, tab);
+      bfly_load<+1, 16, S::n / 16, kL2>(work, tab, v, j);
+      CxT<ST>* orow = row_ptr(pr);
+#pragma unroll
+      for (int r = 0; r < 16; ++r) stc<ST>(&orow[j + r * S::stride].x, v[r]);
+    }
+    __syncthreads();
+  }
+}
+
+// Backward middle pass, CTA (h, a) over ALL pairs (so the dK spectrum of row
+// a is complete in one CTA, fixed order => deterministic):
+//   DY = FFT(X1dy), U = FFT(X1u); acc += conj(U) DY; X1dy <- IFFT(DY conj(Kf2))
+//   finally wdk[h][a] = IFFT(acc)  (fp32)
+template <typename ST>
+__global__ void __launch_bounds__(kL / 16, 1)
+    tp_pass2_bwd_kernel(CxT<ST>* __restrict__ x1dy, const CxT<ST>* __restrict__ x1u,
+                        const float2* __restrict__ kf2, float2* __restrict__ wdk,
+                        const float2* __restrict__ tab_g, int npairs, int H, int m) {
+  using S = FftShape<kL2>;
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  __shared__ __align__(8) uint64_t bars[1];
+  float2* work = reinterpret_cast<float2*>(smem_raw);
+  float2* acc = work + S::work_len;
+  float2* tab = acc + S::n;
+  CxT<ST>* stage = reinterpret_cast<CxT<ST>*>(tab + ((S::tab_len + 1) & ~1u));  // [l]
+  const int ha = blockIdx.x, h = ha / m, a = ha % m;
+  const uint32_t j = threadIdx.x;
+  const float2* kh = kf2 + (size_t)ha * S::n;
+  if (j == 0) {
+    ptx::mbar_init(&bars[0], 1);
+    ptx::fence_barrier_init();
+  }
+  for (uint32_t i = j; i < S::tab_len; i += S::T) tab[i] = __ldg(tab_g + i);
+#pragma unroll
+  for (int r = 0; r < 16; ++r) acc[j + r * S::stride] = make_float2(0.f, 0.f);
+  __syncthreads();
+  auto rp = [&](const CxT<ST>* base, int pr) {
+    return base + ((size_t)pr * H + h) * (size_t)m * kL + (size_t)a * kL;
+  };
+  uint32_t phase = 0;
+  if (npairs > 0) stage_row<ST>(stage, rp(x1dy, 0), &bars[0]);
+  for (int pr = 0; pr < npairs; ++pr) {
+    float2 gv[16], v[16];
+    ptx::mbar_wait(&bars[0], phase);
+    phase ^= 1;
+#pragma unroll
+    for (int r = 0; r < 16; ++r) v[r] = cx_load(stage + j + r * S::stride);
+    __syncthreads();  // stage consumed
+    stage_row<ST>(stage, rp(x1u, pr), &bars[0]);
+    dft_reg<-1, 16>(v);
+    bfly_store<16, 1>(work, v, j);
+    __syncthreads();
+    mid_passes<-1, kL2, 16>(work, tab);
+    bfly_load<-1, 16, S::n / 16, kL2>(work, tab, gv, j);
+    ptx::mbar_wait(&bars[0], phase);
+    phase ^= 1;
+#pragma unroll
+    for (int r = 0; r < 16; ++r) v[r] = cx_load(stage + j + r * S::stride);
+    dft_reg<-1, 16>(v);
+    __syncthreads();
+    if (pr + 1 < npairs) stage_row<ST>(stage, rp(x1dy, pr + 1), &bars[0]);
+    bfly_store<16, 1>(work, v, j);
+    __syncthreads();
+    mid_passes<-1, kL2, 16>(work, tab);
+    bfly_load<-1, 16, S::n / 16, kL2>(work, tab, v, j);
+#pragma unroll
+    for (int r = 0; r < 16; ++r) {
+      const uint32_t e = j + r * S::stride;
+      acc[e] = cadd(acc[e], cconjmul(v[r], gv[r]));
+      v[r] = cmulc(gv[r], __ldg(kh + e));
+    }
+    dft_reg<+1, 16>(v);
+    __syncthreads();
+    bfly_store<16, 1>(work, v, j);
+    __syncthreads();
+    mid_passes<+1, kL2, 16>(work, tab);
+    bfly_load<+1, 16, S::n / 16, kL2>(work, tab, v, j);
+    CxT<ST>* orow = const_cast<CxT<ST>*>(rp(x1dy, pr));
+#pragma unroll
+    for (int r = 0; r < 16; ++r) stc<ST>(&orow[j + r * S::stride].x, v[r]);
+    __syncthreads();
+  }
+  // dK spectrum row -> IFFT_l -> wdk (fp32)
+  float2 v[16];
+#pragma unroll
+  for (int r = 0; r < 16; ++r) v[r] = acc[j + r * S::stride];
+  dft_reg<+1, 16>(v);
+  __syncthreads();
+  bfly_store<16, 1>(work, v, j);
+  __syncthreads();
+  mid_passes<+1, kL2, 16>(work, tab);
+  bfly_load<+1, 16, S::n / 16, kL2>(work, tab, v, j);
+  float2* orow = wdk + (size_t)ha * S::n;
+#pragma unroll
+  for (int r = 0; r < 16; ++r) orow[j + r * S::stride] = v[r];
+}
+
+// ---------------------------------------------------------------- pass 3
+// MODE 0: signal pairs -> out[b][h][t] = y + D * skip[b][h][t]
+// MODE 1: dK row per head (fp32 complex) -> dkbar[h][t] = Re(.) * scale
+template <typename ST, typename IO, int M, int MODE>
+__global__ void __launch_bounds__(kColThreads)
+    tp_pass3_kernel(const CxT<ST>* __restrict__ w_in, const IO* __restrict__ skip,
+                    IO* __restrict__ out, const float* __restrict__ D, float* __restrict__ dkbar,
+                    const float2* __restrict__ tab_g, int B, int H, uint32_t N, int causal,
+                    float scale) {
+  __shared__ float2 tab[64 + (kL * M) / 64];
+  for (uint32_t i = threadIdx.x; i < 64 + (kL * M) / 64; i += blockDim.x) tab[i] = __ldg(tab_g + i);
+  __syncthreads();
+  const uint32_t tau = blockIdx.x * kColThreads + threadIdx.x;
+  const int h = blockIdx.y, pr = blockIdx.z;
+  float2 v[M];
+  const CxT<ST>* src = w_in + ((size_t)pr * H + h) * (size_t)M * kL;
+#pragma unroll
+  for (int a = 0; a < M; ++a) v[a] = cx_load(src + a * kL + tau);
+  apply_tw<+1, M>(v, tab, tau);
+  dft_reg<+1, M>(v);
+  const int cmax = causal ? M / 2 : M;
+  if constexpr (MODE == 0) {
+    const int b0 = 2 * pr, b1 = b0 + 1;
+    const bool has1 = b1 < B;
+    const float d = __ldg(D + h);
+    const size_t o0 = ((size_t)b0 * H + h) * N, o1 = ((size_t)b1 * H + h) * N;
+#pragma unroll
+    for (int c = 0; c < M; ++c) {
+      const uint32_t t = c * kL + tau;
+      if (c < cmax && t < N) {
+        st(out + o0 + t, fmaf(d, ld(skip + o0 + t), v[c].x));
+        if (has1) st(out + o1 + t, fmaf(d, ld(skip + o1 + t), v[c].y));
+      }
+    }
+  } else {
+#pragma unroll
+    for (int c = 0; c < M; ++c) {
+      const uint32_t t = c * kL + tau;
+      if (c < cmax && t < N) dkbar[(size_t)h * N + t] = v[c].x * scale;
+    }
+  }
+}
+
+__global__ void tp_dd_reduce_kernel(const float* __restrict__ ddpart, float* __restrict__ dD,
+                                    int per_head) {
+  const int h = blockIdx.x;
+  if (threadIdx.x == 0) {
+    float t = 0.f;
+    for (int i = 0; i < per_head; ++i) t += ddpart[(size_t)h * per_head + i];
+    dD[h] = t;
+  }
+}
+
+// ---------------------------------------------------------------- host side
+namespace {
+
+template <typename ST>
+size_t pass2_smem() {
+  using S = FftShape<kL2>;
+  return (S::work_len + (sizeof(ST) < 4 ? S::n : 0) + ((S::tab_len + 1) & ~1u)) * sizeof(float2) +
+         2 * kL * sizeof(CxT<ST>);
+}
+template <typename ST>
+size_t pass2_bwd_smem() {
+  using S = FftShape<kL2>;
+  return (S::work_len + S::n + ((S::tab_len + 1) & ~1u)) * sizeof(float2) + kL * sizeof(CxT<ST>);
+}
+
+template <class F>
+void with_m(int64_t m, F&& f) {
+  switch (m) {
+    case 2: f(std::integral_constant<int, 2>{}); break;
+    case 4: f(std::integral_constant<int, 4>{}); break;
+    case 8: f(std::integral_constant<int, 8>{}); break;
+    default: f(std::integral_constant<int, 16>{}); break;
+  }
+}
+template <class F>
+void with_io(int dtype, F&& f) {
+  switch (dtype) {
+    case FB_F32: f(float{}); break;
+    case FB_BF16: f(__nv_bfloat16{}); break;
+    default: f(__half{}); break;
+  }
+}
+
+size_t inter_bytes(const fb_plan* p, int64_t npairs) {
+  const size_t es = p->dtype == FB_F32 ? 8 : 4;  // complex storage element
+  return ((size_t)npairs * p->H * p->n * es + 255) & ~size_t(255);
+}
+
+int pass2_chunks(const fb_plan* p, int64_t npairs) {
+  const int64_t rows = p->H * p->m;
+  int64_t c = (p->num_sms + rows - 1) / rows;
+  return (int)std::max<int64_t>(1, std::min<int64_t>(c, npairs));
+}
+
+}  // namespace
+
+int tp_prep(fb_plan* p, const float* K, cudaStream_t s) {
+  int rc = regularize_bank_dev(p, K, s);
+  if (rc) return rc;
+  // kernel rows through pass 1 (fp32 storage) into a scratch, then spectrum
+  CxT<float>* x1k = nullptr;
+  rc = cuda_status(cudaMallocAsync(&x1k, (size_t)p->H * p->n * sizeof(CxT<float>), s),
+                   "cudaMallocAsync(tp_prep)");
+  if (rc) return rc;
+  const int causal = p->mode == FB_MODE_CAUSAL;
+  with_m(p->m, [&](auto mc) {
+    constexpr int M = decltype(mc)::value;
+    tp_pass1_kernel<float, float, M, 2><<<dim3(kL / kColThreads, (unsigned)p->H, 1), kColThreads, 0, s>>>(
+        nullptr, nullptr, p->kbar, x1k, nullptr, nullptr, p->tw2, 2, (int)p->H, (uint32_t)p->N,
+        causal);
+  });
+  const size_t sm = pass2_smem<float>();
+  auto k = tp_pass2_kernel<float, 1>;
+  cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+  k<<<dim3((unsigned)(p->H * p->m), 1), kL / 16, sm, s>>>(x1k, nullptr, p->kf, p->tw_l, 1,
+                                                          (int)p->H, (int)p->m, 1,
+                                                          1.0f / (float)p->n);
+  rc = cuda_status(cudaGetLastError(), "tp_prep");
+  cudaFreeAsync(x1k, s);
+  return rc;
+}
+
+size_t tp_workspace(const fb_plan* p, int64_t B) {
+  const int64_t npairs = (B + 1) / 2;
+  size_t bytes = 2 * inter_bytes(p, npairs);                            // X1dy/X1u (fwd: X1)
+  bytes += ((size_t)p->H * p->n * sizeof(float2) + 255) & ~size_t(255); // dK rows
+  bytes += ((size_t)p->H * p->N * sizeof(float) + 255) & ~size_t(255);  // dKbar scratch
+  bytes += ((size_t)p->H * npairs * (kL / kColThreads) * sizeof(float) + 255) & ~size_t(255);
+  return bytes + 256;
+}
+
+int tp_fwd(fb_plan* p, const void* u, void* y, int64_t B, void* ws, cudaStream_t s) {
+  const int64_t npairs = (B + 1) / 2;
+  const int causal = p->mode == FB_MODE_CAUSAL;
+  if (p->periodic) {
+    set_error("three-pass: circular mode needs N == n");
+    return FB_ERR_UNSUPPORTED;
+  }
+  with_io(p->dtype, [&](auto io) {
+    using IO = decltype(io);
+    using ST = IO;
+    auto* x1 = reinterpret_cast<CxT<ST>*>(ws);
+    with_m(p->m, [&](auto mc) {
+      constexpr int M = decltype(mc)::value;
+      tp_pass1_kernel<IO, ST, M, 0>
+          <<<dim3(kL / kColThreads, (unsigned)p->H, (unsigned)npairs), kColThreads, 0, s>>>(
+              (const IO*)u, nullptr, nullptr, x1, nullptr, nullptr, p->tw2, (int)B, (int)p->H,
+              (uint32_t)p->N, causal);
+      const size_t sm = pass2_smem<ST>();
+      auto k2 = tp_pass2_kernel<ST, 0>;
+      cudaFuncSetAttribute(k2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+      const int chunks = pass2_chunks(p, npairs);
+      const int ppc = (int)((npairs + chunks - 1) / chunks);
+      k2<<<dim3((unsigned)(p->H * p->m), (unsigned)chunks), kL / 16, sm, s>>>(
+          x1, p->kf, nullptr, p->tw_l, (int)npairs, (int)p->H, (int)p->m, ppc, 0.f);
+      tp_pass3_kernel<ST, IO, M, 0>
+          <<<dim3(kL / kColThreads, (unsigned)p->H, (unsigned)npairs), kColThreads, 0, s>>>(
+              x1, (const IO*)u, (IO*)y, p->d, nullptr, p->tw2, (int)B, (int)p->H, (uint32_t)p->N,
+              causal, 1.f);
+    });
+  });
+  return cuda_status(cudaGetLastError(), "tp_fwd");
+}
+
+int tp_bwd(fb_plan* p, const void* dy, const void* u, void* du, float* dK, float* dKbar, float* dD,
+           int64_t B, void* ws, cudaStream_t s) {
+  const int64_t npairs = (B + 1) / 2;
+  const int causal = p->mode == FB_MODE_CAUSAL;
+  if (p->periodic) {
+    set_error("three-pass: circular mode needs N == n");
+    return FB_ERR_UNSUPPORTED;
+  }
+  char* w = (char*)ws;
+  const size_t ib = inter_bytes(p, npairs);
+  char* x1dy_raw = w;
+  char* x1u_raw = w + ib;
+  float2* wdk = (float2*)(w + 2 * ib);
+  size_t off = 2 * ib + (((size_t)p->H * p->n * sizeof(float2) + 255) & ~size_t(255));
+  float* dkbar_s = (float*)(w + off);
+  off += ((size_t)p->H * p->N * sizeof(float) + 255) & ~size_t(255);
+  float* ddpart = (float*)(w + off);
+  float* dkbar = dKbar ? dKbar : dkbar_s;
+  with_io(p->dtype, [&](auto io) {
+    using IO = decltype(io);
+    using ST = IO;
+    auto* x1dy = reinterpret_cast<CxT<ST>*>(x1dy_raw);
+    auto* x1u = reinterpret_cast<CxT<ST>*>(x1u_raw);
+    with_m(p->m, [&](auto mc) {
+      constexpr int M = decltype(mc)::value;
+      tp_pass1_kernel<IO, ST, M, 1>
+          <<<dim3(kL / kColThreads, (unsigned)p->H, (unsigned)npairs), kColThreads, 0, s>>>(
+              (const IO*)dy, (const IO*)u, nullptr, x1dy, x1u, ddpart, p->tw2, (int)B, (int)p->H,
+              (uint32_t)p->N, causal);
+      const size_t sm = pass2_bwd_smem<ST>();
+      auto k2 = tp_pass2_bwd_kernel<ST>;
+      cudaFuncSetAttribute(k2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+      k2<<<(unsigned)(p->H * p->m), kL / 16, sm, s>>>(x1dy, x1u, p->kf, wdk, p->tw_l, (int)npairs,
+                                                       (int)p->H, (int)p->m);
+      tp_pass3_kernel<ST, IO, M, 0>
+          <<<dim3(kL / kColThreads, (unsigned)p->H, (unsigned)npairs), kColThreads, 0, s>>>(
+              x1dy, (const IO*)dy, (IO*)du, p->d, nullptr, p->tw2, (int)B, (int)p->H,
+              (uint32_t)p->N, causal, 1.f);
+      tp_pass3_kernel<float, float, M, 1>
+          <<<dim3(kL / kColThreads, (unsigned)p->H, 1), kColThreads, 0, s>>>(
+              reinterpret_cast<const CxT<float>*>(wdk), nullptr, nullptr, nullptr, dkbar, p->tw2,
+              2, (int)p->H, (uint32_t)p->N, causal, 1.0f / (float)p->n);
+    });
+  });
+  tp_dd_reduce_kernel<<<(unsigned)p->H, 32, 0, s>>>(ddpart, dD,
+                                                    (int)(npairs * (kL / kColThreads)));
+  int rc = cuda_status(cudaGetLastError(), "tp_bwd");
+  if (rc) return rc;
+  return regularizer_backward_dev(p, dkbar, dK, s);
+}
+
+}  // namespace fb

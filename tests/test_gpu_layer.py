@@ -161,3 +161,48 @@ def test_dimension_errors():
         fb.LongConvPlan(64, 2).prep(torch.zeros(2, 64, device="cuda"),
                                     torch.zeros(2, device="cuda"),
                                     fb.RegularizationConfig(lambda_=-1.0))
+
+
+# ------------------------------------------------------------ three-pass (K3/K4b)
+@pytest.mark.parametrize("B,H,N,mode", [(2, 2, 8192, 1), (3, 2, 16384, 1), (2, 1, 65536, 1),
+                                        (2, 2, 16384, 0)])
+def test_three_pass_fp32(lc, B, H, N, mode):
+    inp = layer_inputs(lc, B, H, N, torch.float32)
+    cfg = fb.RegularizationConfig(**CFG)
+    plan, got = run_layer(inp, N, H, torch.float32, cfg, mode=mode, engine=2)
+    assert plan.engine == fb.Engine.THREE_PASS and plan.m == (2 * N if mode else N) // 8192
+    assert_parity(got, oracle_layer(lc, inp, cfg, causal=bool(mode)), 1e-5)
+
+
+@pytest.mark.parametrize("dtype", [torch.bfloat16, torch.float16])
+def test_three_pass_16bit(lc, dtype):
+    inp = layer_inputs(lc, 3, 2, 32768, dtype)
+    cfg = fb.RegularizationConfig(**CFG)
+    _, got = run_layer(inp, 32768, 2, dtype, cfg, engine=2)
+    assert_parity(got, oracle_layer(lc, inp, cfg), 2e-2)
+
+
+def test_config3_heads_sample(lc):
+    """BASELINE config 3 shape (B=16 H=128 N=65536 bf16, three-pass) on the
+    GPU; a sample of heads (all batches, so dK is complete) vs the oracle."""
+    B, H, N = 16, 128, 65536
+    dtype = torch.bfloat16
+    g = torch.Generator(device="cuda").manual_seed(5)
+    u = torch.randn(B, H, N, device="cuda", generator=g).to(dtype)
+    dy = torch.randn(B, H, N, device="cuda", generator=g).to(dtype)
+    K, D = lc.init_kernels(1, H, N, 3)
+    tK = torch.tensor(K, dtype=torch.float32, device="cuda")
+    tD = torch.tensor(D, dtype=torch.float32, device="cuda")
+    cfg = fb.RegularizationConfig(**CFG)
+    plan = fb.LongConvPlan(N, H, fb.ConvMode.CAUSAL, dtype, fb.Engine.AUTO)
+    assert plan.engine == fb.Engine.THREE_PASS and plan.m == 16
+    plan.prep(tK, tD, cfg)
+    y = plan.forward(u)
+    du, dK, dD = plan.backward(dy, u)
+    torch.cuda.synchronize()
+    heads = [0, 77]
+    sub = dict(u=to_np(u[:, heads]), dy=to_np(dy[:, heads]), K=to_np(tK[heads]), D=to_np(tD[heads]))
+    want = oracle_layer(lc, sub, cfg)
+    got = dict(y=to_np(y[:, heads]), du=to_np(du[:, heads]), dK=to_np(dK[heads]),
+               dD=to_np(dD[heads]))
+    assert_parity(got, want, 2e-2, keys=("y", "du", "dK", "dD"))
