@@ -17,9 +17,10 @@ from .longconv import (  # noqa: F401
     regularized_long_conv_backward,
 )
 from ._lib import DimensionError, FBError, PlanError  # noqa: F401
+from .learned import LearnedButterflyPlan, learned_butterfly  # noqa: F401
 
 __all__ = [
     "ConvMode", "Engine", "LongConvPlan", "RegularizationConfig", "SmoothDomain", "long_conv",
     "regularized_long_conv", "regularized_long_conv_backward", "DimensionError", "FBError",
-    "PlanError",
+    "PlanError", "LearnedButterflyPlan", "learned_butterfly",
 ]

@@ -264,6 +264,40 @@ __device__ __forceinline__ void apply_tw(float2 (&v)[R], const float2* tab, uint
   }
 }
 
+// Same as apply_tw, from a full global table tw[t] = w^t (t < n): four
+// L1/L2-resident lookups per column instead of a per-CTA smem table.
+template <int SIGN, int R>
+__device__ __forceinline__ void apply_tw_g(float2 (&v)[R], const float2* __restrict__ tw,
+                                           uint32_t base) {
+  const float2 w1 = tw_lookup<SIGN>(tw, base);
+  v[1] = cmul(v[1], w1);
+  if constexpr (R >= 4) {
+    const float2 w2 = tw_lookup<SIGN>(tw, 2 * base);
+    const float2 w3 = cmul(w1, w2);
+    v[2] = cmul(v[2], w2);
+    v[3] = cmul(v[3], w3);
+    if constexpr (R >= 8) {
+      const float2 w4 = tw_lookup<SIGN>(tw, 4 * base);
+      v[4] = cmul(v[4], w4);
+      v[5] = cmul(v[5], cmul(w1, w4));
+      v[6] = cmul(v[6], cmul(w2, w4));
+      const float2 w7 = cmul(w3, w4);
+      v[7] = cmul(v[7], w7);
+      if constexpr (R >= 16) {
+        const float2 w8 = tw_lookup<SIGN>(tw, 8 * base);
+        v[8] = cmul(v[8], w8);
+        v[9] = cmul(v[9], cmul(w1, w8));
+        v[10] = cmul(v[10], cmul(w2, w8));
+        v[11] = cmul(v[11], cmul(w3, w8));
+        v[12] = cmul(v[12], cmul(w4, w8));
+        v[13] = cmul(v[13], cmul(cmul(w1, w4), w8));
+        v[14] = cmul(v[14], cmul(cmul(w2, w4), w8));
+        v[15] = cmul(v[15], cmul(w7, w8));
+      }
+    }
+  }
+}
+
 // Load + twiddle + DFT of one radix-R butterfly j of the pass at Ns = NS.
 template <int SIGN, int R, uint32_t NS, int LOG2N>
 __device__ __forceinline__ void bfly_load(const float2* s, const float2* tab, float2 (&v)[R],

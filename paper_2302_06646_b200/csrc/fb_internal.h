@@ -34,6 +34,7 @@ struct fb_learned_plan {
   int nstages = 0;
   int64_t factors[32] = {0};
   int64_t param_count = 0;
+  void* ext = nullptr;  // device tables (fb_learned.cu)
 };
 
 namespace fb {

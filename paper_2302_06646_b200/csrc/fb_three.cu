@@ -47,10 +47,7 @@ __global__ void __launch_bounds__(kColThreads)
                     const float* __restrict__ kbar, CxT<ST>* __restrict__ out_a,
                     CxT<ST>* __restrict__ out_b, float* __restrict__ ddpart,
                     const float2* __restrict__ tab_g, int B, int H, uint32_t N, int causal) {
-  __shared__ float2 tab[64 + (kL * M) / 64];
   __shared__ float red[kColThreads / 32];
-  for (uint32_t i = threadIdx.x; i < 64 + (kL * M) / 64; i += blockDim.x) tab[i] = __ldg(tab_g + i);
-  __syncthreads();
   const uint32_t tau = blockIdx.x * kColThreads + threadIdx.x;
   const int h = blockIdx.y, pr = blockIdx.z;
   const int b0 = 2 * pr, b1 = b0 + 1;
@@ -86,13 +83,13 @@ __global__ void __launch_bounds__(kColThreads)
 #pragma unroll
     for (int c = 0; c < M; ++c) dd = fmaf(v[c].x, w[c].x, fmaf(v[c].y, w[c].y, dd));
     dft_reg<-1, M>(w);
-    apply_tw<-1, M>(w, tab, tau);
+    apply_tw_g<-1, M>(w, tab_g, tau);
     CxT<ST>* ob = out_b + ((size_t)pr * H + h) * (size_t)M * kL;
 #pragma unroll
     for (int a = 0; a < M; ++a) stc<ST>(&ob[a * kL + tau].x, w[a]);
   }
   dft_reg<-1, M>(v);
-  apply_tw<-1, M>(v, tab, tau);
+  apply_tw_g<-1, M>(v, tab_g, tau);
   CxT<ST>* oa = out_a + ((size_t)pr * H + h) * (size_t)M * kL;
 #pragma unroll
   for (int a = 0; a < M; ++a) stc<ST>(&oa[a * kL + tau].x, v[a]);
@@ -297,16 +294,13 @@ __global__ void __launch_bounds__(kColThreads)
                     IO* __restrict__ out, const float* __restrict__ D, float* __restrict__ dkbar,
                     const float2* __restrict__ tab_g, int B, int H, uint32_t N, int causal,
                     float scale) {
-  __shared__ float2 tab[64 + (kL * M) / 64];
-  for (uint32_t i = threadIdx.x; i < 64 + (kL * M) / 64; i += blockDim.x) tab[i] = __ldg(tab_g + i);
-  __syncthreads();
   const uint32_t tau = blockIdx.x * kColThreads + threadIdx.x;
   const int h = blockIdx.y, pr = blockIdx.z;
   float2 v[M];
   const CxT<ST>* src = w_in + ((size_t)pr * H + h) * (size_t)M * kL;
 #pragma unroll
   for (int a = 0; a < M; ++a) v[a] = cx_load(src + a * kL + tau);
-  apply_tw<+1, M>(v, tab, tau);
+  apply_tw_g<+1, M>(v, tab_g, tau);
   dft_reg<+1, M>(v);
   const int cmax = causal ? M / 2 : M;
   if constexpr (MODE == 0) {
@@ -399,7 +393,7 @@ int tp_prep(fb_plan* p, const float* K, cudaStream_t s) {
   with_m(p->m, [&](auto mc) {
     constexpr int M = decltype(mc)::value;
     tp_pass1_kernel<float, float, M, 2><<<dim3(kL / kColThreads, (unsigned)p->H, 1), kColThreads, 0, s>>>(
-        nullptr, nullptr, p->kbar, x1k, nullptr, nullptr, p->tw2, 2, (int)p->H, (uint32_t)p->N,
+        nullptr, nullptr, p->kbar, x1k, nullptr, nullptr, p->tw_n, 2, (int)p->H, (uint32_t)p->N,
         causal);
   });
   const size_t sm = pass2_smem<float>();
@@ -437,7 +431,7 @@ int tp_fwd(fb_plan* p, const void* u, void* y, int64_t B, void* ws, cudaStream_t
       constexpr int M = decltype(mc)::value;
       tp_pass1_kernel<IO, ST, M, 0>
           <<<dim3(kL / kColThreads, (unsigned)p->H, (unsigned)npairs), kColThreads, 0, s>>>(
-              (const IO*)u, nullptr, nullptr, x1, nullptr, nullptr, p->tw2, (int)B, (int)p->H,
+              (const IO*)u, nullptr, nullptr, x1, nullptr, nullptr, p->tw_n, (int)B, (int)p->H,
               (uint32_t)p->N, causal);
       const size_t sm = pass2_smem<ST>();
       auto k2 = tp_pass2_kernel<ST, 0>;
@@ -448,7 +442,7 @@ int tp_fwd(fb_plan* p, const void* u, void* y, int64_t B, void* ws, cudaStream_t
           x1, p->kf, nullptr, p->tw_l, (int)npairs, (int)p->H, (int)p->m, ppc, 0.f);
       tp_pass3_kernel<ST, IO, M, 0>
           <<<dim3(kL / kColThreads, (unsigned)p->H, (unsigned)npairs), kColThreads, 0, s>>>(
-              x1, (const IO*)u, (IO*)y, p->d, nullptr, p->tw2, (int)B, (int)p->H, (uint32_t)p->N,
+              x1, (const IO*)u, (IO*)y, p->d, nullptr, p->tw_n, (int)B, (int)p->H, (uint32_t)p->N,
               causal, 1.f);
     });
   });
@@ -482,7 +476,7 @@ int tp_bwd(fb_plan* p, const void* dy, const void* u, void* du, float* dK, float
       constexpr int M = decltype(mc)::value;
       tp_pass1_kernel<IO, ST, M, 1>
           <<<dim3(kL / kColThreads, (unsigned)p->H, (unsigned)npairs), kColThreads, 0, s>>>(
-              (const IO*)dy, (const IO*)u, nullptr, x1dy, x1u, ddpart, p->tw2, (int)B, (int)p->H,
+              (const IO*)dy, (const IO*)u, nullptr, x1dy, x1u, ddpart, p->tw_n, (int)B, (int)p->H,
               (uint32_t)p->N, causal);
       const size_t sm = pass2_bwd_smem<ST>();
       auto k2 = tp_pass2_bwd_kernel<ST>;
@@ -491,11 +485,11 @@ int tp_bwd(fb_plan* p, const void* dy, const void* u, void* du, float* dK, float
                                                        (int)p->H, (int)p->m);
       tp_pass3_kernel<ST, IO, M, 0>
           <<<dim3(kL / kColThreads, (unsigned)p->H, (unsigned)npairs), kColThreads, 0, s>>>(
-              x1dy, (const IO*)dy, (IO*)du, p->d, nullptr, p->tw2, (int)B, (int)p->H,
+              x1dy, (const IO*)dy, (IO*)du, p->d, nullptr, p->tw_n, (int)B, (int)p->H,
               (uint32_t)p->N, causal, 1.f);
       tp_pass3_kernel<float, float, M, 1>
           <<<dim3(kL / kColThreads, (unsigned)p->H, 1), kColThreads, 0, s>>>(
-              reinterpret_cast<const CxT<float>*>(wdk), nullptr, nullptr, nullptr, dkbar, p->tw2,
+              reinterpret_cast<const CxT<float>*>(wdk), nullptr, nullptr, nullptr, dkbar, p->tw_n,
               2, (int)p->H, (uint32_t)p->N, causal, 1.0f / (float)p->n);
     });
   });
