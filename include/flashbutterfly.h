@@ -46,8 +46,16 @@ enum fb_status {
 enum fb_mode { FB_MODE_CIRCULAR = 0, FB_MODE_CAUSAL = 1 };
 
 /* Engine (regularize.hpp:17) minus kNaive (the O(N^2) oracle stays in
- * oracle/): AUTO picks single-pass when the transform fits in shared memory. */
-enum fb_engine { FB_ENGINE_AUTO = 0, FB_ENGINE_SINGLE = 1, FB_ENGINE_THREE = 2 };
+ * oracle/): AUTO picks single-pass when the transform fits in shared memory.
+ * SINGLE uses the tcgen05 tensor-core kernels when the shape/dtype allow
+ * (16-bit I/O, causal, N = 4096); SINGLE_SIMT forces the fp32 CUDA-core
+ * single-pass kernels. */
+enum fb_engine {
+  FB_ENGINE_AUTO = 0,
+  FB_ENGINE_SINGLE = 1,
+  FB_ENGINE_THREE = 2,
+  FB_ENGINE_SINGLE_SIMT = 3
+};
 
 /* I/O element type of u, y, dy, du. K, D, dK, dD are always f32. */
 enum fb_dtype { FB_F32 = 0, FB_BF16 = 1, FB_F16 = 2 };
@@ -72,6 +80,7 @@ typedef struct fb_plan_info {
   int64_t l, m;    /* three-pass split n = l*m (l = n, m = 1 single)    */
   int engine;      /* resolved fb_engine                                */
   int dtype, mode;
+  int tensor_cores; /* 1 when the tcgen05 kernels run this plan         */
 } fb_plan_info;
 
 /* Plan for a bank of H kernels of length N.  Replaces the per-call

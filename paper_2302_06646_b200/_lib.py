@@ -12,7 +12,7 @@ LIB_PATH = Path(__file__).resolve().parent / "libflashbutterfly.so"
 
 FB_OK, FB_ERR_DIM, FB_ERR_PLAN, FB_ERR_CUDA, FB_ERR_NCCL, FB_ERR_ARG, FB_ERR_UNSUPPORTED = range(7)
 FB_MODE_CIRCULAR, FB_MODE_CAUSAL = 0, 1
-FB_ENGINE_AUTO, FB_ENGINE_SINGLE, FB_ENGINE_THREE = 0, 1, 2
+FB_ENGINE_AUTO, FB_ENGINE_SINGLE, FB_ENGINE_THREE, FB_ENGINE_SINGLE_SIMT = 0, 1, 2, 3
 FB_F32, FB_BF16, FB_F16 = 0, 1, 2
 FB_SMOOTH_TIME, FB_SMOOTH_FREQUENCY = 0, 1
 
@@ -46,7 +46,8 @@ class RegConfig(C.Structure):
 
 class PlanInfo(C.Structure):
     _fields_ = [("N", C.c_int64), ("H", C.c_int64), ("n", C.c_int64), ("l", C.c_int64),
-                ("m", C.c_int64), ("engine", C.c_int), ("dtype", C.c_int), ("mode", C.c_int)]
+                ("m", C.c_int64), ("engine", C.c_int), ("dtype", C.c_int), ("mode", C.c_int),
+                ("tensor_cores", C.c_int)]
 
 
 _lib = None

@@ -84,7 +84,7 @@ int fb_plan_create(fb_plan** out, int64_t N, int64_t H, int mode, int dtype, int
   if (mode != FB_MODE_CAUSAL && mode != FB_MODE_CIRCULAR)
     return fail(FB_ERR_ARG, "fb_plan_create: bad mode");
   if (dtype < FB_F32 || dtype > FB_F16) return fail(FB_ERR_ARG, "fb_plan_create: bad dtype");
-  if (engine < FB_ENGINE_AUTO || engine > FB_ENGINE_THREE)
+  if (engine < FB_ENGINE_AUTO || engine > FB_ENGINE_SINGLE_SIMT)
     return fail(FB_ERR_ARG, "fb_plan_create: bad engine");
   if (mode == FB_MODE_CIRCULAR && !is_pow2(N))
     return fail(FB_ERR_PLAN, "fb_plan_create: circular mode needs a power-of-two N "
@@ -101,6 +101,8 @@ int fb_plan_create(fb_plan** out, int64_t N, int64_t H, int mode, int dtype, int
   if (n < kMinTransform) n = kMinTransform;
   p->n = n;
   p->periodic = (mode == FB_MODE_CIRCULAR) && n > N;
+  const bool simt = engine == FB_ENGINE_SINGLE_SIMT;
+  if (simt) engine = FB_ENGINE_SINGLE;
   if (engine == FB_ENGINE_AUTO) engine = n <= kSinglePassMax ? FB_ENGINE_SINGLE : FB_ENGINE_THREE;
   if (engine == FB_ENGINE_SINGLE && n > kSinglePassMax) {
     delete p;
@@ -123,12 +125,14 @@ int fb_plan_create(fb_plan** out, int64_t N, int64_t H, int mode, int dtype, int
     p->m = 1;
   }
   cudaDeviceGetAttribute(&p->num_sms, cudaDevAttrMultiProcessorCount, device);
+  p->use_tc = engine == FB_ENGINE_SINGLE && !simt && tc_eligible(p);
   rc = upload_twiddles(&p->tw_n, n);
   if (!rc) rc = upload_twiddles2(&p->tw2, n);
   if (!rc && engine == FB_ENGINE_THREE) rc = upload_twiddles2(&p->tw_l, p->l);
   if (!rc) rc = cuda_status(cudaMalloc(&p->kf, sizeof(float2) * H * n), "cudaMalloc(kf)");
   if (!rc) rc = cuda_status(cudaMalloc(&p->kbar, sizeof(float) * H * N), "cudaMalloc(kbar)");
   if (!rc) rc = cuda_status(cudaMalloc(&p->d, sizeof(float) * H), "cudaMalloc(D)");
+  if (!rc && p->use_tc) rc = tc_init(p);
   if (rc) {
     fb_plan_destroy(p);
     return rc;
@@ -146,6 +150,8 @@ int fb_plan_destroy(fb_plan* p) {
   cudaFree(p->kbar);
   cudaFree(p->keep);
   cudaFree(p->d);
+  cudaFree(p->tc_mats);
+  cudaFree(p->kf_tc);
   delete p;
   return FB_OK;
 }
@@ -160,6 +166,7 @@ int fb_plan_get_info(const fb_plan* p, fb_plan_info* info) {
   info->engine = p->engine;
   info->dtype = p->dtype;
   info->mode = p->mode;
+  info->tensor_cores = p->use_tc ? 1 : 0;
   return FB_OK;
 }
 

@@ -20,6 +20,9 @@ struct fb_plan {
   float* kbar = nullptr;   // [H][N] regularized kernels
   uint8_t* keep = nullptr; // [H][N] dropout keep flags (training only)
   float* d = nullptr;      // [H] skip gains
+  bool use_tc = false;       // tcgen05 single-pass path (fb_single_tc.cu)
+  void* tc_mats = nullptr;   // DFT blocks in UMMA smem images
+  float2* kf_tc = nullptr;   // k_f permuted to the tensor-core frequency layout
   bool prepared = false;
   bool use_keep = false;
   double lambda = 0.0, keep_scale = 1.0;
@@ -46,6 +49,15 @@ int sp_prep(fb_plan* p, const float* K, cudaStream_t s);
 int sp_fwd(fb_plan* p, const void* u, void* y, int64_t B, cudaStream_t s);
 size_t sp_workspace(const fb_plan* p, int64_t B);
 int sp_bwd(fb_plan* p, const void* dy, const void* u, void* du, float* dK, float* dKbar, float* dD,
+           int64_t B, void* ws, cudaStream_t s);
+
+// tcgen05 single-pass (fb_single_tc.cu)
+bool tc_eligible(const fb_plan* p);
+int tc_init(fb_plan* p);
+int tc_prep_permute(fb_plan* p, cudaStream_t s);
+int tc_fwd(fb_plan* p, const void* u, void* y, int64_t B, cudaStream_t s);
+size_t tc_workspace(const fb_plan* p, int64_t B);
+int tc_bwd(fb_plan* p, const void* dy, const void* u, void* du, float* dK, float* dKbar, float* dD,
            int64_t B, void* ws, cudaStream_t s);
 
 // three-pass (fb_three.cu)

@@ -474,10 +474,19 @@ int sp_prep(fb_plan* p, const float* K, cudaStream_t s) {
   int rc = regularize_bank_dev(p, K, s);
   if (rc) return rc;
   with_log2n(p->n, [&](auto ks) { ks.spectrum(s, p); });
-  return cuda_status(cudaGetLastError(), "sp_prep");
+  rc = cuda_status(cudaGetLastError(), "sp_prep");
+  if (!rc && p->use_tc) rc = tc_prep_permute(p, s);
+  return rc;
+}
+
+int sp_finalize(fb_plan* p, const float2* spart, const float* ddpart, int chunks, float* dkbar,
+                float* dD, cudaStream_t s) {
+  with_log2n(p->n, [&](auto ks) { ks.finalize(s, p, spart, ddpart, chunks, dkbar, dD); });
+  return cuda_status(cudaGetLastError(), "sp_finalize");
 }
 
 int sp_fwd(fb_plan* p, const void* u, void* y, int64_t B, cudaStream_t s) {
+  if (p->use_tc) return tc_fwd(p, u, y, B, s);
   const int chunks = chunks_for(p, B);
   const int64_t npairs = (B + 1) / 2;
   const int ppc = (int)((npairs + chunks - 1) / chunks);
@@ -492,6 +501,7 @@ int sp_fwd(fb_plan* p, const void* u, void* y, int64_t B, cudaStream_t s) {
 }
 
 size_t sp_workspace(const fb_plan* p, int64_t B) {
+  if (p->use_tc) return tc_workspace(p, B);
   const int c = chunks_for(p, B);
   size_t bytes = (size_t)p->H * c * p->n * sizeof(float2);  // spectral partials
   bytes += (size_t)p->H * c * sizeof(float);                 // dD partials
@@ -502,6 +512,7 @@ size_t sp_workspace(const fb_plan* p, int64_t B) {
 
 int sp_bwd(fb_plan* p, const void* dy, const void* u, void* du, float* dK, float* dKbar, float* dD,
            int64_t B, void* ws, cudaStream_t s) {
+  if (p->use_tc) return tc_bwd(p, dy, u, du, dK, dKbar, dD, B, ws, s);
   const int chunks = chunks_for(p, B);
   const int64_t npairs = (B + 1) / 2;
   const int ppc = (int)((npairs + chunks - 1) / chunks);

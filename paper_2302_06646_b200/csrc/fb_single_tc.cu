@@ -1,0 +1,831 @@
+// FlashButterfly-B200 single-pass engine on the 5th-gen tensor cores
+// (tcgen05 + TMEM + TMA) for the 16-bit I/O modes at n = 8192 (N = 4096,
+// causal) — BASELINE config 2.
+//
+// The reference's butterfly (apply_stages, proj/src/butterfly.cpp:124-163)
+// computes F_n x as dense DFT blocks joined by twiddles.  Here F_8192 is
+// the three-factor Monarch product  n = 16 (t1) x 16 (t2) x 32 (t3),
+// t = 512 t1 + 32 t2 + t3,  f = f1 + 16 f2 + 256 f3:
+//   A: DFT16 over t1       rows m_A = 32 t2 + t3     (512)   K 16  N 32
+//      twiddle  w_8192^(f1 m_A)
+//   B: DFT16 over t2       rows m_B = 32 f1 + t3     (512)   K 32  N 32
+//      twiddle  w_512^(f2 t3)
+//   C: DFT32 over t3       rows m_C = 16 f1 + f2     (256)   K 64  N 64
+// and the inverse C' -> B' -> A' runs the conjugate blocks back.  Every
+// dense block is one tcgen05.mma (bf16/fp16 operands, complex split into
+// real-stacked K = [re | im], fp32 accumulate in TMEM).  The causal
+// zero-padding is pruned: stage A reads only t1 < 8 (K = 16 instead of 32)
+// and A' produces only t1 < 8 (N = 16).  Twiddles, the k_f product and the
+// bf16 re-quantisation happen in the TMEM -> register -> smem epilogues;
+// the u pair arrives by one 4-D TMA load per 64-row block, written by the
+// TMA straight into the MN-major 128B-swizzled UMMA operand layout.
+// Two real channels (b, b+1) of one head ride as re/im of one transform.
+#include <cuda.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <type_traits>
+#include <vector>
+
+#include "fb_common.cuh"
+#include "fb_fft.cuh"
+#include "fb_internal.h"
+#include "fb_ptx.cuh"
+#include "fb_tc.cuh"
+
+namespace fb {
+namespace tcfft {
+
+constexpr uint32_t kN = 8192;
+constexpr uint32_t kThreads = 512;
+
+// shared memory map (bytes, 1024-aligned where swizzled operands live)
+constexpr uint32_t SA = 0;                    // [2][16 KB] input pairs (MN-major, [mb][kg][8][64])
+constexpr uint32_t SB = SA + 2 * 16384;       // 32 KB B / B' operand (MN-major [kg 4][mb 8][8][64])
+constexpr uint32_t SC = SB + 32768;           // 32 KB C / C' operand (K-major SW128, 256 x 64)
+constexpr uint32_t SA2 = SC + 32768;          // 32 KB A' operand (MN-major [kg 4][mb 8][8][64])
+constexpr uint32_t SMAT = SA2 + 32768;        // 22 KB DFT blocks
+constexpr uint32_t MAT_FA = 0, MAT_FB = 1024, MAT_FC = 3072, MAT_IC = 11264, MAT_IB = 19456,
+                   MAT_IA = 21504, MAT_BYTES = 22528;
+constexpr uint32_t SKF = SMAT + MAT_BYTES;    // 64 KB k_f, [f3 32][m_C 256] float2
+constexpr uint32_t STAB = SKF + 65536;        // two-level twiddle table (192 float2)
+constexpr uint32_t SMEM_BYTES = STAB + 1536 + 1024;  // + alignment slack
+
+// TMEM column regions (512 allocated)
+constexpr uint32_t R1 = 0, R2 = 128, R3 = 256, R4 = 384;
+
+// element offsets of the MN-major operands
+__device__ __forceinline__ uint32_t sw128(uint32_t lin) { return lin ^ ((lin >> 3) & 0x70u); }
+// input pair layout [m/64][k/8][k%8][m%64] (the TMA box order)
+__device__ __forceinline__ uint32_t off_in(uint32_t m, uint32_t k) {
+  return sw128((m >> 6) * 2048 + (k >> 3) * 1024 + (k & 7) * 128 + (m & 63) * 2);
+}
+// K = 32 operands, layout [k/8][m/64][k%8][m%64]
+__device__ __forceinline__ uint32_t off_mn(uint32_t m, uint32_t k) {
+  return sw128((k >> 3) * 8192 + (m >> 6) * 1024 + (k & 7) * 128 + (m & 63) * 2);
+}
+
+template <typename T>
+struct Fmt;
+template <>
+struct Fmt<__nv_bfloat16> {
+  static constexpr uint32_t ab = 1;  // UMMA a/b format BF16
+  static constexpr CUtensorMapDataType tma = CU_TENSOR_MAP_DATA_TYPE_BFLOAT16;
+};
+template <>
+struct Fmt<__half> {
+  static constexpr uint32_t ab = 0;  // F16
+  static constexpr CUtensorMapDataType tma = CU_TENSOR_MAP_DATA_TYPE_FLOAT16;
+};
+
+template <typename T>
+__host__ __device__ constexpr uint32_t idesc(uint32_t M, uint32_t N, bool a_mn) {
+  return (1u << 4) | (Fmt<T>::ab << 7) | (Fmt<T>::ab << 10) | ((a_mn ? 1u : 0u) << 15) |
+         ((N >> 3) << 17) | ((M >> 4) << 24);
+}
+
+template <typename T>
+__device__ __forceinline__ void st16(unsigned char* base, uint32_t off, float v) {
+  *reinterpret_cast<T*>(base + off) = cvt<T>(v);
+}
+template <typename T>
+__device__ __forceinline__ uint32_t pack2(float a, float b);
+template <>
+__device__ __forceinline__ uint32_t pack2<__nv_bfloat16>(float a, float b) {
+  __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
+  return *reinterpret_cast<uint32_t*>(&h);
+}
+template <>
+__device__ __forceinline__ uint32_t pack2<__half>(float a, float b) {
+  __half2 h = __floats2half2_rn(a, b);
+  return *reinterpret_cast<uint32_t*>(&h);
+}
+// 8 consecutive values -> one 16-byte store
+template <typename T>
+__device__ __forceinline__ void st8(unsigned char* p, const float* v) {
+  uint4 q;
+  q.x = pack2<T>(v[0], v[1]);
+  q.y = pack2<T>(v[2], v[3]);
+  q.z = pack2<T>(v[4], v[5]);
+  q.w = pack2<T>(v[6], v[7]);
+  *reinterpret_cast<uint4*>(p) = q;
+}
+
+__device__ __forceinline__ void ld16(uint32_t taddr, float (&v)[16]) {
+  uint32_t* r = reinterpret_cast<uint32_t*>(v);
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,"
+      "%15}, [%16];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+        "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),
+        "=r"(r[14]), "=r"(r[15])
+      : "r"(taddr));
+}
+__device__ __forceinline__ void st32(uint32_t taddr, const float (&v)[32]) {
+  const uint32_t* r = reinterpret_cast<const uint32_t*>(v);
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,"
+      "%14,%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};" ::"r"(taddr),
+      "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]),
+      "r"(r[8]), "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]),
+      "r"(r[15]), "r"(r[16]), "r"(r[17]), "r"(r[18]), "r"(r[19]), "r"(r[20]), "r"(r[21]),
+      "r"(r[22]), "r"(r[23]), "r"(r[24]), "r"(r[25]), "r"(r[26]), "r"(r[27]), "r"(r[28]),
+      "r"(r[29]), "r"(r[30]), "r"(r[31])
+      : "memory");
+}
+__device__ __forceinline__ void st_wait() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
+
+__device__ __forceinline__ void tma_load_4d(void* dst, const CUtensorMap* map, int c0, int c1, int c2,
+                                            int c3, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, "
+      "%3, %4, %5}], [%6];" ::"r"(ptx::smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(c3),
+      "r"(ptx::smem_u32(bar))
+      : "memory");
+}
+
+// The 8 TMA boxes of one channel pair (b0, b0+1) of head h: box [64 m][8 t1]
+// [1 h][2 b] lands as [kgroup b][8 t1][64 m] = 2 KB per 64-row block.
+__device__ __forceinline__ void load_pair(unsigned char* dst, const CUtensorMap* map, int h, int b0,
+                                          uint64_t* bar) {
+  ptx::mbar_arrive_expect_tx(bar, 8 * 2048);
+  for (int mb = 0; mb < 8; ++mb) tma_load_4d(dst + mb * 2048, map, mb * 64, 0, h, b0, bar);
+}
+
+// --------------------------------------------------------------------------
+// Per-CTA state and the stage sequence shared by the forward and backward
+// kernels.  Thread (warp w, lane): slab s = w & 3 (TMEM lanes 32s..32s+31),
+// group g = w >> 2.
+// --------------------------------------------------------------------------
+struct Ctx {
+  unsigned char* sm;
+  uint32_t smb;    // shared address of sm
+  uint32_t tmem;   // TMEM base
+  uint64_t* mma_bar;
+  uint32_t mma_phase;
+  const float2* tab;
+  uint32_t g, s, lane;
+};
+
+__device__ __forceinline__ void mma_wait(Ctx& c) {
+  ptx::mbar_wait(c.mma_bar, c.mma_phase);
+  c.mma_phase ^= 1;
+  tc::fence_after();
+}
+
+// all threads: make generic smem writes + TMEM reads visible, then one
+// thread issues the stage's MMAs and commits them to the barrier.
+__device__ __forceinline__ void publish(const Ctx& c) {
+  ptx::fence_proxy_async_smem();
+  tc::fence_before();
+  __syncthreads();
+  tc::fence_after();
+}
+
+template <typename T>
+__device__ __forceinline__ void mma_A(const Ctx& c, uint32_t sa_off) {
+  // 4 M-tiles x (N 32, K 16): A = input pair (MN-major, LBO 2048, SBO 1024)
+  const uint32_t id = idesc<T>(128, 32, true);
+  const uint64_t bd = tc::smem_desc(c.smb + SMAT + MAT_FA, 256, tc::kSw32);
+  for (uint32_t t = 0; t < 4; ++t) {
+    const uint64_t ad = tc::smem_desc(c.smb + sa_off + t * 4096, 1024, tc::kSw128, 2048);
+    tc::mma_bf16(c.tmem + R1 + 32 * t, ad, bd, id, 0);
+  }
+}
+// K = 32, MN-major operand at `op` ([kg][mb][8][64]: LBO 1024, SBO 8192)
+template <typename T>
+__device__ __forceinline__ void mma_mn32(const Ctx& c, uint32_t op, uint32_t mat, uint32_t N,
+                                         uint32_t dcol, uint32_t mat_sbo, int mat_swz) {
+  const uint32_t id = idesc<T>(128, N, true);
+  for (uint32_t t = 0; t < 4; ++t)
+    for (uint32_t ks = 0; ks < 2; ++ks) {
+      const uint64_t ad = tc::smem_desc(c.smb + op + t * 2048 + ks * 2 * 8192, 8192, tc::kSw128, 1024);
+      const uint64_t bd = tc::smem_desc(c.smb + SMAT + mat + ks * 32, mat_sbo, mat_swz);
+      tc::mma_bf16(c.tmem + dcol + N * t, ad, bd, id, ks);
+    }
+}
+// stage C / C': 2 M-tiles x (N 64, K 64), A K-major SW128 (256 x 128 B)
+template <typename T>
+__device__ __forceinline__ void mma_C(const Ctx& c, uint32_t mat, uint32_t dcol) {
+  const uint32_t id = idesc<T>(128, 64, false);
+  for (uint32_t t = 0; t < 2; ++t)
+    for (uint32_t ks = 0; ks < 4; ++ks) {
+      const uint64_t ad = tc::smem_desc(c.smb + SC + t * 16384 + ks * 32, 1024, tc::kSw128);
+      const uint64_t bd = tc::smem_desc(c.smb + SMAT + mat + ks * 32, 1024, tc::kSw128);
+      tc::mma_bf16(c.tmem + dcol + 64 * t, ad, bd, id, ks);
+    }
+}
+
+__device__ __forceinline__ uint32_t lane_addr(const Ctx& c, uint32_t col) {
+  return c.tmem + ((32u * c.s) << 16) + col;
+}
+
+// Forward transform of the pair staged at sa_off: leaves X[f] in TMEM R3
+// (D_C: rows m_C, cols [re f3 0..15 | im 0..15 | re 16..31 | im 16..31]).
+template <typename T>
+__device__ __forceinline__ void forward_fft(Ctx& c, uint32_t sa_off, uint64_t* in_bar,
+                                            uint32_t in_phase, bool* in_free_hook) {
+  // ---- stage A
+  ptx::mbar_wait(in_bar, in_phase);
+  tc::fence_after();
+  if (threadIdx.x == 0) {
+    mma_A<T>(c, sa_off);
+    tc::commit(c.mma_bar);
+  }
+  mma_wait(c);
+  if (in_free_hook) *in_free_hook = true;
+  // ---- A -> B: twiddle w^(f1 m_A)
+  {
+    const uint32_t m = 128 * c.g + 32 * c.s + c.lane;  // = 32 t2 + t3
+    const uint32_t t2 = m >> 5, t3 = c.lane;
+    float v[32];
+    tc::ld32(lane_addr(c, R1 + 32 * c.g), v);
+    tc::ld_wait();
+    float2 X[16];
+#pragma unroll
+    for (int f = 0; f < 16; ++f) X[f] = make_float2(v[f], v[16 + f]);
+    apply_tw<-1, 16>(X, c.tab, m);
+    unsigned char* sb = c.sm + SB;
+#pragma unroll
+    for (int f1 = 0; f1 < 16; ++f1) {
+      const uint32_t mb = 32 * f1 + t3;
+      st16<T>(sb, off_mn(mb, t2), X[f1].x);
+      st16<T>(sb, off_mn(mb, 16 + t2), X[f1].y);
+    }
+  }
+  publish(c);
+  if (threadIdx.x == 0) {
+    mma_mn32<T>(c, SB, MAT_FB, 32, R2, 512, tc::kSw64);
+    tc::commit(c.mma_bar);
+  }
+  mma_wait(c);
+  // ---- B -> C: twiddle w_512^(f2 t3)
+  {
+    const uint32_t mB = 128 * c.g + 32 * c.s + c.lane;  // = 32 f1 + t3
+    const uint32_t f1 = mB >> 5, t3 = c.lane;
+    float v[32];
+    tc::ld32(lane_addr(c, R2 + 32 * c.g), v);
+    tc::ld_wait();
+    float2 Y[16];
+#pragma unroll
+    for (int f = 0; f < 16; ++f) Y[f] = make_float2(v[f], v[16 + f]);
+    apply_tw<-1, 16>(Y, c.tab, 16 * t3);
+    unsigned char* sc = c.sm + SC;
+#pragma unroll
+    for (int f2 = 0; f2 < 16; ++f2) {
+      const uint32_t mC = 16 * f1 + f2;
+      st16<T>(sc, tc::kmajor_off<tc::kSw128>(mC, t3), Y[f2].x);
+      st16<T>(sc, tc::kmajor_off<tc::kSw128>(mC, 32 + t3), Y[f2].y);
+    }
+  }
+  publish(c);
+  if (threadIdx.x == 0) {
+    mma_C<T>(c, MAT_FC, R3);
+    tc::commit(c.mma_bar);
+  }
+  mma_wait(c);
+}
+
+// Spectrum row owned by this thread at the C exit: m_C and half h.
+__device__ __forceinline__ void c_row(const Ctx& c, uint32_t& mC, uint32_t& h) {
+  mC = 128 * (c.g & 1) + 32 * c.s + c.lane;
+  h = c.g >> 1;
+}
+
+// Write Z[j] (f3 = 16h + j) as the C' operand row (K-major SW128).
+template <typename T>
+__device__ __forceinline__ void write_cprime(const Ctx& c, uint32_t mC, uint32_t h, const float2 (&Z)[16]) {
+  unsigned char* sc = c.sm + SC;
+  float re[16], im[16];
+#pragma unroll
+  for (int j = 0; j < 16; ++j) {
+    re[j] = Z[j].x;
+    im[j] = Z[j].y;
+  }
+  st8<T>(sc + tc::kmajor_off<tc::kSw128>(mC, 16 * h), re);
+  st8<T>(sc + tc::kmajor_off<tc::kSw128>(mC, 16 * h + 8), re + 8);
+  st8<T>(sc + tc::kmajor_off<tc::kSw128>(mC, 32 + 16 * h), im);
+  st8<T>(sc + tc::kmajor_off<tc::kSw128>(mC, 32 + 16 * h + 8), im + 8);
+}
+
+// Inverse transform from the C' operand in SC; leaves z[t] (t1 < 8) in
+// TMEM R2 cols 16 T + [re t1 0..7 | im t1 0..7] of tile T = row block.
+template <typename T>
+__device__ __forceinline__ void inverse_fft(Ctx& c) {
+  publish(c);
+  if (threadIdx.x == 0) {
+    mma_C<T>(c, MAT_IC, R3);
+    tc::commit(c.mma_bar);
+  }
+  mma_wait(c);
+  // ---- C' -> B': twiddle w_512^(-f2 t3)
+  {
+    uint32_t mC, h;
+    c_row(c, mC, h);
+    const uint32_t f1 = mC >> 4, f2 = mC & 15;
+    float v[32];
+    tc::ld32(lane_addr(c, R3 + 64 * (c.g & 1) + 32 * h), v);
+    tc::ld_wait();
+    float2 W[16];
+#pragma unroll
+    for (int j = 0; j < 16; ++j) W[j] = make_float2(v[j], v[16 + j]);
+    apply_tw<+1, 16>(W, c.tab, 16 * f2);
+    if (h) {
+      const float2 w = tw2<+1>(c.tab, 256 * f2);
+#pragma unroll
+      for (int j = 0; j < 16; ++j) W[j] = cmul(W[j], w);
+    }
+    // B' operand: rows m_B = 32 f1 + 16 h + j, k = f2 (re) / 16 + f2 (im)
+    unsigned char* sb = c.sm + SB;
+    float re[16], im[16];
+#pragma unroll
+    for (int j = 0; j < 16; ++j) {
+      re[j] = W[j].x;
+      im[j] = W[j].y;
+    }
+    const uint32_t m0 = 32 * f1 + 16 * h;
+    st8<T>(sb + off_mn(m0, f2), re);
+    st8<T>(sb + off_mn(m0 + 8, f2), re + 8);
+    st8<T>(sb + off_mn(m0, 16 + f2), im);
+    st8<T>(sb + off_mn(m0 + 8, 16 + f2), im + 8);
+  }
+  publish(c);
+  if (threadIdx.x == 0) {
+    mma_mn32<T>(c, SB, MAT_IB, 32, R1, 512, tc::kSw64);
+    tc::commit(c.mma_bar);
+  }
+  mma_wait(c);
+  // ---- B' -> A': twiddle w^(-f1 (32 t2 + t3))
+  {
+    const uint32_t mB = 128 * c.g + 32 * c.s + c.lane;  // = 32 f1 + t3
+    const uint32_t f1 = mB >> 5, t3 = c.lane;
+    float v[32];
+    tc::ld32(lane_addr(c, R1 + 32 * c.g), v);
+    tc::ld_wait();
+    float2 V[16];
+#pragma unroll
+    for (int t = 0; t < 16; ++t) V[t] = make_float2(v[t], v[16 + t]);
+    apply_tw<+1, 16>(V, c.tab, 32 * f1);
+    const float2 w = tw2<+1>(c.tab, f1 * t3);
+    unsigned char* sa2 = c.sm + SA2;
+#pragma unroll
+    for (int t2 = 0; t2 < 16; ++t2) {
+      const float2 z = cmul(V[t2], w);
+      const uint32_t mA = 32 * t2 + t3;
+      st16<T>(sa2, off_mn(mA, f1), z.x);
+      st16<T>(sa2, off_mn(mA, 16 + f1), z.y);
+    }
+  }
+  publish(c);
+  if (threadIdx.x == 0) {
+    mma_mn32<T>(c, SA2, MAT_IA, 16, R2, 512, tc::kSw64);
+    tc::commit(c.mma_bar);
+  }
+  mma_wait(c);
+}
+
+__device__ __forceinline__ void setup(Ctx& c, unsigned char* sm, uint32_t* tmem_slot, uint64_t* bars,
+                                      const uint4* __restrict__ mats, const float2* __restrict__ kf_h,
+                                      const float2* __restrict__ tab_g, bool load_kf) {
+  c.sm = sm;
+  c.smb = ptx::smem_u32(sm);
+  c.lane = threadIdx.x & 31;
+  c.s = (threadIdx.x >> 5) & 3;
+  c.g = threadIdx.x >> 7;
+  c.mma_bar = &bars[0];
+  c.mma_phase = 0;
+  c.tab = reinterpret_cast<const float2*>(sm + STAB);
+  if (threadIdx.x < 32) tc::alloc<512>(tmem_slot);
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < 4; ++i) ptx::mbar_init(&bars[i], 1);
+    ptx::fence_barrier_init();
+  }
+  uint4* dm = reinterpret_cast<uint4*>(sm + SMAT);
+  for (uint32_t i = threadIdx.x; i < MAT_BYTES / 16; i += kThreads) dm[i] = __ldg(mats + i);
+  float2* tab = reinterpret_cast<float2*>(sm + STAB);
+  for (uint32_t i = threadIdx.x; i < 192; i += kThreads) tab[i] = __ldg(tab_g + i);
+  if (load_kf) {
+    const float4* src = reinterpret_cast<const float4*>(kf_h);
+    float4* dst = reinterpret_cast<float4*>(sm + SKF);
+    for (uint32_t i = threadIdx.x; i < kN / 2; i += kThreads) dst[i] = __ldg(src + i);
+  }
+  ptx::fence_proxy_async_smem();
+  tc::fence_before();
+  __syncthreads();
+  tc::fence_after();
+  c.tmem = *tmem_slot;
+}
+
+__device__ __forceinline__ void teardown(const Ctx& c) {
+  tc::fence_before();
+  __syncthreads();
+  if (threadIdx.x < 32) tc::dealloc<512>(c.tmem);
+}
+
+// ------------------------------------------------------------------ forward
+template <typename T>
+__global__ void __launch_bounds__(kThreads, 1)
+    tc_fwd_kernel(const __grid_constant__ CUtensorMap umap, const T* __restrict__ u,
+                  T* __restrict__ y, const float2* __restrict__ kfp, const uint4* __restrict__ mats,
+                  const float* __restrict__ D, const float2* __restrict__ tab_g, int B, int H,
+                  int ppc) {
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  __shared__ uint32_t tmem_slot;
+  __shared__ __align__(8) uint64_t bars[4];  // 0: mma, 1: input
+  unsigned char* sm = reinterpret_cast<unsigned char*>(
+      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  const int h = blockIdx.x;
+  const int npairs = (B + 1) / 2;
+  const int p0 = blockIdx.y * ppc, p1 = min(npairs, p0 + ppc);
+  if (p0 >= p1) return;
+  Ctx c;
+  setup(c, sm, &tmem_slot, bars, mats, kfp + (size_t)h * kN, tab_g, true);
+  const float d = __ldg(D + h);
+  const float2* kfs = reinterpret_cast<const float2*>(sm + SKF);
+  if (threadIdx.x == 0) load_pair(sm + SA, &umap, h, 2 * p0, &bars[1]);
+  uint32_t in_phase = 0;
+  for (int pr = p0; pr < p1; ++pr) {
+    const int b0 = 2 * pr, b1 = b0 + 1;
+    const bool has1 = b1 < B;
+    bool in_free = false;
+    forward_fft<T>(c, SA, &bars[1], in_phase, &in_free);
+    in_phase ^= 1;
+    // stage A has consumed the input: prefetch the next pair behind the
+    // remaining five stages
+    if (threadIdx.x == 0 && pr + 1 < p1) load_pair(sm + SA, &umap, h, 2 * (pr + 1), &bars[1]);
+    // ---- C exit: Z = X * k_f  -> C' operand
+    {
+      uint32_t mC, hh;
+      c_row(c, mC, hh);
+      float v[32];
+      tc::ld32(lane_addr(c, R3 + 64 * (c.g & 1) + 32 * hh), v);
+      tc::ld_wait();
+      float2 Z[16];
+#pragma unroll
+      for (int j = 0; j < 16; ++j)
+        Z[j] = cmul(make_float2(v[j], v[16 + j]), kfs[(16 * hh + j) * 256 + mC]);
+      write_cprime<T>(c, mC, hh, Z);
+    }
+    inverse_fft<T>(c);
+    // ---- A' exit: y = z + D u   (t = 512 t1 + m_A, t1 < 8)
+    {
+      const uint32_t mA = 128 * c.g + 32 * c.s + c.lane;
+      float v[16];
+      ld16(lane_addr(c, R2 + 16 * c.g), v);
+      tc::ld_wait();
+      const size_t o0 = ((size_t)b0 * H + h) * 4096, o1 = ((size_t)b1 * H + h) * 4096;
+#pragma unroll
+      for (int t1 = 0; t1 < 8; ++t1) {
+        const uint32_t t = 512 * t1 + mA;
+        st(y + o0 + t, fmaf(d, ld(u + o0 + t), v[t1]));
+        if (has1) st(y + o1 + t, fmaf(d, ld(u + o1 + t), v[8 + t1]));
+      }
+    }
+    tc::fence_before();
+    __syncthreads();
+    tc::fence_after();
+  }
+  teardown(c);
+}
+
+// ------------------------------------------------------------------ backward
+// Per pair: DY = F(dy), U = F(u); S += conj(U) DY (S resident in TMEM R4);
+// du = F^-1(DY conj(k_f)) + D dy; dD partial.  S of the CTA's pairs is
+// written in natural frequency order for the finalize kernel.
+template <typename T>
+__global__ void __launch_bounds__(kThreads, 1)
+    tc_bwd_kernel(const __grid_constant__ CUtensorMap dymap, const __grid_constant__ CUtensorMap umap,
+                  const T* __restrict__ dy, const T* __restrict__ u, T* __restrict__ du,
+                  const float2* __restrict__ kfp, const uint4* __restrict__ mats,
+                  const float* __restrict__ D, const float2* __restrict__ tab_g,
+                  float2* __restrict__ spart, float* __restrict__ ddpart, int B, int H, int ppc) {
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  __shared__ uint32_t tmem_slot;
+  __shared__ __align__(8) uint64_t bars[4];  // 0: mma, 1: dy, 2: u
+  __shared__ float red[kThreads / 32];
+  unsigned char* sm = reinterpret_cast<unsigned char*>(
+      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  const int h = blockIdx.x, chunk = blockIdx.y, chunks = gridDim.y;
+  const int npairs = (B + 1) / 2;
+  const int p0 = chunk * ppc, p1 = min(npairs, p0 + ppc);
+  Ctx c;
+  setup(c, sm, &tmem_slot, bars, mats, kfp + (size_t)h * kN, tab_g, true);
+  const float d = __ldg(D + h);
+  const float2* kfs = reinterpret_cast<const float2*>(sm + SKF);
+  uint32_t mC, hh;
+  c_row(c, mC, hh);
+  // S := 0 in TMEM R4 (this thread's row / half)
+  {
+    float z[32];
+#pragma unroll
+    for (int i = 0; i < 32; ++i) z[i] = 0.f;
+    st32(lane_addr(c, R4 + 64 * (c.g & 1) + 32 * hh), z);
+    st_wait();
+  }
+  float dd = 0.f;
+  if (threadIdx.x == 0 && p0 < p1) {
+    load_pair(sm + SA, &dymap, h, 2 * p0, &bars[1]);
+    load_pair(sm + SA + 16384, &umap, h, 2 * p0, &bars[2]);
+  }
+  uint32_t ph = 0;
+  for (int pr = p0; pr < p1; ++pr) {
+    const int b0 = 2 * pr, b1 = b0 + 1;
+    const bool has1 = b1 < B;
+    const bool more = pr + 1 < p1;
+    // ---- DY = F(dy)
+    forward_fft<T>(c, SA, &bars[1], ph, nullptr);
+    if (threadIdx.x == 0 && more) load_pair(sm + SA, &dymap, h, 2 * (pr + 1), &bars[1]);
+    float2 DY[16];
+    {
+      float v[32];
+      tc::ld32(lane_addr(c, R3 + 64 * (c.g & 1) + 32 * hh), v);
+      tc::ld_wait();
+#pragma unroll
+      for (int j = 0; j < 16; ++j) DY[j] = make_float2(v[j], v[16 + j]);
+    }
+    tc::fence_before();
+    __syncthreads();  // R3 read before F(u) overwrites it
+    tc::fence_after();
+    // ---- U = F(u)
+    forward_fft<T>(c, SA + 16384, &bars[2], ph, nullptr);
+    if (threadIdx.x == 0 && more) load_pair(sm + SA + 16384, &umap, h, 2 * (pr + 1), &bars[2]);
+    ph ^= 1;
+    {
+      float v[32], sacc[32];
+      tc::ld32(lane_addr(c, R3 + 64 * (c.g & 1) + 32 * hh), v);
+      tc::ld32(lane_addr(c, R4 + 64 * (c.g & 1) + 32 * hh), sacc);
+      tc::ld_wait();
+      float2 Z[16];
+#pragma unroll
+      for (int j = 0; j < 16; ++j) {
+        const float2 U = make_float2(v[j], v[16 + j]);
+        const float2 a = cconjmul(U, DY[j]);
+        sacc[j] += a.x;
+        sacc[16 + j] += a.y;
+        Z[j] = cmulc(DY[j], kfs[(16 * hh + j) * 256 + mC]);
+      }
+      st32(lane_addr(c, R4 + 64 * (c.g & 1) + 32 * hh), sacc);
+      st_wait();
+      write_cprime<T>(c, mC, hh, Z);
+    }
+    inverse_fft<T>(c);
+    // ---- A' exit: du = z + D dy; dD partial from dy * u
+    {
+      const uint32_t mA = 128 * c.g + 32 * c.s + c.lane;
+      float v[16];
+      ld16(lane_addr(c, R2 + 16 * c.g), v);
+      tc::ld_wait();
+      const size_t o0 = ((size_t)b0 * H + h) * 4096, o1 = ((size_t)b1 * H + h) * 4096;
+#pragma unroll
+      for (int t1 = 0; t1 < 8; ++t1) {
+        const uint32_t t = 512 * t1 + mA;
+        const float g0 = ld(dy + o0 + t);
+        st(du + o0 + t, fmaf(d, g0, v[t1]));
+        dd = fmaf(g0, ld(u + o0 + t), dd);
+        if (has1) {
+          const float g1 = ld(dy + o1 + t);
+          st(du + o1 + t, fmaf(d, g1, v[8 + t1]));
+          dd = fmaf(g1, ld(u + o1 + t), dd);
+        }
+      }
+    }
+    tc::fence_before();
+    __syncthreads();
+    tc::fence_after();
+  }
+  // ---- S (natural order f = f1 + 16 f2 + 256 f3) and dD partials
+  {
+    float sacc[32];
+    tc::ld32(lane_addr(c, R4 + 64 * (c.g & 1) + 32 * hh), sacc);
+    tc::ld_wait();
+    float2* sp = spart + ((size_t)h * chunks + chunk) * kN;
+    const uint32_t f1 = mC >> 4, f2 = mC & 15;
+#pragma unroll
+    for (int j = 0; j < 16; ++j) sp[f1 + 16 * f2 + 256 * (16 * hh + j)] = make_float2(sacc[j], sacc[16 + j]);
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) dd += __shfl_xor_sync(0xffffffffu, dd, o);
+  if (c.lane == 0) red[threadIdx.x >> 5] = dd;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    float t = 0.f;
+    for (int w = 0; w < (int)(kThreads / 32); ++w) t += red[w];
+    ddpart[(size_t)h * chunks + chunk] = t;
+  }
+  teardown(c);
+}
+
+// k_f (natural order, / n) -> [h][f3][m_C], m_C = 16 f1 + f2, f = f1 + 16 f2 + 256 f3
+__global__ void permute_kf_kernel(const float2* __restrict__ kf, float2* __restrict__ kfp, int H) {
+  const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= (uint32_t)H * kN) return;
+  const uint32_t h = i / kN, r = i % kN, f3 = r / 256, mC = r % 256;
+  const uint32_t f = (mC >> 4) + 16 * (mC & 15) + 256 * f3;
+  kfp[i] = kf[(size_t)h * kN + f];
+}
+
+}  // namespace tcfft
+
+// ---------------------------------------------------------------- host side
+namespace {
+
+using namespace tcfft;
+
+// dense real-stacked DFT block in its K-major swizzled smem image
+template <typename T>
+void put(std::vector<uint8_t>& img, uint32_t base, int swz, uint32_t row, uint32_t k, double v) {
+  uint32_t off;
+  if (swz == tc::kSw32) off = tc::kmajor_off<tc::kSw32>(row, k);
+  else if (swz == tc::kSw64) off = tc::kmajor_off<tc::kSw64>(row, k);
+  else off = tc::kmajor_off<tc::kSw128>(row, k);
+  T h;
+  if constexpr (std::is_same<T, __nv_bfloat16>::value) h = __float2bfloat16_rn((float)v);
+  else h = __float2half_rn((float)v);
+  std::memcpy(&img[base + off], &h, 2);
+}
+
+// out-rows / in-cols of a complex block given by callback M(o, i) -> (re, im);
+// K order [re in 0..KI-1 | im in 0..KI-1]; N order given by nmap(row) ->
+// (output index, is_imag).
+template <typename T, class MF, class NM>
+void build_block(std::vector<uint8_t>& img, uint32_t base, int swz, int KI, int NROWS, MF M, NM nmap) {
+  for (int r = 0; r < NROWS; ++r) {
+    int o;
+    bool imag;
+    nmap(r, o, imag);
+    for (int i = 0; i < KI; ++i) {
+      double mr, mi;
+      M(o, i, mr, mi);
+      if (!imag) {
+        put<T>(img, base, swz, r, i, mr);
+        put<T>(img, base, swz, r, KI + i, -mi);
+      } else {
+        put<T>(img, base, swz, r, i, mi);
+        put<T>(img, base, swz, r, KI + i, mr);
+      }
+    }
+  }
+}
+
+template <typename T>
+std::vector<uint8_t> build_mats() {
+  std::vector<uint8_t> img(MAT_BYTES, 0);
+  auto dft = [](int r, double sign) {
+    return [r, sign](int o, int i, double& re, double& im) {
+      const double a = sign * 2.0 * M_PI * (double)((o * i) % r) / (double)r;
+      re = std::cos(a);
+      im = std::sin(a);
+    };
+  };
+  // natural N order: rows [re 0..n-1 | im 0..n-1]
+  auto nat = [](int n) { return [n](int r, int& o, bool& im) { o = r % n; im = r >= n; }; };
+  // 32-output blocks split in halves: [re 0..15 | im 0..15 | re 16..31 | im 16..31]
+  auto halves = [](int r, int& o, bool& im) {
+    const int hblk = r / 32, q = r % 32;
+    o = 16 * hblk + (q % 16);
+    im = q >= 16;
+  };
+  build_block<T>(img, MAT_FA, tc::kSw32, 8, 32, dft(16, -1.0), nat(16));   // t1 < 8 only
+  build_block<T>(img, MAT_FB, tc::kSw64, 16, 32, dft(16, -1.0), nat(16));
+  build_block<T>(img, MAT_FC, tc::kSw128, 32, 64, dft(32, -1.0), halves);
+  build_block<T>(img, MAT_IC, tc::kSw128, 32, 64, dft(32, +1.0), halves);
+  build_block<T>(img, MAT_IB, tc::kSw64, 16, 32, dft(16, +1.0), nat(16));
+  build_block<T>(img, MAT_IA, tc::kSw64, 16, 16, dft(16, +1.0), nat(8));  // t1 < 8 only
+  return img;
+}
+
+using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                              const cuuint64_t*, const cuuint32_t*, const cuuint32_t*,
+                              CUtensorMapInterleave, CUtensorMapSwizzle, CUtensorMapL2promotion,
+                              CUtensorMapFloatOOBfill);
+
+EncodeFn encode_fn() {
+  static EncodeFn fn = nullptr;
+  if (!fn) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeFn>(p);
+  }
+  return fn;
+}
+
+// signal [B][H][4096] viewed as [B][H][8 t1][512 m]; box [64 m][8 t1][1][2 b]
+template <typename T>
+int make_map(CUtensorMap* map, const void* ptr, int64_t B, int64_t H) {
+  EncodeFn enc = encode_fn();
+  if (!enc) {
+    set_error("tcgen05 path: cuTensorMapEncodeTiled unavailable");
+    return FB_ERR_CUDA;
+  }
+  const cuuint64_t dims[4] = {512, 8, (cuuint64_t)H, (cuuint64_t)B};
+  const cuuint64_t strides[3] = {512 * 2, 4096 * 2, (cuuint64_t)H * 4096 * 2};
+  const cuuint32_t box[4] = {64, 8, 1, 2};
+  const cuuint32_t es[4] = {1, 1, 1, 1};
+  CUresult r = enc(map, Fmt<T>::tma, 4, const_cast<void*>(ptr), dims, strides, box, es,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) {
+    set_error("cuTensorMapEncodeTiled failed (" + std::to_string((int)r) + ")");
+    return FB_ERR_CUDA;
+  }
+  return FB_OK;
+}
+
+int chunks_tc(const fb_plan* p, int64_t B) {
+  const int64_t npairs = (B + 1) / 2;
+  int64_t c = (p->num_sms + p->H - 1) / p->H;
+  return (int)std::max<int64_t>(1, std::min<int64_t>(c, npairs));
+}
+
+}  // namespace
+
+bool tc_eligible(const fb_plan* p) {
+  return p->mode == FB_MODE_CAUSAL && p->N == 4096 && p->n == 8192 &&
+         (p->dtype == FB_BF16 || p->dtype == FB_F16);
+}
+
+int tc_init(fb_plan* p) {
+  std::vector<uint8_t> img = p->dtype == FB_BF16 ? build_mats<__nv_bfloat16>() : build_mats<__half>();
+  int rc = cuda_status(cudaMalloc(&p->tc_mats, img.size()), "cudaMalloc(tc mats)");
+  if (!rc)
+    rc = cuda_status(cudaMemcpy(p->tc_mats, img.data(), img.size(), cudaMemcpyHostToDevice),
+                     "copy tc mats");
+  if (!rc)
+    rc = cuda_status(cudaMalloc(&p->kf_tc, sizeof(float2) * p->H * kN), "cudaMalloc(kf_tc)");
+  return rc;
+}
+
+int tc_prep_permute(fb_plan* p, cudaStream_t s) {
+  const uint32_t total = (uint32_t)(p->H * kN);
+  permute_kf_kernel<<<(total + 255) / 256, 256, 0, s>>>(p->kf, p->kf_tc, (int)p->H);
+  return cuda_status(cudaGetLastError(), "tc permute kf");
+}
+
+int tc_fwd(fb_plan* p, const void* u, void* y, int64_t B, cudaStream_t s) {
+  const int chunks = chunks_tc(p, B);
+  const int64_t npairs = (B + 1) / 2;
+  const int ppc = (int)((npairs + chunks - 1) / chunks);
+  CUtensorMap map;
+  auto go = [&](auto tv) {
+    using T = decltype(tv);
+    int rc = make_map<T>(&map, u, B, p->H);
+    if (rc) return rc;
+    auto k = tc_fwd_kernel<T>;
+    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM_BYTES);
+    k<<<dim3((unsigned)p->H, (unsigned)chunks), kThreads, SMEM_BYTES, s>>>(
+        map, (const T*)u, (T*)y, p->kf_tc, (const uint4*)p->tc_mats, p->d, p->tw2, (int)B,
+        (int)p->H, ppc);
+    return cuda_status(cudaGetLastError(), "tc_fwd");
+  };
+  return p->dtype == FB_BF16 ? go(__nv_bfloat16{}) : go(__half{});
+}
+
+size_t tc_workspace(const fb_plan* p, int64_t B) {
+  const int c = chunks_tc(p, B);
+  size_t bytes = (size_t)p->H * c * kN * sizeof(float2);
+  bytes += (size_t)p->H * c * sizeof(float);
+  bytes = (bytes + 255) & ~size_t(255);
+  bytes += (size_t)p->H * p->N * sizeof(float);
+  return bytes + 256;
+}
+
+int sp_finalize(fb_plan* p, const float2* spart, const float* ddpart, int chunks, float* dkbar,
+                float* dD, cudaStream_t s);
+
+int tc_bwd(fb_plan* p, const void* dy, const void* u, void* du, float* dK, float* dKbar, float* dD,
+           int64_t B, void* ws, cudaStream_t s) {
+  const int chunks = chunks_tc(p, B);
+  const int64_t npairs = (B + 1) / 2;
+  const int ppc = (int)((npairs + chunks - 1) / chunks);
+  char* w = (char*)ws;
+  float2* spart = (float2*)w;
+  size_t off = (size_t)p->H * chunks * kN * sizeof(float2);
+  float* ddpart = (float*)(w + off);
+  off += (size_t)p->H * chunks * sizeof(float);
+  off = (off + 255) & ~size_t(255);
+  float* dkbar = dKbar ? dKbar : (float*)(w + off);
+  CUtensorMap dmap, umap;
+  auto go = [&](auto tv) {
+    using T = decltype(tv);
+    int rc = make_map<T>(&dmap, dy, B, p->H);
+    if (!rc) rc = make_map<T>(&umap, u, B, p->H);
+    if (rc) return rc;
+    auto k = tc_bwd_kernel<T>;
+    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM_BYTES);
+    k<<<dim3((unsigned)p->H, (unsigned)chunks), kThreads, SMEM_BYTES, s>>>(
+        dmap, umap, (const T*)dy, (const T*)u, (T*)du, p->kf_tc, (const uint4*)p->tc_mats, p->d,
+        p->tw2, spart, ddpart, (int)B, (int)p->H, ppc);
+    return cuda_status(cudaGetLastError(), "tc_bwd");
+  };
+  int rc = p->dtype == FB_BF16 ? go(__nv_bfloat16{}) : go(__half{});
+  if (rc) return rc;
+  rc = sp_finalize(p, spart, ddpart, chunks, dkbar, dD, s);
+  if (rc) return rc;
+  return regularizer_backward_dev(p, dkbar, dK, s);
+}
+
+}  // namespace fb

@@ -42,6 +42,16 @@ __host__ __device__ __forceinline__ uint32_t kmajor_off(uint32_t row, uint32_t k
   return lin ^ ((lin >> 3) & mask);
 }
 
+// Byte offset of element (m, k) in an MN-major SW128 operand of MT rows
+// (MT % 64 == 0): atoms of 8 k x 64 m (1024 B), laid out
+// [k / 8][m / 64][k % 8][m % 64]  =>  LBO (MN-block stride) = 1024 B,
+// SBO (8-k group stride) = (MT / 64) * 1024 B; canonical
+// ((8,n),(8,k)):((1,LBO),(8,SBO)) in 16-byte units.
+__host__ __device__ __forceinline__ uint32_t mnmajor_off(uint32_t m, uint32_t k, uint32_t MT) {
+  const uint32_t lin = (k >> 3) * (MT / 64) * 1024 + (m >> 6) * 1024 + (k & 7) * 128 + (m & 63) * 2;
+  return lin ^ ((lin >> 3) & 0x70u);
+}
+
 __device__ __forceinline__ uint64_t smem_desc(uint32_t saddr, uint32_t sbo_bytes, int swz,
                                               uint32_t lbo_bytes = 16) {
   uint64_t d = 0;

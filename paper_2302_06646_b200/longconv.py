@@ -33,6 +33,7 @@ class Engine(enum.IntEnum):
     AUTO = _lib.FB_ENGINE_AUTO
     BUTTERFLY = _lib.FB_ENGINE_SINGLE  # single-pass fused kernel
     THREE_PASS = _lib.FB_ENGINE_THREE
+    BUTTERFLY_SIMT = _lib.FB_ENGINE_SINGLE_SIMT  # single-pass on CUDA cores (fp32 FFT)
 
 
 class ConvMode(enum.IntEnum):  # butterfly.hpp:69
@@ -90,6 +91,7 @@ class LongConvPlan:
         info = _lib.PlanInfo()
         check(_lib.lib().fb_plan_get_info(h, C.byref(info)))
         self.n, self.l, self.m, self.engine = info.n, info.l, info.m, Engine(info.engine)
+        self.tensor_cores = bool(info.tensor_cores)
         self._token = None
 
     def __del__(self):

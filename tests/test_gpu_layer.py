@@ -163,6 +163,56 @@ def test_dimension_errors():
                                     fb.RegularizationConfig(lambda_=-1.0))
 
 
+# ------------------------------------------------------------ tcgen05 single-pass
+@pytest.mark.parametrize("dtype", [torch.bfloat16, torch.float16])
+@pytest.mark.parametrize("B,H", [(2, 2), (3, 3), (5, 1)])
+def test_tensor_core_single_pass(lc, dtype, B, H):
+    N = 4096
+    inp = layer_inputs(lc, B, H, N, dtype)
+    cfg = fb.RegularizationConfig(**CFG)
+    plan, got = run_layer(inp, N, H, dtype, cfg, engine=1)
+    assert plan.tensor_cores, "16-bit causal N=4096 must run on tcgen05"
+    assert_parity(got, oracle_layer(lc, inp, cfg), TOL[dtype])
+
+
+def test_tensor_core_matches_simt(lc):
+    """tcgen05 path vs the fp32 CUDA-core path on identical bf16 inputs."""
+    B, H, N = 4, 2, 4096
+    inp = layer_inputs(lc, B, H, N, torch.bfloat16)
+    cfg = fb.RegularizationConfig(**CFG)
+    _, a = run_layer(inp, N, H, torch.bfloat16, cfg, engine=1)
+    _, b = run_layer(inp, N, H, torch.bfloat16, cfg, engine=3)
+    for k in ("y", "du", "dK", "dD"):
+        assert rel_l2(a[k], b[k]) < 2e-2, k
+
+
+def test_config2_heads_sample_tensor_core(lc):
+    """BASELINE config 2 (B=32 H=256 N=4096 bf16) on tcgen05; a head sample
+    (all batches, so dK is complete) against the fp64 oracle."""
+    B, H, N = 32, 256, 4096
+    dtype = torch.bfloat16
+    g = torch.Generator(device="cuda").manual_seed(7)
+    u = torch.randn(B, H, N, device="cuda", generator=g).to(dtype)
+    dy = torch.randn(B, H, N, device="cuda", generator=g).to(dtype)
+    K, D = lc.init_kernels(1, H, N, 3)
+    tK = torch.tensor(K, dtype=torch.float32, device="cuda")
+    tD = torch.tensor(D, dtype=torch.float32, device="cuda")
+    cfg = fb.RegularizationConfig(**CFG)
+    plan = fb.LongConvPlan(N, H, fb.ConvMode.CAUSAL, dtype)
+    assert plan.tensor_cores
+    plan.prep(tK, tD, cfg)
+    y = plan.forward(u)
+    du, dK, dD = plan.backward(dy, u)
+    torch.cuda.synchronize()
+    heads = [0, 131, 255]
+    sub = dict(u=to_np(u[:, heads]), dy=to_np(dy[:, heads]), K=to_np(tK[heads]), D=to_np(tD[heads]))
+    want = oracle_layer(lc, sub, cfg)
+    got = dict(y=to_np(y[:, heads]), du=to_np(du[:, heads]), dK=to_np(dK[heads]),
+               dD=to_np(dD[heads]))
+    errs = assert_parity(got, want, 2e-2, keys=("y", "du", "dK", "dD"))
+    print("config2 tcgen05 rel-L2:", errs)
+
+
 # ------------------------------------------------------------ three-pass (K3/K4b)
 @pytest.mark.parametrize("B,H,N,mode", [(2, 2, 8192, 1), (3, 2, 16384, 1), (2, 1, 65536, 1),
                                         (2, 2, 16384, 0)])
