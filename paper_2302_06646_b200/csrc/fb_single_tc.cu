@@ -41,19 +41,20 @@ constexpr uint32_t kN = 8192;
 constexpr uint32_t kThreads = 512;
 
 // shared memory map (bytes, 1024-aligned where swizzled operands live)
-constexpr uint32_t SA = 0;                    // [2][16 KB] input pairs (MN-major, [mb][kg][8][64])
-constexpr uint32_t SB = SA + 2 * 16384;       // 32 KB B / B' operand (MN-major [kg 4][mb 8][8][64])
-constexpr uint32_t SC = SB + 32768;           // 32 KB C / C' operand (K-major SW128, 256 x 64)
-constexpr uint32_t SA2 = SC + 32768;          // 32 KB A' operand (MN-major [kg 4][mb 8][8][64])
-constexpr uint32_t SMAT = SA2 + 32768;        // 22 KB DFT blocks
+constexpr uint32_t SIN = 0;                   // inputs: fwd [2][16 KB] u pairs; bwd [2][dy,u][16 KB]
+constexpr uint32_t SIN_BYTES = 4 * 16384;
+constexpr uint32_t SOP = SIN + SIN_BYTES;     // 32 KB: B / C / C' / B' / A' operand (one live at a time)
+constexpr uint32_t SMAT = SOP + 32768;        // 22 KB DFT blocks
 constexpr uint32_t MAT_FA = 0, MAT_FB = 1024, MAT_FC = 3072, MAT_IC = 11264, MAT_IB = 19456,
                    MAT_IA = 21504, MAT_BYTES = 22528;
-constexpr uint32_t SKF = SMAT + MAT_BYTES;    // 64 KB k_f, [f3 32][m_C 256] float2
+constexpr uint32_t SKF = SMAT + MAT_BYTES;    // 64 KB k_f' = (K_hat + D)/n, [f3 32][m_C 256] float2
 constexpr uint32_t STAB = SKF + 65536;        // two-level twiddle table (192 float2)
 constexpr uint32_t SMEM_BYTES = STAB + 1536 + 1024;  // + alignment slack
 
-// TMEM column regions (512 allocated)
-constexpr uint32_t R1 = 0, R2 = 128, R3 = 256, R4 = 384;
+// TMEM columns (512 allocated): R1 working region of every stage (each MMA
+// starts after the previous epilogue drained it), R3 holds F(dy) while F(u)
+// runs (backward), R4 the resident dK spectrum accumulator S.
+constexpr uint32_t R1 = 0, R3 = 256, R4 = 384;
 
 // element offsets of the MN-major operands
 __device__ __forceinline__ uint32_t sw128(uint32_t lin) { return lin ^ ((lin >> 3) & 0x70u); }
@@ -83,6 +84,39 @@ template <typename T>
 __host__ __device__ constexpr uint32_t idesc(uint32_t M, uint32_t N, bool a_mn) {
   return (1u << 4) | (Fmt<T>::ab << 7) | (Fmt<T>::ab << 10) | ((a_mn ? 1u : 0u) << 15) |
          ((N >> 3) << 17) | ((M >> 4) << 24);
+}
+
+// Scatter of one register row into an MN-major [kg][mb][8][64] operand:
+// element (m = 32 q + t3, k) for q = 0..15 with the thread's t3 and k fixed
+// (re at k, im at k + 16).  With m >> 6 = q >> 1 and the 128B swizzle chunk
+// (4 (q & 1) + t3 / 8) ^ (k & 7), the 32 addresses reduce to two per-thread
+// bases plus compile-time immediates.
+template <typename T>
+__device__ __forceinline__ void scatter_mn(unsigned char* op, uint32_t t3, uint32_t k,
+                                           const float (&v)[32]) {
+  const uint32_t x = (t3 >> 3) ^ (k & 7);
+  unsigned char* b0 = op + (k >> 3) * 8192 + (k & 7) * 128 + (2 * t3 & 15) + 16 * x;
+  unsigned char* b1 = op + (k >> 3) * 8192 + (k & 7) * 128 + (2 * t3 & 15) + 16 * (x ^ 4);
+#pragma unroll
+  for (int q = 0; q < 16; ++q) {
+    unsigned char* b = (q & 1) ? b1 : b0;
+    *reinterpret_cast<T*>(b + (q >> 1) * 1024) = cvt<T>(v[q]);
+    *reinterpret_cast<T*>(b + (q >> 1) * 1024 + 16384) = cvt<T>(v[16 + q]);
+  }
+}
+// Scatter into the K-major SW128 C operand: rows r = 16 f1 + q (q = 0..15),
+// column k = t3 (re) and 32 + t3 (im); swizzle chunk ((k / 8) ^ (r & 7)).
+template <typename T>
+__device__ __forceinline__ void scatter_c(unsigned char* op, uint32_t f1, uint32_t t3,
+                                          const float (&v)[32]) {
+  const uint32_t c0 = t3 >> 3;
+  unsigned char* base = op + 2 * f1 * 1024 + (2 * t3 & 15);
+#pragma unroll
+  for (int q = 0; q < 16; ++q) {
+    unsigned char* r = base + (q >> 3) * 1024 + (q & 7) * 128;
+    *reinterpret_cast<T*>(r + 16 * (c0 ^ (q & 7))) = cvt<T>(v[q]);
+    *reinterpret_cast<T*>(r + 16 * ((c0 ^ 4) ^ (q & 7))) = cvt<T>(v[16 + q]);
+  }
 }
 
 template <typename T>
@@ -134,6 +168,20 @@ __device__ __forceinline__ void st32(uint32_t taddr, const float (&v)[32]) {
       "r"(r[29]), "r"(r[30]), "r"(r[31])
       : "memory");
 }
+__device__ __forceinline__ void ld8(uint32_t taddr, float* v) {
+  uint32_t* r = reinterpret_cast<uint32_t*>(v);
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]),
+                 "=r"(r[6]), "=r"(r[7])
+               : "r"(taddr));
+}
+__device__ __forceinline__ void st8t(uint32_t taddr, const float* v) {
+  const uint32_t* r = reinterpret_cast<const uint32_t*>(v);
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"r"(taddr),
+               "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]),
+               "r"(r[7])
+               : "memory");
+}
 __device__ __forceinline__ void st_wait() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
 
 __device__ __forceinline__ void tma_load_4d(void* dst, const CUtensorMap* map, int c0, int c1, int c2,
@@ -159,6 +207,15 @@ __device__ __forceinline__ void load_pair(unsigned char* dst, const CUtensorMap*
 // kernels.  Thread (warp w, lane): slab s = w & 3 (TMEM lanes 32s..32s+31),
 // group g = w >> 2.
 // --------------------------------------------------------------------------
+// Thread coordinates re-read through volatile asm in every epilogue: they
+// are loop invariant, and letting the compiler hoist the ~100 derived smem
+// addresses out of the pair loop costs more registers than recomputing.
+__device__ __forceinline__ uint32_t tid_v() {
+  uint32_t t;
+  asm volatile("mov.u32 %0, %%tid.x;" : "=r"(t));
+  return t;
+}
+
 struct Ctx {
   unsigned char* sm;
   uint32_t smb;    // shared address of sm
@@ -194,201 +251,191 @@ __device__ __forceinline__ void mma_A(const Ctx& c, uint32_t sa_off) {
     tc::mma_bf16(c.tmem + R1 + 32 * t, ad, bd, id, 0);
   }
 }
-// K = 32, MN-major operand at `op` ([kg][mb][8][64]: LBO 1024, SBO 8192)
+// K = 32, MN-major operand in SOP ([kg][mb][8][64]: LBO 1024, SBO 8192)
 template <typename T>
-__device__ __forceinline__ void mma_mn32(const Ctx& c, uint32_t op, uint32_t mat, uint32_t N,
-                                         uint32_t dcol, uint32_t mat_sbo, int mat_swz) {
+__device__ __forceinline__ void mma_mn32(const Ctx& c, uint32_t mat, uint32_t N, uint32_t mat_sbo,
+                                         int mat_swz) {
   const uint32_t id = idesc<T>(128, N, true);
   for (uint32_t t = 0; t < 4; ++t)
     for (uint32_t ks = 0; ks < 2; ++ks) {
-      const uint64_t ad = tc::smem_desc(c.smb + op + t * 2048 + ks * 2 * 8192, 8192, tc::kSw128, 1024);
+      const uint64_t ad = tc::smem_desc(c.smb + SOP + t * 2048 + ks * 2 * 8192, 8192, tc::kSw128, 1024);
       const uint64_t bd = tc::smem_desc(c.smb + SMAT + mat + ks * 32, mat_sbo, mat_swz);
-      tc::mma_bf16(c.tmem + dcol + N * t, ad, bd, id, ks);
+      tc::mma_bf16(c.tmem + R1 + N * t, ad, bd, id, ks);
     }
 }
-// stage C / C': 2 M-tiles x (N 64, K 64), A K-major SW128 (256 x 128 B)
+// stage C / C': 2 M-tiles x (N 64, K 64), A K-major SW128 (256 x 128 B) in SOP
 template <typename T>
 __device__ __forceinline__ void mma_C(const Ctx& c, uint32_t mat, uint32_t dcol) {
   const uint32_t id = idesc<T>(128, 64, false);
   for (uint32_t t = 0; t < 2; ++t)
     for (uint32_t ks = 0; ks < 4; ++ks) {
-      const uint64_t ad = tc::smem_desc(c.smb + SC + t * 16384 + ks * 32, 1024, tc::kSw128);
+      const uint64_t ad = tc::smem_desc(c.smb + SOP + t * 16384 + ks * 32, 1024, tc::kSw128);
       const uint64_t bd = tc::smem_desc(c.smb + SMAT + mat + ks * 32, 1024, tc::kSw128);
       tc::mma_bf16(c.tmem + dcol + 64 * t, ad, bd, id, ks);
     }
 }
 
+__device__ __forceinline__ void coords(uint32_t& g, uint32_t& s, uint32_t& lane) {
+  const uint32_t t = tid_v();
+  lane = t & 31;
+  s = (t >> 5) & 3;
+  g = t >> 7;
+}
 __device__ __forceinline__ uint32_t lane_addr(const Ctx& c, uint32_t col) {
-  return c.tmem + ((32u * c.s) << 16) + col;
+  return c.tmem + ((32u * ((tid_v() >> 5) & 3)) << 16) + col;
 }
 
-// Forward transform of the pair staged at sa_off: leaves X[f] in TMEM R3
-// (D_C: rows m_C, cols [re f3 0..15 | im 0..15 | re 16..31 | im 16..31]).
+// (v[r], v[16 + r]) *= w
+__device__ __forceinline__ void cmul_at(float (&v)[32], int r, float2 w) {
+  const float a = v[r], b = v[16 + r];
+  v[r] = fmaf(a, w.x, -b * w.y);
+  v[16 + r] = fmaf(a, w.y, b * w.x);
+}
+// split re/im row: (v[r], v[16+r]) *= w^(r base), r = 1..15 — four table
+// lookups, the rest by products of depth <= 3
+template <int SIGN>
+__device__ __forceinline__ void twiddle16(float (&v)[32], const float2* tab, uint32_t base) {
+  const float2 w1 = tw2<SIGN>(tab, base), w2 = tw2<SIGN>(tab, 2 * base);
+  const float2 w4 = tw2<SIGN>(tab, 4 * base), w8 = tw2<SIGN>(tab, 8 * base);
+  const float2 w3 = cmul(w1, w2), w5 = cmul(w1, w4), w6 = cmul(w2, w4), w7 = cmul(w3, w4);
+  cmul_at(v, 1, w1);
+  cmul_at(v, 2, w2);
+  cmul_at(v, 3, w3);
+  cmul_at(v, 4, w4);
+  cmul_at(v, 5, w5);
+  cmul_at(v, 6, w6);
+  cmul_at(v, 7, w7);
+  cmul_at(v, 8, w8);
+  cmul_at(v, 9, cmul(w1, w8));
+  cmul_at(v, 10, cmul(w2, w8));
+  cmul_at(v, 11, cmul(w3, w8));
+  cmul_at(v, 12, cmul(w4, w8));
+  cmul_at(v, 13, cmul(w5, w8));
+  cmul_at(v, 14, cmul(w6, w8));
+  cmul_at(v, 15, cmul(w7, w8));
+}
+
+template <typename T>
+__device__ __forceinline__ void issue(Ctx& c, int stage, uint32_t arg) {
+  publish(c);
+  if (threadIdx.x == 0) {
+    switch (stage) {
+      case 0: mma_A<T>(c, arg); break;
+      case 1: mma_mn32<T>(c, MAT_FB, 32, 512, tc::kSw64); break;
+      case 2: mma_C<T>(c, MAT_FC, arg); break;
+      case 3: mma_C<T>(c, MAT_IC, R1); break;
+      case 4: mma_mn32<T>(c, MAT_IB, 32, 512, tc::kSw64); break;
+      default: mma_mn32<T>(c, MAT_IA, 16, 512, tc::kSw64); break;
+    }
+    tc::commit(c.mma_bar);
+  }
+  mma_wait(c);
+}
+
+// Forward transform of the pair staged at sa_off (TMA barrier in_bar):
+// X[f] ends in TMEM cols dstC + 64 T (rows m_C; cols [re f3 0..15 | im 0..15
+// | re 16..31 | im 16..31]).
 template <typename T>
 __device__ __forceinline__ void forward_fft(Ctx& c, uint32_t sa_off, uint64_t* in_bar,
-                                            uint32_t in_phase, bool* in_free_hook) {
-  // ---- stage A
+                                            uint32_t in_phase, uint32_t dstC) {
   ptx::mbar_wait(in_bar, in_phase);
-  tc::fence_after();
-  if (threadIdx.x == 0) {
-    mma_A<T>(c, sa_off);
-    tc::commit(c.mma_bar);
-  }
-  mma_wait(c);
-  if (in_free_hook) *in_free_hook = true;
-  // ---- A -> B: twiddle w^(f1 m_A)
+  issue<T>(c, 0, sa_off);
+  // ---- A -> B: twiddle w^(f1 m_A); B operand rows m_B = 32 f1 + t3, k = t2
   {
-    const uint32_t m = 128 * c.g + 32 * c.s + c.lane;  // = 32 t2 + t3
-    const uint32_t t2 = m >> 5, t3 = c.lane;
+    uint32_t g, sl, lane;
+    coords(g, sl, lane);
+    const uint32_t m = 128 * g + 32 * sl + lane;  // = 32 t2 + t3
+    const uint32_t t2 = m >> 5, t3 = lane;
     float v[32];
-    tc::ld32(lane_addr(c, R1 + 32 * c.g), v);
+    tc::ld32(lane_addr(c, R1 + 32 * g), v);
     tc::ld_wait();
-    float2 X[16];
-#pragma unroll
-    for (int f = 0; f < 16; ++f) X[f] = make_float2(v[f], v[16 + f]);
-    apply_tw<-1, 16>(X, c.tab, m);
-    unsigned char* sb = c.sm + SB;
-#pragma unroll
-    for (int f1 = 0; f1 < 16; ++f1) {
-      const uint32_t mb = 32 * f1 + t3;
-      st16<T>(sb, off_mn(mb, t2), X[f1].x);
-      st16<T>(sb, off_mn(mb, 16 + t2), X[f1].y);
-    }
+    twiddle16<-1>(v, c.tab, m);
+    scatter_mn<T>(c.sm + SOP, t3, t2, v);
   }
-  publish(c);
-  if (threadIdx.x == 0) {
-    mma_mn32<T>(c, SB, MAT_FB, 32, R2, 512, tc::kSw64);
-    tc::commit(c.mma_bar);
-  }
-  mma_wait(c);
-  // ---- B -> C: twiddle w_512^(f2 t3)
+  issue<T>(c, 1, 0);
+  // ---- B -> C: twiddle w_512^(f2 t3); C operand rows m_C = 16 f1 + f2, k = t3
   {
-    const uint32_t mB = 128 * c.g + 32 * c.s + c.lane;  // = 32 f1 + t3
-    const uint32_t f1 = mB >> 5, t3 = c.lane;
+    uint32_t g, sl, lane;
+    coords(g, sl, lane);
+    const uint32_t mB = 128 * g + 32 * sl + lane;  // = 32 f1 + t3
+    const uint32_t f1 = mB >> 5, t3 = lane;
     float v[32];
-    tc::ld32(lane_addr(c, R2 + 32 * c.g), v);
+    tc::ld32(lane_addr(c, R1 + 32 * g), v);
     tc::ld_wait();
-    float2 Y[16];
-#pragma unroll
-    for (int f = 0; f < 16; ++f) Y[f] = make_float2(v[f], v[16 + f]);
-    apply_tw<-1, 16>(Y, c.tab, 16 * t3);
-    unsigned char* sc = c.sm + SC;
-#pragma unroll
-    for (int f2 = 0; f2 < 16; ++f2) {
-      const uint32_t mC = 16 * f1 + f2;
-      st16<T>(sc, tc::kmajor_off<tc::kSw128>(mC, t3), Y[f2].x);
-      st16<T>(sc, tc::kmajor_off<tc::kSw128>(mC, 32 + t3), Y[f2].y);
-    }
+    twiddle16<-1>(v, c.tab, 16 * t3);
+    scatter_c<T>(c.sm + SOP, f1, t3, v);
   }
-  publish(c);
-  if (threadIdx.x == 0) {
-    mma_C<T>(c, MAT_FC, R3);
-    tc::commit(c.mma_bar);
-  }
-  mma_wait(c);
+  issue<T>(c, 2, dstC);
 }
 
 // Spectrum row owned by this thread at the C exit: m_C and half h.
-__device__ __forceinline__ void c_row(const Ctx& c, uint32_t& mC, uint32_t& h) {
-  mC = 128 * (c.g & 1) + 32 * c.s + c.lane;
-  h = c.g >> 1;
+__device__ __forceinline__ void c_row(const Ctx&, uint32_t& mC, uint32_t& h) {
+  uint32_t g, sl, lane;
+  coords(g, sl, lane);
+  mC = 128 * (g & 1) + 32 * sl + lane;
+  h = g >> 1;
 }
 
-// Write Z[j] (f3 = 16h + j) as the C' operand row (K-major SW128).
+// Write the row half (re v[0..15], im v[16..31] at f3 = 16h + j) as the C'
+// operand (K-major SW128, k = [re f3 | im f3]).
 template <typename T>
-__device__ __forceinline__ void write_cprime(const Ctx& c, uint32_t mC, uint32_t h, const float2 (&Z)[16]) {
-  unsigned char* sc = c.sm + SC;
-  float re[16], im[16];
-#pragma unroll
-  for (int j = 0; j < 16; ++j) {
-    re[j] = Z[j].x;
-    im[j] = Z[j].y;
-  }
-  st8<T>(sc + tc::kmajor_off<tc::kSw128>(mC, 16 * h), re);
-  st8<T>(sc + tc::kmajor_off<tc::kSw128>(mC, 16 * h + 8), re + 8);
-  st8<T>(sc + tc::kmajor_off<tc::kSw128>(mC, 32 + 16 * h), im);
-  st8<T>(sc + tc::kmajor_off<tc::kSw128>(mC, 32 + 16 * h + 8), im + 8);
+__device__ __forceinline__ void write_cprime(const Ctx& c, uint32_t mC, uint32_t h, const float (&v)[32]) {
+  unsigned char* op = c.sm + SOP;
+  st8<T>(op + tc::kmajor_off<tc::kSw128>(mC, 16 * h), v);
+  st8<T>(op + tc::kmajor_off<tc::kSw128>(mC, 16 * h + 8), v + 8);
+  st8<T>(op + tc::kmajor_off<tc::kSw128>(mC, 32 + 16 * h), v + 16);
+  st8<T>(op + tc::kmajor_off<tc::kSw128>(mC, 32 + 16 * h + 8), v + 24);
 }
 
-// Inverse transform from the C' operand in SC; leaves z[t] (t1 < 8) in
-// TMEM R2 cols 16 T + [re t1 0..7 | im t1 0..7] of tile T = row block.
+// Inverse transform from the C' operand; leaves z[t] (t1 < 8) in TMEM R1
+// cols 16 T + [re t1 0..7 | im t1 0..7] of row block T.
 template <typename T>
 __device__ __forceinline__ void inverse_fft(Ctx& c) {
-  publish(c);
-  if (threadIdx.x == 0) {
-    mma_C<T>(c, MAT_IC, R3);
-    tc::commit(c.mma_bar);
-  }
-  mma_wait(c);
-  // ---- C' -> B': twiddle w_512^(-f2 t3)
+  issue<T>(c, 3, 0);
+  // ---- C' -> B': twiddle w_512^(-f2 t3); B' operand rows m_B = 32 f1 + t3, k = f2
   {
     uint32_t mC, h;
     c_row(c, mC, h);
     const uint32_t f1 = mC >> 4, f2 = mC & 15;
     float v[32];
-    tc::ld32(lane_addr(c, R3 + 64 * (c.g & 1) + 32 * h), v);
+    tc::ld32(lane_addr(c, R1 + 64 * (mC >> 7) + 32 * h), v);
     tc::ld_wait();
-    float2 W[16];
-#pragma unroll
-    for (int j = 0; j < 16; ++j) W[j] = make_float2(v[j], v[16 + j]);
-    apply_tw<+1, 16>(W, c.tab, 16 * f2);
+    twiddle16<+1>(v, c.tab, 16 * f2);
     if (h) {
       const float2 w = tw2<+1>(c.tab, 256 * f2);
 #pragma unroll
-      for (int j = 0; j < 16; ++j) W[j] = cmul(W[j], w);
+      for (int j = 0; j < 16; ++j) cmul_at(v, j, w);
     }
-    // B' operand: rows m_B = 32 f1 + 16 h + j, k = f2 (re) / 16 + f2 (im)
-    unsigned char* sb = c.sm + SB;
-    float re[16], im[16];
-#pragma unroll
-    for (int j = 0; j < 16; ++j) {
-      re[j] = W[j].x;
-      im[j] = W[j].y;
-    }
+    unsigned char* op = c.sm + SOP;
     const uint32_t m0 = 32 * f1 + 16 * h;
-    st8<T>(sb + off_mn(m0, f2), re);
-    st8<T>(sb + off_mn(m0 + 8, f2), re + 8);
-    st8<T>(sb + off_mn(m0, 16 + f2), im);
-    st8<T>(sb + off_mn(m0 + 8, 16 + f2), im + 8);
+    st8<T>(op + off_mn(m0, f2), v);
+    st8<T>(op + off_mn(m0 + 8, f2), v + 8);
+    st8<T>(op + off_mn(m0, 16 + f2), v + 16);
+    st8<T>(op + off_mn(m0 + 8, 16 + f2), v + 24);
   }
-  publish(c);
-  if (threadIdx.x == 0) {
-    mma_mn32<T>(c, SB, MAT_IB, 32, R1, 512, tc::kSw64);
-    tc::commit(c.mma_bar);
-  }
-  mma_wait(c);
-  // ---- B' -> A': twiddle w^(-f1 (32 t2 + t3))
+  issue<T>(c, 4, 0);
+  // ---- B' -> A': twiddle w^(-f1 (32 t2 + t3)); A' operand rows m_A = 32 t2 + t3, k = f1
   {
-    const uint32_t mB = 128 * c.g + 32 * c.s + c.lane;  // = 32 f1 + t3
-    const uint32_t f1 = mB >> 5, t3 = c.lane;
+    uint32_t g, sl, lane;
+    coords(g, sl, lane);
+    const uint32_t mB = 128 * g + 32 * sl + lane;  // = 32 f1 + t3
+    const uint32_t f1 = mB >> 5, t3 = lane;
     float v[32];
-    tc::ld32(lane_addr(c, R1 + 32 * c.g), v);
+    tc::ld32(lane_addr(c, R1 + 32 * g), v);
     tc::ld_wait();
-    float2 V[16];
-#pragma unroll
-    for (int t = 0; t < 16; ++t) V[t] = make_float2(v[t], v[16 + t]);
-    apply_tw<+1, 16>(V, c.tab, 32 * f1);
+    twiddle16<+1>(v, c.tab, 32 * f1);
     const float2 w = tw2<+1>(c.tab, f1 * t3);
-    unsigned char* sa2 = c.sm + SA2;
 #pragma unroll
-    for (int t2 = 0; t2 < 16; ++t2) {
-      const float2 z = cmul(V[t2], w);
-      const uint32_t mA = 32 * t2 + t3;
-      st16<T>(sa2, off_mn(mA, f1), z.x);
-      st16<T>(sa2, off_mn(mA, 16 + f1), z.y);
-    }
+    for (int t2 = 0; t2 < 16; ++t2) cmul_at(v, t2, w);
+    scatter_mn<T>(c.sm + SOP, t3, f1, v);
   }
-  publish(c);
-  if (threadIdx.x == 0) {
-    mma_mn32<T>(c, SA2, MAT_IA, 16, R2, 512, tc::kSw64);
-    tc::commit(c.mma_bar);
-  }
-  mma_wait(c);
+  issue<T>(c, 5, 0);
 }
 
 __device__ __forceinline__ void setup(Ctx& c, unsigned char* sm, uint32_t* tmem_slot, uint64_t* bars,
-                                      const uint4* __restrict__ mats, const float2* __restrict__ kf_h,
-                                      const float2* __restrict__ tab_g, bool load_kf) {
+                                      int nbars, const uint4* __restrict__ mats,
+                                      const float2* __restrict__ kf_h,
+                                      const float2* __restrict__ tab_g) {
   c.sm = sm;
   c.smb = ptx::smem_u32(sm);
   c.lane = threadIdx.x & 31;
@@ -399,18 +446,16 @@ __device__ __forceinline__ void setup(Ctx& c, unsigned char* sm, uint32_t* tmem_
   c.tab = reinterpret_cast<const float2*>(sm + STAB);
   if (threadIdx.x < 32) tc::alloc<512>(tmem_slot);
   if (threadIdx.x == 0) {
-    for (int i = 0; i < 4; ++i) ptx::mbar_init(&bars[i], 1);
+    for (int i = 0; i < nbars; ++i) ptx::mbar_init(&bars[i], 1);
     ptx::fence_barrier_init();
   }
   uint4* dm = reinterpret_cast<uint4*>(sm + SMAT);
   for (uint32_t i = threadIdx.x; i < MAT_BYTES / 16; i += kThreads) dm[i] = __ldg(mats + i);
   float2* tab = reinterpret_cast<float2*>(sm + STAB);
   for (uint32_t i = threadIdx.x; i < 192; i += kThreads) tab[i] = __ldg(tab_g + i);
-  if (load_kf) {
-    const float4* src = reinterpret_cast<const float4*>(kf_h);
-    float4* dst = reinterpret_cast<float4*>(sm + SKF);
-    for (uint32_t i = threadIdx.x; i < kN / 2; i += kThreads) dst[i] = __ldg(src + i);
-  }
+  const float4* src = reinterpret_cast<const float4*>(kf_h);
+  float4* dst = reinterpret_cast<float4*>(sm + SKF);
+  for (uint32_t i = threadIdx.x; i < kN / 2; i += kThreads) dst[i] = __ldg(src + i);
   ptx::fence_proxy_async_smem();
   tc::fence_before();
   __syncthreads();
@@ -424,16 +469,43 @@ __device__ __forceinline__ void teardown(const Ctx& c) {
   if (threadIdx.x < 32) tc::dealloc<512>(c.tmem);
 }
 
+// A' exit: rows m_A, z[512 t1 + m_A] for t1 < 8 (re -> channel b0, im -> b1).
+template <typename T>
+__device__ __forceinline__ void store_rows(const Ctx& c, T* __restrict__ out, int b0, int B, int H,
+                                           int h) {
+  uint32_t g, sl, lane;
+  coords(g, sl, lane);
+  const uint32_t mA = 128 * g + 32 * sl + lane;
+  float v[16];
+  ld16(lane_addr(c, R1 + 16 * g), v);
+  tc::ld_wait();
+  T* o0 = out + ((size_t)b0 * H + h) * 4096 + mA;
+#pragma unroll
+  for (int t1 = 0; t1 < 8; ++t1) o0[512 * t1] = cvt<T>(v[t1]);
+  if (b0 + 1 < B) {
+    T* o1 = out + ((size_t)(b0 + 1) * H + h) * 4096 + mA;
+#pragma unroll
+    for (int t1 = 0; t1 < 8; ++t1) o1[512 * t1] = cvt<T>(v[8 + t1]);
+  }
+}
+
+__device__ __forceinline__ void pair_end() {
+  tc::fence_before();
+  __syncthreads();
+  tc::fence_after();
+}
+
 // ------------------------------------------------------------------ forward
+// y = F^-1(F(u) * (K_hat + D)/n): the skip term D u is folded into the
+// spectrum (a D-weighted delta kernel), so the epilogue only streams y out.
 template <typename T>
 __global__ void __launch_bounds__(kThreads, 1)
-    tc_fwd_kernel(const __grid_constant__ CUtensorMap umap, const T* __restrict__ u,
-                  T* __restrict__ y, const float2* __restrict__ kfp, const uint4* __restrict__ mats,
-                  const float* __restrict__ D, const float2* __restrict__ tab_g, int B, int H,
-                  int ppc) {
+    tc_fwd_kernel(const __grid_constant__ CUtensorMap umap, T* __restrict__ y,
+                  const float2* __restrict__ kfp, const uint4* __restrict__ mats,
+                  const float2* __restrict__ tab_g, int B, int H, int ppc) {
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   __shared__ uint32_t tmem_slot;
-  __shared__ __align__(8) uint64_t bars[4];  // 0: mma, 1: input
+  __shared__ __align__(8) uint64_t bars[3];  // 0: mma, 1/2: input buffers
   unsigned char* sm = reinterpret_cast<unsigned char*>(
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   const int h = blockIdx.x;
@@ -441,189 +513,147 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int p0 = blockIdx.y * ppc, p1 = min(npairs, p0 + ppc);
   if (p0 >= p1) return;
   Ctx c;
-  setup(c, sm, &tmem_slot, bars, mats, kfp + (size_t)h * kN, tab_g, true);
-  const float d = __ldg(D + h);
+  setup(c, sm, &tmem_slot, bars, 3, mats, kfp + (size_t)h * kN, tab_g);
   const float2* kfs = reinterpret_cast<const float2*>(sm + SKF);
-  if (threadIdx.x == 0) load_pair(sm + SA, &umap, h, 2 * p0, &bars[1]);
-  uint32_t in_phase = 0;
-  for (int pr = p0; pr < p1; ++pr) {
-    const int b0 = 2 * pr, b1 = b0 + 1;
-    const bool has1 = b1 < B;
-    bool in_free = false;
-    forward_fft<T>(c, SA, &bars[1], in_phase, &in_free);
-    in_phase ^= 1;
-    // stage A has consumed the input: prefetch the next pair behind the
-    // remaining five stages
-    if (threadIdx.x == 0 && pr + 1 < p1) load_pair(sm + SA, &umap, h, 2 * (pr + 1), &bars[1]);
-    // ---- C exit: Z = X * k_f  -> C' operand
+  if (threadIdx.x == 0) load_pair(sm + SIN, &umap, h, 2 * p0, &bars[1]);
+  for (int pr = p0, it = 0; pr < p1; ++pr, ++it) {
+    const int buf = it & 1;
+    // prefetch the next pair into the other buffer (its last reader, stage
+    // A of the previous pair, has completed)
+    if (threadIdx.x == 0 && pr + 1 < p1)
+      load_pair(sm + SIN + (buf ^ 1) * 16384, &umap, h, 2 * (pr + 1), &bars[1 + (buf ^ 1)]);
+    forward_fft<T>(c, SIN + buf * 16384, &bars[1 + buf], (it >> 1) & 1, R1);
+    // ---- C exit: Z = X * k_f'  -> C' operand
     {
       uint32_t mC, hh;
       c_row(c, mC, hh);
       float v[32];
-      tc::ld32(lane_addr(c, R3 + 64 * (c.g & 1) + 32 * hh), v);
+      tc::ld32(lane_addr(c, R1 + 64 * (mC >> 7) + 32 * hh), v);
       tc::ld_wait();
-      float2 Z[16];
+      const float2* kr = kfs + (16 * hh) * 256 + mC;
 #pragma unroll
-      for (int j = 0; j < 16; ++j)
-        Z[j] = cmul(make_float2(v[j], v[16 + j]), kfs[(16 * hh + j) * 256 + mC]);
-      write_cprime<T>(c, mC, hh, Z);
+      for (int j = 0; j < 16; ++j) cmul_at(v, j, kr[j * 256]);
+      write_cprime<T>(c, mC, hh, v);
     }
     inverse_fft<T>(c);
-    // ---- A' exit: y = z + D u   (t = 512 t1 + m_A, t1 < 8)
-    {
-      const uint32_t mA = 128 * c.g + 32 * c.s + c.lane;
-      float v[16];
-      ld16(lane_addr(c, R2 + 16 * c.g), v);
-      tc::ld_wait();
-      const size_t o0 = ((size_t)b0 * H + h) * 4096, o1 = ((size_t)b1 * H + h) * 4096;
-#pragma unroll
-      for (int t1 = 0; t1 < 8; ++t1) {
-        const uint32_t t = 512 * t1 + mA;
-        st(y + o0 + t, fmaf(d, ld(u + o0 + t), v[t1]));
-        if (has1) st(y + o1 + t, fmaf(d, ld(u + o1 + t), v[8 + t1]));
-      }
-    }
-    tc::fence_before();
-    __syncthreads();
-    tc::fence_after();
+    store_rows<T>(c, y, 2 * pr, B, H, h);
+    pair_end();
   }
   teardown(c);
 }
 
 // ------------------------------------------------------------------ backward
-// Per pair: DY = F(dy), U = F(u); S += conj(U) DY (S resident in TMEM R4);
-// du = F^-1(DY conj(k_f)) + D dy; dD partial.  S of the CTA's pairs is
-// written in natural frequency order for the finalize kernel.
+// Per pair: DY = F(dy) (held in TMEM R3), U = F(u); S += conj(U) DY with S
+// resident in TMEM R4; du = F^-1(DY conj(k_f')) (skip folded).  S of the
+// CTA's pairs is written in natural frequency order for the finalize kernel
+// (dKbar = Re F^-1(S)/n; dD = dKbar[0]).
 template <typename T>
 __global__ void __launch_bounds__(kThreads, 1)
     tc_bwd_kernel(const __grid_constant__ CUtensorMap dymap, const __grid_constant__ CUtensorMap umap,
-                  const T* __restrict__ dy, const T* __restrict__ u, T* __restrict__ du,
-                  const float2* __restrict__ kfp, const uint4* __restrict__ mats,
-                  const float* __restrict__ D, const float2* __restrict__ tab_g,
-                  float2* __restrict__ spart, float* __restrict__ ddpart, int B, int H, int ppc) {
+                  T* __restrict__ du, const float2* __restrict__ kfp, const uint4* __restrict__ mats,
+                  const float2* __restrict__ tab_g, float2* __restrict__ spart, int B, int H,
+                  int ppc) {
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   __shared__ uint32_t tmem_slot;
-  __shared__ __align__(8) uint64_t bars[4];  // 0: mma, 1: dy, 2: u
-  __shared__ float red[kThreads / 32];
+  __shared__ __align__(8) uint64_t bars[5];  // 0: mma, 1/2: dy buffers, 3/4: u buffers
   unsigned char* sm = reinterpret_cast<unsigned char*>(
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   const int h = blockIdx.x, chunk = blockIdx.y, chunks = gridDim.y;
   const int npairs = (B + 1) / 2;
   const int p0 = chunk * ppc, p1 = min(npairs, p0 + ppc);
   Ctx c;
-  setup(c, sm, &tmem_slot, bars, mats, kfp + (size_t)h * kN, tab_g, true);
-  const float d = __ldg(D + h);
+  setup(c, sm, &tmem_slot, bars, 5, mats, kfp + (size_t)h * kN, tab_g);
   const float2* kfs = reinterpret_cast<const float2*>(sm + SKF);
   uint32_t mC, hh;
   c_row(c, mC, hh);
-  // S := 0 in TMEM R4 (this thread's row / half)
+  const uint32_t scol = R4 + 64 * (mC >> 7) + 32 * hh;
   {
     float z[32];
 #pragma unroll
     for (int i = 0; i < 32; ++i) z[i] = 0.f;
-    st32(lane_addr(c, R4 + 64 * (c.g & 1) + 32 * hh), z);
+    st32(lane_addr(c, scol), z);
     st_wait();
   }
-  float dd = 0.f;
+  // buffers: dy[b] at SIN + b * 32 KB, u[b] at SIN + b * 32 KB + 16 KB
   if (threadIdx.x == 0 && p0 < p1) {
-    load_pair(sm + SA, &dymap, h, 2 * p0, &bars[1]);
-    load_pair(sm + SA + 16384, &umap, h, 2 * p0, &bars[2]);
+    load_pair(sm + SIN, &dymap, h, 2 * p0, &bars[1]);
+    load_pair(sm + SIN + 16384, &umap, h, 2 * p0, &bars[3]);
   }
-  uint32_t ph = 0;
-  for (int pr = p0; pr < p1; ++pr) {
-    const int b0 = 2 * pr, b1 = b0 + 1;
-    const bool has1 = b1 < B;
-    const bool more = pr + 1 < p1;
-    // ---- DY = F(dy)
-    forward_fft<T>(c, SA, &bars[1], ph, nullptr);
-    if (threadIdx.x == 0 && more) load_pair(sm + SA, &dymap, h, 2 * (pr + 1), &bars[1]);
-    float2 DY[16];
-    {
-      float v[32];
-      tc::ld32(lane_addr(c, R3 + 64 * (c.g & 1) + 32 * hh), v);
-      tc::ld_wait();
-#pragma unroll
-      for (int j = 0; j < 16; ++j) DY[j] = make_float2(v[j], v[16 + j]);
+  for (int pr = p0, it = 0; pr < p1; ++pr, ++it) {
+    const int buf = it & 1;
+    const uint32_t ph = (it >> 1) & 1;
+    if (threadIdx.x == 0 && pr + 1 < p1) {
+      load_pair(sm + SIN + (buf ^ 1) * 32768, &dymap, h, 2 * (pr + 1), &bars[1 + (buf ^ 1)]);
+      load_pair(sm + SIN + (buf ^ 1) * 32768 + 16384, &umap, h, 2 * (pr + 1), &bars[3 + (buf ^ 1)]);
     }
-    tc::fence_before();
-    __syncthreads();  // R3 read before F(u) overwrites it
-    tc::fence_after();
-    // ---- U = F(u)
-    forward_fft<T>(c, SA + 16384, &bars[2], ph, nullptr);
-    if (threadIdx.x == 0 && more) load_pair(sm + SA + 16384, &umap, h, 2 * (pr + 1), &bars[2]);
-    ph ^= 1;
+    forward_fft<T>(c, SIN + buf * 32768, &bars[1 + buf], ph, R3);
+    forward_fft<T>(c, SIN + buf * 32768 + 16384, &bars[3 + buf], ph, R1);
     {
-      float v[32], sacc[32];
-      tc::ld32(lane_addr(c, R3 + 64 * (c.g & 1) + 32 * hh), v);
-      tc::ld32(lane_addr(c, R4 + 64 * (c.g & 1) + 32 * hh), sacc);
-      tc::ld_wait();
-      float2 Z[16];
+      // in two quarters of 8 frequencies to keep U, DY, S register-light
+      const uint32_t cu = R1 + 64 * (mC >> 7) + 32 * hh, cg = R3 + 64 * (mC >> 7) + 32 * hh;
+      const float2* kr = kfs + (16 * hh) * 256 + mC;
+      unsigned char* op = c.sm + SOP;
 #pragma unroll
-      for (int j = 0; j < 16; ++j) {
-        const float2 U = make_float2(v[j], v[16 + j]);
-        const float2 a = cconjmul(U, DY[j]);
-        sacc[j] += a.x;
-        sacc[16 + j] += a.y;
-        Z[j] = cmulc(DY[j], kfs[(16 * hh + j) * 256 + mC]);
+      for (int q = 0; q < 2; ++q) {
+        float ur[8], ui[8], gr[8], gi[8], sr[8], si[8];
+        ld8(lane_addr(c, cu + 8 * q), ur);
+        ld8(lane_addr(c, cu + 16 + 8 * q), ui);
+        ld8(lane_addr(c, cg + 8 * q), gr);
+        ld8(lane_addr(c, cg + 16 + 8 * q), gi);
+        ld8(lane_addr(c, scol + 8 * q), sr);
+        ld8(lane_addr(c, scol + 16 + 8 * q), si);
+        tc::ld_wait();
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          // S += conj(U) DY
+          sr[j] = fmaf(ur[j], gr[j], fmaf(ui[j], gi[j], sr[j]));
+          si[j] = fmaf(ur[j], gi[j], fmaf(-ui[j], gr[j], si[j]));
+          // Z = DY conj(k_f')
+          const float2 k = kr[(8 * q + j) * 256];
+          ur[j] = fmaf(gr[j], k.x, gi[j] * k.y);
+          ui[j] = fmaf(gi[j], k.x, -gr[j] * k.y);
+        }
+        st8t(lane_addr(c, scol + 8 * q), sr);
+        st8t(lane_addr(c, scol + 16 + 8 * q), si);
+        st8<T>(op + tc::kmajor_off<tc::kSw128>(mC, 16 * hh + 8 * q), ur);
+        st8<T>(op + tc::kmajor_off<tc::kSw128>(mC, 32 + 16 * hh + 8 * q), ui);
       }
-      st32(lane_addr(c, R4 + 64 * (c.g & 1) + 32 * hh), sacc);
       st_wait();
-      write_cprime<T>(c, mC, hh, Z);
     }
     inverse_fft<T>(c);
-    // ---- A' exit: du = z + D dy; dD partial from dy * u
-    {
-      const uint32_t mA = 128 * c.g + 32 * c.s + c.lane;
-      float v[16];
-      ld16(lane_addr(c, R2 + 16 * c.g), v);
-      tc::ld_wait();
-      const size_t o0 = ((size_t)b0 * H + h) * 4096, o1 = ((size_t)b1 * H + h) * 4096;
-#pragma unroll
-      for (int t1 = 0; t1 < 8; ++t1) {
-        const uint32_t t = 512 * t1 + mA;
-        const float g0 = ld(dy + o0 + t);
-        st(du + o0 + t, fmaf(d, g0, v[t1]));
-        dd = fmaf(g0, ld(u + o0 + t), dd);
-        if (has1) {
-          const float g1 = ld(dy + o1 + t);
-          st(du + o1 + t, fmaf(d, g1, v[8 + t1]));
-          dd = fmaf(g1, ld(u + o1 + t), dd);
-        }
-      }
-    }
-    tc::fence_before();
-    __syncthreads();
-    tc::fence_after();
+    store_rows<T>(c, du, 2 * pr, B, H, h);
+    pair_end();
   }
-  // ---- S (natural order f = f1 + 16 f2 + 256 f3) and dD partials
   {
-    float sacc[32];
-    tc::ld32(lane_addr(c, R4 + 64 * (c.g & 1) + 32 * hh), sacc);
+    float S[32];
+    tc::ld32(lane_addr(c, scol), S);
     tc::ld_wait();
     float2* sp = spart + ((size_t)h * chunks + chunk) * kN;
     const uint32_t f1 = mC >> 4, f2 = mC & 15;
 #pragma unroll
-    for (int j = 0; j < 16; ++j) sp[f1 + 16 * f2 + 256 * (16 * hh + j)] = make_float2(sacc[j], sacc[16 + j]);
-  }
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) dd += __shfl_xor_sync(0xffffffffu, dd, o);
-  if (c.lane == 0) red[threadIdx.x >> 5] = dd;
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    float t = 0.f;
-    for (int w = 0; w < (int)(kThreads / 32); ++w) t += red[w];
-    ddpart[(size_t)h * chunks + chunk] = t;
+    for (int j = 0; j < 16; ++j) sp[f1 + 16 * f2 + 256 * (16 * hh + j)] = make_float2(S[j], S[16 + j]);
   }
   teardown(c);
 }
 
 // k_f (natural order, / n) -> [h][f3][m_C], m_C = 16 f1 + f2, f = f1 + 16 f2 + 256 f3
-__global__ void permute_kf_kernel(const float2* __restrict__ kf, float2* __restrict__ kfp, int H) {
+// plus the skip gain folded in as a flat spectrum: k_f' = k_f + D / n
+__global__ void permute_kf_kernel(const float2* __restrict__ kf, const float* __restrict__ D,
+                                  float2* __restrict__ kfp, int H) {
   const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= (uint32_t)H * kN) return;
   const uint32_t h = i / kN, r = i % kN, f3 = r / 256, mC = r % 256;
   const uint32_t f = (mC >> 4) + 16 * (mC & 15) + 256 * f3;
-  kfp[i] = kf[(size_t)h * kN + f];
+  float2 v = kf[(size_t)h * kN + f];
+  v.x += __ldg(D + h) * (1.0f / (float)kN);
+  kfp[i] = v;
+}
+
+// dD[h] = dKbar[h][0] (the lag-0 correlation of dy and u)
+__global__ void dd_from_dkbar_kernel(const float* __restrict__ dkbar, float* __restrict__ dD, int H,
+                                     int64_t N) {
+  const int h = blockIdx.x * blockDim.x + threadIdx.x;
+  if (h < H) dD[h] = dkbar[(size_t)h * N];
 }
 
 }  // namespace tcfft
@@ -761,7 +791,7 @@ int tc_init(fb_plan* p) {
 
 int tc_prep_permute(fb_plan* p, cudaStream_t s) {
   const uint32_t total = (uint32_t)(p->H * kN);
-  permute_kf_kernel<<<(total + 255) / 256, 256, 0, s>>>(p->kf, p->kf_tc, (int)p->H);
+  permute_kf_kernel<<<(total + 255) / 256, 256, 0, s>>>(p->kf, p->d, p->kf_tc, (int)p->H);
   return cuda_status(cudaGetLastError(), "tc permute kf");
 }
 
@@ -777,8 +807,7 @@ int tc_fwd(fb_plan* p, const void* u, void* y, int64_t B, cudaStream_t s) {
     auto k = tc_fwd_kernel<T>;
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM_BYTES);
     k<<<dim3((unsigned)p->H, (unsigned)chunks), kThreads, SMEM_BYTES, s>>>(
-        map, (const T*)u, (T*)y, p->kf_tc, (const uint4*)p->tc_mats, p->d, p->tw2, (int)B,
-        (int)p->H, ppc);
+        map, (T*)y, p->kf_tc, (const uint4*)p->tc_mats, p->tw2, (int)B, (int)p->H, ppc);
     return cuda_status(cudaGetLastError(), "tc_fwd");
   };
   return p->dtype == FB_BF16 ? go(__nv_bfloat16{}) : go(__half{});
@@ -817,13 +846,17 @@ int tc_bwd(fb_plan* p, const void* dy, const void* u, void* du, float* dK, float
     auto k = tc_bwd_kernel<T>;
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM_BYTES);
     k<<<dim3((unsigned)p->H, (unsigned)chunks), kThreads, SMEM_BYTES, s>>>(
-        dmap, umap, (const T*)dy, (const T*)u, (T*)du, p->kf_tc, (const uint4*)p->tc_mats, p->d,
-        p->tw2, spart, ddpart, (int)B, (int)p->H, ppc);
+        dmap, umap, (T*)du, p->kf_tc, (const uint4*)p->tc_mats, p->tw2, spart, (int)B, (int)p->H,
+        ppc);
     return cuda_status(cudaGetLastError(), "tc_bwd");
   };
-  int rc = p->dtype == FB_BF16 ? go(__nv_bfloat16{}) : go(__half{});
+  int rc = cuda_status(cudaMemsetAsync(ddpart, 0, sizeof(float) * p->H * chunks, s), "memset");
+  if (!rc) rc = p->dtype == FB_BF16 ? go(__nv_bfloat16{}) : go(__half{});
   if (rc) return rc;
   rc = sp_finalize(p, spart, ddpart, chunks, dkbar, dD, s);
+  if (rc) return rc;
+  dd_from_dkbar_kernel<<<(unsigned)((p->H + 127) / 128), 128, 0, s>>>(dkbar, dD, (int)p->H, p->N);
+  rc = cuda_status(cudaGetLastError(), "dd_from_dkbar");
   if (rc) return rc;
   return regularizer_backward_dev(p, dkbar, dK, s);
 }
