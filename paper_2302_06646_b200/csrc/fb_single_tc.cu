@@ -41,20 +41,20 @@ constexpr uint32_t kN = 8192;
 constexpr uint32_t kThreads = 512;
 
 // shared memory map (bytes, 1024-aligned where swizzled operands live)
-constexpr uint32_t SIN = 0;                   // inputs: fwd [2][16 KB] u pairs; bwd [2][dy,u][16 KB]
+constexpr uint32_t SIN = 0;                   // inputs: fwd [slot][16 KB] u pairs; bwd [2][dy,u][16 KB]
 constexpr uint32_t SIN_BYTES = 4 * 16384;
-constexpr uint32_t SOP = SIN + SIN_BYTES;     // 32 KB: B / C / C' / B' / A' operand (one live at a time)
-constexpr uint32_t SMAT = SOP + 32768;        // 22 KB DFT blocks
+constexpr uint32_t SOP = SIN + SIN_BYTES;     // [slot][32 KB]: B / C / C' / B' / A' operand (one live at a time)
+constexpr uint32_t SMAT = SOP + 2 * 32768;    // 22 KB DFT blocks
 constexpr uint32_t MAT_FA = 0, MAT_FB = 1024, MAT_FC = 3072, MAT_IC = 11264, MAT_IB = 19456,
                    MAT_IA = 21504, MAT_BYTES = 22528;
 constexpr uint32_t SKF = SMAT + MAT_BYTES;    // 64 KB k_f' = (K_hat + D)/n, [f3 32][m_C 256] float2
 constexpr uint32_t STAB = SKF + 65536;        // two-level twiddle table (192 float2)
 constexpr uint32_t SMEM_BYTES = STAB + 1536 + 1024;  // + alignment slack
 
-// TMEM columns (512 allocated): R1 working region of every stage (each MMA
-// starts after the previous epilogue drained it), R3 holds F(dy) while F(u)
-// runs (backward), R4 the resident dK spectrum accumulator S.
-constexpr uint32_t R1 = 0, R3 = 256, R4 = 384;
+// TMEM (512 columns allocated): each slot's stages share one 128-column
+// working region (an MMA starts only after the previous epilogue drained
+// it); the backward additionally holds F(dy) at 256 and the resident dK
+// spectrum accumulator S at 384.
 
 // element offsets of the MN-major operands
 __device__ __forceinline__ uint32_t sw128(uint32_t lin) { return lin ^ ((lin >> 3) & 0x70u); }
@@ -203,9 +203,13 @@ __device__ __forceinline__ void load_pair(unsigned char* dst, const CUtensorMap*
 }
 
 // --------------------------------------------------------------------------
-// Per-CTA state and the stage sequence shared by the forward and backward
-// kernels.  Thread (warp w, lane): slab s = w & 3 (TMEM lanes 32s..32s+31),
-// group g = w >> 2.
+// Per-slot state and the stage sequence shared by the forward and backward
+// kernels.  The CTA's 16 warps form NSLOT independent slots (8 or 16 warps);
+// each slot runs its own channel pairs through the six stages with its own
+// operand buffer, TMEM region, barriers and named CTA barrier, so one slot's
+// epilogues overlap the other slot's tensor-core work and latencies.
+// Within a slot, warp w has TMEM lane slab s = w & 3; row tiles are
+// tile = gl + (WS / 4) * i for the thread's items i < NSLOT.
 // --------------------------------------------------------------------------
 // Thread coordinates re-read through volatile asm in every epilogue: they
 // are loop invariant, and letting the compiler hoist the ~100 derived smem
@@ -216,14 +220,23 @@ __device__ __forceinline__ uint32_t tid_v() {
   return t;
 }
 
+template <int NSLOT>
+struct Slot {
+  static constexpr uint32_t TS = kThreads / NSLOT;  // threads per slot
+  static constexpr uint32_t WS = TS / 32;           // warps per slot
+  static constexpr uint32_t GL = WS / 4;            // lane-slab groups per slot
+};
+
 struct Ctx {
   unsigned char* sm;
   uint32_t smb;    // shared address of sm
-  uint32_t tmem;   // TMEM base
+  uint32_t tmem;   // TMEM base of this slot's region
+  uint32_t sop;    // smem offset of this slot's operand buffer
   uint64_t* mma_bar;
   uint32_t mma_phase;
   const float2* tab;
-  uint32_t g, s, lane;
+  uint32_t slot;
+  bool leader;     // issues this slot's MMAs
 };
 
 __device__ __forceinline__ void mma_wait(Ctx& c) {
@@ -232,12 +245,22 @@ __device__ __forceinline__ void mma_wait(Ctx& c) {
   tc::fence_after();
 }
 
-// all threads: make generic smem writes + TMEM reads visible, then one
-// thread issues the stage's MMAs and commits them to the barrier.
+template <int NSLOT>
+__device__ __forceinline__ void slot_sync(const Ctx& c) {
+  if constexpr (NSLOT == 1) {
+    __syncthreads();
+  } else {
+    asm volatile("bar.sync %0, %1;" ::"r"(1 + c.slot), "n"(Slot<NSLOT>::TS) : "memory");
+  }
+}
+
+// make this slot's generic smem writes + TMEM reads visible to the
+// tensor-core (async) proxy before its leader issues the next MMAs
+template <int NSLOT>
 __device__ __forceinline__ void publish(const Ctx& c) {
   ptx::fence_proxy_async_smem();
   tc::fence_before();
-  __syncthreads();
+  slot_sync<NSLOT>(c);
   tc::fence_after();
 }
 
@@ -248,38 +271,40 @@ __device__ __forceinline__ void mma_A(const Ctx& c, uint32_t sa_off) {
   const uint64_t bd = tc::smem_desc(c.smb + SMAT + MAT_FA, 256, tc::kSw32);
   for (uint32_t t = 0; t < 4; ++t) {
     const uint64_t ad = tc::smem_desc(c.smb + sa_off + t * 4096, 1024, tc::kSw128, 2048);
-    tc::mma_bf16(c.tmem + R1 + 32 * t, ad, bd, id, 0);
+    tc::mma_bf16(c.tmem + 32 * t, ad, bd, id, 0);
   }
 }
-// K = 32, MN-major operand in SOP ([kg][mb][8][64]: LBO 1024, SBO 8192)
+// K = 32, MN-major operand ([kg][mb][8][64]: LBO 1024, SBO 8192)
 template <typename T>
 __device__ __forceinline__ void mma_mn32(const Ctx& c, uint32_t mat, uint32_t N, uint32_t mat_sbo,
                                          int mat_swz) {
   const uint32_t id = idesc<T>(128, N, true);
   for (uint32_t t = 0; t < 4; ++t)
     for (uint32_t ks = 0; ks < 2; ++ks) {
-      const uint64_t ad = tc::smem_desc(c.smb + SOP + t * 2048 + ks * 2 * 8192, 8192, tc::kSw128, 1024);
+      const uint64_t ad = tc::smem_desc(c.smb + c.sop + t * 2048 + ks * 2 * 8192, 8192, tc::kSw128, 1024);
       const uint64_t bd = tc::smem_desc(c.smb + SMAT + mat + ks * 32, mat_sbo, mat_swz);
-      tc::mma_bf16(c.tmem + R1 + N * t, ad, bd, id, ks);
+      tc::mma_bf16(c.tmem + N * t, ad, bd, id, ks);
     }
 }
-// stage C / C': 2 M-tiles x (N 64, K 64), A K-major SW128 (256 x 128 B) in SOP
+// stage C / C': 2 M-tiles x (N 64, K 64), A K-major SW128 (256 x 128 B)
 template <typename T>
 __device__ __forceinline__ void mma_C(const Ctx& c, uint32_t mat, uint32_t dcol) {
   const uint32_t id = idesc<T>(128, 64, false);
   for (uint32_t t = 0; t < 2; ++t)
     for (uint32_t ks = 0; ks < 4; ++ks) {
-      const uint64_t ad = tc::smem_desc(c.smb + SOP + t * 16384 + ks * 32, 1024, tc::kSw128);
+      const uint64_t ad = tc::smem_desc(c.smb + c.sop + t * 16384 + ks * 32, 1024, tc::kSw128);
       const uint64_t bd = tc::smem_desc(c.smb + SMAT + mat + ks * 32, 1024, tc::kSw128);
       tc::mma_bf16(c.tmem + dcol + 64 * t, ad, bd, id, ks);
     }
 }
 
-__device__ __forceinline__ void coords(uint32_t& g, uint32_t& s, uint32_t& lane) {
-  const uint32_t t = tid_v();
+// thread coordinates within the slot: lane, slab s, group gl
+template <int NSLOT>
+__device__ __forceinline__ void coords(uint32_t& gl, uint32_t& s, uint32_t& lane) {
+  const uint32_t t = tid_v() % Slot<NSLOT>::TS;
   lane = t & 31;
   s = (t >> 5) & 3;
-  g = t >> 7;
+  gl = t >> 7;
 }
 __device__ __forceinline__ uint32_t lane_addr(const Ctx& c, uint32_t col) {
   return c.tmem + ((32u * ((tid_v() >> 5) & 3)) << 16) + col;
@@ -315,15 +340,15 @@ __device__ __forceinline__ void twiddle16(float (&v)[32], const float2* tab, uin
   cmul_at(v, 15, cmul(w7, w8));
 }
 
-template <typename T>
+template <typename T, int NSLOT>
 __device__ __forceinline__ void issue(Ctx& c, int stage, uint32_t arg) {
-  publish(c);
-  if (threadIdx.x == 0) {
+  publish<NSLOT>(c);
+  if (c.leader) {
     switch (stage) {
       case 0: mma_A<T>(c, arg); break;
       case 1: mma_mn32<T>(c, MAT_FB, 32, 512, tc::kSw64); break;
       case 2: mma_C<T>(c, MAT_FC, arg); break;
-      case 3: mma_C<T>(c, MAT_IC, R1); break;
+      case 3: mma_C<T>(c, MAT_IC, 0); break;
       case 4: mma_mn32<T>(c, MAT_IB, 32, 512, tc::kSw64); break;
       default: mma_mn32<T>(c, MAT_IA, 16, 512, tc::kSw64); break;
     }
@@ -332,73 +357,80 @@ __device__ __forceinline__ void issue(Ctx& c, int stage, uint32_t arg) {
   mma_wait(c);
 }
 
-// Forward transform of the pair staged at sa_off (TMA barrier in_bar):
-// X[f] ends in TMEM cols dstC + 64 T (rows m_C; cols [re f3 0..15 | im 0..15
-// | re 16..31 | im 16..31]).
-template <typename T>
+// Forward transform of the pair staged at sa_off (TMA barrier in_bar): X[f]
+// ends in the slot's TMEM cols dstC + 64 T (rows m_C; cols [re f3 0..15 |
+// im 0..15 | re 16..31 | im 16..31]).
+template <typename T, int NSLOT>
 __device__ __forceinline__ void forward_fft(Ctx& c, uint32_t sa_off, uint64_t* in_bar,
                                             uint32_t in_phase, uint32_t dstC) {
+  using SL = Slot<NSLOT>;
   ptx::mbar_wait(in_bar, in_phase);
-  issue<T>(c, 0, sa_off);
+  issue<T, NSLOT>(c, 0, sa_off);
   // ---- A -> B: twiddle w^(f1 m_A); B operand rows m_B = 32 f1 + t3, k = t2
-  {
-    uint32_t g, sl, lane;
-    coords(g, sl, lane);
-    const uint32_t m = 128 * g + 32 * sl + lane;  // = 32 t2 + t3
-    const uint32_t t2 = m >> 5, t3 = lane;
+#pragma unroll 1
+  for (int i = 0; i < NSLOT; ++i) {
+    uint32_t gl, sl, lane;
+    coords<NSLOT>(gl, sl, lane);
+    const uint32_t tile = gl + SL::GL * i;
+    const uint32_t m = 128 * tile + 32 * sl + lane;  // = 32 t2 + t3
     float v[32];
-    tc::ld32(lane_addr(c, R1 + 32 * g), v);
+    tc::ld32(lane_addr(c, 32 * tile), v);
     tc::ld_wait();
     twiddle16<-1>(v, c.tab, m);
-    scatter_mn<T>(c.sm + SOP, t3, t2, v);
+    scatter_mn<T>(c.sm + c.sop, lane, m >> 5, v);
   }
-  issue<T>(c, 1, 0);
+  issue<T, NSLOT>(c, 1, 0);
   // ---- B -> C: twiddle w_512^(f2 t3); C operand rows m_C = 16 f1 + f2, k = t3
-  {
-    uint32_t g, sl, lane;
-    coords(g, sl, lane);
-    const uint32_t mB = 128 * g + 32 * sl + lane;  // = 32 f1 + t3
-    const uint32_t f1 = mB >> 5, t3 = lane;
+#pragma unroll 1
+  for (int i = 0; i < NSLOT; ++i) {
+    uint32_t gl, sl, lane;
+    coords<NSLOT>(gl, sl, lane);
+    const uint32_t tile = gl + SL::GL * i;
+    const uint32_t mB = 128 * tile + 32 * sl + lane;  // = 32 f1 + t3
     float v[32];
-    tc::ld32(lane_addr(c, R1 + 32 * g), v);
+    tc::ld32(lane_addr(c, 32 * tile), v);
     tc::ld_wait();
-    twiddle16<-1>(v, c.tab, 16 * t3);
-    scatter_c<T>(c.sm + SOP, f1, t3, v);
+    twiddle16<-1>(v, c.tab, 16 * lane);
+    scatter_c<T>(c.sm + c.sop, mB >> 5, lane, v);
   }
-  issue<T>(c, 2, dstC);
+  issue<T, NSLOT>(c, 2, dstC);
 }
 
-// Spectrum row owned by this thread at the C exit: m_C and half h.
-__device__ __forceinline__ void c_row(const Ctx&, uint32_t& mC, uint32_t& h) {
-  uint32_t g, sl, lane;
-  coords(g, sl, lane);
-  mC = 128 * (g & 1) + 32 * sl + lane;
-  h = g >> 1;
+// C-exit item i of this thread: spectrum row m_C and half h.
+template <int NSLOT>
+__device__ __forceinline__ void c_item(int i, uint32_t& mC, uint32_t& h) {
+  uint32_t gl, sl, lane;
+  coords<NSLOT>(gl, sl, lane);
+  const uint32_t combo = gl + Slot<NSLOT>::GL * i;  // (T, h) = (combo & 1, combo >> 1)
+  mC = 128 * (combo & 1) + 32 * sl + lane;
+  h = combo >> 1;
 }
 
 // Write the row half (re v[0..15], im v[16..31] at f3 = 16h + j) as the C'
 // operand (K-major SW128, k = [re f3 | im f3]).
 template <typename T>
 __device__ __forceinline__ void write_cprime(const Ctx& c, uint32_t mC, uint32_t h, const float (&v)[32]) {
-  unsigned char* op = c.sm + SOP;
+  unsigned char* op = c.sm + c.sop;
   st8<T>(op + tc::kmajor_off<tc::kSw128>(mC, 16 * h), v);
   st8<T>(op + tc::kmajor_off<tc::kSw128>(mC, 16 * h + 8), v + 8);
   st8<T>(op + tc::kmajor_off<tc::kSw128>(mC, 32 + 16 * h), v + 16);
   st8<T>(op + tc::kmajor_off<tc::kSw128>(mC, 32 + 16 * h + 8), v + 24);
 }
 
-// Inverse transform from the C' operand; leaves z[t] (t1 < 8) in TMEM R1
-// cols 16 T + [re t1 0..7 | im t1 0..7] of row block T.
-template <typename T>
+// Inverse transform from the C' operand; leaves z[t] (t1 < 8) in the slot's
+// TMEM cols 16 T + [re t1 0..7 | im t1 0..7] of row block T.
+template <typename T, int NSLOT>
 __device__ __forceinline__ void inverse_fft(Ctx& c) {
-  issue<T>(c, 3, 0);
+  using SL = Slot<NSLOT>;
+  issue<T, NSLOT>(c, 3, 0);
   // ---- C' -> B': twiddle w_512^(-f2 t3); B' operand rows m_B = 32 f1 + t3, k = f2
-  {
+#pragma unroll 1
+  for (int i = 0; i < NSLOT; ++i) {
     uint32_t mC, h;
-    c_row(c, mC, h);
+    c_item<NSLOT>(i, mC, h);
     const uint32_t f1 = mC >> 4, f2 = mC & 15;
     float v[32];
-    tc::ld32(lane_addr(c, R1 + 64 * (mC >> 7) + 32 * h), v);
+    tc::ld32(lane_addr(c, 64 * (mC >> 7) + 32 * h), v);
     tc::ld_wait();
     twiddle16<+1>(v, c.tab, 16 * f2);
     if (h) {
@@ -406,30 +438,31 @@ __device__ __forceinline__ void inverse_fft(Ctx& c) {
 #pragma unroll
       for (int j = 0; j < 16; ++j) cmul_at(v, j, w);
     }
-    unsigned char* op = c.sm + SOP;
+    unsigned char* op = c.sm + c.sop;
     const uint32_t m0 = 32 * f1 + 16 * h;
     st8<T>(op + off_mn(m0, f2), v);
     st8<T>(op + off_mn(m0 + 8, f2), v + 8);
     st8<T>(op + off_mn(m0, 16 + f2), v + 16);
     st8<T>(op + off_mn(m0 + 8, 16 + f2), v + 24);
   }
-  issue<T>(c, 4, 0);
+  issue<T, NSLOT>(c, 4, 0);
   // ---- B' -> A': twiddle w^(-f1 (32 t2 + t3)); A' operand rows m_A = 32 t2 + t3, k = f1
-  {
-    uint32_t g, sl, lane;
-    coords(g, sl, lane);
-    const uint32_t mB = 128 * g + 32 * sl + lane;  // = 32 f1 + t3
-    const uint32_t f1 = mB >> 5, t3 = lane;
+#pragma unroll 1
+  for (int i = 0; i < NSLOT; ++i) {
+    uint32_t gl, sl, lane;
+    coords<NSLOT>(gl, sl, lane);
+    const uint32_t tile = gl + SL::GL * i;
+    const uint32_t f1 = (128 * tile + 32 * sl + lane) >> 5;  // m_B = 32 f1 + t3
     float v[32];
-    tc::ld32(lane_addr(c, R1 + 32 * g), v);
+    tc::ld32(lane_addr(c, 32 * tile), v);
     tc::ld_wait();
     twiddle16<+1>(v, c.tab, 32 * f1);
-    const float2 w = tw2<+1>(c.tab, f1 * t3);
+    const float2 w = tw2<+1>(c.tab, f1 * lane);
 #pragma unroll
     for (int t2 = 0; t2 < 16; ++t2) cmul_at(v, t2, w);
-    scatter_mn<T>(c.sm + SOP, t3, f1, v);
+    scatter_mn<T>(c.sm + c.sop, lane, f1, v);
   }
-  issue<T>(c, 5, 0);
+  issue<T, NSLOT>(c, 5, 0);
 }
 
 __device__ __forceinline__ void setup(Ctx& c, unsigned char* sm, uint32_t* tmem_slot, uint64_t* bars,
@@ -438,11 +471,6 @@ __device__ __forceinline__ void setup(Ctx& c, unsigned char* sm, uint32_t* tmem_
                                       const float2* __restrict__ tab_g) {
   c.sm = sm;
   c.smb = ptx::smem_u32(sm);
-  c.lane = threadIdx.x & 31;
-  c.s = (threadIdx.x >> 5) & 3;
-  c.g = threadIdx.x >> 7;
-  c.mma_bar = &bars[0];
-  c.mma_phase = 0;
   c.tab = reinterpret_cast<const float2*>(sm + STAB);
   if (threadIdx.x < 32) tc::alloc<512>(tmem_slot);
   if (threadIdx.x == 0) {
@@ -460,52 +488,60 @@ __device__ __forceinline__ void setup(Ctx& c, unsigned char* sm, uint32_t* tmem_
   tc::fence_before();
   __syncthreads();
   tc::fence_after();
-  c.tmem = *tmem_slot;
 }
 
-__device__ __forceinline__ void teardown(const Ctx& c) {
+__device__ __forceinline__ void teardown(uint32_t tmem_base) {
   tc::fence_before();
   __syncthreads();
-  if (threadIdx.x < 32) tc::dealloc<512>(c.tmem);
+  if (threadIdx.x < 32) tc::dealloc<512>(tmem_base);
 }
 
 // A' exit: rows m_A, z[512 t1 + m_A] for t1 < 8 (re -> channel b0, im -> b1).
-template <typename T>
+template <typename T, int NSLOT>
 __device__ __forceinline__ void store_rows(const Ctx& c, T* __restrict__ out, int b0, int B, int H,
                                            int h) {
-  uint32_t g, sl, lane;
-  coords(g, sl, lane);
-  const uint32_t mA = 128 * g + 32 * sl + lane;
-  float v[16];
-  ld16(lane_addr(c, R1 + 16 * g), v);
-  tc::ld_wait();
-  T* o0 = out + ((size_t)b0 * H + h) * 4096 + mA;
+#pragma unroll 1
+  for (int i = 0; i < NSLOT; ++i) {
+    uint32_t gl, sl, lane;
+    coords<NSLOT>(gl, sl, lane);
+    const uint32_t tile = gl + Slot<NSLOT>::GL * i;
+    const uint32_t mA = 128 * tile + 32 * sl + lane;
+    float v[16];
+    ld16(lane_addr(c, 16 * tile), v);
+    tc::ld_wait();
+    T* o0 = out + ((size_t)b0 * H + h) * 4096 + mA;
 #pragma unroll
-  for (int t1 = 0; t1 < 8; ++t1) o0[512 * t1] = cvt<T>(v[t1]);
-  if (b0 + 1 < B) {
-    T* o1 = out + ((size_t)(b0 + 1) * H + h) * 4096 + mA;
+    for (int t1 = 0; t1 < 8; ++t1) o0[512 * t1] = cvt<T>(v[t1]);
+    if (b0 + 1 < B) {
+      T* o1 = out + ((size_t)(b0 + 1) * H + h) * 4096 + mA;
 #pragma unroll
-    for (int t1 = 0; t1 < 8; ++t1) o1[512 * t1] = cvt<T>(v[8 + t1]);
+      for (int t1 = 0; t1 < 8; ++t1) o1[512 * t1] = cvt<T>(v[8 + t1]);
+    }
   }
 }
 
-__device__ __forceinline__ void pair_end() {
+template <int NSLOT>
+__device__ __forceinline__ void pair_end(const Ctx& c) {
   tc::fence_before();
-  __syncthreads();
+  slot_sync<NSLOT>(c);
   tc::fence_after();
 }
 
 // ------------------------------------------------------------------ forward
 // y = F^-1(F(u) * (K_hat + D)/n): the skip term D u is folded into the
 // spectrum (a D-weighted delta kernel), so the epilogue only streams y out.
+// Two slots of 8 warps each process alternate channel pairs.
+constexpr int kFwdSlots = 2;
+
 template <typename T>
 __global__ void __launch_bounds__(kThreads, 1)
     tc_fwd_kernel(const __grid_constant__ CUtensorMap umap, T* __restrict__ y,
                   const float2* __restrict__ kfp, const uint4* __restrict__ mats,
                   const float2* __restrict__ tab_g, int B, int H, int ppc) {
+  constexpr int NS = kFwdSlots;
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   __shared__ uint32_t tmem_slot;
-  __shared__ __align__(8) uint64_t bars[3];  // 0: mma, 1/2: input buffers
+  __shared__ __align__(8) uint64_t bars[2 * NS];  // [slot]: mma, input
   unsigned char* sm = reinterpret_cast<unsigned char*>(
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   const int h = blockIdx.x;
@@ -513,33 +549,42 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int p0 = blockIdx.y * ppc, p1 = min(npairs, p0 + ppc);
   if (p0 >= p1) return;
   Ctx c;
-  setup(c, sm, &tmem_slot, bars, 3, mats, kfp + (size_t)h * kN, tab_g);
+  setup(c, sm, &tmem_slot, bars, 2 * NS, mats, kfp + (size_t)h * kN, tab_g);
+  const uint32_t slot = threadIdx.x / Slot<NS>::TS;
+  c.slot = slot;
+  c.leader = (threadIdx.x % Slot<NS>::TS) == 0;
+  c.tmem = tmem_slot + 256 * slot;
+  c.sop = SOP + 32768 * slot;
+  c.mma_bar = &bars[2 * slot];
+  c.mma_phase = 0;
+  uint64_t* in_bar = &bars[2 * slot + 1];
+  const uint32_t sin = SIN + 16384 * slot;
   const float2* kfs = reinterpret_cast<const float2*>(sm + SKF);
-  if (threadIdx.x == 0) load_pair(sm + SIN, &umap, h, 2 * p0, &bars[1]);
-  for (int pr = p0, it = 0; pr < p1; ++pr, ++it) {
-    const int buf = it & 1;
-    // prefetch the next pair into the other buffer (its last reader, stage
-    // A of the previous pair, has completed)
-    if (threadIdx.x == 0 && pr + 1 < p1)
-      load_pair(sm + SIN + (buf ^ 1) * 16384, &umap, h, 2 * (pr + 1), &bars[1 + (buf ^ 1)]);
-    forward_fft<T>(c, SIN + buf * 16384, &bars[1 + buf], (it >> 1) & 1, R1);
+  if (c.leader && p0 + (int)slot < p1) load_pair(sm + sin, &umap, h, 2 * (p0 + slot), in_bar);
+  uint32_t in_phase = 0;
+  for (int pr = p0 + slot; pr < p1; pr += NS) {
+    forward_fft<T, NS>(c, sin, in_bar, in_phase, 0);
+    in_phase ^= 1;
+    // stage A consumed the input: prefetch this slot's next pair
+    if (c.leader && pr + NS < p1) load_pair(sm + sin, &umap, h, 2 * (pr + NS), in_bar);
     // ---- C exit: Z = X * k_f'  -> C' operand
-    {
+#pragma unroll 1
+    for (int i = 0; i < NS; ++i) {
       uint32_t mC, hh;
-      c_row(c, mC, hh);
+      c_item<NS>(i, mC, hh);
       float v[32];
-      tc::ld32(lane_addr(c, R1 + 64 * (mC >> 7) + 32 * hh), v);
+      tc::ld32(lane_addr(c, 64 * (mC >> 7) + 32 * hh), v);
       tc::ld_wait();
       const float2* kr = kfs + (16 * hh) * 256 + mC;
 #pragma unroll
       for (int j = 0; j < 16; ++j) cmul_at(v, j, kr[j * 256]);
       write_cprime<T>(c, mC, hh, v);
     }
-    inverse_fft<T>(c);
-    store_rows<T>(c, y, 2 * pr, B, H, h);
-    pair_end();
+    inverse_fft<T, NS>(c);
+    store_rows<T, NS>(c, y, 2 * pr, B, H, h);
+    pair_end<NS>(c);
   }
-  teardown(c);
+  teardown(tmem_slot);
 }
 
 // ------------------------------------------------------------------ backward
@@ -553,6 +598,8 @@ __global__ void __launch_bounds__(kThreads, 1)
                   T* __restrict__ du, const float2* __restrict__ kfp, const uint4* __restrict__ mats,
                   const float2* __restrict__ tab_g, float2* __restrict__ spart, int B, int H,
                   int ppc) {
+  constexpr int NS = 1;
+  constexpr uint32_t R3 = 256, R4 = 384;
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   __shared__ uint32_t tmem_slot;
   __shared__ __align__(8) uint64_t bars[5];  // 0: mma, 1/2: dy buffers, 3/4: u buffers
@@ -563,9 +610,15 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int p0 = chunk * ppc, p1 = min(npairs, p0 + ppc);
   Ctx c;
   setup(c, sm, &tmem_slot, bars, 5, mats, kfp + (size_t)h * kN, tab_g);
+  c.slot = 0;
+  c.leader = threadIdx.x == 0;
+  c.tmem = tmem_slot;
+  c.sop = SOP;
+  c.mma_bar = &bars[0];
+  c.mma_phase = 0;
   const float2* kfs = reinterpret_cast<const float2*>(sm + SKF);
   uint32_t mC, hh;
-  c_row(c, mC, hh);
+  c_item<NS>(0, mC, hh);
   const uint32_t scol = R4 + 64 * (mC >> 7) + 32 * hh;
   {
     float z[32];
@@ -586,13 +639,13 @@ __global__ void __launch_bounds__(kThreads, 1)
       load_pair(sm + SIN + (buf ^ 1) * 32768, &dymap, h, 2 * (pr + 1), &bars[1 + (buf ^ 1)]);
       load_pair(sm + SIN + (buf ^ 1) * 32768 + 16384, &umap, h, 2 * (pr + 1), &bars[3 + (buf ^ 1)]);
     }
-    forward_fft<T>(c, SIN + buf * 32768, &bars[1 + buf], ph, R3);
-    forward_fft<T>(c, SIN + buf * 32768 + 16384, &bars[3 + buf], ph, R1);
+    forward_fft<T, NS>(c, SIN + buf * 32768, &bars[1 + buf], ph, R3);
+    forward_fft<T, NS>(c, SIN + buf * 32768 + 16384, &bars[3 + buf], ph, 0);
     {
       // in two quarters of 8 frequencies to keep U, DY, S register-light
-      const uint32_t cu = R1 + 64 * (mC >> 7) + 32 * hh, cg = R3 + 64 * (mC >> 7) + 32 * hh;
+      const uint32_t cu = 64 * (mC >> 7) + 32 * hh, cg = R3 + 64 * (mC >> 7) + 32 * hh;
       const float2* kr = kfs + (16 * hh) * 256 + mC;
-      unsigned char* op = c.sm + SOP;
+      unsigned char* op = c.sm + c.sop;
 #pragma unroll
       for (int q = 0; q < 2; ++q) {
         float ur[8], ui[8], gr[8], gi[8], sr[8], si[8];
@@ -620,9 +673,9 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       st_wait();
     }
-    inverse_fft<T>(c);
-    store_rows<T>(c, du, 2 * pr, B, H, h);
-    pair_end();
+    inverse_fft<T, NS>(c);
+    store_rows<T, NS>(c, du, 2 * pr, B, H, h);
+    pair_end<NS>(c);
   }
   {
     float S[32];
@@ -633,7 +686,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
     for (int j = 0; j < 16; ++j) sp[f1 + 16 * f2 + 256 * (16 * hh + j)] = make_float2(S[j], S[16 + j]);
   }
-  teardown(c);
+  teardown(tmem_slot);
 }
 
 // k_f (natural order, / n) -> [h][f3][m_C], m_C = 16 f1 + f2, f = f1 + 16 f2 + 256 f3
