@@ -63,6 +63,24 @@ static int upload_twiddles2(float2** dst, int64_t n) {
                      "cudaMemcpy(twiddles2)");
 }
 
+// [w^t (t < 4096) | w^(4096 i) (i < n/4096)], w = exp(-2 pi i / n)
+static int upload_twiddles_big(float2** dst, int64_t n) {
+  const int64_t hi = std::max<int64_t>(1, n / 4096);
+  std::vector<float2> h((size_t)(4096 + hi));
+  for (int64_t t = 0; t < 4096; ++t) {
+    const double a = -2.0 * M_PI * (double)t / (double)n;
+    h[(size_t)t] = make_float2((float)std::cos(a), (float)std::sin(a));
+  }
+  for (int64_t i = 0; i < hi; ++i) {
+    const double a = -2.0 * M_PI * (double)(4096 * i) / (double)n;
+    h[(size_t)(4096 + i)] = make_float2((float)std::cos(a), (float)std::sin(a));
+  }
+  int rc = cuda_status(cudaMalloc(dst, sizeof(float2) * h.size()), "cudaMalloc(twiddles big)");
+  if (rc) return rc;
+  return cuda_status(cudaMemcpy(*dst, h.data(), sizeof(float2) * h.size(), cudaMemcpyHostToDevice),
+                     "cudaMemcpy(twiddles big)");
+}
+
 constexpr int64_t kSinglePassMax = 8192;   // fp32 complex transform in smem
 constexpr int64_t kThreePassRow = 8192;    // l: row length of pass 2
 constexpr int64_t kMinTransform = 256;
@@ -109,12 +127,12 @@ int fb_plan_create(fb_plan** out, int64_t N, int64_t H, int mode, int dtype, int
     return fail(FB_ERR_PLAN, "fb_plan_create: single-pass engine supports transforms up to " +
                                  std::to_string(kSinglePassMax) + " points; use three-pass");
   }
-  if (engine == FB_ENGINE_THREE && (n < 2 * kThreePassRow || n > 16 * kThreePassRow)) {
+  if (engine == FB_ENGINE_THREE && (n < 2 * kThreePassRow || n > 1024 * kThreePassRow)) {
     delete p;
     return fail(FB_ERR_PLAN, "fb_plan_create: three-pass engine needs a transform of " +
                                  std::to_string(2 * kThreePassRow) + ".." +
-                                 std::to_string(16 * kThreePassRow) + " points (l = " +
-                                 std::to_string(kThreePassRow) + ", m = 2..16)");
+                                 std::to_string(1024 * kThreePassRow) + " points (l = " +
+                                 std::to_string(kThreePassRow) + ", m = 2..1024)");
   }
   p->engine = engine;
   if (engine == FB_ENGINE_THREE) {
@@ -126,9 +144,11 @@ int fb_plan_create(fb_plan** out, int64_t N, int64_t H, int mode, int dtype, int
   }
   cudaDeviceGetAttribute(&p->num_sms, cudaDevAttrMultiProcessorCount, device);
   p->use_tc = engine == FB_ENGINE_SINGLE && !simt && tc_eligible(p);
-  rc = upload_twiddles(&p->tw_n, n);
-  if (!rc) rc = upload_twiddles2(&p->tw2, n);
+  rc = upload_twiddles2(&p->tw2, n);
+  if (!rc && engine == FB_ENGINE_THREE && p->m <= 16) rc = upload_twiddles(&p->tw_n, n);
   if (!rc && engine == FB_ENGINE_THREE) rc = upload_twiddles2(&p->tw_l, p->l);
+  if (!rc && engine == FB_ENGINE_THREE && p->m > 16) rc = upload_twiddles(&p->tw_m, p->m);
+  if (!rc && engine == FB_ENGINE_THREE && p->m > 16) rc = upload_twiddles_big(&p->tw_big, n);
   if (!rc) rc = cuda_status(cudaMalloc(&p->kf, sizeof(float2) * H * n), "cudaMalloc(kf)");
   if (!rc) rc = cuda_status(cudaMalloc(&p->kbar, sizeof(float) * H * N), "cudaMalloc(kbar)");
   if (!rc) rc = cuda_status(cudaMalloc(&p->d, sizeof(float) * H), "cudaMalloc(D)");
@@ -146,6 +166,8 @@ int fb_plan_destroy(fb_plan* p) {
   cudaFree(p->tw_n);
   cudaFree(p->tw2);
   cudaFree(p->tw_l);
+  cudaFree(p->tw_m);
+  cudaFree(p->tw_big);
   cudaFree(p->kf);
   cudaFree(p->kbar);
   cudaFree(p->keep);

@@ -16,6 +16,8 @@ struct fb_plan {
   float2* tw_n = nullptr;  // exp(-2 pi i t / n), t < n
   float2* tw2 = nullptr;   // two-level table for n: [w^i, i<64 | w^(64 i), i<n/64]
   float2* tw_l = nullptr;  // two-level table for l (three-pass pass 2)
+  float2* tw_m = nullptr;  // full table exp(-2 pi i t / m)      (three-pass, m > 16)
+  float2* tw_big = nullptr; // [w^t, t < 4096 | w^(4096 i), i < n/4096], w = e^{-2 pi i/n}
   float2* kf = nullptr;    // per-head spectrum / n: single [H][n]; three [H][m][l]
   float* kbar = nullptr;   // [H][N] regularized kernels
   uint8_t* keep = nullptr; // [H][N] dropout keep flags (training only)

@@ -335,6 +335,127 @@ __global__ void tp_dd_reduce_kernel(const float* __restrict__ ddpart, float* __r
   }
 }
 
+// ---------------------------------------------------------------- passes 1/3, m > 16
+// A CTA owns TAU = 8192/m consecutive columns tau and all m rows: the tile
+// (m x TAU complex, fp32) is staged in shared memory with coalesced row
+// segments, the TAU independent m-point DFTs run as batched Stockham passes
+// (element e of column c at s[pad16(e) * TAU + c]), and the w_n^(a tau)
+// twiddle is applied on the way out (pass 1) / in (pass 3) from a two-level
+// table  w_n^t = lo[t & 4095] * hi[t >> 12].
+constexpr uint32_t kBigTile = 8192;  // complex elements per tile
+constexpr uint32_t kBigThreads = kBigTile / 16;
+
+template <int SIGN>
+__device__ __forceinline__ float2 tw_big(const float2* __restrict__ tb, uint32_t t) {
+  const float2 w = cmul(__ldg(tb + (t & 4095u)), __ldg(tb + 4096u + (t >> 12)));
+  return SIGN < 0 ? w : make_float2(w.x, -w.y);
+}
+
+template <typename IO, typename ST, int SMALL, int SRC>
+__global__ void __launch_bounds__(kBigThreads, 1)
+    tp_pass1_big_kernel(const IO* __restrict__ a_in, const IO* __restrict__ b_in,
+                        const float* __restrict__ kbar, CxT<ST>* __restrict__ out_a,
+                        CxT<ST>* __restrict__ out_b, float* __restrict__ ddpart,
+                        const float2* __restrict__ tw_m, const float2* __restrict__ tb, int B,
+                        int H, uint32_t N, int causal, uint32_t m) {
+  extern __shared__ __align__(16) float2 tsm[];
+  __shared__ float red[kBigThreads / 32];
+  const uint32_t TAU = kBigTile / m;
+  const uint32_t plen = padded_len(m) * TAU;
+  float2* sa = tsm;
+  float2* sb = tsm + plen;
+  const uint32_t tau0 = blockIdx.x * TAU;
+  const int h = blockIdx.y, pr = blockIdx.z;
+  const int b0 = 2 * pr, b1 = b0 + 1;
+  const bool has1 = b1 < B;
+  const uint32_t cmax = causal ? m / 2 : m;
+  float dd = 0.f;
+  for (uint32_t i = threadIdx.x; i < kBigTile; i += kBigThreads) {
+    const uint32_t e = i / TAU, c = i % TAU;
+    const uint32_t t = e * kL + tau0 + c;
+    const bool ok = e < cmax && t < N;
+    float2 v = make_float2(0.f, 0.f), w = make_float2(0.f, 0.f);
+    if constexpr (SRC == 2) {
+      v.x = ok ? __ldg(kbar + (size_t)h * N + t) : 0.f;
+    } else {
+      const size_t o0 = ((size_t)b0 * H + h) * N, o1 = ((size_t)b1 * H + h) * N;
+      v.x = ok ? ld(a_in + o0 + t) : 0.f;
+      v.y = (ok && has1) ? ld(a_in + o1 + t) : 0.f;
+      if constexpr (SRC == 1) {
+        w.x = ok ? ld(b_in + o0 + t) : 0.f;
+        w.y = (ok && has1) ? ld(b_in + o1 + t) : 0.f;
+        dd = fmaf(v.x, w.x, fmaf(v.y, w.y, dd));
+        sb[pad16(e) * TAU + c] = w;
+      }
+    }
+    sa[pad16(e) * TAU + c] = v;
+  }
+  __syncthreads();
+  smem_passes<-1, SMALL>(sa, m, TAU, 1, m, tw_m);
+  if constexpr (SRC == 1) smem_passes<-1, SMALL>(sb, m, TAU, 1, m, tw_m);
+  CxT<ST>* oa = out_a + ((size_t)pr * H + h) * (size_t)m * kL;
+  CxT<ST>* ob = SRC == 1 ? out_b + ((size_t)pr * H + h) * (size_t)m * kL : nullptr;
+  for (uint32_t i = threadIdx.x; i < kBigTile; i += kBigThreads) {
+    const uint32_t a = i / TAU, c = i % TAU;
+    const float2 w = tw_big<-1>(tb, a * (tau0 + c));
+    stc<ST>(&oa[(size_t)a * kL + tau0 + c].x, cmul(sa[pad16(a) * TAU + c], w));
+    if constexpr (SRC == 1) stc<ST>(&ob[(size_t)a * kL + tau0 + c].x, cmul(sb[pad16(a) * TAU + c], w));
+  }
+  if constexpr (SRC == 1) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) dd += __shfl_xor_sync(0xffffffffu, dd, o);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = dd;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      float t = 0.f;
+      for (uint32_t w = 0; w < kBigThreads / 32; ++w) t += red[w];
+      ddpart[((size_t)h * gridDim.z + pr) * gridDim.x + blockIdx.x] = t;
+    }
+  }
+}
+
+template <typename ST, typename IO, int SMALL, int MODE>
+__global__ void __launch_bounds__(kBigThreads, 1)
+    tp_pass3_big_kernel(const CxT<ST>* __restrict__ w_in, const IO* __restrict__ skip,
+                        IO* __restrict__ out, const float* __restrict__ D,
+                        float* __restrict__ dkbar, const float2* __restrict__ tw_m,
+                        const float2* __restrict__ tb, int B, int H, uint32_t N, int causal,
+                        float scale, uint32_t m) {
+  extern __shared__ __align__(16) float2 tsm[];
+  const uint32_t TAU = kBigTile / m;
+  const uint32_t tau0 = blockIdx.x * TAU;
+  const int h = blockIdx.y, pr = blockIdx.z;
+  const CxT<ST>* src = w_in + ((size_t)pr * H + h) * (size_t)m * kL;
+  for (uint32_t i = threadIdx.x; i < kBigTile; i += kBigThreads) {
+    const uint32_t a = i / TAU, c = i % TAU;
+    tsm[pad16(a) * TAU + c] = cmul(cx_load(src + (size_t)a * kL + tau0 + c), tw_big<+1>(tb, a * (tau0 + c)));
+  }
+  __syncthreads();
+  smem_passes<+1, SMALL>(tsm, m, TAU, 1, m, tw_m);
+  const uint32_t cmax = causal ? m / 2 : m;
+  if constexpr (MODE == 0) {
+    const int b0 = 2 * pr, b1 = b0 + 1;
+    const bool has1 = b1 < B;
+    const float d = __ldg(D + h);
+    const size_t o0 = ((size_t)b0 * H + h) * N, o1 = ((size_t)b1 * H + h) * N;
+    for (uint32_t i = threadIdx.x; i < cmax * TAU; i += kBigThreads) {
+      const uint32_t cc = i / TAU, c = i % TAU;
+      const uint32_t t = cc * kL + tau0 + c;
+      if (t < N) {
+        const float2 v = tsm[pad16(cc) * TAU + c];
+        st(out + o0 + t, fmaf(d, ld(skip + o0 + t), v.x));
+        if (has1) st(out + o1 + t, fmaf(d, ld(skip + o1 + t), v.y));
+      }
+    }
+  } else {
+    for (uint32_t i = threadIdx.x; i < cmax * TAU; i += kBigThreads) {
+      const uint32_t cc = i / TAU, c = i % TAU;
+      const uint32_t t = cc * kL + tau0 + c;
+      if (t < N) dkbar[(size_t)h * N + t] = tsm[pad16(cc) * TAU + c].x * scale;
+    }
+  }
+}
+
 // ---------------------------------------------------------------- host side
 namespace {
 
@@ -368,6 +489,79 @@ void with_io(int dtype, F&& f) {
   }
 }
 
+int log2u(int64_t v) {
+  int k = 0;
+  while ((int64_t(1) << k) < v) ++k;
+  return k;
+}
+
+template <class F>
+void with_small(int64_t m, F&& f) {
+  switch (log2u(m) % 4) {
+    case 0: f(std::integral_constant<int, 1>{}); break;
+    case 1: f(std::integral_constant<int, 2>{}); break;
+    case 2: f(std::integral_constant<int, 4>{}); break;
+    default: f(std::integral_constant<int, 8>{}); break;
+  }
+}
+
+size_t big_smem(int src) {
+  return (size_t)(src == 1 ? 2 : 1) * padded_len(kBigTile) * sizeof(float2) + 64 * sizeof(float2);
+}
+
+// pass 1: register kernel for m <= 16, tiled smem kernel above
+template <typename IO, typename ST, int SRC>
+uint32_t launch_pass1(const fb_plan* p, const IO* a, const IO* b, CxT<ST>* oa, CxT<ST>* ob,
+                      float* ddpart, int B, int npairs, cudaStream_t s) {
+  const int causal = p->mode == FB_MODE_CAUSAL;
+  if (p->m <= 16) {
+    with_m(p->m, [&](auto mc) {
+      constexpr int M = decltype(mc)::value;
+      tp_pass1_kernel<IO, ST, M, SRC><<<dim3(kL / kColThreads, (unsigned)p->H, (unsigned)npairs),
+                                        kColThreads, 0, s>>>(a, b, p->kbar, oa, ob, ddpart, p->tw_n,
+                                                             B, (int)p->H, (uint32_t)p->N, causal);
+    });
+    return kL / kColThreads;
+  }
+  const uint32_t gx = (uint32_t)(kL / (kBigTile / p->m));
+  with_small(p->m, [&](auto sc) {
+    constexpr int SM = decltype(sc)::value;
+    auto k = tp_pass1_big_kernel<IO, ST, SM, SRC>;
+    const size_t sm = big_smem(SRC);
+    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    k<<<dim3(gx, (unsigned)p->H, (unsigned)npairs), kBigThreads, sm, s>>>(
+        a, b, p->kbar, oa, ob, ddpart, p->tw_m, p->tw_big, B, (int)p->H, (uint32_t)p->N, causal,
+        (uint32_t)p->m);
+  });
+  return gx;
+}
+
+template <typename ST, typename IO, int MODE>
+void launch_pass3(const fb_plan* p, const CxT<ST>* w, const IO* skip, IO* out, float* dkbar,
+                  int B, int npairs, float scale, cudaStream_t s) {
+  const int causal = p->mode == FB_MODE_CAUSAL;
+  if (p->m <= 16) {
+    with_m(p->m, [&](auto mc) {
+      constexpr int M = decltype(mc)::value;
+      tp_pass3_kernel<ST, IO, M, MODE><<<dim3(kL / kColThreads, (unsigned)p->H, (unsigned)npairs),
+                                         kColThreads, 0, s>>>(w, skip, out, p->d, dkbar, p->tw_n, B,
+                                                              (int)p->H, (uint32_t)p->N, causal,
+                                                              scale);
+    });
+    return;
+  }
+  const uint32_t gx = (uint32_t)(kL / (kBigTile / p->m));
+  with_small(p->m, [&](auto sc) {
+    constexpr int SM = decltype(sc)::value;
+    auto k = tp_pass3_big_kernel<ST, IO, SM, MODE>;
+    const size_t sm = big_smem(0);
+    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    k<<<dim3(gx, (unsigned)p->H, (unsigned)npairs), kBigThreads, sm, s>>>(
+        w, skip, out, p->d, dkbar, p->tw_m, p->tw_big, B, (int)p->H, (uint32_t)p->N, causal, scale,
+        (uint32_t)p->m);
+  });
+}
+
 size_t inter_bytes(const fb_plan* p, int64_t npairs) {
   const size_t es = p->dtype == FB_F32 ? 8 : 4;  // complex storage element
   return ((size_t)npairs * p->H * p->n * es + 255) & ~size_t(255);
@@ -389,13 +583,7 @@ int tp_prep(fb_plan* p, const float* K, cudaStream_t s) {
   rc = cuda_status(cudaMallocAsync(&x1k, (size_t)p->H * p->n * sizeof(CxT<float>), s),
                    "cudaMallocAsync(tp_prep)");
   if (rc) return rc;
-  const int causal = p->mode == FB_MODE_CAUSAL;
-  with_m(p->m, [&](auto mc) {
-    constexpr int M = decltype(mc)::value;
-    tp_pass1_kernel<float, float, M, 2><<<dim3(kL / kColThreads, (unsigned)p->H, 1), kColThreads, 0, s>>>(
-        nullptr, nullptr, p->kbar, x1k, nullptr, nullptr, p->tw_n, 2, (int)p->H, (uint32_t)p->N,
-        causal);
-  });
+  launch_pass1<float, float, 2>(p, nullptr, nullptr, x1k, nullptr, nullptr, 2, 1, s);
   const size_t sm = pass2_smem<float>();
   auto k = tp_pass2_kernel<float, 1>;
   cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
@@ -412,13 +600,12 @@ size_t tp_workspace(const fb_plan* p, int64_t B) {
   size_t bytes = 2 * inter_bytes(p, npairs);                            // X1dy/X1u (fwd: X1)
   bytes += ((size_t)p->H * p->n * sizeof(float2) + 255) & ~size_t(255); // dK rows
   bytes += ((size_t)p->H * p->N * sizeof(float) + 255) & ~size_t(255);  // dKbar scratch
-  bytes += ((size_t)p->H * npairs * (kL / kColThreads) * sizeof(float) + 255) & ~size_t(255);
+  bytes += ((size_t)p->H * npairs * 1024 * sizeof(float) + 255) & ~size_t(255);  // dD partials
   return bytes + 256;
 }
 
 int tp_fwd(fb_plan* p, const void* u, void* y, int64_t B, void* ws, cudaStream_t s) {
   const int64_t npairs = (B + 1) / 2;
-  const int causal = p->mode == FB_MODE_CAUSAL;
   if (p->periodic) {
     set_error("three-pass: circular mode needs N == n");
     return FB_ERR_UNSUPPORTED;
@@ -427,24 +614,15 @@ int tp_fwd(fb_plan* p, const void* u, void* y, int64_t B, void* ws, cudaStream_t
     using IO = decltype(io);
     using ST = IO;
     auto* x1 = reinterpret_cast<CxT<ST>*>(ws);
-    with_m(p->m, [&](auto mc) {
-      constexpr int M = decltype(mc)::value;
-      tp_pass1_kernel<IO, ST, M, 0>
-          <<<dim3(kL / kColThreads, (unsigned)p->H, (unsigned)npairs), kColThreads, 0, s>>>(
-              (const IO*)u, nullptr, nullptr, x1, nullptr, nullptr, p->tw_n, (int)B, (int)p->H,
-              (uint32_t)p->N, causal);
-      const size_t sm = pass2_smem<ST>();
-      auto k2 = tp_pass2_kernel<ST, 0>;
-      cudaFuncSetAttribute(k2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-      const int chunks = pass2_chunks(p, npairs);
-      const int ppc = (int)((npairs + chunks - 1) / chunks);
-      k2<<<dim3((unsigned)(p->H * p->m), (unsigned)chunks), kL / 16, sm, s>>>(
-          x1, p->kf, nullptr, p->tw_l, (int)npairs, (int)p->H, (int)p->m, ppc, 0.f);
-      tp_pass3_kernel<ST, IO, M, 0>
-          <<<dim3(kL / kColThreads, (unsigned)p->H, (unsigned)npairs), kColThreads, 0, s>>>(
-              x1, (const IO*)u, (IO*)y, p->d, nullptr, p->tw_n, (int)B, (int)p->H, (uint32_t)p->N,
-              causal, 1.f);
-    });
+    launch_pass1<IO, ST, 0>(p, (const IO*)u, nullptr, x1, nullptr, nullptr, (int)B, (int)npairs, s);
+    const size_t sm = pass2_smem<ST>();
+    auto k2 = tp_pass2_kernel<ST, 0>;
+    cudaFuncSetAttribute(k2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    const int chunks = pass2_chunks(p, npairs);
+    const int ppc = (int)((npairs + chunks - 1) / chunks);
+    k2<<<dim3((unsigned)(p->H * p->m), (unsigned)chunks), kL / 16, sm, s>>>(
+        x1, p->kf, nullptr, p->tw_l, (int)npairs, (int)p->H, (int)p->m, ppc, 0.f);
+    launch_pass3<ST, IO, 0>(p, x1, (const IO*)u, (IO*)y, nullptr, (int)B, (int)npairs, 1.f, s);
   });
   return cuda_status(cudaGetLastError(), "tp_fwd");
 }
@@ -452,12 +630,12 @@ int tp_fwd(fb_plan* p, const void* u, void* y, int64_t B, void* ws, cudaStream_t
 int tp_bwd(fb_plan* p, const void* dy, const void* u, void* du, float* dK, float* dKbar, float* dD,
            int64_t B, void* ws, cudaStream_t s) {
   const int64_t npairs = (B + 1) / 2;
-  const int causal = p->mode == FB_MODE_CAUSAL;
   if (p->periodic) {
     set_error("three-pass: circular mode needs N == n");
     return FB_ERR_UNSUPPORTED;
   }
   char* w = (char*)ws;
+  uint32_t gx = 0;
   const size_t ib = inter_bytes(p, npairs);
   char* x1dy_raw = w;
   char* x1u_raw = w + ib;
@@ -472,29 +650,18 @@ int tp_bwd(fb_plan* p, const void* dy, const void* u, void* du, float* dK, float
     using ST = IO;
     auto* x1dy = reinterpret_cast<CxT<ST>*>(x1dy_raw);
     auto* x1u = reinterpret_cast<CxT<ST>*>(x1u_raw);
-    with_m(p->m, [&](auto mc) {
-      constexpr int M = decltype(mc)::value;
-      tp_pass1_kernel<IO, ST, M, 1>
-          <<<dim3(kL / kColThreads, (unsigned)p->H, (unsigned)npairs), kColThreads, 0, s>>>(
-              (const IO*)dy, (const IO*)u, nullptr, x1dy, x1u, ddpart, p->tw_n, (int)B, (int)p->H,
-              (uint32_t)p->N, causal);
-      const size_t sm = pass2_bwd_smem<ST>();
-      auto k2 = tp_pass2_bwd_kernel<ST>;
-      cudaFuncSetAttribute(k2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-      k2<<<(unsigned)(p->H * p->m), kL / 16, sm, s>>>(x1dy, x1u, p->kf, wdk, p->tw_l, (int)npairs,
-                                                       (int)p->H, (int)p->m);
-      tp_pass3_kernel<ST, IO, M, 0>
-          <<<dim3(kL / kColThreads, (unsigned)p->H, (unsigned)npairs), kColThreads, 0, s>>>(
-              x1dy, (const IO*)dy, (IO*)du, p->d, nullptr, p->tw_n, (int)B, (int)p->H,
-              (uint32_t)p->N, causal, 1.f);
-      tp_pass3_kernel<float, float, M, 1>
-          <<<dim3(kL / kColThreads, (unsigned)p->H, 1), kColThreads, 0, s>>>(
-              reinterpret_cast<const CxT<float>*>(wdk), nullptr, nullptr, nullptr, dkbar, p->tw_n,
-              2, (int)p->H, (uint32_t)p->N, causal, 1.0f / (float)p->n);
-    });
+    gx = launch_pass1<IO, ST, 1>(p, (const IO*)dy, (const IO*)u, x1dy, x1u, ddpart, (int)B,
+                                 (int)npairs, s);
+    const size_t sm = pass2_bwd_smem<ST>();
+    auto k2 = tp_pass2_bwd_kernel<ST>;
+    cudaFuncSetAttribute(k2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    k2<<<(unsigned)(p->H * p->m), kL / 16, sm, s>>>(x1dy, x1u, p->kf, wdk, p->tw_l, (int)npairs,
+                                                     (int)p->H, (int)p->m);
+    launch_pass3<ST, IO, 0>(p, x1dy, (const IO*)dy, (IO*)du, nullptr, (int)B, (int)npairs, 1.f, s);
+    launch_pass3<float, float, 1>(p, reinterpret_cast<const CxT<float>*>(wdk), nullptr, nullptr,
+                                  dkbar, 2, 1, 1.0f / (float)p->n, s);
   });
-  tp_dd_reduce_kernel<<<(unsigned)p->H, 32, 0, s>>>(ddpart, dD,
-                                                    (int)(npairs * (kL / kColThreads)));
+  tp_dd_reduce_kernel<<<(unsigned)p->H, 32, 0, s>>>(ddpart, dD, (int)(npairs * gx));
   int rc = cuda_status(cudaGetLastError(), "tp_bwd");
   if (rc) return rc;
   return regularizer_backward_dev(p, dkbar, dK, s);

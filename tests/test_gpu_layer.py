@@ -224,6 +224,27 @@ def test_three_pass_fp32(lc, B, H, N, mode):
     assert_parity(got, oracle_layer(lc, inp, cfg, causal=bool(mode)), 1e-5)
 
 
+@pytest.mark.parametrize("B,H,N", [(2, 1, 131072), (3, 1, 262144)])
+def test_three_pass_tiled_columns_fp32(lc, B, H, N):
+    """m = 2N / 8192 > 16: passes 1/3 run as smem-tiled batched column FFTs."""
+    inp = layer_inputs(lc, B, H, N, torch.float32)
+    cfg = fb.RegularizationConfig(**CFG)
+    plan, got = run_layer(inp, N, H, torch.float32, cfg, engine=2)
+    assert plan.m == 2 * N // 8192 and plan.m > 16
+    assert_parity(got, oracle_layer(lc, inp, cfg), 1e-5)
+
+
+@pytest.mark.slow
+def test_sweep_1m_bf16(lc):
+    """Top of the BASELINE sweep: N = 2^20 (m = 256 columns), one pair, bf16."""
+    B, H, N = 2, 1, 1 << 20
+    inp = layer_inputs(lc, B, H, N, torch.bfloat16)
+    cfg = fb.RegularizationConfig(**CFG)
+    plan, got = run_layer(inp, N, H, torch.bfloat16, cfg)
+    assert plan.engine == fb.Engine.THREE_PASS and plan.m == 256
+    assert_parity(got, oracle_layer(lc, inp, cfg), 2e-2, keys=("y", "du", "dK", "dD"))
+
+
 @pytest.mark.parametrize("dtype", [torch.bfloat16, torch.float16])
 def test_three_pass_16bit(lc, dtype):
     inp = layer_inputs(lc, 3, 2, 32768, dtype)
