@@ -15,6 +15,9 @@ from pathlib import Path
 PKG = Path(__file__).resolve().parent
 CSRC = PKG / "csrc"
 LIB = PKG / "libflashbutterfly.so"
+COMPAT_SRC = CSRC / "compat" / "longconv_compat.cpp"
+COMPAT_LIB = PKG / "liblongconv_b200.so"
+CUDA_HOME = Path(os.environ.get("CUDA_HOME", "/usr/local/cuda"))
 INCLUDE = PKG.parent / "include"
 
 SOURCES = ["fb_capi.cu", "fb_prep.cu", "fb_single.cu", "fb_single_tc.cu", "fb_three.cu",
@@ -40,6 +43,7 @@ def build(force: bool = False, verbose: bool = True) -> Path:
     deps = [CSRC / s for s in SOURCES] + list(CSRC.glob("*.cuh")) + list(CSRC.glob("*.h"))
     deps += list(INCLUDE.glob("*.h"))
     if not force and not _stale(LIB, deps):
+        build_compat()
         return LIB
     objdir = PKG / "build"
     objdir.mkdir(exist_ok=True)
@@ -61,7 +65,20 @@ def build(force: bool = False, verbose: bool = True) -> Path:
             print(out, file=sys.stderr)
     cmd = [_nvcc(), *ARCH, "-shared", "-o", str(LIB), *map(str, objs), "-lcudart"]
     subprocess.run(cmd, check=True)
+    build_compat(force=True)
     return LIB
+
+
+def build_compat(force: bool = False) -> Path:
+    """liblongconv_b200.so: the reference-shaped C++ API (include/longconv_b200.hpp)."""
+    deps = [COMPAT_SRC, INCLUDE / "longconv_b200.hpp", INCLUDE / "flashbutterfly.h", LIB]
+    if not force and not _stale(COMPAT_LIB, deps):
+        return COMPAT_LIB
+    cmd = ["g++", "-std=c++20", "-O2", "-fPIC", "-shared", "-Wall", "-Wextra", f"-I{INCLUDE}",
+           f"-I{CUDA_HOME / 'include'}", str(COMPAT_SRC), f"-L{PKG}", "-lflashbutterfly",
+           f"-L{CUDA_HOME / 'lib64'}", "-lcudart", "-Wl,-rpath,$ORIGIN", "-o", str(COMPAT_LIB)]
+    subprocess.run(cmd, check=True)
+    return COMPAT_LIB
 
 
 if __name__ == "__main__":
