@@ -38,6 +38,11 @@ CONFIGS = {
             workload="config2: LRA-scale B=32 H=256 N=4096 single-pass fwd+bwd, Squash/Smooth"),
     3: dict(B=16, H=128, N=65536, dtype="bf16", engine="three",
             workload="config3: Path256-scale B=16 H=128 N=65536 three-pass fwd+bwd"),
+    4: dict(B=8, H=768, N=1024, dtype="bf16", engine="learned", r=16,
+            workload="config4: learned-butterfly B=8 H=768 n=1024 fwd+bwd incl. block gradients"),
+    # config 5 (sweep N=256..1M at B*H=2048): --config 5 --n N
+    5: dict(B=8, H=256, N=4096, dtype="bf16", engine="auto",
+            workload="config5: sequence-length sweep at B*H=2048"),
 }
 LAM, P = 0.003, 1
 
@@ -60,6 +65,7 @@ class ClockSampler:
     def __init__(self, index: int):
         self.index = index
         self.samples = []
+        self.mark_at = 0
         self._stop = threading.Event()
         self._t = threading.Thread(target=self._run, daemon=True)
 
@@ -73,7 +79,11 @@ class ClockSampler:
                     self.samples.append([x.strip() for x in out.split(",")])
             except Exception:
                 pass
-            self._stop.wait(0.2)
+            self._stop.wait(0.05)
+
+    def mark(self):
+        """Start of the timed region (samples before it come from warm-up)."""
+        self.mark_at = len(self.samples)
 
     def __enter__(self):
         self._t.start()
@@ -84,8 +94,12 @@ class ClockSampler:
         self._t.join(timeout=10)
 
     def summary(self):
-        if not self.samples:
+        # timed-region samples, plus the last warm-up sample when the timed
+        # region is shorter than one polling interval
+        timed = self.samples[max(0, self.mark_at - 1):]
+        if not timed:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        self.samples = timed
         sm = sorted(float(s[0]) for s in self.samples)
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         reasons = sorted({names[i] for s in self.samples for i in range(4)
@@ -159,15 +173,18 @@ def run_ours(args, cfg, rank, world, local_rank):
         if rec is not None:
             rec[2].record(stream)
 
-    for _ in range(args.warmup):
-        step()
-    torch.cuda.synchronize()
     recs = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(args.steps)]
     t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    if dist:
-        dist.barrier()
-    torch.cuda.synchronize()
+    # the sampler runs from warm-up through the timed region (nvidia-smi polls
+    # every ~50 ms; a short timed region alone would see one sample)
     with ClockSampler(local_rank) as clk:
+        for _ in range(args.warmup):
+            step()
+        torch.cuda.synchronize()
+        if dist:
+            dist.barrier()
+        torch.cuda.synchronize()
+        clk.mark()
         t0.record(stream)
         for i in range(args.steps):
             step(recs[i])
@@ -287,6 +304,125 @@ def run_ours(args, cfg, rank, world, local_rank):
     return out
 
 
+def run_learned(args, cfg, rank, world, local_rank):
+    """Config 4: learned butterfly fwd + bwd (block + input gradients) over
+    B*H rows of n complex, bf16 rows, per-head fp32 complex blocks."""
+    import torch
+
+    import paper_2302_06646_b200 as fb
+
+    dev = torch.device("cuda", local_rank)
+    torch.cuda.set_device(dev)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=dev)
+    B, H, n, r = cfg["B"], cfg["H"], cfg["N"], cfg["r"]
+    dt = torch.bfloat16
+    plan = fb.LearnedButterflyPlan(n, r, H, dt, dev)
+    g = torch.Generator(device=dev)
+    g.manual_seed(99 + rank)
+    blocks = plan.dft_blocks() + 0.1 * torch.randn(H, plan.param_count, dtype=torch.complex64,
+                                                   device=dev, generator=g)
+    x = torch.randn(B, H, n, 2, device=dev, generator=g).to(dt)
+    up = torch.randn(B, H, n, 2, device=dev, generator=g).to(dt)
+    stream = torch.cuda.current_stream()
+    recs = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(args.steps)]
+    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+
+    def step(rec=None):
+        if rec:
+            rec[0].record(stream)
+        plan.forward(blocks, x)
+        if rec:
+            rec[1].record(stream)
+        plan.gradients(blocks, x, up)
+        if rec:
+            rec[2].record(stream)
+
+    with ClockSampler(local_rank) as clk:
+        for _ in range(args.warmup):
+            step()
+        torch.cuda.synchronize()
+        if dist:
+            dist.barrier()
+        clk.mark()
+        t0.record(stream)
+        for i in range(args.steps):
+            step(recs[i])
+        t1.record(stream)
+        torch.cuda.synchronize()
+    tmax = torch.tensor([t0.elapsed_time(t1)], device=dev)
+    if dist:
+        dist.all_reduce(tmax, op=dist.ReduceOp.MAX)
+    ms_step = float(tmax.item()) / args.steps
+    fwd_ms = sum(q[0].elapsed_time(q[1]) for q in recs) / args.steps
+    bwd_ms = sum(q[1].elapsed_time(q[2]) for q in recs) / args.steps
+    E = B * H * n
+    value = E * world / (ms_step / 1e3)
+    # e2e: host rows in, host results out
+    hx, hu = x.cpu().pin_memory(), up.cpu().pin_memory()
+    hy = torch.empty_like(hx).pin_memory()
+    hdx = torch.empty_like(hx).pin_memory()
+    hdb = torch.empty(H, plan.param_count, dtype=torch.complex64).pin_memory()
+    xx, uu = torch.empty_like(x), torch.empty_like(up)
+
+    def e2e():
+        xx.copy_(hx, non_blocking=True)
+        uu.copy_(hu, non_blocking=True)
+        yy = plan.forward(blocks, xx)
+        db, dx = plan.gradients(blocks, xx, uu)
+        hy.copy_(yy, non_blocking=True)
+        hdx.copy_(dx, non_blocking=True)
+        hdb.copy_(db, non_blocking=True)
+
+    e2e()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    k = max(1, min(args.steps, 10))
+    e0.record(stream)
+    for _ in range(k):
+        e2e()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    ems = e0.elapsed_time(e1) / k
+    if rank != 0:
+        if dist:
+            dist.destroy_process_group()
+        return None
+    hbm_peak, _, peak_kind = load_peaks()
+    bytes_step = 20 * E  # bf16 complex rows: fwd x,y; bwd x,g,dx (SURVEY.md §8d)
+    out = {
+        "metric": "learned-butterfly fwd+bwd rows*n elements/sec (incl. block gradients)",
+        "value": value, "unit": "elements/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
+        "data": "synthetic (randn rows, DFT-initialised blocks + 0.1 randn)",
+        "config": {"workload": cfg["workload"], "B": B, "H": H, "n": n, "r": r,
+                   "factors": plan.factors, "params_per_head": plan.param_count,
+                   "l2": "rows 100 MiB per tensor"},
+        "fwd_ms": fwd_ms, "bwd_ms": bwd_ms,
+        "roofline": {"bound": "hbm", "kernel": "lb_bwd_kernel", "achieved": 12 * E / (bwd_ms / 1e3) / 1e9,
+                     "peak": hbm_peak, "unit": "GB/s",
+                     "frac": 12 * E / (bwd_ms / 1e3) / 1e9 / hbm_peak, "traffic": None,
+                     "alg_bytes_per_launch": 12 * E, "peak_kind": peak_kind},
+        "step_roofline": {"alg_bytes": bytes_step,
+                          "achieved_GBs": bytes_step / (ms_step / 1e3) / 1e9,
+                          "frac": bytes_step / (ms_step / 1e3) / 1e9 / hbm_peak},
+        "e2e": {"value": E * world / (ems / 1e3), "unit": "elements/s",
+                "h2d_bytes_per_step": 2 * E * 4, "d2h_bytes_per_step": 2 * E * 4 + H * plan.param_count * 8,
+                "ms_per_step": ems},
+        "cpu_baseline": None if args.no_cpu_baseline else cpu_baseline(cfg, args.cpu_sample_heads),
+        "clocks": clk.summary(),
+        "gpu_launches": 2 * args.steps,
+    }
+    print(json.dumps(out), flush=True)
+    if dist:
+        dist.destroy_process_group()
+    return out
+
+
 def reference_cpu_run(cfg, heads, steps=1, threads=None):
     """Reference CPU path (oracle/_ref = unmodified reference sources):
     regularized_long_conv(kButterfly, kCausal, threads=nproc) + the backward
@@ -300,6 +436,20 @@ def reference_cpu_run(cfg, heads, steps=1, threads=None):
     ref = RefOracle(threads)
     B, N = cfg["B"], cfg["N"]
     rng = np.random.default_rng(0)
+    if cfg["engine"] == "learned":
+        # learned_forward + learned_gradients (butterfly.cpp:235-307) per row
+        r = cfg["r"]
+        base = ref.learned_init(N, r)
+        blocks = base + 0.1 * (rng.standard_normal(base.size) + 1j * rng.standard_normal(base.size))
+        x = rng.standard_normal((B, heads, N)) + 1j * rng.standard_normal((B, heads, N))
+        g = rng.standard_normal((B, heads, N)) + 1j * rng.standard_normal((B, heads, N))
+        t0 = time.perf_counter()
+        for _ in range(steps):
+            for b in range(B):
+                for h in range(heads):
+                    ref.learned_forward(blocks, x[b, h], r)
+                    ref.learned_gradients(blocks, x[b, h], g[b, h], r)
+        return B * heads * N * steps, time.perf_counter() - t0
     u = rng.standard_normal((B, heads, N))
     dy = rng.standard_normal((B, heads, N))
     K, D = ref.init_kernels(1, heads, N, 3)
@@ -320,6 +470,8 @@ def cpu_baseline(cfg, heads):
         el, sec = reference_cpu_run(cfg, heads, 1, threads)
     except Exception as e:  # pragma: no cover
         return {"value": None, "unit": "elements/s", "error": str(e)}
+    if cfg["engine"] == "learned":
+        threads = 1  # learned_forward / learned_gradients are single-threaded per row
     return {"value": el / sec, "unit": "elements/s", "cores": threads, "kind": "reference",
             "sample": f"B={cfg['B']} H={heads} (of {cfg['H']}) N={cfg['N']}, fp64, "
                       f"{sec:.1f}s: regularize_bank + regularized_long_conv(kButterfly) + "
@@ -363,11 +515,18 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--cpu-sample-heads", type=int, default=32)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--n", type=int, default=None, help="sequence length (config 5 sweep)")
     args = ap.parse_args()
     rank = int(os.environ.get("RANK", 0))
     world = int(os.environ.get("WORLD_SIZE", 1))
     local_rank = int(os.environ.get("LOCAL_RANK", 0))
-    cfg = CONFIGS[args.config]
+    cfg = dict(CONFIGS[args.config])
+    if args.n is not None:
+        cfg["N"] = args.n
+        cfg["workload"] = cfg["workload"] + f", N={args.n}"
+    if args.config == 4 and args.impl == "ours":
+        run_learned(args, cfg, rank, world, local_rank)
+        return
     if args.impl == "reference":
         run_reference(args, cfg, rank)
         return

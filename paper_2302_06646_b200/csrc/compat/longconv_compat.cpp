@@ -257,7 +257,8 @@ LearnedBatchGradients learned_gradients_batched(std::size_t n, std::size_t r, st
   auto xd = upload_io(x);
   auto gd = upload_io(upstream);
   DevBuf dxd(x.size() * io_size()), dbd(blocks.size() * 4);
-  check(fb_learned_bwd(p, (const float*)bl->p, xd->p, gd->p, dxd.p, (float*)dbd.p, (int64_t)B, nullptr,
+  DevBuf wsd(fb_learned_workspace_size(p, (int64_t)B));
+  check(fb_learned_bwd(p, (const float*)bl->p, xd->p, gd->p, dxd.p, (float*)dbd.p, (int64_t)B, wsd.p,
                        nullptr),
         "fb_learned_bwd");
   cuda(cudaDeviceSynchronize(), "sync");

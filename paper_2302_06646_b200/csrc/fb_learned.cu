@@ -89,26 +89,30 @@ __global__ void __launch_bounds__(kLbThreads)
   }
 }
 
-// One CTA per head: all B rows in order (deterministic dblocks).
+// CTA (h, split): rows b in [split * rows, ...) of head h, in order; the
+// block gradient partial of the split goes to gpart[split][h] and
+// lb_reduce_kernel sums the splits in a fixed order (deterministic).
 template <typename IO>
 __global__ void __launch_bounds__(kLbThreads)
     lb_bwd_kernel(const float* __restrict__ blocks, const IO* __restrict__ x,
-                  const IO* __restrict__ g, IO* __restrict__ dx, float* __restrict__ dblocks,
+                  const IO* __restrict__ g, IO* __restrict__ dx, float2* __restrict__ gpart,
                   const uint32_t* __restrict__ omap, const float2* __restrict__ tw, LbStages st,
-                  int B, int H, uint32_t n, int P) {
+                  int B, int H, uint32_t n, int P, int rows) {
   extern __shared__ __align__(16) float2 lsm[];
   float2* W = lsm;                          // [P]
   float2* G = W + P;                        // [P] gradient accumulator
-  float2* saved = G + P;                    // [S][n] stage inputs
+  float2* red = G + P;                      // [kLbThreads] column-split partials
+  float2* saved = red + kLbThreads;         // [S][n] stage inputs
   float2* ga = saved + (size_t)st.nstages * n;  // [n]
   float2* gb = ga + n;                      // [n]
   const int h = blockIdx.x;
+  const int b_begin = blockIdx.y * rows, b_end = min(B, b_begin + rows);
   const float2* wg = reinterpret_cast<const float2*>(blocks) + (size_t)h * P;
   for (int i = threadIdx.x; i < P; i += blockDim.x) {
     W[i] = wg[i];
     G[i] = make_float2(0.f, 0.f);
   }
-  for (int b = 0; b < B; ++b) {
+  for (int b = b_begin; b < b_end; ++b) {
     const IO* xr = x + ((size_t)b * H + h) * 2 * n;
     const IO* gr = g + ((size_t)b * H + h) * 2 * n;
     __syncthreads();
@@ -133,17 +137,32 @@ __global__ void __launch_bounds__(kLbThreads)
         ga[i] = cmulc(ga[i], __ldg(tw + (size_t)a * q * (n / L)));
       }
       __syncthreads();
-      // G[a][p] += sum_{seg, q} w[a][q] conj(v[p][q])   (thread per (a,p))
-      for (int e = threadIdx.x; e < f * f; e += blockDim.x) {
-        const int a = e / f, p = e % f;
-        float2 acc = G[st.off[k] + e];
-        for (uint32_t seg = 0; seg < n; seg += L)
-          for (int q = 0; q < rest; ++q) {
-            const float2 wv = ga[seg + a * rest + q], vv = v[seg + p * rest + q];
+      // G[a][p] += sum_{seg, q} w[a][q] conj(v[p][q]): entry e = (a, p) by
+      // ns threads, each over every ns-th column, then a fixed-order sum
+      {
+        const int ff = f * f;
+        const int ns = ff >= (int)blockDim.x ? 1 : (int)blockDim.x / ff;
+        const uint32_t cols = n / f;  // (segment, q) pairs
+        for (int t = threadIdx.x; t < ff * ns; t += blockDim.x) {
+          const int e = t % ff, grp = t / ff, a = e / f, p = e % f;
+          float2 acc = make_float2(0.f, 0.f);
+          for (uint32_t cidx = grp; cidx < cols; cidx += ns) {
+            const uint32_t off = (cidx / rest) * L + (cidx % rest);
+            const float2 wv = ga[off + a * rest], vv = v[off + p * rest];
             acc.x = fmaf(wv.x, vv.x, fmaf(wv.y, vv.y, acc.x));
             acc.y = fmaf(wv.y, vv.x, fmaf(-wv.x, vv.y, acc.y));
           }
-        G[st.off[k] + e] = acc;
+          if (ns == 1) G[st.off[k] + e] = cadd(G[st.off[k] + e], acc);
+          else red[t] = acc;
+        }
+        if (ns > 1) {
+          __syncthreads();
+          for (int e = threadIdx.x; e < ff; e += blockDim.x) {
+            float2 acc = G[st.off[k] + e];
+            for (int grp = 0; grp < ns; ++grp) acc = cadd(acc, red[grp * ff + e]);
+            G[st.off[k] + e] = acc;
+          }
+        }
       }
       // g' = W^H w
       for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) {
@@ -165,8 +184,17 @@ __global__ void __launch_bounds__(kLbThreads)
     for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) stc<IO>(dr + 2 * i, ga[i]);
   }
   __syncthreads();
-  float2* dg = reinterpret_cast<float2*>(dblocks) + (size_t)h * P;
+  float2* dg = gpart + ((size_t)blockIdx.y * H + h) * P;
   for (int i = threadIdx.x; i < P; i += blockDim.x) dg[i] = G[i];
+}
+
+__global__ void lb_reduce_kernel(const float2* __restrict__ gpart, float2* __restrict__ dblocks,
+                                 int splits, size_t HP) {
+  const size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= HP) return;
+  float2 acc = make_float2(0.f, 0.f);
+  for (int sp = 0; sp < splits; ++sp) acc = cadd(acc, gpart[(size_t)sp * HP + i]);
+  dblocks[i] = acc;
 }
 
 struct LbDevice {
@@ -330,7 +358,18 @@ int fb_learned_plan_factors(const fb_learned_plan* p, int64_t* factors, int64_t*
   return FB_OK;
 }
 
-size_t fb_learned_workspace_size(const fb_learned_plan*, int64_t) { return 0; }
+// Row splits per head for the backward: enough CTAs to fill the SMs twice.
+static int lb_splits(const fb_learned_plan* p, int64_t B) {
+  int dev_sms = 148;
+  cudaDeviceGetAttribute(&dev_sms, cudaDevAttrMultiProcessorCount, p->device);
+  int64_t s = (2 * dev_sms + p->H - 1) / p->H;
+  return (int)std::max<int64_t>(1, std::min<int64_t>(s, B));
+}
+
+size_t fb_learned_workspace_size(const fb_learned_plan* p, int64_t B) {
+  if (!p || B < 1) return 0;
+  return (size_t)lb_splits(p, B) * p->H * p->param_count * sizeof(float2);
+}
 
 int fb_learned_fwd(fb_learned_plan* p, const float* blocks, const void* x, void* y, int64_t B,
                    void*, void* stream) {
@@ -364,7 +403,7 @@ int fb_learned_fwd(fb_learned_plan* p, const float* blocks, const void* x, void*
 }
 
 int fb_learned_bwd(fb_learned_plan* p, const float* blocks, const void* x, const void* g, void* dx,
-                   float* dblocks, int64_t B, void*, void* stream) {
+                   float* dblocks, int64_t B, void* ws, void* stream) {
   if (!p || !blocks || !x || !g || !dx || !dblocks) {
     set_error("fb_learned_bwd: null argument");
     return FB_ERR_ARG;
@@ -377,7 +416,13 @@ int fb_learned_bwd(fb_learned_plan* p, const float* blocks, const void* x, const
   if (rc) return rc;
   fb_learned_ext* ext = ext_of(p);
   cudaStream_t s = (cudaStream_t)stream;
-  const size_t sm = (2 * p->param_count + (p->nstages + 2) * p->n) * sizeof(float2);
+  if (!ws) {
+    set_error("fb_learned_bwd: workspace required (fb_learned_workspace_size)");
+    return FB_ERR_ARG;
+  }
+  const int splits = lb_splits(p, B);
+  const int rows = (int)((B + splits - 1) / splits);
+  const size_t sm = (2 * p->param_count + kLbThreads + (p->nstages + 2) * p->n) * sizeof(float2);
   if (sm > 227 * 1024) {
     set_error("learned_gradients: row too long for the on-chip backward");
     return FB_ERR_UNSUPPORTED;
@@ -386,13 +431,16 @@ int fb_learned_bwd(fb_learned_plan* p, const float* blocks, const void* x, const
     using IO = decltype(io);
     auto k = lb_bwd_kernel<IO>;
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-    k<<<(unsigned)p->H, kLbThreads, sm, s>>>(blocks, (const IO*)x, (const IO*)g, (IO*)dx, dblocks,
-                                             ext->dev.omap, ext->dev.tw, ext->dev.st, (int)B,
-                                             (int)p->H, (uint32_t)p->n, (int)p->param_count);
+    k<<<dim3((unsigned)p->H, (unsigned)splits), kLbThreads, sm, s>>>(
+        blocks, (const IO*)x, (const IO*)g, (IO*)dx, (float2*)ws, ext->dev.omap, ext->dev.tw,
+        ext->dev.st, (int)B, (int)p->H, (uint32_t)p->n, (int)p->param_count, rows);
   };
   if (p->dtype == FB_F32) go(float{});
   else if (p->dtype == FB_BF16) go(__nv_bfloat16{});
   else go(__half{});
+  const size_t HP = (size_t)p->H * p->param_count;
+  lb_reduce_kernel<<<(unsigned)((HP + 255) / 256), 256, 0, s>>>((const float2*)ws, (float2*)dblocks,
+                                                               splits, HP);
   return cuda_status(cudaGetLastError(), "fb_learned_bwd");
 }
 

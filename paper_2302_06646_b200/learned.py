@@ -99,8 +99,10 @@ class LearnedButterflyPlan:
         blocks = self._blocks(blocks)
         dx = torch.empty_like(x)
         db = torch.empty_like(blocks)
+        nbytes = _lib.lib().fb_learned_workspace_size(self._h, B)
+        ws = torch.empty(max(int(nbytes), 1), dtype=torch.uint8, device=self.device)
         check(_lib.lib().fb_learned_bwd(self._h, _ptr(blocks), _ptr(x), _ptr(upstream), _ptr(dx),
-                                        _ptr(db), B, C.c_void_p(0), _stream()))
+                                        _ptr(db), B, _ptr(ws), _stream()))
         return db, dx
 
 
