@@ -258,8 +258,15 @@ def run_ours(args, cfg, rank, world, local_rank):
     hbm_peak, tc_peak, peak_kind = load_peaks()
     # dominant kernel: the backward (K4a sp_bwd / K4b passes)
     HN = H * N
-    bwd_bytes = 3 * s * E + 16 * HN
-    fwd_bytes = 2 * s * E + 16 * HN
+    # algorithmic bytes per launch: single-pass reads/writes each
+    # signal once plus k_f (8 B per bin, n = 2N bins per head); three-pass adds
+    # the complex intermediates (2s bytes per real element each, 2N-padded)
+    if plan.engine == fb.Engine.THREE_PASS:
+        bwd_bytes = 16 * s * E + 52 * HN
+        fwd_bytes = 11 * s * E + 16 * HN
+    else:
+        bwd_bytes = 3 * s * E + 16 * HN
+        fwd_bytes = 2 * s * E + 16 * HN
     dom = "bwd" if bwd_ms >= fwd_ms else "fwd"
     dom_bytes, dom_ms = (bwd_bytes, bwd_ms) if dom == "bwd" else (fwd_bytes, fwd_ms)
     achieved = dom_bytes / (dom_ms / 1e3) / 1e9
@@ -285,7 +292,10 @@ def run_ours(args, cfg, rank, world, local_rank):
                    "l2": "inputs larger than L2 (u, dy, y, du = "
                          f"{4 * E * s / 2**20:.0f} MiB per GPU)"},
         "fwd_ms": fwd_ms, "bwd_ms": bwd_ms,
-        "roofline": {"bound": "hbm", "kernel": f"{dom} (sp_{dom}_kernel)" if plan.engine.name != "THREE_PASS" else dom,
+        "roofline": {"bound": "hbm",
+                     "kernel": (f"{dom}: tc_{dom}_kernel (tcgen05)" if plan.tensor_cores else
+                                f"{dom}: sp_{dom}_kernel" if plan.engine.name != "THREE_PASS" else
+                                f"{dom}: three-pass launches (pass1, pass2, pass3)"),
                      "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
                      "frac": achieved / hbm_peak, "traffic": traffic,
                      "alg_bytes_per_launch": dom_bytes, "peak_kind": peak_kind},

@@ -1,0 +1,113 @@
+"""Multi-rank host logic on CPU (gloo, world size 2 and 4):
+
+* B*H sharding: every rank runs its head slice with no collective and the
+  concatenation equals the unsharded layer (oracle compute per rank);
+* sequence-sharded four-step (config 5-4M): the two all-to-all transposes of
+  paper_2302_06646_b200.seqshard move the data so that, with a numpy
+  restatement of the three local passes, the sharded circular convolution
+  equals the single-process one.
+"""
+import os
+import tempfile
+
+import numpy as np
+import pytest
+import torch
+
+from paper_2302_06646_b200 import seqshard as ss
+
+L_COLS, M_ROWS = 64, 16  # n = l * m = 1024
+
+
+class NumpyPasses:
+    """numpy restatement of three_pass.cpp:225-254 on a rank's slice."""
+
+    def __init__(self, kf2_full: np.ndarray):
+        self.kf2 = kf2_full  # [C][m][l] = K_hat[a + m s] (per channel)
+
+    def pass1(self, x, sh):
+        n = sh.l * sh.m
+        X = np.fft.fft(x.numpy(), axis=1)  # over c: sum_c w_m^(a c)
+        tau = np.arange(sh.tau0, sh.tau0 + sh.lp)
+        a = np.arange(sh.m)[:, None]
+        return torch.from_numpy(X * np.exp(-2j * np.pi * a * tau[None, :] / n)).to(torch.complex64)
+
+    def pass2(self, rows, sh):
+        Z = np.fft.fft(rows.numpy(), axis=2)
+        Z = Z * self.kf2[:, sh.a0:sh.a0 + sh.mp, :]
+        return torch.from_numpy(np.fft.ifft(Z, axis=2) * sh.l).to(torch.complex64)
+
+    def pass3(self, w, sh):
+        n = sh.l * sh.m
+        tau = np.arange(sh.tau0, sh.tau0 + sh.lp)
+        a = np.arange(sh.m)[:, None]
+        W = w.numpy() * np.exp(2j * np.pi * a * tau[None, :] / n)
+        return torch.from_numpy(np.fft.ifft(W, axis=1) * sh.m / n).to(torch.complex64)
+
+
+def _problem(C=3, seed=0):
+    rng = np.random.default_rng(seed)
+    n = L_COLS * M_ROWS
+    x = (rng.standard_normal((C, n)) + 1j * rng.standard_normal((C, n))).astype(np.complex64)
+    k = rng.standard_normal((C, n)).astype(np.float32)
+    khat = np.fft.fft(k, axis=1)
+    s = np.arange(L_COLS)
+    a = np.arange(M_ROWS)
+    kf2 = khat[:, a[:, None] + M_ROWS * s[None, :]]  # [C][m][l] = K_hat[a + m s]
+    want = np.fft.ifft(np.fft.fft(x, axis=1) * khat, axis=1)
+    return x, kf2, want
+
+
+def _seq_worker(rank, world):
+    x, kf2, _ = _problem()
+    sh = ss.SeqShard(L_COLS, M_ROWS, world, rank)
+    cols = ss.scatter_tau(torch.from_numpy(x), sh)
+    y = ss.four_step_conv(cols, sh, NumpyPasses(kf2))
+    np.save(os.path.join(os.environ["FB_TEST_DIR"], f"seq_{world}_{rank}.npy"), y.numpy())
+
+
+@pytest.mark.parametrize("world", [2, 4])
+def test_seq_sharded_four_step_gloo(world, monkeypatch):
+    d = tempfile.mkdtemp()
+    monkeypatch.setenv("FB_TEST_DIR", d)
+    ss.run_ranks(world, _seq_worker, port=29571 + world)
+    x, _, want = _problem()
+    sh = ss.SeqShard(L_COLS, M_ROWS, world, 0)
+    parts = [torch.from_numpy(np.load(os.path.join(d, f"seq_{world}_{r}.npy"))) for r in range(world)]
+    got = ss.gather_tau(parts, sh).numpy()
+    assert np.abs(got - want).max() / np.abs(want).max() < 1e-5
+
+
+def test_transposes_are_inverse_single_rank():
+    # world 1: no exchange, identity layouts
+    sh = ss.SeqShard(8, 4, 1, 0)
+    x = torch.randn(2, 4, 8, dtype=torch.complex64)
+    assert torch.equal(ss.scatter_tau(x.reshape(2, 32), sh), x)
+
+
+def _head_worker(rank, world):
+    from oracle.oracle import LcOracle
+
+    lc = LcOracle()
+    B, H, N = 2, 8, 256
+    u = lc.signal_batch(1, B, H, N)
+    K, D = lc.init_kernels(1, H, N, 3)
+    sl = ss.head_shard(H, world, rank)
+    y = lc.regularized_long_conv(u[:, sl], K[sl], D[sl], 0.003, 1)
+    gathered = [torch.zeros(B, H // world, N, dtype=torch.float64) for _ in range(world)]
+    torch.distributed.all_gather(gathered, torch.from_numpy(y))
+    if rank == 0:
+        np.save(os.path.join(os.environ["FB_TEST_DIR"], f"heads_{world}.npy"),
+                torch.cat(gathered, dim=1).numpy())
+
+
+@pytest.mark.parametrize("world", [2, 4])
+def test_head_sharding_gloo(world, monkeypatch, lc):
+    d = tempfile.mkdtemp()
+    monkeypatch.setenv("FB_TEST_DIR", d)
+    ss.run_ranks(world, _head_worker, port=29581 + world)
+    B, H, N = 2, 8, 256
+    u = lc.signal_batch(1, B, H, N)
+    K, D = lc.init_kernels(1, H, N, 3)
+    want = lc.regularized_long_conv(u, K, D, 0.003, 1)
+    assert np.array_equal(np.load(os.path.join(d, f"heads_{world}.npy")), want)
