@@ -3,23 +3,26 @@
 // causal) — BASELINE config 2.
 //
 // The reference's butterfly (apply_stages, proj/src/butterfly.cpp:124-163)
-// computes F_n x as dense DFT blocks joined by twiddles.  Here F_8192 is
-// the three-factor Monarch product  n = 16 (t1) x 16 (t2) x 32 (t3),
-// t = 512 t1 + 32 t2 + t3,  f = f1 + 16 f2 + 256 f3:
-//   A: DFT16 over t1       rows m_A = 32 t2 + t3     (512)   K 16  N 32
-//      twiddle  w_8192^(f1 m_A)
-//   B: DFT16 over t2       rows m_B = 32 f1 + t3     (512)   K 32  N 32
-//      twiddle  w_512^(f2 t3)
-//   C: DFT32 over t3       rows m_C = 16 f1 + f2     (256)   K 64  N 64
-// and the inverse C' -> B' -> A' runs the conjugate blocks back.  Every
-// dense block is one tcgen05.mma (bf16/fp16 operands, complex split into
-// real-stacked K = [re | im], fp32 accumulate in TMEM).  The causal
-// zero-padding is pruned: stage A reads only t1 < 8 (K = 16 instead of 32)
-// and A' produces only t1 < 8 (N = 16).  Twiddles, the k_f product and the
-// bf16 re-quantisation happen in the TMEM -> register -> smem epilogues;
-// the u pair arrives by one 4-D TMA load per 64-row block, written by the
-// TMA straight into the MN-major 128B-swizzled UMMA operand layout.
-// Two real channels (b, b+1) of one head ride as re/im of one transform.
+// computes F_n x as dense DFT blocks joined by twiddles.  Here F_8192 is the
+// two-factor Monarch product n = 64 (t1) x 128 (t2), t = 128 t1 + t2,
+// f = f1 + 64 f2:
+//   A : DFT64 over t1        D[t2][f1]   M 128 (t2)  N 128 (f1 re|im)  K 64 (t1<32 re|im)
+//       twiddle w_8192^(f1 t2)
+//   B : DFT128 over t2       D[f2][f1]   M 128 (f2)  N 64 (f1) x {re, im}  K 128 (t2)
+//       (the DFT128 block is the A operand: Xr = Fr.Ar - Fi.Ai, Xi = Fi.Ar + Fr.Ai,
+//        four real GEMMs, the minus via the instruction descriptor's negate bit)
+//   x k_f' = (K_hat + D)/n   (the skip D u is a flat spectrum)
+//   B': IDFT128 over f2      D[t2][f1]   (conj block: Fr.Zr + Fi.Zi, Fr.Zi - Fi.Zr)
+//       twiddle w_8192^(-f1 t2)
+//   A': IDFT64 over f1       D[t2][t1]   M 128  N 64 (t1<32 re|im)  K 128 (f1 re|im)
+// Causal zero padding is pruned on both ends (t1 < 32 in A and A').  Every
+// dense block is a tcgen05.mma on bf16/fp16 operands with fp32 accumulation
+// in TMEM.  Each stage boundary is one TMEM -> register -> smem epilogue in
+// which a thread owns 16 consecutive elements of the next operand, so every
+// operand write is a pair of 16-byte stores into a 128B-swizzled UMMA
+// layout; the u pair arrives by 4-D TMA boxes written straight into the
+// MN-major swizzled operand.  Two real channels (b, b+1) of one head ride as
+// re/im of one transform.
 #include <cuda.h>
 
 #include <algorithm>
@@ -40,89 +43,65 @@ namespace tcfft {
 constexpr uint32_t kN = 8192;
 constexpr uint32_t kThreads = 512;
 
-// shared memory map (bytes, 1024-aligned where swizzled operands live)
-constexpr uint32_t SIN = 0;                   // inputs: fwd [slot][16 KB] u pairs; bwd [2][dy,u][16 KB]
-constexpr uint32_t SIN_BYTES = 4 * 16384;
-constexpr uint32_t SOP = SIN + SIN_BYTES;     // [slot][32 KB]: B / C / C' / B' / A' operand (one live at a time)
-constexpr uint32_t SMAT = SOP + 2 * 32768;    // 22 KB DFT blocks
-constexpr uint32_t MAT_FA = 0, MAT_FB = 1024, MAT_FC = 3072, MAT_IC = 11264, MAT_IB = 19456,
-                   MAT_IA = 21504, MAT_BYTES = 22528;
-constexpr uint32_t SKF = SMAT + MAT_BYTES;    // 64 KB k_f' = (K_hat + D)/n, [f3 32][m_C 256] float2
-constexpr uint32_t STAB = SKF + 65536;        // two-level twiddle table (192 float2)
-constexpr uint32_t SMEM_BYTES = STAB + 1536 + 1024;  // + alignment slack
+// ---------------------------------------------------------------- smem map
+// inputs  : [buf][mb 2][kg 8][8 k][64 m] bf16 (16 KB per pair), kg 0-3 = u_b0
+//           t1 0..31, kg 4-7 = u_b1 (the TMA box order)
+// op      : 32 KB — Ar|Ai (stage B), Zr|Zi (stage B'), A' operand; one live
+// FA64    : stage-A block  [128 rows (f1 re|im)][64 k (t1<32 re|im)] K-major SW128
+// FR, FI  : DFT128 real / imaginary [128 rows][128 k] K-major SW128 (2 k-blocks)
+// GA64    : stage-A' block [64 rows (t1<32 re|im)][128 k (f1 re|im)] K-major SW128
+// KF      : k_f' [f1 64][f2 128] float2
+constexpr uint32_t SIN = 0;
+constexpr uint32_t SOP = SIN + 2 * 16384;
+constexpr uint32_t SMAT = SOP + 32768;
+constexpr uint32_t MAT_FA = 0, MAT_FR = 16384, MAT_FI = 49152, MAT_GA = 81920, MAT_BYTES = 98304;
+constexpr uint32_t SKF = SMAT + MAT_BYTES;
+constexpr uint32_t STAB = SKF + 65536;
+// 226 KB: the whole opt-in budget next to the 1 KB of static smem; the
+// extern buffer is declared __align__(1024) (checked at run time) so the
+// swizzled operands need no alignment slack.
+constexpr uint32_t SMEM_BYTES = STAB + 1536;
 
-// TMEM (512 columns allocated): each slot's stages share one 128-column
-// working region (an MMA starts only after the previous epilogue drained
-// it); the backward additionally holds F(dy) at 256 and the resident dK
-// spectrum accumulator S at 384.
-
-// element offsets of the MN-major operands
-__device__ __forceinline__ uint32_t sw128(uint32_t lin) { return lin ^ ((lin >> 3) & 0x70u); }
-// input pair layout [m/64][k/8][k%8][m%64] (the TMA box order)
-__device__ __forceinline__ uint32_t off_in(uint32_t m, uint32_t k) {
-  return sw128((m >> 6) * 2048 + (k >> 3) * 1024 + (k & 7) * 128 + (m & 63) * 2);
+__device__ __forceinline__ unsigned char* smem_base(unsigned char* raw) {
+  if (reinterpret_cast<uintptr_t>(raw) & 1023) __trap();  // swizzle atoms need 1 KB alignment
+  return raw;
 }
-// K = 32 operands, layout [k/8][m/64][k%8][m%64]
-__device__ __forceinline__ uint32_t off_mn(uint32_t m, uint32_t k) {
-  return sw128((k >> 3) * 8192 + (m >> 6) * 1024 + (k & 7) * 128 + (m & 63) * 2);
+
+// TMEM columns (512 allocated): W working region of every stage, R3 holds
+// F(dy) while F(u) runs (backward), R4 the resident dK spectrum S.
+constexpr uint32_t TW = 0, R3 = 128, R4 = 256;
+
+__host__ __device__ __forceinline__ uint32_t sw128(uint32_t lin) { return lin ^ ((lin >> 3) & 0x70u); }
+// MN-major B operand with N = 64: [kg][8 k][64 n]
+__host__ __device__ __forceinline__ uint32_t off_bmn(uint32_t n, uint32_t k) {
+  return sw128((k >> 3) * 1024 + (k & 7) * 128 + n * 2);
+}
+// K-major SW128 operand with 128-byte rows, K split in 64-element blocks of
+// `kblock` bytes: [k / 64][row / 8][row % 8][k % 64]
+__host__ __device__ __forceinline__ uint32_t off_kmaj(uint32_t row, uint32_t k, uint32_t kblock) {
+  return sw128((k >> 6) * kblock + (row >> 3) * 1024 + (row & 7) * 128 + (k & 63) * 2);
 }
 
 template <typename T>
 struct Fmt;
 template <>
 struct Fmt<__nv_bfloat16> {
-  static constexpr uint32_t ab = 1;  // UMMA a/b format BF16
+  static constexpr uint32_t ab = 1;
   static constexpr CUtensorMapDataType tma = CU_TENSOR_MAP_DATA_TYPE_BFLOAT16;
 };
 template <>
 struct Fmt<__half> {
-  static constexpr uint32_t ab = 0;  // F16
+  static constexpr uint32_t ab = 0;
   static constexpr CUtensorMapDataType tma = CU_TENSOR_MAP_DATA_TYPE_FLOAT16;
 };
 
 template <typename T>
-__host__ __device__ constexpr uint32_t idesc(uint32_t M, uint32_t N, bool a_mn) {
-  return (1u << 4) | (Fmt<T>::ab << 7) | (Fmt<T>::ab << 10) | ((a_mn ? 1u : 0u) << 15) |
-         ((N >> 3) << 17) | ((M >> 4) << 24);
+__host__ __device__ constexpr uint32_t idesc(uint32_t M, uint32_t N, bool a_mn, bool b_mn,
+                                             bool neg_a = false) {
+  return (1u << 4) | (Fmt<T>::ab << 7) | (Fmt<T>::ab << 10) | ((neg_a ? 1u : 0u) << 13) |
+         ((a_mn ? 1u : 0u) << 15) | ((b_mn ? 1u : 0u) << 16) | ((N >> 3) << 17) | ((M >> 4) << 24);
 }
 
-// Scatter of one register row into an MN-major [kg][mb][8][64] operand:
-// element (m = 32 q + t3, k) for q = 0..15 with the thread's t3 and k fixed
-// (re at k, im at k + 16).  With m >> 6 = q >> 1 and the 128B swizzle chunk
-// (4 (q & 1) + t3 / 8) ^ (k & 7), the 32 addresses reduce to two per-thread
-// bases plus compile-time immediates.
-template <typename T>
-__device__ __forceinline__ void scatter_mn(unsigned char* op, uint32_t t3, uint32_t k,
-                                           const float (&v)[32]) {
-  const uint32_t x = (t3 >> 3) ^ (k & 7);
-  unsigned char* b0 = op + (k >> 3) * 8192 + (k & 7) * 128 + (2 * t3 & 15) + 16 * x;
-  unsigned char* b1 = op + (k >> 3) * 8192 + (k & 7) * 128 + (2 * t3 & 15) + 16 * (x ^ 4);
-#pragma unroll
-  for (int q = 0; q < 16; ++q) {
-    unsigned char* b = (q & 1) ? b1 : b0;
-    *reinterpret_cast<T*>(b + (q >> 1) * 1024) = cvt<T>(v[q]);
-    *reinterpret_cast<T*>(b + (q >> 1) * 1024 + 16384) = cvt<T>(v[16 + q]);
-  }
-}
-// Scatter into the K-major SW128 C operand: rows r = 16 f1 + q (q = 0..15),
-// column k = t3 (re) and 32 + t3 (im); swizzle chunk ((k / 8) ^ (r & 7)).
-template <typename T>
-__device__ __forceinline__ void scatter_c(unsigned char* op, uint32_t f1, uint32_t t3,
-                                          const float (&v)[32]) {
-  const uint32_t c0 = t3 >> 3;
-  unsigned char* base = op + 2 * f1 * 1024 + (2 * t3 & 15);
-#pragma unroll
-  for (int q = 0; q < 16; ++q) {
-    unsigned char* r = base + (q >> 3) * 1024 + (q & 7) * 128;
-    *reinterpret_cast<T*>(r + 16 * (c0 ^ (q & 7))) = cvt<T>(v[q]);
-    *reinterpret_cast<T*>(r + 16 * ((c0 ^ 4) ^ (q & 7))) = cvt<T>(v[16 + q]);
-  }
-}
-
-template <typename T>
-__device__ __forceinline__ void st16(unsigned char* base, uint32_t off, float v) {
-  *reinterpret_cast<T*>(base + off) = cvt<T>(v);
-}
 template <typename T>
 __device__ __forceinline__ uint32_t pack2(float a, float b);
 template <>
@@ -135,7 +114,6 @@ __device__ __forceinline__ uint32_t pack2<__half>(float a, float b) {
   __half2 h = __floats2half2_rn(a, b);
   return *reinterpret_cast<uint32_t*>(&h);
 }
-// 8 consecutive values -> one 16-byte store
 template <typename T>
 __device__ __forceinline__ void st8(unsigned char* p, const float* v) {
   uint4 q;
@@ -146,7 +124,10 @@ __device__ __forceinline__ void st8(unsigned char* p, const float* v) {
   *reinterpret_cast<uint4*>(p) = q;
 }
 
-__device__ __forceinline__ void ld16(uint32_t taddr, float (&v)[16]) {
+template <int NC>
+__device__ __forceinline__ void tld(uint32_t taddr, float* v);
+template <>
+__device__ __forceinline__ void tld<16>(uint32_t taddr, float* v) {
   uint32_t* r = reinterpret_cast<uint32_t*>(v);
   asm volatile(
       "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,"
@@ -156,33 +137,22 @@ __device__ __forceinline__ void ld16(uint32_t taddr, float (&v)[16]) {
         "=r"(r[14]), "=r"(r[15])
       : "r"(taddr));
 }
-__device__ __forceinline__ void st32(uint32_t taddr, const float (&v)[32]) {
-  const uint32_t* r = reinterpret_cast<const uint32_t*>(v);
-  asm volatile(
-      "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,"
-      "%14,%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};" ::"r"(taddr),
-      "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]),
-      "r"(r[8]), "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]),
-      "r"(r[15]), "r"(r[16]), "r"(r[17]), "r"(r[18]), "r"(r[19]), "r"(r[20]), "r"(r[21]),
-      "r"(r[22]), "r"(r[23]), "r"(r[24]), "r"(r[25]), "r"(r[26]), "r"(r[27]), "r"(r[28]),
-      "r"(r[29]), "r"(r[30]), "r"(r[31])
-      : "memory");
-}
-__device__ __forceinline__ void ld8(uint32_t taddr, float* v) {
+template <>
+__device__ __forceinline__ void tld<8>(uint32_t taddr, float* v) {
   uint32_t* r = reinterpret_cast<uint32_t*>(v);
   asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
                : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]),
                  "=r"(r[6]), "=r"(r[7])
                : "r"(taddr));
 }
-__device__ __forceinline__ void st8t(uint32_t taddr, const float* v) {
+__device__ __forceinline__ void tst8(uint32_t taddr, const float* v) {
   const uint32_t* r = reinterpret_cast<const uint32_t*>(v);
   asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"r"(taddr),
                "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]),
                "r"(r[7])
                : "memory");
 }
-__device__ __forceinline__ void st_wait() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
+__device__ __forceinline__ void tst_wait() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
 
 __device__ __forceinline__ void tma_load_4d(void* dst, const CUtensorMap* map, int c0, int c1, int c2,
                                             int c3, uint64_t* bar) {
@@ -194,275 +164,212 @@ __device__ __forceinline__ void tma_load_4d(void* dst, const CUtensorMap* map, i
       : "memory");
 }
 
-// The 8 TMA boxes of one channel pair (b0, b0+1) of head h: box [64 m][8 t1]
-// [1 h][2 b] lands as [kgroup b][8 t1][64 m] = 2 KB per 64-row block.
+// Channel pair (b0, b0+1) of head h: 4 boxes [64 t2][32 t1] (4 KB each),
+// channel c of 64-row block mb at dst + mb * 8 KB + c * 4 KB.  An odd batch's
+// missing partner is out of bounds and arrives as zeros.
 __device__ __forceinline__ void load_pair(unsigned char* dst, const CUtensorMap* map, int h, int b0,
                                           uint64_t* bar) {
-  ptx::mbar_arrive_expect_tx(bar, 8 * 2048);
-  for (int mb = 0; mb < 8; ++mb) tma_load_4d(dst + mb * 2048, map, mb * 64, 0, h, b0, bar);
+  ptx::mbar_arrive_expect_tx(bar, 4 * 4096);
+#pragma unroll
+  for (int mb = 0; mb < 2; ++mb)
+#pragma unroll
+    for (int c = 0; c < 2; ++c) tma_load_4d(dst + mb * 8192 + c * 4096, map, mb * 64, 0, h, b0 + c, bar);
 }
 
-// --------------------------------------------------------------------------
-// Per-slot state and the stage sequence shared by the forward and backward
-// kernels.  The CTA's 16 warps form NSLOT independent slots (8 or 16 warps);
-// each slot runs its own channel pairs through the six stages with its own
-// operand buffer, TMEM region, barriers and named CTA barrier, so one slot's
-// epilogues overlap the other slot's tensor-core work and latencies.
-// Within a slot, warp w has TMEM lane slab s = w & 3; row tiles are
-// tile = gl + (WS / 4) * i for the thread's items i < NSLOT.
-// --------------------------------------------------------------------------
-// Thread coordinates re-read through volatile asm in every epilogue: they
-// are loop invariant, and letting the compiler hoist the ~100 derived smem
-// addresses out of the pair loop costs more registers than recomputing.
+// Thread coordinates re-read through volatile asm inside the epilogues (they
+// are loop invariant; hoisting the derived addresses costs more registers
+// than recomputing them).
 __device__ __forceinline__ uint32_t tid_v() {
   uint32_t t;
   asm volatile("mov.u32 %0, %%tid.x;" : "=r"(t));
   return t;
 }
-
-template <int NSLOT>
-struct Slot {
-  static constexpr uint32_t TS = kThreads / NSLOT;  // threads per slot
-  static constexpr uint32_t WS = TS / 32;           // warps per slot
-  static constexpr uint32_t GL = WS / 4;            // lane-slab groups per slot
-};
+// lane = TMEM row within the warp's slab, s = slab, g = column group (0..3)
+__device__ __forceinline__ void coords(uint32_t& row, uint32_t& g) {
+  const uint32_t t = tid_v();
+  row = 32 * ((t >> 5) & 3) + (t & 31);
+  g = t >> 7;
+}
 
 struct Ctx {
   unsigned char* sm;
-  uint32_t smb;    // shared address of sm
-  uint32_t tmem;   // TMEM base of this slot's region
-  uint32_t sop;    // smem offset of this slot's operand buffer
+  uint32_t smb;
+  uint32_t tmem;
   uint64_t* mma_bar;
   uint32_t mma_phase;
   const float2* tab;
-  uint32_t slot;
-  bool leader;     // issues this slot's MMAs
 };
 
+__device__ __forceinline__ uint32_t taddr(const Ctx& c, uint32_t col) {
+  return c.tmem + ((32u * ((tid_v() >> 5) & 3)) << 16) + col;
+}
+
+// make generic smem writes and TMEM reads visible before the next MMAs
+__device__ __forceinline__ void publish() {
+  ptx::fence_proxy_async_smem();
+  tc::fence_before();
+  __syncthreads();
+  tc::fence_after();
+}
 __device__ __forceinline__ void mma_wait(Ctx& c) {
   ptx::mbar_wait(c.mma_bar, c.mma_phase);
   c.mma_phase ^= 1;
   tc::fence_after();
 }
 
-template <int NSLOT>
-__device__ __forceinline__ void slot_sync(const Ctx& c) {
-  if constexpr (NSLOT == 1) {
-    __syncthreads();
-  } else {
-    asm volatile("bar.sync %0, %1;" ::"r"(1 + c.slot), "n"(Slot<NSLOT>::TS) : "memory");
+// ---------------------------------------------------------------- stages
+template <typename T>
+__device__ __forceinline__ void mma_stage_A(const Ctx& c, uint32_t in_off) {
+  const uint32_t id = idesc<T>(128, 128, true, false);
+#pragma unroll
+  for (uint32_t s = 0; s < 4; ++s) {
+    const uint64_t ad = tc::smem_desc(c.smb + in_off + s * 2048, 1024, tc::kSw128, 8192);
+    const uint64_t bd = tc::smem_desc(c.smb + SMAT + MAT_FA + s * 32, 1024, tc::kSw128);
+    tc::mma_bf16(c.tmem + TW, ad, bd, id, s);
+  }
+}
+// DFT128 with the data as the B operand (MN-major [kg][8][64] at SOP, re
+// plane then im plane 16 KB apart).  inverse: conjugate block.
+template <typename T, bool INV>
+__device__ __forceinline__ void mma_stage_B(const Ctx& c, uint32_t dcol) {
+  const uint32_t id_p = idesc<T>(128, 64, false, true, false);
+  const uint32_t id_n = idesc<T>(128, 64, false, true, true);
+  const uint32_t fr = c.smb + SMAT + MAT_FR, fi = c.smb + SMAT + MAT_FI;
+  const uint32_t br = c.smb + SOP, bi = c.smb + SOP + 16384;
+#pragma unroll
+  for (uint32_t s = 0; s < 8; ++s) {
+    const uint32_t ko = (s >> 2) * 16384 + (s & 3) * 32;
+    const uint64_t dr = tc::smem_desc(fr + ko, 1024, tc::kSw128);
+    const uint64_t di = tc::smem_desc(fi + ko, 1024, tc::kSw128);
+    const uint64_t xr = tc::smem_desc(br + s * 2048, 1024, tc::kSw128, 1024);
+    const uint64_t xi = tc::smem_desc(bi + s * 2048, 1024, tc::kSw128, 1024);
+    if (!INV) {
+      // re = Fr.Ar - Fi.Ai ; im = Fi.Ar + Fr.Ai
+      tc::mma_bf16(c.tmem + dcol, dr, xr, id_p, s);
+      tc::mma_bf16(c.tmem + dcol, di, xi, id_n, 1);
+      tc::mma_bf16(c.tmem + dcol + 64, di, xr, id_p, s);
+      tc::mma_bf16(c.tmem + dcol + 64, dr, xi, id_p, 1);
+    } else {
+      // conj(F) Z: re = Fr.Zr + Fi.Zi ; im = Fr.Zi - Fi.Zr
+      tc::mma_bf16(c.tmem + dcol, dr, xr, id_p, s);
+      tc::mma_bf16(c.tmem + dcol, di, xi, id_p, 1);
+      tc::mma_bf16(c.tmem + dcol + 64, dr, xi, id_p, s);
+      tc::mma_bf16(c.tmem + dcol + 64, di, xr, id_n, 1);
+    }
+  }
+}
+template <typename T>
+__device__ __forceinline__ void mma_stage_Ap(const Ctx& c) {
+  const uint32_t id = idesc<T>(128, 64, false, false);
+#pragma unroll
+  for (uint32_t s = 0; s < 8; ++s) {
+    const uint32_t ko = (s & 3) * 32;
+    const uint64_t ad = tc::smem_desc(c.smb + SOP + (s >> 2) * 16384 + ko, 1024, tc::kSw128);
+    const uint64_t bd = tc::smem_desc(c.smb + SMAT + MAT_GA + (s >> 2) * 8192 + ko, 1024, tc::kSw128);
+    tc::mma_bf16(c.tmem + TW, ad, bd, id, s);
   }
 }
 
-// make this slot's generic smem writes + TMEM reads visible to the
-// tensor-core (async) proxy before its leader issues the next MMAs
-template <int NSLOT>
-__device__ __forceinline__ void publish(const Ctx& c) {
-  ptx::fence_proxy_async_smem();
-  tc::fence_before();
-  slot_sync<NSLOT>(c);
-  tc::fence_after();
-}
-
 template <typename T>
-__device__ __forceinline__ void mma_A(const Ctx& c, uint32_t sa_off) {
-  // 4 M-tiles x (N 32, K 16): A = input pair (MN-major, LBO 2048, SBO 1024)
-  const uint32_t id = idesc<T>(128, 32, true);
-  const uint64_t bd = tc::smem_desc(c.smb + SMAT + MAT_FA, 256, tc::kSw32);
-  for (uint32_t t = 0; t < 4; ++t) {
-    const uint64_t ad = tc::smem_desc(c.smb + sa_off + t * 4096, 1024, tc::kSw128, 2048);
-    tc::mma_bf16(c.tmem + 32 * t, ad, bd, id, 0);
-  }
-}
-// K = 32, MN-major operand ([kg][mb][8][64]: LBO 1024, SBO 8192)
-template <typename T>
-__device__ __forceinline__ void mma_mn32(const Ctx& c, uint32_t mat, uint32_t N, uint32_t mat_sbo,
-                                         int mat_swz) {
-  const uint32_t id = idesc<T>(128, N, true);
-  for (uint32_t t = 0; t < 4; ++t)
-    for (uint32_t ks = 0; ks < 2; ++ks) {
-      const uint64_t ad = tc::smem_desc(c.smb + c.sop + t * 2048 + ks * 2 * 8192, 8192, tc::kSw128, 1024);
-      const uint64_t bd = tc::smem_desc(c.smb + SMAT + mat + ks * 32, mat_sbo, mat_swz);
-      tc::mma_bf16(c.tmem + N * t, ad, bd, id, ks);
-    }
-}
-// stage C / C': 2 M-tiles x (N 64, K 64), A K-major SW128 (256 x 128 B)
-template <typename T>
-__device__ __forceinline__ void mma_C(const Ctx& c, uint32_t mat, uint32_t dcol) {
-  const uint32_t id = idesc<T>(128, 64, false);
-  for (uint32_t t = 0; t < 2; ++t)
-    for (uint32_t ks = 0; ks < 4; ++ks) {
-      const uint64_t ad = tc::smem_desc(c.smb + c.sop + t * 16384 + ks * 32, 1024, tc::kSw128);
-      const uint64_t bd = tc::smem_desc(c.smb + SMAT + mat + ks * 32, 1024, tc::kSw128);
-      tc::mma_bf16(c.tmem + dcol + 64 * t, ad, bd, id, ks);
-    }
-}
-
-// thread coordinates within the slot: lane, slab s, group gl
-template <int NSLOT>
-__device__ __forceinline__ void coords(uint32_t& gl, uint32_t& s, uint32_t& lane) {
-  const uint32_t t = tid_v() % Slot<NSLOT>::TS;
-  lane = t & 31;
-  s = (t >> 5) & 3;
-  gl = t >> 7;
-}
-__device__ __forceinline__ uint32_t lane_addr(const Ctx& c, uint32_t col) {
-  return c.tmem + ((32u * ((tid_v() >> 5) & 3)) << 16) + col;
-}
-
-// (v[r], v[16 + r]) *= w
-__device__ __forceinline__ void cmul_at(float (&v)[32], int r, float2 w) {
-  const float a = v[r], b = v[16 + r];
-  v[r] = fmaf(a, w.x, -b * w.y);
-  v[16 + r] = fmaf(a, w.y, b * w.x);
-}
-// split re/im row: (v[r], v[16+r]) *= w^(r base), r = 1..15 — four table
-// lookups, the rest by products of depth <= 3
-template <int SIGN>
-__device__ __forceinline__ void twiddle16(float (&v)[32], const float2* tab, uint32_t base) {
-  const float2 w1 = tw2<SIGN>(tab, base), w2 = tw2<SIGN>(tab, 2 * base);
-  const float2 w4 = tw2<SIGN>(tab, 4 * base), w8 = tw2<SIGN>(tab, 8 * base);
-  const float2 w3 = cmul(w1, w2), w5 = cmul(w1, w4), w6 = cmul(w2, w4), w7 = cmul(w3, w4);
-  cmul_at(v, 1, w1);
-  cmul_at(v, 2, w2);
-  cmul_at(v, 3, w3);
-  cmul_at(v, 4, w4);
-  cmul_at(v, 5, w5);
-  cmul_at(v, 6, w6);
-  cmul_at(v, 7, w7);
-  cmul_at(v, 8, w8);
-  cmul_at(v, 9, cmul(w1, w8));
-  cmul_at(v, 10, cmul(w2, w8));
-  cmul_at(v, 11, cmul(w3, w8));
-  cmul_at(v, 12, cmul(w4, w8));
-  cmul_at(v, 13, cmul(w5, w8));
-  cmul_at(v, 14, cmul(w6, w8));
-  cmul_at(v, 15, cmul(w7, w8));
-}
-
-template <typename T, int NSLOT>
 __device__ __forceinline__ void issue(Ctx& c, int stage, uint32_t arg) {
-  publish<NSLOT>(c);
-  if (c.leader) {
+  publish();
+  if (threadIdx.x == 0) {
     switch (stage) {
-      case 0: mma_A<T>(c, arg); break;
-      case 1: mma_mn32<T>(c, MAT_FB, 32, 512, tc::kSw64); break;
-      case 2: mma_C<T>(c, MAT_FC, arg); break;
-      case 3: mma_C<T>(c, MAT_IC, 0); break;
-      case 4: mma_mn32<T>(c, MAT_IB, 32, 512, tc::kSw64); break;
-      default: mma_mn32<T>(c, MAT_IA, 16, 512, tc::kSw64); break;
+      case 0: mma_stage_A<T>(c, arg); break;
+      case 1: mma_stage_B<T, false>(c, arg); break;
+      case 2: mma_stage_B<T, true>(c, TW); break;
+      default: mma_stage_Ap<T>(c); break;
     }
     tc::commit(c.mma_bar);
   }
   mma_wait(c);
 }
 
-// Forward transform of the pair staged at sa_off (TMA barrier in_bar): X[f]
-// ends in the slot's TMEM cols dstC + 64 T (rows m_C; cols [re f3 0..15 |
-// im 0..15 | re 16..31 | im 16..31]).
-template <typename T, int NSLOT>
-__device__ __forceinline__ void forward_fft(Ctx& c, uint32_t sa_off, uint64_t* in_bar,
-                                            uint32_t in_phase, uint32_t dstC) {
-  using SL = Slot<NSLOT>;
-  ptx::mbar_wait(in_bar, in_phase);
-  issue<T, NSLOT>(c, 0, sa_off);
-  // ---- A -> B: twiddle w^(f1 m_A); B operand rows m_B = 32 f1 + t3, k = t2
-#pragma unroll 1
-  for (int i = 0; i < NSLOT; ++i) {
-    uint32_t gl, sl, lane;
-    coords<NSLOT>(gl, sl, lane);
-    const uint32_t tile = gl + SL::GL * i;
-    const uint32_t m = 128 * tile + 32 * sl + lane;  // = 32 t2 + t3
-    float v[32];
-    tc::ld32(lane_addr(c, 32 * tile), v);
-    tc::ld_wait();
-    twiddle16<-1>(v, c.tab, m);
-    scatter_mn<T>(c.sm + c.sop, lane, m >> 5, v);
+// (re[j], im[j]) *= w^((off + j) base), j = 0..15, from the two-level table
+template <int SIGN>
+__device__ __forceinline__ void twiddle_row(float* re, float* im, const float2* tab, uint32_t base,
+                                            uint32_t off) {
+  const float2 c0 = tw2<SIGN>(tab, off * base);
+  const float2 w1 = tw2<SIGN>(tab, base), w2 = tw2<SIGN>(tab, 2 * base);
+  const float2 w4 = tw2<SIGN>(tab, 4 * base), w8 = tw2<SIGN>(tab, 8 * base);
+  const float2 w3 = cmul(w1, w2), w5 = cmul(w1, w4), w6 = cmul(w2, w4), w7 = cmul(w3, w4);
+  const float2 ws[8] = {make_float2(1.f, 0.f), w1, w2, w3, w4, w5, w6, w7};
+  const float2 c8 = cmul(c0, w8);
+#pragma unroll
+  for (int j = 0; j < 16; ++j) {
+    const float2 w = cmul(j < 8 ? c0 : c8, ws[j & 7]);
+    const float a = re[j], b = im[j];
+    re[j] = fmaf(a, w.x, -b * w.y);
+    im[j] = fmaf(a, w.y, b * w.x);
   }
-  issue<T, NSLOT>(c, 1, 0);
-  // ---- B -> C: twiddle w_512^(f2 t3); C operand rows m_C = 16 f1 + f2, k = t3
-#pragma unroll 1
-  for (int i = 0; i < NSLOT; ++i) {
-    uint32_t gl, sl, lane;
-    coords<NSLOT>(gl, sl, lane);
-    const uint32_t tile = gl + SL::GL * i;
-    const uint32_t mB = 128 * tile + 32 * sl + lane;  // = 32 f1 + t3
-    float v[32];
-    tc::ld32(lane_addr(c, 32 * tile), v);
-    tc::ld_wait();
-    twiddle16<-1>(v, c.tab, 16 * lane);
-    scatter_c<T>(c.sm + c.sop, mB >> 5, lane, v);
-  }
-  issue<T, NSLOT>(c, 2, dstC);
 }
 
-// C-exit item i of this thread: spectrum row m_C and half h.
-template <int NSLOT>
-__device__ __forceinline__ void c_item(int i, uint32_t& mC, uint32_t& h) {
-  uint32_t gl, sl, lane;
-  coords<NSLOT>(gl, sl, lane);
-  const uint32_t combo = gl + Slot<NSLOT>::GL * i;  // (T, h) = (combo & 1, combo >> 1)
-  mC = 128 * (combo & 1) + 32 * sl + lane;
-  h = combo >> 1;
-}
-
-// Write the row half (re v[0..15], im v[16..31] at f3 = 16h + j) as the C'
-// operand (K-major SW128, k = [re f3 | im f3]).
+// Forward transform of the pair staged at in_off: X[f1 + 64 f2] ends in TMEM
+// cols dstB (re, f1 0..63) and dstB + 64 (im), lane = f2.
 template <typename T>
-__device__ __forceinline__ void write_cprime(const Ctx& c, uint32_t mC, uint32_t h, const float (&v)[32]) {
-  unsigned char* op = c.sm + c.sop;
-  st8<T>(op + tc::kmajor_off<tc::kSw128>(mC, 16 * h), v);
-  st8<T>(op + tc::kmajor_off<tc::kSw128>(mC, 16 * h + 8), v + 8);
-  st8<T>(op + tc::kmajor_off<tc::kSw128>(mC, 32 + 16 * h), v + 16);
-  st8<T>(op + tc::kmajor_off<tc::kSw128>(mC, 32 + 16 * h + 8), v + 24);
+__device__ __forceinline__ void forward_fft(Ctx& c, uint32_t in_off, uint64_t* in_bar,
+                                            uint32_t in_phase, uint32_t dstB) {
+  ptx::mbar_wait(in_bar, in_phase);
+  issue<T>(c, 0, in_off);
+  // ---- A -> B: w^(f1 t2); Ar/Ai[k = t2][n = f1]
+  {
+    uint32_t t2, g;
+    coords(t2, g);
+    float re[16], im[16];
+    tld<16>(taddr(c, TW + 16 * g), re);
+    tld<16>(taddr(c, TW + 64 + 16 * g), im);
+    tc::ld_wait();
+    twiddle_row<-1>(re, im, c.tab, t2, 16 * g);
+    unsigned char* op = c.sm + SOP;
+    st8<T>(op + off_bmn(16 * g, t2), re);
+    st8<T>(op + off_bmn(16 * g + 8, t2), re + 8);
+    st8<T>(op + 16384 + off_bmn(16 * g, t2), im);
+    st8<T>(op + 16384 + off_bmn(16 * g + 8, t2), im + 8);
+  }
+  issue<T>(c, 1, dstB);
 }
 
-// Inverse transform from the C' operand; leaves z[t] (t1 < 8) in the slot's
-// TMEM cols 16 T + [re t1 0..7 | im t1 0..7] of row block T.
-template <typename T, int NSLOT>
+// Inverse from Zr/Zi (MN-major in SOP); leaves z[128 t1 + t2] (t1 < 32) in
+// TMEM cols TW + t1 (re) / TW + 32 + t1 (im), lane = t2.
+template <typename T>
 __device__ __forceinline__ void inverse_fft(Ctx& c) {
-  using SL = Slot<NSLOT>;
-  issue<T, NSLOT>(c, 3, 0);
-  // ---- C' -> B': twiddle w_512^(-f2 t3); B' operand rows m_B = 32 f1 + t3, k = f2
-#pragma unroll 1
-  for (int i = 0; i < NSLOT; ++i) {
-    uint32_t mC, h;
-    c_item<NSLOT>(i, mC, h);
-    const uint32_t f1 = mC >> 4, f2 = mC & 15;
-    float v[32];
-    tc::ld32(lane_addr(c, 64 * (mC >> 7) + 32 * h), v);
+  issue<T>(c, 2, 0);
+  // ---- B' -> A': w^(-f1 t2); A' operand row t2, k = f1 (re) / 64 + f1 (im)
+  {
+    uint32_t t2, g;
+    coords(t2, g);
+    float re[16], im[16];
+    tld<16>(taddr(c, TW + 16 * g), re);
+    tld<16>(taddr(c, TW + 64 + 16 * g), im);
     tc::ld_wait();
-    twiddle16<+1>(v, c.tab, 16 * f2);
-    if (h) {
-      const float2 w = tw2<+1>(c.tab, 256 * f2);
-#pragma unroll
-      for (int j = 0; j < 16; ++j) cmul_at(v, j, w);
-    }
-    unsigned char* op = c.sm + c.sop;
-    const uint32_t m0 = 32 * f1 + 16 * h;
-    st8<T>(op + off_mn(m0, f2), v);
-    st8<T>(op + off_mn(m0 + 8, f2), v + 8);
-    st8<T>(op + off_mn(m0, 16 + f2), v + 16);
-    st8<T>(op + off_mn(m0 + 8, 16 + f2), v + 24);
+    twiddle_row<+1>(re, im, c.tab, t2, 16 * g);
+    unsigned char* op = c.sm + SOP;
+    st8<T>(op + off_kmaj(t2, 16 * g, 16384), re);
+    st8<T>(op + off_kmaj(t2, 16 * g + 8, 16384), re + 8);
+    st8<T>(op + off_kmaj(t2, 64 + 16 * g, 16384), im);
+    st8<T>(op + off_kmaj(t2, 64 + 16 * g + 8, 16384), im + 8);
   }
-  issue<T, NSLOT>(c, 4, 0);
-  // ---- B' -> A': twiddle w^(-f1 (32 t2 + t3)); A' operand rows m_A = 32 t2 + t3, k = f1
-#pragma unroll 1
-  for (int i = 0; i < NSLOT; ++i) {
-    uint32_t gl, sl, lane;
-    coords<NSLOT>(gl, sl, lane);
-    const uint32_t tile = gl + SL::GL * i;
-    const uint32_t f1 = (128 * tile + 32 * sl + lane) >> 5;  // m_B = 32 f1 + t3
-    float v[32];
-    tc::ld32(lane_addr(c, 32 * tile), v);
-    tc::ld_wait();
-    twiddle16<+1>(v, c.tab, 32 * f1);
-    const float2 w = tw2<+1>(c.tab, f1 * lane);
+  issue<T>(c, 3, 0);
+}
+
+// A' exit: rows t2, z[128 t1 + t2] for t1 = 8 g + j (re -> b0, im -> b1)
+template <typename T>
+__device__ __forceinline__ void store_rows(const Ctx& c, T* __restrict__ out, int b0, int B, int H,
+                                           int h) {
+  uint32_t t2, g;
+  coords(t2, g);
+  float re[8], im[8];
+  tld<8>(taddr(c, TW + 8 * g), re);
+  tld<8>(taddr(c, TW + 32 + 8 * g), im);
+  tc::ld_wait();
+  T* o0 = out + ((size_t)b0 * H + h) * 4096 + 128 * (8 * g) + t2;
 #pragma unroll
-    for (int t2 = 0; t2 < 16; ++t2) cmul_at(v, t2, w);
-    scatter_mn<T>(c.sm + c.sop, lane, f1, v);
+  for (int j = 0; j < 8; ++j) o0[128 * j] = cvt<T>(re[j]);
+  if (b0 + 1 < B) {
+    T* o1 = out + ((size_t)(b0 + 1) * H + h) * 4096 + 128 * (8 * g) + t2;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) o1[128 * j] = cvt<T>(im[j]);
   }
-  issue<T, NSLOT>(c, 5, 0);
 }
 
 __device__ __forceinline__ void setup(Ctx& c, unsigned char* sm, uint32_t* tmem_slot, uint64_t* bars,
@@ -472,6 +379,8 @@ __device__ __forceinline__ void setup(Ctx& c, unsigned char* sm, uint32_t* tmem_
   c.sm = sm;
   c.smb = ptx::smem_u32(sm);
   c.tab = reinterpret_cast<const float2*>(sm + STAB);
+  c.mma_bar = &bars[0];
+  c.mma_phase = 0;
   if (threadIdx.x < 32) tc::alloc<512>(tmem_slot);
   if (threadIdx.x == 0) {
     for (int i = 0; i < nbars; ++i) ptx::mbar_init(&bars[i], 1);
@@ -488,216 +397,176 @@ __device__ __forceinline__ void setup(Ctx& c, unsigned char* sm, uint32_t* tmem_
   tc::fence_before();
   __syncthreads();
   tc::fence_after();
+  c.tmem = *tmem_slot;
 }
 
-__device__ __forceinline__ void teardown(uint32_t tmem_base) {
+__device__ __forceinline__ void teardown(const Ctx& c) {
   tc::fence_before();
   __syncthreads();
-  if (threadIdx.x < 32) tc::dealloc<512>(tmem_base);
+  if (threadIdx.x < 32) tc::dealloc<512>(c.tmem);
 }
 
-// A' exit: rows m_A, z[512 t1 + m_A] for t1 < 8 (re -> channel b0, im -> b1).
-template <typename T, int NSLOT>
-__device__ __forceinline__ void store_rows(const Ctx& c, T* __restrict__ out, int b0, int B, int H,
-                                           int h) {
-#pragma unroll 1
-  for (int i = 0; i < NSLOT; ++i) {
-    uint32_t gl, sl, lane;
-    coords<NSLOT>(gl, sl, lane);
-    const uint32_t tile = gl + Slot<NSLOT>::GL * i;
-    const uint32_t mA = 128 * tile + 32 * sl + lane;
-    float v[16];
-    ld16(lane_addr(c, 16 * tile), v);
-    tc::ld_wait();
-    T* o0 = out + ((size_t)b0 * H + h) * 4096 + mA;
-#pragma unroll
-    for (int t1 = 0; t1 < 8; ++t1) o0[512 * t1] = cvt<T>(v[t1]);
-    if (b0 + 1 < B) {
-      T* o1 = out + ((size_t)(b0 + 1) * H + h) * 4096 + mA;
-#pragma unroll
-      for (int t1 = 0; t1 < 8; ++t1) o1[512 * t1] = cvt<T>(v[8 + t1]);
-    }
-  }
-}
-
-template <int NSLOT>
-__device__ __forceinline__ void pair_end(const Ctx& c) {
+__device__ __forceinline__ void pair_end() {
   tc::fence_before();
-  slot_sync<NSLOT>(c);
+  __syncthreads();
   tc::fence_after();
 }
 
 // ------------------------------------------------------------------ forward
-// y = F^-1(F(u) * (K_hat + D)/n): the skip term D u is folded into the
-// spectrum (a D-weighted delta kernel), so the epilogue only streams y out.
-// Two slots of 8 warps each process alternate channel pairs.
-constexpr int kFwdSlots = 2;
-
 template <typename T>
 __global__ void __launch_bounds__(kThreads, 1)
     tc_fwd_kernel(const __grid_constant__ CUtensorMap umap, T* __restrict__ y,
                   const float2* __restrict__ kfp, const uint4* __restrict__ mats,
                   const float2* __restrict__ tab_g, int B, int H, int ppc) {
-  constexpr int NS = kFwdSlots;
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   __shared__ uint32_t tmem_slot;
-  __shared__ __align__(8) uint64_t bars[2 * NS];  // [slot]: mma, input
-  unsigned char* sm = reinterpret_cast<unsigned char*>(
-      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  __shared__ __align__(8) uint64_t bars[3];  // 0: mma, 1/2: input buffers
+  unsigned char* sm = smem_base(smem_raw);
   const int h = blockIdx.x;
   const int npairs = (B + 1) / 2;
   const int p0 = blockIdx.y * ppc, p1 = min(npairs, p0 + ppc);
   if (p0 >= p1) return;
   Ctx c;
-  setup(c, sm, &tmem_slot, bars, 2 * NS, mats, kfp + (size_t)h * kN, tab_g);
-  const uint32_t slot = threadIdx.x / Slot<NS>::TS;
-  c.slot = slot;
-  c.leader = (threadIdx.x % Slot<NS>::TS) == 0;
-  c.tmem = tmem_slot + 256 * slot;
-  c.sop = SOP + 32768 * slot;
-  c.mma_bar = &bars[2 * slot];
-  c.mma_phase = 0;
-  uint64_t* in_bar = &bars[2 * slot + 1];
-  const uint32_t sin = SIN + 16384 * slot;
+  setup(c, sm, &tmem_slot, bars, 3, mats, kfp + (size_t)h * kN, tab_g);
   const float2* kfs = reinterpret_cast<const float2*>(sm + SKF);
-  if (c.leader && p0 + (int)slot < p1) load_pair(sm + sin, &umap, h, 2 * (p0 + slot), in_bar);
-  uint32_t in_phase = 0;
-  for (int pr = p0 + slot; pr < p1; pr += NS) {
-    forward_fft<T, NS>(c, sin, in_bar, in_phase, 0);
-    in_phase ^= 1;
-    // stage A consumed the input: prefetch this slot's next pair
-    if (c.leader && pr + NS < p1) load_pair(sm + sin, &umap, h, 2 * (pr + NS), in_bar);
-    // ---- C exit: Z = X * k_f'  -> C' operand
-#pragma unroll 1
-    for (int i = 0; i < NS; ++i) {
-      uint32_t mC, hh;
-      c_item<NS>(i, mC, hh);
-      float v[32];
-      tc::ld32(lane_addr(c, 64 * (mC >> 7) + 32 * hh), v);
+  if (threadIdx.x == 0) load_pair(sm + SIN, &umap, h, 2 * p0, &bars[1]);
+  for (int pr = p0, it = 0; pr < p1; ++pr, ++it) {
+    const int buf = it & 1;
+    // the other buffer's last reader (stage A of the previous pair) is done
+    if (threadIdx.x == 0 && pr + 1 < p1)
+      load_pair(sm + SIN + (buf ^ 1) * 16384, &umap, h, 2 * (pr + 1), &bars[1 + (buf ^ 1)]);
+    forward_fft<T>(c, SIN + buf * 16384, &bars[1 + buf], (it >> 1) & 1, TW);
+    // ---- B exit: Z = X * k_f' -> Zr/Zi[k = f2][n = f1]
+    {
+      uint32_t f2, g;
+      coords(f2, g);
+      float re[16], im[16];
+      tld<16>(taddr(c, TW + 16 * g), re);
+      tld<16>(taddr(c, TW + 64 + 16 * g), im);
       tc::ld_wait();
-      const float2* kr = kfs + (16 * hh) * 256 + mC;
+      const float2* kr = kfs + (16 * g) * 128 + f2;
 #pragma unroll
-      for (int j = 0; j < 16; ++j) cmul_at(v, j, kr[j * 256]);
-      write_cprime<T>(c, mC, hh, v);
+      for (int j = 0; j < 16; ++j) {
+        const float2 k = kr[j * 128];
+        const float a = re[j], b = im[j];
+        re[j] = fmaf(a, k.x, -b * k.y);
+        im[j] = fmaf(a, k.y, b * k.x);
+      }
+      unsigned char* op = c.sm + SOP;
+      st8<T>(op + off_bmn(16 * g, f2), re);
+      st8<T>(op + off_bmn(16 * g + 8, f2), re + 8);
+      st8<T>(op + 16384 + off_bmn(16 * g, f2), im);
+      st8<T>(op + 16384 + off_bmn(16 * g + 8, f2), im + 8);
     }
-    inverse_fft<T, NS>(c);
-    store_rows<T, NS>(c, y, 2 * pr, B, H, h);
-    pair_end<NS>(c);
+    inverse_fft<T>(c);
+    store_rows<T>(c, y, 2 * pr, B, H, h);
+    pair_end();
   }
-  teardown(tmem_slot);
+  teardown(c);
 }
 
 // ------------------------------------------------------------------ backward
-// Per pair: DY = F(dy) (held in TMEM R3), U = F(u); S += conj(U) DY with S
-// resident in TMEM R4; du = F^-1(DY conj(k_f')) (skip folded).  S of the
-// CTA's pairs is written in natural frequency order for the finalize kernel
-// (dKbar = Re F^-1(S)/n; dD = dKbar[0]).
+// Per pair: DY = F(dy) (kept in TMEM R3), U = F(u); S += conj(U) DY with S
+// resident in TMEM R4 for the CTA's whole run; du = F^-1(DY conj(k_f')).
+// S is written in natural order for the finalize kernel (dKbar =
+// Re F^-1(S)/n, dD = dKbar[0]).
 template <typename T>
 __global__ void __launch_bounds__(kThreads, 1)
     tc_bwd_kernel(const __grid_constant__ CUtensorMap dymap, const __grid_constant__ CUtensorMap umap,
                   T* __restrict__ du, const float2* __restrict__ kfp, const uint4* __restrict__ mats,
                   const float2* __restrict__ tab_g, float2* __restrict__ spart, int B, int H,
                   int ppc) {
-  constexpr int NS = 1;
-  constexpr uint32_t R3 = 256, R4 = 384;
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   __shared__ uint32_t tmem_slot;
-  __shared__ __align__(8) uint64_t bars[5];  // 0: mma, 1/2: dy buffers, 3/4: u buffers
-  unsigned char* sm = reinterpret_cast<unsigned char*>(
-      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  __shared__ __align__(8) uint64_t bars[3];  // 0: mma, 1: dy, 2: u
+  unsigned char* sm = smem_base(smem_raw);
   const int h = blockIdx.x, chunk = blockIdx.y, chunks = gridDim.y;
   const int npairs = (B + 1) / 2;
   const int p0 = chunk * ppc, p1 = min(npairs, p0 + ppc);
   Ctx c;
-  setup(c, sm, &tmem_slot, bars, 5, mats, kfp + (size_t)h * kN, tab_g);
-  c.slot = 0;
-  c.leader = threadIdx.x == 0;
-  c.tmem = tmem_slot;
-  c.sop = SOP;
-  c.mma_bar = &bars[0];
-  c.mma_phase = 0;
+  setup(c, sm, &tmem_slot, bars, 3, mats, kfp + (size_t)h * kN, tab_g);
   const float2* kfs = reinterpret_cast<const float2*>(sm + SKF);
-  uint32_t mC, hh;
-  c_item<NS>(0, mC, hh);
-  const uint32_t scol = R4 + 64 * (mC >> 7) + 32 * hh;
   {
-    float z[32];
+    uint32_t f2, g;
+    coords(f2, g);
+    float z[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
 #pragma unroll
-    for (int i = 0; i < 32; ++i) z[i] = 0.f;
-    st32(lane_addr(c, scol), z);
-    st_wait();
+    for (int q = 0; q < 2; ++q) {
+      tst8(taddr(c, R4 + 16 * g + 8 * q), z);
+      tst8(taddr(c, R4 + 64 + 16 * g + 8 * q), z);
+    }
+    tst_wait();
   }
-  // buffers: dy[b] at SIN + b * 32 KB, u[b] at SIN + b * 32 KB + 16 KB
+  // dy at SIN, u at SIN + 16 KB (single-buffered: each is refilled as soon
+  // as its stage-A MMA has consumed it)
   if (threadIdx.x == 0 && p0 < p1) {
     load_pair(sm + SIN, &dymap, h, 2 * p0, &bars[1]);
-    load_pair(sm + SIN + 16384, &umap, h, 2 * p0, &bars[3]);
+    load_pair(sm + SIN + 16384, &umap, h, 2 * p0, &bars[2]);
   }
   for (int pr = p0, it = 0; pr < p1; ++pr, ++it) {
-    const int buf = it & 1;
-    const uint32_t ph = (it >> 1) & 1;
-    if (threadIdx.x == 0 && pr + 1 < p1) {
-      load_pair(sm + SIN + (buf ^ 1) * 32768, &dymap, h, 2 * (pr + 1), &bars[1 + (buf ^ 1)]);
-      load_pair(sm + SIN + (buf ^ 1) * 32768 + 16384, &umap, h, 2 * (pr + 1), &bars[3 + (buf ^ 1)]);
-    }
-    forward_fft<T, NS>(c, SIN + buf * 32768, &bars[1 + buf], ph, R3);
-    forward_fft<T, NS>(c, SIN + buf * 32768 + 16384, &bars[3 + buf], ph, 0);
+    const uint32_t ph = it & 1;
+    const bool more = pr + 1 < p1;
+    forward_fft<T>(c, SIN, &bars[1], ph, R3);
+    if (threadIdx.x == 0 && more) load_pair(sm + SIN, &dymap, h, 2 * (pr + 1), &bars[1]);
+    forward_fft<T>(c, SIN + 16384, &bars[2], ph, TW);
+    if (threadIdx.x == 0 && more) load_pair(sm + SIN + 16384, &umap, h, 2 * (pr + 1), &bars[2]);
     {
-      // in two quarters of 8 frequencies to keep U, DY, S register-light
-      const uint32_t cu = 64 * (mC >> 7) + 32 * hh, cg = R3 + 64 * (mC >> 7) + 32 * hh;
-      const float2* kr = kfs + (16 * hh) * 256 + mC;
-      unsigned char* op = c.sm + c.sop;
+      uint32_t f2, g;
+      coords(f2, g);
+      const float2* kr = kfs + (16 * g) * 128 + f2;
+      unsigned char* op = c.sm + SOP;
 #pragma unroll
       for (int q = 0; q < 2; ++q) {
+        const uint32_t col = 16 * g + 8 * q;
         float ur[8], ui[8], gr[8], gi[8], sr[8], si[8];
-        ld8(lane_addr(c, cu + 8 * q), ur);
-        ld8(lane_addr(c, cu + 16 + 8 * q), ui);
-        ld8(lane_addr(c, cg + 8 * q), gr);
-        ld8(lane_addr(c, cg + 16 + 8 * q), gi);
-        ld8(lane_addr(c, scol + 8 * q), sr);
-        ld8(lane_addr(c, scol + 16 + 8 * q), si);
+        tld<8>(taddr(c, TW + col), ur);
+        tld<8>(taddr(c, TW + 64 + col), ui);
+        tld<8>(taddr(c, R3 + col), gr);
+        tld<8>(taddr(c, R3 + 64 + col), gi);
+        tld<8>(taddr(c, R4 + col), sr);
+        tld<8>(taddr(c, R4 + 64 + col), si);
         tc::ld_wait();
 #pragma unroll
         for (int j = 0; j < 8; ++j) {
-          // S += conj(U) DY
-          sr[j] = fmaf(ur[j], gr[j], fmaf(ui[j], gi[j], sr[j]));
+          sr[j] = fmaf(ur[j], gr[j], fmaf(ui[j], gi[j], sr[j]));   // S += conj(U) DY
           si[j] = fmaf(ur[j], gi[j], fmaf(-ui[j], gr[j], si[j]));
-          // Z = DY conj(k_f')
-          const float2 k = kr[(8 * q + j) * 256];
+          const float2 k = kr[(8 * q + j) * 128];                  // Z = DY conj(k_f')
           ur[j] = fmaf(gr[j], k.x, gi[j] * k.y);
           ui[j] = fmaf(gi[j], k.x, -gr[j] * k.y);
         }
-        st8t(lane_addr(c, scol + 8 * q), sr);
-        st8t(lane_addr(c, scol + 16 + 8 * q), si);
-        st8<T>(op + tc::kmajor_off<tc::kSw128>(mC, 16 * hh + 8 * q), ur);
-        st8<T>(op + tc::kmajor_off<tc::kSw128>(mC, 32 + 16 * hh + 8 * q), ui);
+        tst8(taddr(c, R4 + col), sr);
+        tst8(taddr(c, R4 + 64 + col), si);
+        st8<T>(op + off_bmn(col, f2), ur);
+        st8<T>(op + 16384 + off_bmn(col, f2), ui);
       }
-      st_wait();
+      tst_wait();
     }
-    inverse_fft<T, NS>(c);
-    store_rows<T, NS>(c, du, 2 * pr, B, H, h);
-    pair_end<NS>(c);
+    inverse_fft<T>(c);
+    store_rows<T>(c, du, 2 * pr, B, H, h);
+    pair_end();
   }
   {
-    float S[32];
-    tc::ld32(lane_addr(c, scol), S);
+    uint32_t f2, g;
+    coords(f2, g);
+    float sr[16], si[16];
+    tld<16>(taddr(c, R4 + 16 * g), sr);
+    tld<16>(taddr(c, R4 + 64 + 16 * g), si);
     tc::ld_wait();
-    float2* sp = spart + ((size_t)h * chunks + chunk) * kN;
-    const uint32_t f1 = mC >> 4, f2 = mC & 15;
+    float2* sp = spart + ((size_t)h * chunks + chunk) * kN + 64 * f2 + 16 * g;
 #pragma unroll
-    for (int j = 0; j < 16; ++j) sp[f1 + 16 * f2 + 256 * (16 * hh + j)] = make_float2(S[j], S[16 + j]);
+    for (int j = 0; j < 16; ++j) sp[j] = make_float2(sr[j], si[j]);
   }
-  teardown(tmem_slot);
+  teardown(c);
 }
 
-// k_f (natural order, / n) -> [h][f3][m_C], m_C = 16 f1 + f2, f = f1 + 16 f2 + 256 f3
-// plus the skip gain folded in as a flat spectrum: k_f' = k_f + D / n
+// k_f (natural order, / n) -> [h][f1][f2] (f = f1 + 64 f2) with the skip
+// gain folded in as a flat spectrum: k_f' = k_f + D / n
 __global__ void permute_kf_kernel(const float2* __restrict__ kf, const float* __restrict__ D,
                                   float2* __restrict__ kfp, int H) {
   const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= (uint32_t)H * kN) return;
-  const uint32_t h = i / kN, r = i % kN, f3 = r / 256, mC = r % 256;
-  const uint32_t f = (mC >> 4) + 16 * (mC & 15) + 256 * f3;
-  float2 v = kf[(size_t)h * kN + f];
+  const uint32_t h = i / kN, r = i % kN, f1 = r / 128, f2 = r % 128;
+  float2 v = kf[(size_t)h * kN + f1 + 64 * f2];
   v.x += __ldg(D + h) * (1.0f / (float)kN);
   kfp[i] = v;
 }
@@ -716,66 +585,47 @@ namespace {
 
 using namespace tcfft;
 
-// dense real-stacked DFT block in its K-major swizzled smem image
 template <typename T>
-void put(std::vector<uint8_t>& img, uint32_t base, int swz, uint32_t row, uint32_t k, double v) {
-  uint32_t off;
-  if (swz == tc::kSw32) off = tc::kmajor_off<tc::kSw32>(row, k);
-  else if (swz == tc::kSw64) off = tc::kmajor_off<tc::kSw64>(row, k);
-  else off = tc::kmajor_off<tc::kSw128>(row, k);
+void put(std::vector<uint8_t>& img, uint32_t off, double v) {
   T h;
   if constexpr (std::is_same<T, __nv_bfloat16>::value) h = __float2bfloat16_rn((float)v);
   else h = __float2half_rn((float)v);
-  std::memcpy(&img[base + off], &h, 2);
-}
-
-// out-rows / in-cols of a complex block given by callback M(o, i) -> (re, im);
-// K order [re in 0..KI-1 | im in 0..KI-1]; N order given by nmap(row) ->
-// (output index, is_imag).
-template <typename T, class MF, class NM>
-void build_block(std::vector<uint8_t>& img, uint32_t base, int swz, int KI, int NROWS, MF M, NM nmap) {
-  for (int r = 0; r < NROWS; ++r) {
-    int o;
-    bool imag;
-    nmap(r, o, imag);
-    for (int i = 0; i < KI; ++i) {
-      double mr, mi;
-      M(o, i, mr, mi);
-      if (!imag) {
-        put<T>(img, base, swz, r, i, mr);
-        put<T>(img, base, swz, r, KI + i, -mi);
-      } else {
-        put<T>(img, base, swz, r, i, mi);
-        put<T>(img, base, swz, r, KI + i, mr);
-      }
-    }
-  }
+  std::memcpy(&img[off], &h, 2);
 }
 
 template <typename T>
 std::vector<uint8_t> build_mats() {
   std::vector<uint8_t> img(MAT_BYTES, 0);
-  auto dft = [](int r, double sign) {
-    return [r, sign](int o, int i, double& re, double& im) {
-      const double a = sign * 2.0 * M_PI * (double)((o * i) % r) / (double)r;
-      re = std::cos(a);
-      im = std::sin(a);
-    };
-  };
-  // natural N order: rows [re 0..n-1 | im 0..n-1]
-  auto nat = [](int n) { return [n](int r, int& o, bool& im) { o = r % n; im = r >= n; }; };
-  // 32-output blocks split in halves: [re 0..15 | im 0..15 | re 16..31 | im 16..31]
-  auto halves = [](int r, int& o, bool& im) {
-    const int hblk = r / 32, q = r % 32;
-    o = 16 * hblk + (q % 16);
-    im = q >= 16;
-  };
-  build_block<T>(img, MAT_FA, tc::kSw32, 8, 32, dft(16, -1.0), nat(16));   // t1 < 8 only
-  build_block<T>(img, MAT_FB, tc::kSw64, 16, 32, dft(16, -1.0), nat(16));
-  build_block<T>(img, MAT_FC, tc::kSw128, 32, 64, dft(32, -1.0), halves);
-  build_block<T>(img, MAT_IC, tc::kSw128, 32, 64, dft(32, +1.0), halves);
-  build_block<T>(img, MAT_IB, tc::kSw64, 16, 32, dft(16, +1.0), nat(16));
-  build_block<T>(img, MAT_IA, tc::kSw64, 16, 16, dft(16, +1.0), nat(8));  // t1 < 8 only
+  // stage A: rows f1 re (0..63) | im (64..127); k t1 re (0..31) | im (32..63)
+  for (int r = 0; r < 128; ++r) {
+    const int f1 = r % 64;
+    const bool imag = r >= 64;
+    for (int t1 = 0; t1 < 32; ++t1) {
+      const double a = -2.0 * M_PI * (double)((f1 * t1) % 64) / 64.0;
+      const double fr = std::cos(a), fi = std::sin(a);
+      put<T>(img, MAT_FA + off_kmaj(r, t1, 0), imag ? fi : fr);
+      put<T>(img, MAT_FA + off_kmaj(r, 32 + t1, 0), imag ? fr : -fi);
+    }
+  }
+  // DFT128: Fr[f2][t2] = cos, Fi = -sin (symmetric; also serves the inverse)
+  for (int r = 0; r < 128; ++r)
+    for (int k = 0; k < 128; ++k) {
+      const double a = -2.0 * M_PI * (double)((r * k) % 128) / 128.0;
+      put<T>(img, MAT_FR + off_kmaj(r, k, 16384), std::cos(a));
+      put<T>(img, MAT_FI + off_kmaj(r, k, 16384), std::sin(a));
+    }
+  // stage A': rows t1 re (0..31) | im (32..63); k f1 re (0..63) | im (64..127);
+  // G = conj(F64): z = G w  ->  re row [Gr | -Gi], im row [Gi | Gr]
+  for (int r = 0; r < 64; ++r) {
+    const int t1 = r % 32;
+    const bool imag = r >= 32;
+    for (int f1 = 0; f1 < 64; ++f1) {
+      const double a = 2.0 * M_PI * (double)((f1 * t1) % 64) / 64.0;
+      const double gr = std::cos(a), gi = std::sin(a);
+      put<T>(img, MAT_GA + off_kmaj(r, f1, 8192), imag ? gi : gr);
+      put<T>(img, MAT_GA + off_kmaj(r, 64 + f1, 8192), imag ? gr : -gi);
+    }
+  }
   return img;
 }
 
@@ -796,7 +646,7 @@ EncodeFn encode_fn() {
   return fn;
 }
 
-// signal [B][H][4096] viewed as [B][H][8 t1][512 m]; box [64 m][8 t1][1][2 b]
+// signal [B][H][4096] viewed as [B][H][32 t1][128 t2]; box [64 t2][32 t1][1][1]
 template <typename T>
 int make_map(CUtensorMap* map, const void* ptr, int64_t B, int64_t H) {
   EncodeFn enc = encode_fn();
@@ -804,9 +654,9 @@ int make_map(CUtensorMap* map, const void* ptr, int64_t B, int64_t H) {
     set_error("tcgen05 path: cuTensorMapEncodeTiled unavailable");
     return FB_ERR_CUDA;
   }
-  const cuuint64_t dims[4] = {512, 8, (cuuint64_t)H, (cuuint64_t)B};
-  const cuuint64_t strides[3] = {512 * 2, 4096 * 2, (cuuint64_t)H * 4096 * 2};
-  const cuuint32_t box[4] = {64, 8, 1, 2};
+  const cuuint64_t dims[4] = {128, 32, (cuuint64_t)H, (cuuint64_t)B};
+  const cuuint64_t strides[3] = {128 * 2, 4096 * 2, (cuuint64_t)H * 4096 * 2};
+  const cuuint32_t box[4] = {64, 32, 1, 1};
   const cuuint32_t es[4] = {1, 1, 1, 1};
   CUresult r = enc(map, Fmt<T>::tma, 4, const_cast<void*>(ptr), dims, strides, box, es,
                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
