@@ -174,6 +174,7 @@ int fb_plan_destroy(fb_plan* p) {
   cudaFree(p->d);
   cudaFree(p->tc_mats);
   cudaFree(p->kf_tc);
+  cudaFree(p->kf_scale);
   delete p;
   return FB_OK;
 }

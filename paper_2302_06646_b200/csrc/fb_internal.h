@@ -24,7 +24,8 @@ struct fb_plan {
   float* d = nullptr;      // [H] skip gains
   bool use_tc = false;       // tcgen05 single-pass path (fb_single_tc.cu)
   void* tc_mats = nullptr;   // DFT blocks in UMMA smem images
-  float2* kf_tc = nullptr;   // k_f permuted to the tensor-core frequency layout
+  void* kf_tc = nullptr;     // k_f' = k_f + D/n as fp16 pairs [H][f1 64][f2 128], scaled
+  float* kf_scale = nullptr; // [H] inverse of that per-head power-of-two scale
   bool prepared = false;
   bool use_keep = false;
   double lambda = 0.0, keep_scale = 1.0;
@@ -53,10 +54,18 @@ size_t sp_workspace(const fb_plan* p, int64_t B);
 int sp_bwd(fb_plan* p, const void* dy, const void* u, void* du, float* dK, float* dKbar, float* dD,
            int64_t B, void* ws, cudaStream_t s);
 
+// Where the persistent tcgen05 backward leaves its dK spectrum partials:
+// spart[cta * maxseg + seg] for the CTAs' contiguous shares of the
+// total = H x npairs head-major pairs (fb_single_tc.cu).
+struct SpartMap {
+  int ctas, total, npairs, maxseg;
+};
+int sp_finalize(fb_plan* p, const float2* spart, const float* ddpart, int chunks, float* dkbar,
+                float* dD, float* dK, int dd_lag0, const SpartMap* map, cudaStream_t s);
+
 // tcgen05 single-pass (fb_single_tc.cu)
 bool tc_eligible(const fb_plan* p);
 int tc_init(fb_plan* p);
-int tc_prep_permute(fb_plan* p, cudaStream_t s);
 int tc_fwd(fb_plan* p, const void* u, void* y, int64_t B, cudaStream_t s);
 size_t tc_workspace(const fb_plan* p, int64_t B);
 int tc_bwd(fb_plan* p, const void* dy, const void* u, void* du, float* dK, float* dKbar, float* dD,

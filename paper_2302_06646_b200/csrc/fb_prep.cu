@@ -16,6 +16,7 @@
 // which is real, so smooth_frequency(k) = k * w (and is self-adjoint).
 #include "fb_common.cuh"
 #include "fb_internal.h"
+#include "fb_reg.cuh"
 
 namespace fb {
 
@@ -67,21 +68,6 @@ __global__ void dropout_keep_kernel(uint8_t* __restrict__ keep, int H, int64_t N
   for (int64_t i = 0; i < N; ++i) k[i] = (r.uniform01() < rate) ? 0 : 1;
 }
 
-__device__ __forceinline__ double dropped(const float* __restrict__ K, const uint8_t* keep,
-                                          double keep_scale, size_t idx) {
-  const double v = (double)__ldg(K + idx);
-  if (!keep) return v;
-  return keep[idx] ? v * keep_scale : 0.0;
-}
-
-// Dirichlet window of smooth_frequency (see header comment).
-__device__ __forceinline__ double freq_window(int64_t t, int64_t N, int64_t p) {
-  double acc = 1.0;
-  const double step = 2.0 * 3.14159265358979323846 / (double)N;
-  for (int64_t d = 1; d <= p; ++d) acc += 2.0 * cos(step * (double)((d * t) % N));
-  return acc / (double)(2 * p + 1);
-}
-
 // kbar[h][t] = squash(smooth(dropout(K))[t], lambda)
 __global__ void regularize_kernel(const float* __restrict__ K, const uint8_t* __restrict__ keep,
                                   float* __restrict__ kbar, int64_t N, int64_t p, double lambda,
@@ -89,19 +75,7 @@ __global__ void regularize_kernel(const float* __restrict__ K, const uint8_t* __
   const int64_t t = (int64_t)blockIdx.y * blockDim.x + threadIdx.x;
   if (t >= N) return;
   const size_t base = (size_t)blockIdx.x * N;
-  double s;
-  if (freq) {
-    s = dropped(K, keep, keep_scale, base + t) * freq_window(t, N, p);
-  } else {
-    const double inv_w = 1.0 / (double)(2 * p + 1);
-    const int64_t lo = t >= p ? t - p : 0;
-    const int64_t hi = (t + p < N - 1) ? t + p : N - 1;
-    double acc = 0.0;
-    for (int64_t j = lo; j <= hi; ++j) acc += dropped(K, keep, keep_scale, base + j);
-    s = acc * inv_w;
-  }
-  const double mag = fabs(s) - lambda;
-  kbar[base + t] = mag > 0.0 ? (float)copysign(mag, s) : 0.0f;
+  kbar[base + t] = reg_value(K, keep, keep_scale, base, t, N, p, lambda, freq);
 }
 
 // dK[h][t] = dropout'(t) * smooth^T(1[kbar != 0] * dkbar)[t]
@@ -113,20 +87,8 @@ __global__ void regularizer_backward_kernel(const float* __restrict__ kbar,
   const int64_t t = (int64_t)blockIdx.y * blockDim.x + threadIdx.x;
   if (t >= N) return;
   const size_t base = (size_t)blockIdx.x * N;
-  double g;
-  if (freq) {
-    g = (__ldg(kbar + base + t) != 0.f ? (double)__ldg(dkbar + base + t) : 0.0) *
-        freq_window(t, N, p);
-  } else {
-    const int64_t lo = t >= p ? t - p : 0;
-    const int64_t hi = (t + p < N - 1) ? t + p : N - 1;
-    double acc = 0.0;
-    for (int64_t j = lo; j <= hi; ++j)
-      if (__ldg(kbar + base + j) != 0.f) acc += (double)__ldg(dkbar + base + j);
-    g = acc / (double)(2 * p + 1);
-  }
-  if (keep) g = keep[base + t] ? g * keep_scale : 0.0;
-  dK[base + t] = (float)g;
+  dK[base + t] = reg_grad(kbar + base, dkbar + base, keep ? keep + base : nullptr, t, N, p,
+                          keep_scale, freq);
 }
 
 int dropout_keep_dev(fb_plan* p, double rate, uint64_t seed, cudaStream_t s) {

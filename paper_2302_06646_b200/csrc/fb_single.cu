@@ -19,6 +19,7 @@
 #include "fb_fft.cuh"
 #include "fb_internal.h"
 #include "fb_ptx.cuh"
+#include "fb_reg.cuh"
 
 namespace fb {
 
@@ -65,23 +66,39 @@ __device__ __forceinline__ void load_table(float2* tab, const float2* __restrict
 }
 
 // ---------------------------------------------------------------- K1 (spectrum)
-// kf[h][e] = FFT_n(zero-pad(kbar[h]))[e] / n
+// One CTA per head, the whole of K1 in one launch: kbar[h] = squash(smooth(
+// dropout(K[h]))) (fb_reg.cuh, fp64) is written once for the backward's mask
+// and transformed in place: kf[h][f] = FFT_n(zero-pad(kbar[h]))[f] / n.  With
+// kf_tc set (tcgen05 path) the spectrum goes out instead in the tensor-core
+// layout [h][f1 64][f2 128] (f = f1 + 64 f2) with the skip gain folded in
+// as a flat spectrum, k_f' = k_f + D/n, as fp16 pairs scaled by the power
+// of two that brings the head's largest component to <= 2^15; kf_scale[h]
+// is the inverse (the tensor-core kernels fold it into their output).
 template <int LOG2N>
 __global__ void __launch_bounds__(FftShape<LOG2N>::T, 1)
-    sp_spectrum_kernel(const float* __restrict__ kbar, float2* __restrict__ kf,
-                       const float2* __restrict__ tab_g, uint32_t N) {
+    sp_spectrum_kernel(const float* __restrict__ K, const uint8_t* __restrict__ keep,
+                       float* __restrict__ kbar, float2* __restrict__ kf, __half2* __restrict__ kf_tc,
+                       float* __restrict__ kf_scale, const float* __restrict__ D,
+                       const float2* __restrict__ tab_g, uint32_t N, int64_t p, double lambda,
+                       double keep_scale, int freq) {
   using S = FftShape<LOG2N>;
   extern __shared__ __align__(128) unsigned char smem_raw[];
+  __shared__ float red[32];
   float2* work = reinterpret_cast<float2*>(smem_raw);
   float2* tab = work + S::work_len;
   const uint32_t h = blockIdx.x, j = threadIdx.x;
   load_table<LOG2N>(tab, tab_g);
-  const float* kh = kbar + (size_t)h * N;
+  const size_t base = (size_t)h * N;
   float2 v[16];
 #pragma unroll
   for (int r = 0; r < 16; ++r) {
     const uint32_t t = j + r * S::stride;
-    v[r] = make_float2(t < N ? __ldg(kh + t) : 0.f, 0.f);
+    float kv = 0.f;
+    if (t < N) {
+      kv = reg_value(K, keep, keep_scale, base, t, N, p, lambda, freq);
+      kbar[base + t] = kv;
+    }
+    v[r] = make_float2(kv, 0.f);
   }
   dft_reg<-1, 16>(v);
   bfly_store<16, 1>(work, v, j);
@@ -89,9 +106,49 @@ __global__ void __launch_bounds__(FftShape<LOG2N>::T, 1)
   mid_passes<-1, LOG2N, 16>(work, tab);
   bfly_load<-1, 16, S::n / 16, LOG2N>(work, tab, v, j);
   const float inv_n = 1.0f / (float)S::n;
-  float2* out = kf + (size_t)h * S::n;
+  if (kf_tc == nullptr) {
+    float2* out = kf + (size_t)h * S::n;
 #pragma unroll
-  for (int r = 0; r < 16; ++r) out[j + r * S::stride] = cscale(v[r], inv_n);
+    for (int r = 0; r < 16; ++r) out[j + r * S::stride] = cscale(v[r], inv_n);
+    return;
+  }
+  // f = j + r * stride -> slot (f % 64) * 128 + f / 64, padded by one per 128
+  const float dn = __ldg(D + h) * inv_n;
+  float mx = 0.f;
+#pragma unroll
+  for (int r = 0; r < 16; ++r) {
+    v[r] = cscale(v[r], inv_n);
+    v[r].x += dn;
+    mx = fmaxf(mx, fmaxf(fabsf(v[r].x), fabsf(v[r].y)));
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  if ((j & 31) == 0) red[j >> 5] = mx;
+  __syncthreads();
+  if (j < 32) {
+    float m = j < (S::T + 31) / 32 ? red[j] : 0.f;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+    if (j == 0) red[0] = m;
+  }
+  __syncthreads();
+  int e = 0;
+  if (red[0] > 0.f) frexpf(red[0], &e);
+  const float sc = red[0] > 0.f ? ldexpf(1.f, 15 - e) : 1.f;
+  if (j == 0) kf_scale[h] = red[0] > 0.f ? ldexpf(1.f, e - 15) : 1.f;
+#pragma unroll
+  for (int r = 0; r < 16; ++r) {
+    const uint32_t f = j + r * S::stride, i = (f & 63u) * 128u + (f >> 6);
+    work[i + (i >> 7)] = cscale(v[r], sc);
+  }
+  __syncthreads();
+  __half2* out = kf_tc + (size_t)h * S::n;
+#pragma unroll
+  for (int r = 0; r < 16; ++r) {
+    const uint32_t i = j + r * S::stride;
+    const float2 w = work[i + (i >> 7)];
+    out[i] = __floats2half2_rn(w.x, w.y);
+  }
 }
 
 // ---------------------------------------------------------------- K2 forward
@@ -332,12 +389,19 @@ __global__ void __launch_bounds__(FftShape<LOG2N>::T, 1)
   }
 }
 
-// dKbar[h][t] = scale * Re IFFT(sum_c spart[h][c])[t] / n ; dD[h] = sum_c ddpart.
+// Backward tail, one CTA per head: dKbar[h][t] = scale * Re IFFT(sum_c
+// spart[h][c])[t] / n (chunk partials summed in a fixed order), staged in
+// smem and pushed through the regularizer chain rule (fb_reg.cuh) into
+// dK[h]; dD[h] = sum_c ddpart (SIMT) or the lag-0 correlation dKbar[h][0]
+// (tcgen05 path, where D is folded into k_f').  dkbar_out is optional.
 template <int LOG2N>
 __global__ void __launch_bounds__(FftShape<LOG2N>::T, 1)
     sp_dk_finalize_kernel(const float2* __restrict__ spart, const float* __restrict__ ddpart,
-                          int chunks, float* __restrict__ dkbar, float* __restrict__ dD,
-                          const float2* __restrict__ tab_g, uint32_t N, float scale) {
+                          int chunks, float* __restrict__ dkbar_out, float* __restrict__ dD,
+                          const float* __restrict__ kbar, const uint8_t* __restrict__ keep,
+                          float* __restrict__ dK, const float2* __restrict__ tab_g, uint32_t N,
+                          float scale, int64_t p, double keep_scale, int freq, int dd_lag0,
+                          SpartMap map) {
   using S = FftShape<LOG2N>;
   extern __shared__ __align__(128) unsigned char smem_raw[];
   float2* work = reinterpret_cast<float2*>(smem_raw);
@@ -347,10 +411,24 @@ __global__ void __launch_bounds__(FftShape<LOG2N>::T, 1)
   float2 v[16];
 #pragma unroll
   for (int r = 0; r < 16; ++r) v[r] = make_float2(0.f, 0.f);
-  for (int c = 0; c < chunks; ++c) {
-    const float2* sp = spart + ((size_t)h * chunks + c) * S::n;
+  if (map.ctas > 0) {
+    // the CTAs whose shares meet head h's pairs [h np, (h+1) np), in order
+    const int64_t G = map.ctas, T = map.total, np = map.npairs;
+    const int c0 = (int)((((int64_t)h * np + 1) * G - 1) / T);
+    const int c1 = (int)(((((int64_t)h + 1) * np) * G - 1) / T);
+    for (int c = c0; c <= c1; ++c) {
+      const int64_t start = (int64_t)c * T / G;
+      const int seg = (int)h - (int)(start / np);
+      const float2* sp = spart + ((size_t)c * map.maxseg + seg) * S::n;
 #pragma unroll
-    for (int r = 0; r < 16; ++r) v[r] = cadd(v[r], __ldg(sp + j + r * S::stride));
+      for (int r = 0; r < 16; ++r) v[r] = cadd(v[r], __ldg(sp + j + r * S::stride));
+    }
+  } else {
+    for (int c = 0; c < chunks; ++c) {
+      const float2* sp = spart + ((size_t)h * chunks + c) * S::n;
+#pragma unroll
+      for (int r = 0; r < 16; ++r) v[r] = cadd(v[r], __ldg(sp + j + r * S::stride));
+    }
   }
   dft_reg<+1, 16>(v);
   bfly_store<16, 1>(work, v, j);
@@ -358,15 +436,30 @@ __global__ void __launch_bounds__(FftShape<LOG2N>::T, 1)
   mid_passes<+1, LOG2N, 16>(work, tab);
   bfly_load<+1, 16, S::n / 16, LOG2N>(work, tab, v, j);
   const float s = scale / (float)S::n;
+  const size_t base = (size_t)h * N;
+  float* row = reinterpret_cast<float*>(work);
+  __syncthreads();
 #pragma unroll
   for (int r = 0; r < 16; ++r) {
     const uint32_t t = j + r * S::stride;
-    if (t < N) dkbar[(size_t)h * N + t] = v[r].x * s;
+    if (t < N) {
+      const float g = v[r].x * s;
+      row[t] = g;
+      if (dkbar_out) dkbar_out[base + t] = g;
+    }
   }
+  __syncthreads();
+  for (uint32_t t = j; t < N; t += S::T)
+    dK[base + t] = reg_grad(kbar + base, row, keep ? keep + base : nullptr, t, N, p, keep_scale,
+                            freq);
   if (j == 0) {
-    float t = 0.f;
-    for (int c = 0; c < chunks; ++c) t += ddpart[(size_t)h * chunks + c];
-    dD[h] = t;
+    if (dd_lag0) {
+      dD[h] = row[0];
+    } else {
+      float t = 0.f;
+      for (int c = 0; c < chunks; ++c) t += ddpart[(size_t)h * chunks + c];
+      dD[h] = t;
+    }
   }
 }
 
@@ -430,20 +523,26 @@ struct Sp {
                                            p->periodic ? 1 : 0, ppc, tma);
     }
   }
-  static void spectrum(cudaStream_t s, const fb_plan* p) {
+  static void spectrum(cudaStream_t s, const fb_plan* p, const float* K) {
     const size_t sm = base_smem<LOG2N>(false);
     auto k = sp_spectrum_kernel<LOG2N>;
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-    k<<<(unsigned)p->H, FftShape<LOG2N>::T, sm, s>>>(p->kbar, p->kf, p->tw2, (uint32_t)p->N);
+    k<<<(unsigned)p->H, FftShape<LOG2N>::T, sm, s>>>(
+        K, p->use_keep ? p->keep : nullptr, p->kbar, p->kf,
+        p->use_tc ? (__half2*)p->kf_tc : nullptr, p->kf_scale, p->d, p->tw2, (uint32_t)p->N, p->p, p->lambda, p->keep_scale,
+        p->smooth_domain == FB_SMOOTH_FREQUENCY);
   }
   static void finalize(cudaStream_t s, const fb_plan* p, const float2* spart, const float* ddpart,
-                       int chunks, float* dkbar, float* dD) {
+                       int chunks, float* dkbar, float* dD, float* dK, int dd_lag0,
+                       const SpartMap* map) {
     const size_t sm = base_smem<LOG2N>(false);
     auto k = sp_dk_finalize_kernel<LOG2N>;
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     const float scale = p->periodic ? (float)p->N / (float)p->n : 1.0f;
-    k<<<(unsigned)p->H, FftShape<LOG2N>::T, sm, s>>>(spart, ddpart, chunks, dkbar, dD, p->tw2,
-                                                      (uint32_t)p->N, scale);
+    k<<<(unsigned)p->H, FftShape<LOG2N>::T, sm, s>>>(
+        spart, ddpart, chunks, dkbar, dD, p->kbar, p->use_keep ? p->keep : nullptr, dK, p->tw2,
+        (uint32_t)p->N, scale, p->p, p->keep_scale, p->smooth_domain == FB_SMOOTH_FREQUENCY,
+        dd_lag0, map ? *map : SpartMap{0, 0, 0, 0});
   }
 };
 
@@ -471,17 +570,15 @@ int chunks_for(const fb_plan* p, int64_t B) {
 }  // namespace
 
 int sp_prep(fb_plan* p, const float* K, cudaStream_t s) {
-  int rc = regularize_bank_dev(p, K, s);
-  if (rc) return rc;
-  with_log2n(p->n, [&](auto ks) { ks.spectrum(s, p); });
-  rc = cuda_status(cudaGetLastError(), "sp_prep");
-  if (!rc && p->use_tc) rc = tc_prep_permute(p, s);
-  return rc;
+  with_log2n(p->n, [&](auto ks) { ks.spectrum(s, p, K); });
+  return cuda_status(cudaGetLastError(), "sp_prep");
 }
 
 int sp_finalize(fb_plan* p, const float2* spart, const float* ddpart, int chunks, float* dkbar,
-                float* dD, cudaStream_t s) {
-  with_log2n(p->n, [&](auto ks) { ks.finalize(s, p, spart, ddpart, chunks, dkbar, dD); });
+                float* dD, float* dK, int dd_lag0, const SpartMap* map, cudaStream_t s) {
+  with_log2n(p->n, [&](auto ks) {
+    ks.finalize(s, p, spart, ddpart, chunks, dkbar, dD, dK, dd_lag0, map);
+  });
   return cuda_status(cudaGetLastError(), "sp_finalize");
 }
 
@@ -522,18 +619,15 @@ int sp_bwd(fb_plan* p, const void* dy, const void* u, void* du, float* dK, float
   float* ddpart = (float*)(w + off);
   off += (size_t)p->H * chunks * sizeof(float);
   off = (off + 255) & ~size_t(255);
-  float* dkbar = dKbar ? dKbar : (float*)(w + off);
   with_log2n(p->n, [&](auto ks) {
     switch (p->dtype) {
       case FB_F32: ks.template bwd<float>(s, p, dy, u, du, spart, ddpart, (int)B, chunks, ppc); break;
       case FB_BF16: ks.template bwd<__nv_bfloat16>(s, p, dy, u, du, spart, ddpart, (int)B, chunks, ppc); break;
       default: ks.template bwd<__half>(s, p, dy, u, du, spart, ddpart, (int)B, chunks, ppc); break;
     }
-    ks.finalize(s, p, spart, ddpart, chunks, dkbar, dD);
+    ks.finalize(s, p, spart, ddpart, chunks, dKbar, dD, dK, 0, nullptr);
   });
-  int rc = cuda_status(cudaGetLastError(), "sp_bwd");
-  if (rc) return rc;
-  return regularizer_backward_dev(p, dkbar, dK, s);
+  return cuda_status(cudaGetLastError(), "sp_bwd");
 }
 
 }  // namespace fb

@@ -44,32 +44,38 @@ constexpr uint32_t kN = 8192;
 constexpr uint32_t kThreads = 512;
 
 // ---------------------------------------------------------------- smem map
-// inputs  : [buf][mb 2][kg 8][8 k][64 m] bf16 (16 KB per pair), kg 0-3 = u_b0
-//           t1 0..31, kg 4-7 = u_b1 (the TMA box order)
-// op      : 32 KB — Ar|Ai (stage B), Zr|Zi (stage B'), A' operand; one live
-// FA64    : stage-A block  [128 rows (f1 re|im)][64 k (t1<32 re|im)] K-major SW128
-// FR, FI  : DFT128 real / imaginary [128 rows][128 k] K-major SW128 (2 k-blocks)
-// GA64    : stage-A' block [64 rows (t1<32 re|im)][128 k (f1 re|im)] K-major SW128
-// KF      : k_f' [f1 64][f2 128] float2
+// Two independent 8-warp slots per CTA; each slot runs its own channel pair
+// through A -> B -> (x k_f') -> B' -> A', so one slot's epilogue (CUDA cores)
+// overlaps the other slot's MMAs (tensor pipe).
+//   SIN  [slot]: u/dy pair, [mb 2][kg 8][8 k][64 m] bf16 (16 KB), kg 0-3 =
+//               channel b0 t1 0..31, kg 4-7 = b1 (the TMA box order)
+//   SOP  [slot]: 32 KB operand of stages B, B', A' (one live at a time)
+//   FA         : stage-A block [128 rows (f1 re|im)][64 k (t1<32 re|im)]
+//               K-major SW128; read as an MN-major B operand it is exactly the
+//               stage-A' block (conj(F64) restricted to t1 < 32), so A' needs
+//               no matrix of its own
+//   FR, FI     : DFT128 real / imaginary [128][128] K-major SW128 (2 k-blocks)
+//   KF   (bwd) : k_f' as fp16 pairs [f1 64][f2 128] x per-head scale
+constexpr uint32_t kSlotThreads = 256;
 constexpr uint32_t SIN = 0;
 constexpr uint32_t SOP = SIN + 2 * 16384;
-constexpr uint32_t SMAT = SOP + 32768;
-constexpr uint32_t MAT_FA = 0, MAT_FR = 16384, MAT_FI = 49152, MAT_GA = 81920, MAT_BYTES = 98304;
-constexpr uint32_t SKF = SMAT + MAT_BYTES;
-constexpr uint32_t STAB = SKF + 65536;
-// 226 KB: the whole opt-in budget next to the 1 KB of static smem; the
-// extern buffer is declared __align__(1024) (checked at run time) so the
-// swizzled operands need no alignment slack.
-constexpr uint32_t SMEM_BYTES = STAB + 1536;
+constexpr uint32_t SMAT = SOP + 2 * 32768;
+constexpr uint32_t MAT_FA = 0, MAT_FR = 16384, MAT_FI = 49152, MAT_BYTES = 81920;
+constexpr uint32_t STAB = SMAT + MAT_BYTES;
+constexpr uint32_t SKF = STAB + 2048;
+constexpr uint32_t SMEM_FWD = STAB + 1536;
+constexpr uint32_t SMEM_BWD = SKF + 32768;
 
 __device__ __forceinline__ unsigned char* smem_base(unsigned char* raw) {
   if (reinterpret_cast<uintptr_t>(raw) & 1023) __trap();  // swizzle atoms need 1 KB alignment
   return raw;
 }
 
-// TMEM columns (512 allocated): W working region of every stage, R3 holds
-// F(dy) while F(u) runs (backward), R4 the resident dK spectrum S.
-constexpr uint32_t TW = 0, R3 = 128, R4 = 256;
+// TMEM columns (512 allocated).  Slot s works in [128 s, 128 s + 128).
+// Forward: the slot's k_f' copy at 256 + 128 s (re f1 0..63 | im).
+// Backward: U parked as bf16 pairs at 256 + 64 s, the CTA's dK spectrum
+// accumulator S at 384..511 (shared by the slots, updated in pair order).
+constexpr uint32_t TKF = 256, TPK = 256, TS = 384;
 
 __host__ __device__ __forceinline__ uint32_t sw128(uint32_t lin) { return lin ^ ((lin >> 3) & 0x70u); }
 // MN-major B operand with N = 64: [kg][8 k][64 n]
@@ -184,31 +190,58 @@ __device__ __forceinline__ uint32_t tid_v() {
   asm volatile("mov.u32 %0, %%tid.x;" : "=r"(t));
   return t;
 }
-// lane = TMEM row within the warp's slab, s = slab, g = column group (0..3)
+// Slot-local coordinates: TMEM lane row = 32 (warp % 4) + lane (a warp may
+// only touch its lane quarter) and column half g (warps 0-3 / 4-7 of the slot).
 __device__ __forceinline__ void coords(uint32_t& row, uint32_t& g) {
   const uint32_t t = tid_v();
   row = 32 * ((t >> 5) & 3) + (t & 31);
-  g = t >> 7;
+  g = (t >> 7) & 1;
 }
+__device__ __forceinline__ bool slot_leader() { return (tid_v() & (kSlotThreads - 1)) == 0; }
 
 struct Ctx {
   unsigned char* sm;
   uint32_t smb;
-  uint32_t tmem;
+  uint32_t tmem;    // TMEM base (lane 0, column 0)
+  uint32_t tw;      // the slot's working columns
+  uint32_t aux;     // fwd: the slot's k_f' columns; bwd: the slot's parked-U columns
+  uint32_t in_off;  // the slot's input buffer (bytes into smem)
+  uint32_t sop;     // the slot's operand buffer
+  uint32_t bar_id;  // the slot's named barrier
   uint64_t* mma_bar;
   uint32_t mma_phase;
   const float2* tab;
 };
 
+__device__ __forceinline__ Ctx make_ctx(unsigned char* sm, uint32_t tmem, uint32_t slot,
+                                        uint64_t* mma_bar) {
+  Ctx c;
+  c.sm = sm;
+  c.smb = ptx::smem_u32(sm);
+  c.tmem = tmem;
+  c.tw = 128 * slot;
+  c.aux = 0;
+  c.in_off = SIN + 16384 * slot;
+  c.sop = SOP + 32768 * slot;
+  c.bar_id = 1 + slot;
+  c.mma_bar = mma_bar;
+  c.mma_phase = 0;
+  c.tab = reinterpret_cast<const float2*>(sm + STAB);
+  return c;
+}
+
 __device__ __forceinline__ uint32_t taddr(const Ctx& c, uint32_t col) {
   return c.tmem + ((32u * ((tid_v() >> 5) & 3)) << 16) + col;
 }
 
-// make generic smem writes and TMEM reads visible before the next MMAs
-__device__ __forceinline__ void publish() {
+__device__ __forceinline__ void slot_sync(const Ctx& c) {
+  asm volatile("bar.sync %0, %1;" ::"r"(c.bar_id), "n"(kSlotThreads) : "memory");
+}
+// make the slot's generic smem writes and TMEM reads visible before its next MMAs
+__device__ __forceinline__ void publish(const Ctx& c) {
   ptx::fence_proxy_async_smem();
   tc::fence_before();
-  __syncthreads();
+  slot_sync(c);
   tc::fence_after();
 }
 __device__ __forceinline__ void mma_wait(Ctx& c) {
@@ -216,26 +249,33 @@ __device__ __forceinline__ void mma_wait(Ctx& c) {
   c.mma_phase ^= 1;
   tc::fence_after();
 }
+__device__ __forceinline__ void cta_sync_tc() {
+  tc::fence_before();
+  __syncthreads();
+  tc::fence_after();
+}
 
 // ---------------------------------------------------------------- stages
+// A: DFT64 over t1 (pruned to t1 < 32), data = MN-major A operand from TMA
 template <typename T>
-__device__ __forceinline__ void mma_stage_A(const Ctx& c, uint32_t in_off) {
+__device__ __forceinline__ void mma_stage_A(const Ctx& c) {
   const uint32_t id = idesc<T>(128, 128, true, false);
 #pragma unroll
   for (uint32_t s = 0; s < 4; ++s) {
-    const uint64_t ad = tc::smem_desc(c.smb + in_off + s * 2048, 1024, tc::kSw128, 8192);
+    const uint64_t ad = tc::smem_desc(c.smb + c.in_off + s * 2048, 1024, tc::kSw128, 8192);
     const uint64_t bd = tc::smem_desc(c.smb + SMAT + MAT_FA + s * 32, 1024, tc::kSw128);
-    tc::mma_bf16(c.tmem + TW, ad, bd, id, s);
+    tc::mma_bf16(c.tmem + c.tw, ad, bd, id, s);
   }
 }
-// DFT128 with the data as the B operand (MN-major [kg][8][64] at SOP, re
-// plane then im plane 16 KB apart).  inverse: conjugate block.
+// B / B': DFT128 with the data as the B operand (MN-major [kg][8][64] in the
+// slot's SOP, re plane then im plane 16 KB apart).  INV: conjugate block.
 template <typename T, bool INV>
-__device__ __forceinline__ void mma_stage_B(const Ctx& c, uint32_t dcol) {
+__device__ __forceinline__ void mma_stage_B(const Ctx& c) {
   const uint32_t id_p = idesc<T>(128, 64, false, true, false);
   const uint32_t id_n = idesc<T>(128, 64, false, true, true);
   const uint32_t fr = c.smb + SMAT + MAT_FR, fi = c.smb + SMAT + MAT_FI;
-  const uint32_t br = c.smb + SOP, bi = c.smb + SOP + 16384;
+  const uint32_t br = c.smb + c.sop, bi = br + 16384;
+  const uint32_t d = c.tmem + c.tw;
 #pragma unroll
   for (uint32_t s = 0; s < 8; ++s) {
     const uint32_t ko = (s >> 2) * 16384 + (s & 3) * 32;
@@ -245,39 +285,41 @@ __device__ __forceinline__ void mma_stage_B(const Ctx& c, uint32_t dcol) {
     const uint64_t xi = tc::smem_desc(bi + s * 2048, 1024, tc::kSw128, 1024);
     if (!INV) {
       // re = Fr.Ar - Fi.Ai ; im = Fi.Ar + Fr.Ai
-      tc::mma_bf16(c.tmem + dcol, dr, xr, id_p, s);
-      tc::mma_bf16(c.tmem + dcol, di, xi, id_n, 1);
-      tc::mma_bf16(c.tmem + dcol + 64, di, xr, id_p, s);
-      tc::mma_bf16(c.tmem + dcol + 64, dr, xi, id_p, 1);
+      tc::mma_bf16(d, dr, xr, id_p, s);
+      tc::mma_bf16(d, di, xi, id_n, 1);
+      tc::mma_bf16(d + 64, di, xr, id_p, s);
+      tc::mma_bf16(d + 64, dr, xi, id_p, 1);
     } else {
       // conj(F) Z: re = Fr.Zr + Fi.Zi ; im = Fr.Zi - Fi.Zr
-      tc::mma_bf16(c.tmem + dcol, dr, xr, id_p, s);
-      tc::mma_bf16(c.tmem + dcol, di, xi, id_p, 1);
-      tc::mma_bf16(c.tmem + dcol + 64, dr, xi, id_p, s);
-      tc::mma_bf16(c.tmem + dcol + 64, di, xr, id_n, 1);
+      tc::mma_bf16(d, dr, xr, id_p, s);
+      tc::mma_bf16(d, di, xi, id_p, 1);
+      tc::mma_bf16(d + 64, dr, xi, id_p, s);
+      tc::mma_bf16(d + 64, di, xr, id_n, 1);
     }
   }
 }
+// A': IDFT64 over f1 to t1 < 32; the B operand is FA read MN-major (= the
+// conj(F64) block transposed, see the smem map)
 template <typename T>
 __device__ __forceinline__ void mma_stage_Ap(const Ctx& c) {
-  const uint32_t id = idesc<T>(128, 64, false, false);
+  const uint32_t id = idesc<T>(128, 64, false, true);
 #pragma unroll
   for (uint32_t s = 0; s < 8; ++s) {
-    const uint32_t ko = (s & 3) * 32;
-    const uint64_t ad = tc::smem_desc(c.smb + SOP + (s >> 2) * 16384 + ko, 1024, tc::kSw128);
-    const uint64_t bd = tc::smem_desc(c.smb + SMAT + MAT_GA + (s >> 2) * 8192 + ko, 1024, tc::kSw128);
-    tc::mma_bf16(c.tmem + TW, ad, bd, id, s);
+    const uint64_t ad =
+        tc::smem_desc(c.smb + c.sop + (s >> 2) * 16384 + (s & 3) * 32, 1024, tc::kSw128);
+    const uint64_t bd = tc::smem_desc(c.smb + SMAT + MAT_FA + s * 2048, 1024, tc::kSw128, 1024);
+    tc::mma_bf16(c.tmem + c.tw, ad, bd, id, s);
   }
 }
 
 template <typename T>
-__device__ __forceinline__ void issue(Ctx& c, int stage, uint32_t arg) {
-  publish();
-  if (threadIdx.x == 0) {
+__device__ __forceinline__ void issue(Ctx& c, int stage) {
+  publish(c);
+  if (slot_leader()) {
     switch (stage) {
-      case 0: mma_stage_A<T>(c, arg); break;
-      case 1: mma_stage_B<T, false>(c, arg); break;
-      case 2: mma_stage_B<T, true>(c, TW); break;
+      case 0: mma_stage_A<T>(c); break;
+      case 1: mma_stage_B<T, false>(c); break;
+      case 2: mma_stage_B<T, true>(c); break;
       default: mma_stage_Ap<T>(c); break;
     }
     tc::commit(c.mma_bar);
@@ -304,278 +346,357 @@ __device__ __forceinline__ void twiddle_row(float* re, float* im, const float2* 
   }
 }
 
-// Forward transform of the pair staged at in_off: X[f1 + 64 f2] ends in TMEM
-// cols dstB (re, f1 0..63) and dstB + 64 (im), lane = f2.
+// A exit: X[t2][f1] w^(f1 t2) -> stage-B operand (MN-major, k = t2, n = f1)
 template <typename T>
-__device__ __forceinline__ void forward_fft(Ctx& c, uint32_t in_off, uint64_t* in_bar,
-                                            uint32_t in_phase, uint32_t dstB) {
-  ptx::mbar_wait(in_bar, in_phase);
-  issue<T>(c, 0, in_off);
-  // ---- A -> B: w^(f1 t2); Ar/Ai[k = t2][n = f1]
-  {
-    uint32_t t2, g;
-    coords(t2, g);
+__device__ __forceinline__ void epi_A_exit(const Ctx& c) {
+  uint32_t t2, g;
+  coords(t2, g);
+  unsigned char* op = c.sm + c.sop;
+#pragma unroll
+  for (uint32_t q = 0; q < 2; ++q) {
+    const uint32_t cb = 16 * (g + 2 * q);
     float re[16], im[16];
-    tld<16>(taddr(c, TW + 16 * g), re);
-    tld<16>(taddr(c, TW + 64 + 16 * g), im);
+    tld<16>(taddr(c, c.tw + cb), re);
+    tld<16>(taddr(c, c.tw + 64 + cb), im);
     tc::ld_wait();
-    twiddle_row<-1>(re, im, c.tab, t2, 16 * g);
-    unsigned char* op = c.sm + SOP;
-    st8<T>(op + off_bmn(16 * g, t2), re);
-    st8<T>(op + off_bmn(16 * g + 8, t2), re + 8);
-    st8<T>(op + 16384 + off_bmn(16 * g, t2), im);
-    st8<T>(op + 16384 + off_bmn(16 * g + 8, t2), im + 8);
+    twiddle_row<-1>(re, im, c.tab, t2, cb);
+    st8<T>(op + off_bmn(cb, t2), re);
+    st8<T>(op + off_bmn(cb + 8, t2), re + 8);
+    st8<T>(op + 16384 + off_bmn(cb, t2), im);
+    st8<T>(op + 16384 + off_bmn(cb + 8, t2), im + 8);
   }
-  issue<T>(c, 1, dstB);
 }
 
-// Inverse from Zr/Zi (MN-major in SOP); leaves z[128 t1 + t2] (t1 < 32) in
-// TMEM cols TW + t1 (re) / TW + 32 + t1 (im), lane = t2.
+// B' exit: w^(-f1 t2) -> stage-A' operand (K-major rows t2, k = f1 re | im)
 template <typename T>
-__device__ __forceinline__ void inverse_fft(Ctx& c) {
-  issue<T>(c, 2, 0);
-  // ---- B' -> A': w^(-f1 t2); A' operand row t2, k = f1 (re) / 64 + f1 (im)
-  {
-    uint32_t t2, g;
-    coords(t2, g);
+__device__ __forceinline__ void epi_Bp_exit(const Ctx& c) {
+  uint32_t t2, g;
+  coords(t2, g);
+  unsigned char* op = c.sm + c.sop;
+#pragma unroll
+  for (uint32_t q = 0; q < 2; ++q) {
+    const uint32_t cb = 16 * (g + 2 * q);
     float re[16], im[16];
-    tld<16>(taddr(c, TW + 16 * g), re);
-    tld<16>(taddr(c, TW + 64 + 16 * g), im);
+    tld<16>(taddr(c, c.tw + cb), re);
+    tld<16>(taddr(c, c.tw + 64 + cb), im);
     tc::ld_wait();
-    twiddle_row<+1>(re, im, c.tab, t2, 16 * g);
-    unsigned char* op = c.sm + SOP;
-    st8<T>(op + off_kmaj(t2, 16 * g, 16384), re);
-    st8<T>(op + off_kmaj(t2, 16 * g + 8, 16384), re + 8);
-    st8<T>(op + off_kmaj(t2, 64 + 16 * g, 16384), im);
-    st8<T>(op + off_kmaj(t2, 64 + 16 * g + 8, 16384), im + 8);
+    twiddle_row<+1>(re, im, c.tab, t2, cb);
+    st8<T>(op + off_kmaj(t2, cb, 16384), re);
+    st8<T>(op + off_kmaj(t2, cb + 8, 16384), re + 8);
+    st8<T>(op + off_kmaj(t2, 64 + cb, 16384), im);
+    st8<T>(op + off_kmaj(t2, 64 + cb + 8, 16384), im + 8);
   }
-  issue<T>(c, 3, 0);
 }
 
-// A' exit: rows t2, z[128 t1 + t2] for t1 = 8 g + j (re -> b0, im -> b1)
+// A' exit: rows t2, z[128 t1 + t2] for t1 = 16 g + j (re -> b0, im -> b1)
 template <typename T>
 __device__ __forceinline__ void store_rows(const Ctx& c, T* __restrict__ out, int b0, int B, int H,
                                            int h) {
   uint32_t t2, g;
   coords(t2, g);
-  float re[8], im[8];
-  tld<8>(taddr(c, TW + 8 * g), re);
-  tld<8>(taddr(c, TW + 32 + 8 * g), im);
+  float re[16], im[16];
+  tld<16>(taddr(c, c.tw + 16 * g), re);
+  tld<16>(taddr(c, c.tw + 32 + 16 * g), im);
   tc::ld_wait();
-  T* o0 = out + ((size_t)b0 * H + h) * 4096 + 128 * (8 * g) + t2;
+  T* o0 = out + ((size_t)b0 * H + h) * 4096 + 128 * (16 * g) + t2;
 #pragma unroll
-  for (int j = 0; j < 8; ++j) o0[128 * j] = cvt<T>(re[j]);
+  for (int j = 0; j < 16; ++j) o0[128 * j] = cvt<T>(re[j]);
   if (b0 + 1 < B) {
-    T* o1 = out + ((size_t)(b0 + 1) * H + h) * 4096 + 128 * (8 * g) + t2;
+    T* o1 = out + ((size_t)(b0 + 1) * H + h) * 4096 + 128 * (16 * g) + t2;
 #pragma unroll
-    for (int j = 0; j < 8; ++j) o1[128 * j] = cvt<T>(im[j]);
+    for (int j = 0; j < 16; ++j) o1[128 * j] = cvt<T>(im[j]);
   }
 }
 
-__device__ __forceinline__ void setup(Ctx& c, unsigned char* sm, uint32_t* tmem_slot, uint64_t* bars,
-                                      int nbars, const uint4* __restrict__ mats,
-                                      const float2* __restrict__ kf_h,
+__device__ __forceinline__ void setup(unsigned char* sm, uint32_t* tmem_slot, uint64_t* bars,
+                                      int nbars, int nbars_slot, const uint4* __restrict__ mats,
                                       const float2* __restrict__ tab_g) {
-  c.sm = sm;
-  c.smb = ptx::smem_u32(sm);
-  c.tab = reinterpret_cast<const float2*>(sm + STAB);
-  c.mma_bar = &bars[0];
-  c.mma_phase = 0;
   if (threadIdx.x < 32) tc::alloc<512>(tmem_slot);
   if (threadIdx.x == 0) {
-    for (int i = 0; i < nbars; ++i) ptx::mbar_init(&bars[i], 1);
+    for (int i = 0; i < nbars; ++i) ptx::mbar_init(&bars[i], i < nbars - nbars_slot ? 1 : kSlotThreads);
     ptx::fence_barrier_init();
   }
   uint4* dm = reinterpret_cast<uint4*>(sm + SMAT);
   for (uint32_t i = threadIdx.x; i < MAT_BYTES / 16; i += kThreads) dm[i] = __ldg(mats + i);
   float2* tab = reinterpret_cast<float2*>(sm + STAB);
   for (uint32_t i = threadIdx.x; i < 192; i += kThreads) tab[i] = __ldg(tab_g + i);
-  const float4* src = reinterpret_cast<const float4*>(kf_h);
-  float4* dst = reinterpret_cast<float4*>(sm + SKF);
-  for (uint32_t i = threadIdx.x; i < kN / 2; i += kThreads) dst[i] = __ldg(src + i);
   ptx::fence_proxy_async_smem();
-  tc::fence_before();
-  __syncthreads();
-  tc::fence_after();
-  c.tmem = *tmem_slot;
+  cta_sync_tc();
 }
 
-__device__ __forceinline__ void teardown(const Ctx& c) {
-  tc::fence_before();
-  __syncthreads();
-  if (threadIdx.x < 32) tc::dealloc<512>(c.tmem);
+__device__ __forceinline__ void teardown(uint32_t tmem) {
+  cta_sync_tc();
+  if (threadIdx.x < 32) tc::dealloc<512>(tmem);
 }
 
-__device__ __forceinline__ void pair_end() {
-  tc::fence_before();
-  __syncthreads();
-  tc::fence_after();
+// The CTA's contiguous share [i0, i1) of the B/2 x H (head-major) channel pairs
+__device__ __forceinline__ void cta_range(int total, int& i0, int& i1) {
+  i0 = (int)(((int64_t)blockIdx.x * total) / gridDim.x);
+  i1 = (int)(((int64_t)(blockIdx.x + 1) * total) / gridDim.x);
 }
 
 // ------------------------------------------------------------------ forward
+// Persistent: CTA c owns pairs [i0, i1) in head-major order; slot s takes
+// i0 + s, i0 + s + 2, ...  Each slot keeps its head's k_f' (fp16 pairs
+// x scale, from K1) in its own TMEM columns, reloaded when its head changes.
+__device__ __forceinline__ void load_kf_tmem(const Ctx& c, const __half2* __restrict__ kf, float sc) {
+  uint32_t f2, g;
+  coords(f2, g);
+#pragma unroll
+  for (uint32_t q = 0; q < 2; ++q) {
+    const uint32_t cb = 16 * (g + 2 * q);
+    float re[16], im[16];
+#pragma unroll
+    for (int j = 0; j < 16; ++j) {
+      const float2 v = __half22float2(kf[(cb + j) * 128 + f2]);
+      re[j] = v.x * sc;
+      im[j] = v.y * sc;
+    }
+    tst8(taddr(c, c.aux + cb), re);
+    tst8(taddr(c, c.aux + cb + 8), re + 8);
+    tst8(taddr(c, c.aux + 64 + cb), im);
+    tst8(taddr(c, c.aux + 64 + cb + 8), im + 8);
+  }
+  tst_wait();
+}
+
 template <typename T>
 __global__ void __launch_bounds__(kThreads, 1)
     tc_fwd_kernel(const __grid_constant__ CUtensorMap umap, T* __restrict__ y,
-                  const float2* __restrict__ kfp, const uint4* __restrict__ mats,
-                  const float2* __restrict__ tab_g, int B, int H, int ppc) {
+                  const __half2* __restrict__ kf16, const float* __restrict__ kscale,
+                  const uint4* __restrict__ mats, const float2* __restrict__ tab_g, int B, int H,
+                  int total) {
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   __shared__ uint32_t tmem_slot;
-  __shared__ __align__(8) uint64_t bars[3];  // 0: mma, 1/2: input buffers
+  __shared__ __align__(8) uint64_t bars[4];  // mma[2], in[2]
   unsigned char* sm = smem_base(smem_raw);
-  const int h = blockIdx.x;
   const int npairs = (B + 1) / 2;
-  const int p0 = blockIdx.y * ppc, p1 = min(npairs, p0 + ppc);
-  if (p0 >= p1) return;
-  Ctx c;
-  setup(c, sm, &tmem_slot, bars, 3, mats, kfp + (size_t)h * kN, tab_g);
-  const float2* kfs = reinterpret_cast<const float2*>(sm + SKF);
-  if (threadIdx.x == 0) load_pair(sm + SIN, &umap, h, 2 * p0, &bars[1]);
-  for (int pr = p0, it = 0; pr < p1; ++pr, ++it) {
-    const int buf = it & 1;
-    // the other buffer's last reader (stage A of the previous pair) is done
-    if (threadIdx.x == 0 && pr + 1 < p1)
-      load_pair(sm + SIN + (buf ^ 1) * 16384, &umap, h, 2 * (pr + 1), &bars[1 + (buf ^ 1)]);
-    forward_fft<T>(c, SIN + buf * 16384, &bars[1 + buf], (it >> 1) & 1, TW);
+  int i0, i1;
+  cta_range(total, i0, i1);
+  setup(sm, &tmem_slot, bars, 4, 0, mats, tab_g);
+  const uint32_t slot = threadIdx.x / kSlotThreads;
+  Ctx c = make_ctx(sm, tmem_slot, slot, &bars[slot]);
+  c.aux = TKF + 128 * slot;
+  uint64_t* in_bar = &bars[2 + slot];
+  const bool lead = slot_leader();
+  int item = i0 + (int)slot;
+  if (lead && item < i1) load_pair(sm + c.in_off, &umap, item / npairs, 2 * (item % npairs), in_bar);
+  int cur_h = -1;
+  for (uint32_t it = 0; item < i1; item += 2, ++it) {
+    const int h = item / npairs, pr = item % npairs;
+    if (h != cur_h) {
+      load_kf_tmem(c, kf16 + (size_t)h * kN, __ldg(kscale + h));
+      cur_h = h;
+    }
+    ptx::mbar_wait(in_bar, it & 1);
+    issue<T>(c, 0);
+    if (lead && item + 2 < i1)
+      load_pair(sm + c.in_off, &umap, (item + 2) / npairs, 2 * ((item + 2) % npairs), in_bar);
+    epi_A_exit<T>(c);
+    issue<T>(c, 1);
     // ---- B exit: Z = X * k_f' -> Zr/Zi[k = f2][n = f1]
     {
       uint32_t f2, g;
       coords(f2, g);
-      float re[16], im[16];
-      tld<16>(taddr(c, TW + 16 * g), re);
-      tld<16>(taddr(c, TW + 64 + 16 * g), im);
-      tc::ld_wait();
-      const float2* kr = kfs + (16 * g) * 128 + f2;
+      unsigned char* op = c.sm + c.sop;
 #pragma unroll
-      for (int j = 0; j < 16; ++j) {
-        const float2 k = kr[j * 128];
-        const float a = re[j], b = im[j];
-        re[j] = fmaf(a, k.x, -b * k.y);
-        im[j] = fmaf(a, k.y, b * k.x);
+      for (uint32_t q = 0; q < 2; ++q) {
+        const uint32_t cb = 16 * (g + 2 * q);
+        float re[16], im[16], kr[16], ki[16];
+        tld<16>(taddr(c, c.tw + cb), re);
+        tld<16>(taddr(c, c.tw + 64 + cb), im);
+        tld<16>(taddr(c, c.aux + cb), kr);
+        tld<16>(taddr(c, c.aux + 64 + cb), ki);
+        tc::ld_wait();
+#pragma unroll
+        for (int j = 0; j < 16; ++j) {
+          const float a = re[j], b = im[j];
+          re[j] = fmaf(a, kr[j], -b * ki[j]);
+          im[j] = fmaf(a, ki[j], b * kr[j]);
+        }
+        st8<T>(op + off_bmn(cb, f2), re);
+        st8<T>(op + off_bmn(cb + 8, f2), re + 8);
+        st8<T>(op + 16384 + off_bmn(cb, f2), im);
+        st8<T>(op + 16384 + off_bmn(cb + 8, f2), im + 8);
       }
-      unsigned char* op = c.sm + SOP;
-      st8<T>(op + off_bmn(16 * g, f2), re);
-      st8<T>(op + off_bmn(16 * g + 8, f2), re + 8);
-      st8<T>(op + 16384 + off_bmn(16 * g, f2), im);
-      st8<T>(op + 16384 + off_bmn(16 * g + 8, f2), im + 8);
     }
-    inverse_fft<T>(c);
+    issue<T>(c, 2);
+    epi_Bp_exit<T>(c);
+    issue<T>(c, 3);
     store_rows<T>(c, y, 2 * pr, B, H, h);
-    pair_end();
   }
-  teardown(c);
+  teardown(tmem_slot);
 }
 
 // ------------------------------------------------------------------ backward
-// Per pair: DY = F(dy) (kept in TMEM R3), U = F(u); S += conj(U) DY with S
-// resident in TMEM R4 for the CTA's whole run; du = F^-1(DY conj(k_f')).
-// S is written in natural order for the finalize kernel (dKbar =
-// Re F^-1(S)/n, dD = dKbar[0]).
+// Persistent like the forward.  The CTA walks its pairs head segment by head
+// segment; inside a segment slot s takes local pairs s, s+2, ...  Per pair:
+// U = F(u) is parked in TMEM as bf16 pairs, DY = F(dy); then S += conj(U) DY
+// (S = the CTA's dK spectrum, fp32 in TMEM, updated strictly in pair order
+// across the slots through two mbarriers so the sum is deterministic) and
+// du = F^-1(DY conj(k_f')).  At a segment end S goes to spart[cta][seg]
+// (natural order) for the finalize kernel (dKbar = Re F^-1(sum S)/n,
+// dD = dKbar[0]).
+__device__ __forceinline__ uint32_t pack_bf2(float a, float b) {
+  __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
+  return *reinterpret_cast<uint32_t*>(&h);
+}
+__device__ __forceinline__ float2 unpack_bf2(uint32_t v) {
+  return __bfloat1622float2(*reinterpret_cast<__nv_bfloat162*>(&v));
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(ptx::smem_u32(bar)) : "memory");
+}
+
 template <typename T>
 __global__ void __launch_bounds__(kThreads, 1)
     tc_bwd_kernel(const __grid_constant__ CUtensorMap dymap, const __grid_constant__ CUtensorMap umap,
-                  T* __restrict__ du, const float2* __restrict__ kfp, const uint4* __restrict__ mats,
+                  T* __restrict__ du, const __half2* __restrict__ kf16,
+                  const float* __restrict__ kscale, const uint4* __restrict__ mats,
                   const float2* __restrict__ tab_g, float2* __restrict__ spart, int B, int H,
-                  int ppc) {
+                  int total, int maxseg) {
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   __shared__ uint32_t tmem_slot;
-  __shared__ __align__(8) uint64_t bars[3];  // 0: mma, 1: dy, 2: u
+  __shared__ __align__(8) uint64_t bars[6];  // mma[2], in[2], S chain[2] (256 arrivals)
   unsigned char* sm = smem_base(smem_raw);
-  const int h = blockIdx.x, chunk = blockIdx.y, chunks = gridDim.y;
   const int npairs = (B + 1) / 2;
-  const int p0 = chunk * ppc, p1 = min(npairs, p0 + ppc);
-  Ctx c;
-  setup(c, sm, &tmem_slot, bars, 3, mats, kfp + (size_t)h * kN, tab_g);
-  const float2* kfs = reinterpret_cast<const float2*>(sm + SKF);
-  {
-    uint32_t f2, g;
-    coords(f2, g);
-    float z[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
-#pragma unroll
-    for (int q = 0; q < 2; ++q) {
-      tst8(taddr(c, R4 + 16 * g + 8 * q), z);
-      tst8(taddr(c, R4 + 64 + 16 * g + 8 * q), z);
-    }
-    tst_wait();
-  }
-  // dy at SIN, u at SIN + 16 KB (single-buffered: each is refilled as soon
-  // as its stage-A MMA has consumed it)
-  if (threadIdx.x == 0 && p0 < p1) {
-    load_pair(sm + SIN, &dymap, h, 2 * p0, &bars[1]);
-    load_pair(sm + SIN + 16384, &umap, h, 2 * p0, &bars[2]);
-  }
-  for (int pr = p0, it = 0; pr < p1; ++pr, ++it) {
-    const uint32_t ph = it & 1;
-    const bool more = pr + 1 < p1;
-    forward_fft<T>(c, SIN, &bars[1], ph, R3);
-    if (threadIdx.x == 0 && more) load_pair(sm + SIN, &dymap, h, 2 * (pr + 1), &bars[1]);
-    forward_fft<T>(c, SIN + 16384, &bars[2], ph, TW);
-    if (threadIdx.x == 0 && more) load_pair(sm + SIN + 16384, &umap, h, 2 * (pr + 1), &bars[2]);
+  int i0, i1;
+  cta_range(total, i0, i1);
+  setup(sm, &tmem_slot, bars, 6, 2, mats, tab_g);
+  const uint32_t slot = threadIdx.x / kSlotThreads;
+  Ctx c = make_ctx(sm, tmem_slot, slot, &bars[slot]);
+  c.aux = TPK + 64 * slot;
+  uint64_t* in_bar = &bars[2 + slot];
+  uint64_t* chain_mine = &bars[4 + slot];
+  uint64_t* chain_other = &bars[5 - slot];
+  const bool lead = slot_leader();
+  const uint32_t* kfs = reinterpret_cast<const uint32_t*>(sm + SKF);
+  uint32_t in_cnt = 0, base0 = 0, base1 = 0;
+  int seg = 0;
+  for (int a = i0; a < i1; ++seg) {
+    const int h = a / npairs;
+    const int L = min(i1, (h + 1) * npairs) - a;
+    // ---- segment start (whole CTA): k_f' of head h to smem, S = 0
     {
-      uint32_t f2, g;
-      coords(f2, g);
-      const float2* kr = kfs + (16 * g) * 128 + f2;
-      unsigned char* op = c.sm + SOP;
+      const uint4* src = reinterpret_cast<const uint4*>(kf16 + (size_t)h * kN);
+      uint4* dst = reinterpret_cast<uint4*>(sm + SKF);
+      for (uint32_t i = threadIdx.x; i < kN * 4 / 16; i += kThreads) dst[i] = __ldg(src + i);
+      const uint32_t t = threadIdx.x;
+      const uint32_t lane_off = (32u * ((t >> 5) & 3)) << 16, g4 = t >> 7;
+      float z[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
 #pragma unroll
       for (int q = 0; q < 2; ++q) {
-        const uint32_t col = 16 * g + 8 * q;
-        float ur[8], ui[8], gr[8], gi[8], sr[8], si[8];
-        tld<8>(taddr(c, TW + col), ur);
-        tld<8>(taddr(c, TW + 64 + col), ui);
-        tld<8>(taddr(c, R3 + col), gr);
-        tld<8>(taddr(c, R3 + 64 + col), gi);
-        tld<8>(taddr(c, R4 + col), sr);
-        tld<8>(taddr(c, R4 + 64 + col), si);
-        tc::ld_wait();
-#pragma unroll
-        for (int j = 0; j < 8; ++j) {
-          sr[j] = fmaf(ur[j], gr[j], fmaf(ui[j], gi[j], sr[j]));   // S += conj(U) DY
-          si[j] = fmaf(ur[j], gi[j], fmaf(-ui[j], gr[j], si[j]));
-          const float2 k = kr[(8 * q + j) * 128];                  // Z = DY conj(k_f')
-          ur[j] = fmaf(gr[j], k.x, gi[j] * k.y);
-          ui[j] = fmaf(gi[j], k.x, -gr[j] * k.y);
-        }
-        tst8(taddr(c, R4 + col), sr);
-        tst8(taddr(c, R4 + 64 + col), si);
-        st8<T>(op + off_bmn(col, f2), ur);
-        st8<T>(op + 16384 + off_bmn(col, f2), ui);
+        tst8(tmem_slot + lane_off + TS + 16 * g4 + 8 * q, z);
+        tst8(tmem_slot + lane_off + TS + 64 + 16 * g4 + 8 * q, z);
       }
       tst_wait();
+      cta_sync_tc();
     }
-    inverse_fft<T>(c);
-    store_rows<T>(c, du, 2 * pr, B, H, h);
-    pair_end();
-  }
-  {
-    uint32_t f2, g;
-    coords(f2, g);
-    float sr[16], si[16];
-    tld<16>(taddr(c, R4 + 16 * g), sr);
-    tld<16>(taddr(c, R4 + 64 + 16 * g), si);
-    tc::ld_wait();
-    float2* sp = spart + ((size_t)h * chunks + chunk) * kN + 64 * f2 + 16 * g;
+    const float osc = __ldg(kscale + h);
+    if (lead && (int)slot < L) {
+      const int it = a + (int)slot;
+      load_pair(sm + c.in_off, &umap, h, 2 * (it - h * npairs), in_bar);
+    }
+    for (int j = (int)slot, k = 0; j < L; j += 2, ++k) {
+      const int b0 = 2 * (a + j - h * npairs);
+      // ---- U = F(u), parked as bf16 pairs
+      ptx::mbar_wait(in_bar, in_cnt & 1);
+      ++in_cnt;
+      issue<T>(c, 0);
+      if (lead) load_pair(sm + c.in_off, &dymap, h, b0, in_bar);
+      epi_A_exit<T>(c);
+      issue<T>(c, 1);
+      {
+        uint32_t f2, g;
+        coords(f2, g);
 #pragma unroll
-    for (int j = 0; j < 16; ++j) sp[j] = make_float2(sr[j], si[j]);
+        for (uint32_t q = 0; q < 2; ++q) {
+          const uint32_t cb = 16 * (g + 2 * q);
+          float re[16], im[16];
+          tld<16>(taddr(c, c.tw + cb), re);
+          tld<16>(taddr(c, c.tw + 64 + cb), im);
+          tc::ld_wait();
+          float pk[16];
+#pragma unroll
+          for (int jj = 0; jj < 16; ++jj) pk[jj] = __uint_as_float(pack_bf2(re[jj], im[jj]));
+          tst8(taddr(c, c.aux + cb), pk);
+          tst8(taddr(c, c.aux + cb + 8), pk + 8);
+        }
+        tst_wait();
+      }
+      // ---- DY = F(dy)
+      ptx::mbar_wait(in_bar, in_cnt & 1);
+      ++in_cnt;
+      issue<T>(c, 0);
+      if (lead && j + 2 < L) load_pair(sm + c.in_off, &umap, h, b0 + 4, in_bar);
+      epi_A_exit<T>(c);
+      issue<T>(c, 1);
+      // ---- S += conj(U) DY (in pair order), Z = DY conj(k_f') -> B' operand
+      if (j > 0) {
+        const uint32_t idx = slot ? base0 + (uint32_t)k : base1 + (uint32_t)k - 1;
+        ptx::mbar_wait(chain_other, idx & 1);
+        tc::fence_after();
+      }
+      {
+        uint32_t f2, g;
+        coords(f2, g);
+        unsigned char* op = c.sm + c.sop;
+#pragma unroll
+        for (uint32_t q = 0; q < 4; ++q) {
+          const uint32_t col = 16 * (g + 2 * (q >> 1)) + 8 * (q & 1);
+          float dr[8], di[8], pk[8], sr[8], si[8];
+          tld<8>(taddr(c, c.tw + col), dr);
+          tld<8>(taddr(c, c.tw + 64 + col), di);
+          tld<8>(taddr(c, c.aux + col), pk);
+          tld<8>(taddr(c, TS + col), sr);
+          tld<8>(taddr(c, TS + 64 + col), si);
+          tc::ld_wait();
+#pragma unroll
+          for (int jj = 0; jj < 8; ++jj) {
+            const float2 u = unpack_bf2(__float_as_uint(pk[jj]));
+            sr[jj] = fmaf(u.x, dr[jj], fmaf(u.y, di[jj], sr[jj]));
+            si[jj] = fmaf(u.x, di[jj], fmaf(-u.y, dr[jj], si[jj]));
+            float2 kv = __half22float2(
+                *reinterpret_cast<const __half2*>(&kfs[(col + jj) * 128 + f2]));
+            kv.x *= osc;
+            kv.y *= osc;
+            const float a0 = dr[jj], b = di[jj];
+            dr[jj] = fmaf(a0, kv.x, b * kv.y);
+            di[jj] = fmaf(b, kv.x, -a0 * kv.y);
+          }
+          tst8(taddr(c, TS + col), sr);
+          tst8(taddr(c, TS + 64 + col), si);
+          st8<T>(op + off_bmn(col, f2), dr);
+          st8<T>(op + 16384 + off_bmn(col, f2), di);
+        }
+        tst_wait();
+        tc::fence_before();
+        mbar_arrive(chain_mine);
+      }
+      issue<T>(c, 2);
+      epi_Bp_exit<T>(c);
+      issue<T>(c, 3);
+      store_rows<T>(c, du, b0, B, H, h);
+    }
+    base0 += (uint32_t)(L + 1) / 2;
+    base1 += (uint32_t)L / 2;
+    // ---- segment end: flush S (natural order f = f1 + 64 f2)
+    cta_sync_tc();
+    {
+      const uint32_t t = threadIdx.x;
+      const uint32_t f2 = 32 * ((t >> 5) & 3) + (t & 31), g4 = t >> 7;
+      const uint32_t lane_off = (32u * ((t >> 5) & 3)) << 16;
+      float sr[16], si[16];
+      tld<16>(tmem_slot + lane_off + TS + 16 * g4, sr);
+      tld<16>(tmem_slot + lane_off + TS + 64 + 16 * g4, si);
+      tc::ld_wait();
+      float2* sp = spart + ((size_t)blockIdx.x * maxseg + seg) * kN + 64 * f2 + 16 * g4;
+#pragma unroll
+      for (int jj = 0; jj < 16; ++jj) sp[jj] = make_float2(sr[jj], si[jj]);
+    }
+    a += L;
   }
-  teardown(c);
-}
-
-// k_f (natural order, / n) -> [h][f1][f2] (f = f1 + 64 f2) with the skip
-// gain folded in as a flat spectrum: k_f' = k_f + D / n
-__global__ void permute_kf_kernel(const float2* __restrict__ kf, const float* __restrict__ D,
-                                  float2* __restrict__ kfp, int H) {
-  const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= (uint32_t)H * kN) return;
-  const uint32_t h = i / kN, r = i % kN, f1 = r / 128, f2 = r % 128;
-  float2 v = kf[(size_t)h * kN + f1 + 64 * f2];
-  v.x += __ldg(D + h) * (1.0f / (float)kN);
-  kfp[i] = v;
-}
-
-// dD[h] = dKbar[h][0] (the lag-0 correlation of dy and u)
-__global__ void dd_from_dkbar_kernel(const float* __restrict__ dkbar, float* __restrict__ dD, int H,
-                                     int64_t N) {
-  const int h = blockIdx.x * blockDim.x + threadIdx.x;
-  if (h < H) dD[h] = dkbar[(size_t)h * N];
+  teardown(tmem_slot);
 }
 
 }  // namespace tcfft
@@ -614,18 +735,6 @@ std::vector<uint8_t> build_mats() {
       put<T>(img, MAT_FR + off_kmaj(r, k, 16384), std::cos(a));
       put<T>(img, MAT_FI + off_kmaj(r, k, 16384), std::sin(a));
     }
-  // stage A': rows t1 re (0..31) | im (32..63); k f1 re (0..63) | im (64..127);
-  // G = conj(F64): z = G w  ->  re row [Gr | -Gi], im row [Gi | Gr]
-  for (int r = 0; r < 64; ++r) {
-    const int t1 = r % 32;
-    const bool imag = r >= 32;
-    for (int f1 = 0; f1 < 64; ++f1) {
-      const double a = 2.0 * M_PI * (double)((f1 * t1) % 64) / 64.0;
-      const double gr = std::cos(a), gi = std::sin(a);
-      put<T>(img, MAT_GA + off_kmaj(r, f1, 8192), imag ? gi : gr);
-      put<T>(img, MAT_GA + off_kmaj(r, 64 + f1, 8192), imag ? gr : -gi);
-    }
-  }
   return img;
 }
 
@@ -668,10 +777,19 @@ int make_map(CUtensorMap* map, const void* ptr, int64_t B, int64_t H) {
   return FB_OK;
 }
 
-int chunks_tc(const fb_plan* p, int64_t B) {
-  const int64_t npairs = (B + 1) / 2;
-  int64_t c = (p->num_sms + p->H - 1) / p->H;
-  return (int)std::max<int64_t>(1, std::min<int64_t>(c, npairs));
+// Persistent grid: one CTA per SM (or per pair when there are fewer),
+// contiguous head-major shares of the B/2 x H channel pairs.
+struct TcGrid {
+  int ctas, total, npairs, maxseg;
+};
+TcGrid tc_grid(const fb_plan* p, int64_t B) {
+  TcGrid g;
+  g.npairs = (int)((B + 1) / 2);
+  g.total = (int)(p->H * g.npairs);
+  g.ctas = std::max(1, std::min(p->num_sms, g.total));
+  const int per = (g.total + g.ctas - 1) / g.ctas;
+  g.maxseg = (per + g.npairs - 1) / g.npairs + 1;  // head segments one CTA can touch
+  return g;
 }
 
 }  // namespace
@@ -687,59 +805,37 @@ int tc_init(fb_plan* p) {
   if (!rc)
     rc = cuda_status(cudaMemcpy(p->tc_mats, img.data(), img.size(), cudaMemcpyHostToDevice),
                      "copy tc mats");
-  if (!rc)
-    rc = cuda_status(cudaMalloc(&p->kf_tc, sizeof(float2) * p->H * kN), "cudaMalloc(kf_tc)");
+  if (!rc) rc = cuda_status(cudaMalloc(&p->kf_tc, sizeof(__half2) * p->H * kN), "cudaMalloc(kf_tc)");
+  if (!rc) rc = cuda_status(cudaMalloc(&p->kf_scale, sizeof(float) * p->H), "cudaMalloc(kf_scale)");
   return rc;
 }
 
-int tc_prep_permute(fb_plan* p, cudaStream_t s) {
-  const uint32_t total = (uint32_t)(p->H * kN);
-  permute_kf_kernel<<<(total + 255) / 256, 256, 0, s>>>(p->kf, p->d, p->kf_tc, (int)p->H);
-  return cuda_status(cudaGetLastError(), "tc permute kf");
-}
-
 int tc_fwd(fb_plan* p, const void* u, void* y, int64_t B, cudaStream_t s) {
-  const int chunks = chunks_tc(p, B);
-  const int64_t npairs = (B + 1) / 2;
-  const int ppc = (int)((npairs + chunks - 1) / chunks);
+  const TcGrid gr = tc_grid(p, B);
   CUtensorMap map;
   auto go = [&](auto tv) {
     using T = decltype(tv);
     int rc = make_map<T>(&map, u, B, p->H);
     if (rc) return rc;
     auto k = tc_fwd_kernel<T>;
-    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM_BYTES);
-    k<<<dim3((unsigned)p->H, (unsigned)chunks), kThreads, SMEM_BYTES, s>>>(
-        map, (T*)y, p->kf_tc, (const uint4*)p->tc_mats, p->tw2, (int)B, (int)p->H, ppc);
+    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM_FWD);
+    k<<<(unsigned)gr.ctas, kThreads, SMEM_FWD, s>>>(map, (T*)y, (const __half2*)p->kf_tc,
+                                                     p->kf_scale, (const uint4*)p->tc_mats, p->tw2,
+                                                     (int)B, (int)p->H, gr.total);
     return cuda_status(cudaGetLastError(), "tc_fwd");
   };
   return p->dtype == FB_BF16 ? go(__nv_bfloat16{}) : go(__half{});
 }
 
 size_t tc_workspace(const fb_plan* p, int64_t B) {
-  const int c = chunks_tc(p, B);
-  size_t bytes = (size_t)p->H * c * kN * sizeof(float2);
-  bytes += (size_t)p->H * c * sizeof(float);
-  bytes = (bytes + 255) & ~size_t(255);
-  bytes += (size_t)p->H * p->N * sizeof(float);
-  return bytes + 256;
+  const TcGrid gr = tc_grid(p, B);
+  return (size_t)gr.ctas * gr.maxseg * kN * sizeof(float2) + 256;
 }
-
-int sp_finalize(fb_plan* p, const float2* spart, const float* ddpart, int chunks, float* dkbar,
-                float* dD, cudaStream_t s);
 
 int tc_bwd(fb_plan* p, const void* dy, const void* u, void* du, float* dK, float* dKbar, float* dD,
            int64_t B, void* ws, cudaStream_t s) {
-  const int chunks = chunks_tc(p, B);
-  const int64_t npairs = (B + 1) / 2;
-  const int ppc = (int)((npairs + chunks - 1) / chunks);
-  char* w = (char*)ws;
-  float2* spart = (float2*)w;
-  size_t off = (size_t)p->H * chunks * kN * sizeof(float2);
-  float* ddpart = (float*)(w + off);
-  off += (size_t)p->H * chunks * sizeof(float);
-  off = (off + 255) & ~size_t(255);
-  float* dkbar = dKbar ? dKbar : (float*)(w + off);
+  const TcGrid gr = tc_grid(p, B);
+  float2* spart = (float2*)ws;
   CUtensorMap dmap, umap;
   auto go = [&](auto tv) {
     using T = decltype(tv);
@@ -747,21 +843,16 @@ int tc_bwd(fb_plan* p, const void* dy, const void* u, void* du, float* dK, float
     if (!rc) rc = make_map<T>(&umap, u, B, p->H);
     if (rc) return rc;
     auto k = tc_bwd_kernel<T>;
-    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM_BYTES);
-    k<<<dim3((unsigned)p->H, (unsigned)chunks), kThreads, SMEM_BYTES, s>>>(
-        dmap, umap, (T*)du, p->kf_tc, (const uint4*)p->tc_mats, p->tw2, spart, (int)B, (int)p->H,
-        ppc);
+    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM_BWD);
+    k<<<(unsigned)gr.ctas, kThreads, SMEM_BWD, s>>>(
+        dmap, umap, (T*)du, (const __half2*)p->kf_tc, p->kf_scale, (const uint4*)p->tc_mats,
+        p->tw2, spart, (int)B, (int)p->H, gr.total, gr.maxseg);
     return cuda_status(cudaGetLastError(), "tc_bwd");
   };
-  int rc = cuda_status(cudaMemsetAsync(ddpart, 0, sizeof(float) * p->H * chunks, s), "memset");
-  if (!rc) rc = p->dtype == FB_BF16 ? go(__nv_bfloat16{}) : go(__half{});
+  int rc = p->dtype == FB_BF16 ? go(__nv_bfloat16{}) : go(__half{});
   if (rc) return rc;
-  rc = sp_finalize(p, spart, ddpart, chunks, dkbar, dD, s);
-  if (rc) return rc;
-  dd_from_dkbar_kernel<<<(unsigned)((p->H + 127) / 128), 128, 0, s>>>(dkbar, dD, (int)p->H, p->N);
-  rc = cuda_status(cudaGetLastError(), "dd_from_dkbar");
-  if (rc) return rc;
-  return regularizer_backward_dev(p, dkbar, dK, s);
+  const SpartMap m{gr.ctas, gr.total, gr.npairs, gr.maxseg};
+  return sp_finalize(p, spart, nullptr, 0, dKbar, dD, dK, 1, &m, s);
 }
 
 }  // namespace fb

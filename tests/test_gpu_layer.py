@@ -175,6 +175,30 @@ def test_tensor_core_single_pass(lc, dtype, B, H):
     assert_parity(got, oracle_layer(lc, inp, cfg), TOL[dtype])
 
 
+@pytest.mark.parametrize("B,H", [(32, 20), (9, 37), (64, 6)])
+def test_tensor_core_persistent_shares(lc, B, H):
+    """Pair counts above the SM count: the persistent CTAs' shares straddle
+    head boundaries (several head segments per CTA, several CTAs per head),
+    which exercises the k_f' reloads and the dK-partial bookkeeping."""
+    N = 4096
+    dtype = torch.bfloat16
+    inp = layer_inputs(lc, B, H, N, dtype)
+    cfg = fb.RegularizationConfig(**CFG)
+    plan, got = run_layer(inp, N, H, dtype, cfg, engine=1)
+    assert plan.tensor_cores
+    assert_parity(got, oracle_layer(lc, inp, cfg), TOL[dtype], keys=("y", "du", "dK", "dD"))
+
+
+def test_tensor_core_deterministic(lc):
+    B, H, N = 32, 20, 4096
+    inp = layer_inputs(lc, B, H, N, torch.bfloat16)
+    cfg = fb.RegularizationConfig(**CFG)
+    _, a = run_layer(inp, N, H, torch.bfloat16, cfg, engine=1)
+    _, b = run_layer(inp, N, H, torch.bfloat16, cfg, engine=1)
+    for k in a:
+        assert np.array_equal(a[k], b[k]), k
+
+
 def test_tensor_core_matches_simt(lc):
     """tcgen05 path vs the fp32 CUDA-core path on identical bf16 inputs."""
     B, H, N = 4, 2, 4096
