@@ -41,10 +41,10 @@ namespace fb {
 namespace tcfft {
 
 constexpr uint32_t kN = 8192;
-constexpr uint32_t kThreads = 512;
+constexpr uint32_t kThreads = 1024;
 
 // ---------------------------------------------------------------- smem map
-// Two independent 8-warp slots per CTA; each slot runs its own channel pair
+// Two independent 16-warp slots per CTA; each slot runs its own channel pair
 // through A -> B -> (x k_f') -> B' -> A', so one slot's epilogue (CUDA cores)
 // overlaps the other slot's MMAs (tensor pipe).
 //   SIN  [slot]: u/dy pair, [mb 2][kg 8][8 k][64 m] bf16 (16 KB), kg 0-3 =
@@ -56,7 +56,11 @@ constexpr uint32_t kThreads = 512;
 //               no matrix of its own
 //   FR, FI     : DFT128 real / imaginary [128][128] K-major SW128 (2 k-blocks)
 //   KF   (bwd) : k_f' as fp16 pairs [f1 64][f2 128] x per-head scale
-constexpr uint32_t kSlotThreads = 256;
+constexpr uint32_t kSlotThreads = 512;
+// a slot's 16 warps: 4 per TMEM lane quarter, so each thread owns 1/kGroups
+// of a row's columns (16 of the 64 complex columns of a stage)
+constexpr uint32_t kGroups = kSlotThreads / 128;
+constexpr uint32_t kColsPer = 64 / kGroups;
 constexpr uint32_t SIN = 0;
 constexpr uint32_t SOP = SIN + 2 * 16384;
 constexpr uint32_t SMAT = SOP + 2 * 32768;
@@ -195,7 +199,7 @@ __device__ __forceinline__ uint32_t tid_v() {
 __device__ __forceinline__ void coords(uint32_t& row, uint32_t& g) {
   const uint32_t t = tid_v();
   row = 32 * ((t >> 5) & 3) + (t & 31);
-  g = (t >> 7) & 1;
+  g = (t >> 7) & (kGroups - 1);
 }
 __device__ __forceinline__ bool slot_leader() { return (tid_v() & (kSlotThreads - 1)) == 0; }
 
@@ -211,6 +215,18 @@ struct Ctx {
   uint64_t* mma_bar;
   uint32_t mma_phase;
   const float2* tab;
+  // MMA token: the slots' MMA batches alternate on the tensor pipe (slot 0,
+  // slot 1, slot 0, ...) so one slot's MMAs run while the other slot is in
+  // its epilogue, instead of both slots queueing behind each other and then
+  // idling in lock-step.  Batch j of the current segment (nb - seg0) waits
+  // for the other slot's batch j - 1 (slot 0) / j (slot 1) to complete, as
+  // long as the other slot has that many batches in the segment.
+  uint32_t slot;
+  uint64_t* other_bar;
+  uint32_t nb;       // batches this slot issued so far
+  uint32_t seg0;     // nb at the start of the current segment
+  uint32_t obase;    // the other slot's batch count at the segment start
+  uint32_t on;       // the other slot's batches in the segment
 };
 
 __device__ __forceinline__ Ctx make_ctx(unsigned char* sm, uint32_t tmem, uint32_t slot,
@@ -227,6 +243,9 @@ __device__ __forceinline__ Ctx make_ctx(unsigned char* sm, uint32_t tmem, uint32
   c.mma_bar = mma_bar;
   c.mma_phase = 0;
   c.tab = reinterpret_cast<const float2*>(sm + STAB);
+  c.slot = slot;
+  c.other_bar = mma_bar + (slot ? -1 : 1);
+  c.nb = c.seg0 = c.obase = c.on = 0;
   return c;
 }
 
@@ -312,10 +331,44 @@ __device__ __forceinline__ void mma_stage_Ap(const Ctx& c) {
   }
 }
 
+#ifdef FB_TC_TIMING
+// experiment only: per (cta, slot, stage) cycle sums of epilogue / slot sync /
+// MMA issue / MMA completion, read back through fb_debug_tc_timing()
+__device__ unsigned long long g_tc_timing[148 * 2 * 32];
+__device__ unsigned long long g_last[148 * 2];
+#endif
+
+// experiment: time a region into slot counter k (16..31)
+#ifdef FB_TC_TIMING
+#define TT_BEGIN unsigned long long _tt0 = clock64();
+#define TT_END(k)                                                                        \
+  if (slot_leader() && blockIdx.x < 148)                                                 \
+    g_tc_timing[(blockIdx.x * 2 + (threadIdx.x / kSlotThreads)) * 32 + (k)] += clock64() - _tt0;
+#else
+#define TT_BEGIN
+#define TT_END(k)
+#endif
+
 template <typename T>
 __device__ __forceinline__ void issue(Ctx& c, int stage) {
+#ifdef FB_TC_TIMING
+  const bool tl = slot_leader() && blockIdx.x < 148;
+  const uint32_t ts = (blockIdx.x * 2 + (threadIdx.x / kSlotThreads));
+  unsigned long long t0 = clock64();
+  if (tl && g_last[ts]) g_tc_timing[ts * 32 + stage] += t0 - g_last[ts];
+#endif
   publish(c);
+#ifdef FB_TC_TIMING
+  unsigned long long t1 = clock64();
+  if (tl) g_tc_timing[ts * 32 + 4 + stage] += t1 - t0;
+#endif
   if (slot_leader()) {
+    const uint32_t j = c.nb - c.seg0;
+    if (c.slot == 0) {
+      if (j >= 1 && j - 1 < c.on) ptx::mbar_wait(c.other_bar, (c.obase + j - 1) & 1);
+    } else if (j < c.on) {
+      ptx::mbar_wait(c.other_bar, (c.obase + j) & 1);
+    }
     switch (stage) {
       case 0: mma_stage_A<T>(c); break;
       case 1: mma_stage_B<T, false>(c); break;
@@ -324,25 +377,35 @@ __device__ __forceinline__ void issue(Ctx& c, int stage) {
     }
     tc::commit(c.mma_bar);
   }
+  ++c.nb;
+#ifdef FB_TC_TIMING
+  unsigned long long t2 = clock64();
+  if (tl) g_tc_timing[ts * 32 + 8 + stage] += t2 - t1;
+#endif
   mma_wait(c);
+#ifdef FB_TC_TIMING
+  unsigned long long t3 = clock64();
+  if (tl) {
+    g_tc_timing[ts * 32 + 12 + stage] += t3 - t2;
+    g_last[ts] = t3;
+  }
+#endif
 }
 
-// (re[j], im[j]) *= w^((off + j) base), j = 0..15, from the two-level table
+// (re[j], im[j]) *= w^((off + j) base), j = 0..15: two table lookups, then
+// a rotation recurrence (16 steps: a few fp32 ulp, far below the bf16
+// operand rounding that follows)
 template <int SIGN>
 __device__ __forceinline__ void twiddle_row(float* re, float* im, const float2* tab, uint32_t base,
                                             uint32_t off) {
-  const float2 c0 = tw2<SIGN>(tab, off * base);
-  const float2 w1 = tw2<SIGN>(tab, base), w2 = tw2<SIGN>(tab, 2 * base);
-  const float2 w4 = tw2<SIGN>(tab, 4 * base), w8 = tw2<SIGN>(tab, 8 * base);
-  const float2 w3 = cmul(w1, w2), w5 = cmul(w1, w4), w6 = cmul(w2, w4), w7 = cmul(w3, w4);
-  const float2 ws[8] = {make_float2(1.f, 0.f), w1, w2, w3, w4, w5, w6, w7};
-  const float2 c8 = cmul(c0, w8);
+  float2 w = tw2<SIGN>(tab, off * base);
+  const float2 st = tw2<SIGN>(tab, base);
 #pragma unroll
   for (int j = 0; j < 16; ++j) {
-    const float2 w = cmul(j < 8 ? c0 : c8, ws[j & 7]);
     const float a = re[j], b = im[j];
     re[j] = fmaf(a, w.x, -b * w.y);
     im[j] = fmaf(a, w.y, b * w.x);
+    if (j < 15) w = cmul(w, st);
   }
 }
 
@@ -353,8 +416,8 @@ __device__ __forceinline__ void epi_A_exit(const Ctx& c) {
   coords(t2, g);
   unsigned char* op = c.sm + c.sop;
 #pragma unroll
-  for (uint32_t q = 0; q < 2; ++q) {
-    const uint32_t cb = 16 * (g + 2 * q);
+  for (uint32_t q = 0; q < kColsPer / 16; ++q) {
+    const uint32_t cb = kColsPer * g + 16 * q;
     float re[16], im[16];
     tld<16>(taddr(c, c.tw + cb), re);
     tld<16>(taddr(c, c.tw + 64 + cb), im);
@@ -374,8 +437,8 @@ __device__ __forceinline__ void epi_Bp_exit(const Ctx& c) {
   coords(t2, g);
   unsigned char* op = c.sm + c.sop;
 #pragma unroll
-  for (uint32_t q = 0; q < 2; ++q) {
-    const uint32_t cb = 16 * (g + 2 * q);
+  for (uint32_t q = 0; q < kColsPer / 16; ++q) {
+    const uint32_t cb = kColsPer * g + 16 * q;
     float re[16], im[16];
     tld<16>(taddr(c, c.tw + cb), re);
     tld<16>(taddr(c, c.tw + 64 + cb), im);
@@ -388,23 +451,24 @@ __device__ __forceinline__ void epi_Bp_exit(const Ctx& c) {
   }
 }
 
-// A' exit: rows t2, z[128 t1 + t2] for t1 = 16 g + j (re -> b0, im -> b1)
+// A' exit: rows t2, z[128 t1 + t2] for t1 = R g + j (re -> b0, im -> b1)
 template <typename T>
 __device__ __forceinline__ void store_rows(const Ctx& c, T* __restrict__ out, int b0, int B, int H,
                                            int h) {
   uint32_t t2, g;
   coords(t2, g);
-  float re[16], im[16];
-  tld<16>(taddr(c, c.tw + 16 * g), re);
-  tld<16>(taddr(c, c.tw + 32 + 16 * g), im);
+  constexpr int R = 32 / kGroups;
+  float re[R], im[R];
+  tld<R>(taddr(c, c.tw + R * g), re);
+  tld<R>(taddr(c, c.tw + 32 + R * g), im);
   tc::ld_wait();
-  T* o0 = out + ((size_t)b0 * H + h) * 4096 + 128 * (16 * g) + t2;
+  T* o0 = out + ((size_t)b0 * H + h) * 4096 + 128 * (R * g) + t2;
 #pragma unroll
-  for (int j = 0; j < 16; ++j) o0[128 * j] = cvt<T>(re[j]);
+  for (int j = 0; j < R; ++j) o0[128 * j] = cvt<T>(re[j]);
   if (b0 + 1 < B) {
-    T* o1 = out + ((size_t)(b0 + 1) * H + h) * 4096 + 128 * (16 * g) + t2;
+    T* o1 = out + ((size_t)(b0 + 1) * H + h) * 4096 + 128 * (R * g) + t2;
 #pragma unroll
-    for (int j = 0; j < 16; ++j) o1[128 * j] = cvt<T>(im[j]);
+    for (int j = 0; j < R; ++j) o1[128 * j] = cvt<T>(im[j]);
   }
 }
 
@@ -443,8 +507,8 @@ __device__ __forceinline__ void load_kf_tmem(const Ctx& c, const __half2* __rest
   uint32_t f2, g;
   coords(f2, g);
 #pragma unroll
-  for (uint32_t q = 0; q < 2; ++q) {
-    const uint32_t cb = 16 * (g + 2 * q);
+  for (uint32_t q = 0; q < kColsPer / 16; ++q) {
+    const uint32_t cb = kColsPer * g + 16 * q;
     float re[16], im[16];
 #pragma unroll
     for (int j = 0; j < 16; ++j) {
@@ -477,6 +541,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   const uint32_t slot = threadIdx.x / kSlotThreads;
   Ctx c = make_ctx(sm, tmem_slot, slot, &bars[slot]);
   c.aux = TKF + 128 * slot;
+  c.on = 4u * (uint32_t)((i1 - i0 + (int)slot) / 2);  // the other slot's pairs x 4 stages
   uint64_t* in_bar = &bars[2 + slot];
   const bool lead = slot_leader();
   int item = i0 + (int)slot;
@@ -485,14 +550,14 @@ __global__ void __launch_bounds__(kThreads, 1)
   for (uint32_t it = 0; item < i1; item += 2, ++it) {
     const int h = item / npairs, pr = item % npairs;
     if (h != cur_h) {
-      load_kf_tmem(c, kf16 + (size_t)h * kN, __ldg(kscale + h));
+      { TT_BEGIN load_kf_tmem(c, kf16 + (size_t)h * kN, __ldg(kscale + h)); TT_END(17) }
       cur_h = h;
     }
-    ptx::mbar_wait(in_bar, it & 1);
+    { TT_BEGIN ptx::mbar_wait(in_bar, it & 1); TT_END(16) }
     issue<T>(c, 0);
     if (lead && item + 2 < i1)
       load_pair(sm + c.in_off, &umap, (item + 2) / npairs, 2 * ((item + 2) % npairs), in_bar);
-    epi_A_exit<T>(c);
+    { TT_BEGIN epi_A_exit<T>(c); TT_END(18) }
     issue<T>(c, 1);
     // ---- B exit: Z = X * k_f' -> Zr/Zi[k = f2][n = f1]
     {
@@ -500,30 +565,28 @@ __global__ void __launch_bounds__(kThreads, 1)
       coords(f2, g);
       unsigned char* op = c.sm + c.sop;
 #pragma unroll
-      for (uint32_t q = 0; q < 2; ++q) {
-        const uint32_t cb = 16 * (g + 2 * q);
-        float re[16], im[16], kr[16], ki[16];
-        tld<16>(taddr(c, c.tw + cb), re);
-        tld<16>(taddr(c, c.tw + 64 + cb), im);
-        tld<16>(taddr(c, c.aux + cb), kr);
-        tld<16>(taddr(c, c.aux + 64 + cb), ki);
+      for (uint32_t q = 0; q < kColsPer / 8; ++q) {
+        const uint32_t cb = kColsPer * g + 8 * q;
+        float re[8], im[8], kr[8], ki[8];
+        tld<8>(taddr(c, c.tw + cb), re);
+        tld<8>(taddr(c, c.tw + 64 + cb), im);
+        tld<8>(taddr(c, c.aux + cb), kr);
+        tld<8>(taddr(c, c.aux + 64 + cb), ki);
         tc::ld_wait();
 #pragma unroll
-        for (int j = 0; j < 16; ++j) {
+        for (int j = 0; j < 8; ++j) {
           const float a = re[j], b = im[j];
           re[j] = fmaf(a, kr[j], -b * ki[j]);
           im[j] = fmaf(a, ki[j], b * kr[j]);
         }
         st8<T>(op + off_bmn(cb, f2), re);
-        st8<T>(op + off_bmn(cb + 8, f2), re + 8);
         st8<T>(op + 16384 + off_bmn(cb, f2), im);
-        st8<T>(op + 16384 + off_bmn(cb + 8, f2), im + 8);
       }
     }
     issue<T>(c, 2);
-    epi_Bp_exit<T>(c);
+    { TT_BEGIN epi_Bp_exit<T>(c); TT_END(20) }
     issue<T>(c, 3);
-    store_rows<T>(c, y, 2 * pr, B, H, h);
+    { TT_BEGIN store_rows<T>(c, y, 2 * pr, B, H, h); TT_END(21) }
   }
   teardown(tmem_slot);
 }
@@ -582,17 +645,21 @@ __global__ void __launch_bounds__(kThreads, 1)
       uint4* dst = reinterpret_cast<uint4*>(sm + SKF);
       for (uint32_t i = threadIdx.x; i < kN * 4 / 16; i += kThreads) dst[i] = __ldg(src + i);
       const uint32_t t = threadIdx.x;
-      const uint32_t lane_off = (32u * ((t >> 5) & 3)) << 16, g4 = t >> 7;
+      constexpr uint32_t W = 64 / (kThreads / 128);  // columns per thread
+      const uint32_t lane_off = (32u * ((t >> 5) & 3)) << 16, g8 = t >> 7;
       float z[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
 #pragma unroll
-      for (int q = 0; q < 2; ++q) {
-        tst8(tmem_slot + lane_off + TS + 16 * g4 + 8 * q, z);
-        tst8(tmem_slot + lane_off + TS + 64 + 16 * g4 + 8 * q, z);
+      for (uint32_t q = 0; q < W / 8; ++q) {
+        tst8(tmem_slot + lane_off + TS + W * g8 + 8 * q, z);
+        tst8(tmem_slot + lane_off + TS + 64 + W * g8 + 8 * q, z);
       }
       tst_wait();
       cta_sync_tc();
     }
     const float osc = __ldg(kscale + h);
+    // the MMA token measured slower here than free interleaving (the backward's
+    // epilogues are longer than its MMA batches): c.on stays 0, no waits
+    c.seg0 = c.nb;
     if (lead && (int)slot < L) {
       const int it = a + (int)slot;
       load_pair(sm + c.in_off, &umap, h, 2 * (it - h * npairs), in_bar);
@@ -600,50 +667,48 @@ __global__ void __launch_bounds__(kThreads, 1)
     for (int j = (int)slot, k = 0; j < L; j += 2, ++k) {
       const int b0 = 2 * (a + j - h * npairs);
       // ---- U = F(u), parked as bf16 pairs
-      ptx::mbar_wait(in_bar, in_cnt & 1);
+      { TT_BEGIN ptx::mbar_wait(in_bar, in_cnt & 1); TT_END(22) }
       ++in_cnt;
       issue<T>(c, 0);
       if (lead) load_pair(sm + c.in_off, &dymap, h, b0, in_bar);
-      epi_A_exit<T>(c);
+      { TT_BEGIN epi_A_exit<T>(c); TT_END(25) }
       issue<T>(c, 1);
       {
         uint32_t f2, g;
         coords(f2, g);
 #pragma unroll
-        for (uint32_t q = 0; q < 2; ++q) {
-          const uint32_t cb = 16 * (g + 2 * q);
-          float re[16], im[16];
-          tld<16>(taddr(c, c.tw + cb), re);
-          tld<16>(taddr(c, c.tw + 64 + cb), im);
+        for (uint32_t q = 0; q < kColsPer / 8; ++q) {
+          const uint32_t cb = kColsPer * g + 8 * q;
+          float re[8], im[8];
+          tld<8>(taddr(c, c.tw + cb), re);
+          tld<8>(taddr(c, c.tw + 64 + cb), im);
           tc::ld_wait();
-          float pk[16];
 #pragma unroll
-          for (int jj = 0; jj < 16; ++jj) pk[jj] = __uint_as_float(pack_bf2(re[jj], im[jj]));
-          tst8(taddr(c, c.aux + cb), pk);
-          tst8(taddr(c, c.aux + cb + 8), pk + 8);
+          for (int jj = 0; jj < 8; ++jj) re[jj] = __uint_as_float(pack_bf2(re[jj], im[jj]));
+          tst8(taddr(c, c.aux + cb), re);
         }
         tst_wait();
       }
       // ---- DY = F(dy)
-      ptx::mbar_wait(in_bar, in_cnt & 1);
+      { TT_BEGIN ptx::mbar_wait(in_bar, in_cnt & 1); TT_END(23) }
       ++in_cnt;
       issue<T>(c, 0);
       if (lead && j + 2 < L) load_pair(sm + c.in_off, &umap, h, b0 + 4, in_bar);
-      epi_A_exit<T>(c);
+      { TT_BEGIN epi_A_exit<T>(c); TT_END(25) }
       issue<T>(c, 1);
       // ---- S += conj(U) DY (in pair order), Z = DY conj(k_f') -> B' operand
       if (j > 0) {
         const uint32_t idx = slot ? base0 + (uint32_t)k : base1 + (uint32_t)k - 1;
-        ptx::mbar_wait(chain_other, idx & 1);
+        TT_BEGIN ptx::mbar_wait(chain_other, idx & 1); TT_END(24)
         tc::fence_after();
       }
       {
         uint32_t f2, g;
         coords(f2, g);
         unsigned char* op = c.sm + c.sop;
-#pragma unroll
-        for (uint32_t q = 0; q < 4; ++q) {
-          const uint32_t col = 16 * (g + 2 * (q >> 1)) + 8 * (q & 1);
+#pragma unroll 1
+        for (uint32_t q = 0; q < kColsPer / 8; ++q) {
+          const uint32_t col = kColsPer * g + 8 * q;
           float dr[8], di[8], pk[8], sr[8], si[8];
           tld<8>(taddr(c, c.tw + col), dr);
           tld<8>(taddr(c, c.tw + 64 + col), di);
@@ -674,9 +739,9 @@ __global__ void __launch_bounds__(kThreads, 1)
         mbar_arrive(chain_mine);
       }
       issue<T>(c, 2);
-      epi_Bp_exit<T>(c);
+      { TT_BEGIN epi_Bp_exit<T>(c); TT_END(28) }
       issue<T>(c, 3);
-      store_rows<T>(c, du, b0, B, H, h);
+      { TT_BEGIN store_rows<T>(c, du, b0, B, H, h); TT_END(29) }
     }
     base0 += (uint32_t)(L + 1) / 2;
     base1 += (uint32_t)L / 2;
@@ -684,15 +749,16 @@ __global__ void __launch_bounds__(kThreads, 1)
     cta_sync_tc();
     {
       const uint32_t t = threadIdx.x;
-      const uint32_t f2 = 32 * ((t >> 5) & 3) + (t & 31), g4 = t >> 7;
+      constexpr uint32_t W = 64 / (kThreads / 128);
+      const uint32_t f2 = 32 * ((t >> 5) & 3) + (t & 31), g8 = t >> 7;
       const uint32_t lane_off = (32u * ((t >> 5) & 3)) << 16;
-      float sr[16], si[16];
-      tld<16>(tmem_slot + lane_off + TS + 16 * g4, sr);
-      tld<16>(tmem_slot + lane_off + TS + 64 + 16 * g4, si);
+      float sr[W], si[W];
+      tld<W>(tmem_slot + lane_off + TS + W * g8, sr);
+      tld<W>(tmem_slot + lane_off + TS + 64 + W * g8, si);
       tc::ld_wait();
-      float2* sp = spart + ((size_t)blockIdx.x * maxseg + seg) * kN + 64 * f2 + 16 * g4;
+      float2* sp = spart + ((size_t)blockIdx.x * maxseg + seg) * kN + 64 * f2 + W * g8;
 #pragma unroll
-      for (int jj = 0; jj < 16; ++jj) sp[jj] = make_float2(sr[jj], si[jj]);
+      for (uint32_t jj = 0; jj < W; ++jj) sp[jj] = make_float2(sr[jj], si[jj]);
     }
     a += L;
   }
@@ -855,4 +921,15 @@ int tc_bwd(fb_plan* p, const void* dy, const void* u, void* du, float* dK, float
   return sp_finalize(p, spart, nullptr, 0, dKbar, dD, dK, 1, &m, s);
 }
 
+#ifdef FB_TC_TIMING
+extern "C" int fb_debug_tc_timing(unsigned long long* out, int reset) {
+  if (reset) {
+    static unsigned long long z[148 * 2 * 32] = {0};
+    cudaMemcpyToSymbol(tcfft::g_tc_timing, z, sizeof(z));
+    cudaMemcpyToSymbol(tcfft::g_last, z, sizeof(unsigned long long) * 296);
+    return 0;
+  }
+  return (int)cudaMemcpyFromSymbol(out, tcfft::g_tc_timing, sizeof(unsigned long long) * 148 * 2 * 32);
+}
+#endif
 }  // namespace fb
