@@ -188,6 +188,281 @@ __global__ void __launch_bounds__(kLbThreads)
   for (int i = threadIdx.x; i < P; i += blockDim.x) dg[i] = G[i];
 }
 
+// ---------------------------------------------------------------- fast path
+// Power-of-two factor chains with every factor <= 16 (config 4: n = 1024 =
+// 16 x 16 x 4) run through specialised kernels: the stage loops are unrolled
+// per factor F (templated), R rows of one head go through each stage
+// together, index math is shifts and masks, the twiddle table sits in smem,
+// and the backward's block gradients are register tiles (4 x 4 entries per
+// thread, column groups reduced by shuffles, warps in a fixed order) so
+// neither the stage inputs nor the gradients are read with bank conflicts.
+// One stage in the forward direction (stage k of apply_stages,
+// butterfly.cpp:136-157, in the matrix form of this file's header):
+//   dst[seg L + a rest + q] = w_L^(a q) sum_p W[a][p] src[seg L + p rest + q]
+// The adjoint pass writes g' = W^H w and immediately applies the next
+// (lower) stage's conj twiddle, so every adjoint stage reads its w ready.
+constexpr int kLxThreads = 256;
+constexpr int kLxMaxF = 16;
+
+struct LxGeo {
+  int nst, lgn;
+  int lgf[kLbMaxStages];
+  int lgL[kLbMaxStages];
+  int off[kLbMaxStages];
+};
+
+template <int F>
+struct Lg2;
+template <> struct Lg2<2> { static constexpr int v = 1; };
+template <> struct Lg2<4> { static constexpr int v = 2; };
+template <> struct Lg2<8> { static constexpr int v = 3; };
+template <> struct Lg2<16> { static constexpr int v = 4; };
+
+// column `col` of R rows under stage geometry (lgL, F): element offset of p = 0
+__device__ __forceinline__ int lx_base(int col, int lgcpr, int lgrest, int lgL, int lgn) {
+  const int r = col >> lgcpr, cc = col & ((1 << lgcpr) - 1);
+  return (r << lgn) + ((cc >> lgrest) << lgL) + (cc & ((1 << lgrest) - 1));
+}
+
+template <int F>
+__device__ __forceinline__ void lx_fwd_stage(const float2* __restrict__ src, float2* __restrict__ dst,
+                                             const float2* __restrict__ W, int lgL, int lgn, int R,
+                                             const float2* __restrict__ tw) {
+  constexpr int LGF = Lg2<F>::v;
+  const int lgrest = lgL - LGF, lgcpr = lgn - LGF;
+  const int C = R << lgcpr;
+  for (int col = threadIdx.x; col < C; col += kLxThreads) {
+    const int base = lx_base(col, lgcpr, lgrest, lgL, lgn);
+    const int ts = (col & ((1 << lgrest) - 1)) << (lgn - lgL);  // q n / L
+    float2 x[F];
+#pragma unroll
+    for (int p = 0; p < F; ++p) x[p] = src[base + (p << lgrest)];
+    // one output row at a time: the W row is a broadcast load (all lanes read
+    // the same entry), so a full unroll would only hoist F^2 registers
+#pragma unroll 1
+    for (int a = 0; a < F; ++a) {
+      float ar = 0.f, ai = 0.f;
+#pragma unroll
+      for (int p = 0; p < F; ++p) {
+        const float2 w = W[a * F + p];
+        ar = fmaf(w.x, x[p].x, fmaf(-w.y, x[p].y, ar));
+        ai = fmaf(w.x, x[p].y, fmaf(w.y, x[p].x, ai));
+      }
+      dst[base + (a << lgrest)] = cmul(make_float2(ar, ai), tw[a * ts]);
+    }
+  }
+}
+
+// g'[p] = sum_a conj(W[a][p]) w[a]; then (plgL >= 0) times conj of the lower
+// stage's twiddle at that element, i.e. the lower stage's w
+template <int F>
+__device__ __forceinline__ void lx_adj_stage(const float2* __restrict__ w, float2* __restrict__ gout,
+                                             const float2* __restrict__ W, int lgL, int lgn, int R,
+                                             const float2* __restrict__ tw, int plgL, int plgf) {
+  constexpr int LGF = Lg2<F>::v;
+  const int lgrest = lgL - LGF, lgcpr = lgn - LGF;
+  const int plgrest = plgL - plgf;
+  const int C = R << lgcpr;
+  for (int col = threadIdx.x; col < C; col += kLxThreads) {
+    const int base = lx_base(col, lgcpr, lgrest, lgL, lgn);
+    float2 v[F];
+#pragma unroll
+    for (int a = 0; a < F; ++a) v[a] = w[base + (a << lgrest)];
+#pragma unroll 1
+    for (int p = 0; p < F; ++p) {
+      float ar = 0.f, ai = 0.f;
+#pragma unroll
+      for (int a = 0; a < F; ++a) {
+        const float2 m = W[a * F + p];  // conj(m) v
+        ar = fmaf(m.x, v[a].x, fmaf(m.y, v[a].y, ar));
+        ai = fmaf(m.x, v[a].y, fmaf(-m.y, v[a].x, ai));
+      }
+      const int idx = base + (p << lgrest);
+      float2 o = make_float2(ar, ai);
+      if (plgL >= 0) {
+        const int loc = idx & ((1 << plgL) - 1);
+        const int pa = loc >> plgrest, pq = loc & ((1 << plgrest) - 1);
+        o = cmulc(o, tw[(pa * pq) << (lgn - plgL)]);
+      }
+      gout[idx] = o;
+    }
+  }
+}
+
+// G[a][p] += sum_cols w[a] conj(v[p]) over the R rows' columns
+template <int F>
+__device__ __forceinline__ void lx_grad(const float2* __restrict__ w, const float2* __restrict__ v,
+                                        float2* __restrict__ G, float2* __restrict__ red, int lgL,
+                                        int lgn, int R) {
+  constexpr int LGF = Lg2<F>::v;
+  constexpr int TS = F < 4 ? F : 4;
+  constexpr int NTS = F / TS, NT = NTS * NTS, CG = kLxThreads / NT;
+  const int lgrest = lgL - LGF, lgcpr = lgn - LGF;
+  const int t = threadIdx.x, tile = t % NT, cg = t / NT;
+  const int a0 = (tile / NTS) * TS, p0 = (tile % NTS) * TS;
+  float2 acc[TS][TS];
+#pragma unroll
+  for (int i = 0; i < TS; ++i)
+#pragma unroll
+    for (int j = 0; j < TS; ++j) acc[i][j] = make_float2(0.f, 0.f);
+  const int C = R << lgcpr;
+  for (int col = cg; col < C; col += CG) {
+    const int base = lx_base(col, lgcpr, lgrest, lgL, lgn);
+    float2 wv[TS], vv[TS];
+#pragma unroll
+    for (int i = 0; i < TS; ++i) {
+      wv[i] = w[base + ((a0 + i) << lgrest)];
+      vv[i] = v[base + ((p0 + i) << lgrest)];
+    }
+#pragma unroll
+    for (int i = 0; i < TS; ++i)
+#pragma unroll
+      for (int j = 0; j < TS; ++j) {
+        acc[i][j].x = fmaf(wv[i].x, vv[j].x, fmaf(wv[i].y, vv[j].y, acc[i][j].x));
+        acc[i][j].y = fmaf(wv[i].y, vv[j].x, fmaf(-wv[i].x, vv[j].y, acc[i][j].y));
+      }
+  }
+  // lanes l and l ^ o (o a multiple of NT) hold the same tile
+#pragma unroll
+  for (int o = NT; o < 32; o <<= 1)
+#pragma unroll
+    for (int i = 0; i < TS; ++i)
+#pragma unroll
+      for (int j = 0; j < TS; ++j) {
+        acc[i][j].x += __shfl_xor_sync(0xffffffffu, acc[i][j].x, o);
+        acc[i][j].y += __shfl_xor_sync(0xffffffffu, acc[i][j].y, o);
+      }
+  const int warp = t >> 5, lane = t & 31;
+  if (lane < NT) {
+#pragma unroll
+    for (int i = 0; i < TS; ++i)
+#pragma unroll
+      for (int j = 0; j < TS; ++j) red[warp * F * F + (a0 + i) * F + (p0 + j)] = acc[i][j];
+  }
+  __syncthreads();
+  for (int e = t; e < F * F; e += kLxThreads) {
+    float2 s = G[e];
+    for (int wq = 0; wq < kLxThreads / 32; ++wq) s = cadd(s, red[wq * F * F + e]);
+    G[e] = s;
+  }
+  __syncthreads();
+}
+
+#define LX_DISPATCH(lgf, CALL)        \
+  switch (lgf) {                      \
+    case 1: { constexpr int F = 2; CALL; } break;  \
+    case 2: { constexpr int F = 4; CALL; } break;  \
+    case 3: { constexpr int F = 8; CALL; } break;  \
+    default: { constexpr int F = 16; CALL; } break; \
+  }
+
+template <typename IO>
+__global__ void __launch_bounds__(kLxThreads)
+    lx_fwd_kernel(const float* __restrict__ blocks, const IO* __restrict__ x, IO* __restrict__ y,
+                  const uint32_t* __restrict__ omap, const float2* __restrict__ tw_g, LxGeo geo,
+                  int B, int H, int P, int R) {
+  extern __shared__ __align__(16) float2 lsm[];
+  const int n = 1 << geo.lgn;
+  float2* W = lsm;
+  float2* tw = W + P;
+  float2* bufA = tw + n;
+  float2* bufB = bufA + (size_t)R * n;
+  const int h = blockIdx.x;
+  const float2* wg = reinterpret_cast<const float2*>(blocks) + (size_t)h * P;
+  for (int i = threadIdx.x; i < P; i += kLxThreads) W[i] = wg[i];
+  for (int i = threadIdx.x; i < n; i += kLxThreads) tw[i] = __ldg(tw_g + i);
+  const int b0 = blockIdx.y * R, rows = min(R, B - b0);
+  for (int i = threadIdx.x; i < R * n; i += kLxThreads) {
+    const int r = i >> geo.lgn, e = i & (n - 1);
+    bufA[i] = r < rows ? ldc<IO>(x + ((size_t)(b0 + r) * H + h) * 2 * n + 2 * e) : make_float2(0.f, 0.f);
+  }
+  __syncthreads();
+  float2 *s = bufA, *d = bufB;
+  for (int k = 0; k < geo.nst; ++k) {
+    LX_DISPATCH(geo.lgf[k], (lx_fwd_stage<F>(s, d, W + geo.off[k], geo.lgL[k], geo.lgn, R, tw)));
+    __syncthreads();
+    float2* tmp = s;
+    s = d;
+    d = tmp;
+  }
+  for (int i = threadIdx.x; i < rows * n; i += kLxThreads) {
+    const int r = i >> geo.lgn, e = i & (n - 1);
+    stc<IO>(y + ((size_t)(b0 + r) * H + h) * 2 * n + 2 * e, s[(r << geo.lgn) + __ldg(omap + e)]);
+  }
+}
+
+// CTA (h, split): rows [split * rps, +rps) of head h, R at a time, in order;
+// the split's block-gradient partial goes to gpart[split][h] (lb_reduce_kernel
+// sums the splits in a fixed order).
+template <typename IO>
+__global__ void __launch_bounds__(kLxThreads)
+    lx_bwd_kernel(const float* __restrict__ blocks, const IO* __restrict__ x,
+                  const IO* __restrict__ g, IO* __restrict__ dx, float2* __restrict__ gpart,
+                  const uint32_t* __restrict__ omap, const float2* __restrict__ tw_g, LxGeo geo,
+                  int B, int H, int P, int R, int rps) {
+  extern __shared__ __align__(16) float2 lsm[];
+  const int n = 1 << geo.lgn, S = geo.nst;
+  float2* W = lsm;
+  float2* G = W + P;
+  float2* tw = G + P;
+  float2* red = tw + n;                                    // [8 warps][16 x 16]
+  float2* v = red + (kLxThreads / 32) * kLxMaxF * kLxMaxF;  // [S][R n] stage inputs
+  float2* ga = v + (size_t)S * R * n;
+  float2* gb = ga + (size_t)R * n;
+  const int h = blockIdx.x;
+  const float2* wg = reinterpret_cast<const float2*>(blocks) + (size_t)h * P;
+  for (int i = threadIdx.x; i < P; i += kLxThreads) {
+    W[i] = wg[i];
+    G[i] = make_float2(0.f, 0.f);
+  }
+  for (int i = threadIdx.x; i < n; i += kLxThreads) tw[i] = __ldg(tw_g + i);
+  const int lgLt = geo.lgL[S - 1], lgft = geo.lgf[S - 1];
+  const int b_end = min(B, (blockIdx.y + 1) * rps);
+  for (int b0 = blockIdx.y * rps; b0 < b_end; b0 += R) {
+    const int rows = min(R, b_end - b0);
+    __syncthreads();
+    for (int i = threadIdx.x; i < R * n; i += kLxThreads) {
+      const int r = i >> geo.lgn, e = i & (n - 1);
+      float2 xv = make_float2(0.f, 0.f), gv = make_float2(0.f, 0.f);
+      if (r < rows) {
+        const size_t row = ((size_t)(b0 + r) * H + h) * 2 * n;
+        xv = ldc<IO>(x + row + 2 * e);
+        gv = ldc<IO>(g + row + 2 * e);
+      }
+      v[i] = xv;
+      // adjoint of the output permutation, then the top stage's conj twiddle
+      const int idx = __ldg(omap + e);
+      const int loc = idx & ((1 << lgLt) - 1), lgr = lgLt - lgft;
+      const int pa = loc >> lgr, pq = loc & ((1 << lgr) - 1);
+      ga[(r << geo.lgn) + idx] = cmulc(gv, tw[(pa * pq) << (geo.lgn - lgLt)]);
+    }
+    __syncthreads();
+    for (int k = 0; k + 1 < S; ++k) {
+      LX_DISPATCH(geo.lgf[k], (lx_fwd_stage<F>(v + (size_t)k * R * n, v + (size_t)(k + 1) * R * n,
+                                               W + geo.off[k], geo.lgL[k], geo.lgn, R, tw)));
+      __syncthreads();
+    }
+    for (int k = S - 1; k >= 0; --k) {
+      LX_DISPATCH(geo.lgf[k], (lx_grad<F>(ga, v + (size_t)k * R * n, G + geo.off[k], red, geo.lgL[k],
+                                          geo.lgn, R)));
+      const int plgL = k > 0 ? geo.lgL[k - 1] : -1, plgf = k > 0 ? geo.lgf[k - 1] : 0;
+      LX_DISPATCH(geo.lgf[k], (lx_adj_stage<F>(ga, gb, W + geo.off[k], geo.lgL[k], geo.lgn, R, tw,
+                                               plgL, plgf)));
+      __syncthreads();
+      float2* tmp = ga;
+      ga = gb;
+      gb = tmp;
+    }
+    for (int i = threadIdx.x; i < rows * n; i += kLxThreads) {
+      const int r = i >> geo.lgn, e = i & (n - 1);
+      stc<IO>(dx + ((size_t)(b0 + r) * H + h) * 2 * n + 2 * e, ga[i]);
+    }
+  }
+  __syncthreads();
+  float2* dg = gpart + ((size_t)blockIdx.y * H + h) * P;
+  for (int i = threadIdx.x; i < P; i += kLxThreads) dg[i] = G[i];
+}
+
 __global__ void lb_reduce_kernel(const float2* __restrict__ gpart, float2* __restrict__ dblocks,
                                  int splits, size_t HP) {
   const size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -201,7 +476,24 @@ struct LbDevice {
   uint32_t* omap = nullptr;
   float2* tw = nullptr;
   LbStages st{};
+  bool fast = false;  // power-of-two factors <= 16: the lx_* kernels
+  LxGeo geo{};
 };
+
+// rows per pass for the fast kernels: the largest R in {4, 2, 1} whose smem
+// fits `budget` bytes
+inline int lx_rows(size_t fixed, size_t per_row, size_t budget) {
+  for (int R = 4; R >= 1; R >>= 1)
+    if (fixed + per_row * R <= budget) return R;
+  return 0;
+}
+inline size_t lx_fwd_fixed(const fb_learned_plan* p) { return (p->param_count + p->n) * sizeof(float2); }
+inline size_t lx_bwd_fixed(const fb_learned_plan* p) {
+  return (2 * p->param_count + p->n + (kLxThreads / 32) * kLxMaxF * kLxMaxF) * sizeof(float2);
+}
+inline size_t lx_bwd_per_row(const fb_learned_plan* p) {
+  return (size_t)(p->nstages + 2) * p->n * sizeof(float2);
+}
 
 }  // namespace fb
 
@@ -310,6 +602,25 @@ int fb_learned_plan_create(fb_learned_plan** out, int64_t n, int64_t r, int64_t 
     L /= f[i];
   }
   p->param_count = off;
+  {
+    bool fast = (n & (n - 1)) == 0;
+    for (int64_t fi : f) fast = fast && fi <= kLxMaxF && (fi & (fi - 1)) == 0 && fi >= 2;
+    LxGeo& gg = ext->dev.geo;
+    gg.nst = (int)f.size();
+    int lg = 0;
+    while ((int64_t(1) << lg) < n) ++lg;
+    gg.lgn = lg;
+    for (size_t i = 0; i < f.size(); ++i) {
+      int lf = 0;
+      while ((int64_t(1) << lf) < f[i]) ++lf;
+      int ll = 0;
+      while ((int64_t(1) << ll) < st.L[i]) ++ll;
+      gg.lgf[i] = lf;
+      gg.lgL[i] = ll;
+      gg.off[i] = st.off[i];
+    }
+    ext->dev.fast = fast && n >= 2;
+  }
   std::vector<uint32_t> om = output_map(n, f);
   std::vector<float2> tw((size_t)n);
   for (int64_t t = 0; t < n; ++t) {
@@ -358,10 +669,25 @@ int fb_learned_plan_factors(const fb_learned_plan* p, int64_t* factors, int64_t*
   return FB_OK;
 }
 
-// Row splits per head for the backward: enough CTAs to fill the SMs twice.
+static bool lx_fast_bwd(const fb_learned_plan* p) {
+  return ext_of(p)->dev.fast && lx_rows(lx_bwd_fixed(p), lx_bwd_per_row(p), 227 * 1024) > 0;
+}
+static int lx_bwd_R(const fb_learned_plan* p) {
+  // two CTAs per SM when two rows fit in half the smem, else as many rows as fit
+  const int R2 = lx_rows(lx_bwd_fixed(p), lx_bwd_per_row(p), 113 * 1024);
+  return R2 >= 2 ? R2 : lx_rows(lx_bwd_fixed(p), lx_bwd_per_row(p), 227 * 1024);
+}
+
+// Row splits per head for the backward: enough CTAs to fill the SMs (a few
+// waves), each split a whole number of the fast kernel's R-row passes.
 static int lb_splits(const fb_learned_plan* p, int64_t B) {
   int dev_sms = 148;
   cudaDeviceGetAttribute(&dev_sms, cudaDevAttrMultiProcessorCount, p->device);
+  if (lx_fast_bwd(p)) {
+    const int64_t R = lx_bwd_R(p), passes = (B + R - 1) / R;
+    int64_t s = (4 * dev_sms + p->H - 1) / p->H;
+    return (int)std::max<int64_t>(1, std::min<int64_t>(s, passes));
+  }
   int64_t s = (2 * dev_sms + p->H - 1) / p->H;
   return (int)std::max<int64_t>(1, std::min<int64_t>(s, B));
 }
@@ -385,6 +711,26 @@ int fb_learned_fwd(fb_learned_plan* p, const float* blocks, const void* x, void*
   if (rc) return rc;
   fb_learned_ext* ext = ext_of(p);
   cudaStream_t s = (cudaStream_t)stream;
+  if (ext->dev.fast) {
+    const int R = lx_rows(lx_fwd_fixed(p), 2 * p->n * sizeof(float2), 113 * 1024) > 0
+                      ? lx_rows(lx_fwd_fixed(p), 2 * p->n * sizeof(float2), 113 * 1024)
+                      : lx_rows(lx_fwd_fixed(p), 2 * p->n * sizeof(float2), 227 * 1024);
+    if (R > 0) {
+      const size_t sm = lx_fwd_fixed(p) + 2 * (size_t)R * p->n * sizeof(float2);
+      const dim3 g((unsigned)p->H, (unsigned)((B + R - 1) / R));
+      auto go = [&](auto io) {
+        using IO = decltype(io);
+        auto k = lx_fwd_kernel<IO>;
+        cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+        k<<<g, kLxThreads, sm, s>>>(blocks, (const IO*)x, (IO*)y, ext->dev.omap, ext->dev.tw,
+                                    ext->dev.geo, (int)B, (int)p->H, (int)p->param_count, R);
+      };
+      if (p->dtype == FB_F32) go(float{});
+      else if (p->dtype == FB_BF16) go(__nv_bfloat16{});
+      else go(__half{});
+      return cuda_status(cudaGetLastError(), "fb_learned_fwd");
+    }
+  }
   const size_t sm = (p->param_count + 2 * p->n) * sizeof(float2);
   const int rows = 4;
   const dim3 g((unsigned)p->H, (unsigned)((B + rows - 1) / rows));
@@ -421,6 +767,27 @@ int fb_learned_bwd(fb_learned_plan* p, const float* blocks, const void* x, const
     return FB_ERR_ARG;
   }
   const int splits = lb_splits(p, B);
+  if (lx_fast_bwd(p)) {
+    const int R = lx_bwd_R(p);
+    const int64_t passes = (B + R - 1) / R;
+    const int rps = (int)(((passes + splits - 1) / splits) * R);
+    const size_t sm = lx_bwd_fixed(p) + lx_bwd_per_row(p) * R;
+    auto go = [&](auto io) {
+      using IO = decltype(io);
+      auto k = lx_bwd_kernel<IO>;
+      cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+      k<<<dim3((unsigned)p->H, (unsigned)splits), kLxThreads, sm, s>>>(
+          blocks, (const IO*)x, (const IO*)g, (IO*)dx, (float2*)ws, ext->dev.omap, ext->dev.tw,
+          ext->dev.geo, (int)B, (int)p->H, (int)p->param_count, R, rps);
+    };
+    if (p->dtype == FB_F32) go(float{});
+    else if (p->dtype == FB_BF16) go(__nv_bfloat16{});
+    else go(__half{});
+    const size_t HP = (size_t)p->H * p->param_count;
+    lb_reduce_kernel<<<(unsigned)((HP + 255) / 256), 256, 0, s>>>((const float2*)ws,
+                                                                 (float2*)dblocks, splits, HP);
+    return cuda_status(cudaGetLastError(), "fb_learned_bwd");
+  }
   const int rows = (int)((B + splits - 1) / splits);
   const size_t sm = (2 * p->param_count + kLbThreads + (p->nstages + 2) * p->n) * sizeof(float2);
   if (sm > 227 * 1024) {
