@@ -231,7 +231,11 @@ __device__ __forceinline__ void lx_fwd_stage(const float2* __restrict__ src, flo
   constexpr int LGF = Lg2<F>::v;
   const int lgrest = lgL - LGF, lgcpr = lgn - LGF;
   const int C = R << lgcpr;
-  for (int col = threadIdx.x; col < C; col += kLxThreads) {
+  // fewer columns than threads: split each column's F outputs over `sp` threads
+  const int sp = C >= kLxThreads ? 1 : min(F, kLxThreads / C);
+  const int part = threadIdx.x / C, per = F / sp;
+  if (part >= sp) return;
+  for (int col = threadIdx.x % C; col < C; col += kLxThreads / sp) {
     const int base = lx_base(col, lgcpr, lgrest, lgL, lgn);
     const int ts = (col & ((1 << lgrest) - 1)) << (lgn - lgL);  // q n / L
     float2 x[F];
@@ -240,42 +244,52 @@ __device__ __forceinline__ void lx_fwd_stage(const float2* __restrict__ src, flo
     // one output row at a time: the W row is a broadcast load (all lanes read
     // the same entry), so a full unroll would only hoist F^2 registers
 #pragma unroll 1
-    for (int a = 0; a < F; ++a) {
+    for (int a = part * per; a < (part + 1) * per; ++a) {
       float ar = 0.f, ai = 0.f;
+      const float4* wr = reinterpret_cast<const float4*>(W + a * F);  // two entries per load
 #pragma unroll
-      for (int p = 0; p < F; ++p) {
-        const float2 w = W[a * F + p];
-        ar = fmaf(w.x, x[p].x, fmaf(-w.y, x[p].y, ar));
-        ai = fmaf(w.x, x[p].y, fmaf(w.y, x[p].x, ai));
+      for (int p = 0; p < F; p += 2) {
+        const float4 w2 = wr[p >> 1];
+        ar = fmaf(w2.x, x[p].x, fmaf(-w2.y, x[p].y, ar));
+        ai = fmaf(w2.x, x[p].y, fmaf(w2.y, x[p].x, ai));
+        ar = fmaf(w2.z, x[p + 1].x, fmaf(-w2.w, x[p + 1].y, ar));
+        ai = fmaf(w2.z, x[p + 1].y, fmaf(w2.w, x[p + 1].x, ai));
       }
       dst[base + (a << lgrest)] = cmul(make_float2(ar, ai), tw[a * ts]);
     }
   }
 }
 
-// g'[p] = sum_a conj(W[a][p]) w[a]; then (plgL >= 0) times conj of the lower
+// g'[p] = sum_a conj(W[a][p]) w[a] (WT = the stage block transposed); then
+// (plgL >= 0) times conj of the lower
 // stage's twiddle at that element, i.e. the lower stage's w
 template <int F>
 __device__ __forceinline__ void lx_adj_stage(const float2* __restrict__ w, float2* __restrict__ gout,
-                                             const float2* __restrict__ W, int lgL, int lgn, int R,
+                                             const float2* __restrict__ WT, int lgL, int lgn, int R,
                                              const float2* __restrict__ tw, int plgL, int plgf) {
   constexpr int LGF = Lg2<F>::v;
   const int lgrest = lgL - LGF, lgcpr = lgn - LGF;
   const int plgrest = plgL - plgf;
   const int C = R << lgcpr;
-  for (int col = threadIdx.x; col < C; col += kLxThreads) {
+  const int sp = C >= kLxThreads ? 1 : min(F, kLxThreads / C);
+  const int part = threadIdx.x / C, per = F / sp;
+  if (part >= sp) return;
+  for (int col = threadIdx.x % C; col < C; col += kLxThreads / sp) {
     const int base = lx_base(col, lgcpr, lgrest, lgL, lgn);
     float2 v[F];
 #pragma unroll
     for (int a = 0; a < F; ++a) v[a] = w[base + (a << lgrest)];
 #pragma unroll 1
-    for (int p = 0; p < F; ++p) {
+    for (int p = part * per; p < (part + 1) * per; ++p) {
       float ar = 0.f, ai = 0.f;
+      const float4* wr = reinterpret_cast<const float4*>(WT + p * F);  // W^T row p
 #pragma unroll
-      for (int a = 0; a < F; ++a) {
-        const float2 m = W[a * F + p];  // conj(m) v
-        ar = fmaf(m.x, v[a].x, fmaf(m.y, v[a].y, ar));
-        ai = fmaf(m.x, v[a].y, fmaf(-m.y, v[a].x, ai));
+      for (int a = 0; a < F; a += 2) {
+        const float4 m2 = wr[a >> 1];  // conj(m) v
+        ar = fmaf(m2.x, v[a].x, fmaf(m2.y, v[a].y, ar));
+        ai = fmaf(m2.x, v[a].y, fmaf(-m2.y, v[a].x, ai));
+        ar = fmaf(m2.z, v[a + 1].x, fmaf(m2.w, v[a + 1].y, ar));
+        ai = fmaf(m2.z, v[a + 1].y, fmaf(-m2.w, v[a + 1].x, ai));
       }
       const int idx = base + (p << lgrest);
       float2 o = make_float2(ar, ai);
@@ -403,10 +417,10 @@ __global__ void __launch_bounds__(kLxThreads)
   extern __shared__ __align__(16) float2 lsm[];
   const int n = 1 << geo.lgn, S = geo.nst;
   float2* W = lsm;
-  float2* G = W + P;
+  float2* WT = W + P;  // per stage block transposed (the adjoint's rows)
+  float2* G = WT + P;
   float2* tw = G + P;
-  float2* red = tw + n;                                    // [8 warps][16 x 16]
-  float2* v = red + (kLxThreads / 32) * kLxMaxF * kLxMaxF;  // [S][R n] stage inputs
+  float2* v = tw + n;  // [S][R n] stage inputs
   float2* ga = v + (size_t)S * R * n;
   float2* gb = ga + (size_t)R * n;
   const int h = blockIdx.x;
@@ -414,6 +428,10 @@ __global__ void __launch_bounds__(kLxThreads)
   for (int i = threadIdx.x; i < P; i += kLxThreads) {
     W[i] = wg[i];
     G[i] = make_float2(0.f, 0.f);
+  }
+  for (int k = 0; k < S; ++k) {
+    const int f = 1 << geo.lgf[k], o = geo.off[k];
+    for (int i = threadIdx.x; i < f * f; i += kLxThreads) WT[o + (i % f) * f + i / f] = wg[o + i];
   }
   for (int i = threadIdx.x; i < n; i += kLxThreads) tw[i] = __ldg(tw_g + i);
   const int lgLt = geo.lgL[S - 1], lgft = geo.lgf[S - 1];
@@ -443,10 +461,12 @@ __global__ void __launch_bounds__(kLxThreads)
       __syncthreads();
     }
     for (int k = S - 1; k >= 0; --k) {
-      LX_DISPATCH(geo.lgf[k], (lx_grad<F>(ga, v + (size_t)k * R * n, G + geo.off[k], red, geo.lgL[k],
+      // gb is free until the adjoint pass: it holds the gradient pass's
+      // per-warp partials (R n >= 8 f^2 is a condition of the fast path)
+      LX_DISPATCH(geo.lgf[k], (lx_grad<F>(ga, v + (size_t)k * R * n, G + geo.off[k], gb, geo.lgL[k],
                                           geo.lgn, R)));
       const int plgL = k > 0 ? geo.lgL[k - 1] : -1, plgf = k > 0 ? geo.lgf[k - 1] : 0;
-      LX_DISPATCH(geo.lgf[k], (lx_adj_stage<F>(ga, gb, W + geo.off[k], geo.lgL[k], geo.lgn, R, tw,
+      LX_DISPATCH(geo.lgf[k], (lx_adj_stage<F>(ga, gb, WT + geo.off[k], geo.lgL[k], geo.lgn, R, tw,
                                                plgL, plgf)));
       __syncthreads();
       float2* tmp = ga;
@@ -482,14 +502,20 @@ struct LbDevice {
 
 // rows per pass for the fast kernels: the largest R in {4, 2, 1} whose smem
 // fits `budget` bytes
-inline int lx_rows(size_t fixed, size_t per_row, size_t budget) {
-  for (int R = 4; R >= 1; R >>= 1)
-    if (fixed + per_row * R <= budget) return R;
+inline int lx_rows(size_t fixed, size_t per_row, size_t budget, int64_t min_elems = 0,
+                   int64_t n = 1) {
+  for (int R = 8; R >= 1; R >>= 1)
+    if (fixed + per_row * R <= budget && R * n >= min_elems) return R;
   return 0;
+}
+inline int64_t lx_maxf(const fb_learned_plan* p) {
+  int64_t m = 0;
+  for (int i = 0; i < p->nstages; ++i) m = std::max(m, p->factors[i]);
+  return m;
 }
 inline size_t lx_fwd_fixed(const fb_learned_plan* p) { return (p->param_count + p->n) * sizeof(float2); }
 inline size_t lx_bwd_fixed(const fb_learned_plan* p) {
-  return (2 * p->param_count + p->n + (kLxThreads / 32) * kLxMaxF * kLxMaxF) * sizeof(float2);
+  return (3 * p->param_count + p->n) * sizeof(float2);
 }
 inline size_t lx_bwd_per_row(const fb_learned_plan* p) {
   return (size_t)(p->nstages + 2) * p->n * sizeof(float2);
@@ -669,13 +695,15 @@ int fb_learned_plan_factors(const fb_learned_plan* p, int64_t* factors, int64_t*
   return FB_OK;
 }
 
+static int lx_bwd_R(const fb_learned_plan* p);
 static bool lx_fast_bwd(const fb_learned_plan* p) {
-  return ext_of(p)->dev.fast && lx_rows(lx_bwd_fixed(p), lx_bwd_per_row(p), 227 * 1024) > 0;
+  return ext_of(p)->dev.fast && lx_bwd_R(p) > 0;
 }
 static int lx_bwd_R(const fb_learned_plan* p) {
   // two CTAs per SM when two rows fit in half the smem, else as many rows as fit
-  const int R2 = lx_rows(lx_bwd_fixed(p), lx_bwd_per_row(p), 113 * 1024);
-  return R2 >= 2 ? R2 : lx_rows(lx_bwd_fixed(p), lx_bwd_per_row(p), 227 * 1024);
+  const int64_t red = (kLxThreads / 32) * lx_maxf(p) * lx_maxf(p);  // gradient partials in gb
+  const int R2 = lx_rows(lx_bwd_fixed(p), lx_bwd_per_row(p), 113 * 1024, red, p->n);
+  return R2 >= 2 ? R2 : lx_rows(lx_bwd_fixed(p), lx_bwd_per_row(p), 227 * 1024, red, p->n);
 }
 
 // Row splits per head for the backward: enough CTAs to fill the SMs (a few
@@ -685,7 +713,7 @@ static int lb_splits(const fb_learned_plan* p, int64_t B) {
   cudaDeviceGetAttribute(&dev_sms, cudaDevAttrMultiProcessorCount, p->device);
   if (lx_fast_bwd(p)) {
     const int64_t R = lx_bwd_R(p), passes = (B + R - 1) / R;
-    int64_t s = (4 * dev_sms + p->H - 1) / p->H;
+    int64_t s = (16 * dev_sms + p->H - 1) / p->H;  // many small CTAs: loads overlap compute
     return (int)std::max<int64_t>(1, std::min<int64_t>(s, passes));
   }
   int64_t s = (2 * dev_sms + p->H - 1) / p->H;
