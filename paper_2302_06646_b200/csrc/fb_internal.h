@@ -1,5 +1,6 @@
 // FlashButterfly-B200: host-side plan object and internal launcher API.
 #pragma once
+#include <cuda.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -62,6 +63,10 @@ struct SpartMap {
 };
 int sp_finalize(fb_plan* p, const float2* spart, const float* ddpart, int chunks, float* dkbar,
                 float* dD, float* dK, int dd_lag0, const SpartMap* map, cudaStream_t s);
+
+// Unswizzled 3-D TMA tensor map (fb_single_tc.cu)
+int encode_map_3d(CUtensorMap* map, CUtensorMapDataType type, const void* ptr, const uint64_t dims[3],
+                  const uint64_t strides[2], const uint32_t box[3]);
 
 // tcgen05 single-pass (fb_single_tc.cu)
 bool tc_eligible(const fb_plan* p);

@@ -821,6 +821,33 @@ EncodeFn encode_fn() {
   return fn;
 }
 
+}  // namespace
+
+// Plain (unswizzled) 3-D tiled tensor map, shared with the three-pass column
+// kernels: dims {d0, d1, d2} elements of `esize` bytes, row strides in bytes.
+int encode_map_3d(CUtensorMap* map, CUtensorMapDataType type, const void* ptr, const uint64_t dims[3],
+                  const uint64_t strides[2], const uint32_t box[3]) {
+  EncodeFn enc = encode_fn();
+  if (!enc) {
+    set_error("cuTensorMapEncodeTiled unavailable");
+    return FB_ERR_CUDA;
+  }
+  const cuuint64_t d[3] = {dims[0], dims[1], dims[2]};
+  const cuuint64_t st[2] = {strides[0], strides[1]};
+  const cuuint32_t bx[3] = {box[0], box[1], box[2]};
+  const cuuint32_t es[3] = {1, 1, 1};
+  CUresult r = enc(map, type, 3, const_cast<void*>(ptr), d, st, bx, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                   CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) {
+    set_error("cuTensorMapEncodeTiled (3-D) failed (" + std::to_string((int)r) + ")");
+    return FB_ERR_CUDA;
+  }
+  return FB_OK;
+}
+
+namespace {
+
 // signal [B][H][4096] viewed as [B][H][32 t1][128 t2]; box [64 t2][32 t1][1][1]
 template <typename T>
 int make_map(CUtensorMap* map, const void* ptr, int64_t B, int64_t H) {

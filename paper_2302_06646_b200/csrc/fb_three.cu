@@ -19,6 +19,7 @@
 // passes 1/3 give one column tau per thread (consecutive threads =
 // consecutive tau), pass 2 moves whole rows by TMA bulk copies.
 #include <algorithm>
+#include <type_traits>
 
 #include "fb_common.cuh"
 #include "fb_fft.cuh"
@@ -325,6 +326,189 @@ __global__ void __launch_bounds__(kColThreads)
   }
 }
 
+// ---------------------------------------------------------------- streaming column passes
+// Passes 1 and 3 for m <= 16 as persistent streaming kernels: a CTA walks
+// tiles of TB = 256 columns tau of one (pair, head); each tile's input rows
+// arrive by 3-D TMA boxes into a ring of smem stages (kColStages tiles in
+// flight per CTA), so HBM latency is hidden behind the other tiles instead of
+// each thread's 16 dependent loads.  Thread j owns column tau = tile + j:
+// column DFT + twiddle in registers, coalesced stores.
+constexpr uint32_t kTB = 256;  // columns per tile (= threads)
+constexpr int kColMaxStages = 4;
+
+__device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, int c0, int c1, int c2,
+                                            uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, "
+      "%3, %4}], [%5];" ::"r"(ptx::smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(ptx::smem_u32(bar))
+      : "memory");
+}
+
+// tile t -> (pair, head, column block): column blocks fastest
+struct ColTile {
+  int pr, h, tb;
+};
+__device__ __forceinline__ ColTile col_tile(int t, int H) {
+  constexpr int NB = kL / kTB;
+  ColTile c;
+  c.tb = t % NB;
+  c.h = (t / NB) % H;
+  c.pr = t / (NB * H);
+  return c;
+}
+
+// Pass 1, SRC 0: signal pairs (channels 2 pr, 2 pr + 1 -> re, im);
+// SRC 1: dy and u pairs at once, plus the lag-0 dD partial.  Signal maps view
+// [B*H][rows][l] with rows = N / l data rows (the causal pad is implicit).
+template <typename IO, typename ST, int M, int SRC>
+__global__ void __launch_bounds__(kTB)
+    tp_col1_kernel(const __grid_constant__ CUtensorMap amap, const __grid_constant__ CUtensorMap bmap,
+                   CxT<ST>* __restrict__ out_a, CxT<ST>* __restrict__ out_b,
+                   float* __restrict__ ddpart, const float2* __restrict__ tab_g, int H, int npairs,
+                   int rows, int ntiles, int nstages) {
+  extern __shared__ __align__(128) unsigned char csm[];
+  __shared__ __align__(8) uint64_t full[kColMaxStages];
+  __shared__ float red[kTB / 32];
+  constexpr int NCH = SRC == 1 ? 4 : 2;
+  const uint32_t chb = (uint32_t)rows * kTB * sizeof(IO);
+  const uint32_t stage_bytes = NCH * chb;
+  const int j = threadIdx.x;
+  if (j == 0) {
+    for (int i = 0; i < nstages; ++i) ptx::mbar_init(&full[i], 1);
+    ptx::fence_barrier_init();
+  }
+  __syncthreads();
+  auto issue = [&](int t, int st) {
+    const ColTile c = col_tile(t, H);
+    unsigned char* dst = csm + (size_t)st * stage_bytes;
+    ptx::mbar_arrive_expect_tx(&full[st], stage_bytes);
+#pragma unroll
+    for (int ch = 0; ch < NCH; ++ch) {
+      const CUtensorMap* mp = (SRC == 1 && ch >= 2) ? &bmap : &amap;
+      const int b = 2 * c.pr + (ch & 1);
+      tma_load_3d(dst + ch * chb, mp, c.tb * (int)kTB, 0, b * H + c.h, &full[st]);
+    }
+  };
+  const int first = blockIdx.x, step = gridDim.x;
+  if (j == 0)
+    for (int i = 0; i < nstages - 1; ++i)
+      if (first + i * step < ntiles) issue(first + i * step, i);
+  int it = 0;
+  for (int t = first; t < ntiles; t += step, ++it) {
+    const int sg = it % nstages;
+    if (j == 0 && t + (nstages - 1) * step < ntiles) issue(t + (nstages - 1) * step, (it + nstages - 1) % nstages);
+    ptx::mbar_wait(&full[sg], (uint32_t)(it / nstages) & 1);
+    const ColTile c = col_tile(t, H);
+    const uint32_t tau = c.tb * kTB + j;
+    const IO* sv = reinterpret_cast<const IO*>(csm + (size_t)sg * stage_bytes);
+    auto column = [&](int ch0, float2 (&v)[M]) {
+#pragma unroll
+      for (int r = 0; r < M; ++r) {
+        const bool ok = r < rows;
+        v[r].x = ok ? tof(sv[(ch0 * rows + r) * kTB + j]) : 0.f;
+        v[r].y = ok ? tof(sv[((ch0 + 1) * rows + r) * kTB + j]) : 0.f;
+      }
+    };
+    float2 v[M];
+    column(0, v);
+    float dd = 0.f;
+    if constexpr (SRC == 1) {
+      float2 w[M];
+      column(2, w);
+#pragma unroll
+      for (int r = 0; r < M; ++r) dd = fmaf(v[r].x, w[r].x, fmaf(v[r].y, w[r].y, dd));
+      dft_reg<-1, M>(w);
+      apply_tw_g<-1, M>(w, tab_g, tau);
+      CxT<ST>* ob = out_b + ((size_t)c.pr * H + c.h) * (size_t)M * kL;
+#pragma unroll
+      for (int a = 0; a < M; ++a) stc<ST>(&ob[a * kL + tau].x, w[a]);
+    }
+    dft_reg<-1, M>(v);
+    apply_tw_g<-1, M>(v, tab_g, tau);
+    CxT<ST>* oa = out_a + ((size_t)c.pr * H + c.h) * (size_t)M * kL;
+#pragma unroll
+    for (int a = 0; a < M; ++a) stc<ST>(&oa[a * kL + tau].x, v[a]);
+    if constexpr (SRC == 1) {
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) dd += __shfl_xor_sync(0xffffffffu, dd, o);
+      if ((j & 31) == 0) red[j >> 5] = dd;
+    }
+    __syncthreads();  // stage sg fully read (and red written) before reuse
+    if constexpr (SRC == 1) {
+      if (j == 0) {
+        float s = 0.f;
+        for (int w2 = 0; w2 < (int)(kTB / 32); ++w2) s += red[w2];
+        ddpart[((size_t)c.h * npairs + c.pr) * (kL / kTB) + c.tb] = s;
+      }
+    }
+  }
+}
+
+// Pass 3 (MODE 0): W rows [pair*H + h][M][l] (complex ST) -> out[b][h][c l + tau]
+// = Re/Im(column IDFT) + D[h] skip[b][h][c l + tau], c < rows.
+template <typename ST, typename IO, int M>
+__global__ void __launch_bounds__(kTB)
+    tp_col3_kernel(const __grid_constant__ CUtensorMap wmap, const __grid_constant__ CUtensorMap smap,
+                   IO* __restrict__ out, const float* __restrict__ D,
+                   const float2* __restrict__ tab_g, int B, int H, uint32_t N, int rows, int ntiles,
+                   int nstages) {
+  extern __shared__ __align__(128) unsigned char csm[];
+  __shared__ __align__(8) uint64_t full[kColMaxStages];
+  const uint32_t wb = M * kTB * sizeof(CxT<ST>);
+  const uint32_t chb = (uint32_t)rows * kTB * sizeof(IO);
+  const uint32_t stage_bytes = wb + 2 * chb;
+  const int j = threadIdx.x;
+  if (j == 0) {
+    for (int i = 0; i < nstages; ++i) ptx::mbar_init(&full[i], 1);
+    ptx::fence_barrier_init();
+  }
+  __syncthreads();
+  auto issue = [&](int t, int st) {
+    const ColTile c = col_tile(t, H);
+    unsigned char* dst = csm + (size_t)st * stage_bytes;
+    ptx::mbar_arrive_expect_tx(&full[st], stage_bytes);
+    tma_load_3d(dst, &wmap, c.tb * (int)kTB, 0, c.pr * H + c.h, &full[st]);
+#pragma unroll
+    for (int ch = 0; ch < 2; ++ch)
+      tma_load_3d(dst + wb + ch * chb, &smap, c.tb * (int)kTB, 0, (2 * c.pr + ch) * H + c.h,
+                  &full[st]);
+  };
+  const int first = blockIdx.x, step = gridDim.x;
+  if (j == 0)
+    for (int i = 0; i < nstages - 1; ++i)
+      if (first + i * step < ntiles) issue(first + i * step, i);
+  int it = 0;
+  for (int t = first; t < ntiles; t += step, ++it) {
+    const int sg = it % nstages;
+    if (j == 0 && t + (nstages - 1) * step < ntiles) issue(t + (nstages - 1) * step, (it + nstages - 1) % nstages);
+    ptx::mbar_wait(&full[sg], (uint32_t)(it / nstages) & 1);
+    const ColTile c = col_tile(t, H);
+    const uint32_t tau = c.tb * kTB + j;
+    const unsigned char* base = csm + (size_t)sg * stage_bytes;
+    const CxT<ST>* sw = reinterpret_cast<const CxT<ST>*>(base);
+    const IO* sk = reinterpret_cast<const IO*>(base + wb);
+    float2 v[M];
+#pragma unroll
+    for (int a = 0; a < M; ++a) v[a] = cx_load(sw + a * kTB + j);
+    apply_tw_g<+1, M>(v, tab_g, tau);
+    dft_reg<+1, M>(v);
+    const int b0 = 2 * c.pr, b1 = b0 + 1;
+    const bool has1 = b1 < B;
+    const float d = __ldg(D + c.h);
+    const size_t o0 = ((size_t)b0 * H + c.h) * N, o1 = ((size_t)b1 * H + c.h) * N;
+#pragma unroll
+    for (int r = 0; r < M; ++r) {
+      if (r < rows) {
+        const uint32_t tt = r * kL + tau;
+        st(out + o0 + tt, fmaf(d, tof(sk[r * kTB + j]), v[r].x));
+        if (has1) st(out + o1 + tt, fmaf(d, tof(sk[(rows + r) * kTB + j]), v[r].y));
+      }
+    }
+    __syncthreads();
+  }
+}
+
 __global__ void tp_dd_reduce_kernel(const float* __restrict__ ddpart, float* __restrict__ dD,
                                     int per_head) {
   const int h = blockIdx.x;
@@ -509,11 +693,61 @@ size_t big_smem(int src) {
   return (size_t)(src == 1 ? 2 : 1) * padded_len(kBigTile) * sizeof(float2) + 64 * sizeof(float2);
 }
 
-// pass 1: register kernel for m <= 16, tiled smem kernel above
+template <typename T>
+constexpr CUtensorMapDataType tma_type() {
+  if constexpr (std::is_same<T, float>::value) return CU_TENSOR_MAP_DATA_TYPE_FLOAT32;
+  else if constexpr (std::is_same<T, __nv_bfloat16>::value) return CU_TENSOR_MAP_DATA_TYPE_BFLOAT16;
+  else return CU_TENSOR_MAP_DATA_TYPE_FLOAT16;
+}
+
+// signal [B][H][N] as [B*H][rows = N / l][l], box [256][rows][1]
+template <typename IO>
+int signal_map(CUtensorMap* m, const fb_plan* p, const IO* ptr, int B) {
+  const uint64_t rows = (uint64_t)(p->N / kL);
+  const uint64_t dims[3] = {kL, rows, (uint64_t)B * p->H};
+  const uint64_t strides[2] = {kL * sizeof(IO), (uint64_t)p->N * sizeof(IO)};
+  const uint32_t box[3] = {kTB, (uint32_t)rows, 1};
+  return encode_map_3d(m, tma_type<IO>(), ptr, dims, strides, box);
+}
+// intermediates [npairs*H][m][l] complex, box [256][m][1]
+template <typename ST>
+int inter_map(CUtensorMap* mp, const fb_plan* p, const CxT<ST>* ptr, int npairs) {
+  constexpr size_t es = sizeof(CxT<ST>);
+  const uint64_t dims[3] = {kL, (uint64_t)p->m, (uint64_t)npairs * p->H};
+  const uint64_t strides[2] = {kL * es, (uint64_t)p->m * kL * es};
+  const uint32_t box[3] = {kTB, (uint32_t)p->m, 1};
+  return encode_map_3d(mp, es == 4 ? CU_TENSOR_MAP_DATA_TYPE_UINT32 : CU_TENSOR_MAP_DATA_TYPE_UINT64,
+                       ptr, dims, strides, box);
+}
+int col_stages(size_t stage_bytes) {
+  return (int)std::max<size_t>(2, std::min<size_t>(kColMaxStages, (96 * 1024) / stage_bytes));
+}
+
+// pass 1: streaming TMA column kernel (signals, m <= 16), register kernel for
+// the kernel bank, tiled smem kernel for m > 16
 template <typename IO, typename ST, int SRC>
 uint32_t launch_pass1(const fb_plan* p, const IO* a, const IO* b, CxT<ST>* oa, CxT<ST>* ob,
                       float* ddpart, int B, int npairs, cudaStream_t s) {
   const int causal = p->mode == FB_MODE_CAUSAL;
+  if constexpr (SRC != 2) {
+    if (p->m <= 16) {
+      CUtensorMap am, bm;
+      const bool maps = !signal_map<IO>(&am, p, a, B) && !signal_map<IO>(&bm, p, SRC == 1 ? b : a, B);
+      const int rows = (int)(p->N / kL);
+      const size_t stage = (size_t)(SRC == 1 ? 4 : 2) * rows * kTB * sizeof(IO);
+      const int ns = col_stages(stage);
+      const int ntiles = (int)(npairs * p->H * (kL / kTB));
+      const int grid = std::min(ntiles, 2 * p->num_sms);
+      if (maps) with_m(p->m, [&](auto mc) {
+        constexpr int M = decltype(mc)::value;
+        auto k = tp_col1_kernel<IO, ST, M, SRC>;
+        cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(stage * ns));
+        k<<<grid, kTB, stage * ns, s>>>(am, bm, oa, ob, ddpart, p->tw_n, (int)p->H, npairs, rows,
+                                        ntiles, ns);
+      });
+      if (maps) return kL / kTB;
+    }
+  }
   if (p->m <= 16) {
     with_m(p->m, [&](auto mc) {
       constexpr int M = decltype(mc)::value;
@@ -540,6 +774,25 @@ template <typename ST, typename IO, int MODE>
 void launch_pass3(const fb_plan* p, const CxT<ST>* w, const IO* skip, IO* out, float* dkbar,
                   int B, int npairs, float scale, cudaStream_t s) {
   const int causal = p->mode == FB_MODE_CAUSAL;
+  if constexpr (MODE == 0) {
+    if (p->m <= 16) {
+      CUtensorMap wm, sm;
+      const bool maps = !inter_map<ST>(&wm, p, w, npairs) && !signal_map<IO>(&sm, p, skip, B);
+      const int rows = (int)(p->N / kL);
+      const size_t stage = p->m * kTB * sizeof(CxT<ST>) + 2 * (size_t)rows * kTB * sizeof(IO);
+      const int ns = col_stages(stage);
+      const int ntiles = (int)(npairs * p->H * (kL / kTB));
+      const int grid = std::min(ntiles, 2 * p->num_sms);
+      if (maps) with_m(p->m, [&](auto mc) {
+        constexpr int M = decltype(mc)::value;
+        auto k = tp_col3_kernel<ST, IO, M>;
+        cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(stage * ns));
+        k<<<grid, kTB, stage * ns, s>>>(wm, sm, out, p->d, p->tw_n, B, (int)p->H, (uint32_t)p->N,
+                                        rows, ntiles, ns);
+      });
+      if (maps) return;  // else: the register column kernel below
+    }
+  }
   if (p->m <= 16) {
     with_m(p->m, [&](auto mc) {
       constexpr int M = decltype(mc)::value;
