@@ -91,6 +91,65 @@ __global__ void regularizer_backward_kernel(const float* __restrict__ kbar,
                           keep_scale, freq);
 }
 
+// Time-domain fast path (smooth width p <= kRegHalo): a CTA stages a tile of
+// the row (plus the +-p halo) in smem once and every output reads its window
+// from there, with 32-bit indexing; same fp64 arithmetic and summation order
+// as reg_value / reg_grad.
+constexpr int kRegTile = 2048, kRegHalo = 32, kRegThreads = 256;
+
+__global__ void __launch_bounds__(kRegThreads)
+    regularize_tile_kernel(const float* __restrict__ K, const uint8_t* __restrict__ keep,
+                           float* __restrict__ kbar, int N, int p, double lambda, double keep_scale) {
+  __shared__ double sk[kRegTile + 2 * kRegHalo];
+  const size_t base = (size_t)blockIdx.y * N;
+  const int t0 = blockIdx.x * kRegTile;
+  for (int i = threadIdx.x; i < kRegTile + 2 * p; i += kRegThreads) {
+    const int t = t0 - p + i;
+    sk[i] = (t >= 0 && t < N) ? dropped(K, keep, keep_scale, base + t) : 0.0;
+  }
+  __syncthreads();
+  const double inv_w = 1.0 / (double)(2 * p + 1);
+  for (int i = threadIdx.x; i < kRegTile; i += kRegThreads) {
+    const int t = t0 + i;
+    if (t >= N) break;
+    const int lo = t >= p ? -p : -t;
+    const int hi = (t + p < N - 1) ? p : N - 1 - t;
+    double acc = 0.0;
+    for (int d = lo; d <= hi; ++d) acc += sk[i + p + d];
+    const double sv = acc * inv_w;
+    const double mag = fabs(sv) - lambda;
+    kbar[base + t] = mag > 0.0 ? (float)copysign(mag, sv) : 0.0f;
+  }
+}
+
+__global__ void __launch_bounds__(kRegThreads)
+    regularizer_backward_tile_kernel(const float* __restrict__ kbar, const float* __restrict__ dkbar,
+                                     const uint8_t* __restrict__ keep, float* __restrict__ dK, int N,
+                                     int p, double keep_scale) {
+  __shared__ double sg[kRegTile + 2 * kRegHalo];  // 1[kbar != 0] dkbar
+  const size_t base = (size_t)blockIdx.y * N;
+  const int t0 = blockIdx.x * kRegTile;
+  for (int i = threadIdx.x; i < kRegTile + 2 * p; i += kRegThreads) {
+    const int t = t0 - p + i;
+    double g = 0.0;
+    if (t >= 0 && t < N && __ldg(kbar + base + t) != 0.f) g = (double)__ldg(dkbar + base + t);
+    sg[i] = g;
+  }
+  __syncthreads();
+  const double w = (double)(2 * p + 1);
+  for (int i = threadIdx.x; i < kRegTile; i += kRegThreads) {
+    const int t = t0 + i;
+    if (t >= N) break;
+    const int lo = t >= p ? -p : -t;
+    const int hi = (t + p < N - 1) ? p : N - 1 - t;
+    double acc = 0.0;
+    for (int d = lo; d <= hi; ++d) acc += sg[i + p + d];
+    double g = acc / w;
+    if (keep) g = keep[base + t] ? g * keep_scale : 0.0;
+    dK[base + t] = (float)g;
+  }
+}
+
 int dropout_keep_dev(fb_plan* p, double rate, uint64_t seed, cudaStream_t s) {
   dropout_keep_kernel<<<(unsigned)((p->H + 127) / 128), 128, 0, s>>>(p->keep, (int)p->H, p->N,
                                                                        rate, seed);
@@ -98,6 +157,12 @@ int dropout_keep_dev(fb_plan* p, double rate, uint64_t seed, cudaStream_t s) {
 }
 
 int regularize_bank_dev(fb_plan* p, const float* K, cudaStream_t s) {
+  if (p->smooth_domain != FB_SMOOTH_FREQUENCY && p->p <= kRegHalo && p->N < (int64_t(1) << 30)) {
+    const dim3 g((unsigned)((p->N + kRegTile - 1) / kRegTile), (unsigned)p->H);
+    regularize_tile_kernel<<<g, kRegThreads, 0, s>>>(K, p->use_keep ? p->keep : nullptr, p->kbar,
+                                                     (int)p->N, (int)p->p, p->lambda, p->keep_scale);
+    return cuda_status(cudaGetLastError(), "regularize_bank");
+  }
   const dim3 g((unsigned)p->H, (unsigned)((p->N + 255) / 256));
   regularize_kernel<<<g, 256, 0, s>>>(K, p->use_keep ? p->keep : nullptr, p->kbar, p->N, p->p,
                                       p->lambda, p->keep_scale,
@@ -106,6 +171,12 @@ int regularize_bank_dev(fb_plan* p, const float* K, cudaStream_t s) {
 }
 
 int regularizer_backward_dev(fb_plan* p, const float* dkbar, float* dK, cudaStream_t s) {
+  if (p->smooth_domain != FB_SMOOTH_FREQUENCY && p->p <= kRegHalo && p->N < (int64_t(1) << 30)) {
+    const dim3 g((unsigned)((p->N + kRegTile - 1) / kRegTile), (unsigned)p->H);
+    regularizer_backward_tile_kernel<<<g, kRegThreads, 0, s>>>(
+        p->kbar, dkbar, p->use_keep ? p->keep : nullptr, dK, (int)p->N, (int)p->p, p->keep_scale);
+    return cuda_status(cudaGetLastError(), "regularizer_backward");
+  }
   const dim3 g((unsigned)p->H, (unsigned)((p->N + 255) / 256));
   regularizer_backward_kernel<<<g, 256, 0, s>>>(p->kbar, dkbar, p->use_keep ? p->keep : nullptr,
                                                 dK, p->N, p->p, p->keep_scale,
