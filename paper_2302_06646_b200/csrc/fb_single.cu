@@ -74,8 +74,10 @@ __device__ __forceinline__ void load_table(float2* tab, const float2* __restrict
 // as a flat spectrum, k_f' = k_f + D/n, as fp16 pairs scaled by the power
 // of two that brings the head's largest component to <= 2^15; kf_scale[h]
 // is the inverse (the tensor-core kernels fold it into their output).
+// (two CTAs per SM: one wave for H <= 2 x the SM count; per-head work is a
+// latency-bound chain, so co-residency is what hides it)
 template <int LOG2N>
-__global__ void __launch_bounds__(FftShape<LOG2N>::T, 1)
+__global__ void __launch_bounds__(FftShape<LOG2N>::T, 2)
     sp_spectrum_kernel(const float* __restrict__ K, const uint8_t* __restrict__ keep,
                        float* __restrict__ kbar, float2* __restrict__ kf, __half2* __restrict__ kf_tc,
                        float* __restrict__ kf_scale, const float* __restrict__ D,
@@ -395,7 +397,7 @@ __global__ void __launch_bounds__(FftShape<LOG2N>::T, 1)
 // dK[h]; dD[h] = sum_c ddpart (SIMT) or the lag-0 correlation dKbar[h][0]
 // (tcgen05 path, where D is folded into k_f').  dkbar_out is optional.
 template <int LOG2N>
-__global__ void __launch_bounds__(FftShape<LOG2N>::T, 1)
+__global__ void __launch_bounds__(FftShape<LOG2N>::T, 2)
     sp_dk_finalize_kernel(const float2* __restrict__ spart, const float* __restrict__ ddpart,
                           int chunks, float* __restrict__ dkbar_out, float* __restrict__ dD,
                           const float* __restrict__ kbar, const uint8_t* __restrict__ keep,
