@@ -67,8 +67,15 @@ constexpr uint32_t SMAT = SOP + 2 * 32768;
 constexpr uint32_t MAT_FA = 0, MAT_FR = 16384, MAT_FI = 49152, MAT_BYTES = 81920;
 constexpr uint32_t STAB = SMAT + MAT_BYTES;
 constexpr uint32_t SKF = STAB + 2048;
-constexpr uint32_t SMEM_FWD = STAB + 1536;
 constexpr uint32_t SMEM_BWD = SKF + 32768;
+// Forward layout: three 16 KB operand planes per slot so each stage-B/B'
+// K-step is two N = 128 MMAs (a 2-plane window of [Xr | Xi] or [-Xi | Xr]
+// against Fr / Fi) instead of four N = 64 ones — 61 % vs 46 % of the tensor
+// peak (profiles/r01_microbench_tcgen05.md).
+constexpr uint32_t SOP3 = SIN + 2 * 16384;
+constexpr uint32_t SMAT3 = SOP3 + 2 * 49152;
+constexpr uint32_t STAB3 = SMAT3 + MAT_BYTES;
+constexpr uint32_t SMEM_FWD = STAB3 + 1536;
 
 __device__ __forceinline__ unsigned char* smem_base(unsigned char* raw) {
   if (reinterpret_cast<uintptr_t>(raw) & 1023) __trap();  // swizzle atoms need 1 KB alignment
@@ -131,6 +138,16 @@ __device__ __forceinline__ void st8(unsigned char* p, const float* v) {
   q.y = pack2<T>(v[2], v[3]);
   q.z = pack2<T>(v[4], v[5]);
   q.w = pack2<T>(v[6], v[7]);
+  *reinterpret_cast<uint4*>(p) = q;
+}
+
+template <typename T>
+__device__ __forceinline__ void st8n(unsigned char* p, const float* v) {
+  uint4 q;
+  q.x = pack2<T>(-v[0], -v[1]);
+  q.y = pack2<T>(-v[2], -v[3]);
+  q.z = pack2<T>(-v[4], -v[5]);
+  q.w = pack2<T>(-v[6], -v[7]);
   *reinterpret_cast<uint4*>(p) = q;
 }
 
@@ -211,6 +228,7 @@ struct Ctx {
   uint32_t aux;     // fwd: the slot's k_f' columns; bwd: the slot's parked-U columns
   uint32_t in_off;  // the slot's input buffer (bytes into smem)
   uint32_t sop;     // the slot's operand buffer
+  uint32_t smat;    // DFT blocks (bytes into smem)
   uint32_t bar_id;  // the slot's named barrier
   uint64_t* mma_bar;
   uint32_t mma_phase;
@@ -230,7 +248,7 @@ struct Ctx {
 };
 
 __device__ __forceinline__ Ctx make_ctx(unsigned char* sm, uint32_t tmem, uint32_t slot,
-                                        uint64_t* mma_bar) {
+                                        uint64_t* mma_bar, bool w3 = false) {
   Ctx c;
   c.sm = sm;
   c.smb = ptx::smem_u32(sm);
@@ -238,11 +256,12 @@ __device__ __forceinline__ Ctx make_ctx(unsigned char* sm, uint32_t tmem, uint32
   c.tw = 128 * slot;
   c.aux = 0;
   c.in_off = SIN + 16384 * slot;
-  c.sop = SOP + 32768 * slot;
+  c.sop = w3 ? SOP3 + 49152 * slot : SOP + 32768 * slot;
+  c.smat = w3 ? SMAT3 : SMAT;
   c.bar_id = 1 + slot;
   c.mma_bar = mma_bar;
   c.mma_phase = 0;
-  c.tab = reinterpret_cast<const float2*>(sm + STAB);
+  c.tab = reinterpret_cast<const float2*>(sm + (w3 ? STAB3 : STAB));
   c.slot = slot;
   c.other_bar = mma_bar + (slot ? -1 : 1);
   c.nb = c.seg0 = c.obase = c.on = 0;
@@ -282,17 +301,37 @@ __device__ __forceinline__ void mma_stage_A(const Ctx& c) {
 #pragma unroll
   for (uint32_t s = 0; s < 4; ++s) {
     const uint64_t ad = tc::smem_desc(c.smb + c.in_off + s * 2048, 1024, tc::kSw128, 8192);
-    const uint64_t bd = tc::smem_desc(c.smb + SMAT + MAT_FA + s * 32, 1024, tc::kSw128);
+    const uint64_t bd = tc::smem_desc(c.smb + c.smat + MAT_FA + s * 32, 1024, tc::kSw128);
     tc::mma_bf16(c.tmem + c.tw, ad, bd, id, s);
   }
 }
 // B / B': DFT128 with the data as the B operand (MN-major [kg][8][64] in the
 // slot's SOP, re plane then im plane 16 KB apart).  INV: conjugate block.
-template <typename T, bool INV>
+template <typename T, bool INV, bool W3>
 __device__ __forceinline__ void mma_stage_B(const Ctx& c) {
+  if constexpr (W3) {
+    // planes: forward [-Xi | Xr | Xi], inverse [Zr | Zi | -Zr] (16 KB each)
+    const uint32_t id = idesc<T>(128, 128, false, true, false);
+    const uint32_t fr = c.smb + c.smat + MAT_FR, fi = c.smb + c.smat + MAT_FI;
+    const uint32_t p0 = c.smb + c.sop, p1 = p0 + 16384;
+    const uint32_t d = c.tmem + c.tw;
+#pragma unroll
+    for (uint32_t s = 0; s < 8; ++s) {
+      const uint32_t ko = (s >> 2) * 16384 + (s & 3) * 32;
+      const uint64_t dr = tc::smem_desc(fr + ko, 1024, tc::kSw128);
+      const uint64_t di = tc::smem_desc(fi + ko, 1024, tc::kSw128);
+      const uint64_t w0 = tc::smem_desc(p0 + s * 2048, 1024, tc::kSw128, 16384);
+      const uint64_t w1 = tc::smem_desc(p1 + s * 2048, 1024, tc::kSw128, 16384);
+      // forward: [re | im] += Fr [Xr | Xi] + Fi [-Xi | Xr]
+      // inverse: [re | im] += Fr [Zr | Zi] + Fi [Zi | -Zr]
+      tc::mma_bf16(d, dr, INV ? w0 : w1, id, s);
+      tc::mma_bf16(d, di, INV ? w1 : w0, id, 1);
+    }
+    return;
+  }
   const uint32_t id_p = idesc<T>(128, 64, false, true, false);
   const uint32_t id_n = idesc<T>(128, 64, false, true, true);
-  const uint32_t fr = c.smb + SMAT + MAT_FR, fi = c.smb + SMAT + MAT_FI;
+  const uint32_t fr = c.smb + c.smat + MAT_FR, fi = c.smb + c.smat + MAT_FI;
   const uint32_t br = c.smb + c.sop, bi = br + 16384;
   const uint32_t d = c.tmem + c.tw;
 #pragma unroll
@@ -326,7 +365,7 @@ __device__ __forceinline__ void mma_stage_Ap(const Ctx& c) {
   for (uint32_t s = 0; s < 8; ++s) {
     const uint64_t ad =
         tc::smem_desc(c.smb + c.sop + (s >> 2) * 16384 + (s & 3) * 32, 1024, tc::kSw128);
-    const uint64_t bd = tc::smem_desc(c.smb + SMAT + MAT_FA + s * 2048, 1024, tc::kSw128, 1024);
+    const uint64_t bd = tc::smem_desc(c.smb + c.smat + MAT_FA + s * 2048, 1024, tc::kSw128, 1024);
     tc::mma_bf16(c.tmem + c.tw, ad, bd, id, s);
   }
 }
@@ -349,7 +388,7 @@ __device__ unsigned long long g_last[148 * 2];
 #define TT_END(k)
 #endif
 
-template <typename T>
+template <typename T, bool W3 = false>
 __device__ __forceinline__ void issue(Ctx& c, int stage) {
 #ifdef FB_TC_TIMING
   const bool tl = slot_leader() && blockIdx.x < 148;
@@ -371,8 +410,8 @@ __device__ __forceinline__ void issue(Ctx& c, int stage) {
     }
     switch (stage) {
       case 0: mma_stage_A<T>(c); break;
-      case 1: mma_stage_B<T, false>(c); break;
-      case 2: mma_stage_B<T, true>(c); break;
+      case 1: mma_stage_B<T, false, W3>(c); break;
+      case 2: mma_stage_B<T, true, W3>(c); break;
       default: mma_stage_Ap<T>(c); break;
     }
     tc::commit(c.mma_bar);
@@ -410,7 +449,7 @@ __device__ __forceinline__ void twiddle_row(float* re, float* im, const float2* 
 }
 
 // A exit: X[t2][f1] w^(f1 t2) -> stage-B operand (MN-major, k = t2, n = f1)
-template <typename T>
+template <typename T, bool W3 = false>
 __device__ __forceinline__ void epi_A_exit(const Ctx& c) {
   uint32_t t2, g;
   coords(t2, g);
@@ -423,10 +462,19 @@ __device__ __forceinline__ void epi_A_exit(const Ctx& c) {
     tld<16>(taddr(c, c.tw + 64 + cb), im);
     tc::ld_wait();
     twiddle_row<-1>(re, im, c.tab, t2, cb);
-    st8<T>(op + off_bmn(cb, t2), re);
-    st8<T>(op + off_bmn(cb + 8, t2), re + 8);
-    st8<T>(op + 16384 + off_bmn(cb, t2), im);
-    st8<T>(op + 16384 + off_bmn(cb + 8, t2), im + 8);
+    if constexpr (W3) {  // planes [-Xi | Xr | Xi]
+      st8n<T>(op + off_bmn(cb, t2), im);
+      st8n<T>(op + off_bmn(cb + 8, t2), im + 8);
+      st8<T>(op + 16384 + off_bmn(cb, t2), re);
+      st8<T>(op + 16384 + off_bmn(cb + 8, t2), re + 8);
+      st8<T>(op + 32768 + off_bmn(cb, t2), im);
+      st8<T>(op + 32768 + off_bmn(cb + 8, t2), im + 8);
+    } else {
+      st8<T>(op + off_bmn(cb, t2), re);
+      st8<T>(op + off_bmn(cb + 8, t2), re + 8);
+      st8<T>(op + 16384 + off_bmn(cb, t2), im);
+      st8<T>(op + 16384 + off_bmn(cb + 8, t2), im + 8);
+    }
   }
 }
 
@@ -474,15 +522,16 @@ __device__ __forceinline__ void store_rows(const Ctx& c, T* __restrict__ out, in
 
 __device__ __forceinline__ void setup(unsigned char* sm, uint32_t* tmem_slot, uint64_t* bars,
                                       int nbars, int nbars_slot, const uint4* __restrict__ mats,
-                                      const float2* __restrict__ tab_g) {
+                                      const float2* __restrict__ tab_g, uint32_t smat = SMAT,
+                                      uint32_t stab = STAB) {
   if (threadIdx.x < 32) tc::alloc<512>(tmem_slot);
   if (threadIdx.x == 0) {
     for (int i = 0; i < nbars; ++i) ptx::mbar_init(&bars[i], i < nbars - nbars_slot ? 1 : kSlotThreads);
     ptx::fence_barrier_init();
   }
-  uint4* dm = reinterpret_cast<uint4*>(sm + SMAT);
+  uint4* dm = reinterpret_cast<uint4*>(sm + smat);
   for (uint32_t i = threadIdx.x; i < MAT_BYTES / 16; i += kThreads) dm[i] = __ldg(mats + i);
-  float2* tab = reinterpret_cast<float2*>(sm + STAB);
+  float2* tab = reinterpret_cast<float2*>(sm + stab);
   for (uint32_t i = threadIdx.x; i < 192; i += kThreads) tab[i] = __ldg(tab_g + i);
   ptx::fence_proxy_async_smem();
   cta_sync_tc();
@@ -537,9 +586,9 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int npairs = (B + 1) / 2;
   int i0, i1;
   cta_range(total, i0, i1);
-  setup(sm, &tmem_slot, bars, 4, 0, mats, tab_g);
+  setup(sm, &tmem_slot, bars, 4, 0, mats, tab_g, SMAT3, STAB3);
   const uint32_t slot = threadIdx.x / kSlotThreads;
-  Ctx c = make_ctx(sm, tmem_slot, slot, &bars[slot]);
+  Ctx c = make_ctx(sm, tmem_slot, slot, &bars[slot], true);
   c.aux = TKF + 128 * slot;
   c.on = 4u * (uint32_t)((i1 - i0 + (int)slot) / 2);  // the other slot's pairs x 4 stages
   uint64_t* in_bar = &bars[2 + slot];
@@ -554,11 +603,11 @@ __global__ void __launch_bounds__(kThreads, 1)
       cur_h = h;
     }
     { TT_BEGIN ptx::mbar_wait(in_bar, it & 1); TT_END(16) }
-    issue<T>(c, 0);
+    issue<T, true>(c, 0);
     if (lead && item + 2 < i1)
       load_pair(sm + c.in_off, &umap, (item + 2) / npairs, 2 * ((item + 2) % npairs), in_bar);
-    { TT_BEGIN epi_A_exit<T>(c); TT_END(18) }
-    issue<T>(c, 1);
+    { TT_BEGIN epi_A_exit<T, true>(c); TT_END(18) }
+    issue<T, true>(c, 1);
     // ---- B exit: Z = X * k_f' -> Zr/Zi[k = f2][n = f1]
     {
       uint32_t f2, g;
@@ -579,13 +628,14 @@ __global__ void __launch_bounds__(kThreads, 1)
           re[j] = fmaf(a, kr[j], -b * ki[j]);
           im[j] = fmaf(a, ki[j], b * kr[j]);
         }
-        st8<T>(op + off_bmn(cb, f2), re);
+        st8<T>(op + off_bmn(cb, f2), re);  // planes [Zr | Zi | -Zr]
         st8<T>(op + 16384 + off_bmn(cb, f2), im);
+        st8n<T>(op + 32768 + off_bmn(cb, f2), re);
       }
     }
-    issue<T>(c, 2);
+    issue<T, true>(c, 2);
     { TT_BEGIN epi_Bp_exit<T>(c); TT_END(20) }
-    issue<T>(c, 3);
+    issue<T, true>(c, 3);
     { TT_BEGIN store_rows<T>(c, y, 2 * pr, B, H, h); TT_END(21) }
   }
   teardown(tmem_slot);
