@@ -76,6 +76,13 @@ constexpr uint32_t SOP3 = SIN + 2 * 16384;
 constexpr uint32_t SMAT3 = SOP3 + 2 * 49152;
 constexpr uint32_t STAB3 = SMAT3 + MAT_BYTES;
 constexpr uint32_t SMEM_FWD = STAB3 + 1536;
+// Backward: same planes, plus half of k_f' — K-bar and D are real, so
+// k_f'[n - f] = conj(k_f'[f]) and rows f2 <= 64 ([f1 64][65] fp16 pairs)
+// cover the spectrum.  231168 B of the 231424 B left next to the 1 KB of
+// static smem.
+constexpr uint32_t KFH_ROW = 65;
+constexpr uint32_t SKF3 = STAB3 + 1536;
+constexpr uint32_t SMEM_BWD3 = SKF3 + 64 * KFH_ROW * 4;
 
 __device__ __forceinline__ unsigned char* smem_base(unsigned char* raw) {
   if (reinterpret_cast<uintptr_t>(raw) & 1023) __trap();  // swizzle atoms need 1 KB alignment
@@ -675,15 +682,15 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int npairs = (B + 1) / 2;
   int i0, i1;
   cta_range(total, i0, i1);
-  setup(sm, &tmem_slot, bars, 6, 2, mats, tab_g);
+  setup(sm, &tmem_slot, bars, 6, 2, mats, tab_g, SMAT3, STAB3);
   const uint32_t slot = threadIdx.x / kSlotThreads;
-  Ctx c = make_ctx(sm, tmem_slot, slot, &bars[slot]);
+  Ctx c = make_ctx(sm, tmem_slot, slot, &bars[slot], true);
   c.aux = TPK + 64 * slot;
   uint64_t* in_bar = &bars[2 + slot];
   uint64_t* chain_mine = &bars[4 + slot];
   uint64_t* chain_other = &bars[5 - slot];
   const bool lead = slot_leader();
-  const uint32_t* kfs = reinterpret_cast<const uint32_t*>(sm + SKF);
+  const uint32_t* kfs = reinterpret_cast<const uint32_t*>(sm + SKF3);
   uint32_t in_cnt = 0, base0 = 0, base1 = 0;
   int seg = 0;
   for (int a = i0; a < i1; ++seg) {
@@ -691,9 +698,10 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int L = min(i1, (h + 1) * npairs) - a;
     // ---- segment start (whole CTA): k_f' of head h to smem, S = 0
     {
-      const uint4* src = reinterpret_cast<const uint4*>(kf16 + (size_t)h * kN);
-      uint4* dst = reinterpret_cast<uint4*>(sm + SKF);
-      for (uint32_t i = threadIdx.x; i < kN * 4 / 16; i += kThreads) dst[i] = __ldg(src + i);
+      const uint32_t* src = reinterpret_cast<const uint32_t*>(kf16 + (size_t)h * kN);
+      uint32_t* dst = reinterpret_cast<uint32_t*>(sm + SKF3);
+      for (uint32_t i = threadIdx.x; i < 64 * KFH_ROW; i += kThreads)
+        dst[i] = __ldg(src + (i / KFH_ROW) * 128 + i % KFH_ROW);
       const uint32_t t = threadIdx.x;
       constexpr uint32_t W = 64 / (kThreads / 128);  // columns per thread
       const uint32_t lane_off = (32u * ((t >> 5) & 3)) << 16, g8 = t >> 7;
@@ -719,10 +727,10 @@ __global__ void __launch_bounds__(kThreads, 1)
       // ---- U = F(u), parked as bf16 pairs
       { TT_BEGIN ptx::mbar_wait(in_bar, in_cnt & 1); TT_END(22) }
       ++in_cnt;
-      issue<T>(c, 0);
+      issue<T, true>(c, 0);
       if (lead) load_pair(sm + c.in_off, &dymap, h, b0, in_bar);
-      { TT_BEGIN epi_A_exit<T>(c); TT_END(25) }
-      issue<T>(c, 1);
+      { TT_BEGIN epi_A_exit<T, true>(c); TT_END(25) }
+      issue<T, true>(c, 1);
       {
         uint32_t f2, g;
         coords(f2, g);
@@ -742,10 +750,10 @@ __global__ void __launch_bounds__(kThreads, 1)
       // ---- DY = F(dy)
       { TT_BEGIN ptx::mbar_wait(in_bar, in_cnt & 1); TT_END(23) }
       ++in_cnt;
-      issue<T>(c, 0);
+      issue<T, true>(c, 0);
       if (lead && j + 2 < L) load_pair(sm + c.in_off, &umap, h, b0 + 4, in_bar);
-      { TT_BEGIN epi_A_exit<T>(c); TT_END(25) }
-      issue<T>(c, 1);
+      { TT_BEGIN epi_A_exit<T, true>(c); TT_END(25) }
+      issue<T, true>(c, 1);
       // ---- S += conj(U) DY (in pair order), Z = DY conj(k_f') -> B' operand
       if (j > 0) {
         const uint32_t idx = slot ? base0 + (uint32_t)k : base1 + (uint32_t)k - 1;
@@ -771,26 +779,31 @@ __global__ void __launch_bounds__(kThreads, 1)
             const float2 u = unpack_bf2(__float_as_uint(pk[jj]));
             sr[jj] = fmaf(u.x, dr[jj], fmaf(u.y, di[jj], sr[jj]));
             si[jj] = fmaf(u.x, di[jj], fmaf(-u.y, dr[jj], si[jj]));
-            float2 kv = __half22float2(
-                *reinterpret_cast<const __half2*>(&kfs[(col + jj) * 128 + f2]));
+            // k_f'[f1 + 64 f2]; upper half (f2 >= 64) by conjugate symmetry
+            const uint32_t f1 = col + jj;
+            const bool up = f2 >= 64;
+            const uint32_t idx = !up ? f1 * KFH_ROW + f2
+                                     : (f1 ? (64 - f1) * KFH_ROW + (127 - f2) : 128 - f2);
+            float2 kv = __half22float2(*reinterpret_cast<const __half2*>(&kfs[idx]));
             kv.x *= osc;
-            kv.y *= osc;
+            kv.y *= up ? -osc : osc;
             const float a0 = dr[jj], b = di[jj];
             dr[jj] = fmaf(a0, kv.x, b * kv.y);
             di[jj] = fmaf(b, kv.x, -a0 * kv.y);
           }
           tst8(taddr(c, TS + col), sr);
           tst8(taddr(c, TS + 64 + col), si);
-          st8<T>(op + off_bmn(col, f2), dr);
+          st8<T>(op + off_bmn(col, f2), dr);  // planes [Zr | Zi | -Zr]
           st8<T>(op + 16384 + off_bmn(col, f2), di);
+          st8n<T>(op + 32768 + off_bmn(col, f2), dr);
         }
         tst_wait();
         tc::fence_before();
         mbar_arrive(chain_mine);
       }
-      issue<T>(c, 2);
+      issue<T, true>(c, 2);
       { TT_BEGIN epi_Bp_exit<T>(c); TT_END(28) }
-      issue<T>(c, 3);
+      issue<T, true>(c, 3);
       { TT_BEGIN store_rows<T>(c, du, b0, B, H, h); TT_END(29) }
     }
     base0 += (uint32_t)(L + 1) / 2;
@@ -986,8 +999,8 @@ int tc_bwd(fb_plan* p, const void* dy, const void* u, void* du, float* dK, float
     if (!rc) rc = make_map<T>(&umap, u, B, p->H);
     if (rc) return rc;
     auto k = tc_bwd_kernel<T>;
-    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM_BWD);
-    k<<<(unsigned)gr.ctas, kThreads, SMEM_BWD, s>>>(
+    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM_BWD3);
+    k<<<(unsigned)gr.ctas, kThreads, SMEM_BWD3, s>>>(
         dmap, umap, (T*)du, (const __half2*)p->kf_tc, p->kf_scale, (const uint4*)p->tc_mats,
         p->tw2, spart, (int)B, (int)p->H, gr.total, gr.maxseg);
     return cuda_status(cudaGetLastError(), "tc_bwd");
