@@ -19,6 +19,7 @@
 // passes 1/3 give one column tau per thread (consecutive threads =
 // consecutive tau), pass 2 moves whole rows by TMA bulk copies.
 #include <algorithm>
+#include <cstdlib>
 #include <type_traits>
 
 #include "fb_common.cuh"
@@ -132,7 +133,7 @@ __device__ __forceinline__ float2 cx_load(const CxT<__half>* p) {
 template <typename ST, int MODE>
 __global__ void __launch_bounds__(kL / 16, 1)
     tp_pass2_kernel(CxT<ST>* __restrict__ x1, const float2* __restrict__ kf2,
-                    float2* __restrict__ kf2_out, const float2* __restrict__ tab_g, int npairs,
+                    float2* kf2_out, const float2* __restrict__ tab_g, int npairs,
                     int H, int m, int ppc, float inv_n) {
   using S = FftShape<kL2>;
   extern __shared__ __align__(128) unsigned char smem_raw[];
@@ -640,6 +641,212 @@ __global__ void __launch_bounds__(kBigThreads, 1)
   }
 }
 
+// ---------------------------------------------------------------- streaming big column passes
+// Passes 1/3 for m > 16 as persistent kernels: a CTA walks tiles of
+// TAU = 8192 / m columns x all m rows of one (pair, head); the next tile's
+// input boxes stream in by TMA (2-stage ring, <= 256 rows per box) while the
+// current tile runs its batched m-point column FFT in smem.
+constexpr int kBigStages = 2;
+
+// column twiddle w^(a (tau0 + c)) for the rows a = a0 + 16 k a thread visits
+// (kBigThreads is a multiple of TAU, so c is fixed per thread): two table
+// lookups per tile, then a 16-step rotation recurrence (fp32, a few ulp)
+template <int SIGN>
+struct ColTw {
+  float2 w, step;
+  __device__ __forceinline__ ColTw(const float2* __restrict__ tb, uint32_t a0, uint32_t tcol,
+                                   uint32_t astep) {
+    w = tw_big<SIGN>(tb, a0 * tcol);
+    step = tw_big<SIGN>(tb, astep * tcol);
+  }
+  __device__ __forceinline__ float2 next() {
+    const float2 r = w;
+    w = cmul(w, step);
+    return r;
+  }
+};
+
+// two CTAs per SM where the smem allows it (single-signal pass 1)
+template <typename IO, typename ST, int SMALL, int SRC>
+__global__ void __launch_bounds__(kBigThreads, SRC == 1 ? 1 : 2)
+    tp_bigs1_kernel(const __grid_constant__ CUtensorMap amap, const __grid_constant__ CUtensorMap bmap,
+                    CxT<ST>* __restrict__ out_a, CxT<ST>* __restrict__ out_b,
+                    float* __restrict__ ddpart, const float2* __restrict__ tw_m,
+                    const float2* __restrict__ tb, int H, int npairs, int rows, uint32_t m,
+                    int ntiles) {
+  extern __shared__ __align__(128) float2 tsm[];
+  __shared__ __align__(8) uint64_t full[kBigStages];
+  __shared__ float red[kBigThreads / 32];
+  constexpr int NCH = SRC == 1 ? 4 : (SRC == 2 ? 1 : 2);
+  const uint32_t TAU = kBigTile / m, NBk = kL / TAU;
+  const uint32_t plen = padded_len(m) * TAU;
+  float2* sa = tsm;
+  float2* sb = tsm + plen;
+  unsigned char* ring = reinterpret_cast<unsigned char*>(tsm + (SRC == 1 ? 2 : 1) * plen);
+  const uint32_t chb = (uint32_t)rows * TAU * sizeof(IO);
+  const uint32_t stage_bytes = NCH * chb;
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < kBigStages; ++i) ptx::mbar_init(&full[i], 1);
+    ptx::fence_barrier_init();
+  }
+  __syncthreads();
+  auto tile_of = [&](int t, int& pr, int& h, int& tbk) {
+    tbk = t % NBk;
+    h = (t / NBk) % H;
+    pr = t / (NBk * H);
+  };
+  auto issue = [&](int t, int sg) {
+    int pr, h, tbk;
+    tile_of(t, pr, h, tbk);
+    unsigned char* dst = ring + (size_t)sg * stage_bytes;
+    ptx::mbar_arrive_expect_tx(&full[sg], stage_bytes);
+    for (int ch = 0; ch < NCH; ++ch) {
+      const CUtensorMap* mp = (SRC == 1 && ch >= 2) ? &bmap : &amap;
+      const int row = SRC == 2 ? h : (2 * pr + (ch & 1)) * H + h;
+      for (int r0 = 0; r0 < rows; r0 += 256)
+        tma_load_3d(dst + ch * chb + (size_t)r0 * TAU * sizeof(IO), mp, tbk * (int)TAU, r0, row,
+                    &full[sg]);
+    }
+  };
+  const int first = blockIdx.x, step = gridDim.x;
+  if (threadIdx.x == 0 && first < ntiles) issue(first, 0);
+  int it = 0;
+  for (int t = first; t < ntiles; t += step, ++it) {
+    const int sg = it % kBigStages;
+    int pr, h, tbk;
+    tile_of(t, pr, h, tbk);
+    const uint32_t tau0 = tbk * TAU;
+    if (threadIdx.x == 0 && t + step < ntiles) issue(t + step, (it + 1) % kBigStages);
+    ptx::mbar_wait(&full[sg], (uint32_t)(it / kBigStages) & 1);
+    const IO* sv = reinterpret_cast<const IO*>(ring + (size_t)sg * stage_bytes);
+    float dd = 0.f;
+    for (uint32_t i = threadIdx.x; i < kBigTile; i += kBigThreads) {
+      const uint32_t e = i / TAU, c = i % TAU;
+      const bool ok = e < (uint32_t)rows;
+      float2 v = make_float2(0.f, 0.f);
+      if (ok) {
+        v.x = tof(sv[e * TAU + c]);
+        if constexpr (SRC != 2) v.y = tof(sv[(rows + e) * TAU + c]);
+      }
+      if constexpr (SRC == 1) {
+        float2 w = make_float2(0.f, 0.f);
+        if (ok) {
+          w.x = tof(sv[(2 * rows + e) * TAU + c]);
+          w.y = tof(sv[(3 * rows + e) * TAU + c]);
+        }
+        dd = fmaf(v.x, w.x, fmaf(v.y, w.y, dd));
+        sb[pad16(e) * TAU + c] = w;
+      }
+      sa[pad16(e) * TAU + c] = v;
+    }
+    __syncthreads();  // stage sg consumed (refilled two tiles from now)
+    smem_passes<-1, SMALL>(sa, m, TAU, 1, m, tw_m);
+    if constexpr (SRC == 1) smem_passes<-1, SMALL>(sb, m, TAU, 1, m, tw_m);
+    CxT<ST>* oa = out_a + ((size_t)pr * H + h) * (size_t)m * kL;
+    CxT<ST>* ob = SRC == 1 ? out_b + ((size_t)pr * H + h) * (size_t)m * kL : nullptr;
+    ColTw<-1> ctw(tb, threadIdx.x / TAU, tau0 + threadIdx.x % TAU, kBigThreads / TAU);
+    for (uint32_t i = threadIdx.x; i < kBigTile; i += kBigThreads) {
+      const uint32_t a = i / TAU, c = i % TAU;
+      const float2 w = ctw.next();
+      stc<ST>(&oa[(size_t)a * kL + tau0 + c].x, cmul(sa[pad16(a) * TAU + c], w));
+      if constexpr (SRC == 1) stc<ST>(&ob[(size_t)a * kL + tau0 + c].x, cmul(sb[pad16(a) * TAU + c], w));
+    }
+    if constexpr (SRC == 1) {
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) dd += __shfl_xor_sync(0xffffffffu, dd, o);
+      if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = dd;
+    }
+    __syncthreads();  // tile buffers free for the next tile
+    if constexpr (SRC == 1) {
+      if (threadIdx.x == 0) {
+        float s = 0.f;
+        for (uint32_t w2 = 0; w2 < kBigThreads / 32; ++w2) s += red[w2];
+        ddpart[((size_t)h * npairs + pr) * NBk + tbk] = s;
+      }
+    }
+  }
+}
+
+template <typename ST, typename IO, int SMALL, int MODE>
+__global__ void __launch_bounds__(kBigThreads, 1)
+    tp_bigs3_kernel(const __grid_constant__ CUtensorMap wmap, const __grid_constant__ CUtensorMap smap,
+                    IO* __restrict__ out, const float* __restrict__ D, float* __restrict__ dkbar,
+                    const float2* __restrict__ tw_m, const float2* __restrict__ tb, int B, int H,
+                    uint32_t N, int rows, uint32_t m, float scale, int ntiles) {
+  extern __shared__ __align__(128) float2 tsm[];
+  __shared__ __align__(8) uint64_t full[kBigStages];
+  const uint32_t TAU = kBigTile / m, NBk = kL / TAU;
+  const uint32_t plen = padded_len(m) * TAU;
+  unsigned char* ring = reinterpret_cast<unsigned char*>(tsm + plen);
+  const uint32_t wb = m * TAU * sizeof(CxT<ST>);
+  const uint32_t chb = MODE == 0 ? (uint32_t)rows * TAU * sizeof(IO) : 0;
+  const uint32_t stage_bytes = wb + 2 * chb;
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < kBigStages; ++i) ptx::mbar_init(&full[i], 1);
+    ptx::fence_barrier_init();
+  }
+  __syncthreads();
+  auto tile_of = [&](int t, int& pr, int& h, int& tbk) {
+    tbk = t % NBk;
+    h = (t / NBk) % H;
+    pr = t / (NBk * H);
+  };
+  auto issue = [&](int t, int sg) {
+    int pr, h, tbk;
+    tile_of(t, pr, h, tbk);
+    unsigned char* dst = ring + (size_t)sg * stage_bytes;
+    ptx::mbar_arrive_expect_tx(&full[sg], stage_bytes);
+    for (uint32_t r0 = 0; r0 < m; r0 += 256)
+      tma_load_3d(dst + (size_t)r0 * TAU * sizeof(CxT<ST>), &wmap, tbk * (int)TAU, (int)r0,
+                  pr * H + h, &full[sg]);
+    if constexpr (MODE == 0)
+      for (int ch = 0; ch < 2; ++ch)
+        for (int r0 = 0; r0 < rows; r0 += 256)
+          tma_load_3d(dst + wb + ch * chb + (size_t)r0 * TAU * sizeof(IO), &smap, tbk * (int)TAU,
+                      r0, (2 * pr + ch) * H + h, &full[sg]);
+  };
+  const int first = blockIdx.x, step = gridDim.x;
+  if (threadIdx.x == 0 && first < ntiles) issue(first, 0);
+  int it = 0;
+  for (int t = first; t < ntiles; t += step, ++it) {
+    const int sg = it % kBigStages;
+    int pr, h, tbk;
+    tile_of(t, pr, h, tbk);
+    const uint32_t tau0 = tbk * TAU;
+    if (threadIdx.x == 0 && t + step < ntiles) issue(t + step, (it + 1) % kBigStages);
+    ptx::mbar_wait(&full[sg], (uint32_t)(it / kBigStages) & 1);
+    const unsigned char* base = ring + (size_t)sg * stage_bytes;
+    const CxT<ST>* sw = reinterpret_cast<const CxT<ST>*>(base);
+    ColTw<+1> ctw(tb, threadIdx.x / TAU, tau0 + threadIdx.x % TAU, kBigThreads / TAU);
+    for (uint32_t i = threadIdx.x; i < kBigTile; i += kBigThreads) {
+      const uint32_t a = i / TAU, c = i % TAU;
+      tsm[pad16(a) * TAU + c] = cmul(cx_load(sw + a * TAU + c), ctw.next());
+    }
+    __syncthreads();
+    smem_passes<+1, SMALL>(tsm, m, TAU, 1, m, tw_m);
+    if constexpr (MODE == 0) {
+      const IO* sk = reinterpret_cast<const IO*>(base + wb);
+      const int b0 = 2 * pr, b1 = b0 + 1;
+      const bool has1 = b1 < B;
+      const float d = __ldg(D + h);
+      const size_t o0 = ((size_t)b0 * H + h) * N, o1 = ((size_t)b1 * H + h) * N;
+      for (uint32_t i = threadIdx.x; i < (uint32_t)rows * TAU; i += kBigThreads) {
+        const uint32_t cc = i / TAU, c = i % TAU;
+        const uint32_t tt = cc * kL + tau0 + c;
+        const float2 v = tsm[pad16(cc) * TAU + c];
+        st(out + o0 + tt, fmaf(d, tof(sk[cc * TAU + c]), v.x));
+        if (has1) st(out + o1 + tt, fmaf(d, tof(sk[(rows + cc) * TAU + c]), v.y));
+      }
+    } else {
+      for (uint32_t i = threadIdx.x; i < (uint32_t)rows * TAU; i += kBigThreads) {
+        const uint32_t cc = i / TAU, c = i % TAU;
+        dkbar[(size_t)h * N + cc * kL + tau0 + c] = tsm[pad16(cc) * TAU + c].x * scale;
+      }
+    }
+    __syncthreads();  // tile and stage sg free
+  }
+}
+
 // ---------------------------------------------------------------- host side
 namespace {
 
@@ -719,6 +926,32 @@ int inter_map(CUtensorMap* mp, const fb_plan* p, const CxT<ST>* ptr, int npairs)
   return encode_map_3d(mp, es == 4 ? CU_TENSOR_MAP_DATA_TYPE_UINT32 : CU_TENSOR_MAP_DATA_TYPE_UINT64,
                        ptr, dims, strides, box);
 }
+// [outer][rows][l] view (rows l apart, outer blocks outer_stride elements
+// apart) with a {tau, min(rows, 256), 1} box
+template <typename T>
+int rows_map(CUtensorMap* mp, CUtensorMapDataType type, const T* ptr, uint64_t outer, uint64_t rows,
+             uint64_t outer_stride, uint32_t tau) {
+  const uint64_t dims[3] = {kL, rows, outer};
+  const uint64_t strides[2] = {kL * sizeof(T), outer_stride * sizeof(T)};
+  const uint32_t box[3] = {tau, (uint32_t)std::min<uint64_t>(rows, 256), 1};
+  return encode_map_3d(mp, type, ptr, dims, strides, box);
+}
+template <typename ST>
+constexpr CUtensorMapDataType cx_type() {
+  return sizeof(CxT<ST>) == 4 ? CU_TENSOR_MAP_DATA_TYPE_UINT32 : CU_TENSOR_MAP_DATA_TYPE_UINT64;
+}
+// FB_BIGS=0 / 1 / 3 (debug): streaming big-column kernels off / pass 1 only / pass 3 only
+int bigs_mask() {
+  static int v = [] {
+    const char* e = getenv("FB_BIGS");
+    return e ? atoi(e) : 3 | 1;
+  }();
+  return v;
+}
+size_t bigs_smem(uint32_t m, int tiles, size_t stage) {
+  return (size_t)tiles * padded_len(kBigTile) * sizeof(float2) + kBigStages * stage;
+}
+
 int col_stages(size_t stage_bytes) {
   return (int)std::max<size_t>(2, std::min<size_t>(kColMaxStages, (96 * 1024) / stage_bytes));
 }
@@ -758,6 +991,38 @@ uint32_t launch_pass1(const fb_plan* p, const IO* a, const IO* b, CxT<ST>* oa, C
     return kL / kColThreads;
   }
   const uint32_t gx = (uint32_t)(kL / (kBigTile / p->m));
+  {
+    // streaming big-column kernel (TMA ring)
+    const uint32_t TAU = (uint32_t)(kBigTile / p->m);
+    const int rows = (int)(p->N / kL);
+    CUtensorMap am, bm;
+    bool maps;
+    if constexpr (SRC == 2) {
+      maps = !rows_map<float>(&am, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, p->kbar, (uint64_t)p->H, rows,
+                              (uint64_t)p->N, TAU);
+      bm = am;
+    } else {
+      maps = !rows_map<IO>(&am, tma_type<IO>(), a, (uint64_t)B * p->H, rows, (uint64_t)p->N, TAU) &&
+             !rows_map<IO>(&bm, tma_type<IO>(), SRC == 1 ? b : a, (uint64_t)B * p->H, rows,
+                           (uint64_t)p->N, TAU);
+    }
+    const int nch = SRC == 1 ? 4 : (SRC == 2 ? 1 : 2);
+    const size_t stage = (size_t)nch * rows * TAU * sizeof(IO);
+    const size_t sm = bigs_smem((uint32_t)p->m, SRC == 1 ? 2 : 1, stage);
+    const int ntiles = (int)((SRC == 2 ? 1 : npairs) * p->H * gx);
+    if (maps && sm <= 227 * 1024 && (bigs_mask() & 1)) {
+      with_small(p->m, [&](auto sc) {
+        constexpr int SM = decltype(sc)::value;
+        auto k = tp_bigs1_kernel<IO, ST, SM, SRC>;
+        cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+        const int per_sm = (SRC != 1 && sm <= 113 * 1024) ? 2 : 1;
+        k<<<std::min(ntiles, per_sm * p->num_sms), kBigThreads, sm, s>>>(am, bm, oa, ob, ddpart, p->tw_m,
+                                                                p->tw_big, (int)p->H, npairs, rows,
+                                                                (uint32_t)p->m, ntiles);
+      });
+      return gx;
+    }
+  }
   with_small(p->m, [&](auto sc) {
     constexpr int SM = decltype(sc)::value;
     auto k = tp_pass1_big_kernel<IO, ST, SM, SRC>;
@@ -804,6 +1069,34 @@ void launch_pass3(const fb_plan* p, const CxT<ST>* w, const IO* skip, IO* out, f
     return;
   }
   const uint32_t gx = (uint32_t)(kL / (kBigTile / p->m));
+  {
+    const uint32_t TAU = (uint32_t)(kBigTile / p->m);
+    const int rows = (int)(p->N / kL);
+    const int np = MODE == 0 ? npairs : 1;
+    CUtensorMap wm, sm_map;
+    bool maps = !rows_map<CxT<ST>>(&wm, cx_type<ST>(), w, (uint64_t)np * p->H, (uint64_t)p->m,
+                                   (uint64_t)p->m * kL, TAU);
+    if constexpr (MODE == 0)
+      maps = maps && !rows_map<IO>(&sm_map, tma_type<IO>(), skip, (uint64_t)B * p->H, rows,
+                                   (uint64_t)p->N, TAU);
+    else
+      sm_map = wm;
+    const size_t stage = (size_t)p->m * TAU * sizeof(CxT<ST>) +
+                         (MODE == 0 ? 2 * (size_t)rows * TAU * sizeof(IO) : 0);
+    const size_t smb = bigs_smem((uint32_t)p->m, 1, stage);
+    const int ntiles = (int)(np * p->H * gx);
+    if (maps && smb <= 227 * 1024 && (bigs_mask() & 2)) {
+      with_small(p->m, [&](auto sc) {
+        constexpr int SM = decltype(sc)::value;
+        auto k = tp_bigs3_kernel<ST, IO, SM, MODE>;
+        cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smb);
+        k<<<std::min(ntiles, p->num_sms), kBigThreads, smb, s>>>(
+            wm, sm_map, out, p->d, dkbar, p->tw_m, p->tw_big, B, (int)p->H, (uint32_t)p->N, rows,
+            (uint32_t)p->m, scale, ntiles);
+      });
+      return;
+    }
+  }
   with_small(p->m, [&](auto sc) {
     constexpr int SM = decltype(sc)::value;
     auto k = tp_pass3_big_kernel<ST, IO, SM, MODE>;
@@ -831,11 +1124,9 @@ int pass2_chunks(const fb_plan* p, int64_t npairs) {
 int tp_prep(fb_plan* p, const float* K, cudaStream_t s) {
   int rc = regularize_bank_dev(p, K, s);
   if (rc) return rc;
-  // kernel rows through pass 1 (fp32 storage) into a scratch, then spectrum
-  CxT<float>* x1k = nullptr;
-  rc = cuda_status(cudaMallocAsync(&x1k, (size_t)p->H * p->n * sizeof(CxT<float>), s),
-                   "cudaMallocAsync(tp_prep)");
-  if (rc) return rc;
+  // kernel rows through pass 1 (fp32) straight into the spectrum buffer, then
+  // each row's FFT in place (a CTA stages its whole row before writing it)
+  auto* x1k = reinterpret_cast<CxT<float>*>(p->kf);
   launch_pass1<float, float, 2>(p, nullptr, nullptr, x1k, nullptr, nullptr, 2, 1, s);
   const size_t sm = pass2_smem<float>();
   auto k = tp_pass2_kernel<float, 1>;
@@ -843,9 +1134,7 @@ int tp_prep(fb_plan* p, const float* K, cudaStream_t s) {
   k<<<dim3((unsigned)(p->H * p->m), 1), kL / 16, sm, s>>>(x1k, nullptr, p->kf, p->tw_l, 1,
                                                           (int)p->H, (int)p->m, 1,
                                                           1.0f / (float)p->n);
-  rc = cuda_status(cudaGetLastError(), "tp_prep");
-  cudaFreeAsync(x1k, s);
-  return rc;
+  return cuda_status(cudaGetLastError(), "tp_prep");
 }
 
 size_t tp_workspace(const fb_plan* p, int64_t B) {

@@ -248,7 +248,7 @@ def test_three_pass_fp32(lc, B, H, N, mode):
     assert_parity(got, oracle_layer(lc, inp, cfg, causal=bool(mode)), 1e-5)
 
 
-@pytest.mark.parametrize("B,H,N", [(2, 1, 131072), (3, 1, 262144)])
+@pytest.mark.parametrize("B,H,N", [(2, 1, 131072), (3, 1, 262144), (3, 2, 131072)])
 def test_three_pass_tiled_columns_fp32(lc, B, H, N):
     """m = 2N / 8192 > 16: passes 1/3 run as smem-tiled batched column FFTs."""
     inp = layer_inputs(lc, B, H, N, torch.float32)
