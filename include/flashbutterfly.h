@@ -123,6 +123,29 @@ int fb_fwd(fb_plan* plan, const void* u, void* y, int64_t B, void* workspace, vo
 int fb_bwd(fb_plan* plan, const void* dy, const void* u, void* du, float* dK, float* dKbar,
            float* dD, int64_t B, void* workspace, void* stream);
 
+/* Host-buffer layer runner: the whole regularized_long_conv forward +
+ * backward (regularize.hpp:67-70 with the SURVEY.md §8c backward) on HOST
+ * arrays, pipelined.  The H heads are independent, so the runner walks them
+ * in chunks of Hc (a divisor of H): while chunk c computes, chunk c+1's
+ * inputs copy in and chunk c-1's results copy out (three CUDA streams,
+ * double-buffered device staging), which overlaps both PCIe directions with
+ * the kernels.  Host pointers should be pinned (cudaHostAlloc /
+ * torch.pin_memory) for the copies to be asynchronous.
+ *   u, dy, y, du: [B][H][N] in the plan dtype;  K, dK: [H][N] f32;
+ *   D, dD: [H] f32.
+ * fb_host_runner_run is stream-ordered: it starts after the work already on
+ * `stream` and `stream` waits for all of it (so CUDA events recorded on
+ * `stream` around the call time the whole step, copies included). */
+typedef struct fb_host_runner fb_host_runner;
+int fb_host_runner_create(fb_host_runner** runner, int64_t N, int64_t H, int mode, int dtype,
+                          int engine, int device, int64_t B, int64_t heads_per_chunk);
+int fb_host_runner_destroy(fb_host_runner* runner);
+/* heads actually used per chunk (the largest divisor of H <= the request) */
+int64_t fb_host_runner_chunk_heads(const fb_host_runner* runner);
+int fb_host_runner_run(fb_host_runner* runner, const fb_reg_config* cfg, int training,
+                       const void* u, const void* dy, const float* K, const float* D, void* y,
+                       void* du, float* dK, float* dD, void* stream);
+
 /* Learned butterfly (K5).  Replaces learned_forward / learned_gradients
  * (butterfly.hpp:88-108, butterfly.cpp:221-307) batched over rows: rows
  * [B][H] of complex length n, with per-head block parameters (one factor x

@@ -9,6 +9,7 @@ reference interface.
 from .longconv import (  # noqa: F401
     ConvMode,
     Engine,
+    HostRunner,
     LongConvPlan,
     RegularizationConfig,
     SmoothDomain,
@@ -20,7 +21,7 @@ from ._lib import DimensionError, FBError, PlanError  # noqa: F401
 from .learned import LearnedButterflyPlan, learned_butterfly  # noqa: F401
 
 __all__ = [
-    "ConvMode", "Engine", "LongConvPlan", "RegularizationConfig", "SmoothDomain", "long_conv",
+    "ConvMode", "Engine", "HostRunner", "LongConvPlan", "RegularizationConfig", "SmoothDomain", "long_conv",
     "regularized_long_conv", "regularized_long_conv_backward", "DimensionError", "FBError",
     "PlanError", "LearnedButterflyPlan", "learned_butterfly",
 ]

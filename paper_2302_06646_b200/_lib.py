@@ -21,7 +21,8 @@ EXPORTED = [
     "fb_plan_create", "fb_plan_destroy", "fb_plan_get_info", "fb_kernel_prep", "fb_plan_copy_kbar",
     "fb_workspace_size", "fb_fwd", "fb_bwd", "fb_learned_plan_create", "fb_learned_plan_destroy",
     "fb_learned_plan_factors", "fb_learned_workspace_size", "fb_learned_fwd", "fb_learned_bwd",
-    "fb_last_error", "fb_version",
+    "fb_last_error", "fb_version", "fb_host_runner_create", "fb_host_runner_destroy",
+    "fb_host_runner_chunk_heads", "fb_host_runner_run",
 ]
 
 
@@ -78,6 +79,13 @@ def lib() -> C.CDLL:
         L.fb_learned_workspace_size.restype = sz
         L.fb_learned_fwd.argtypes = [vp, vp, vp, vp, i64, vp, vp]
         L.fb_learned_bwd.argtypes = [vp, vp, vp, vp, vp, vp, i64, vp, vp]
+        L.fb_host_runner_create.argtypes = [C.POINTER(vp), i64, i64, C.c_int, C.c_int, C.c_int,
+                                             C.c_int, i64, i64]
+        L.fb_host_runner_destroy.argtypes = [vp]
+        L.fb_host_runner_chunk_heads.argtypes = [vp]
+        L.fb_host_runner_chunk_heads.restype = i64
+        L.fb_host_runner_run.argtypes = [vp, C.POINTER(RegConfig), C.c_int, vp, vp, vp, vp, vp,
+                                         vp, vp, vp, vp]
         L.fb_last_error.restype = C.c_char_p
         _lib = L
     return _lib

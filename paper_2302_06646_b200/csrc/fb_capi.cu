@@ -1,6 +1,7 @@
 // FlashButterfly-B200 C ABI (include/flashbutterfly.h): plan lifetime, engine
 // resolution, argument checking and dispatch.  No CPU compute path exists:
 // every entry point either launches sm_100a kernels or returns an error.
+#include <algorithm>
 #include <cmath>
 #include <cstring>
 #include <string>
@@ -267,3 +268,153 @@ int fb_bwd(fb_plan* p, const void* dy, const void* u, void* du, float* dK, float
 }
 
 }  // extern "C"
+
+// ---------------------------------------------------------------- host runner
+struct fb_host_runner {
+  fb_plan* plan = nullptr;  // Hc heads, reused chunk after chunk on the compute stream
+  int64_t N = 0, H = 0, Hc = 0, B = 0;
+  size_t es = 2;
+  cudaStream_t s_in = nullptr, s_comp = nullptr, s_out = nullptr;
+  cudaEvent_t start = nullptr;
+  struct Buf {
+    void *u = nullptr, *dy = nullptr, *y = nullptr, *du = nullptr, *ws = nullptr;
+    float *K = nullptr, *D = nullptr, *dK = nullptr, *dD = nullptr;
+    cudaEvent_t in_ready = nullptr, comp_done = nullptr, out_done = nullptr;
+    bool used = false;
+  } buf[2];
+};
+
+extern "C" {
+
+int fb_host_runner_destroy(fb_host_runner* r) {
+  if (!r) return FB_OK;
+  if (r->plan) cudaSetDevice(r->plan->device);
+  for (auto& b : r->buf) {
+    cudaFree(b.u);
+    cudaFree(b.dy);
+    cudaFree(b.y);
+    cudaFree(b.du);
+    cudaFree(b.ws);
+    cudaFree(b.K);
+    cudaFree(b.D);
+    cudaFree(b.dK);
+    cudaFree(b.dD);
+    if (b.in_ready) cudaEventDestroy(b.in_ready);
+    if (b.comp_done) cudaEventDestroy(b.comp_done);
+    if (b.out_done) cudaEventDestroy(b.out_done);
+  }
+  if (r->start) cudaEventDestroy(r->start);
+  if (r->s_in) cudaStreamDestroy(r->s_in);
+  if (r->s_comp) cudaStreamDestroy(r->s_comp);
+  if (r->s_out) cudaStreamDestroy(r->s_out);
+  fb_plan_destroy(r->plan);
+  delete r;
+  return FB_OK;
+}
+
+int fb_host_runner_create(fb_host_runner** out, int64_t N, int64_t H, int mode, int dtype,
+                          int engine, int device, int64_t B, int64_t heads_per_chunk) {
+  if (!out) return fail(FB_ERR_ARG, "fb_host_runner_create: null output");
+  *out = nullptr;
+  if (H < 1 || B < 1 || heads_per_chunk < 1)
+    return fail(FB_ERR_DIM, "fb_host_runner_create: H, B and heads_per_chunk must be >= 1");
+  int64_t hc = std::min(H, heads_per_chunk);
+  while (H % hc) --hc;
+  auto* r = new fb_host_runner();
+  r->N = N;
+  r->H = H;
+  r->Hc = hc;
+  r->B = B;
+  r->es = dtype == FB_F32 ? 4 : 2;
+  int rc = fb_plan_create(&r->plan, N, hc, mode, dtype, engine, device);
+  if (rc) {
+    delete r;
+    return rc;
+  }
+  const size_t sig = (size_t)B * hc * N * r->es, bank = (size_t)hc * N * sizeof(float);
+  const size_t wsb = fb_workspace_size(r->plan, B);
+  auto mk = [&](void** p2, size_t bytes) {
+    return rc ? rc : (rc = cuda_status(cudaMalloc(p2, bytes), "fb_host_runner: cudaMalloc"));
+  };
+  for (auto& b : r->buf) {
+    mk(&b.u, sig);
+    mk(&b.dy, sig);
+    mk(&b.y, sig);
+    mk(&b.du, sig);
+    mk(&b.ws, wsb);
+    mk((void**)&b.K, bank);
+    mk((void**)&b.D, hc * sizeof(float));
+    mk((void**)&b.dK, bank);
+    mk((void**)&b.dD, hc * sizeof(float));
+    if (!rc) rc = cuda_status(cudaEventCreateWithFlags(&b.in_ready, cudaEventDisableTiming), "event");
+    if (!rc) rc = cuda_status(cudaEventCreateWithFlags(&b.comp_done, cudaEventDisableTiming), "event");
+    if (!rc) rc = cuda_status(cudaEventCreateWithFlags(&b.out_done, cudaEventDisableTiming), "event");
+  }
+  if (!rc) rc = cuda_status(cudaEventCreateWithFlags(&r->start, cudaEventDisableTiming), "event");
+  if (!rc) rc = cuda_status(cudaStreamCreateWithFlags(&r->s_in, cudaStreamNonBlocking), "stream");
+  if (!rc) rc = cuda_status(cudaStreamCreateWithFlags(&r->s_comp, cudaStreamNonBlocking), "stream");
+  if (!rc) rc = cuda_status(cudaStreamCreateWithFlags(&r->s_out, cudaStreamNonBlocking), "stream");
+  if (rc) {
+    fb_host_runner_destroy(r);
+    return rc;
+  }
+  *out = r;
+  return FB_OK;
+}
+
+int64_t fb_host_runner_chunk_heads(const fb_host_runner* r) { return r ? r->Hc : 0; }
+
+int fb_host_runner_run(fb_host_runner* r, const fb_reg_config* cfg, int training, const void* u,
+                       const void* dy, const float* K, const float* D, void* y, void* du,
+                       float* dK, float* dD, void* stream) {
+  if (!r || !cfg || !u || !dy || !K || !D || !y || !du || !dK || !dD)
+    return fail(FB_ERR_ARG, "fb_host_runner_run: null argument");
+  fb_plan* p = r->plan;
+  int rc = cuda_status(cudaSetDevice(p->device), "cudaSetDevice");
+  if (rc) return rc;
+  cudaStream_t caller = (cudaStream_t)stream;
+  const int64_t N = r->N, H = r->H, Hc = r->Hc, B = r->B;
+  const size_t es = r->es;
+  const size_t row = (size_t)Hc * N * es, pitch = (size_t)H * N * es;  // one batch row of a chunk
+  rc = cuda_status(cudaEventRecord(r->start, caller), "event record");
+  for (cudaStream_t s : {r->s_in, r->s_comp, r->s_out})
+    if (!rc) rc = cuda_status(cudaStreamWaitEvent(s, r->start, 0), "stream wait");
+  const int64_t chunks = H / Hc;
+  for (int64_t c = 0; c < chunks && !rc; ++c) {
+    auto& b = r->buf[c & 1];
+    const int64_t h0 = c * Hc;
+    const char* hu = (const char*)u + h0 * N * es;
+    const char* hdy = (const char*)dy + h0 * N * es;
+    // inputs: the previous user of this buffer must be done reading u / dy
+    if (b.used) rc = cuda_status(cudaStreamWaitEvent(r->s_in, b.comp_done, 0), "wait");
+    if (!rc) rc = cuda_status(cudaMemcpy2DAsync(b.u, row, hu, pitch, row, B, cudaMemcpyHostToDevice, r->s_in), "h2d u");
+    if (!rc) rc = cuda_status(cudaMemcpy2DAsync(b.dy, row, hdy, pitch, row, B, cudaMemcpyHostToDevice, r->s_in), "h2d dy");
+    if (!rc) rc = cuda_status(cudaMemcpyAsync(b.K, K + h0 * N, Hc * N * sizeof(float), cudaMemcpyHostToDevice, r->s_in), "h2d K");
+    if (!rc) rc = cuda_status(cudaMemcpyAsync(b.D, D + h0, Hc * sizeof(float), cudaMemcpyHostToDevice, r->s_in), "h2d D");
+    if (!rc) rc = cuda_status(cudaEventRecord(b.in_ready, r->s_in), "event record");
+    // compute: inputs landed, and the previous results of this buffer copied out
+    if (!rc) rc = cuda_status(cudaStreamWaitEvent(r->s_comp, b.in_ready, 0), "wait");
+    if (!rc && b.used) rc = cuda_status(cudaStreamWaitEvent(r->s_comp, b.out_done, 0), "wait");
+    p->head0 = h0;
+    if (!rc) rc = fb_kernel_prep(p, b.K, b.D, cfg, training, r->s_comp);
+    if (!rc) rc = fb_fwd(p, b.u, b.y, B, b.ws, r->s_comp);
+    if (!rc) rc = fb_bwd(p, b.dy, b.u, b.du, b.dK, nullptr, b.dD, B, b.ws, r->s_comp);
+    if (!rc) rc = cuda_status(cudaEventRecord(b.comp_done, r->s_comp), "event record");
+    // outputs
+    if (!rc) rc = cuda_status(cudaStreamWaitEvent(r->s_out, b.comp_done, 0), "wait");
+    if (!rc) rc = cuda_status(cudaMemcpy2DAsync((char*)y + h0 * N * es, pitch, b.y, row, row, B, cudaMemcpyDeviceToHost, r->s_out), "d2h y");
+    if (!rc) rc = cuda_status(cudaMemcpy2DAsync((char*)du + h0 * N * es, pitch, b.du, row, row, B, cudaMemcpyDeviceToHost, r->s_out), "d2h du");
+    if (!rc) rc = cuda_status(cudaMemcpyAsync(dK + h0 * N, b.dK, Hc * N * sizeof(float), cudaMemcpyDeviceToHost, r->s_out), "d2h dK");
+    if (!rc) rc = cuda_status(cudaMemcpyAsync(dD + h0, b.dD, Hc * sizeof(float), cudaMemcpyDeviceToHost, r->s_out), "d2h dD");
+    if (!rc) rc = cuda_status(cudaEventRecord(b.out_done, r->s_out), "event record");
+    b.used = true;
+  }
+  p->head0 = 0;
+  // the caller's stream resumes after everything
+  for (auto& b : r->buf)
+    if (!rc && b.used) rc = cuda_status(cudaStreamWaitEvent(caller, b.out_done, 0), "wait");
+  return rc;
+}
+
+}  // extern "C"
+

@@ -33,6 +33,7 @@ struct fb_plan {
   int64_t p = 0;
   int smooth_domain = FB_SMOOTH_TIME;
   int num_sms = 148;
+  int64_t head0 = 0;  // first global head of this plan (dropout child streams)
 };
 
 struct fb_learned_plan {

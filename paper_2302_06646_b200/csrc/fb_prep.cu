@@ -59,11 +59,11 @@ struct DevRng {
 // keep[h][i] = !(uniform01() < rate), drawn in order from child stream h.
 // The stream is sequential by construction, so one thread walks one head.
 __global__ void dropout_keep_kernel(uint8_t* __restrict__ keep, int H, int64_t N, double rate,
-                                    uint64_t seed) {
+                                    uint64_t seed, int64_t head0) {
   const int h = blockIdx.x * blockDim.x + threadIdx.x;
   if (h >= H) return;
   DevRng r;
-  r.child_of(seed, (uint64_t)h);
+  r.child_of(seed, (uint64_t)(head0 + h));
   uint8_t* k = keep + (size_t)h * N;
   for (int64_t i = 0; i < N; ++i) k[i] = (r.uniform01() < rate) ? 0 : 1;
 }
@@ -152,7 +152,7 @@ __global__ void __launch_bounds__(kRegThreads)
 
 int dropout_keep_dev(fb_plan* p, double rate, uint64_t seed, cudaStream_t s) {
   dropout_keep_kernel<<<(unsigned)((p->H + 127) / 128), 128, 0, s>>>(p->keep, (int)p->H, p->N,
-                                                                       rate, seed);
+                                                                       rate, seed, p->head0);
   return cuda_status(cudaGetLastError(), "dropout_keep");
 }
 

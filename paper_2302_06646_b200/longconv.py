@@ -162,6 +162,55 @@ class LongConvPlan:
         return (du, dK, dD, dKbar) if want_dkbar else (du, dK, dD)
 
 
+class HostRunner:
+    """regularized_long_conv forward + backward on HOST tensors
+    (fb_host_runner_*): heads in chunks, copies in / kernels / copies out
+    overlapped on three streams.  Host tensors should be pinned."""
+
+    def __init__(self, N: int, H: int, B: int, dtype: torch.dtype = torch.bfloat16,
+                 mode: ConvMode = ConvMode.CAUSAL, engine: Engine = Engine.AUTO,
+                 heads_per_chunk: int | None = None, device: int | torch.device | None = None):
+        if dtype not in _DT:
+            raise TypeError(f"unsupported I/O dtype {dtype}")
+        dev = torch.device("cuda", torch.cuda.current_device()) if device is None else torch.device(device)
+        self.N, self.H, self.B, self.dtype, self.device = int(N), int(H), int(B), dtype, dev
+        hc = heads_per_chunk if heads_per_chunk else max(1, self.H // 8)
+        h = C.c_void_p()
+        with torch.cuda.device(dev):
+            check(_lib.lib().fb_host_runner_create(C.byref(h), self.N, self.H, int(mode), _DT[dtype],
+                                                   int(engine), dev.index or 0, self.B, int(hc)))
+        self._h = h
+        self.chunk_heads = int(_lib.lib().fb_host_runner_chunk_heads(h))
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h is not None and h.value:
+            try:
+                _lib.lib().fb_host_runner_destroy(h)
+            except Exception:
+                pass
+            self._h = None
+
+    def run(self, u, dy, K, D, cfg: RegularizationConfig, training: bool = False, out=None):
+        """-> (y, du, dK, dD) host tensors; stream-ordered on the current stream."""
+        B, H, N = self.B, self.H, self.N
+        for x, name, shape, dt in ((u, "u", (B, H, N), self.dtype), (dy, "dy", (B, H, N), self.dtype),
+                                   (K, "K", (H, N), torch.float32), (D, "D", (H,), torch.float32)):
+            if tuple(x.shape) != shape or x.dtype != dt or x.is_cuda or not x.is_contiguous():
+                raise DimensionError(_lib.FB_ERR_DIM, f"{name}: expected contiguous host {dt} "
+                                                      f"{list(shape)}")
+        if out is None:
+            out = (torch.empty_like(u, pin_memory=True), torch.empty_like(u, pin_memory=True),
+                   torch.empty_like(K, pin_memory=True), torch.empty_like(D, pin_memory=True))
+        y, du, dK, dD = out
+        c = cfg.to_c()
+        with torch.cuda.device(self.device):
+            check(_lib.lib().fb_host_runner_run(self._h, C.byref(c), int(training), _ptr(u), _ptr(dy),
+                                                _ptr(K), _ptr(D), _ptr(y), _ptr(du), _ptr(dK),
+                                                _ptr(dD), _stream()))
+        return y, du, dK, dD
+
+
 _PLANS: dict = {}
 
 

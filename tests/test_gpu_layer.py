@@ -301,3 +301,27 @@ def test_config3_heads_sample(lc):
     got = dict(y=to_np(y[:, heads]), du=to_np(du[:, heads]), dK=to_np(dK[heads]),
                dD=to_np(dD[heads]))
     assert_parity(got, want, 2e-2, keys=("y", "du", "dK", "dD"))
+
+
+# ------------------------------------------------------------ host-buffer runner
+@pytest.mark.parametrize("dtype,H,hc,training", [(torch.bfloat16, 12, 4, False),
+                                                 (torch.float32, 6, 2, True)])
+def test_host_runner_matches_device_path(lc, dtype, H, hc, training):
+    """fb_host_runner (pinned host buffers, heads in pipelined chunks) gives
+    the device path's results: y / du per channel bit-identical, dK / dD up to
+    the fixed-order partial grouping; dropout streams follow the global head."""
+    B, N = 5, 4096
+    inp = layer_inputs(lc, B, H, N, dtype)
+    cfg = fb.RegularizationConfig(lambda_=0.003, smooth_width=1,
+                                  dropout_rate=0.2 if training else 0.0, seed=7)
+    _, want = run_layer(inp, N, H, dtype, cfg, training=training)
+    r = fb.HostRunner(N, H, B, dtype, heads_per_chunk=hc)
+    assert r.chunk_heads == hc
+    pin = lambda t: t.cpu().contiguous().pin_memory()  # noqa: E731
+    y, du, dK, dD = r.run(pin(inp["tu"]), pin(inp["tdy"]), pin(inp["tK"]), pin(inp["tD"]), cfg,
+                          training=training)
+    torch.cuda.synchronize()
+    assert np.array_equal(to_np(y), want["y"])
+    assert np.array_equal(to_np(du), want["du"])
+    assert rel_l2(to_np(dK), want["dK"]) < 1e-6
+    assert rel_l2(to_np(dD), want["dD"]) < 1e-6
