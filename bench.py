@@ -161,15 +161,21 @@ def run_ours(args, cfg, rank, world, local_rank):
     h = plan._h
     n_events = []
 
+    # training step: the forward keeps its transform of u for the backward
+    # (tensor-core plans; fb_saved_size is 0 otherwise and the calls recompute)
+    nsaved = plan.saved_size(B)
+    saved = torch.empty(max(nsaved, 1), dtype=torch.uint8, device=dev)
+    Ps = P_(saved) if nsaved else C.c_void_p(0)
+
     def step(rec=None):
         _lib.check(L.fb_kernel_prep(h, P_(K), P_(D), C.byref(c), 0, C.c_void_p(sp)))
         if rec is not None:
             rec[0].record(stream)
-        _lib.check(L.fb_fwd(h, P_(u), P_(y), B, P_(ws), C.c_void_p(sp)))
+        _lib.check(L.fb_fwd_save(h, P_(u), P_(y), Ps, B, P_(ws), C.c_void_p(sp)))
         if rec is not None:
             rec[1].record(stream)
-        _lib.check(L.fb_bwd(h, P_(dy), P_(u), P_(du), P_(dK), C.c_void_p(0), P_(dD), B, P_(ws),
-                            C.c_void_p(sp)))
+        _lib.check(L.fb_bwd_saved(h, P_(dy), P_(u), Ps, P_(du), P_(dK), C.c_void_p(0), P_(dD), B,
+                                  P_(ws), C.c_void_p(sp)))
         if rec is not None:
             rec[2].record(stream)
 
@@ -279,6 +285,8 @@ def run_ours(args, cfg, rank, world, local_rank):
                    "engine": plan.engine.name.lower(), "transform_len": plan.n,
                    "lambda": LAM, "smooth_width": P, "mode": "causal",
                    "sharding": f"heads, {H} per GPU, no communication",
+                   "saved_activation": ("bwd reuses the fwd transform of u "
+                                        f"({nsaved / 2**20:.0f} MiB, bf16)" if nsaved else None),
                    "l2": "inputs larger than L2 (u, dy, y, du = "
                          f"{4 * E * s / 2**20:.0f} MiB per GPU)"},
         "fwd_ms": fwd_ms, "bwd_ms": bwd_ms,

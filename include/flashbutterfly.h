@@ -123,6 +123,19 @@ int fb_fwd(fb_plan* plan, const void* u, void* y, int64_t B, void* workspace, vo
 int fb_bwd(fb_plan* plan, const void* dy, const void* u, void* du, float* dK, float* dKbar,
            float* dD, int64_t B, void* workspace, void* stream);
 
+/* Training-step variant: fb_fwd_save also writes the forward's own
+ * transform of u (U = F(u), bf16 pairs, fb_saved_size bytes, caller-owned)
+ * and fb_bwd_saved reads it instead of transforming u again — the saved
+ * activation of an autograd step.  Results are identical to fb_fwd / fb_bwd
+ * (the recompute path parks exactly these bf16 values).  fb_saved_size is 0
+ * for plans without the tensor-core path; both calls then fall back to
+ * fb_fwd / fb_bwd (and fb_bwd_saved needs u). */
+size_t fb_saved_size(const fb_plan* plan, int64_t B);
+int fb_fwd_save(fb_plan* plan, const void* u, void* y, void* saved, int64_t B, void* workspace,
+                void* stream);
+int fb_bwd_saved(fb_plan* plan, const void* dy, const void* u, const void* saved, void* du,
+                 float* dK, float* dKbar, float* dD, int64_t B, void* workspace, void* stream);
+
 /* Host-buffer layer runner: the whole regularized_long_conv forward +
  * backward (regularize.hpp:67-70 with the SURVEY.md §8c backward) on HOST
  * arrays, pipelined.  The H heads are independent, so the runner walks them

@@ -22,7 +22,8 @@ EXPORTED = [
     "fb_workspace_size", "fb_fwd", "fb_bwd", "fb_learned_plan_create", "fb_learned_plan_destroy",
     "fb_learned_plan_factors", "fb_learned_workspace_size", "fb_learned_fwd", "fb_learned_bwd",
     "fb_last_error", "fb_version", "fb_host_runner_create", "fb_host_runner_destroy",
-    "fb_host_runner_chunk_heads", "fb_host_runner_run",
+    "fb_host_runner_chunk_heads", "fb_host_runner_run", "fb_saved_size", "fb_fwd_save",
+    "fb_bwd_saved",
 ]
 
 
@@ -79,6 +80,10 @@ def lib() -> C.CDLL:
         L.fb_learned_workspace_size.restype = sz
         L.fb_learned_fwd.argtypes = [vp, vp, vp, vp, i64, vp, vp]
         L.fb_learned_bwd.argtypes = [vp, vp, vp, vp, vp, vp, i64, vp, vp]
+        L.fb_saved_size.argtypes = [vp, i64]
+        L.fb_saved_size.restype = sz
+        L.fb_fwd_save.argtypes = [vp, vp, vp, vp, i64, vp, vp]
+        L.fb_bwd_saved.argtypes = [vp, vp, vp, vp, vp, vp, vp, vp, i64, vp, vp]
         L.fb_host_runner_create.argtypes = [C.POINTER(vp), i64, i64, C.c_int, C.c_int, C.c_int,
                                              C.c_int, i64, i64]
         L.fb_host_runner_destroy.argtypes = [vp]

@@ -257,6 +257,29 @@ int fb_fwd(fb_plan* p, const void* u, void* y, int64_t B, void* ws, void* stream
   return p->engine == FB_ENGINE_SINGLE ? sp_fwd(p, u, y, B, s) : tp_fwd(p, u, y, B, ws, s);
 }
 
+size_t fb_saved_size(const fb_plan* p, int64_t B) {
+  if (!p || B < 1 || !p->use_tc) return 0;
+  return tc_saved_size(p, B);
+}
+
+int fb_fwd_save(fb_plan* p, const void* u, void* y, void* saved, int64_t B, void* ws,
+                void* stream) {
+  if (!saved || !p || !p->use_tc) return fb_fwd(p, u, y, B, ws, stream);
+  int rc = check_run(p, B, "fb_fwd_save");
+  if (rc) return rc;
+  if (!u || !y) return fail(FB_ERR_ARG, "fb_fwd_save: null tensor");
+  return tc_fwd(p, u, y, B, (cudaStream_t)stream, saved);
+}
+
+int fb_bwd_saved(fb_plan* p, const void* dy, const void* u, const void* saved, void* du,
+                 float* dK, float* dKbar, float* dD, int64_t B, void* ws, void* stream) {
+  if (!saved || !p || !p->use_tc) return fb_bwd(p, dy, u, du, dK, dKbar, dD, B, ws, stream);
+  int rc = check_run(p, B, "fb_bwd_saved");
+  if (rc) return rc;
+  if (!dy || !du || !dK || !dD || !ws) return fail(FB_ERR_ARG, "fb_bwd_saved: null argument");
+  return tc_bwd(p, dy, u, du, dK, dKbar, dD, B, ws, (cudaStream_t)stream, saved);
+}
+
 int fb_bwd(fb_plan* p, const void* dy, const void* u, void* du, float* dK, float* dKbar,
            float* dD, int64_t B, void* ws, void* stream) {
   int rc = check_run(p, B, "fb_bwd");
@@ -278,6 +301,7 @@ struct fb_host_runner {
   cudaEvent_t start = nullptr;
   struct Buf {
     void *u = nullptr, *dy = nullptr, *y = nullptr, *du = nullptr, *ws = nullptr;
+    void* saved = nullptr;  // the forward's transform of u (tensor-core plans)
     float *K = nullptr, *D = nullptr, *dK = nullptr, *dD = nullptr;
     cudaEvent_t in_ready = nullptr, comp_done = nullptr, out_done = nullptr;
     bool used = false;
@@ -295,6 +319,7 @@ int fb_host_runner_destroy(fb_host_runner* r) {
     cudaFree(b.y);
     cudaFree(b.du);
     cudaFree(b.ws);
+    cudaFree(b.saved);
     cudaFree(b.K);
     cudaFree(b.D);
     cudaFree(b.dK);
@@ -342,6 +367,7 @@ int fb_host_runner_create(fb_host_runner** out, int64_t N, int64_t H, int mode, 
     mk(&b.y, sig);
     mk(&b.du, sig);
     mk(&b.ws, wsb);
+    if (const size_t sv = fb_saved_size(r->plan, B)) mk(&b.saved, sv);
     mk((void**)&b.K, bank);
     mk((void**)&b.D, hc * sizeof(float));
     mk((void**)&b.dK, bank);
@@ -397,8 +423,8 @@ int fb_host_runner_run(fb_host_runner* r, const fb_reg_config* cfg, int training
     if (!rc && b.used) rc = cuda_status(cudaStreamWaitEvent(r->s_comp, b.out_done, 0), "wait");
     p->head0 = h0;
     if (!rc) rc = fb_kernel_prep(p, b.K, b.D, cfg, training, r->s_comp);
-    if (!rc) rc = fb_fwd(p, b.u, b.y, B, b.ws, r->s_comp);
-    if (!rc) rc = fb_bwd(p, b.dy, b.u, b.du, b.dK, nullptr, b.dD, B, b.ws, r->s_comp);
+    if (!rc) rc = fb_fwd_save(p, b.u, b.y, b.saved, B, b.ws, r->s_comp);
+    if (!rc) rc = fb_bwd_saved(p, b.dy, b.u, b.saved, b.du, b.dK, nullptr, b.dD, B, b.ws, r->s_comp);
     if (!rc) rc = cuda_status(cudaEventRecord(b.comp_done, r->s_comp), "event record");
     // outputs
     if (!rc) rc = cuda_status(cudaStreamWaitEvent(r->s_out, b.comp_done, 0), "wait");

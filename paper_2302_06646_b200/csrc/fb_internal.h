@@ -72,10 +72,13 @@ int encode_map_3d(CUtensorMap* map, CUtensorMapDataType type, const void* ptr, c
 // tcgen05 single-pass (fb_single_tc.cu)
 bool tc_eligible(const fb_plan* p);
 int tc_init(fb_plan* p);
-int tc_fwd(fb_plan* p, const void* u, void* y, int64_t B, cudaStream_t s);
+// usave (optional): the forward writes U = F(u) there (tc_saved_size bytes)
+// and the backward reads it instead of recomputing (u may then be null)
+size_t tc_saved_size(const fb_plan* p, int64_t B);
+int tc_fwd(fb_plan* p, const void* u, void* y, int64_t B, cudaStream_t s, void* usave = nullptr);
 size_t tc_workspace(const fb_plan* p, int64_t B);
 int tc_bwd(fb_plan* p, const void* dy, const void* u, void* du, float* dK, float* dKbar, float* dD,
-           int64_t B, void* ws, cudaStream_t s);
+           int64_t B, void* ws, cudaStream_t s, const void* usave = nullptr);
 
 // three-pass (fb_three.cu)
 int tp_prep(fb_plan* p, const float* K, cudaStream_t s);

@@ -555,6 +555,13 @@ __device__ __forceinline__ void cta_range(int total, int& i0, int& i1) {
   i1 = (int)(((int64_t)(blockIdx.x + 1) * total) / gridDim.x);
 }
 
+__device__ __forceinline__ uint32_t pack_bf2(float a, float b) {
+  __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
+  return *reinterpret_cast<uint32_t*>(&h);
+}
+__device__ __forceinline__ float2 unpack_bf2(uint32_t v) {
+  return __bfloat1622float2(*reinterpret_cast<__nv_bfloat162*>(&v));
+}
 // ------------------------------------------------------------------ forward
 // Persistent: CTA c owns pairs [i0, i1) in head-major order; slot s takes
 // i0 + s, i0 + s + 2, ...  Each slot keeps its head's k_f' (fp16 pairs
@@ -585,7 +592,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     tc_fwd_kernel(const __grid_constant__ CUtensorMap umap, T* __restrict__ y,
                   const __half2* __restrict__ kf16, const float* __restrict__ kscale,
                   const uint4* __restrict__ mats, const float2* __restrict__ tab_g, int B, int H,
-                  int total) {
+                  int total, uint32_t* __restrict__ usave) {
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   __shared__ uint32_t tmem_slot;
   __shared__ __align__(8) uint64_t bars[4];  // mma[2], in[2]
@@ -629,6 +636,11 @@ __global__ void __launch_bounds__(kThreads, 1)
         tld<8>(taddr(c, c.aux + cb), kr);
         tld<8>(taddr(c, c.aux + 64 + cb), ki);
         tc::ld_wait();
+        if (usave) {  // U = F(u) for the backward, bf16 pairs [pair][f1][f2]
+          uint32_t* us = usave + (size_t)item * kN + (size_t)cb * 128 + f2;
+#pragma unroll
+          for (int j = 0; j < 8; ++j) us[j * 128] = pack_bf2(re[j], im[j]);
+        }
 #pragma unroll
         for (int j = 0; j < 8; ++j) {
           const float a = re[j], b = im[j];
@@ -657,24 +669,19 @@ __global__ void __launch_bounds__(kThreads, 1)
 // du = F^-1(DY conj(k_f')).  At a segment end S goes to spart[cta][seg]
 // (natural order) for the finalize kernel (dKbar = Re F^-1(sum S)/n,
 // dD = dKbar[0]).
-__device__ __forceinline__ uint32_t pack_bf2(float a, float b) {
-  __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
-  return *reinterpret_cast<uint32_t*>(&h);
-}
-__device__ __forceinline__ float2 unpack_bf2(uint32_t v) {
-  return __bfloat1622float2(*reinterpret_cast<__nv_bfloat162*>(&v));
-}
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(ptx::smem_u32(bar)) : "memory");
 }
 
-template <typename T>
+// SAVED: U comes from the forward's usave (bf16 pairs, exactly what the
+// recompute path parks) instead of F(u): one transform per pair fewer.
+template <typename T, bool SAVED>
 __global__ void __launch_bounds__(kThreads, 1)
     tc_bwd_kernel(const __grid_constant__ CUtensorMap dymap, const __grid_constant__ CUtensorMap umap,
                   T* __restrict__ du, const __half2* __restrict__ kf16,
                   const float* __restrict__ kscale, const uint4* __restrict__ mats,
                   const float2* __restrict__ tab_g, float2* __restrict__ spart, int B, int H,
-                  int total, int maxseg) {
+                  int total, int maxseg, const uint32_t* __restrict__ usave) {
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   __shared__ uint32_t tmem_slot;
   __shared__ __align__(8) uint64_t bars[6];  // mma[2], in[2], S chain[2] (256 arrivals)
@@ -720,10 +727,19 @@ __global__ void __launch_bounds__(kThreads, 1)
     c.seg0 = c.nb;
     if (lead && (int)slot < L) {
       const int it = a + (int)slot;
-      load_pair(sm + c.in_off, &umap, h, 2 * (it - h * npairs), in_bar);
+      load_pair(sm + c.in_off, SAVED ? &dymap : &umap, h, 2 * (it - h * npairs), in_bar);
     }
     for (int j = (int)slot, k = 0; j < L; j += 2, ++k) {
       const int b0 = 2 * (a + j - h * npairs);
+      uint32_t ur[kColsPer];
+      if constexpr (SAVED) {
+        // ---- U from the forward (loads in flight across DY's stage A)
+        uint32_t f2, g;
+        coords(f2, g);
+        const uint32_t* us = usave + (size_t)(a + j) * kN + (size_t)(kColsPer * g) * 128 + f2;
+#pragma unroll
+        for (uint32_t jj = 0; jj < kColsPer; ++jj) ur[jj] = __ldg(us + jj * 128);
+      } else {
       // ---- U = F(u), parked as bf16 pairs
       { TT_BEGIN ptx::mbar_wait(in_bar, in_cnt & 1); TT_END(22) }
       ++in_cnt;
@@ -747,11 +763,20 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         tst_wait();
       }
+      }
       // ---- DY = F(dy)
       { TT_BEGIN ptx::mbar_wait(in_bar, in_cnt & 1); TT_END(23) }
       ++in_cnt;
       issue<T, true>(c, 0);
-      if (lead && j + 2 < L) load_pair(sm + c.in_off, &umap, h, b0 + 4, in_bar);
+      if (lead && j + 2 < L) load_pair(sm + c.in_off, SAVED ? &dymap : &umap, h, b0 + 4, in_bar);
+      if constexpr (SAVED) {  // the saved U into this slot's parking columns
+        uint32_t f2, g;
+        coords(f2, g);
+#pragma unroll
+        for (uint32_t q = 0; q < kColsPer / 8; ++q)
+          tst8(taddr(c, c.aux + kColsPer * g + 8 * q), reinterpret_cast<const float*>(ur + 8 * q));
+        tst_wait();
+      }
       { TT_BEGIN epi_A_exit<T, true>(c); TT_END(25) }
       issue<T, true>(c, 1);
       // ---- S += conj(U) DY (in pair order), Z = DY conj(k_f') -> B' operand
@@ -966,7 +991,11 @@ int tc_init(fb_plan* p) {
   return rc;
 }
 
-int tc_fwd(fb_plan* p, const void* u, void* y, int64_t B, cudaStream_t s) {
+size_t tc_saved_size(const fb_plan* p, int64_t B) {
+  return (size_t)tc_grid(p, B).total * kN * sizeof(uint32_t);
+}
+
+int tc_fwd(fb_plan* p, const void* u, void* y, int64_t B, cudaStream_t s, void* usave) {
   const TcGrid gr = tc_grid(p, B);
   CUtensorMap map;
   auto go = [&](auto tv) {
@@ -977,7 +1006,8 @@ int tc_fwd(fb_plan* p, const void* u, void* y, int64_t B, cudaStream_t s) {
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM_FWD);
     k<<<(unsigned)gr.ctas, kThreads, SMEM_FWD, s>>>(map, (T*)y, (const __half2*)p->kf_tc,
                                                      p->kf_scale, (const uint4*)p->tc_mats, p->tw2,
-                                                     (int)B, (int)p->H, gr.total);
+                                                     (int)B, (int)p->H, gr.total,
+                                                     (uint32_t*)usave);
     return cuda_status(cudaGetLastError(), "tc_fwd");
   };
   return p->dtype == FB_BF16 ? go(__nv_bfloat16{}) : go(__half{});
@@ -989,20 +1019,23 @@ size_t tc_workspace(const fb_plan* p, int64_t B) {
 }
 
 int tc_bwd(fb_plan* p, const void* dy, const void* u, void* du, float* dK, float* dKbar, float* dD,
-           int64_t B, void* ws, cudaStream_t s) {
+           int64_t B, void* ws, cudaStream_t s, const void* usave) {
   const TcGrid gr = tc_grid(p, B);
   float2* spart = (float2*)ws;
   CUtensorMap dmap, umap;
   auto go = [&](auto tv) {
     using T = decltype(tv);
     int rc = make_map<T>(&dmap, dy, B, p->H);
-    if (!rc) rc = make_map<T>(&umap, u, B, p->H);
+    if (!rc) rc = make_map<T>(&umap, usave ? dy : u, B, p->H);
     if (rc) return rc;
-    auto k = tc_bwd_kernel<T>;
-    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM_BWD3);
-    k<<<(unsigned)gr.ctas, kThreads, SMEM_BWD3, s>>>(
-        dmap, umap, (T*)du, (const __half2*)p->kf_tc, p->kf_scale, (const uint4*)p->tc_mats,
-        p->tw2, spart, (int)B, (int)p->H, gr.total, gr.maxseg);
+    auto launch = [&](auto kern) {
+      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM_BWD3);
+      kern<<<(unsigned)gr.ctas, kThreads, SMEM_BWD3, s>>>(
+          dmap, umap, (T*)du, (const __half2*)p->kf_tc, p->kf_scale, (const uint4*)p->tc_mats,
+          p->tw2, spart, (int)B, (int)p->H, gr.total, gr.maxseg, (const uint32_t*)usave);
+    };
+    if (usave) launch(tc_bwd_kernel<T, true>);
+    else launch(tc_bwd_kernel<T, false>);
     return cuda_status(cudaGetLastError(), "tc_bwd");
   };
   int rc = p->dtype == FB_BF16 ? go(__nv_bfloat16{}) : go(__half{});

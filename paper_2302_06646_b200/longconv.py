@@ -137,28 +137,50 @@ class LongConvPlan:
         return x.shape[0]
 
     # -- K2/K3 ------------------------------------------------------------------
+    def saved_size(self, B: int) -> int:
+        """Bytes of the forward's saved transform (0: this plan recomputes)."""
+        return int(_lib.lib().fb_saved_size(self._h, int(B)))
+
     def forward(self, u: torch.Tensor, out: torch.Tensor | None = None,
-                workspace: torch.Tensor | None = None) -> torch.Tensor:
+                workspace: torch.Tensor | None = None, save: bool | torch.Tensor = False):
+        """y (and, with save=True or a buffer, (y, saved) for backward(saved=...))."""
         B = self._check_signal(u, "u")
         y = torch.empty_like(u) if out is None else out
         ws = self.workspace(B) if workspace is None else workspace
-        check(_lib.lib().fb_fwd(self._h, _ptr(u), _ptr(y), B, _ptr(ws), _stream()))
-        return y
+        if save is False:
+            check(_lib.lib().fb_fwd(self._h, _ptr(u), _ptr(y), B, _ptr(ws), _stream()))
+            return y
+        nbytes = self.saved_size(B)
+        saved = None
+        if nbytes:
+            saved = save if isinstance(save, torch.Tensor) else torch.empty(
+                nbytes, dtype=torch.uint8, device=self.device)
+        check(_lib.lib().fb_fwd_save(self._h, _ptr(u), _ptr(y), _ptr(saved), B, _ptr(ws),
+                                     _stream()))
+        return y, saved
 
     # -- K4 ------------------------------------------------------------------
-    def backward(self, dy: torch.Tensor, u: torch.Tensor, want_dkbar: bool = False,
-                 workspace: torch.Tensor | None = None):
-        """-> (du, dK, dD[, dKbar]); dK w.r.t. the raw K given to prep()."""
+    def backward(self, dy: torch.Tensor, u: torch.Tensor | None, want_dkbar: bool = False,
+                 workspace: torch.Tensor | None = None, saved: torch.Tensor | None = None,
+                 out: tuple | None = None):
+        """-> (du, dK, dD[, dKbar]); dK w.r.t. the raw K given to prep().  With the
+        forward's `saved` transform u may be None (tensor-core plans)."""
         B = self._check_signal(dy, "dy")
-        if self._check_signal(u, "u") != B:
-            raise DimensionError(_lib.FB_ERR_DIM, "backward: dy and u batch mismatch")
-        du = torch.empty_like(u)
-        dK = torch.empty(self.H, self.N, dtype=torch.float32, device=self.device)
-        dD = torch.empty(self.H, dtype=torch.float32, device=self.device)
+        if saved is None or u is not None:
+            if u is None:
+                raise DimensionError(_lib.FB_ERR_DIM, "backward: u is required without saved")
+            if self._check_signal(u, "u") != B:
+                raise DimensionError(_lib.FB_ERR_DIM, "backward: dy and u batch mismatch")
+        if out is None:
+            du = torch.empty_like(dy)
+            dK = torch.empty(self.H, self.N, dtype=torch.float32, device=self.device)
+            dD = torch.empty(self.H, dtype=torch.float32, device=self.device)
+        else:
+            du, dK, dD = out
         dKbar = torch.empty_like(dK) if want_dkbar else None
         ws = self.workspace(B) if workspace is None else workspace
-        check(_lib.lib().fb_bwd(self._h, _ptr(dy), _ptr(u), _ptr(du), _ptr(dK), _ptr(dKbar),
-                                _ptr(dD), B, _ptr(ws), _stream()))
+        check(_lib.lib().fb_bwd_saved(self._h, _ptr(dy), _ptr(u), _ptr(saved), _ptr(du), _ptr(dK),
+                                      _ptr(dKbar), _ptr(dD), B, _ptr(ws), _stream()))
         return (du, dK, dD, dKbar) if want_dkbar else (du, dK, dD)
 
 
@@ -257,8 +279,11 @@ class _LongConvFn(torch.autograd.Function):
         B, H, N = u.shape
         plan = get_plan(N, H, mode, u.dtype, engine, u.device)
         plan.prep(K, D, cfg, training)
-        y = plan.forward(u.contiguous())
+        # tensor-core plans also keep the forward's transform of u (the
+        # backward then skips recomputing it)
+        y, saved = plan.forward(u.contiguous(), save=True)
         ctx.save_for_backward(u, K, D)
+        ctx.saved_u = saved
         ctx.cfg, ctx.plan, ctx.training = cfg, plan, training
         ctx.token = plan._token
         return y
@@ -269,7 +294,8 @@ class _LongConvFn(torch.autograd.Function):
         plan = ctx.plan
         if plan._token != ctx.token:  # plan re-prepared by another call meanwhile
             plan.prep(K, D, ctx.cfg, ctx.training)
-        du, dK, dD = plan.backward(dy.contiguous().to(u.dtype), u.contiguous())
+        du, dK, dD = plan.backward(dy.contiguous().to(u.dtype), u.contiguous(), saved=ctx.saved_u)
+        ctx.saved_u = None
         return du, dK.to(K.dtype), dD.to(D.dtype), None, None, None, None
 
 

@@ -325,3 +325,20 @@ def test_host_runner_matches_device_path(lc, dtype, H, hc, training):
     assert np.array_equal(to_np(du), want["du"])
     assert rel_l2(to_np(dK), want["dK"]) < 1e-6
     assert rel_l2(to_np(dD), want["dD"]) < 1e-6
+
+
+@pytest.mark.parametrize("B,H", [(32, 20), (7, 3)])
+def test_tensor_core_saved_transform(lc, B, H):
+    """fb_fwd_save / fb_bwd_saved (the backward reads the forward's transform
+    of u) gives bit-identical results to the recompute path: it parks exactly
+    the same bf16 values."""
+    N, dtype = 4096, torch.bfloat16
+    inp = layer_inputs(lc, B, H, N, dtype)
+    cfg = fb.RegularizationConfig(**CFG)
+    plan, want = run_layer(inp, N, H, dtype, cfg, engine=1)
+    assert plan.saved_size(B) == ((B + 1) // 2) * H * 8192 * 4
+    y, saved = plan.forward(inp["tu"], save=True)
+    du, dK, dD = plan.backward(inp["tdy"], None, saved=saved)
+    torch.cuda.synchronize()
+    for k, v in (("y", y), ("du", du), ("dK", dK), ("dD", dD)):
+        assert np.array_equal(to_np(v), want[k]), k
