@@ -61,6 +61,7 @@ int sp_bwd(fb_plan* p, const void* dy, const void* u, void* du, float* dK, float
 // total = H x npairs head-major pairs (fb_single_tc.cu).
 struct SpartMap {
   int ctas, total, npairs, maxseg;
+  int even = 0;  // CTA shares start at 2 floor(c ceil(total/2) / ctas)
 };
 int sp_finalize(fb_plan* p, const float2* spart, const float* ddpart, int chunks, float* dkbar,
                 float* dD, float* dK, int dd_lag0, const SpartMap* map, cudaStream_t s);

@@ -416,10 +416,14 @@ __global__ void __launch_bounds__(FftShape<LOG2N>::T, 2)
   if (map.ctas > 0) {
     // the CTAs whose shares meet head h's pairs [h np, (h+1) np), in order
     const int64_t G = map.ctas, T = map.total, np = map.npairs;
-    const int c0 = (int)((((int64_t)h * np + 1) * G - 1) / T);
-    const int c1 = (int)(((((int64_t)h + 1) * np) * G - 1) / T);
+    // CTA owning pair i: the last c with start(c) <= i
+    const int64_t U = (T + 1) / 2;
+    auto owner = [&](int64_t i) {
+      return map.even ? (int)((((i / 2) + 1) * G - 1) / U) : (int)(((i + 1) * G - 1) / T);
+    };
+    const int c0 = owner((int64_t)h * np), c1 = owner(((int64_t)h + 1) * np - 1);
     for (int c = c0; c <= c1; ++c) {
-      const int64_t start = (int64_t)c * T / G;
+      const int64_t start = map.even ? 2 * ((int64_t)c * U / G) : (int64_t)c * T / G;
       const int seg = (int)h - (int)(start / np);
       const float2* sp = spart + ((size_t)c * map.maxseg + seg) * S::n;
 #pragma unroll
@@ -544,7 +548,7 @@ struct Sp {
     k<<<(unsigned)p->H, FftShape<LOG2N>::T, sm, s>>>(
         spart, ddpart, chunks, dkbar, dD, p->kbar, p->use_keep ? p->keep : nullptr, dK, p->tw2,
         (uint32_t)p->N, scale, p->p, p->keep_scale, p->smooth_domain == FB_SMOOTH_FREQUENCY,
-        dd_lag0, map ? *map : SpartMap{0, 0, 0, 0});
+        dd_lag0, map ? *map : SpartMap{0, 0, 0, 0, 0});
   }
 };
 

@@ -550,6 +550,15 @@ __device__ __forceinline__ void teardown(uint32_t tmem) {
 }
 
 // The CTA's contiguous share [i0, i1) of the B/2 x H (head-major) channel pairs
+// Backward: shares start on even pair indices (heads hold an even number of
+// pairs whenever B/2 is even), so each head segment splits evenly over the two
+// slots and neither idles a whole pair at the segment barrier.  CTA c starts
+// at 2 floor(c U / G), U = ceil(total / 2) (mirrored by the finalize).
+__device__ __forceinline__ void cta_range_even(int total, int& i0, int& i1) {
+  const int64_t U = (total + 1) / 2;
+  i0 = min(total, (int)(2 * ((int64_t)blockIdx.x * U / gridDim.x)));
+  i1 = min(total, (int)(2 * ((int64_t)(blockIdx.x + 1) * U / gridDim.x)));
+}
 __device__ __forceinline__ void cta_range(int total, int& i0, int& i1) {
   i0 = (int)(((int64_t)blockIdx.x * total) / gridDim.x);
   i1 = (int)(((int64_t)(blockIdx.x + 1) * total) / gridDim.x);
@@ -688,7 +697,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   unsigned char* sm = smem_base(smem_raw);
   const int npairs = (B + 1) / 2;
   int i0, i1;
-  cta_range(total, i0, i1);
+  cta_range_even(total, i0, i1);
   setup(sm, &tmem_slot, bars, 6, 2, mats, tab_g, SMAT3, STAB3);
   const uint32_t slot = threadIdx.x / kSlotThreads;
   Ctx c = make_ctx(sm, tmem_slot, slot, &bars[slot], true);
@@ -961,14 +970,17 @@ int make_map(CUtensorMap* map, const void* ptr, int64_t B, int64_t H) {
 // Persistent grid: one CTA per SM (or per pair when there are fewer),
 // contiguous head-major shares of the B/2 x H channel pairs.
 struct TcGrid {
-  int ctas, total, npairs, maxseg;
+  int ctas, total, npairs;
+  int bctas, maxseg;  // backward: CTAs over even-aligned shares (none empty), segments per CTA
 };
 TcGrid tc_grid(const fb_plan* p, int64_t B) {
   TcGrid g;
   g.npairs = (int)((B + 1) / 2);
   g.total = (int)(p->H * g.npairs);
   g.ctas = std::max(1, std::min(p->num_sms, g.total));
-  const int per = (g.total + g.ctas - 1) / g.ctas;
+  const int U = (g.total + 1) / 2;
+  g.bctas = std::max(1, std::min(p->num_sms, U));
+  const int per = 2 * ((U + g.bctas - 1) / g.bctas);
   g.maxseg = (per + g.npairs - 1) / g.npairs + 1;  // head segments one CTA can touch
   return g;
 }
@@ -1015,7 +1027,7 @@ int tc_fwd(fb_plan* p, const void* u, void* y, int64_t B, cudaStream_t s, void* 
 
 size_t tc_workspace(const fb_plan* p, int64_t B) {
   const TcGrid gr = tc_grid(p, B);
-  return (size_t)gr.ctas * gr.maxseg * kN * sizeof(float2) + 256;
+  return (size_t)gr.bctas * gr.maxseg * kN * sizeof(float2) + 256;
 }
 
 int tc_bwd(fb_plan* p, const void* dy, const void* u, void* du, float* dK, float* dKbar, float* dD,
@@ -1030,7 +1042,7 @@ int tc_bwd(fb_plan* p, const void* dy, const void* u, void* du, float* dK, float
     if (rc) return rc;
     auto launch = [&](auto kern) {
       cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM_BWD3);
-      kern<<<(unsigned)gr.ctas, kThreads, SMEM_BWD3, s>>>(
+      kern<<<(unsigned)gr.bctas, kThreads, SMEM_BWD3, s>>>(
           dmap, umap, (T*)du, (const __half2*)p->kf_tc, p->kf_scale, (const uint4*)p->tc_mats,
           p->tw2, spart, (int)B, (int)p->H, gr.total, gr.maxseg, (const uint32_t*)usave);
     };
@@ -1040,7 +1052,7 @@ int tc_bwd(fb_plan* p, const void* dy, const void* u, void* du, float* dK, float
   };
   int rc = p->dtype == FB_BF16 ? go(__nv_bfloat16{}) : go(__half{});
   if (rc) return rc;
-  const SpartMap m{gr.ctas, gr.total, gr.npairs, gr.maxseg};
+  const SpartMap m{gr.bctas, gr.total, gr.npairs, gr.maxseg, 1};
   return sp_finalize(p, spart, nullptr, 0, dKbar, dD, dK, 1, &m, s);
 }
 
