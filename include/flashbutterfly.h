@@ -159,6 +159,25 @@ int fb_host_runner_run(fb_host_runner* runner, const fb_reg_config* cfg, int tra
                        const void* u, const void* dy, const float* K, const float* D, void* y,
                        void* du, float* dK, float* dD, void* stream);
 
+/* Sequence-sharded local passes (config 5-4M: the transform n = l m itself
+ * split over ranks, paper_2302_06646_b200/seqshard.py; three_pass.cpp:225-254
+ * with the all-to-all transposes between the passes).  l = 8192 and
+ * 16 <= m = n / l <= 1024.  Data is complex f32 (interleaved re, im).
+ *   fb_shard_columns: [C][m][lp] columns tau0 .. tau0+lp of every row;
+ *     inverse = 0:  out[a][t] = w_n^(-a tau) sum_c w_m^(-a c) in[c][t]   (pass 1)
+ *     inverse = 1:  out[c][t] = (1/n) sum_a w_m^(+a c) w_n^(+a tau) in[a][t]  (pass 3)
+ *   fb_shard_rows: [C][mp][l] rows, in place:
+ *     mode 0:  rows = sum_s w_l^(+s t) FFT_l(rows)[s] kf2[s]   (kf2 [C][mp][l])
+ *     mode 1:  kf2_out = scale FFT_l(rows)                      (spectrum rows) */
+typedef struct fb_shard_plan fb_shard_plan;
+int fb_shard_plan_create(fb_shard_plan** plan, int64_t n, int device);
+int fb_shard_plan_destroy(fb_shard_plan* plan);
+int fb_shard_plan_dims(const fb_shard_plan* plan, int64_t* l, int64_t* m);
+int fb_shard_columns(fb_shard_plan* plan, const void* in, void* out, int64_t C, int64_t tau0,
+                     int64_t lp, int inverse, void* stream);
+int fb_shard_rows(fb_shard_plan* plan, void* rows, const void* kf2, void* kf2_out, int64_t C,
+                  int64_t mp, int mode, float scale, void* stream);
+
 /* Learned butterfly (K5).  Replaces learned_forward / learned_gradients
  * (butterfly.hpp:88-108, butterfly.cpp:221-307) batched over rows: rows
  * [B][H] of complex length n, with per-head block parameters (one factor x

@@ -23,7 +23,8 @@ EXPORTED = [
     "fb_learned_plan_factors", "fb_learned_workspace_size", "fb_learned_fwd", "fb_learned_bwd",
     "fb_last_error", "fb_version", "fb_host_runner_create", "fb_host_runner_destroy",
     "fb_host_runner_chunk_heads", "fb_host_runner_run", "fb_saved_size", "fb_fwd_save",
-    "fb_bwd_saved",
+    "fb_bwd_saved", "fb_shard_plan_create", "fb_shard_plan_destroy", "fb_shard_plan_dims",
+    "fb_shard_columns", "fb_shard_rows",
 ]
 
 
@@ -80,6 +81,11 @@ def lib() -> C.CDLL:
         L.fb_learned_workspace_size.restype = sz
         L.fb_learned_fwd.argtypes = [vp, vp, vp, vp, i64, vp, vp]
         L.fb_learned_bwd.argtypes = [vp, vp, vp, vp, vp, vp, i64, vp, vp]
+        L.fb_shard_plan_create.argtypes = [C.POINTER(vp), i64, C.c_int]
+        L.fb_shard_plan_destroy.argtypes = [vp]
+        L.fb_shard_plan_dims.argtypes = [vp, C.POINTER(i64), C.POINTER(i64)]
+        L.fb_shard_columns.argtypes = [vp, vp, vp, i64, i64, i64, C.c_int, vp]
+        L.fb_shard_rows.argtypes = [vp, vp, vp, vp, i64, i64, C.c_int, C.c_float, vp]
         L.fb_saved_size.argtypes = [vp, i64]
         L.fb_saved_size.restype = sz
         L.fb_fwd_save.argtypes = [vp, vp, vp, vp, i64, vp, vp]

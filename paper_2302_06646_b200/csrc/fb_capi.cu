@@ -82,6 +82,13 @@ static int upload_twiddles_big(float2** dst, int64_t n) {
                      "cudaMemcpy(twiddles big)");
 }
 
+// kind 0: full table, 1: two-level (64), 2: two-level (4096) — shared with
+// the sequence-sharded plan in fb_three.cu
+int upload_table(float2** dst, int64_t n, int kind) {
+  return kind == 0 ? upload_twiddles(dst, n) : kind == 1 ? upload_twiddles2(dst, n)
+                                                         : upload_twiddles_big(dst, n);
+}
+
 constexpr int64_t kSinglePassMax = 8192;   // fp32 complex transform in smem
 constexpr int64_t kThreePassRow = 8192;    // l: row length of pass 2
 constexpr int64_t kMinTransform = 256;

@@ -847,6 +847,39 @@ __global__ void __launch_bounds__(kBigThreads, 1)
   }
 }
 
+// ---------------------------------------------------------------- sequence-sharded passes
+// Local passes of the four-step convolution when the transform itself is
+// sharded over ranks (config 5-4M, paper_2302_06646_b200/seqshard.py): rank r
+// holds columns tau in [tau0, tau0 + lp) of every row c of n = l m, as complex
+// fp32 [C][m][lp].  Same arithmetic as passes 1 / 3 (three_pass.cpp:225-254)
+// with the global column index in the twiddle:
+//   SIGN -1:  out[a][tau] = w_n^(-a tau) sum_c w_m^(-a c) in[c][tau]
+//   SIGN +1:  out[c][tau] = scale sum_a w_m^(+a c) w_n^(+a tau) in[a][tau]
+template <int SIGN, int SMALL>
+__global__ void __launch_bounds__(kBigThreads, 1)
+    tp_shard_cols_kernel(const float2* __restrict__ in, float2* __restrict__ out,
+                         const float2* __restrict__ tw_m, const float2* __restrict__ tb, uint32_t m,
+                         uint32_t lp, uint32_t tau0, float scale) {
+  extern __shared__ __align__(16) float2 tsm[];
+  const uint32_t TAU = kBigTile / m;
+  const uint32_t c0 = blockIdx.x * TAU;
+  const size_t ch = (size_t)blockIdx.y * m * lp;
+  for (uint32_t i = threadIdx.x; i < kBigTile; i += kBigThreads) {
+    const uint32_t e = i / TAU, c = i % TAU;
+    float2 v = __ldg(in + ch + (size_t)e * lp + c0 + c);
+    if (SIGN > 0) v = cmul(v, tw_big<+1>(tb, e * (tau0 + c0 + c)));
+    tsm[pad16(e) * TAU + c] = v;
+  }
+  __syncthreads();
+  smem_passes<SIGN, SMALL>(tsm, m, TAU, 1, m, tw_m);
+  for (uint32_t i = threadIdx.x; i < kBigTile; i += kBigThreads) {
+    const uint32_t a = i / TAU, c = i % TAU;
+    float2 v = tsm[pad16(a) * TAU + c];
+    v = SIGN < 0 ? cmul(v, tw_big<-1>(tb, a * (tau0 + c0 + c))) : cscale(v, scale);
+    out[ch + (size_t)a * lp + c0 + c] = v;
+  }
+}
+
 // ---------------------------------------------------------------- host side
 namespace {
 
@@ -1210,3 +1243,130 @@ int tp_bwd(fb_plan* p, const void* dy, const void* u, void* du, float* dK, float
 }
 
 }  // namespace fb
+
+// ---------------------------------------------------------------- sequence-sharded C ABI
+namespace fb {
+int upload_table(float2** dst, int64_t n, int kind);  // fb_capi.cu
+}
+using namespace fb;
+
+struct fb_shard_plan {
+  int64_t l = kL, m = 0, n = 0;
+  int device = 0;
+  float2* tw_m = nullptr;    // exp(-2 pi i t / m)
+  float2* tw_big = nullptr;  // two-level exp(-2 pi i t / n)
+  float2* tw_l = nullptr;    // two-level table of the l-point row FFT
+};
+
+extern "C" {
+
+int fb_shard_plan_destroy(fb_shard_plan* sp) {
+  if (!sp) return FB_OK;
+  cudaFree(sp->tw_m);
+  cudaFree(sp->tw_big);
+  cudaFree(sp->tw_l);
+  delete sp;
+  return FB_OK;
+}
+
+int fb_shard_plan_create(fb_shard_plan** out, int64_t n, int device) {
+  if (!out) {
+    set_error("fb_shard_plan_create: null output");
+    return FB_ERR_ARG;
+  }
+  *out = nullptr;
+  if (n < 16 * (int64_t)kL || (n & (n - 1)) || n / kL > 1024) {
+    set_error("fb_shard_plan_create: n must be a power of two with 16 <= n / 8192 <= 1024");
+    return FB_ERR_PLAN;
+  }
+  int rc = cuda_status(cudaSetDevice(device), "cudaSetDevice");
+  if (rc) return rc;
+  auto* sp = new fb_shard_plan();
+  sp->n = n;
+  sp->m = n / kL;
+  sp->device = device;
+  rc = upload_table(&sp->tw_m, sp->m, 0);
+  if (!rc) rc = upload_table(&sp->tw_big, n, 2);
+  if (!rc) rc = upload_table(&sp->tw_l, kL, 1);
+  if (rc) {
+    fb_shard_plan_destroy(sp);
+    return rc;
+  }
+  *out = sp;
+  return FB_OK;
+}
+
+int fb_shard_plan_dims(const fb_shard_plan* sp, int64_t* l, int64_t* m) {
+  if (!sp) {
+    set_error("fb_shard_plan_dims: null plan");
+    return FB_ERR_ARG;
+  }
+  if (l) *l = sp->l;
+  if (m) *m = sp->m;
+  return FB_OK;
+}
+
+int fb_shard_columns(fb_shard_plan* sp, const void* in, void* out, int64_t C, int64_t tau0,
+                     int64_t lp, int inverse, void* stream) {
+  if (!sp || !in || !out) {
+    set_error("fb_shard_columns: null argument");
+    return FB_ERR_ARG;
+  }
+  const uint32_t TAU = (uint32_t)(kBigTile / sp->m);
+  if (C < 1 || lp < TAU || lp % TAU || tau0 < 0 || tau0 + lp > sp->l || C > 65535) {
+    set_error("fb_shard_columns: bad shard geometry (lp must be a multiple of 8192 / m)");
+    return FB_ERR_DIM;
+  }
+  int rc = cuda_status(cudaSetDevice(sp->device), "cudaSetDevice");
+  if (rc) return rc;
+  cudaStream_t s = (cudaStream_t)stream;
+  const size_t sm = padded_len(kBigTile) * sizeof(float2);
+  const dim3 g((unsigned)(lp / TAU), (unsigned)C);
+  const float scale = 1.0f / (float)sp->n;
+  with_small(sp->m, [&](auto sc) {
+    constexpr int SM = decltype(sc)::value;
+    if (inverse) {
+      auto k = tp_shard_cols_kernel<+1, SM>;
+      cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+      k<<<g, kBigThreads, sm, s>>>((const float2*)in, (float2*)out, sp->tw_m, sp->tw_big,
+                                   (uint32_t)sp->m, (uint32_t)lp, (uint32_t)tau0, scale);
+    } else {
+      auto k = tp_shard_cols_kernel<-1, SM>;
+      cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+      k<<<g, kBigThreads, sm, s>>>((const float2*)in, (float2*)out, sp->tw_m, sp->tw_big,
+                                   (uint32_t)sp->m, (uint32_t)lp, (uint32_t)tau0, scale);
+    }
+  });
+  return cuda_status(cudaGetLastError(), "fb_shard_columns");
+}
+
+int fb_shard_rows(fb_shard_plan* sp, void* rows, const void* kf2, void* kf2_out, int64_t C,
+                  int64_t mp, int mode, float scale, void* stream) {
+  if (!sp || !rows || (mode == 0 && !kf2) || (mode == 1 && !kf2_out)) {
+    set_error("fb_shard_rows: null argument");
+    return FB_ERR_ARG;
+  }
+  if (C < 1 || mp < 1 || C * mp > (int64_t)1 << 31) {
+    set_error("fb_shard_rows: bad shard geometry");
+    return FB_ERR_DIM;
+  }
+  int rc = cuda_status(cudaSetDevice(sp->device), "cudaSetDevice");
+  if (rc) return rc;
+  cudaStream_t s = (cudaStream_t)stream;
+  const size_t sm = pass2_smem<float>();
+  auto* x1 = reinterpret_cast<CxT<float>*>(rows);
+  if (mode == 0) {
+    auto k = tp_pass2_kernel<float, 0>;
+    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    k<<<dim3((unsigned)(C * mp), 1), kL / 16, sm, s>>>(x1, (const float2*)kf2, nullptr, sp->tw_l,
+                                                       1, (int)C, (int)mp, 1, 0.f);
+  } else {
+    auto k = tp_pass2_kernel<float, 1>;
+    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    k<<<dim3((unsigned)(C * mp), 1), kL / 16, sm, s>>>(x1, nullptr, (float2*)kf2_out, sp->tw_l,
+                                                       1, (int)C, (int)mp, 1, scale);
+  }
+  return cuda_status(cudaGetLastError(), "fb_shard_rows");
+}
+
+}  // extern "C"

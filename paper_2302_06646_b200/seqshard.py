@@ -70,7 +70,9 @@ def gather_tau(parts: list[torch.Tensor], shard: SeqShard) -> torch.Tensor:
     return v.reshape(*v.shape[:-2], shard.m * shard.l)
 
 
-def _a2a(x: torch.Tensor, group=None) -> torch.Tensor:
+def _a2a(x: torch.Tensor, group=None, world: int = 2) -> torch.Tensor:
+    if world == 1:  # one rank: the transpose moves nothing (no process group needed)
+        return x
     out = torch.empty_like(x)
     dist.all_to_all_single(out, x, group=group)
     return out
@@ -81,7 +83,7 @@ def columns_to_rows(x1: torch.Tensor, shard: SeqShard, group=None) -> torch.Tens
     C = x1.shape[0]
     P, mp, lp = shard.world, shard.mp, shard.lp
     send = x1.reshape(C, P, mp, lp).permute(1, 0, 2, 3).contiguous()  # [dest][C][mp][lp]
-    recv = _a2a(torch.view_as_real(send), group)                        # [src][C][mp][lp][2]
+    recv = _a2a(torch.view_as_real(send), group, P)                     # [src][C][mp][lp][2]
     recv = torch.view_as_complex(recv)
     return recv.permute(1, 2, 0, 3).reshape(C, mp, P * lp).contiguous()
 
@@ -91,7 +93,7 @@ def rows_to_columns(rows: torch.Tensor, shard: SeqShard, group=None) -> torch.Te
     C = rows.shape[0]
     P, mp, lp = shard.world, shard.mp, shard.lp
     send = rows.reshape(C, mp, P, lp).permute(2, 0, 1, 3).contiguous()  # [dest][C][mp][lp]
-    recv = torch.view_as_complex(_a2a(torch.view_as_real(send), group))  # [src][C][mp][lp]
+    recv = torch.view_as_complex(_a2a(torch.view_as_real(send), group, P))  # [src][C][mp][lp]
     return recv.permute(1, 0, 2, 3).reshape(C, P * mp, lp).contiguous()
 
 
@@ -111,6 +113,80 @@ def four_step_conv(x_cols: torch.Tensor, shard: SeqShard, passes: LocalPasses,
     rows = passes.pass2(rows, shard)
     w = rows_to_columns(rows, shard, group)
     return passes.pass3(w, shard)
+
+
+class GpuPasses:
+    """The three local passes on this rank's GPU with this package's kernels
+    (fb_shard_columns / fb_shard_rows in libflashbutterfly.so): complex64
+    [C, m, lp] column slices and [C, mp, l] row slices, l = 8192.  `kf2` holds
+    this rank's rows of the kernel spectrum, kf2[c][a - a0][s] = K_hat[a + m s]."""
+
+    def __init__(self, n: int, kf2: torch.Tensor | None = None, device=None):
+        import ctypes as C
+
+        from . import _lib
+
+        self._C, self._lib = C, _lib
+        dev = torch.device("cuda", torch.cuda.current_device()) if device is None else torch.device(device)
+        self.device, self.n = dev, int(n)
+        h = C.c_void_p()
+        with torch.cuda.device(dev):
+            _lib.check(_lib.lib().fb_shard_plan_create(C.byref(h), self.n, dev.index or 0))
+        self._h = h
+        l, m = C.c_int64(), C.c_int64()
+        _lib.check(_lib.lib().fb_shard_plan_dims(h, C.byref(l), C.byref(m)))
+        self.l, self.m = l.value, m.value
+        self.kf2 = kf2
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h is not None and h.value:
+            try:
+                self._lib.lib().fb_shard_plan_destroy(h)
+            except Exception:
+                pass
+            self._h = None
+
+    def _p(self, t):
+        return self._C.c_void_p(t.data_ptr()) if t is not None else self._C.c_void_p(0)
+
+    def _stream(self):
+        return self._C.c_void_p(torch.cuda.current_stream(self.device).cuda_stream)
+
+    def _cols(self, x: torch.Tensor, sh: SeqShard, inverse: int) -> torch.Tensor:
+        x = x.contiguous()
+        if x.dtype != torch.complex64 or tuple(x.shape[1:]) != (sh.m, sh.lp):
+            raise ValueError(f"expected complex64 [C, {sh.m}, {sh.lp}], got {x.dtype} {list(x.shape)}")
+        out = torch.empty_like(x)
+        self._lib.check(self._lib.lib().fb_shard_columns(self._h, self._p(x), self._p(out), x.shape[0],
+                                                         sh.tau0, sh.lp, inverse, self._stream()))
+        return out
+
+    def pass1(self, x_cols: torch.Tensor, sh: SeqShard) -> torch.Tensor:
+        return self._cols(x_cols, sh, 0)
+
+    def pass3(self, w_cols: torch.Tensor, sh: SeqShard) -> torch.Tensor:
+        return self._cols(w_cols, sh, 1)
+
+    def pass2(self, rows: torch.Tensor, sh: SeqShard) -> torch.Tensor:
+        rows = rows.contiguous()
+        kf2 = self.kf2.contiguous()
+        self._lib.check(self._lib.lib().fb_shard_rows(self._h, self._p(rows), self._p(kf2), None,
+                                                      rows.shape[0], sh.mp, 0, 1.0, self._stream()))
+        return rows
+
+    def spectrum_rows(self, kbar_cols: torch.Tensor, sh: SeqShard, group=None) -> torch.Tensor:
+        """This rank's kernel-spectrum rows from its real kernel columns
+        kbar_cols [C, m, lp] (float32; zero-padded causal kernels): pass 1,
+        the transpose, then the row FFTs — the sharded build_three_pass
+        (three_pass.cpp:197-203).  Sets and returns self.kf2."""
+        x = torch.complex(kbar_cols.float(), torch.zeros_like(kbar_cols, dtype=torch.float32))
+        rows = columns_to_rows(self.pass1(x, sh), sh, group)
+        kf2 = torch.empty_like(rows)
+        self._lib.check(self._lib.lib().fb_shard_rows(self._h, self._p(rows), None, self._p(kf2),
+                                                      rows.shape[0], sh.mp, 1, 1.0, self._stream()))
+        self.kf2 = kf2
+        return kf2
 
 
 def head_shard(H: int, world: int, rank: int) -> slice:

@@ -342,3 +342,32 @@ def test_tensor_core_saved_transform(lc, B, H):
     torch.cuda.synchronize()
     for k, v in (("y", y), ("du", du), ("dK", dK), ("dD", dD)):
         assert np.array_equal(to_np(v), want[k]), k
+
+
+# ------------------------------------------------------------ sequence-sharded four-step
+@pytest.mark.parametrize("m", [16, 64])
+def test_four_step_gpu_passes_single_rank(m):
+    """seqshard.four_step_conv with the GPU local passes (fb_shard_*) at one
+    rank (the exchange is the identity) against numpy's circular convolution;
+    the multi-rank exchange itself is covered by the gloo tests on CPU."""
+    from paper_2302_06646_b200 import seqshard as ss
+
+    l = 8192
+    n, Cn = l * m, 3
+    rng = np.random.default_rng(5)
+    x = (rng.standard_normal((Cn, n)) + 1j * rng.standard_normal((Cn, n))).astype(np.complex64)
+    k = np.zeros((Cn, n), np.float32)
+    k[:, : n // 2] = rng.standard_normal((Cn, n // 2)) * np.exp(-np.arange(n // 2) / 500.0)
+    want = np.fft.ifft(np.fft.fft(x.astype(np.complex128), axis=1) * np.fft.fft(k, axis=1), axis=1)
+    sh = ss.SeqShard(l=l, m=m, world=1, rank=0)
+    gp = ss.GpuPasses(n)
+    kcols = ss.scatter_tau(torch.from_numpy(k).cuda(), sh)
+    kf2 = gp.spectrum_rows(kcols, sh)
+    khat = np.fft.fft(k.astype(np.float64), axis=1)
+    s_idx, a_idx = np.arange(l), np.arange(m)
+    kf2_want = khat[:, a_idx[:, None] + m * s_idx[None, :]]
+    assert rel_l2(kf2.cpu().numpy(), kf2_want) < 1e-5
+    xc = ss.scatter_tau(torch.from_numpy(x).cuda(), sh)
+    y = ss.four_step_conv(xc, sh, gp)
+    got = ss.gather_tau([y.cpu()], sh).numpy()
+    assert rel_l2(got, want) < 1e-5
