@@ -19,6 +19,7 @@
 // walks all B rows of its head in order, so dblocks (summed over b) are
 // deterministic without atomics.
 #include <algorithm>
+#include <type_traits>
 #include <cmath>
 #include <vector>
 
@@ -362,6 +363,169 @@ __device__ __forceinline__ void lx_grad(const float2* __restrict__ w, const floa
   __syncthreads();
 }
 
+// ---------------------------------------------------------------- F = 16 stages on mma.sync
+// For the 16-bit modes the F = 16 stages (all but the last of config 4's
+// [16, 16, 4]) run on the tensor cores as real-stacked GEMMs with bf16
+// operands and fp32 accumulation: a column's update y = W x (16 x 16
+// complex) is [yr; yi] = [[Wr, -Wi]; [Wi, Wr]] [xr; xi], i.e. a 32 x 32 A
+// operand (kept in registers for the stage) against 8-column B tiles taken
+// from smem — four m16n8k16 MMAs per 8 columns instead of 1024 FFMAs per
+// column.  The block gradient G += sum_cols w conj(v) is the 32 x 32 product
+// [wr; wi] [vr; vi]^T over the columns (Gr = P00 + P11, Gi = P10 - P01),
+// reduced over warps in a fixed order.  (mma.sync rather than tcgen05: the
+// operands are a few KB per head and scattered by the butterfly's strides;
+// the instruction count, not tensor throughput, is what bounds this path.)
+__device__ __forceinline__ uint32_t pk_bf16(float lo, float hi) {
+  __nv_bfloat162 h = __floats2bfloat162_rn(lo, hi);
+  return *reinterpret_cast<uint32_t*>(&h);
+}
+__device__ __forceinline__ void mma_bf16_16816(float (&d)[4], const uint32_t (&a)[4], uint32_t b0,
+                                               uint32_t b1) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, "
+      "{%8,%9}, {%0,%1,%2,%3};"
+      : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+      : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+}
+
+// A fragments of [[Mr, -Mi]; [Mi, Mr]] with M(o, i) = (CONJT ? conj(W[i][o]) : W[o][i])
+template <bool CONJT>
+__device__ __forceinline__ void lx_afrag(uint32_t (&A)[2][2][4], const float2* __restrict__ W) {
+  const int lane = threadIdx.x & 31, g = lane >> 2, tig = lane & 3;
+  auto m = [&](int o, int i) {
+    const float2 w = CONJT ? W[i * 16 + o] : W[o * 16 + i];
+    return CONJT ? make_float2(w.x, -w.y) : w;
+  };
+  auto val = [&](int row, int col) {
+    const float2 w = m(row & 15, col & 15);
+    const bool rr = row < 16, rc = col < 16;
+    return rr ? (rc ? w.x : -w.y) : (rc ? w.y : w.x);
+  };
+#pragma unroll
+  for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+    for (int kt = 0; kt < 2; ++kt)
+#pragma unroll
+      for (int r = 0; r < 4; ++r) {
+        const int row = 16 * mt + g + (r & 1) * 8, col = 16 * kt + 2 * tig + (r >> 1) * 8;
+        A[mt][kt][r] = pk_bf16(val(row, col), val(row, col + 1));
+      }
+}
+
+// dst[col][o] = post(o, col) * sum_i M(o, i) src[col][i] over all columns, F = 16.
+// ADJ = false: M = W and post = the stage twiddle (forward);
+// ADJ = true:  M = W^H and post = conj of the lower stage's twiddle (plgL >= 0).
+template <bool ADJ>
+__device__ __forceinline__ void lx_stage_mma16(const float2* __restrict__ src, float2* __restrict__ dst,
+                                               const float2* __restrict__ W, int lgL, int lgn, int R,
+                                               const float2* __restrict__ tw, int plgL, int plgf) {
+  const int lgrest = lgL - 4, lgcpr = lgn - 4;
+  const int C = R << lgcpr;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, tig = lane & 3;
+  uint32_t A[2][2][4];
+  lx_afrag<ADJ>(A, W);
+  const int plgrest = plgL - plgf;
+  for (int nt = warp; nt * 8 < C; nt += kLxThreads / 32) {
+    const int base = lx_base(nt * 8 + g, lgcpr, lgrest, lgL, lgn);
+    const float2 x0 = src[base + ((2 * tig) << lgrest)], x1 = src[base + ((2 * tig + 1) << lgrest)];
+    const float2 x2 = src[base + ((2 * tig + 8) << lgrest)], x3 = src[base + ((2 * tig + 9) << lgrest)];
+    const uint32_t br0 = pk_bf16(x0.x, x1.x), br1 = pk_bf16(x2.x, x3.x);
+    const uint32_t bi0 = pk_bf16(x0.y, x1.y), bi1 = pk_bf16(x2.y, x3.y);
+    float d[2][4] = {{0.f, 0.f, 0.f, 0.f}, {0.f, 0.f, 0.f, 0.f}};
+#pragma unroll
+    for (int mt = 0; mt < 2; ++mt) {
+      mma_bf16_16816(d[mt], A[mt][0], br0, br1);
+      mma_bf16_16816(d[mt], A[mt][1], bi0, bi1);
+    }
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const int o = g + (e >> 1) * 8, cn = nt * 8 + 2 * tig + (e & 1);
+      const int ob = lx_base(cn, lgcpr, lgrest, lgL, lgn);
+      const int idx = ob + (o << lgrest);
+      float2 y = make_float2(d[0][e], d[1][e]);
+      if (!ADJ) {
+        const int q = cn & ((1 << lgrest) - 1);
+        y = cmul(y, tw[o * (q << (lgn - lgL))]);
+      } else if (plgL >= 0) {
+        const int loc = idx & ((1 << plgL) - 1);
+        const int pa = loc >> plgrest, pq = loc & ((1 << plgrest) - 1);
+        y = cmulc(y, tw[(pa * pq) << (lgn - plgL)]);
+      }
+      dst[idx] = y;
+    }
+  }
+}
+
+// G[a][p] += sum_cols w[a] conj(v[p]), F = 16; red: 8 x 256 float2 scratch
+__device__ __forceinline__ void lx_grad_mma16(const float2* __restrict__ w, const float2* __restrict__ v,
+                                              float2* __restrict__ G, float2* __restrict__ red,
+                                              int lgL, int lgn, int R) {
+  const int lgrest = lgL - 4, lgcpr = lgn - 4;
+  const int C = R << lgcpr;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, tig = lane & 3;
+  float d[2][4][4];
+#pragma unroll
+  for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+    for (int nt = 0; nt < 4; ++nt)
+#pragma unroll
+      for (int e = 0; e < 4; ++e) d[mt][nt][e] = 0.f;
+  // K chunks of 16 columns; thread's columns k = 2 tig, +1, +8, +9 of the chunk
+  for (int kc = warp; kc * 16 < C; kc += kLxThreads / 32) {
+    int cb[4];
+#pragma unroll
+    for (int r = 0; r < 4; ++r)
+      cb[r] = lx_base(kc * 16 + 2 * tig + (r & 1) + (r >> 1) * 8, lgcpr, lgrest, lgL, lgn);
+    // A = [wr; wi] rows a = g, g + 8; B = [vr; vi]^T columns p = g, g + 8
+    float2 wv[2][4], vv[2][4];
+#pragma unroll
+    for (int h8 = 0; h8 < 2; ++h8)
+#pragma unroll
+      for (int r = 0; r < 4; ++r) {
+        wv[h8][r] = w[cb[r] + ((g + 8 * h8) << lgrest)];
+        vv[h8][r] = v[cb[r] + ((g + 8 * h8) << lgrest)];
+      }
+    uint32_t a[2][4];  // [re/im][reg]: reg = (row g / g+8) x (k lo / hi)
+#pragma unroll
+    for (int part = 0; part < 2; ++part)
+#pragma unroll
+      for (int r = 0; r < 4; ++r) {
+        const int h8 = r & 1, kk = (r >> 1) * 2;  // k pair {kk, kk+1} of cb[]
+        const float2 p0 = wv[h8][kk], p1 = wv[h8][kk + 1];
+        a[part][r] = part ? pk_bf16(p0.y, p1.y) : pk_bf16(p0.x, p1.x);
+      }
+#pragma unroll
+    for (int nt = 0; nt < 4; ++nt) {
+      const int part = nt >> 1, h8 = nt & 1;  // columns p = 8 h8 + g of vr (part 0) / vi (1)
+      const float2 q0 = vv[h8][0], q1 = vv[h8][1], q2 = vv[h8][2], q3 = vv[h8][3];
+      const uint32_t b0 = part ? pk_bf16(q0.y, q1.y) : pk_bf16(q0.x, q1.x);
+      const uint32_t b1 = part ? pk_bf16(q2.y, q3.y) : pk_bf16(q2.x, q3.x);
+#pragma unroll
+      for (int mt = 0; mt < 2; ++mt) mma_bf16_16816(d[mt][nt], a[mt], b0, b1);
+    }
+  }
+  // this warp's partial: rows a, columns p of each block
+#pragma unroll
+  for (int h8 = 0; h8 < 2; ++h8)
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const int aa = g + (e >> 1) * 8, pp = 8 * h8 + 2 * tig + (e & 1);
+      const float gr = d[0][h8][e] + d[1][2 + h8][e];   // wr vr + wi vi
+      const float gi = d[1][h8][e] - d[0][2 + h8][e];   // wi vr - wr vi
+      red[warp * 256 + aa * 16 + pp] = make_float2(gr, gi);
+    }
+  __syncthreads();
+  for (int e = threadIdx.x; e < 256; e += kLxThreads) {
+    float2 s = G[e];
+    for (int wq = 0; wq < kLxThreads / 32; ++wq) s = cadd(s, red[wq * 256 + e]);
+    G[e] = s;
+  }
+  __syncthreads();
+}
+
+template <typename IO>
+constexpr bool kTc = !std::is_same<IO, float>::value;  // 16-bit modes: F = 16 stages on mma.sync
+
 #define LX_DISPATCH(lgf, CALL)        \
   switch (lgf) {                      \
     case 1: { constexpr int F = 2; CALL; } break;  \
@@ -393,7 +557,10 @@ __global__ void __launch_bounds__(kLxThreads)
   __syncthreads();
   float2 *s = bufA, *d = bufB;
   for (int k = 0; k < geo.nst; ++k) {
-    LX_DISPATCH(geo.lgf[k], (lx_fwd_stage<F>(s, d, W + geo.off[k], geo.lgL[k], geo.lgn, R, tw)));
+    if (kTc<IO> && geo.lgf[k] == 4)
+      lx_stage_mma16<false>(s, d, W + geo.off[k], geo.lgL[k], geo.lgn, R, tw, -1, 0);
+    else
+      LX_DISPATCH(geo.lgf[k], (lx_fwd_stage<F>(s, d, W + geo.off[k], geo.lgL[k], geo.lgn, R, tw)));
     __syncthreads();
     float2* tmp = s;
     s = d;
@@ -456,6 +623,10 @@ __global__ void __launch_bounds__(kLxThreads)
     }
     __syncthreads();
     for (int k = 0; k + 1 < S; ++k) {
+      if (kTc<IO> && geo.lgf[k] == 4)
+        lx_stage_mma16<false>(v + (size_t)k * R * n, v + (size_t)(k + 1) * R * n, W + geo.off[k],
+                              geo.lgL[k], geo.lgn, R, tw, -1, 0);
+      else
       LX_DISPATCH(geo.lgf[k], (lx_fwd_stage<F>(v + (size_t)k * R * n, v + (size_t)(k + 1) * R * n,
                                                W + geo.off[k], geo.lgL[k], geo.lgn, R, tw)));
       __syncthreads();
@@ -463,9 +634,15 @@ __global__ void __launch_bounds__(kLxThreads)
     for (int k = S - 1; k >= 0; --k) {
       // gb is free until the adjoint pass: it holds the gradient pass's
       // per-warp partials (R n >= 8 f^2 is a condition of the fast path)
+      if (kTc<IO> && geo.lgf[k] == 4)
+        lx_grad_mma16(ga, v + (size_t)k * R * n, G + geo.off[k], gb, geo.lgL[k], geo.lgn, R);
+      else
       LX_DISPATCH(geo.lgf[k], (lx_grad<F>(ga, v + (size_t)k * R * n, G + geo.off[k], gb, geo.lgL[k],
                                           geo.lgn, R)));
       const int plgL = k > 0 ? geo.lgL[k - 1] : -1, plgf = k > 0 ? geo.lgf[k - 1] : 0;
+      if (kTc<IO> && geo.lgf[k] == 4)
+        lx_stage_mma16<true>(ga, gb, W + geo.off[k], geo.lgL[k], geo.lgn, R, tw, plgL, plgf);
+      else
       LX_DISPATCH(geo.lgf[k], (lx_adj_stage<F>(ga, gb, WT + geo.off[k], geo.lgL[k], geo.lgn, R, tw,
                                                plgL, plgf)));
       __syncthreads();
