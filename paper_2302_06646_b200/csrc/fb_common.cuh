@@ -45,6 +45,22 @@ __device__ __forceinline__ float2 ldc<__half>(const __half* p) {
   return __half22float2(__ldg(reinterpret_cast<const __half2*>(p)));
 }
 
+// Same from shared (or any generic) memory: a plain load (__ldg is global-only).
+template <typename T>
+__device__ __forceinline__ float2 ldc_any(const T* p);
+template <>
+__device__ __forceinline__ float2 ldc_any<float>(const float* p) {
+  return *reinterpret_cast<const float2*>(p);
+}
+template <>
+__device__ __forceinline__ float2 ldc_any<__nv_bfloat16>(const __nv_bfloat16* p) {
+  return __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(p));
+}
+template <>
+__device__ __forceinline__ float2 ldc_any<__half>(const __half* p) {
+  return __half22float2(*reinterpret_cast<const __half2*>(p));
+}
+
 template <typename T>
 __device__ __forceinline__ void stc(T* p, float2 v);
 template <>

@@ -225,6 +225,23 @@ __device__ __forceinline__ int lx_base(int col, int lgcpr, int lgrest, int lgL, 
   return (r << lgn) + ((cc >> lgrest) << lgL) + (cc & ((1 << lgrest) - 1));
 }
 
+// 16-byte asynchronous global -> shared copies (LDGSTS): every load of a
+// phase is in flight at once instead of one dependent round trip per element
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(
+                   static_cast<uint32_t>(__cvta_generic_to_shared(smem))),
+               "l"(static_cast<uint64_t>(__cvta_generic_to_global(gmem)))
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() {
+  asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;" ::: "memory");
+}
+// bytes (multiple of 16, 16-byte aligned both sides) with the whole CTA
+__device__ __forceinline__ void cp_async_bytes(void* dst, const void* src, size_t bytes) {
+  for (size_t i = threadIdx.x; i < bytes / 16; i += kLxThreads)
+    cp_async16(static_cast<char*>(dst) + 16 * i, static_cast<const char*>(src) + 16 * i);
+}
+
 template <int F>
 __device__ __forceinline__ void lx_fwd_stage(const float2* __restrict__ src, float2* __restrict__ dst,
                                              const float2* __restrict__ W, int lgL, int lgn, int R,
@@ -547,12 +564,19 @@ __global__ void __launch_bounds__(kLxThreads)
   float2* bufB = bufA + (size_t)R * n;
   const int h = blockIdx.x;
   const float2* wg = reinterpret_cast<const float2*>(blocks) + (size_t)h * P;
-  for (int i = threadIdx.x; i < P; i += kLxThreads) W[i] = wg[i];
-  for (int i = threadIdx.x; i < n; i += kLxThreads) tw[i] = __ldg(tw_g + i);
   const int b0 = blockIdx.y * R, rows = min(R, B - b0);
+  // blocks, twiddles and the raw rows (staged in bufB) all in flight at once
+  IO* raw = reinterpret_cast<IO*>(bufB);
+  cp_async_bytes(W, wg, (size_t)P * sizeof(float2));
+  cp_async_bytes(tw, tw_g, (size_t)n * sizeof(float2));
+  for (int r = 0; r < rows; ++r)
+    cp_async_bytes(raw + (size_t)r * 2 * n, x + ((size_t)(b0 + r) * H + h) * 2 * n,
+                   2 * (size_t)n * sizeof(IO));
+  cp_async_wait_all();
+  __syncthreads();
   for (int i = threadIdx.x; i < R * n; i += kLxThreads) {
-    const int r = i >> geo.lgn, e = i & (n - 1);
-    bufA[i] = r < rows ? ldc<IO>(x + ((size_t)(b0 + r) * H + h) * 2 * n + 2 * e) : make_float2(0.f, 0.f);
+    const int r = i >> geo.lgn;
+    bufA[i] = r < rows ? ldc_any<IO>(raw + 2 * (size_t)i) : make_float2(0.f, 0.f);
   }
   __syncthreads();
   float2 *s = bufA, *d = bufB;
@@ -592,36 +616,45 @@ __global__ void __launch_bounds__(kLxThreads)
   float2* gb = ga + (size_t)R * n;
   const int h = blockIdx.x;
   const float2* wg = reinterpret_cast<const float2*>(blocks) + (size_t)h * P;
-  for (int i = threadIdx.x; i < P; i += kLxThreads) {
-    W[i] = wg[i];
-    G[i] = make_float2(0.f, 0.f);
-  }
+  cp_async_bytes(W, wg, (size_t)P * sizeof(float2));
+  cp_async_bytes(tw, tw_g, (size_t)n * sizeof(float2));
+  cp_async_wait_all();
+  __syncthreads();
+  for (int i = threadIdx.x; i < P; i += kLxThreads) G[i] = make_float2(0.f, 0.f);
   for (int k = 0; k < S; ++k) {
     const int f = 1 << geo.lgf[k], o = geo.off[k];
-    for (int i = threadIdx.x; i < f * f; i += kLxThreads) WT[o + (i % f) * f + i / f] = wg[o + i];
+    for (int i = threadIdx.x; i < f * f; i += kLxThreads) WT[o + (i % f) * f + i / f] = W[o + i];
   }
-  for (int i = threadIdx.x; i < n; i += kLxThreads) tw[i] = __ldg(tw_g + i);
   const int lgLt = geo.lgL[S - 1], lgft = geo.lgf[S - 1];
   const int b_end = min(B, (blockIdx.y + 1) * rps);
   for (int b0 = blockIdx.y * rps; b0 < b_end; b0 += R) {
     const int rows = min(R, b_end - b0);
     __syncthreads();
-    for (int i = threadIdx.x; i < R * n; i += kLxThreads) {
-      const int r = i >> geo.lgn, e = i & (n - 1);
-      float2 xv = make_float2(0.f, 0.f), gv = make_float2(0.f, 0.f);
-      if (r < rows) {
-        const size_t row = ((size_t)(b0 + r) * H + h) * 2 * n;
-        xv = ldc<IO>(x + row + 2 * e);
-        gv = ldc<IO>(g + row + 2 * e);
+    // raw rows staged in gb (free until the first adjoint pass), all loads of
+    // a phase in flight at once: x -> v[0], then g -> ga (permuted + twiddled)
+    IO* raw = reinterpret_cast<IO*>(gb);
+    for (int phase = 0; phase < 2; ++phase) {
+      const IO* src = phase ? g : x;
+      for (int r = 0; r < rows; ++r)
+        cp_async_bytes(raw + (size_t)r * 2 * n, src + ((size_t)(b0 + r) * H + h) * 2 * n,
+                       2 * (size_t)n * sizeof(IO));
+      cp_async_wait_all();
+      __syncthreads();
+      for (int i = threadIdx.x; i < R * n; i += kLxThreads) {
+        const int r = i >> geo.lgn, e = i & (n - 1);
+        const float2 val = r < rows ? ldc_any<IO>(raw + 2 * (size_t)i) : make_float2(0.f, 0.f);
+        if (phase == 0) {
+          v[i] = val;
+        } else {
+          // adjoint of the output permutation, then the top stage's conj twiddle
+          const int idx = __ldg(omap + e);
+          const int loc = idx & ((1 << lgLt) - 1), lgr = lgLt - lgft;
+          const int pa = loc >> lgr, pq = loc & ((1 << lgr) - 1);
+          ga[(r << geo.lgn) + idx] = cmulc(val, tw[(pa * pq) << (geo.lgn - lgLt)]);
+        }
       }
-      v[i] = xv;
-      // adjoint of the output permutation, then the top stage's conj twiddle
-      const int idx = __ldg(omap + e);
-      const int loc = idx & ((1 << lgLt) - 1), lgr = lgLt - lgft;
-      const int pa = loc >> lgr, pq = loc & ((1 << lgr) - 1);
-      ga[(r << geo.lgn) + idx] = cmulc(gv, tw[(pa * pq) << (geo.lgn - lgLt)]);
+      __syncthreads();
     }
-    __syncthreads();
     for (int k = 0; k + 1 < S; ++k) {
       if (kTc<IO> && geo.lgf[k] == 4)
         lx_stage_mma16<false>(v + (size_t)k * R * n, v + (size_t)(k + 1) * R * n, W + geo.off[k],
@@ -917,8 +950,10 @@ int fb_learned_fwd(fb_learned_plan* p, const float* blocks, const void* x, void*
   fb_learned_ext* ext = ext_of(p);
   cudaStream_t s = (cudaStream_t)stream;
   if (ext->dev.fast) {
-    const int R = lx_rows(lx_fwd_fixed(p), 2 * p->n * sizeof(float2), 113 * 1024) > 0
-                      ? lx_rows(lx_fwd_fixed(p), 2 * p->n * sizeof(float2), 113 * 1024)
+    // small CTAs (four per SM): the stage chain is latency-bound, so more
+    // independent CTAs per SM beat wider ones
+    const int R = lx_rows(lx_fwd_fixed(p), 2 * p->n * sizeof(float2), 56 * 1024) > 0
+                      ? lx_rows(lx_fwd_fixed(p), 2 * p->n * sizeof(float2), 56 * 1024)
                       : lx_rows(lx_fwd_fixed(p), 2 * p->n * sizeof(float2), 227 * 1024);
     if (R > 0) {
       const size_t sm = lx_fwd_fixed(p) + 2 * (size_t)R * p->n * sizeof(float2);
