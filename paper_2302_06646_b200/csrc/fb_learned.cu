@@ -454,21 +454,29 @@ __device__ __forceinline__ void lx_stage_mma16(const float2* __restrict__ src, f
       mma_bf16_16816(d[mt], A[mt][0], br0, br1);
       mma_bf16_16816(d[mt], A[mt][1], bi0, bi1);
     }
+    // all four twiddles loaded before any store (smem loads and stores
+    // would otherwise serialise through possible aliasing)
+    int idx[4];
+    float2 t[4];
 #pragma unroll
     for (int e = 0; e < 4; ++e) {
       const int o = g + (e >> 1) * 8, cn = nt * 8 + 2 * tig + (e & 1);
-      const int ob = lx_base(cn, lgcpr, lgrest, lgL, lgn);
-      const int idx = ob + (o << lgrest);
-      float2 y = make_float2(d[0][e], d[1][e]);
+      idx[e] = lx_base(cn, lgcpr, lgrest, lgL, lgn) + (o << lgrest);
       if (!ADJ) {
         const int q = cn & ((1 << lgrest) - 1);
-        y = cmul(y, tw[o * (q << (lgn - lgL))]);
+        t[e] = tw[o * (q << (lgn - lgL))];
       } else if (plgL >= 0) {
-        const int loc = idx & ((1 << plgL) - 1);
+        const int loc = idx[e] & ((1 << plgL) - 1);
         const int pa = loc >> plgrest, pq = loc & ((1 << plgrest) - 1);
-        y = cmulc(y, tw[(pa * pq) << (lgn - plgL)]);
+        t[e] = tw[(pa * pq) << (lgn - plgL)];
+      } else {
+        t[e] = make_float2(1.f, 0.f);
       }
-      dst[idx] = y;
+    }
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const float2 y = make_float2(d[0][e], d[1][e]);
+      dst[idx[e]] = ADJ ? cmulc(y, t[e]) : cmul(y, t[e]);
     }
   }
 }
