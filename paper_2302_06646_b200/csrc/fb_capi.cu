@@ -265,26 +265,32 @@ int fb_fwd(fb_plan* p, const void* u, void* y, int64_t B, void* ws, void* stream
 }
 
 size_t fb_saved_size(const fb_plan* p, int64_t B) {
-  if (!p || B < 1 || !p->use_tc) return 0;
-  return tc_saved_size(p, B);
+  if (!p || B < 1) return 0;
+  if (p->use_tc) return tc_saved_size(p, B);
+  if (p->engine == FB_ENGINE_THREE && !p->periodic) return tp_saved_size(p, B);
+  return 0;
 }
 
 int fb_fwd_save(fb_plan* p, const void* u, void* y, void* saved, int64_t B, void* ws,
                 void* stream) {
-  if (!saved || !p || !p->use_tc) return fb_fwd(p, u, y, B, ws, stream);
+  if (!saved || !p || !fb_saved_size(p, B)) return fb_fwd(p, u, y, B, ws, stream);
   int rc = check_run(p, B, "fb_fwd_save");
   if (rc) return rc;
   if (!u || !y) return fail(FB_ERR_ARG, "fb_fwd_save: null tensor");
-  return tc_fwd(p, u, y, B, (cudaStream_t)stream, saved);
+  if (p->use_tc) return tc_fwd(p, u, y, B, (cudaStream_t)stream, saved);
+  if (!ws) return fail(FB_ERR_ARG, "fb_fwd_save: workspace required");
+  return tp_fwd(p, u, y, B, ws, (cudaStream_t)stream, saved);
 }
 
 int fb_bwd_saved(fb_plan* p, const void* dy, const void* u, const void* saved, void* du,
                  float* dK, float* dKbar, float* dD, int64_t B, void* ws, void* stream) {
-  if (!saved || !p || !p->use_tc) return fb_bwd(p, dy, u, du, dK, dKbar, dD, B, ws, stream);
+  if (!saved || !p || !fb_saved_size(p, B))
+    return fb_bwd(p, dy, u, du, dK, dKbar, dD, B, ws, stream);
   int rc = check_run(p, B, "fb_bwd_saved");
   if (rc) return rc;
   if (!dy || !du || !dK || !dD || !ws) return fail(FB_ERR_ARG, "fb_bwd_saved: null argument");
-  return tc_bwd(p, dy, u, du, dK, dKbar, dD, B, ws, (cudaStream_t)stream, saved);
+  if (p->use_tc) return tc_bwd(p, dy, u, du, dK, dKbar, dD, B, ws, (cudaStream_t)stream, saved);
+  return tp_bwd(p, dy, u, du, dK, dKbar, dD, B, ws, (cudaStream_t)stream, saved);
 }
 
 int fb_bwd(fb_plan* p, const void* dy, const void* u, void* du, float* dK, float* dKbar,

@@ -83,10 +83,14 @@ int tc_bwd(fb_plan* p, const void* dy, const void* u, void* du, float* dK, float
 
 // three-pass (fb_three.cu)
 int tp_prep(fb_plan* p, const float* K, cudaStream_t s);
-int tp_fwd(fb_plan* p, const void* u, void* y, int64_t B, void* ws, cudaStream_t s);
+// usave: the forward keeps its pass-2 row spectra of u (tp_saved_size bytes) and the
+// backward reads them instead of transforming u (u may then be null)
+size_t tp_saved_size(const fb_plan* p, int64_t B);
+int tp_fwd(fb_plan* p, const void* u, void* y, int64_t B, void* ws, cudaStream_t s,
+           void* usave = nullptr);
 size_t tp_workspace(const fb_plan* p, int64_t B);
 int tp_bwd(fb_plan* p, const void* dy, const void* u, void* du, float* dK, float* dKbar, float* dD,
-           int64_t B, void* ws, cudaStream_t s);
+           int64_t B, void* ws, cudaStream_t s, const void* usave = nullptr);
 
 // shared K1 pieces (fb_prep.cu)
 int regularize_bank_dev(fb_plan* p, const float* K, cudaStream_t s);

@@ -134,7 +134,7 @@ template <typename ST, int MODE>
 __global__ void __launch_bounds__(kL / 16, 1)
     tp_pass2_kernel(CxT<ST>* __restrict__ x1, const float2* __restrict__ kf2,
                     float2* kf2_out, const float2* __restrict__ tab_g, int npairs,
-                    int H, int m, int ppc, float inv_n) {
+                    int H, int m, int ppc, float inv_n, CxT<ST>* __restrict__ usave = nullptr) {
   using S = FftShape<kL2>;
   extern __shared__ __align__(128) unsigned char smem_raw[];
   __shared__ __align__(8) uint64_t bars[2];
@@ -182,6 +182,11 @@ __global__ void __launch_bounds__(kL / 16, 1)
 #pragma unroll
       for (int r = 0; r < 16; ++r) out[j + r * S::stride] = cscale(v[r], inv_n);
     } else {
+      if (usave) {  // the row spectrum, kept for the backward (training step)
+        CxT<ST>* us = usave + ((size_t)pr * H + h) * (size_t)m * kL + (size_t)a * kL;
+#pragma unroll
+        for (int r = 0; r < 16; ++r) stc<ST>(&us[j + r * S::stride].x, v[r]);
+      }
 #pragma unroll
       for (int r = 0; r < 16; ++r)
         v[r] = cmul(v[r], KF_SMEM ? kfs[j + r * S::stride] : __ldg(kfg + j + r * S::stride));
@@ -203,7 +208,9 @@ __global__ void __launch_bounds__(kL / 16, 1)
 // a is complete in one CTA, fixed order => deterministic):
 //   DY = FFT(X1dy), U = FFT(X1u); acc += conj(U) DY; X1dy <- IFFT(DY conj(Kf2))
 //   finally wdk[h][a] = IFFT(acc)  (fp32)
-template <typename ST>
+// SAVED: x1u holds the forward's row spectra FFT_l(X1u row) (tp_pass2_kernel
+// usave) instead of the rows, so each pair costs two transforms, not three.
+template <typename ST, bool SAVED = false>
 __global__ void __launch_bounds__(kL / 16, 1)
     tp_pass2_bwd_kernel(CxT<ST>* __restrict__ x1dy, const CxT<ST>* __restrict__ x1u,
                         const float2* __restrict__ kf2, float2* __restrict__ wdk,
@@ -238,23 +245,33 @@ __global__ void __launch_bounds__(kL / 16, 1)
 #pragma unroll
     for (int r = 0; r < 16; ++r) v[r] = cx_load(stage + j + r * S::stride);
     __syncthreads();  // stage consumed
-    stage_row<ST>(stage, rp(x1u, pr), &bars[0]);
+    if constexpr (SAVED) {
+      if (pr + 1 < npairs) stage_row<ST>(stage, rp(x1dy, pr + 1), &bars[0]);
+    } else {
+      stage_row<ST>(stage, rp(x1u, pr), &bars[0]);
+    }
     dft_reg<-1, 16>(v);
     bfly_store<16, 1>(work, v, j);
     __syncthreads();
     mid_passes<-1, kL2, 16>(work, tab);
     bfly_load<-1, 16, S::n / 16, kL2>(work, tab, gv, j);
-    ptx::mbar_wait(&bars[0], phase);
-    phase ^= 1;
+    if constexpr (SAVED) {
+      const CxT<ST>* us = rp(x1u, pr);
 #pragma unroll
-    for (int r = 0; r < 16; ++r) v[r] = cx_load(stage + j + r * S::stride);
-    dft_reg<-1, 16>(v);
-    __syncthreads();
-    if (pr + 1 < npairs) stage_row<ST>(stage, rp(x1dy, pr + 1), &bars[0]);
-    bfly_store<16, 1>(work, v, j);
-    __syncthreads();
-    mid_passes<-1, kL2, 16>(work, tab);
-    bfly_load<-1, 16, S::n / 16, kL2>(work, tab, v, j);
+      for (int r = 0; r < 16; ++r) v[r] = cx_load(us + j + r * S::stride);
+    } else {
+      ptx::mbar_wait(&bars[0], phase);
+      phase ^= 1;
+#pragma unroll
+      for (int r = 0; r < 16; ++r) v[r] = cx_load(stage + j + r * S::stride);
+      dft_reg<-1, 16>(v);
+      __syncthreads();
+      if (pr + 1 < npairs) stage_row<ST>(stage, rp(x1dy, pr + 1), &bars[0]);
+      bfly_store<16, 1>(work, v, j);
+      __syncthreads();
+      mid_passes<-1, kL2, 16>(work, tab);
+      bfly_load<-1, 16, S::n / 16, kL2>(work, tab, v, j);
+    }
 #pragma unroll
     for (int r = 0; r < 16; ++r) {
       const uint32_t e = j + r * S::stride;
@@ -1166,7 +1183,7 @@ int tp_prep(fb_plan* p, const float* K, cudaStream_t s) {
   cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
   k<<<dim3((unsigned)(p->H * p->m), 1), kL / 16, sm, s>>>(x1k, nullptr, p->kf, p->tw_l, 1,
                                                           (int)p->H, (int)p->m, 1,
-                                                          1.0f / (float)p->n);
+                                                          1.0f / (float)p->n, nullptr);
   return cuda_status(cudaGetLastError(), "tp_prep");
 }
 
@@ -1179,7 +1196,15 @@ size_t tp_workspace(const fb_plan* p, int64_t B) {
   return bytes + 256;
 }
 
-int tp_fwd(fb_plan* p, const void* u, void* y, int64_t B, void* ws, cudaStream_t s) {
+size_t tp_saved_size(const fb_plan* p, int64_t B) { return inter_bytes(p, (B + 1) / 2); }
+
+__global__ void tp_dd_lag0_kernel(const float* __restrict__ dkbar, float* __restrict__ dD, int H,
+                                  int64_t N) {
+  const int h = blockIdx.x * blockDim.x + threadIdx.x;
+  if (h < H) dD[h] = dkbar[(size_t)h * N];  // dD = sum_t dy u = dKbar[0] (lag 0)
+}
+
+int tp_fwd(fb_plan* p, const void* u, void* y, int64_t B, void* ws, cudaStream_t s, void* usave) {
   const int64_t npairs = (B + 1) / 2;
   if (p->periodic) {
     set_error("three-pass: circular mode needs N == n");
@@ -1196,14 +1221,15 @@ int tp_fwd(fb_plan* p, const void* u, void* y, int64_t B, void* ws, cudaStream_t
     const int chunks = pass2_chunks(p, npairs);
     const int ppc = (int)((npairs + chunks - 1) / chunks);
     k2<<<dim3((unsigned)(p->H * p->m), (unsigned)chunks), kL / 16, sm, s>>>(
-        x1, p->kf, nullptr, p->tw_l, (int)npairs, (int)p->H, (int)p->m, ppc, 0.f);
+        x1, p->kf, nullptr, p->tw_l, (int)npairs, (int)p->H, (int)p->m, ppc, 0.f,
+        reinterpret_cast<CxT<ST>*>(usave));
     launch_pass3<ST, IO, 0>(p, x1, (const IO*)u, (IO*)y, nullptr, (int)B, (int)npairs, 1.f, s);
   });
   return cuda_status(cudaGetLastError(), "tp_fwd");
 }
 
 int tp_bwd(fb_plan* p, const void* dy, const void* u, void* du, float* dK, float* dKbar, float* dD,
-           int64_t B, void* ws, cudaStream_t s) {
+           int64_t B, void* ws, cudaStream_t s, const void* usave) {
   const int64_t npairs = (B + 1) / 2;
   if (p->periodic) {
     set_error("three-pass: circular mode needs N == n");
@@ -1225,18 +1251,31 @@ int tp_bwd(fb_plan* p, const void* dy, const void* u, void* du, float* dK, float
     using ST = IO;
     auto* x1dy = reinterpret_cast<CxT<ST>*>(x1dy_raw);
     auto* x1u = reinterpret_cast<CxT<ST>*>(x1u_raw);
-    gx = launch_pass1<IO, ST, 1>(p, (const IO*)dy, (const IO*)u, x1dy, x1u, ddpart, (int)B,
-                                 (int)npairs, s);
     const size_t sm = pass2_bwd_smem<ST>();
-    auto k2 = tp_pass2_bwd_kernel<ST>;
-    cudaFuncSetAttribute(k2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-    k2<<<(unsigned)(p->H * p->m), kL / 16, sm, s>>>(x1dy, x1u, p->kf, wdk, p->tw_l, (int)npairs,
-                                                     (int)p->H, (int)p->m);
+    if (usave) {  // the forward's row spectra of u: pass 1 and 2 on dy only
+      launch_pass1<IO, ST, 0>(p, (const IO*)dy, nullptr, x1dy, nullptr, nullptr, (int)B,
+                              (int)npairs, s);
+      auto k2 = tp_pass2_bwd_kernel<ST, true>;
+      cudaFuncSetAttribute(k2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+      k2<<<(unsigned)(p->H * p->m), kL / 16, sm, s>>>(
+          x1dy, reinterpret_cast<const CxT<ST>*>(usave), p->kf, wdk, p->tw_l, (int)npairs,
+          (int)p->H, (int)p->m);
+    } else {
+      gx = launch_pass1<IO, ST, 1>(p, (const IO*)dy, (const IO*)u, x1dy, x1u, ddpart, (int)B,
+                                   (int)npairs, s);
+      auto k2 = tp_pass2_bwd_kernel<ST, false>;
+      cudaFuncSetAttribute(k2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+      k2<<<(unsigned)(p->H * p->m), kL / 16, sm, s>>>(x1dy, x1u, p->kf, wdk, p->tw_l, (int)npairs,
+                                                       (int)p->H, (int)p->m);
+    }
     launch_pass3<ST, IO, 0>(p, x1dy, (const IO*)dy, (IO*)du, nullptr, (int)B, (int)npairs, 1.f, s);
     launch_pass3<float, float, 1>(p, reinterpret_cast<const CxT<float>*>(wdk), nullptr, nullptr,
                                   dkbar, 2, 1, 1.0f / (float)p->n, s);
   });
-  tp_dd_reduce_kernel<<<(unsigned)p->H, 32, 0, s>>>(ddpart, dD, (int)(npairs * gx));
+  if (usave)
+    tp_dd_lag0_kernel<<<(unsigned)((p->H + 127) / 128), 128, 0, s>>>(dkbar, dD, (int)p->H, p->N);
+  else
+    tp_dd_reduce_kernel<<<(unsigned)p->H, 32, 0, s>>>(ddpart, dD, (int)(npairs * gx));
   int rc = cuda_status(cudaGetLastError(), "tp_bwd");
   if (rc) return rc;
   return regularizer_backward_dev(p, dkbar, dK, s);
@@ -1359,12 +1398,12 @@ int fb_shard_rows(fb_shard_plan* sp, void* rows, const void* kf2, void* kf2_out,
     auto k = tp_pass2_kernel<float, 0>;
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     k<<<dim3((unsigned)(C * mp), 1), kL / 16, sm, s>>>(x1, (const float2*)kf2, nullptr, sp->tw_l,
-                                                       1, (int)C, (int)mp, 1, 0.f);
+                                                       1, (int)C, (int)mp, 1, 0.f, nullptr);
   } else {
     auto k = tp_pass2_kernel<float, 1>;
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     k<<<dim3((unsigned)(C * mp), 1), kL / 16, sm, s>>>(x1, nullptr, (float2*)kf2_out, sp->tw_l,
-                                                       1, (int)C, (int)mp, 1, scale);
+                                                       1, (int)C, (int)mp, 1, scale, nullptr);
   }
   return cuda_status(cudaGetLastError(), "fb_shard_rows");
 }

@@ -371,3 +371,24 @@ def test_four_step_gpu_passes_single_rank(m):
     y = ss.four_step_conv(xc, sh, gp)
     got = ss.gather_tau([y.cpu()], sh).numpy()
     assert rel_l2(got, want) < 1e-5
+
+
+@pytest.mark.parametrize("dtype,N", [(torch.float32, 16384), (torch.bfloat16, 32768)])
+def test_three_pass_saved_transform(lc, dtype, N):
+    """Three-pass training step: the forward keeps its pass-2 row spectra of u
+    and the backward runs passes 1/2 on dy only (dD from the lag-0 dKbar).
+    y and du are bit-identical to the recompute path; dK and dD match the
+    oracle at the mode's bar."""
+    B, H = 3, 2
+    inp = layer_inputs(lc, B, H, N, dtype)
+    cfg = fb.RegularizationConfig(**CFG)
+    plan, want = run_layer(inp, N, H, dtype, cfg, engine=2)
+    assert plan.saved_size(B) > 0
+    y, saved = plan.forward(inp["tu"], save=True)
+    du, dK, dD = plan.backward(inp["tdy"], None, saved=saved)
+    torch.cuda.synchronize()
+    assert np.array_equal(to_np(y), want["y"])
+    assert np.array_equal(to_np(du), want["du"])
+    ref = oracle_layer(lc, inp, cfg)
+    assert_parity(dict(y=to_np(y), du=to_np(du), dK=to_np(dK), dD=to_np(dD)), ref, TOL[dtype],
+                  keys=("y", "du", "dK", "dD"))
