@@ -66,8 +66,6 @@ constexpr uint32_t SOP = SIN + 2 * 16384;
 constexpr uint32_t SMAT = SOP + 2 * 32768;
 constexpr uint32_t MAT_FA = 0, MAT_FR = 16384, MAT_FI = 49152, MAT_BYTES = 81920;
 constexpr uint32_t STAB = SMAT + MAT_BYTES;
-constexpr uint32_t SKF = STAB + 2048;
-constexpr uint32_t SMEM_BWD = SKF + 32768;
 // Forward layout: three 16 KB operand planes per slot so each stage-B/B'
 // K-step is two N = 128 MMAs (a 2-plane window of [Xr | Xi] or [-Xi | Xr]
 // against Fr / Fi) instead of four N = 64 ones — 61 % vs 46 % of the tensor

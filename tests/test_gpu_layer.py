@@ -304,13 +304,15 @@ def test_config3_heads_sample(lc):
 
 
 # ------------------------------------------------------------ host-buffer runner
-@pytest.mark.parametrize("dtype,H,hc,training", [(torch.bfloat16, 12, 4, False),
-                                                 (torch.float32, 6, 2, True)])
-def test_host_runner_matches_device_path(lc, dtype, H, hc, training):
+@pytest.mark.parametrize("dtype,H,hc,training,N", [(torch.bfloat16, 12, 4, False, 4096),
+                                                   (torch.float32, 6, 2, True, 4096),
+                                                   (torch.bfloat16, 4, 2, False, 16384)])
+def test_host_runner_matches_device_path(lc, dtype, H, hc, training, N):
     """fb_host_runner (pinned host buffers, heads in pipelined chunks) gives
     the device path's results: y / du per channel bit-identical, dK / dD up to
-    the fixed-order partial grouping; dropout streams follow the global head."""
-    B, N = 5, 4096
+    the fixed-order partial grouping and the saved-transform rounding (three-
+    pass); dropout streams follow the global head."""
+    B = 5
     inp = layer_inputs(lc, B, H, N, dtype)
     cfg = fb.RegularizationConfig(lambda_=0.003, smooth_width=1,
                                   dropout_rate=0.2 if training else 0.0, seed=7)
@@ -323,16 +325,18 @@ def test_host_runner_matches_device_path(lc, dtype, H, hc, training):
     torch.cuda.synchronize()
     assert np.array_equal(to_np(y), want["y"])
     assert np.array_equal(to_np(du), want["du"])
-    assert rel_l2(to_np(dK), want["dK"]) < 1e-6
-    assert rel_l2(to_np(dD), want["dD"]) < 1e-6
+    tol = 1e-6 if N <= 8192 else 1e-2  # three-pass: U saved in the I/O precision
+    assert rel_l2(to_np(dK), want["dK"]) < tol
+    assert rel_l2(to_np(dD), want["dD"]) < tol
 
 
-@pytest.mark.parametrize("B,H", [(32, 20), (7, 3)])
-def test_tensor_core_saved_transform(lc, B, H):
+@pytest.mark.parametrize("B,H,dtype", [(32, 20, torch.bfloat16), (7, 3, torch.bfloat16),
+                                       (6, 4, torch.float16)])
+def test_tensor_core_saved_transform(lc, B, H, dtype):
     """fb_fwd_save / fb_bwd_saved (the backward reads the forward's transform
     of u) gives bit-identical results to the recompute path: it parks exactly
     the same bf16 values."""
-    N, dtype = 4096, torch.bfloat16
+    N = 4096
     inp = layer_inputs(lc, B, H, N, dtype)
     cfg = fb.RegularizationConfig(**CFG)
     plan, want = run_layer(inp, N, H, dtype, cfg, engine=1)
