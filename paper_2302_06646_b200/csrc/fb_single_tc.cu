@@ -712,10 +712,17 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int L = min(i1, (h + 1) * npairs) - a;
     // ---- segment start (whole CTA): k_f' of head h to smem, S = 0
     {
+      TT_BEGIN
       const uint32_t* src = reinterpret_cast<const uint32_t*>(kf16 + (size_t)h * kN);
       uint32_t* dst = reinterpret_cast<uint32_t*>(sm + SKF3);
+      // all of the gather in flight at once (4-byte cp.async), not one
+      // dependent global round trip per element
       for (uint32_t i = threadIdx.x; i < 64 * KFH_ROW; i += kThreads)
-        dst[i] = __ldg(src + (i / KFH_ROW) * 128 + i % KFH_ROW);
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(ptx::smem_u32(dst + i)),
+                     "l"(static_cast<uint64_t>(
+                         __cvta_generic_to_global(src + (i / KFH_ROW) * 128 + i % KFH_ROW)))
+                     : "memory");
+      asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;" ::: "memory");
       const uint32_t t = threadIdx.x;
       constexpr uint32_t W = 64 / (kThreads / 128);  // columns per thread
       const uint32_t lane_off = (32u * ((t >> 5) & 3)) << 16, g8 = t >> 7;
@@ -727,6 +734,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       tst_wait();
       cta_sync_tc();
+      TT_END(30)
     }
     const float osc = __ldg(kscale + h);
     // the MMA token measured slower here than free interleaving (the backward's
@@ -744,8 +752,10 @@ __global__ void __launch_bounds__(kThreads, 1)
         uint32_t f2, g;
         coords(f2, g);
         const uint32_t* us = usave + (size_t)(a + j) * kN + (size_t)(kColsPer * g) * 128 + f2;
+        TT_BEGIN
 #pragma unroll
         for (uint32_t jj = 0; jj < kColsPer; ++jj) ur[jj] = __ldg(us + jj * 128);
+        TT_END(26)
       } else {
       // ---- U = F(u), parked as bf16 pairs
       { TT_BEGIN ptx::mbar_wait(in_bar, in_cnt & 1); TT_END(22) }
@@ -777,12 +787,14 @@ __global__ void __launch_bounds__(kThreads, 1)
       issue<T, true>(c, 0);
       if (lead && j + 2 < L) load_pair(sm + c.in_off, SAVED ? &dymap : &umap, h, b0 + 4, in_bar);
       if constexpr (SAVED) {  // the saved U into this slot's parking columns
+        TT_BEGIN
         uint32_t f2, g;
         coords(f2, g);
 #pragma unroll
         for (uint32_t q = 0; q < kColsPer / 8; ++q)
           tst8(taddr(c, c.aux + kColsPer * g + 8 * q), reinterpret_cast<const float*>(ur + 8 * q));
         tst_wait();
+        TT_END(27)
       }
       { TT_BEGIN epi_A_exit<T, true>(c); TT_END(25) }
       issue<T, true>(c, 1);
@@ -841,7 +853,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     base0 += (uint32_t)(L + 1) / 2;
     base1 += (uint32_t)L / 2;
     // ---- segment end: flush S (natural order f = f1 + 64 f2)
-    cta_sync_tc();
+    { TT_BEGIN cta_sync_tc(); TT_END(31) }
     {
       const uint32_t t = threadIdx.x;
       constexpr uint32_t W = 64 / (kThreads / 128);
