@@ -108,6 +108,14 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(sm)}
 
 
+def _traffic(config, direction):
+    """Measured DRAM bytes per launch of the dominant kernel (profiles/traffic.json)."""
+    prof = ROOT / "profiles" / "traffic.json"
+    if not prof.exists():
+        return None
+    return json.loads(prof.read_text()).get(f"config{config}", {}).get(direction)
+
+
 def alg_bytes(cfg, s):
     """Algorithmic HBM bytes per step."""
     E = cfg["B"] * cfg["H"] * cfg["N"]
@@ -274,7 +282,11 @@ def run_ours(args, cfg, rank, world, local_rank):
     cpu = None
     if not args.no_cpu_baseline:
         cpu = cpu_baseline(cfg, args.cpu_sample_heads)
-    launches_per_step = {"single": 6, "three": 9, "auto": 6}[cfg["engine"]]
+    # our kernel launches per timed step (prep + fwd + bwd, training-step path):
+    # single-pass: K1 spectrum, forward, backward, backward tail;
+    # three-pass: regularize, kernel columns, kernel rows | pass 1, rows, pass 3 |
+    # pass 1 (dy), rows, pass 3 (du), dK rows, dD, regularizer chain rule
+    launches_per_step = 12 if plan.engine == fb.Engine.THREE_PASS else 4
     out = {
         "metric": "long-conv fwd+bwd elements/sec (E=B*H*N per step: K1 prep + fwd + bwd)",
         "value": value, "unit": "elements/s", "n_gpus": world, "steps": args.steps,
@@ -411,9 +423,11 @@ def run_learned(args, cfg, rank, world, local_rank):
                    "factors": plan.factors, "params_per_head": plan.param_count,
                    "l2": "rows 100 MiB per tensor"},
         "fwd_ms": fwd_ms, "bwd_ms": bwd_ms,
-        "roofline": {"bound": "hbm", "kernel": "lb_bwd_kernel", "achieved": 12 * E / (bwd_ms / 1e3) / 1e9,
+        "roofline": {"bound": "hbm", "kernel": "bwd: lx_bwd_kernel + lb_reduce_kernel",
+                     "achieved": 12 * E / (bwd_ms / 1e3) / 1e9,
                      "peak": hbm_peak, "unit": "GB/s",
-                     "frac": 12 * E / (bwd_ms / 1e3) / 1e9 / hbm_peak, "traffic": None,
+                     "frac": 12 * E / (bwd_ms / 1e3) / 1e9 / hbm_peak,
+                     "traffic": _traffic(4, "bwd"),
                      "alg_bytes_per_launch": 12 * E, "peak_kind": peak_kind},
         "step_roofline": {"alg_bytes": bytes_step,
                           "achieved_GBs": bytes_step / (ms_step / 1e3) / 1e9,
@@ -423,7 +437,7 @@ def run_learned(args, cfg, rank, world, local_rank):
                 "ms_per_step": ems},
         "cpu_baseline": None if args.no_cpu_baseline else cpu_baseline(cfg, args.cpu_sample_heads),
         "clocks": clk.summary(),
-        "gpu_launches": 2 * args.steps,
+        "gpu_launches": 3 * args.steps,  # forward, backward, block-gradient reduction
     }
     print(json.dumps(out), flush=True)
     if dist:
