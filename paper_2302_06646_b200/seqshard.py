@@ -189,6 +189,39 @@ class GpuPasses:
         return kf2
 
 
+def sharded_long_conv(u_cols: torch.Tensor, kbar_cols: torch.Tensor, D: torch.Tensor,
+                      shard: SeqShard, passes: "GpuPasses", group=None) -> torch.Tensor:
+    """The layer forward y = conv_causal(u, Kbar) + D u (regularize.cpp:185-187)
+    with the sequence sharded: rank r holds the tau-slice [tau0, tau0 + lp) of
+    every data row c < m/2 of t = c l + tau (N = n / 2 causal; rows c >= m/2
+    are the zero pad and are not stored).
+      u_cols [B, H, m/2, lp] real, kbar_cols [H, m/2, lp] fp32 (regularized),
+      D [H]  ->  y_cols [B, H, m/2, lp] (u's dtype).
+    Two real channels ride as re / im of one complex transform (batch-pair
+    packing, as on a single GPU); the kernel spectrum is built sharded with the
+    same passes (two all-to-alls), the convolution costs two more."""
+    B, H, half, lp = u_cols.shape
+    m = shard.m
+    if half * 2 != m or lp != shard.lp or kbar_cols.shape != (H, half, lp):
+        raise ValueError("sharded_long_conv: expected u [B, H, m/2, lp] and Kbar [H, m/2, lp]")
+    dev = u_cols.device
+    kpad = torch.zeros(H, m, lp, dtype=torch.float32, device=dev)
+    kpad[:, :half] = kbar_cols.float()
+    kf2 = passes.spectrum_rows(kpad, shard, group)  # [H, mp, l]
+    P = (B + 1) // 2
+    uf = u_cols.float()
+    if B % 2:
+        uf = torch.cat([uf, torch.zeros_like(uf[:1])], 0)
+    x = torch.zeros(P, H, m, lp, dtype=torch.complex64, device=dev)
+    x[:, :, :half] = torch.complex(uf[0::2], uf[1::2])
+    passes.kf2 = kf2.repeat(P, 1, 1)  # channel (p, h) uses head h's rows
+    y = four_step_conv(x.reshape(P * H, m, lp), shard, passes, group).reshape(P, H, m, lp)
+    y = y[:, :, :half]
+    out = torch.stack([y.real, y.imag], 1).reshape(2 * P, H, half, lp)[:B]
+    out = out + D.float().view(1, H, 1, 1) * u_cols.float()
+    return out.to(u_cols.dtype)
+
+
 def head_shard(H: int, world: int, rank: int) -> slice:
     """Heads owned by `rank` under B*H sharding (contiguous, no collective:
     K, D, dK, dD are head-local, regularize.cpp:177-188)."""

@@ -396,3 +396,22 @@ def test_three_pass_saved_transform(lc, dtype, N):
     ref = oracle_layer(lc, inp, cfg)
     assert_parity(dict(y=to_np(y), du=to_np(du), dK=to_np(dK), dD=to_np(dD)), ref, TOL[dtype],
                   keys=("y", "du", "dK", "dD"))
+
+
+def test_sharded_long_conv_layer_single_rank(lc):
+    """seqshard.sharded_long_conv (pairs of real channels, causal crop, D u)
+    at one rank against the fp64 layer oracle (N = 65536: l = 8192, m = 16)."""
+    from paper_2302_06646_b200 import seqshard as ss
+
+    B, H, N = 3, 2, 65536
+    l, m = 8192, 16
+    inp = layer_inputs(lc, B, H, N, torch.float32)
+    cfg = fb.RegularizationConfig(**CFG)
+    kbar = lc.regularize_bank(inp["K"], cfg.lambda_, cfg.smooth_width)
+    want = lc.long_conv_forward(inp["u"], kbar, inp["D"])
+    sh = ss.SeqShard(l=l, m=m, world=1, rank=0)
+    u_cols = inp["tu"].reshape(B, H, m // 2, l)
+    k_cols = torch.tensor(kbar, dtype=torch.float32, device="cuda").reshape(H, m // 2, l)
+    y = ss.sharded_long_conv(u_cols, k_cols, inp["tD"], sh, ss.GpuPasses(2 * N))
+    torch.cuda.synchronize()
+    assert rel_l2(to_np(y.reshape(B, H, N)), want) < 1e-5

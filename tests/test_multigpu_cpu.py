@@ -34,7 +34,9 @@ class NumpyPasses:
 
     def pass2(self, rows, sh):
         Z = np.fft.fft(rows.numpy(), axis=2)
-        Z = Z * self.kf2[:, sh.a0:sh.a0 + sh.mp, :]
+        kf2 = self.kf2.numpy() if isinstance(self.kf2, torch.Tensor) else self.kf2
+        # full-height kf2 (unsharded problem) or this rank's rows (sharded_long_conv)
+        Z = Z * (kf2[:, sh.a0:sh.a0 + sh.mp, :] if kf2.shape[1] == sh.m else kf2)
         return torch.from_numpy(np.fft.ifft(Z, axis=2) * sh.l).to(torch.complex64)
 
     def pass3(self, w, sh):
@@ -43,6 +45,13 @@ class NumpyPasses:
         a = np.arange(sh.m)[:, None]
         W = w.numpy() * np.exp(2j * np.pi * a * tau[None, :] / n)
         return torch.from_numpy(np.fft.ifft(W, axis=1) * sh.m / n).to(torch.complex64)
+
+    def spectrum_rows(self, kbar_cols, sh, group=None):
+        """The sharded kernel spectrum, as GpuPasses.spectrum_rows does it."""
+        x = torch.complex(kbar_cols.float(), torch.zeros_like(kbar_cols.float()))
+        rows = ss.columns_to_rows(self.pass1(x, sh), sh, group)
+        self.kf2 = np.fft.fft(rows.numpy(), axis=2)
+        return torch.from_numpy(self.kf2).to(torch.complex64)
 
 
 def _problem(C=3, seed=0):
@@ -111,3 +120,36 @@ def test_head_sharding_gloo(world, monkeypatch, lc):
     K, D = lc.init_kernels(1, H, N, 3)
     want = lc.regularized_long_conv(u, K, D, 0.003, 1)
     assert np.array_equal(np.load(os.path.join(d, f"heads_{world}.npy")), want)
+
+
+def _layer_worker(rank, world):
+    from oracle.oracle import LcOracle
+
+    lc = LcOracle()
+    B, H, N = 3, 2, L_COLS * M_ROWS // 2
+    u = lc.signal_batch(1, B, H, N)
+    K, D = lc.init_kernels(1, H, N, 3)
+    kbar = lc.regularize_bank(K, 0.003, 1)
+    sh = ss.SeqShard(L_COLS, M_ROWS, world, rank)
+    u_cols = torch.from_numpy(u.reshape(B, H, M_ROWS // 2, L_COLS)[..., sh.tau0:sh.tau0 + sh.lp])
+    k_cols = torch.from_numpy(kbar.reshape(H, M_ROWS // 2, L_COLS)[..., sh.tau0:sh.tau0 + sh.lp])
+    y = ss.sharded_long_conv(u_cols.float(), k_cols.float(), torch.from_numpy(D).float(), sh,
+                             NumpyPasses(None))
+    np.save(os.path.join(os.environ["FB_TEST_DIR"], f"layer_{world}_{rank}.npy"), y.numpy())
+
+
+@pytest.mark.parametrize("world", [2, 4])
+def test_sharded_layer_gloo(world, monkeypatch, lc):
+    """seqshard.sharded_long_conv (pair packing, causal crop, D u, sharded kernel
+    spectrum) across ranks equals the fp64 layer oracle."""
+    d = tempfile.mkdtemp()
+    monkeypatch.setenv("FB_TEST_DIR", d)
+    ss.run_ranks(world, _layer_worker, port=29591 + world)
+    B, H, N = 3, 2, L_COLS * M_ROWS // 2
+    u = lc.signal_batch(1, B, H, N)
+    K, D = lc.init_kernels(1, H, N, 3)
+    kbar = lc.regularize_bank(K, 0.003, 1)
+    want = lc.long_conv_forward(u.astype(np.float32).astype(np.float64), kbar, D.astype(np.float32))
+    parts = [np.load(os.path.join(d, f"layer_{world}_{r}.npy")) for r in range(world)]
+    got = np.concatenate(parts, axis=-1).reshape(B, H, N)
+    assert np.linalg.norm(got - want) / np.linalg.norm(want) < 1e-5
