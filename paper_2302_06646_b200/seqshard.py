@@ -175,6 +175,18 @@ class GpuPasses:
                                                       rows.shape[0], sh.mp, 0, 1.0, self._stream()))
         return rows
 
+    def rows_fft(self, rows: torch.Tensor, sh: SeqShard) -> torch.Tensor:
+        """FFT_l of each row [C, mp, l] (fb_shard_rows, spectrum mode)."""
+        rows = rows.contiguous()
+        out = torch.empty_like(rows)
+        self._lib.check(self._lib.lib().fb_shard_rows(self._h, self._p(rows), None, self._p(out),
+                                                      rows.shape[0], sh.mp, 1, 1.0, self._stream()))
+        return out
+
+    def rows_ifft(self, rows: torch.Tensor, sh: SeqShard) -> torch.Tensor:
+        """Unnormalised inverse FFT_l of each row: conj(FFT_l(conj(rows)))."""
+        return torch.conj(self.rows_fft(torch.conj(rows).resolve_conj(), sh)).resolve_conj()
+
     def spectrum_rows(self, kbar_cols: torch.Tensor, sh: SeqShard, group=None) -> torch.Tensor:
         """This rank's kernel-spectrum rows from its real kernel columns
         kbar_cols [C, m, lp] (float32; zero-padded causal kernels): pass 1,
@@ -220,6 +232,63 @@ def sharded_long_conv(u_cols: torch.Tensor, kbar_cols: torch.Tensor, D: torch.Te
     out = torch.stack([y.real, y.imag], 1).reshape(2 * P, H, half, lp)[:B]
     out = out + D.float().view(1, H, 1, 1) * u_cols.float()
     return out.to(u_cols.dtype)
+
+
+def _pack_pairs(sig_cols: torch.Tensor, m: int) -> torch.Tensor:
+    """[B, H, m/2, lp] real -> [P*H, m, lp] complex (channels 2p, 2p+1 -> re, im;
+    rows c >= m/2 are the causal zero pad)."""
+    B, H, half, lp = sig_cols.shape
+    P = (B + 1) // 2
+    f = sig_cols.float()
+    if B % 2:
+        f = torch.cat([f, torch.zeros_like(f[:1])], 0)
+    x = torch.zeros(P, H, m, lp, dtype=torch.complex64, device=sig_cols.device)
+    x[:, :, :half] = torch.complex(f[0::2], f[1::2])
+    return x.reshape(P * H, m, lp)
+
+
+def _unpack_pairs(y: torch.Tensor, B: int, H: int, half: int) -> torch.Tensor:
+    P = (B + 1) // 2
+    y = y.reshape(P, H, -1, y.shape[-1])[:, :, :half]
+    return torch.stack([y.real, y.imag], 1).reshape(2 * P, H, half, y.shape[-1])[:B]
+
+
+def sharded_long_conv_backward(dy_cols: torch.Tensor, u_cols: torch.Tensor,
+                               kbar_cols: torch.Tensor, D: torch.Tensor, shard: SeqShard,
+                               passes: "GpuPasses", group=None):
+    """Backward of sharded_long_conv (SURVEY.md §8c formulas, sequence sharded):
+      du     = corr(dy, Kbar) + D dy   -> IFFT(DY conj(K_hat)), causal crop
+      dKbar  = sum_b corr(dy_b, u_b)   -> Re IFFT(sum_pairs conj(U) DY), lag < N
+      dD     = dKbar[0]                 (lag 0, held by the rank with tau0 = 0)
+    Layouts as in sharded_long_conv; returns (du_cols [B, H, m/2, lp],
+    dkbar_cols [H, m/2, lp] fp32, dD [H] fp32).  The chain rule through the
+    regularizers (smooth needs the +-p neighbours across slices) is left to
+    the caller on the gathered dKbar."""
+    B, H, half, lp = u_cols.shape
+    m = shard.m
+    dev = u_cols.device
+    kpad = torch.zeros(H, m, lp, dtype=torch.float32, device=dev)
+    kpad[:, :half] = kbar_cols.float()
+    kf2 = passes.spectrum_rows(kpad, shard, group)  # [H, mp, l] (K_hat rows)
+    P = (B + 1) // 2
+    xdy = _pack_pairs(dy_cols, m)
+    xu = _pack_pairs(u_cols, m)
+    # row spectra of dy and u (pass 1, transpose, row FFT)
+    DY = passes.rows_fft(columns_to_rows(passes.pass1(xdy, shard), shard, group), shard)
+    U = passes.rows_fft(columns_to_rows(passes.pass1(xu, shard), shard, group), shard)
+    # du: DY conj(K_hat), inverse rows, transpose back, pass 3
+    kc = torch.conj(kf2).resolve_conj().repeat(P, 1, 1)
+    du_rows = passes.rows_ifft(DY * kc, shard)
+    du = _unpack_pairs(passes.pass3(rows_to_columns(du_rows, shard, group), shard), B, H, half)
+    du = du + D.float().view(1, H, 1, 1) * dy_cols.float()
+    # dKbar: sum over the pairs of each head, then the inverse transform
+    S = (torch.conj(U) * DY).reshape(P, H, shard.mp, shard.l).sum(0)
+    dk = passes.pass3(rows_to_columns(passes.rows_ifft(S, shard), shard, group), shard)
+    dkbar = dk.real[:, :half].contiguous()
+    dD = dkbar[:, 0, 0].clone() if shard.tau0 == 0 else torch.zeros(H, device=dev)
+    if shard.world > 1:
+        dist.all_reduce(dD, group=group)
+    return du.to(dy_cols.dtype), dkbar, dD
 
 
 def head_shard(H: int, world: int, rank: int) -> slice:

@@ -415,3 +415,25 @@ def test_sharded_long_conv_layer_single_rank(lc):
     y = ss.sharded_long_conv(u_cols, k_cols, inp["tD"], sh, ss.GpuPasses(2 * N))
     torch.cuda.synchronize()
     assert rel_l2(to_np(y.reshape(B, H, N)), want) < 1e-5
+
+
+def test_sharded_long_conv_backward_single_rank(lc):
+    """seqshard.sharded_long_conv_backward on the GPU passes at one rank vs the
+    fp64 backward oracle (du, dKbar, dD)."""
+    from paper_2302_06646_b200 import seqshard as ss
+
+    B, H, N = 3, 2, 65536
+    l, m = 8192, 16
+    inp = layer_inputs(lc, B, H, N, torch.float32)
+    cfg = fb.RegularizationConfig(**CFG)
+    kbar = lc.regularize_bank(inp["K"], cfg.lambda_, cfg.smooth_width)
+    du_w, dkbar_w, dD_w = lc.long_conv_backward(inp["u"], inp["dy"], kbar, inp["D"])
+    sh = ss.SeqShard(l=l, m=m, world=1, rank=0)
+    cols = lambda t: t.reshape(*t.shape[:-1], m // 2, l)  # noqa: E731
+    kt = torch.tensor(kbar, dtype=torch.float32, device="cuda")
+    du, dkbar, dD = ss.sharded_long_conv_backward(cols(inp["tdy"]), cols(inp["tu"]), cols(kt),
+                                                  inp["tD"], sh, ss.GpuPasses(2 * N))
+    torch.cuda.synchronize()
+    assert rel_l2(to_np(du.reshape(B, H, N)), du_w) < 1e-5
+    assert rel_l2(to_np(dkbar.reshape(H, N)), dkbar_w) < 1e-5
+    assert rel_l2(to_np(dD), dD_w) < 1e-5

@@ -46,6 +46,12 @@ class NumpyPasses:
         W = w.numpy() * np.exp(2j * np.pi * a * tau[None, :] / n)
         return torch.from_numpy(np.fft.ifft(W, axis=1) * sh.m / n).to(torch.complex64)
 
+    def rows_fft(self, rows, sh):
+        return torch.from_numpy(np.fft.fft(rows.numpy(), axis=2)).to(torch.complex64)
+
+    def rows_ifft(self, rows, sh):
+        return torch.from_numpy(np.fft.ifft(rows.numpy(), axis=2) * sh.l).to(torch.complex64)
+
     def spectrum_rows(self, kbar_cols, sh, group=None):
         """The sharded kernel spectrum, as GpuPasses.spectrum_rows does it."""
         x = torch.complex(kbar_cols.float(), torch.zeros_like(kbar_cols.float()))
@@ -153,3 +159,42 @@ def test_sharded_layer_gloo(world, monkeypatch, lc):
     parts = [np.load(os.path.join(d, f"layer_{world}_{r}.npy")) for r in range(world)]
     got = np.concatenate(parts, axis=-1).reshape(B, H, N)
     assert np.linalg.norm(got - want) / np.linalg.norm(want) < 1e-5
+
+
+def _layer_bwd_worker(rank, world):
+    from oracle.oracle import LcOracle
+
+    lc = LcOracle()
+    B, H, N = 3, 2, L_COLS * M_ROWS // 2
+    u = lc.signal_batch(1, B, H, N)
+    dy = lc.signal_batch(2, B, H, N)
+    K, D = lc.init_kernels(1, H, N, 3)
+    kbar = lc.regularize_bank(K, 0.003, 1)
+    sh = ss.SeqShard(L_COLS, M_ROWS, world, rank)
+    cols = lambda a: torch.from_numpy(a.reshape(*a.shape[:-1], M_ROWS // 2, L_COLS)[..., sh.tau0:sh.tau0 + sh.lp]).float()  # noqa: E731
+    du, dkbar, dD = ss.sharded_long_conv_backward(cols(dy), cols(u), cols(kbar),
+                                                  torch.from_numpy(D).float(), sh, NumpyPasses(None))
+    d = os.environ["FB_TEST_DIR"]
+    np.save(os.path.join(d, f"bdu_{world}_{rank}.npy"), du.numpy())
+    np.save(os.path.join(d, f"bdk_{world}_{rank}.npy"), dkbar.numpy())
+    np.save(os.path.join(d, f"bdd_{world}_{rank}.npy"), dD.numpy())
+
+
+@pytest.mark.parametrize("world", [2])
+def test_sharded_layer_backward_gloo(world, monkeypatch, lc):
+    d = tempfile.mkdtemp()
+    monkeypatch.setenv("FB_TEST_DIR", d)
+    ss.run_ranks(world, _layer_bwd_worker, port=29601 + world)
+    B, H, N = 3, 2, L_COLS * M_ROWS // 2
+    u = lc.signal_batch(1, B, H, N).astype(np.float32).astype(np.float64)
+    dy = lc.signal_batch(2, B, H, N).astype(np.float32).astype(np.float64)
+    K, D = lc.init_kernels(1, H, N, 3)
+    kbar = lc.regularize_bank(K, 0.003, 1)
+    du_w, dkbar_w, dD_w = lc.long_conv_backward(u, dy, kbar, D.astype(np.float32))
+    cat = lambda name: np.concatenate([np.load(os.path.join(d, f"{name}_{world}_{r}.npy"))  # noqa: E731
+                                       for r in range(world)], axis=-1)
+    rel = lambda a, b: np.linalg.norm(a - b) / np.linalg.norm(b)  # noqa: E731
+    assert rel(cat("bdu").reshape(B, H, N), du_w) < 1e-5
+    assert rel(cat("bdk").reshape(H, N), dkbar_w) < 1e-5
+    for r in range(world):
+        assert rel(np.load(os.path.join(d, f"bdd_{world}_{r}.npy")), dD_w) < 1e-5
