@@ -43,6 +43,10 @@ CONFIGS = {
     # config 5 (sweep N=256..1M at B*H=2048): --config 5 --n N
     5: dict(B=8, H=256, N=4096, dtype="bf16", engine="auto",
             workload="config5: sequence-length sweep at B*H=2048"),
+    # config 5-4M: N = 4M sequence-sharded over the ranks (report only);
+    # --bh lowers B*H when few GPUs hold the whole sequence
+    6: dict(B=8, H=256, N=4194304, dtype="f32", engine="seqshard",
+            workload="config5-4M: N=4M sequence-sharded four-step fwd+bwd"),
 }
 LAM, P = 0.003, 1
 
@@ -528,6 +532,81 @@ def run_reference(args, cfg, rank):
     print(json.dumps(out), flush=True)
 
 
+def run_seqshard(args, cfg, rank, world, local_rank):
+    """Config 5-4M: the layer forward + backward with the sequence sharded over
+    the ranks (seqshard.sharded_long_conv / _backward: our column and row
+    kernels, NCCL all_to_all_single transposes).  Weak in nothing: the whole
+    job is one sequence batch; value = B*H*N / max-over-ranks step time."""
+    import torch
+
+    from paper_2302_06646_b200 import seqshard as ss
+
+    dev = torch.device("cuda", local_rank)
+    torch.cuda.set_device(dev)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=dev)
+    B, H, N = cfg["B"], cfg["H"], cfg["N"]
+    if args.bh:
+        H = max(1, args.bh // B)
+    n, l = 2 * N, 8192
+    m = n // l
+    sh = ss.SeqShard(l=l, m=m, world=world, rank=rank)
+    g = torch.Generator(device=dev)
+    g.manual_seed(77 + rank)
+    half = m // 2
+    u = torch.randn(B, H, half, sh.lp, device=dev, generator=g)
+    dy = torch.randn(B, H, half, sh.lp, device=dev, generator=g)
+    t = (torch.arange(half, device=dev)[:, None] * l + sh.tau0 +
+         torch.arange(sh.lp, device=dev)[None, :]).float()
+    kbar = torch.randn(H, half, sh.lp, device=dev, generator=g) * torch.exp(-t / 2e5)[None]
+    D = torch.randn(H, device=dev, generator=g)
+    passes = ss.GpuPasses(n, device=dev)
+
+    def step():
+        y = ss.sharded_long_conv(u, kbar, D, sh, passes)
+        du, dk, dD = ss.sharded_long_conv_backward(dy, u, kbar, D, sh, passes)
+        return y, du, dk, dD
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    stream = torch.cuda.current_stream()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local_rank) as clk:
+        e0.record(stream)
+        for _ in range(args.steps):
+            step()
+        e1.record(stream)
+        torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    tmax = torch.tensor([e0.elapsed_time(e1) / args.steps], device=dev)
+    if dist:
+        dist.all_reduce(tmax, op=dist.ReduceOp.MAX)
+    ms = float(tmax.item())
+    E = B * H * N
+    if rank == 0:
+        print(json.dumps({
+            "metric": "long-conv fwd+bwd elements/sec (E=B*H*N per step)", "value": E / (ms / 1e3),
+            "unit": "elements/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": ms, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+            "dtype": "f32", "data": "synthetic (randn signals, decaying random Kbar)",
+            "config": {"workload": cfg["workload"], "B": B, "H": H, "N": N, "transform_len": n,
+                       "l": l, "m": m, "sharding": f"sequence over {world} rank(s), tau-slices of "
+                       f"{sh.lp} columns; 4 all-to-alls fwd, 6 bwd",
+                       "bh_reduced": bool(args.bh), "report_only": True},
+            "roofline": None, "cpu_baseline": None, "clocks": clk.summary(),
+            "gpu_launches": None, "e2e": None}))
+    if dist:
+        dist.destroy_process_group()
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -538,6 +617,7 @@ def main():
     ap.add_argument("--cpu-sample-heads", type=int, default=32)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--n", type=int, default=None, help="sequence length (config 5 sweep)")
+    ap.add_argument("--bh", type=int, default=None, help="B*H override (config 6, few GPUs)")
     args = ap.parse_args()
     rank = int(os.environ.get("RANK", 0))
     world = int(os.environ.get("WORLD_SIZE", 1))
@@ -548,6 +628,9 @@ def main():
         cfg["workload"] = cfg["workload"] + f", N={args.n}"
     if args.config == 4 and args.impl == "ours":
         run_learned(args, cfg, rank, world, local_rank)
+        return
+    if args.config == 6 and args.impl == "ours":
+        run_seqshard(args, cfg, rank, world, local_rank)
         return
     if args.impl == "reference":
         run_reference(args, cfg, rank)
