@@ -91,17 +91,23 @@ __global__ void __launch_bounds__(FftShape<LOG2N>::T, 2)
   const uint32_t h = blockIdx.x, j = threadIdx.x;
   load_table<LOG2N>(tab, tab_g);
   const size_t base = (size_t)h * N;
+  // the fp64 regularizer once per element in a rolled loop (its code inlined
+  // sixteen times next to the FFT thrashed the instruction cache), staged in smem
+  float* kb = reinterpret_cast<float*>(work);
+#pragma unroll 1
+  for (uint32_t t = j; t < N; t += S::T) {
+    const float kv = reg_value(K, keep, keep_scale, base, t, N, p, lambda, freq);
+    kbar[base + t] = kv;
+    kb[t] = kv;
+  }
+  __syncthreads();
   float2 v[16];
 #pragma unroll
   for (int r = 0; r < 16; ++r) {
     const uint32_t t = j + r * S::stride;
-    float kv = 0.f;
-    if (t < N) {
-      kv = reg_value(K, keep, keep_scale, base, t, N, p, lambda, freq);
-      kbar[base + t] = kv;
-    }
-    v[r] = make_float2(kv, 0.f);
+    v[r] = make_float2(t < N ? kb[t] : 0.f, 0.f);
   }
+  __syncthreads();  // kb read before the FFT overwrites work
   dft_reg<-1, 16>(v);
   bfly_store<16, 1>(work, v, j);
   __syncthreads();
