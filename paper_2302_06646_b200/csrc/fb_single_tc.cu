@@ -393,8 +393,16 @@ __device__ unsigned long long g_last[148 * 2];
 #define TT_END(k)
 #endif
 
-template <typename T, bool W3 = false>
-__device__ __forceinline__ void issue(Ctx& c, int stage) {
+// No-op leader hook for issue()
+struct NoHook {
+  __device__ __forceinline__ void operator()() const {}
+};
+
+// publish, MMA batch of `stage` by the slot leader, wait for it.  `hook`
+// runs in the leader right after the commit, i.e. while the MMAs execute:
+// work placed there (the next input's TMA) is off the slot's critical path.
+template <typename T, bool W3 = false, class Hook = NoHook>
+__device__ __forceinline__ void issue(Ctx& c, int stage, const Hook& hook = Hook()) {
 #ifdef FB_TC_TIMING
   const bool tl = slot_leader() && blockIdx.x < 148;
   const uint32_t ts = (blockIdx.x * 2 + (threadIdx.x / kSlotThreads));
@@ -420,6 +428,7 @@ __device__ __forceinline__ void issue(Ctx& c, int stage) {
       default: mma_stage_Ap<T>(c); break;
     }
     tc::commit(c.mma_bar);
+    hook();
   }
   ++c.nb;
 #ifdef FB_TC_TIMING
@@ -625,10 +634,13 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     { TT_BEGIN ptx::mbar_wait(in_bar, it & 1); TT_END(16) }
     issue<T, true>(c, 0);
-    if (lead && item + 2 < i1)
-      load_pair(sm + c.in_off, &umap, (item + 2) / npairs, 2 * ((item + 2) % npairs), in_bar);
     { TT_BEGIN epi_A_exit<T, true>(c); TT_END(18) }
-    issue<T, true>(c, 1);
+    // the input buffer is free since stage A completed: the next pair's TMA
+    // goes out from the leader while the stage-B MMAs run
+    issue<T, true>(c, 1, [&] {
+      if (item + 2 < i1)
+        load_pair(sm + c.in_off, &umap, (item + 2) / npairs, 2 * ((item + 2) % npairs), in_bar);
+    });
     // ---- B exit: Z = X * k_f' -> Zr/Zi[k = f2][n = f1]
     {
       uint32_t f2, g;
@@ -761,9 +773,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       { TT_BEGIN ptx::mbar_wait(in_bar, in_cnt & 1); TT_END(22) }
       ++in_cnt;
       issue<T, true>(c, 0);
-      if (lead) load_pair(sm + c.in_off, &dymap, h, b0, in_bar);
       { TT_BEGIN epi_A_exit<T, true>(c); TT_END(25) }
-      issue<T, true>(c, 1);
+      issue<T, true>(c, 1, [&] { load_pair(sm + c.in_off, &dymap, h, b0, in_bar); });
       {
         uint32_t f2, g;
         coords(f2, g);
@@ -785,7 +796,6 @@ __global__ void __launch_bounds__(kThreads, 1)
       { TT_BEGIN ptx::mbar_wait(in_bar, in_cnt & 1); TT_END(23) }
       ++in_cnt;
       issue<T, true>(c, 0);
-      if (lead && j + 2 < L) load_pair(sm + c.in_off, SAVED ? &dymap : &umap, h, b0 + 4, in_bar);
       if constexpr (SAVED) {  // the saved U into this slot's parking columns
         TT_BEGIN
         uint32_t f2, g;
@@ -797,7 +807,9 @@ __global__ void __launch_bounds__(kThreads, 1)
         TT_END(27)
       }
       { TT_BEGIN epi_A_exit<T, true>(c); TT_END(25) }
-      issue<T, true>(c, 1);
+      issue<T, true>(c, 1, [&] {  // next pair's first input, off the critical path
+        if (j + 2 < L) load_pair(sm + c.in_off, SAVED ? &dymap : &umap, h, b0 + 4, in_bar);
+      });
       // ---- S += conj(U) DY (in pair order), Z = DY conj(k_f') -> B' operand
       if (j > 0) {
         const uint32_t idx = slot ? base0 + (uint32_t)k : base1 + (uint32_t)k - 1;
