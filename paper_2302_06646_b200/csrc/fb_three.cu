@@ -376,46 +376,71 @@ __device__ __forceinline__ ColTile col_tile(int t, int H) {
   return c;
 }
 
+// Producer / consumer ring shared by the streaming column kernels: warp
+// kTB / 32 only issues the TMA boxes (waiting on the per-stage "empty"
+// barriers), the kTB consumer threads wait on "full", copy their column to
+// registers, release the stage at once and compute — the TMA issue is never
+// on a consumer warp's critical path.
+__device__ __forceinline__ void mbar_arrive_cta(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(ptx::smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void consumers_sync() {
+  asm volatile("bar.sync 1, %0;" ::"n"(kTB) : "memory");
+}
+template <class Issue>
+__device__ __forceinline__ void col_producer(int first, int step, int ntiles, int nstages,
+                                             uint64_t* empty, Issue&& issue) {
+  if (threadIdx.x != kTB) return;
+  int k = 0;
+  for (int t = first; t < ntiles; t += step, ++k) {
+    const int sg = k % nstages;
+    if (k >= nstages) ptx::mbar_wait(&empty[sg], (uint32_t)((k / nstages) - 1) & 1);
+    issue(t, sg);
+  }
+}
+
 // Pass 1, SRC 0: signal pairs (channels 2 pr, 2 pr + 1 -> re, im);
 // SRC 1: dy and u pairs at once, plus the lag-0 dD partial.  Signal maps view
 // [B*H][rows][l] with rows = N / l data rows (the causal pad is implicit).
 template <typename IO, typename ST, int M, int SRC>
-__global__ void __launch_bounds__(kTB)
+__global__ void __launch_bounds__(kTB + 32)
     tp_col1_kernel(const __grid_constant__ CUtensorMap amap, const __grid_constant__ CUtensorMap bmap,
                    CxT<ST>* __restrict__ out_a, CxT<ST>* __restrict__ out_b,
                    float* __restrict__ ddpart, const float2* __restrict__ tab_g, int H, int npairs,
                    int rows, int ntiles, int nstages) {
   extern __shared__ __align__(128) unsigned char csm[];
-  __shared__ __align__(8) uint64_t full[kColMaxStages];
-  __shared__ float red[kTB / 32];
+  __shared__ __align__(8) uint64_t full[kColMaxStages], empty[kColMaxStages];
+  __shared__ float red[2][kTB / 32];
   constexpr int NCH = SRC == 1 ? 4 : 2;
   const uint32_t chb = (uint32_t)rows * kTB * sizeof(IO);
   const uint32_t stage_bytes = NCH * chb;
   const int j = threadIdx.x;
   if (j == 0) {
-    for (int i = 0; i < nstages; ++i) ptx::mbar_init(&full[i], 1);
+    for (int i = 0; i < nstages; ++i) {
+      ptx::mbar_init(&full[i], 1);
+      ptx::mbar_init(&empty[i], kTB);
+    }
     ptx::fence_barrier_init();
   }
   __syncthreads();
-  auto issue = [&](int t, int st) {
-    const ColTile c = col_tile(t, H);
-    unsigned char* dst = csm + (size_t)st * stage_bytes;
-    ptx::mbar_arrive_expect_tx(&full[st], stage_bytes);
-#pragma unroll
-    for (int ch = 0; ch < NCH; ++ch) {
-      const CUtensorMap* mp = (SRC == 1 && ch >= 2) ? &bmap : &amap;
-      const int b = 2 * c.pr + (ch & 1);
-      tma_load_3d(dst + ch * chb, mp, c.tb * (int)kTB, 0, b * H + c.h, &full[st]);
-    }
-  };
   const int first = blockIdx.x, step = gridDim.x;
-  if (j == 0)
-    for (int i = 0; i < nstages - 1; ++i)
-      if (first + i * step < ntiles) issue(first + i * step, i);
+  if (j >= (int)kTB) {
+    col_producer(first, step, ntiles, nstages, empty, [&](int t, int st) {
+      const ColTile c = col_tile(t, H);
+      unsigned char* dst = csm + (size_t)st * stage_bytes;
+      ptx::mbar_arrive_expect_tx(&full[st], stage_bytes);
+#pragma unroll
+      for (int ch = 0; ch < NCH; ++ch) {
+        const CUtensorMap* mp = (SRC == 1 && ch >= 2) ? &bmap : &amap;
+        const int b = 2 * c.pr + (ch & 1);
+        tma_load_3d(dst + ch * chb, mp, c.tb * (int)kTB, 0, b * H + c.h, &full[st]);
+      }
+    });
+    return;
+  }
   int it = 0;
   for (int t = first; t < ntiles; t += step, ++it) {
     const int sg = it % nstages;
-    if (j == 0 && t + (nstages - 1) * step < ntiles) issue(t + (nstages - 1) * step, (it + nstages - 1) % nstages);
     ptx::mbar_wait(&full[sg], (uint32_t)(it / nstages) & 1);
     const ColTile c = col_tile(t, H);
     const uint32_t tau = c.tb * kTB + j;
@@ -431,9 +456,10 @@ __global__ void __launch_bounds__(kTB)
     float2 v[M];
     column(0, v);
     float dd = 0.f;
+    float2 w[SRC == 1 ? M : 1];
+    if constexpr (SRC == 1) column(2, w);
+    mbar_arrive_cta(&empty[sg]);  // this thread's reads of the stage are done
     if constexpr (SRC == 1) {
-      float2 w[M];
-      column(2, w);
 #pragma unroll
       for (int r = 0; r < M; ++r) dd = fmaf(v[r].x, w[r].x, fmaf(v[r].y, w[r].y, dd));
       dft_reg<-1, M>(w);
@@ -450,13 +476,11 @@ __global__ void __launch_bounds__(kTB)
     if constexpr (SRC == 1) {
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) dd += __shfl_xor_sync(0xffffffffu, dd, o);
-      if ((j & 31) == 0) red[j >> 5] = dd;
-    }
-    __syncthreads();  // stage sg fully read (and red written) before reuse
-    if constexpr (SRC == 1) {
+      if ((j & 31) == 0) red[it & 1][j >> 5] = dd;
+      consumers_sync();  // red[it & 1] complete (double-buffered by tile parity)
       if (j == 0) {
         float s = 0.f;
-        for (int w2 = 0; w2 < (int)(kTB / 32); ++w2) s += red[w2];
+        for (int w2 = 0; w2 < (int)(kTB / 32); ++w2) s += red[it & 1][w2];
         ddpart[((size_t)c.h * npairs + c.pr) * (kL / kTB) + c.tb] = s;
       }
     }
@@ -466,40 +490,42 @@ __global__ void __launch_bounds__(kTB)
 // Pass 3 (MODE 0): W rows [pair*H + h][M][l] (complex ST) -> out[b][h][c l + tau]
 // = Re/Im(column IDFT) + D[h] skip[b][h][c l + tau], c < rows.
 template <typename ST, typename IO, int M>
-__global__ void __launch_bounds__(kTB)
+__global__ void __launch_bounds__(kTB + 32)
     tp_col3_kernel(const __grid_constant__ CUtensorMap wmap, const __grid_constant__ CUtensorMap smap,
                    IO* __restrict__ out, const float* __restrict__ D,
                    const float2* __restrict__ tab_g, int B, int H, uint32_t N, int rows, int ntiles,
                    int nstages) {
   extern __shared__ __align__(128) unsigned char csm[];
-  __shared__ __align__(8) uint64_t full[kColMaxStages];
+  __shared__ __align__(8) uint64_t full[kColMaxStages], empty[kColMaxStages];
   const uint32_t wb = M * kTB * sizeof(CxT<ST>);
   const uint32_t chb = (uint32_t)rows * kTB * sizeof(IO);
   const uint32_t stage_bytes = wb + 2 * chb;
   const int j = threadIdx.x;
   if (j == 0) {
-    for (int i = 0; i < nstages; ++i) ptx::mbar_init(&full[i], 1);
+    for (int i = 0; i < nstages; ++i) {
+      ptx::mbar_init(&full[i], 1);
+      ptx::mbar_init(&empty[i], kTB);
+    }
     ptx::fence_barrier_init();
   }
   __syncthreads();
-  auto issue = [&](int t, int st) {
-    const ColTile c = col_tile(t, H);
-    unsigned char* dst = csm + (size_t)st * stage_bytes;
-    ptx::mbar_arrive_expect_tx(&full[st], stage_bytes);
-    tma_load_3d(dst, &wmap, c.tb * (int)kTB, 0, c.pr * H + c.h, &full[st]);
-#pragma unroll
-    for (int ch = 0; ch < 2; ++ch)
-      tma_load_3d(dst + wb + ch * chb, &smap, c.tb * (int)kTB, 0, (2 * c.pr + ch) * H + c.h,
-                  &full[st]);
-  };
   const int first = blockIdx.x, step = gridDim.x;
-  if (j == 0)
-    for (int i = 0; i < nstages - 1; ++i)
-      if (first + i * step < ntiles) issue(first + i * step, i);
+  if (j >= (int)kTB) {
+    col_producer(first, step, ntiles, nstages, empty, [&](int t, int st) {
+      const ColTile c = col_tile(t, H);
+      unsigned char* dst = csm + (size_t)st * stage_bytes;
+      ptx::mbar_arrive_expect_tx(&full[st], stage_bytes);
+      tma_load_3d(dst, &wmap, c.tb * (int)kTB, 0, c.pr * H + c.h, &full[st]);
+#pragma unroll
+      for (int ch = 0; ch < 2; ++ch)
+        tma_load_3d(dst + wb + ch * chb, &smap, c.tb * (int)kTB, 0, (2 * c.pr + ch) * H + c.h,
+                    &full[st]);
+    });
+    return;
+  }
   int it = 0;
   for (int t = first; t < ntiles; t += step, ++it) {
     const int sg = it % nstages;
-    if (j == 0 && t + (nstages - 1) * step < ntiles) issue(t + (nstages - 1) * step, (it + nstages - 1) % nstages);
     ptx::mbar_wait(&full[sg], (uint32_t)(it / nstages) & 1);
     const ColTile c = col_tile(t, H);
     const uint32_t tau = c.tb * kTB + j;
@@ -509,6 +535,13 @@ __global__ void __launch_bounds__(kTB)
     float2 v[M];
 #pragma unroll
     for (int a = 0; a < M; ++a) v[a] = cx_load(sw + a * kTB + j);
+    float s0[M], s1[M];
+#pragma unroll
+    for (int r = 0; r < M; ++r) {
+      s0[r] = r < rows ? tof(sk[r * kTB + j]) : 0.f;
+      s1[r] = r < rows ? tof(sk[(rows + r) * kTB + j]) : 0.f;
+    }
+    mbar_arrive_cta(&empty[sg]);
     apply_tw_g<+1, M>(v, tab_g, tau);
     dft_reg<+1, M>(v);
     const int b0 = 2 * c.pr, b1 = b0 + 1;
@@ -519,11 +552,10 @@ __global__ void __launch_bounds__(kTB)
     for (int r = 0; r < M; ++r) {
       if (r < rows) {
         const uint32_t tt = r * kL + tau;
-        st(out + o0 + tt, fmaf(d, tof(sk[r * kTB + j]), v[r].x));
-        if (has1) st(out + o1 + tt, fmaf(d, tof(sk[(rows + r) * kTB + j]), v[r].y));
+        st(out + o0 + tt, fmaf(d, s0[r], v[r].x));
+        if (has1) st(out + o1 + tt, fmaf(d, s1[r], v[r].y));
       }
     }
-    __syncthreads();
   }
 }
 
@@ -1025,8 +1057,8 @@ uint32_t launch_pass1(const fb_plan* p, const IO* a, const IO* b, CxT<ST>* oa, C
         constexpr int M = decltype(mc)::value;
         auto k = tp_col1_kernel<IO, ST, M, SRC>;
         cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(stage * ns));
-        k<<<grid, kTB, stage * ns, s>>>(am, bm, oa, ob, ddpart, p->tw_n, (int)p->H, npairs, rows,
-                                        ntiles, ns);
+        k<<<grid, kTB + 32, stage * ns, s>>>(am, bm, oa, ob, ddpart, p->tw_n, (int)p->H, npairs,
+                                             rows, ntiles, ns);
       });
       if (maps) return kL / kTB;
     }
@@ -1102,8 +1134,8 @@ void launch_pass3(const fb_plan* p, const CxT<ST>* w, const IO* skip, IO* out, f
         constexpr int M = decltype(mc)::value;
         auto k = tp_col3_kernel<ST, IO, M>;
         cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(stage * ns));
-        k<<<grid, kTB, stage * ns, s>>>(wm, sm, out, p->d, p->tw_n, B, (int)p->H, (uint32_t)p->N,
-                                        rows, ntiles, ns);
+        k<<<grid, kTB + 32, stage * ns, s>>>(wm, sm, out, p->d, p->tw_n, B, (int)p->H,
+                                             (uint32_t)p->N, rows, ntiles, ns);
       });
       if (maps) return;  // else: the register column kernel below
     }
