@@ -182,6 +182,7 @@ int fb_plan_destroy(fb_plan* p) {
   cudaFree(p->d);
   cudaFree(p->tc_mats);
   cudaFree(p->kf_tc);
+  cudaFree(p->tcr_mats);
   cudaFree(p->kf_scale);
   delete p;
   return FB_OK;

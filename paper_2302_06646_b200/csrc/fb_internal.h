@@ -27,6 +27,7 @@ struct fb_plan {
   void* tc_mats = nullptr;   // DFT blocks in UMMA smem images
   void* kf_tc = nullptr;     // k_f' = k_f + D/n as fp16 pairs [H][f1 64][f2 128], scaled
   float* kf_scale = nullptr; // [H] inverse of that per-head power-of-two scale
+  void* tcr_mats = nullptr;  // three-pass rows on tcgen05: DFT blocks (fb_single_tc.cu)
   bool prepared = false;
   bool use_keep = false;
   double lambda = 0.0, keep_scale = 1.0;
@@ -72,6 +73,13 @@ int encode_map_3d(CUtensorMap* map, CUtensorMapDataType type, const void* ptr, c
 
 // tcgen05 single-pass (fb_single_tc.cu)
 bool tc_eligible(const fb_plan* p);
+// three-pass pass 2 on tcgen05 (bf16, m <= 16): planar rows in, interleaved out
+bool tc_rows_eligible(const fb_plan* p);
+int tc_rows_fwd(fb_plan* p, void* x1, void* usave, int64_t npairs, cudaStream_t s);
+// backward rows (saved U): planar dy rows in, du rows out in place, wdk = IFFT_l(dK spectrum)
+int tc_rows_spectrum(fb_plan* p, void* x1, int64_t npairs, cudaStream_t s);  // U in place
+int tc_rows_bwd(fb_plan* p, void* x1dy, const void* usave, float2* wdk, int64_t npairs,
+                cudaStream_t s);
 int tc_init(fb_plan* p);
 // usave (optional): the forward writes U = F(u) there (tc_saved_size bytes)
 // and the backward reads it instead of recomputing (u may then be null)

@@ -27,6 +27,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <type_traits>
 #include <vector>
@@ -135,6 +136,16 @@ template <>
 __device__ __forceinline__ uint32_t pack2<__half>(float a, float b) {
   __half2 h = __floats2half2_rn(a, b);
   return *reinterpret_cast<uint32_t*>(&h);
+}
+template <typename T>
+__device__ __forceinline__ float2 unpack2(uint32_t v);
+template <>
+__device__ __forceinline__ float2 unpack2<__nv_bfloat16>(uint32_t v) {
+  return __bfloat1622float2(*reinterpret_cast<__nv_bfloat162*>(&v));
+}
+template <>
+__device__ __forceinline__ float2 unpack2<__half>(uint32_t v) {
+  return __half22float2(*reinterpret_cast<__half2*>(&v));
 }
 template <typename T>
 __device__ __forceinline__ void st8(unsigned char* p, const float* v) {
@@ -375,6 +386,47 @@ __device__ __forceinline__ void mma_stage_Ap(const Ctx& c) {
   }
 }
 
+// ---- three-pass rows (pass 2): full complex rows, no causal pruning.
+// Stage-A block FA split in its two k-blocks around FR / FI, so the FR / FI
+// offsets of the single-pass map still hold: [FA re-k | FR | FI | FA im-k].
+namespace rows {
+constexpr uint32_t SOP = 0;  // [slot] three 16 KB planes; the input row lands in planes 1-2
+constexpr uint32_t SMAT = 2 * 49152;
+constexpr uint32_t FA_KB1 = 81920, MAT_BYTES = 98304;
+constexpr uint32_t STAB = SMAT + MAT_BYTES;
+constexpr uint32_t SMEM = STAB + 1536;
+// backward: Kf2 row as bf16 pairs [f2 128][f1 64], 16-byte chunks XOR-swizzled by f2 & 7
+constexpr uint32_t SKF = SMEM;
+constexpr uint32_t SMEM_BWD = SKF + 32768;
+}  // namespace rows
+
+// A (full): DFT64 over all t1; data = MN-major A operand [mb 2][kg 16][8][64]
+// (kg 0-7 re plane, 8-15 im plane), K = 128
+template <typename T>
+__device__ __forceinline__ void mma_stage_A_full(const Ctx& c) {
+  const uint32_t id = idesc<T>(128, 128, true, false);
+#pragma unroll
+  for (uint32_t s = 0; s < 8; ++s) {
+    const uint64_t ad = tc::smem_desc(c.smb + c.in_off + s * 2048, 1024, tc::kSw128, 16384);
+    const uint64_t bd =
+        tc::smem_desc(c.smb + c.smat + (s >> 2) * rows::FA_KB1 + (s & 3) * 32, 1024, tc::kSw128);
+    tc::mma_bf16(c.tmem + c.tw, ad, bd, id, s);
+  }
+}
+// A' (full): IDFT64 over f1 to all t1 (N = 128: t1 re | t1 im, the two FA
+// k-blocks read MN-major)
+template <typename T>
+__device__ __forceinline__ void mma_stage_Ap_full(const Ctx& c) {
+  const uint32_t id = idesc<T>(128, 128, false, true);
+#pragma unroll
+  for (uint32_t s = 0; s < 8; ++s) {
+    const uint64_t ad =
+        tc::smem_desc(c.smb + c.sop + (s >> 2) * 16384 + (s & 3) * 32, 1024, tc::kSw128);
+    const uint64_t bd = tc::smem_desc(c.smb + c.smat + s * 2048, 1024, tc::kSw128, rows::FA_KB1);
+    tc::mma_bf16(c.tmem + c.tw, ad, bd, id, s);
+  }
+}
+
 #ifdef FB_TC_TIMING
 // experiment only: per (cta, slot, stage) cycle sums of epilogue / slot sync /
 // MMA issue / MMA completion, read back through fb_debug_tc_timing()
@@ -407,12 +459,12 @@ __device__ __forceinline__ void issue(Ctx& c, int stage, const Hook& hook = Hook
   const bool tl = slot_leader() && blockIdx.x < 148;
   const uint32_t ts = (blockIdx.x * 2 + (threadIdx.x / kSlotThreads));
   unsigned long long t0 = clock64();
-  if (tl && g_last[ts]) g_tc_timing[ts * 32 + stage] += t0 - g_last[ts];
+  if (tl && g_last[ts]) g_tc_timing[ts * 32 + (stage & 3)] += t0 - g_last[ts];
 #endif
   publish(c);
 #ifdef FB_TC_TIMING
   unsigned long long t1 = clock64();
-  if (tl) g_tc_timing[ts * 32 + 4 + stage] += t1 - t0;
+  if (tl) g_tc_timing[ts * 32 + 4 + (stage & 3)] += t1 - t0;
 #endif
   if (slot_leader()) {
     const uint32_t j = c.nb - c.seg0;
@@ -425,7 +477,9 @@ __device__ __forceinline__ void issue(Ctx& c, int stage, const Hook& hook = Hook
       case 0: mma_stage_A<T>(c); break;
       case 1: mma_stage_B<T, false, W3>(c); break;
       case 2: mma_stage_B<T, true, W3>(c); break;
-      default: mma_stage_Ap<T>(c); break;
+      case 3: mma_stage_Ap<T>(c); break;
+      case 4: mma_stage_A_full<T>(c); break;
+      default: mma_stage_Ap_full<T>(c); break;
     }
     tc::commit(c.mma_bar);
     hook();
@@ -433,13 +487,13 @@ __device__ __forceinline__ void issue(Ctx& c, int stage, const Hook& hook = Hook
   ++c.nb;
 #ifdef FB_TC_TIMING
   unsigned long long t2 = clock64();
-  if (tl) g_tc_timing[ts * 32 + 8 + stage] += t2 - t1;
+  if (tl) g_tc_timing[ts * 32 + 8 + (stage & 3)] += t2 - t1;
 #endif
   mma_wait(c);
 #ifdef FB_TC_TIMING
   unsigned long long t3 = clock64();
   if (tl) {
-    g_tc_timing[ts * 32 + 12 + stage] += t3 - t2;
+    g_tc_timing[ts * 32 + 12 + (stage & 3)] += t3 - t2;
     g_last[ts] = t3;
   }
 #endif
@@ -537,14 +591,14 @@ __device__ __forceinline__ void store_rows(const Ctx& c, T* __restrict__ out, in
 __device__ __forceinline__ void setup(unsigned char* sm, uint32_t* tmem_slot, uint64_t* bars,
                                       int nbars, int nbars_slot, const uint4* __restrict__ mats,
                                       const float2* __restrict__ tab_g, uint32_t smat = SMAT,
-                                      uint32_t stab = STAB) {
+                                      uint32_t stab = STAB, uint32_t mat_bytes = MAT_BYTES) {
   if (threadIdx.x < 32) tc::alloc<512>(tmem_slot);
   if (threadIdx.x == 0) {
     for (int i = 0; i < nbars; ++i) ptx::mbar_init(&bars[i], i < nbars - nbars_slot ? 1 : kSlotThreads);
     ptx::fence_barrier_init();
   }
   uint4* dm = reinterpret_cast<uint4*>(sm + smat);
-  for (uint32_t i = threadIdx.x; i < MAT_BYTES / 16; i += kThreads) dm[i] = __ldg(mats + i);
+  for (uint32_t i = threadIdx.x; i < mat_bytes / 16; i += kThreads) dm[i] = __ldg(mats + i);
   float2* tab = reinterpret_cast<float2*>(sm + stab);
   for (uint32_t i = threadIdx.x; i < 192; i += kThreads) tab[i] = __ldg(tab_g + i);
   ptx::fence_proxy_async_smem();
@@ -884,6 +938,334 @@ __global__ void __launch_bounds__(kThreads, 1)
   teardown(tmem_slot);
 }
 
+// ------------------------------------------------------------------ three-pass rows
+// Pass 2 of the three-pass engine (fb_three.cu, middle_block of
+// three_pass.cpp:211-221) on the tensor cores: row X1[(pr H + h) m + a] is a
+// full complex length-8192 cyclic convolution W = IFFT(FFT(x) Kf2[h][a]) —
+// the single-pass Monarch without the causal pruning (stage A K = 128, stage
+// A' N = 128).  The row arrives planar ([re 8192 | im 8192] 16-bit, pass 1
+// writes it so) by TMA straight into stage A's MN-major operand in the slot's
+// operand planes 1-2 (dead until the A exit); W leaves interleaved (re, im)
+// in place for pass 3; U = FFT(x) (natural order f = f1 + 64 f2) is kept for
+// the backward.  Items run (h a)-major, pairs inner, so a slot reloads its
+// Kf2 row (fp32, into TMEM) once per npairs / 2 rows.
+__device__ __forceinline__ void load_row(unsigned char* dst, const CUtensorMap* map, int row,
+                                         uint64_t* bar) {
+  ptx::mbar_arrive_expect_tx(bar, 32768);
+#pragma unroll
+  for (int mb = 0; mb < 2; ++mb)
+#pragma unroll
+    for (int pl = 0; pl < 2; ++pl) tma_load_4d(dst + mb * 16384 + pl * 8192, map, mb * 64, 0, pl, row, bar);
+}
+
+__device__ __forceinline__ void load_kf_rows(const Ctx& c, const float2* __restrict__ kf) {
+  uint32_t f2, g;
+  coords(f2, g);
+  const uint32_t cb = kColsPer * g;
+  const float4* src = reinterpret_cast<const float4*>(kf + 64 * f2 + cb);
+  float re[16], im[16];
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    const float4 v = __ldg(src + j);
+    re[2 * j] = v.x;
+    im[2 * j] = v.y;
+    re[2 * j + 1] = v.z;
+    im[2 * j + 1] = v.w;
+  }
+  tst8(taddr(c, c.aux + cb), re);
+  tst8(taddr(c, c.aux + cb + 8), re + 8);
+  tst8(taddr(c, c.aux + 64 + cb), im);
+  tst8(taddr(c, c.aux + 64 + cb + 8), im + 8);
+  tst_wait();
+}
+
+// SPEC: spectrum only (U = FFT(x) to usave, which may alias x1: the row is
+// in smem before its spectrum is written) — the backward's recompute path.
+template <typename T, bool SPEC = false>
+__global__ void __launch_bounds__(kThreads, 1)
+    tc_rows_fwd_kernel(const __grid_constant__ CUtensorMap xmap, uint32_t* __restrict__ x1,
+                       const float2* __restrict__ kf2, const uint4* __restrict__ mats,
+                       const float2* __restrict__ tab_g, int npairs, int hm, int total,
+                       uint32_t* __restrict__ usave) {
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  __shared__ uint32_t tmem_slot;
+  __shared__ __align__(8) uint64_t bars[4];  // mma[2], in[2]
+  unsigned char* sm = smem_base(smem_raw);
+  int i0, i1;
+  cta_range(total, i0, i1);
+  setup(sm, &tmem_slot, bars, 4, 0, mats, tab_g, rows::SMAT, rows::STAB, rows::MAT_BYTES);
+  const uint32_t slot = threadIdx.x / kSlotThreads;
+  Ctx c = make_ctx(sm, tmem_slot, slot, &bars[slot], true);
+  c.sop = rows::SOP + 49152 * slot;
+  c.in_off = c.sop + 16384;
+  c.smat = rows::SMAT;
+  c.tab = reinterpret_cast<const float2*>(sm + rows::STAB);
+  c.aux = TKF + 128 * slot;
+  c.on = (SPEC ? 2u : 4u) * (uint32_t)((i1 - i0 + (int)slot) / 2);
+  uint64_t* in_bar = &bars[2 + slot];
+  const bool lead = slot_leader();
+  auto row_of = [&](int item) { return (item % npairs) * hm + item / npairs; };
+  int item = i0 + (int)slot;
+  if (lead && item < i1) load_row(sm + c.in_off, &xmap, row_of(item), in_bar);
+  int cur = -1;
+  for (uint32_t it = 0; item < i1; item += 2, ++it) {
+    const int ha = item / npairs;
+    const size_t row = (size_t)row_of(item);
+    if (!SPEC && ha != cur) {
+      load_kf_rows(c, kf2 + (size_t)ha * kN);
+      cur = ha;
+    }
+    ptx::mbar_wait(in_bar, it & 1);
+    issue<T, true>(c, 4);
+    epi_A_exit<T, true>(c);
+    issue<T, true>(c, 1);
+    if constexpr (SPEC) {
+      if (lead && item + 2 < i1) load_row(sm + c.in_off, &xmap, row_of(item + 2), in_bar);
+      uint32_t f2, g;
+      coords(f2, g);
+#pragma unroll
+      for (uint32_t q = 0; q < kColsPer / 8; ++q) {
+        const uint32_t cb = kColsPer * g + 8 * q;
+        float re[8], im[8];
+        tld<8>(taddr(c, c.tw + cb), re);
+        tld<8>(taddr(c, c.tw + 64 + cb), im);
+        tc::ld_wait();
+        uint4* us = reinterpret_cast<uint4*>(usave + row * kN + 64 * f2 + cb);
+        us[0] = make_uint4(pack2<T>(re[0], im[0]), pack2<T>(re[1], im[1]), pack2<T>(re[2], im[2]),
+                           pack2<T>(re[3], im[3]));
+        us[1] = make_uint4(pack2<T>(re[4], im[4]), pack2<T>(re[5], im[5]), pack2<T>(re[6], im[6]),
+                           pack2<T>(re[7], im[7]));
+      }
+      continue;
+    }
+    {  // B exit: U -> usave; Z = U Kf2 -> planes [Zr | Zi | -Zr]
+      uint32_t f2, g;
+      coords(f2, g);
+      unsigned char* op = c.sm + c.sop;
+#pragma unroll
+      for (uint32_t q = 0; q < kColsPer / 8; ++q) {
+        const uint32_t cb = kColsPer * g + 8 * q;
+        float re[8], im[8], kr[8], ki[8];
+        tld<8>(taddr(c, c.tw + cb), re);
+        tld<8>(taddr(c, c.tw + 64 + cb), im);
+        tld<8>(taddr(c, c.aux + cb), kr);
+        tld<8>(taddr(c, c.aux + 64 + cb), ki);
+        tc::ld_wait();
+        if (usave) {
+          uint4* us = reinterpret_cast<uint4*>(usave + row * kN + 64 * f2 + cb);
+          us[0] = make_uint4(pack2<T>(re[0], im[0]), pack2<T>(re[1], im[1]), pack2<T>(re[2], im[2]),
+                             pack2<T>(re[3], im[3]));
+          us[1] = make_uint4(pack2<T>(re[4], im[4]), pack2<T>(re[5], im[5]), pack2<T>(re[6], im[6]),
+                             pack2<T>(re[7], im[7]));
+        }
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          const float a = re[j], b = im[j];
+          re[j] = fmaf(a, kr[j], -b * ki[j]);
+          im[j] = fmaf(a, ki[j], b * kr[j]);
+        }
+        st8<T>(op + off_bmn(cb, f2), re);
+        st8<T>(op + 16384 + off_bmn(cb, f2), im);
+        st8n<T>(op + 32768 + off_bmn(cb, f2), re);
+      }
+    }
+    issue<T, true>(c, 2);
+    epi_Bp_exit<T>(c);
+    issue<T, true>(c, 5);
+    // the operand planes are free again: the slot's next row streams in
+    // while this one is stored
+    if (lead && item + 2 < i1) load_row(sm + c.in_off, &xmap, row_of(item + 2), in_bar);
+    {  // A' exit: W[128 t1 + t2] (re, im) for t1 = 16 g + j
+      uint32_t t2, g;
+      coords(t2, g);
+      float re[16], im[16];
+      tld<16>(taddr(c, c.tw + 16 * g), re);
+      tld<16>(taddr(c, c.tw + 64 + 16 * g), im);
+      tc::ld_wait();
+      uint32_t* o = x1 + row * kN + 128 * (16 * g) + t2;
+#pragma unroll
+      for (int j = 0; j < 16; ++j) o[128 * j] = pack2<T>(re[j], im[j]);
+    }
+  }
+  teardown(tmem_slot);
+}
+
+// Backward rows (tp_pass2_bwd_kernel's contract, saved-U form): CTA c owns
+// the (h a) row groups [g0, g1); in a group slot s takes pairs s, s+2, ...:
+//   DY = FFT(x1dy row)  (stage A full, B)
+//   acc_s += conj(U) DY   (U = the forward's saved spectrum; acc_s fp32 in TMEM)
+//   du row = IFFT(DY conj(Kf2))  (B', A'), interleaved, in place
+// At the group end slot 0 sums acc_0 + acc_1 (fixed order: deterministic)
+// and runs it through B', A' into wdk[h a] (fp32, natural t), while slot 1
+// starts the next group.
+__device__ __forceinline__ uint32_t kf_swz(uint32_t f2, uint32_t f1) {
+  return f2 * 64 + ((((f1 >> 2) ^ (f2 & 7)) << 2) | (f1 & 3));
+}
+
+template <typename T>
+__global__ void __launch_bounds__(kThreads, 1)
+    tc_rows_bwd_kernel(const __grid_constant__ CUtensorMap xmap, uint32_t* __restrict__ x1dy,
+                       const uint32_t* __restrict__ usave, const float2* __restrict__ kf2,
+                       float2* __restrict__ wdk, const uint4* __restrict__ mats,
+                       const float2* __restrict__ tab_g, int npairs, int hm) {
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  __shared__ uint32_t tmem_slot;
+  __shared__ __align__(8) uint64_t bars[4];  // mma[2], in[2]
+  unsigned char* sm = smem_base(smem_raw);
+  int g0, g1;
+  cta_range(hm, g0, g1);
+  setup(sm, &tmem_slot, bars, 4, 0, mats, tab_g, rows::SMAT, rows::STAB, rows::MAT_BYTES);
+  const uint32_t slot = threadIdx.x / kSlotThreads;
+  Ctx c = make_ctx(sm, tmem_slot, slot, &bars[slot], true);
+  c.sop = rows::SOP + 49152 * slot;
+  c.in_off = c.sop + 16384;
+  c.smat = rows::SMAT;
+  c.tab = reinterpret_cast<const float2*>(sm + rows::STAB);
+  c.aux = 256 + 128 * slot;  // acc_s
+  uint64_t* in_bar = &bars[2 + slot];
+  const bool lead = slot_leader();
+  uint32_t* kfs = reinterpret_cast<uint32_t*>(sm + rows::SKF);
+  auto load_kf = [&](int ha, uint32_t t0, uint32_t nt) {
+    const float4* src = reinterpret_cast<const float4*>(kf2 + (size_t)ha * kN);
+    for (uint32_t i = t0; i < kN / 2; i += nt) {
+      const float4 v = __ldg(src + i);
+      const uint32_t f = 2 * i;
+      kfs[kf_swz(f >> 6, f & 63)] = pack2<T>(v.x, v.y);
+      kfs[kf_swz(f >> 6, (f & 63) + 1)] = pack2<T>(v.z, v.w);
+    }
+  };
+  {  // acc_s = 0, first Kf2 row
+    uint32_t f2, g;
+    coords(f2, g);
+    const float z[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+    for (uint32_t q = 0; q < 2; ++q) {
+      tst8(taddr(c, c.aux + kColsPer * g + 8 * q), z);
+      tst8(taddr(c, c.aux + 64 + kColsPer * g + 8 * q), z);
+    }
+    tst_wait();
+    if (g0 < g1) load_kf(g0, threadIdx.x, kThreads);
+  }
+  uint32_t in_cnt = 0;
+  cta_sync_tc();  // first Kf2 row in smem, accumulators zeroed
+  for (int ha = g0; ha < g1; ++ha) {
+    if (lead && (int)slot < npairs) load_row(sm + c.in_off, &xmap, (int)slot * hm + ha, in_bar);
+    for (int j = (int)slot; j < npairs; j += 2) {
+      const size_t row = (size_t)j * hm + ha;
+      ptx::mbar_wait(in_bar, in_cnt & 1);
+      ++in_cnt;
+      issue<T, true>(c, 4);
+      epi_A_exit<T, true>(c);
+      uint32_t f2, g;
+      coords(f2, g);
+      // U in flight while the stage-B MMAs run
+      uint4 up[4];
+      {
+        const uint4* us = reinterpret_cast<const uint4*>(usave + row * kN + 64 * f2 + kColsPer * g);
+#pragma unroll
+        for (int i = 0; i < 4; ++i) up[i] = __ldg(us + i);
+      }
+      issue<T, true>(c, 1);
+      {
+        unsigned char* op = c.sm + c.sop;
+#pragma unroll
+        for (uint32_t q = 0; q < 2; ++q) {
+          const uint32_t cb = kColsPer * g + 8 * q;
+          float dr[8], di[8], ar[8], ai[8];
+          tld<8>(taddr(c, c.tw + cb), dr);
+          tld<8>(taddr(c, c.tw + 64 + cb), di);
+          tld<8>(taddr(c, c.aux + cb), ar);
+          tld<8>(taddr(c, c.aux + 64 + cb), ai);
+          const uint4 k0 = *reinterpret_cast<const uint4*>(kfs + kf_swz(f2, cb));
+          const uint4 k1 = *reinterpret_cast<const uint4*>(kfs + kf_swz(f2, cb + 4));
+          tc::ld_wait();
+          const uint32_t uw[8] = {up[2 * q].x, up[2 * q].y, up[2 * q].z, up[2 * q].w,
+                                  up[2 * q + 1].x, up[2 * q + 1].y, up[2 * q + 1].z, up[2 * q + 1].w};
+          const uint32_t kw[8] = {k0.x, k0.y, k0.z, k0.w, k1.x, k1.y, k1.z, k1.w};
+#pragma unroll
+          for (int jj = 0; jj < 8; ++jj) {
+            const float2 u = unpack2<T>(uw[jj]), k = unpack2<T>(kw[jj]);
+            const float a = dr[jj], b = di[jj];
+            ar[jj] = fmaf(u.x, a, fmaf(u.y, b, ar[jj]));   // acc += conj(U) DY
+            ai[jj] = fmaf(u.x, b, fmaf(-u.y, a, ai[jj]));
+            dr[jj] = fmaf(a, k.x, b * k.y);                 // Z = DY conj(Kf2)
+            di[jj] = fmaf(b, k.x, -a * k.y);
+          }
+          tst8(taddr(c, c.aux + cb), ar);
+          tst8(taddr(c, c.aux + 64 + cb), ai);
+          st8<T>(op + off_bmn(cb, f2), dr);  // planes [Zr | Zi | -Zr]
+          st8<T>(op + 16384 + off_bmn(cb, f2), di);
+          st8n<T>(op + 32768 + off_bmn(cb, f2), dr);
+        }
+        tst_wait();
+      }
+      issue<T, true>(c, 2);
+      epi_Bp_exit<T>(c);
+      issue<T, true>(c, 5);
+      if (lead && j + 2 < npairs) load_row(sm + c.in_off, &xmap, (j + 2) * hm + ha, in_bar);
+      {
+        uint32_t t2, gg;
+        coords(t2, gg);
+        float re[16], im[16];
+        tld<16>(taddr(c, c.tw + 16 * gg), re);
+        tld<16>(taddr(c, c.tw + 64 + 16 * gg), im);
+        tc::ld_wait();
+        uint32_t* o = x1dy + row * kN + 128 * (16 * gg) + t2;
+#pragma unroll
+        for (int jj = 0; jj < 16; ++jj) o[128 * jj] = pack2<T>(re[jj], im[jj]);
+      }
+    }
+    cta_sync_tc();  // acc_0, acc_1 complete
+    if (slot == 0) {  // acc_0 + acc_1 -> B' operand planes; zero both accumulators
+      uint32_t f2, g;
+      coords(f2, g);
+      unsigned char* op = c.sm + c.sop;
+      const float z[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+      for (uint32_t q = 0; q < 2; ++q) {
+        const uint32_t cb = kColsPer * g + 8 * q;
+        float r0[8], i0[8], r1[8], i1[8];
+        tld<8>(taddr(c, 256 + cb), r0);
+        tld<8>(taddr(c, 256 + 64 + cb), i0);
+        tld<8>(taddr(c, 384 + cb), r1);
+        tld<8>(taddr(c, 384 + 64 + cb), i1);
+        tc::ld_wait();
+#pragma unroll
+        for (int jj = 0; jj < 8; ++jj) {
+          r0[jj] += r1[jj];
+          i0[jj] += i1[jj];
+        }
+        st8<T>(op + off_bmn(cb, f2), r0);
+        st8<T>(op + 16384 + off_bmn(cb, f2), i0);
+        st8n<T>(op + 32768 + off_bmn(cb, f2), r0);
+        tst8(taddr(c, 256 + cb), z);
+        tst8(taddr(c, 256 + 64 + cb), z);
+        tst8(taddr(c, 384 + cb), z);
+        tst8(taddr(c, 384 + 64 + cb), z);
+      }
+      tst_wait();
+    } else if (ha + 1 < g1) {
+      load_kf(ha + 1, threadIdx.x - kSlotThreads, kSlotThreads);
+    }
+    cta_sync_tc();  // accumulators consumed, next Kf2 row in smem
+    if (slot == 0) {  // dK spectrum row -> IFFT -> wdk (fp32)
+      issue<T, true>(c, 2);
+      epi_Bp_exit<T>(c);
+      issue<T, true>(c, 5);
+      uint32_t t2, gg;
+      coords(t2, gg);
+      float re[16], im[16];
+      tld<16>(taddr(c, c.tw + 16 * gg), re);
+      tld<16>(taddr(c, c.tw + 64 + 16 * gg), im);
+      tc::ld_wait();
+      float2* o = wdk + (size_t)ha * kN + 128 * (16 * gg) + t2;
+#pragma unroll
+      for (int jj = 0; jj < 16; ++jj) o[128 * jj] = make_float2(re[jj], im[jj]);
+    }
+  }
+  teardown(tmem_slot);
+}
+
 }  // namespace tcfft
 
 // ---------------------------------------------------------------- host side
@@ -1076,6 +1458,120 @@ int tc_bwd(fb_plan* p, const void* dy, const void* u, void* du, float* dK, float
   if (rc) return rc;
   const SpartMap m{gr.bctas, gr.total, gr.npairs, gr.maxseg, 1};
   return sp_finalize(p, spart, nullptr, 0, dKbar, dD, dK, 1, &m, s);
+}
+
+// ---------------------------------------------------------------- three-pass rows (host)
+namespace {
+template <typename T>
+std::vector<uint8_t> build_mats_rows() {
+  std::vector<uint8_t> img(rows::MAT_BYTES, 0);
+  // stage A (full): rows f1 re (0..63) | im (64..127); k t1 re (0..63, k-block
+  // at 0) | t1 im (64..127, k-block at FA_KB1)
+  for (int r = 0; r < 128; ++r) {
+    const int f1 = r % 64;
+    const bool imag = r >= 64;
+    for (int t1 = 0; t1 < 64; ++t1) {
+      const double a = -2.0 * M_PI * (double)((f1 * t1) % 64) / 64.0;
+      const double fr = std::cos(a), fi = std::sin(a);
+      put<T>(img, off_kmaj(r, t1, 0), imag ? fi : fr);
+      put<T>(img, rows::FA_KB1 + off_kmaj(r, t1, 0), imag ? fr : -fi);
+    }
+  }
+  for (int r = 0; r < 128; ++r)
+    for (int k = 0; k < 128; ++k) {
+      const double a = -2.0 * M_PI * (double)((r * k) % 128) / 128.0;
+      put<T>(img, MAT_FR + off_kmaj(r, k, 16384), std::cos(a));
+      put<T>(img, MAT_FI + off_kmaj(r, k, 16384), std::sin(a));
+    }
+  return img;
+}
+
+// planar rows [R][2 planes][64 t1][128 t2] 16-bit; box [64 t2][64 t1][1][1]
+template <typename T>
+int make_rows_map(CUtensorMap* map, const void* ptr, int64_t R) {
+  EncodeFn enc = encode_fn();
+  if (!enc) {
+    set_error("tcgen05 rows: cuTensorMapEncodeTiled unavailable");
+    return FB_ERR_CUDA;
+  }
+  const cuuint64_t dims[4] = {128, 64, 2, (cuuint64_t)R};
+  const cuuint64_t strides[3] = {128 * 2, 8192 * 2, 16384 * 2};
+  const cuuint32_t box[4] = {64, 64, 1, 1};
+  const cuuint32_t es[4] = {1, 1, 1, 1};
+  CUresult r = enc(map, Fmt<T>::tma, 4, const_cast<void*>(ptr), dims, strides, box, es,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) {
+    set_error("cuTensorMapEncodeTiled (rows) failed (" + std::to_string((int)r) + ")");
+    return FB_ERR_CUDA;
+  }
+  return FB_OK;
+}
+}  // namespace
+
+bool tc_rows_eligible(const fb_plan* p) {
+  static const int off = [] {
+    const char* e = std::getenv("FB_ROWS_TC");
+    return e && e[0] == '0';
+  }();
+  return !off && p->dtype == FB_BF16 && p->l == 8192 && p->m <= 16;
+}
+
+// x1: npairs x H x m planar bf16 rows in, interleaved (re, im) rows out
+static int rows_mats(fb_plan* p) {
+  if (p->tcr_mats) return FB_OK;
+  std::vector<uint8_t> img = build_mats_rows<__nv_bfloat16>();
+  int rc = cuda_status(cudaMalloc(&p->tcr_mats, img.size()), "cudaMalloc(tc rows mats)");
+  if (!rc)
+    rc = cuda_status(cudaMemcpy(p->tcr_mats, img.data(), img.size(), cudaMemcpyHostToDevice),
+                     "copy tc rows mats");
+  return rc;
+}
+
+int tc_rows_fwd(fb_plan* p, void* x1, void* usave, int64_t npairs, cudaStream_t s) {
+  if (int rc = rows_mats(p)) return rc;
+  const int hm = (int)(p->H * p->m);
+  const int total = (int)(npairs * hm);
+  CUtensorMap map;
+  int rc = make_rows_map<__nv_bfloat16>(&map, x1, total);
+  if (rc) return rc;
+  auto k = tc_rows_fwd_kernel<__nv_bfloat16>;
+  cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rows::SMEM);
+  const int ctas = std::max(1, std::min(p->num_sms, total));
+  k<<<(unsigned)ctas, kThreads, rows::SMEM, s>>>(map, (uint32_t*)x1, p->kf, (const uint4*)p->tcr_mats,
+                                                 p->tw_l, (int)npairs, hm, total, (uint32_t*)usave);
+  return cuda_status(cudaGetLastError(), "tc_rows_fwd");
+}
+
+int tc_rows_spectrum(fb_plan* p, void* x1, int64_t npairs, cudaStream_t s) {
+  if (int rc = rows_mats(p)) return rc;
+  const int hm = (int)(p->H * p->m);
+  const int total = (int)(npairs * hm);
+  CUtensorMap map;
+  int rc = make_rows_map<__nv_bfloat16>(&map, x1, total);
+  if (rc) return rc;
+  auto k = tc_rows_fwd_kernel<__nv_bfloat16, true>;
+  cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rows::SMEM);
+  const int ctas = std::max(1, std::min(p->num_sms, total));
+  k<<<(unsigned)ctas, kThreads, rows::SMEM, s>>>(map, (uint32_t*)x1, p->kf, (const uint4*)p->tcr_mats,
+                                                 p->tw_l, (int)npairs, hm, total, (uint32_t*)x1);
+  return cuda_status(cudaGetLastError(), "tc_rows_spectrum");
+}
+
+int tc_rows_bwd(fb_plan* p, void* x1dy, const void* usave, float2* wdk, int64_t npairs,
+                cudaStream_t s) {
+  if (int rc = rows_mats(p)) return rc;
+  const int hm = (int)(p->H * p->m);
+  CUtensorMap map;
+  int rc = make_rows_map<__nv_bfloat16>(&map, x1dy, npairs * hm);
+  if (rc) return rc;
+  auto k = tc_rows_bwd_kernel<__nv_bfloat16>;
+  cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rows::SMEM_BWD);
+  const int ctas = std::max(1, std::min(p->num_sms, hm));
+  k<<<(unsigned)ctas, kThreads, rows::SMEM_BWD, s>>>(map, (uint32_t*)x1dy, (const uint32_t*)usave,
+                                                     p->kf, wdk, (const uint4*)p->tcr_mats, p->tw_l,
+                                                     (int)npairs, hm);
+  return cuda_status(cudaGetLastError(), "tc_rows_bwd");
 }
 
 #ifdef FB_TC_TIMING

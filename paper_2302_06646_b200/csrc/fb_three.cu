@@ -402,7 +402,8 @@ __device__ __forceinline__ void col_producer(int first, int step, int ntiles, in
 // Pass 1, SRC 0: signal pairs (channels 2 pr, 2 pr + 1 -> re, im);
 // SRC 1: dy and u pairs at once, plus the lag-0 dD partial.  Signal maps view
 // [B*H][rows][l] with rows = N / l data rows (the causal pad is implicit).
-template <typename IO, typename ST, int M, int SRC>
+// PLANAR: rows leave as [re l | im l] (the tcgen05 row pass's TMA layout)
+template <typename IO, typename ST, int M, int SRC, bool PLANAR = false>
 __global__ void __launch_bounds__(kTB + 32)
     tp_col1_kernel(const __grid_constant__ CUtensorMap amap, const __grid_constant__ CUtensorMap bmap,
                    CxT<ST>* __restrict__ out_a, CxT<ST>* __restrict__ out_b,
@@ -471,8 +472,17 @@ __global__ void __launch_bounds__(kTB + 32)
     dft_reg<-1, M>(v);
     apply_tw_g<-1, M>(v, tab_g, tau);
     CxT<ST>* oa = out_a + ((size_t)c.pr * H + c.h) * (size_t)M * kL;
+    if constexpr (PLANAR) {
 #pragma unroll
-    for (int a = 0; a < M; ++a) stc<ST>(&oa[a * kL + tau].x, v[a]);
+      for (int a = 0; a < M; ++a) {
+        ST* r = reinterpret_cast<ST*>(oa + a * kL);
+        st(r + tau, v[a].x);
+        st(r + kL + tau, v[a].y);
+      }
+    } else {
+#pragma unroll
+      for (int a = 0; a < M; ++a) stc<ST>(&oa[a * kL + tau].x, v[a]);
+    }
     if constexpr (SRC == 1) {
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) dd += __shfl_xor_sync(0xffffffffu, dd, o);
@@ -1042,8 +1052,30 @@ int col_stages(size_t stage_bytes) {
 // the kernel bank, tiled smem kernel for m > 16
 template <typename IO, typename ST, int SRC>
 uint32_t launch_pass1(const fb_plan* p, const IO* a, const IO* b, CxT<ST>* oa, CxT<ST>* ob,
-                      float* ddpart, int B, int npairs, cudaStream_t s) {
+                      float* ddpart, int B, int npairs, cudaStream_t s, bool planar = false) {
   const int causal = p->mode == FB_MODE_CAUSAL;
+  if constexpr (SRC == 0) {
+    if (planar) {  // the tcgen05 row pass's input: streaming column kernel only
+      CUtensorMap am;
+      if (p->m > 16 || signal_map<IO>(&am, p, a, B)) {
+        set_error("three-pass: planar pass 1 needs m <= 16 and a signal tensor map");
+        return 0;
+      }
+      const int rows = (int)(p->N / kL);
+      const size_t stage = (size_t)2 * rows * kTB * sizeof(IO);
+      const int ns = col_stages(stage);
+      const int ntiles = (int)(npairs * p->H * (kL / kTB));
+      const int grid = std::min(ntiles, 2 * p->num_sms);
+      with_m(p->m, [&](auto mc) {
+        constexpr int M = decltype(mc)::value;
+        auto k = tp_col1_kernel<IO, ST, M, 0, true>;
+        cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(stage * ns));
+        k<<<grid, kTB + 32, stage * ns, s>>>(am, am, oa, nullptr, nullptr, p->tw_n, (int)p->H,
+                                             npairs, rows, ntiles, ns);
+      });
+      return kL / kTB;
+    }
+  }
   if constexpr (SRC != 2) {
     if (p->m <= 16) {
       CUtensorMap am, bm;
@@ -1242,10 +1274,21 @@ int tp_fwd(fb_plan* p, const void* u, void* y, int64_t B, void* ws, cudaStream_t
     set_error("three-pass: circular mode needs N == n");
     return FB_ERR_UNSUPPORTED;
   }
+  int rc = FB_OK;
   with_io(p->dtype, [&](auto io) {
     using IO = decltype(io);
     using ST = IO;
     auto* x1 = reinterpret_cast<CxT<ST>*>(ws);
+    if (tc_rows_eligible(p)) {  // pass 2 on tcgen05 (planar rows in, interleaved out)
+      if (!launch_pass1<IO, ST, 0>(p, (const IO*)u, nullptr, x1, nullptr, nullptr, (int)B,
+                                   (int)npairs, s, true)) {
+        rc = FB_ERR_UNSUPPORTED;
+        return;
+      }
+      if ((rc = tc_rows_fwd(p, x1, usave, npairs, s))) return;
+      launch_pass3<ST, IO, 0>(p, x1, (const IO*)u, (IO*)y, nullptr, (int)B, (int)npairs, 1.f, s);
+      return;
+    }
     launch_pass1<IO, ST, 0>(p, (const IO*)u, nullptr, x1, nullptr, nullptr, (int)B, (int)npairs, s);
     const size_t sm = pass2_smem<ST>();
     auto k2 = tp_pass2_kernel<ST, 0>;
@@ -1257,6 +1300,7 @@ int tp_fwd(fb_plan* p, const void* u, void* y, int64_t B, void* ws, cudaStream_t
         reinterpret_cast<CxT<ST>*>(usave));
     launch_pass3<ST, IO, 0>(p, x1, (const IO*)u, (IO*)y, nullptr, (int)B, (int)npairs, 1.f, s);
   });
+  if (rc) return rc;
   return cuda_status(cudaGetLastError(), "tp_fwd");
 }
 
@@ -1278,13 +1322,32 @@ int tp_bwd(fb_plan* p, const void* dy, const void* u, void* du, float* dK, float
   off += ((size_t)p->H * p->N * sizeof(float) + 255) & ~size_t(255);
   float* ddpart = (float*)(w + off);
   float* dkbar = dKbar ? dKbar : dkbar_s;
+  int rc = FB_OK;
+  const bool tcr = tc_rows_eligible(p);
   with_io(p->dtype, [&](auto io) {
     using IO = decltype(io);
     using ST = IO;
     auto* x1dy = reinterpret_cast<CxT<ST>*>(x1dy_raw);
     auto* x1u = reinterpret_cast<CxT<ST>*>(x1u_raw);
     const size_t sm = pass2_bwd_smem<ST>();
-    if (usave) {  // the forward's row spectra of u: pass 1 and 2 on dy only
+    if (tcr) {  // rows on tcgen05; without a saved U, recompute it (spectrum-only rows)
+      const void* us = usave;
+      if (!us) {
+        if (!launch_pass1<IO, ST, 0>(p, (const IO*)u, nullptr, x1u, nullptr, nullptr, (int)B,
+                                     (int)npairs, s, true)) {
+          rc = FB_ERR_UNSUPPORTED;
+          return;
+        }
+        if ((rc = tc_rows_spectrum(p, x1u, npairs, s))) return;
+        us = x1u;
+      }
+      if (!launch_pass1<IO, ST, 0>(p, (const IO*)dy, nullptr, x1dy, nullptr, nullptr, (int)B,
+                                   (int)npairs, s, true)) {
+        rc = FB_ERR_UNSUPPORTED;
+        return;
+      }
+      if ((rc = tc_rows_bwd(p, x1dy, us, wdk, npairs, s))) return;
+    } else if (usave) {  // the forward's row spectra of u: pass 1 and 2 on dy only
       launch_pass1<IO, ST, 0>(p, (const IO*)dy, nullptr, x1dy, nullptr, nullptr, (int)B,
                               (int)npairs, s);
       auto k2 = tp_pass2_bwd_kernel<ST, true>;
@@ -1304,11 +1367,12 @@ int tp_bwd(fb_plan* p, const void* dy, const void* u, void* du, float* dK, float
     launch_pass3<float, float, 1>(p, reinterpret_cast<const CxT<float>*>(wdk), nullptr, nullptr,
                                   dkbar, 2, 1, 1.0f / (float)p->n, s);
   });
-  if (usave)
+  if (usave || tcr)
     tp_dd_lag0_kernel<<<(unsigned)((p->H + 127) / 128), 128, 0, s>>>(dkbar, dD, (int)p->H, p->N);
   else
     tp_dd_reduce_kernel<<<(unsigned)p->H, 32, 0, s>>>(ddpart, dD, (int)(npairs * gx));
-  int rc = cuda_status(cudaGetLastError(), "tp_bwd");
+  if (rc) return rc;
+  rc = cuda_status(cudaGetLastError(), "tp_bwd");
   if (rc) return rc;
   return regularizer_backward_dev(p, dkbar, dK, s);
 }
