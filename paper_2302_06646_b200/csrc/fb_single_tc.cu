@@ -42,7 +42,7 @@ namespace fb {
 namespace tcfft {
 
 constexpr uint32_t kN = 8192;
-constexpr uint32_t kThreads = 1024;
+constexpr uint32_t kThreads = 512;
 
 // ---------------------------------------------------------------- smem map
 // Two independent 16-warp slots per CTA; each slot runs its own channel pair
@@ -57,7 +57,7 @@ constexpr uint32_t kThreads = 1024;
 //               no matrix of its own
 //   FR, FI     : DFT128 real / imaginary [128][128] K-major SW128 (2 k-blocks)
 //   KF   (bwd) : k_f' as fp16 pairs [f1 64][f2 128] x per-head scale
-constexpr uint32_t kSlotThreads = 512;
+constexpr uint32_t kSlotThreads = 256;
 // a slot's 16 warps: 4 per TMEM lane quarter, so each thread owns 1/kGroups
 // of a row's columns (16 of the 64 complex columns of a stage)
 constexpr uint32_t kGroups = kSlotThreads / 128;
@@ -458,13 +458,14 @@ __device__ __forceinline__ void issue(Ctx& c, int stage, const Hook& hook = Hook
 #ifdef FB_TC_TIMING
   const bool tl = slot_leader() && blockIdx.x < 148;
   const uint32_t ts = (blockIdx.x * 2 + (threadIdx.x / kSlotThreads));
+  const int sx = stage == 4 ? 0 : (stage == 5 ? 3 : stage);
   unsigned long long t0 = clock64();
-  if (tl && g_last[ts]) g_tc_timing[ts * 32 + (stage & 3)] += t0 - g_last[ts];
+  if (tl && g_last[ts]) g_tc_timing[ts * 32 + sx] += t0 - g_last[ts];
 #endif
   publish(c);
 #ifdef FB_TC_TIMING
   unsigned long long t1 = clock64();
-  if (tl) g_tc_timing[ts * 32 + 4 + (stage & 3)] += t1 - t0;
+  if (tl) g_tc_timing[ts * 32 + 4 + sx] += t1 - t0;
 #endif
   if (slot_leader()) {
     const uint32_t j = c.nb - c.seg0;
@@ -487,13 +488,13 @@ __device__ __forceinline__ void issue(Ctx& c, int stage, const Hook& hook = Hook
   ++c.nb;
 #ifdef FB_TC_TIMING
   unsigned long long t2 = clock64();
-  if (tl) g_tc_timing[ts * 32 + 8 + (stage & 3)] += t2 - t1;
+  if (tl) g_tc_timing[ts * 32 + 8 + sx] += t2 - t1;
 #endif
   mma_wait(c);
 #ifdef FB_TC_TIMING
   unsigned long long t3 = clock64();
   if (tl) {
-    g_tc_timing[ts * 32 + 12 + (stage & 3)] += t3 - t2;
+    g_tc_timing[ts * 32 + 12 + sx] += t3 - t2;
     g_last[ts] = t3;
   }
 #endif
@@ -953,29 +954,30 @@ __device__ __forceinline__ void load_row(unsigned char* dst, const CUtensorMap* 
                                          uint64_t* bar) {
   ptx::mbar_arrive_expect_tx(bar, 32768);
 #pragma unroll
-  for (int mb = 0; mb < 2; ++mb)
-#pragma unroll
-    for (int pl = 0; pl < 2; ++pl) tma_load_4d(dst + mb * 16384 + pl * 8192, map, mb * 64, 0, pl, row, bar);
+  for (int mb = 0; mb < 2; ++mb) tma_load_4d(dst + mb * 16384, map, mb * 64, 0, 0, row, bar);
 }
 
 __device__ __forceinline__ void load_kf_rows(const Ctx& c, const float2* __restrict__ kf) {
   uint32_t f2, g;
   coords(f2, g);
-  const uint32_t cb = kColsPer * g;
-  const float4* src = reinterpret_cast<const float4*>(kf + 64 * f2 + cb);
-  float re[16], im[16];
 #pragma unroll
-  for (int j = 0; j < 8; ++j) {
-    const float4 v = __ldg(src + j);
-    re[2 * j] = v.x;
-    im[2 * j] = v.y;
-    re[2 * j + 1] = v.z;
-    im[2 * j + 1] = v.w;
+  for (uint32_t q = 0; q < kColsPer / 16; ++q) {
+    const uint32_t cb = kColsPer * g + 16 * q;
+    const float4* src = reinterpret_cast<const float4*>(kf + 64 * f2 + cb);
+    float re[16], im[16];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const float4 v = __ldg(src + j);
+      re[2 * j] = v.x;
+      im[2 * j] = v.y;
+      re[2 * j + 1] = v.z;
+      im[2 * j + 1] = v.w;
+    }
+    tst8(taddr(c, c.aux + cb), re);
+    tst8(taddr(c, c.aux + cb + 8), re + 8);
+    tst8(taddr(c, c.aux + 64 + cb), im);
+    tst8(taddr(c, c.aux + 64 + cb + 8), im + 8);
   }
-  tst8(taddr(c, c.aux + cb), re);
-  tst8(taddr(c, c.aux + cb + 8), re + 8);
-  tst8(taddr(c, c.aux + 64 + cb), im);
-  tst8(taddr(c, c.aux + 64 + cb + 8), im + 8);
   tst_wait();
 }
 
@@ -986,7 +988,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     tc_rows_fwd_kernel(const __grid_constant__ CUtensorMap xmap, uint32_t* __restrict__ x1,
                        const float2* __restrict__ kf2, const uint4* __restrict__ mats,
                        const float2* __restrict__ tab_g, int npairs, int hm, int total,
-                       uint32_t* __restrict__ usave) {
+                       uint32_t* __restrict__ usave, int token) {
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   __shared__ uint32_t tmem_slot;
   __shared__ __align__(8) uint64_t bars[4];  // mma[2], in[2]
@@ -1001,7 +1003,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   c.smat = rows::SMAT;
   c.tab = reinterpret_cast<const float2*>(sm + rows::STAB);
   c.aux = TKF + 128 * slot;
-  c.on = (SPEC ? 2u : 4u) * (uint32_t)((i1 - i0 + (int)slot) / 2);
+  c.on = token ? (SPEC ? 2u : 4u) * (uint32_t)((i1 - i0 + (int)slot) / 2) : 0u;
+  if (threadIdx.x == 0) asm volatile("prefetch.tensormap [%0];" ::"l"(&xmap) : "memory");
   uint64_t* in_bar = &bars[2 + slot];
   const bool lead = slot_leader();
   auto row_of = [&](int item) { return (item % npairs) * hm + item / npairs; };
@@ -1012,12 +1015,14 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int ha = item / npairs;
     const size_t row = (size_t)row_of(item);
     if (!SPEC && ha != cur) {
+      TT_BEGIN
       load_kf_rows(c, kf2 + (size_t)ha * kN);
+      TT_END(17)
       cur = ha;
     }
-    ptx::mbar_wait(in_bar, it & 1);
+    { TT_BEGIN ptx::mbar_wait(in_bar, it & 1); TT_END(16) }
     issue<T, true>(c, 4);
-    epi_A_exit<T, true>(c);
+    { TT_BEGIN epi_A_exit<T, true>(c); TT_END(18) }
     issue<T, true>(c, 1);
     if constexpr (SPEC) {
       if (lead && item + 2 < i1) load_row(sm + c.in_off, &xmap, row_of(item + 2), in_bar);
@@ -1039,6 +1044,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       continue;
     }
     {  // B exit: U -> usave; Z = U Kf2 -> planes [Zr | Zi | -Zr]
+      TT_BEGIN
       uint32_t f2, g;
       coords(f2, g);
       unsigned char* op = c.sm + c.sop;
@@ -1068,23 +1074,34 @@ __global__ void __launch_bounds__(kThreads, 1)
         st8<T>(op + 16384 + off_bmn(cb, f2), im);
         st8n<T>(op + 32768 + off_bmn(cb, f2), re);
       }
+      TT_END(19)
     }
     issue<T, true>(c, 2);
-    epi_Bp_exit<T>(c);
+    { TT_BEGIN epi_Bp_exit<T>(c); TT_END(20) }
     issue<T, true>(c, 5);
     // the operand planes are free again: the slot's next row streams in
     // while this one is stored
-    if (lead && item + 2 < i1) load_row(sm + c.in_off, &xmap, row_of(item + 2), in_bar);
+    {
+      TT_BEGIN
+      if (lead && item + 2 < i1) load_row(sm + c.in_off, &xmap, row_of(item + 2), in_bar);
+      TT_END(22)
+    }
     {  // A' exit: W[128 t1 + t2] (re, im) for t1 = 16 g + j
+      TT_BEGIN
       uint32_t t2, g;
       coords(t2, g);
-      float re[16], im[16];
-      tld<16>(taddr(c, c.tw + 16 * g), re);
-      tld<16>(taddr(c, c.tw + 64 + 16 * g), im);
-      tc::ld_wait();
-      uint32_t* o = x1 + row * kN + 128 * (16 * g) + t2;
 #pragma unroll
-      for (int j = 0; j < 16; ++j) o[128 * j] = pack2<T>(re[j], im[j]);
+      for (uint32_t q = 0; q < kColsPer / 16; ++q) {
+        const uint32_t cb = kColsPer * g + 16 * q;
+        float re[16], im[16];
+        tld<16>(taddr(c, c.tw + cb), re);
+        tld<16>(taddr(c, c.tw + 64 + cb), im);
+        tc::ld_wait();
+        uint32_t* o = x1 + row * kN + 128 * cb + t2;
+#pragma unroll
+        for (int j = 0; j < 16; ++j) o[128 * j] = pack2<T>(re[j], im[j]);
+      }
+      TT_END(21)
     }
   }
   teardown(tmem_slot);
@@ -1139,7 +1156,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     coords(f2, g);
     const float z[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
 #pragma unroll
-    for (uint32_t q = 0; q < 2; ++q) {
+    for (uint32_t q = 0; q < kColsPer / 8; ++q) {
       tst8(taddr(c, c.aux + kColsPer * g + 8 * q), z);
       tst8(taddr(c, c.aux + 64 + kColsPer * g + 8 * q), z);
     }
@@ -1159,17 +1176,17 @@ __global__ void __launch_bounds__(kThreads, 1)
       uint32_t f2, g;
       coords(f2, g);
       // U in flight while the stage-B MMAs run
-      uint4 up[4];
+      uint4 up[kColsPer / 4];
       {
         const uint4* us = reinterpret_cast<const uint4*>(usave + row * kN + 64 * f2 + kColsPer * g);
 #pragma unroll
-        for (int i = 0; i < 4; ++i) up[i] = __ldg(us + i);
+        for (uint32_t i = 0; i < kColsPer / 4; ++i) up[i] = __ldg(us + i);
       }
       issue<T, true>(c, 1);
       {
         unsigned char* op = c.sm + c.sop;
 #pragma unroll
-        for (uint32_t q = 0; q < 2; ++q) {
+        for (uint32_t q = 0; q < kColsPer / 8; ++q) {
           const uint32_t cb = kColsPer * g + 8 * q;
           float dr[8], di[8], ar[8], ai[8];
           tld<8>(taddr(c, c.tw + cb), dr);
@@ -1206,13 +1223,17 @@ __global__ void __launch_bounds__(kThreads, 1)
       {
         uint32_t t2, gg;
         coords(t2, gg);
-        float re[16], im[16];
-        tld<16>(taddr(c, c.tw + 16 * gg), re);
-        tld<16>(taddr(c, c.tw + 64 + 16 * gg), im);
-        tc::ld_wait();
-        uint32_t* o = x1dy + row * kN + 128 * (16 * gg) + t2;
 #pragma unroll
-        for (int jj = 0; jj < 16; ++jj) o[128 * jj] = pack2<T>(re[jj], im[jj]);
+        for (uint32_t q = 0; q < kColsPer / 16; ++q) {
+          const uint32_t cb = kColsPer * gg + 16 * q;
+          float re[16], im[16];
+          tld<16>(taddr(c, c.tw + cb), re);
+          tld<16>(taddr(c, c.tw + 64 + cb), im);
+          tc::ld_wait();
+          uint32_t* o = x1dy + row * kN + 128 * cb + t2;
+#pragma unroll
+          for (int jj = 0; jj < 16; ++jj) o[128 * jj] = pack2<T>(re[jj], im[jj]);
+        }
       }
     }
     cta_sync_tc();  // acc_0, acc_1 complete
@@ -1222,7 +1243,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       unsigned char* op = c.sm + c.sop;
       const float z[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
 #pragma unroll
-      for (uint32_t q = 0; q < 2; ++q) {
+      for (uint32_t q = 0; q < kColsPer / 8; ++q) {
         const uint32_t cb = kColsPer * g + 8 * q;
         float r0[8], i0[8], r1[8], i1[8];
         tld<8>(taddr(c, 256 + cb), r0);
@@ -1254,13 +1275,17 @@ __global__ void __launch_bounds__(kThreads, 1)
       issue<T, true>(c, 5);
       uint32_t t2, gg;
       coords(t2, gg);
-      float re[16], im[16];
-      tld<16>(taddr(c, c.tw + 16 * gg), re);
-      tld<16>(taddr(c, c.tw + 64 + 16 * gg), im);
-      tc::ld_wait();
-      float2* o = wdk + (size_t)ha * kN + 128 * (16 * gg) + t2;
 #pragma unroll
-      for (int jj = 0; jj < 16; ++jj) o[128 * jj] = make_float2(re[jj], im[jj]);
+      for (uint32_t q = 0; q < kColsPer / 16; ++q) {
+        const uint32_t cb = kColsPer * gg + 16 * q;
+        float re[16], im[16];
+        tld<16>(taddr(c, c.tw + cb), re);
+        tld<16>(taddr(c, c.tw + 64 + cb), im);
+        tc::ld_wait();
+        float2* o = wdk + (size_t)ha * kN + 128 * cb + t2;
+#pragma unroll
+        for (int jj = 0; jj < 16; ++jj) o[128 * jj] = make_float2(re[jj], im[jj]);
+      }
     }
   }
   teardown(tmem_slot);
@@ -1486,7 +1511,7 @@ std::vector<uint8_t> build_mats_rows() {
   return img;
 }
 
-// planar rows [R][2 planes][64 t1][128 t2] 16-bit; box [64 t2][64 t1][1][1]
+// planar rows [R][2 planes][64 t1][128 t2] 16-bit; box [64 t2][64 t1][2 planes][1]
 template <typename T>
 int make_rows_map(CUtensorMap* map, const void* ptr, int64_t R) {
   EncodeFn enc = encode_fn();
@@ -1496,7 +1521,7 @@ int make_rows_map(CUtensorMap* map, const void* ptr, int64_t R) {
   }
   const cuuint64_t dims[4] = {128, 64, 2, (cuuint64_t)R};
   const cuuint64_t strides[3] = {128 * 2, 8192 * 2, 16384 * 2};
-  const cuuint32_t box[4] = {64, 64, 1, 1};
+  const cuuint32_t box[4] = {64, 64, 2, 1};
   const cuuint32_t es[4] = {1, 1, 1, 1};
   CUresult r = enc(map, Fmt<T>::tma, 4, const_cast<void*>(ptr), dims, strides, box, es,
                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
@@ -1518,6 +1543,14 @@ bool tc_rows_eligible(const fb_plan* p) {
 }
 
 // x1: npairs x H x m planar bf16 rows in, interleaved (re, im) rows out
+static int rows_token() {
+  static const int t = [] {
+    const char* e = std::getenv("FB_ROWS_TOKEN");
+    return e ? std::atoi(e) : 1;
+  }();
+  return t;
+}
+
 static int rows_mats(fb_plan* p) {
   if (p->tcr_mats) return FB_OK;
   std::vector<uint8_t> img = build_mats_rows<__nv_bfloat16>();
@@ -1539,7 +1572,8 @@ int tc_rows_fwd(fb_plan* p, void* x1, void* usave, int64_t npairs, cudaStream_t 
   cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rows::SMEM);
   const int ctas = std::max(1, std::min(p->num_sms, total));
   k<<<(unsigned)ctas, kThreads, rows::SMEM, s>>>(map, (uint32_t*)x1, p->kf, (const uint4*)p->tcr_mats,
-                                                 p->tw_l, (int)npairs, hm, total, (uint32_t*)usave);
+                                                 p->tw_l, (int)npairs, hm, total, (uint32_t*)usave,
+                                                 rows_token());
   return cuda_status(cudaGetLastError(), "tc_rows_fwd");
 }
 
@@ -1554,7 +1588,8 @@ int tc_rows_spectrum(fb_plan* p, void* x1, int64_t npairs, cudaStream_t s) {
   cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rows::SMEM);
   const int ctas = std::max(1, std::min(p->num_sms, total));
   k<<<(unsigned)ctas, kThreads, rows::SMEM, s>>>(map, (uint32_t*)x1, p->kf, (const uint4*)p->tcr_mats,
-                                                 p->tw_l, (int)npairs, hm, total, (uint32_t*)x1);
+                                                 p->tw_l, (int)npairs, hm, total, (uint32_t*)x1,
+                                                 rows_token());
   return cuda_status(cudaGetLastError(), "tc_rows_spectrum");
 }
 
