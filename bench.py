@@ -309,7 +309,8 @@ def run_ours(args, cfg, rank, world, local_rank):
         "roofline": {"bound": "hbm",
                      "kernel": (f"{dom}: tc_{dom}_kernel (tcgen05)" if plan.tensor_cores else
                                 f"{dom}: sp_{dom}_kernel" if plan.engine.name != "THREE_PASS" else
-                                f"{dom}: three-pass launches (pass1, pass2, pass3)"),
+                                f"{dom}: three-pass launches (pass 1 cols, pass 2 rows on "
+                                "tcgen05, pass 3 cols)"),
                      "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
                      "frac": achieved / hbm_peak, "traffic": traffic,
                      "alg_bytes_per_launch": dom_bytes, "peak_kind": peak_kind},
