@@ -277,6 +277,26 @@ def test_three_pass_16bit(lc, dtype):
     assert_parity(got, oracle_layer(lc, inp, cfg), 2e-2)
 
 
+@pytest.mark.parametrize("B,H,N,mode", [(2, 2, 8192, 1), (1, 3, 16384, 0), (5, 2, 65536, 1),
+                                        (4, 3, 16384, 1)])
+def test_three_pass_bf16_tc_rows(lc, B, H, N, mode):
+    """bf16 three-pass with pass 2 on tcgen05 (m = 2 .. 16, causal and
+    circular, odd B = a zero partner channel): recompute and saved-U
+    backward agree bit for bit, both within the 16-bit bar of the oracle."""
+    dtype = torch.bfloat16
+    inp = layer_inputs(lc, B, H, N, dtype)
+    cfg = fb.RegularizationConfig(**CFG)
+    plan, got = run_layer(inp, N, H, dtype, cfg, mode=mode, engine=2)
+    assert plan.engine == fb.Engine.THREE_PASS
+    assert_parity(got, oracle_layer(lc, inp, cfg, causal=bool(mode)), 2e-2,
+                  keys=("y", "du", "dK", "dD"))
+    y, saved = plan.forward(inp["tu"], save=True)
+    du, dK, dD = plan.backward(inp["tdy"], None, saved=saved)
+    torch.cuda.synchronize()
+    assert np.array_equal(to_np(y), got["y"])
+    assert np.array_equal(to_np(du), got["du"])
+
+
 def test_config3_heads_sample(lc):
     """BASELINE config 3 shape (B=16 H=128 N=65536 bf16, three-pass) on the
     GPU; a sample of heads (all batches, so dK is complete) vs the oracle."""
