@@ -377,20 +377,24 @@ __device__ __forceinline__ ColTile col_tile(int t, int H) {
 }
 
 // Producer / consumer ring shared by the streaming column kernels: warp
-// kTB / 32 only issues the TMA boxes (waiting on the per-stage "empty"
-// barriers), the kTB consumer threads wait on "full", copy their column to
-// registers, release the stage at once and compute — the TMA issue is never
-// on a consumer warp's critical path.
+// kCons / 32 only issues the TMA boxes (waiting on the per-stage "empty"
+// barriers), the kCons consumer threads wait on "full", copy their two
+// adjacent columns to registers, release the stage at once and compute — the
+// TMA issue is never on a consumer warp's critical path, and every load and
+// store moves a column pair (half the memory instructions of one column per
+// thread).
+constexpr uint32_t kCons = kTB / 2;
+
 __device__ __forceinline__ void mbar_arrive_cta(uint64_t* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(ptx::smem_u32(bar)) : "memory");
 }
 __device__ __forceinline__ void consumers_sync() {
-  asm volatile("bar.sync 1, %0;" ::"n"(kTB) : "memory");
+  asm volatile("bar.sync 1, %0;" ::"n"(kCons) : "memory");
 }
 template <class Issue>
 __device__ __forceinline__ void col_producer(int first, int step, int ntiles, int nstages,
                                              uint64_t* empty, Issue&& issue) {
-  if (threadIdx.x != kTB) return;
+  if (threadIdx.x != kCons) return;
   int k = 0;
   for (int t = first; t < ntiles; t += step, ++k) {
     const int sg = k % nstages;
@@ -399,19 +403,72 @@ __device__ __forceinline__ void col_producer(int first, int step, int ntiles, in
   }
 }
 
+// two consecutive elements (column pair) in / out
+__device__ __forceinline__ float2 ld2s(const float* p) { return *reinterpret_cast<const float2*>(p); }
+__device__ __forceinline__ float2 ld2s(const __nv_bfloat16* p) {
+  return __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(p));
+}
+__device__ __forceinline__ float2 ld2s(const __half* p) {
+  return __half22float2(*reinterpret_cast<const __half2*>(p));
+}
+__device__ __forceinline__ void st2(float* p, float a, float b) {
+  *reinterpret_cast<float2*>(p) = make_float2(a, b);
+}
+__device__ __forceinline__ void st2(__nv_bfloat16* p, float a, float b) {
+  *reinterpret_cast<__nv_bfloat162*>(p) = __floats2bfloat162_rn(a, b);
+}
+__device__ __forceinline__ void st2(__half* p, float a, float b) {
+  *reinterpret_cast<__half2*>(p) = __floats2half2_rn(a, b);
+}
+__device__ __forceinline__ void st4(float* p, float a, float b, float c, float d) {
+  *reinterpret_cast<float4*>(p) = make_float4(a, b, c, d);
+}
+__device__ __forceinline__ void st4(__nv_bfloat16* p, float a, float b, float c, float d) {
+  const __nv_bfloat162 x = __floats2bfloat162_rn(a, b), y = __floats2bfloat162_rn(c, d);
+  *reinterpret_cast<uint2*>(p) =
+      make_uint2(*reinterpret_cast<const uint32_t*>(&x), *reinterpret_cast<const uint32_t*>(&y));
+}
+__device__ __forceinline__ void st4(__half* p, float a, float b, float c, float d) {
+  const __half2 x = __floats2half2_rn(a, b), y = __floats2half2_rn(c, d);
+  *reinterpret_cast<uint2*>(p) =
+      make_uint2(*reinterpret_cast<const uint32_t*>(&x), *reinterpret_cast<const uint32_t*>(&y));
+}
+// two consecutive complex elements
+__device__ __forceinline__ void cx_load2(const CxT<float>* p, float2& a, float2& b) {
+  const float4 v = *reinterpret_cast<const float4*>(p);
+  a = make_float2(v.x, v.y);
+  b = make_float2(v.z, v.w);
+}
+template <typename H2>
+__device__ __forceinline__ float2 h2f(uint32_t v);
+template <>
+__device__ __forceinline__ float2 h2f<__nv_bfloat16>(uint32_t v) {
+  return __bfloat1622float2(*reinterpret_cast<__nv_bfloat162*>(&v));
+}
+template <>
+__device__ __forceinline__ float2 h2f<__half>(uint32_t v) {
+  return __half22float2(*reinterpret_cast<__half2*>(&v));
+}
+template <typename T>
+__device__ __forceinline__ void cx_load2(const CxT<T>* p, float2& a, float2& b) {
+  const uint2 v = *reinterpret_cast<const uint2*>(p);
+  a = h2f<T>(v.x);
+  b = h2f<T>(v.y);
+}
+
 // Pass 1, SRC 0: signal pairs (channels 2 pr, 2 pr + 1 -> re, im);
 // SRC 1: dy and u pairs at once, plus the lag-0 dD partial.  Signal maps view
 // [B*H][rows][l] with rows = N / l data rows (the causal pad is implicit).
 // PLANAR: rows leave as [re l | im l] (the tcgen05 row pass's TMA layout)
 template <typename IO, typename ST, int M, int SRC, bool PLANAR = false>
-__global__ void __launch_bounds__(kTB + 32)
+__global__ void __launch_bounds__(kCons + 32)
     tp_col1_kernel(const __grid_constant__ CUtensorMap amap, const __grid_constant__ CUtensorMap bmap,
                    CxT<ST>* __restrict__ out_a, CxT<ST>* __restrict__ out_b,
                    float* __restrict__ ddpart, const float2* __restrict__ tab_g, int H, int npairs,
                    int rows, int ntiles, int nstages) {
   extern __shared__ __align__(128) unsigned char csm[];
   __shared__ __align__(8) uint64_t full[kColMaxStages], empty[kColMaxStages];
-  __shared__ float red[2][kTB / 32];
+  __shared__ float red[2][kCons / 32];
   constexpr int NCH = SRC == 1 ? 4 : 2;
   const uint32_t chb = (uint32_t)rows * kTB * sizeof(IO);
   const uint32_t stage_bytes = NCH * chb;
@@ -419,13 +476,13 @@ __global__ void __launch_bounds__(kTB + 32)
   if (j == 0) {
     for (int i = 0; i < nstages; ++i) {
       ptx::mbar_init(&full[i], 1);
-      ptx::mbar_init(&empty[i], kTB);
+      ptx::mbar_init(&empty[i], kCons);
     }
     ptx::fence_barrier_init();
   }
   __syncthreads();
   const int first = blockIdx.x, step = gridDim.x;
-  if (j >= (int)kTB) {
+  if (j >= (int)kCons) {
     col_producer(first, step, ntiles, nstages, empty, [&](int t, int st) {
       const ColTile c = col_tile(t, H);
       unsigned char* dst = csm + (size_t)st * stage_bytes;
@@ -444,45 +501,56 @@ __global__ void __launch_bounds__(kTB + 32)
     const int sg = it % nstages;
     ptx::mbar_wait(&full[sg], (uint32_t)(it / nstages) & 1);
     const ColTile c = col_tile(t, H);
-    const uint32_t tau = c.tb * kTB + j;
+    const uint32_t tau = c.tb * kTB + 2 * j;
     const IO* sv = reinterpret_cast<const IO*>(csm + (size_t)sg * stage_bytes);
-    auto column = [&](int ch0, float2 (&v)[M]) {
+    // columns tau (v0) and tau + 1 (v1) of the channel pair (ch0, ch0 + 1)
+    auto columns = [&](int ch0, float2 (&v0)[M], float2 (&v1)[M]) {
 #pragma unroll
       for (int r = 0; r < M; ++r) {
         const bool ok = r < rows;
-        v[r].x = ok ? tof(sv[(ch0 * rows + r) * kTB + j]) : 0.f;
-        v[r].y = ok ? tof(sv[((ch0 + 1) * rows + r) * kTB + j]) : 0.f;
+        const float2 a = ok ? ld2s(sv + (ch0 * rows + r) * kTB + 2 * j) : make_float2(0.f, 0.f);
+        const float2 b = ok ? ld2s(sv + ((ch0 + 1) * rows + r) * kTB + 2 * j) : make_float2(0.f, 0.f);
+        v0[r] = make_float2(a.x, b.x);
+        v1[r] = make_float2(a.y, b.y);
       }
     };
-    float2 v[M];
-    column(0, v);
+    float2 v0[M], v1[M];
+    columns(0, v0, v1);
     float dd = 0.f;
-    float2 w[SRC == 1 ? M : 1];
-    if constexpr (SRC == 1) column(2, w);
+    float2 w0[SRC == 1 ? M : 1], w1[SRC == 1 ? M : 1];
+    if constexpr (SRC == 1) columns(2, w0, w1);
     mbar_arrive_cta(&empty[sg]);  // this thread's reads of the stage are done
+    auto put = [&](CxT<ST>* o, const float2 (&x0)[M], const float2 (&x1)[M]) {
+      if constexpr (PLANAR) {
+#pragma unroll
+        for (int a = 0; a < M; ++a) {
+          ST* r = reinterpret_cast<ST*>(o + a * kL);
+          st2(r + tau, x0[a].x, x1[a].x);
+          st2(r + kL + tau, x0[a].y, x1[a].y);
+        }
+      } else {
+#pragma unroll
+        for (int a = 0; a < M; ++a)
+          st4(&o[a * kL + tau].x, x0[a].x, x0[a].y, x1[a].x, x1[a].y);
+      }
+    };
     if constexpr (SRC == 1) {
 #pragma unroll
-      for (int r = 0; r < M; ++r) dd = fmaf(v[r].x, w[r].x, fmaf(v[r].y, w[r].y, dd));
-      dft_reg<-1, M>(w);
-      apply_tw_g<-1, M>(w, tab_g, tau);
-      CxT<ST>* ob = out_b + ((size_t)c.pr * H + c.h) * (size_t)M * kL;
-#pragma unroll
-      for (int a = 0; a < M; ++a) stc<ST>(&ob[a * kL + tau].x, w[a]);
-    }
-    dft_reg<-1, M>(v);
-    apply_tw_g<-1, M>(v, tab_g, tau);
-    CxT<ST>* oa = out_a + ((size_t)c.pr * H + c.h) * (size_t)M * kL;
-    if constexpr (PLANAR) {
-#pragma unroll
-      for (int a = 0; a < M; ++a) {
-        ST* r = reinterpret_cast<ST*>(oa + a * kL);
-        st(r + tau, v[a].x);
-        st(r + kL + tau, v[a].y);
+      for (int r = 0; r < M; ++r) {
+        dd = fmaf(v0[r].x, w0[r].x, fmaf(v0[r].y, w0[r].y, dd));
+        dd = fmaf(v1[r].x, w1[r].x, fmaf(v1[r].y, w1[r].y, dd));
       }
-    } else {
-#pragma unroll
-      for (int a = 0; a < M; ++a) stc<ST>(&oa[a * kL + tau].x, v[a]);
+      dft_reg<-1, M>(w0);
+      apply_tw_g<-1, M>(w0, tab_g, tau);
+      dft_reg<-1, M>(w1);
+      apply_tw_g<-1, M>(w1, tab_g, tau + 1);
+      put(out_b + ((size_t)c.pr * H + c.h) * (size_t)M * kL, w0, w1);
     }
+    dft_reg<-1, M>(v0);
+    apply_tw_g<-1, M>(v0, tab_g, tau);
+    dft_reg<-1, M>(v1);
+    apply_tw_g<-1, M>(v1, tab_g, tau + 1);
+    put(out_a + ((size_t)c.pr * H + c.h) * (size_t)M * kL, v0, v1);
     if constexpr (SRC == 1) {
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) dd += __shfl_xor_sync(0xffffffffu, dd, o);
@@ -490,7 +558,7 @@ __global__ void __launch_bounds__(kTB + 32)
       consumers_sync();  // red[it & 1] complete (double-buffered by tile parity)
       if (j == 0) {
         float s = 0.f;
-        for (int w2 = 0; w2 < (int)(kTB / 32); ++w2) s += red[it & 1][w2];
+        for (int w2 = 0; w2 < (int)(kCons / 32); ++w2) s += red[it & 1][w2];
         ddpart[((size_t)c.h * npairs + c.pr) * (kL / kTB) + c.tb] = s;
       }
     }
@@ -500,7 +568,7 @@ __global__ void __launch_bounds__(kTB + 32)
 // Pass 3 (MODE 0): W rows [pair*H + h][M][l] (complex ST) -> out[b][h][c l + tau]
 // = Re/Im(column IDFT) + D[h] skip[b][h][c l + tau], c < rows.
 template <typename ST, typename IO, int M>
-__global__ void __launch_bounds__(kTB + 32)
+__global__ void __launch_bounds__(kCons + 32)
     tp_col3_kernel(const __grid_constant__ CUtensorMap wmap, const __grid_constant__ CUtensorMap smap,
                    IO* __restrict__ out, const float* __restrict__ D,
                    const float2* __restrict__ tab_g, int B, int H, uint32_t N, int rows, int ntiles,
@@ -514,13 +582,13 @@ __global__ void __launch_bounds__(kTB + 32)
   if (j == 0) {
     for (int i = 0; i < nstages; ++i) {
       ptx::mbar_init(&full[i], 1);
-      ptx::mbar_init(&empty[i], kTB);
+      ptx::mbar_init(&empty[i], kCons);
     }
     ptx::fence_barrier_init();
   }
   __syncthreads();
   const int first = blockIdx.x, step = gridDim.x;
-  if (j >= (int)kTB) {
+  if (j >= (int)kCons) {
     col_producer(first, step, ntiles, nstages, empty, [&](int t, int st) {
       const ColTile c = col_tile(t, H);
       unsigned char* dst = csm + (size_t)st * stage_bytes;
@@ -538,22 +606,24 @@ __global__ void __launch_bounds__(kTB + 32)
     const int sg = it % nstages;
     ptx::mbar_wait(&full[sg], (uint32_t)(it / nstages) & 1);
     const ColTile c = col_tile(t, H);
-    const uint32_t tau = c.tb * kTB + j;
+    const uint32_t tau = c.tb * kTB + 2 * j;
     const unsigned char* base = csm + (size_t)sg * stage_bytes;
     const CxT<ST>* sw = reinterpret_cast<const CxT<ST>*>(base);
     const IO* sk = reinterpret_cast<const IO*>(base + wb);
-    float2 v[M];
+    float2 v0[M], v1[M];
 #pragma unroll
-    for (int a = 0; a < M; ++a) v[a] = cx_load(sw + a * kTB + j);
-    float s0[M], s1[M];
+    for (int a = 0; a < M; ++a) cx_load2(sw + a * kTB + 2 * j, v0[a], v1[a]);
+    float2 s0[M], s1[M];  // skip of channels b0 / b1 at (tau, tau + 1)
 #pragma unroll
     for (int r = 0; r < M; ++r) {
-      s0[r] = r < rows ? tof(sk[r * kTB + j]) : 0.f;
-      s1[r] = r < rows ? tof(sk[(rows + r) * kTB + j]) : 0.f;
+      s0[r] = r < rows ? ld2s(sk + r * kTB + 2 * j) : make_float2(0.f, 0.f);
+      s1[r] = r < rows ? ld2s(sk + (rows + r) * kTB + 2 * j) : make_float2(0.f, 0.f);
     }
     mbar_arrive_cta(&empty[sg]);
-    apply_tw_g<+1, M>(v, tab_g, tau);
-    dft_reg<+1, M>(v);
+    apply_tw_g<+1, M>(v0, tab_g, tau);
+    dft_reg<+1, M>(v0);
+    apply_tw_g<+1, M>(v1, tab_g, tau + 1);
+    dft_reg<+1, M>(v1);
     const int b0 = 2 * c.pr, b1 = b0 + 1;
     const bool has1 = b1 < B;
     const float d = __ldg(D + c.h);
@@ -562,8 +632,8 @@ __global__ void __launch_bounds__(kTB + 32)
     for (int r = 0; r < M; ++r) {
       if (r < rows) {
         const uint32_t tt = r * kL + tau;
-        st(out + o0 + tt, fmaf(d, s0[r], v[r].x));
-        if (has1) st(out + o1 + tt, fmaf(d, s1[r], v[r].y));
+        st2(out + o0 + tt, fmaf(d, s0[r].x, v0[r].x), fmaf(d, s0[r].y, v1[r].x));
+        if (has1) st2(out + o1 + tt, fmaf(d, s1[r].x, v0[r].y), fmaf(d, s1[r].y, v1[r].y));
       }
     }
   }
@@ -1045,7 +1115,12 @@ size_t bigs_smem(uint32_t m, int tiles, size_t stage) {
 }
 
 int col_stages(size_t stage_bytes) {
-  return (int)std::max<size_t>(2, std::min<size_t>(kColMaxStages, (96 * 1024) / stage_bytes));
+  return (int)std::max<size_t>(2, std::min<size_t>(kColMaxStages, (52 * 1024) / stage_bytes));
+}
+// resident CTAs per SM as the ring's smem allows (<= 4), persistent over the tiles
+int col_grid(size_t ring_bytes, int ntiles, int sms) {
+  const int per = (int)std::max<size_t>(1, std::min<size_t>(4, (220 * 1024) / (ring_bytes + 2048)));
+  return std::min(ntiles, per * sms);
 }
 
 // pass 1: streaming TMA column kernel (signals, m <= 16), register kernel for
@@ -1065,12 +1140,12 @@ uint32_t launch_pass1(const fb_plan* p, const IO* a, const IO* b, CxT<ST>* oa, C
       const size_t stage = (size_t)2 * rows * kTB * sizeof(IO);
       const int ns = col_stages(stage);
       const int ntiles = (int)(npairs * p->H * (kL / kTB));
-      const int grid = std::min(ntiles, 2 * p->num_sms);
+      const int grid = col_grid(stage * ns, ntiles, p->num_sms);
       with_m(p->m, [&](auto mc) {
         constexpr int M = decltype(mc)::value;
         auto k = tp_col1_kernel<IO, ST, M, 0, true>;
         cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(stage * ns));
-        k<<<grid, kTB + 32, stage * ns, s>>>(am, am, oa, nullptr, nullptr, p->tw_n, (int)p->H,
+        k<<<grid, kCons + 32, stage * ns, s>>>(am, am, oa, nullptr, nullptr, p->tw_n, (int)p->H,
                                              npairs, rows, ntiles, ns);
       });
       return kL / kTB;
@@ -1084,12 +1159,12 @@ uint32_t launch_pass1(const fb_plan* p, const IO* a, const IO* b, CxT<ST>* oa, C
       const size_t stage = (size_t)(SRC == 1 ? 4 : 2) * rows * kTB * sizeof(IO);
       const int ns = col_stages(stage);
       const int ntiles = (int)(npairs * p->H * (kL / kTB));
-      const int grid = std::min(ntiles, 2 * p->num_sms);
+      const int grid = col_grid(stage * ns, ntiles, p->num_sms);
       if (maps) with_m(p->m, [&](auto mc) {
         constexpr int M = decltype(mc)::value;
         auto k = tp_col1_kernel<IO, ST, M, SRC>;
         cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(stage * ns));
-        k<<<grid, kTB + 32, stage * ns, s>>>(am, bm, oa, ob, ddpart, p->tw_n, (int)p->H, npairs,
+        k<<<grid, kCons + 32, stage * ns, s>>>(am, bm, oa, ob, ddpart, p->tw_n, (int)p->H, npairs,
                                              rows, ntiles, ns);
       });
       if (maps) return kL / kTB;
@@ -1161,12 +1236,12 @@ void launch_pass3(const fb_plan* p, const CxT<ST>* w, const IO* skip, IO* out, f
       const size_t stage = p->m * kTB * sizeof(CxT<ST>) + 2 * (size_t)rows * kTB * sizeof(IO);
       const int ns = col_stages(stage);
       const int ntiles = (int)(npairs * p->H * (kL / kTB));
-      const int grid = std::min(ntiles, 2 * p->num_sms);
+      const int grid = col_grid(stage * ns, ntiles, p->num_sms);
       if (maps) with_m(p->m, [&](auto mc) {
         constexpr int M = decltype(mc)::value;
         auto k = tp_col3_kernel<ST, IO, M>;
         cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(stage * ns));
-        k<<<grid, kTB + 32, stage * ns, s>>>(wm, sm, out, p->d, p->tw_n, B, (int)p->H,
+        k<<<grid, kCons + 32, stage * ns, s>>>(wm, sm, out, p->d, p->tw_n, B, (int)p->H,
                                              (uint32_t)p->N, rows, ntiles, ns);
       });
       if (maps) return;  // else: the register column kernel below
