@@ -1169,6 +1169,11 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (lead && (int)slot < npairs) load_row(sm + c.in_off, &xmap, (int)slot * hm + ha, in_bar);
     for (int j = (int)slot; j < npairs; j += 2) {
       const size_t row = (size_t)j * hm + ha;
+      if (j + 2 >= npairs && ha + 1 < g1) {  // the slot's half of the next Kf2 row -> L2
+        const char* nk = reinterpret_cast<const char*>(kf2 + (size_t)(ha + 1) * kN) +
+                         (size_t)(threadIdx.x & (kSlotThreads - 1)) * 256 + slot * 128;
+        asm volatile("prefetch.global.L2 [%0];" ::"l"(nk));
+      }
       ptx::mbar_wait(in_bar, in_cnt & 1);
       ++in_cnt;
       issue<T, true>(c, 4);
@@ -1236,7 +1241,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
       }
     }
-    cta_sync_tc();  // acc_0, acc_1 complete
+    { TT_BEGIN cta_sync_tc(); TT_END(24) }  // acc_0, acc_1 complete
     if (slot == 0) {  // acc_0 + acc_1 -> B' operand planes; zero both accumulators
       uint32_t f2, g;
       coords(f2, g);
@@ -1265,11 +1270,13 @@ __global__ void __launch_bounds__(kThreads, 1)
         tst8(taddr(c, 384 + 64 + cb), z);
       }
       tst_wait();
-    } else if (ha + 1 < g1) {
-      load_kf(ha + 1, threadIdx.x - kSlotThreads, kSlotThreads);
     }
-    cta_sync_tc();  // accumulators consumed, next Kf2 row in smem
+    // next Kf2 row (prefetched into L2 during the group's last pairs): the
+    // whole CTA converts it, slot 0 after reading the accumulators
+    if (ha + 1 < g1) load_kf(ha + 1, threadIdx.x, kThreads);
+    { TT_BEGIN cta_sync_tc(); TT_END(25) }  // accumulators consumed, next Kf2 row in smem
     if (slot == 0) {  // dK spectrum row -> IFFT -> wdk (fp32)
+      TT_BEGIN
       issue<T, true>(c, 2);
       epi_Bp_exit<T>(c);
       issue<T, true>(c, 5);
@@ -1286,6 +1293,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
         for (int jj = 0; jj < 16; ++jj) o[128 * jj] = make_float2(re[jj], im[jj]);
       }
+      TT_END(26)
     }
   }
   teardown(tmem_slot);
