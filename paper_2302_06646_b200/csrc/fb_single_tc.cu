@@ -1547,7 +1547,7 @@ bool tc_rows_eligible(const fb_plan* p) {
     const char* e = std::getenv("FB_ROWS_TC");
     return e && e[0] == '0';
   }();
-  return !off && p->dtype == FB_BF16 && p->l == 8192 && p->m <= 16;
+  return !off && p->dtype == FB_BF16 && p->l == 8192;
 }
 
 // x1: npairs x H x m planar bf16 rows in, interleaved (re, im) rows out

@@ -796,7 +796,8 @@ struct ColTw {
 };
 
 // two CTAs per SM where the smem allows it (single-signal pass 1)
-template <typename IO, typename ST, int SMALL, int SRC>
+// PLANAR: rows leave as [re l | im l] (the tcgen05 row pass's TMA layout)
+template <typename IO, typename ST, int SMALL, int SRC, bool PLANAR = false>
 __global__ void __launch_bounds__(kBigThreads, SRC == 1 ? 1 : 2)
     tp_bigs1_kernel(const __grid_constant__ CUtensorMap amap, const __grid_constant__ CUtensorMap bmap,
                     CxT<ST>* __restrict__ out_a, CxT<ST>* __restrict__ out_b,
@@ -877,7 +878,14 @@ __global__ void __launch_bounds__(kBigThreads, SRC == 1 ? 1 : 2)
     for (uint32_t i = threadIdx.x; i < kBigTile; i += kBigThreads) {
       const uint32_t a = i / TAU, c = i % TAU;
       const float2 w = ctw.next();
-      stc<ST>(&oa[(size_t)a * kL + tau0 + c].x, cmul(sa[pad16(a) * TAU + c], w));
+      if constexpr (PLANAR) {
+        const float2 x = cmul(sa[pad16(a) * TAU + c], w);
+        ST* r = reinterpret_cast<ST*>(oa + (size_t)a * kL);
+        st(r + tau0 + c, x.x);
+        st(r + kL + tau0 + c, x.y);
+      } else {
+        stc<ST>(&oa[(size_t)a * kL + tau0 + c].x, cmul(sa[pad16(a) * TAU + c], w));
+      }
       if constexpr (SRC == 1) stc<ST>(&ob[(size_t)a * kL + tau0 + c].x, cmul(sb[pad16(a) * TAU + c], w));
     }
     if constexpr (SRC == 1) {
@@ -1130,10 +1138,10 @@ uint32_t launch_pass1(const fb_plan* p, const IO* a, const IO* b, CxT<ST>* oa, C
                       float* ddpart, int B, int npairs, cudaStream_t s, bool planar = false) {
   const int causal = p->mode == FB_MODE_CAUSAL;
   if constexpr (SRC == 0) {
-    if (planar) {  // the tcgen05 row pass's input: streaming column kernel only
+    if (planar && p->m <= 16) {  // the tcgen05 row pass's input: streaming column kernel only
       CUtensorMap am;
-      if (p->m > 16 || signal_map<IO>(&am, p, a, B)) {
-        set_error("three-pass: planar pass 1 needs m <= 16 and a signal tensor map");
+      if (signal_map<IO>(&am, p, a, B)) {
+        set_error("three-pass: planar pass 1 needs a signal tensor map");
         return 0;
       }
       const int rows = (int)(p->N / kL);
@@ -1170,6 +1178,7 @@ uint32_t launch_pass1(const fb_plan* p, const IO* a, const IO* b, CxT<ST>* oa, C
       if (maps) return kL / kTB;
     }
   }
+  if (planar && p->m <= 16) return 0;
   if (p->m <= 16) {
     with_m(p->m, [&](auto mc) {
       constexpr int M = decltype(mc)::value;
@@ -1203,6 +1212,8 @@ uint32_t launch_pass1(const fb_plan* p, const IO* a, const IO* b, CxT<ST>* oa, C
       with_small(p->m, [&](auto sc) {
         constexpr int SM = decltype(sc)::value;
         auto k = tp_bigs1_kernel<IO, ST, SM, SRC>;
+        if constexpr (SRC == 0)
+          if (planar) k = tp_bigs1_kernel<IO, ST, SM, SRC, true>;
         cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
         const int per_sm = (SRC != 1 && sm <= 113 * 1024) ? 2 : 1;
         k<<<std::min(ntiles, per_sm * p->num_sms), kBigThreads, sm, s>>>(am, bm, oa, ob, ddpart, p->tw_m,
@@ -1211,6 +1222,10 @@ uint32_t launch_pass1(const fb_plan* p, const IO* a, const IO* b, CxT<ST>* oa, C
       });
       return gx;
     }
+  }
+  if (planar) {
+    set_error("three-pass: planar pass 1 needs the streaming column kernels");
+    return 0;
   }
   with_small(p->m, [&](auto sc) {
     constexpr int SM = decltype(sc)::value;
@@ -1343,6 +1358,16 @@ __global__ void tp_dd_lag0_kernel(const float* __restrict__ dkbar, float* __rest
   if (h < H) dD[h] = dkbar[(size_t)h * N];  // dD = sum_t dy u = dKbar[0] (lag 0)
 }
 
+// pass 2 on tcgen05 when the dtype allows it and pass 1 can write planar rows
+// (streaming column kernels: m <= 16, or the big-column ring fits in smem)
+static bool use_tc_rows(const fb_plan* p) {
+  if (!tc_rows_eligible(p)) return false;
+  if (p->m <= 16) return true;
+  const uint32_t TAU = (uint32_t)(kBigTile / p->m);
+  const size_t stage = (size_t)2 * (p->N / kL) * TAU * 2;
+  return bigs_smem((uint32_t)p->m, 1, stage) <= 227 * 1024 && (bigs_mask() & 1);
+}
+
 int tp_fwd(fb_plan* p, const void* u, void* y, int64_t B, void* ws, cudaStream_t s, void* usave) {
   const int64_t npairs = (B + 1) / 2;
   if (p->periodic) {
@@ -1354,7 +1379,7 @@ int tp_fwd(fb_plan* p, const void* u, void* y, int64_t B, void* ws, cudaStream_t
     using IO = decltype(io);
     using ST = IO;
     auto* x1 = reinterpret_cast<CxT<ST>*>(ws);
-    if (tc_rows_eligible(p)) {  // pass 2 on tcgen05 (planar rows in, interleaved out)
+    if (use_tc_rows(p)) {  // pass 2 on tcgen05 (planar rows in, interleaved out)
       if (!launch_pass1<IO, ST, 0>(p, (const IO*)u, nullptr, x1, nullptr, nullptr, (int)B,
                                    (int)npairs, s, true)) {
         rc = FB_ERR_UNSUPPORTED;
@@ -1398,7 +1423,7 @@ int tp_bwd(fb_plan* p, const void* dy, const void* u, void* du, float* dK, float
   float* ddpart = (float*)(w + off);
   float* dkbar = dKbar ? dKbar : dkbar_s;
   int rc = FB_OK;
-  const bool tcr = tc_rows_eligible(p);
+  const bool tcr = use_tc_rows(p);
   with_io(p->dtype, [&](auto io) {
     using IO = decltype(io);
     using ST = IO;

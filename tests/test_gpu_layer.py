@@ -278,11 +278,12 @@ def test_three_pass_16bit(lc, dtype):
 
 
 @pytest.mark.parametrize("B,H,N,mode", [(2, 2, 8192, 1), (1, 3, 16384, 0), (5, 2, 65536, 1),
-                                        (4, 3, 16384, 1)])
+                                        (4, 3, 16384, 1), (3, 1, 131072, 1), (2, 1, 262144, 1)])
 def test_three_pass_bf16_tc_rows(lc, B, H, N, mode):
-    """bf16 three-pass with pass 2 on tcgen05 (m = 2 .. 16, causal and
-    circular, odd B = a zero partner channel): recompute and saved-U
-    backward agree bit for bit, both within the 16-bit bar of the oracle."""
+    """bf16 three-pass with pass 2 on tcgen05 (m = 2 .. 64: register and
+    big-column pass 1 writing planar rows; causal and circular; odd B = a
+    zero partner channel): recompute and saved-U backward agree bit for bit,
+    both within the 16-bit bar of the oracle."""
     dtype = torch.bfloat16
     inp = layer_inputs(lc, B, H, N, dtype)
     cfg = fb.RegularizationConfig(**CFG)
