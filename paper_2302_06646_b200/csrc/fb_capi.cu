@@ -161,6 +161,11 @@ int fb_plan_create(fb_plan** out, int64_t N, int64_t H, int mode, int dtype, int
   if (!rc) rc = cuda_status(cudaMalloc(&p->kbar, sizeof(float) * H * N), "cudaMalloc(kbar)");
   if (!rc) rc = cuda_status(cudaMalloc(&p->d, sizeof(float) * H), "cudaMalloc(D)");
   if (!rc && p->use_tc) rc = tc_init(p);
+  if (!rc && p->engine == FB_ENGINE_THREE) {
+    rc = cuda_status(cudaStreamCreateWithFlags(&p->aux, cudaStreamNonBlocking), "aux stream");
+    for (cudaEvent_t* e : {&p->ev_fork, &p->ev_prep, &p->ev_join})
+      if (!rc) rc = cuda_status(cudaEventCreateWithFlags(e, cudaEventDisableTiming), "event");
+  }
   if (rc) {
     fb_plan_destroy(p);
     return rc;
@@ -184,6 +189,10 @@ int fb_plan_destroy(fb_plan* p) {
   cudaFree(p->kf_tc);
   cudaFree(p->tcr_mats);
   cudaFree(p->kf_scale);
+  if (p->aux) cudaStreamSynchronize(p->aux);
+  for (cudaEvent_t e : {p->ev_fork, p->ev_prep, p->ev_join})
+    if (e) cudaEventDestroy(e);
+  if (p->aux) cudaStreamDestroy(p->aux);
   delete p;
   return FB_OK;
 }
@@ -204,6 +213,7 @@ int fb_plan_get_info(const fb_plan* p, fb_plan_info* info) {
 
 int fb_plan_copy_kbar(const fb_plan* p, float* dst, void* stream) {
   if (!p || !dst) return fail(FB_ERR_ARG, "fb_plan_copy_kbar: null argument");
+  prep_wait(p, (cudaStream_t)stream);
   return cuda_status(cudaMemcpyAsync(dst, p->kbar, sizeof(float) * p->H * p->N,
                                      cudaMemcpyDeviceToDevice, (cudaStream_t)stream),
                      "fb_plan_copy_kbar");
@@ -221,6 +231,23 @@ int fb_kernel_prep(fb_plan* p, const float* K, const float* D, const fb_reg_conf
   cudaStream_t s = (cudaStream_t)stream;
   int rc = cuda_status(cudaSetDevice(p->device), "cudaSetDevice");
   if (rc) return rc;
+  // three-pass: the prep chain runs on the plan's auxiliary stream (after
+  // everything already queued on s), so the next forward's pass 1 overlaps it;
+  // consumers of the plan state wait on ev_prep.  Not while s is capturing.
+  cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+  cudaStreamIsCapturing(s, &cap);
+  const bool async = p->aux && cap == cudaStreamCaptureStatusNone;
+  if (p->prep_async) {  // the previous prep must be done before its state is rewritten
+    prep_wait(p, s);
+    p->prep_async = false;
+  }
+  cudaStream_t ps = s;
+  if (async) {
+    rc = cuda_status(cudaEventRecord(p->ev_fork, s), "fork");
+    if (!rc) rc = cuda_status(cudaStreamWaitEvent(p->aux, p->ev_fork, 0), "fork wait");
+    if (rc) return rc;
+    ps = p->aux;
+  }
   p->lambda = cfg->lambda;
   p->p = cfg->smooth_width;
   p->smooth_domain = cfg->smooth_domain;
@@ -231,14 +258,19 @@ int fb_kernel_prep(fb_plan* p, const float* K, const float* D, const fb_reg_conf
       rc = cuda_status(cudaMalloc(&p->keep, (size_t)p->H * p->N), "cudaMalloc(keep)");
       if (rc) return rc;
     }
-    rc = dropout_keep_dev(p, cfg->dropout_rate, cfg->seed, s);
+    rc = dropout_keep_dev(p, cfg->dropout_rate, cfg->seed, ps);
     if (rc) return rc;
   }
-  rc = cuda_status(cudaMemcpyAsync(p->d, D, sizeof(float) * p->H, cudaMemcpyDeviceToDevice, s),
+  rc = cuda_status(cudaMemcpyAsync(p->d, D, sizeof(float) * p->H, cudaMemcpyDeviceToDevice, ps),
                    "copy D");
   if (rc) return rc;
-  rc = p->engine == FB_ENGINE_SINGLE ? sp_prep(p, K, s) : tp_prep(p, K, s);
+  rc = p->engine == FB_ENGINE_SINGLE ? sp_prep(p, K, ps) : tp_prep(p, K, ps);
   if (rc) return rc;
+  if (async) {
+    rc = cuda_status(cudaEventRecord(p->ev_prep, p->aux), "prep event");
+    if (rc) return rc;
+    p->prep_async = true;
+  }
   p->prepared = true;
   return FB_OK;
 }
@@ -262,6 +294,7 @@ int fb_fwd(fb_plan* p, const void* u, void* y, int64_t B, void* ws, void* stream
   if (!u || !y) return fail(FB_ERR_ARG, "fb_fwd: null tensor");
   if (p->engine == FB_ENGINE_THREE && !ws) return fail(FB_ERR_ARG, "fb_fwd: workspace required");
   cudaStream_t s = (cudaStream_t)stream;
+  if (p->engine == FB_ENGINE_SINGLE) prep_wait(p, s);  // tp_fwd waits after its pass 1
   return p->engine == FB_ENGINE_SINGLE ? sp_fwd(p, u, y, B, s) : tp_fwd(p, u, y, B, ws, s);
 }
 
@@ -278,7 +311,10 @@ int fb_fwd_save(fb_plan* p, const void* u, void* y, void* saved, int64_t B, void
   int rc = check_run(p, B, "fb_fwd_save");
   if (rc) return rc;
   if (!u || !y) return fail(FB_ERR_ARG, "fb_fwd_save: null tensor");
-  if (p->use_tc) return tc_fwd(p, u, y, B, (cudaStream_t)stream, saved);
+  if (p->use_tc) {
+    prep_wait(p, (cudaStream_t)stream);
+    return tc_fwd(p, u, y, B, (cudaStream_t)stream, saved);
+  }
   if (!ws) return fail(FB_ERR_ARG, "fb_fwd_save: workspace required");
   return tp_fwd(p, u, y, B, ws, (cudaStream_t)stream, saved);
 }
@@ -290,6 +326,7 @@ int fb_bwd_saved(fb_plan* p, const void* dy, const void* u, const void* saved, v
   int rc = check_run(p, B, "fb_bwd_saved");
   if (rc) return rc;
   if (!dy || !du || !dK || !dD || !ws) return fail(FB_ERR_ARG, "fb_bwd_saved: null argument");
+  prep_wait(p, (cudaStream_t)stream);
   if (p->use_tc) return tc_bwd(p, dy, u, du, dK, dKbar, dD, B, ws, (cudaStream_t)stream, saved);
   return tp_bwd(p, dy, u, du, dK, dKbar, dD, B, ws, (cudaStream_t)stream, saved);
 }
@@ -300,6 +337,7 @@ int fb_bwd(fb_plan* p, const void* dy, const void* u, void* du, float* dK, float
   if (rc) return rc;
   if (!dy || !u || !du || !dK || !dD || !ws) return fail(FB_ERR_ARG, "fb_bwd: null argument");
   cudaStream_t s = (cudaStream_t)stream;
+  prep_wait(p, s);
   return p->engine == FB_ENGINE_SINGLE ? sp_bwd(p, dy, u, du, dK, dKbar, dD, B, ws, s)
                                        : tp_bwd(p, dy, u, du, dK, dKbar, dD, B, ws, s);
 }

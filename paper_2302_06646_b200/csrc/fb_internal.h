@@ -35,6 +35,11 @@ struct fb_plan {
   int smooth_domain = FB_SMOOTH_TIME;
   int num_sms = 148;
   int64_t head0 = 0;  // first global head of this plan (dropout child streams)
+  // three-pass: the kernel prep and the backward's dK tail run on an auxiliary
+  // stream, overlapping pass 1 / pass 3 of the signals (fork / join by events)
+  cudaStream_t aux = nullptr;
+  cudaEvent_t ev_fork = nullptr, ev_prep = nullptr, ev_join = nullptr;
+  bool prep_async = false;  // ev_prep guards kbar / kf / D / keep
 };
 
 struct fb_learned_plan {
@@ -105,6 +110,10 @@ int regularize_bank_dev(fb_plan* p, const float* K, cudaStream_t s);
 int dropout_keep_dev(fb_plan* p, double rate, uint64_t seed, cudaStream_t s);
 // dK = chain(dKbar) through dropout/smooth/squash, per head; dkbar_in [H][N]
 int regularizer_backward_dev(fb_plan* p, const float* dkbar, float* dK, cudaStream_t s);
+// make `s` wait for an asynchronous kernel prep (no-op otherwise)
+inline void prep_wait(const fb_plan* p, cudaStream_t s) {
+  if (p->prep_async) cudaStreamWaitEvent(s, p->ev_prep, 0);
+}
 
 // learned (fb_learned.cu)
 size_t lb_workspace(const fb_learned_plan* p, int64_t B);

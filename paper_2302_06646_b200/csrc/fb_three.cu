@@ -1385,11 +1385,13 @@ int tp_fwd(fb_plan* p, const void* u, void* y, int64_t B, void* ws, cudaStream_t
         rc = FB_ERR_UNSUPPORTED;
         return;
       }
+      prep_wait(p, s);  // pass 1 ran alongside an asynchronous kernel prep
       if ((rc = tc_rows_fwd(p, x1, usave, npairs, s))) return;
       launch_pass3<ST, IO, 0>(p, x1, (const IO*)u, (IO*)y, nullptr, (int)B, (int)npairs, 1.f, s);
       return;
     }
     launch_pass1<IO, ST, 0>(p, (const IO*)u, nullptr, x1, nullptr, nullptr, (int)B, (int)npairs, s);
+    prep_wait(p, s);
     const size_t sm = pass2_smem<ST>();
     auto k2 = tp_pass2_kernel<ST, 0>;
     cudaFuncSetAttribute(k2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
@@ -1463,18 +1465,26 @@ int tp_bwd(fb_plan* p, const void* dy, const void* u, void* du, float* dK, float
       k2<<<(unsigned)(p->H * p->m), kL / 16, sm, s>>>(x1dy, x1u, p->kf, wdk, p->tw_l, (int)npairs,
                                                        (int)p->H, (int)p->m);
     }
-    launch_pass3<ST, IO, 0>(p, x1dy, (const IO*)dy, (IO*)du, nullptr, (int)B, (int)npairs, 1.f, s);
+    // the dK tail (dK rows -> dKbar, dD, regularizer chain rule) on the
+    // auxiliary stream, alongside pass 3 of du
+    cudaStream_t ts = s;
+    if (p->aux && !cudaEventRecord(p->ev_fork, s) && !cudaStreamWaitEvent(p->aux, p->ev_fork, 0))
+      ts = p->aux;
     launch_pass3<float, float, 1>(p, reinterpret_cast<const CxT<float>*>(wdk), nullptr, nullptr,
-                                  dkbar, 2, 1, 1.0f / (float)p->n, s);
+                                  dkbar, 2, 1, 1.0f / (float)p->n, ts);
+    if (usave || tcr)
+      tp_dd_lag0_kernel<<<(unsigned)((p->H + 127) / 128), 128, 0, ts>>>(dkbar, dD, (int)p->H, p->N);
+    else
+      tp_dd_reduce_kernel<<<(unsigned)p->H, 32, 0, ts>>>(ddpart, dD, (int)(npairs * gx));
+    if (int r2 = regularizer_backward_dev(p, dkbar, dK, ts)) rc = r2;
+    launch_pass3<ST, IO, 0>(p, x1dy, (const IO*)dy, (IO*)du, nullptr, (int)B, (int)npairs, 1.f, s);
+    if (ts != s) {  // join
+      cudaEventRecord(p->ev_join, ts);
+      cudaStreamWaitEvent(s, p->ev_join, 0);
+    }
   });
-  if (usave || tcr)
-    tp_dd_lag0_kernel<<<(unsigned)((p->H + 127) / 128), 128, 0, s>>>(dkbar, dD, (int)p->H, p->N);
-  else
-    tp_dd_reduce_kernel<<<(unsigned)p->H, 32, 0, s>>>(ddpart, dD, (int)(npairs * gx));
   if (rc) return rc;
-  rc = cuda_status(cudaGetLastError(), "tp_bwd");
-  if (rc) return rc;
-  return regularizer_backward_dev(p, dkbar, dK, s);
+  return cuda_status(cudaGetLastError(), "tp_bwd");
 }
 
 }  // namespace fb
