@@ -523,13 +523,19 @@ __device__ __forceinline__ void epi_A_exit(const Ctx& c) {
   uint32_t t2, g;
   coords(t2, g);
   unsigned char* op = c.sm + c.sop;
+  constexpr uint32_t Q = kColsPer / 16;
+  float rr[Q][16], ii[Q][16];  // all of the thread's columns in flight, one wait
 #pragma unroll
-  for (uint32_t q = 0; q < kColsPer / 16; ++q) {
+  for (uint32_t q = 0; q < Q; ++q) {
+    tld<16>(taddr(c, c.tw + kColsPer * g + 16 * q), rr[q]);
+    tld<16>(taddr(c, c.tw + 64 + kColsPer * g + 16 * q), ii[q]);
+  }
+  tc::ld_wait();
+#pragma unroll
+  for (uint32_t q = 0; q < Q; ++q) {
     const uint32_t cb = kColsPer * g + 16 * q;
-    float re[16], im[16];
-    tld<16>(taddr(c, c.tw + cb), re);
-    tld<16>(taddr(c, c.tw + 64 + cb), im);
-    tc::ld_wait();
+    float* re = rr[q];
+    float* im = ii[q];
     twiddle_row<-1>(re, im, c.tab, t2, cb);
     if constexpr (W3) {  // planes [-Xi | Xr | Xi]
       st8n<T>(op + off_bmn(cb, t2), im);
@@ -553,13 +559,19 @@ __device__ __forceinline__ void epi_Bp_exit(const Ctx& c) {
   uint32_t t2, g;
   coords(t2, g);
   unsigned char* op = c.sm + c.sop;
+  constexpr uint32_t Q = kColsPer / 16;
+  float rr[Q][16], ii[Q][16];
 #pragma unroll
-  for (uint32_t q = 0; q < kColsPer / 16; ++q) {
+  for (uint32_t q = 0; q < Q; ++q) {
+    tld<16>(taddr(c, c.tw + kColsPer * g + 16 * q), rr[q]);
+    tld<16>(taddr(c, c.tw + 64 + kColsPer * g + 16 * q), ii[q]);
+  }
+  tc::ld_wait();
+#pragma unroll
+  for (uint32_t q = 0; q < Q; ++q) {
     const uint32_t cb = kColsPer * g + 16 * q;
-    float re[16], im[16];
-    tld<16>(taddr(c, c.tw + cb), re);
-    tld<16>(taddr(c, c.tw + 64 + cb), im);
-    tc::ld_wait();
+    float* re = rr[q];
+    float* im = ii[q];
     twiddle_row<+1>(re, im, c.tab, t2, cb);
     st8<T>(op + off_kmaj(t2, cb, 16384), re);
     st8<T>(op + off_kmaj(t2, cb + 8, 16384), re + 8);
