@@ -1061,14 +1061,24 @@ __global__ void __launch_bounds__(kThreads, 1)
       coords(f2, g);
       unsigned char* op = c.sm + c.sop;
 #pragma unroll
-      for (uint32_t q = 0; q < kColsPer / 8; ++q) {
-        const uint32_t cb = kColsPer * g + 8 * q;
-        float re[8], im[8], kr[8], ki[8];
-        tld<8>(taddr(c, c.tw + cb), re);
-        tld<8>(taddr(c, c.tw + 64 + cb), im);
-        tld<8>(taddr(c, c.aux + cb), kr);
-        tld<8>(taddr(c, c.aux + 64 + cb), ki);
-        tc::ld_wait();
+      for (uint32_t q2 = 0; q2 < kColsPer / 16; ++q2) {
+       float re2[2][8], im2[2][8], kr2[2][8], ki2[2][8];  // 16 columns per TMEM wait
+#pragma unroll
+       for (uint32_t hh = 0; hh < 2; ++hh) {
+        const uint32_t cb = kColsPer * g + 16 * q2 + 8 * hh;
+        tld<8>(taddr(c, c.tw + cb), re2[hh]);
+        tld<8>(taddr(c, c.tw + 64 + cb), im2[hh]);
+        tld<8>(taddr(c, c.aux + cb), kr2[hh]);
+        tld<8>(taddr(c, c.aux + 64 + cb), ki2[hh]);
+       }
+       tc::ld_wait();
+#pragma unroll
+       for (uint32_t hh = 0; hh < 2; ++hh) {
+        const uint32_t cb = kColsPer * g + 16 * q2 + 8 * hh;
+        float* re = re2[hh];
+        float* im = im2[hh];
+        const float* kr = kr2[hh];
+        const float* ki = ki2[hh];
         if (usave) {
           uint4* us = reinterpret_cast<uint4*>(usave + row * kN + 64 * f2 + cb);
           us[0] = make_uint4(pack2<T>(re[0], im[0]), pack2<T>(re[1], im[1]), pack2<T>(re[2], im[2]),
@@ -1085,6 +1095,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         st8<T>(op + off_bmn(cb, f2), re);
         st8<T>(op + 16384 + off_bmn(cb, f2), im);
         st8n<T>(op + 32768 + off_bmn(cb, f2), re);
+       }
       }
       TT_END(19)
     }
