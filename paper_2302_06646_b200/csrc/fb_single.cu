@@ -451,27 +451,40 @@ __global__ void __launch_bounds__(FftShape<LOG2N>::T, 2)
   const size_t base = (size_t)h * N;
   float* row = reinterpret_cast<float*>(work);
   __syncthreads();
+  // time smoothing: the squash mask 1[kbar != 0] applied once per element
+  // (row holds the masked dKbar; the tap sum below is reg_grad's, same order)
+  const bool tsm = !freq;
 #pragma unroll
   for (int r = 0; r < 16; ++r) {
     const uint32_t t = j + r * S::stride;
     if (t < N) {
       const float g = v[r].x * s;
-      row[t] = g;
+      row[t] = (tsm && __ldg(kbar + base + t) == 0.f) ? 0.f : g;
       if (dkbar_out) dkbar_out[base + t] = g;
+      if (t == 0 && dd_lag0) dD[h] = g;
     }
   }
   __syncthreads();
-  for (uint32_t t = j; t < N; t += S::T)
-    dK[base + t] = reg_grad(kbar + base, row, keep ? keep + base : nullptr, t, N, p, keep_scale,
-                            freq);
-  if (j == 0) {
-    if (dd_lag0) {
-      dD[h] = row[0];
-    } else {
-      float t = 0.f;
-      for (int c = 0; c < chunks; ++c) t += ddpart[(size_t)h * chunks + c];
-      dD[h] = t;
+  if (tsm) {
+    const double w = (double)(2 * p + 1);
+    for (uint32_t t = j; t < N; t += S::T) {
+      const int64_t lo = (int64_t)t >= p ? (int64_t)t - p : 0;
+      const int64_t hi = ((int64_t)t + p < (int64_t)N - 1) ? (int64_t)t + p : (int64_t)N - 1;
+      double acc = 0.0;
+      for (int64_t q = lo; q <= hi; ++q) acc += (double)row[q];
+      double g = acc / w;
+      if (keep) g = keep[base + t] ? g * keep_scale : 0.0;
+      dK[base + t] = (float)g;
     }
+  } else {
+    for (uint32_t t = j; t < N; t += S::T)
+      dK[base + t] = reg_grad(kbar + base, row, keep ? keep + base : nullptr, t, N, p, keep_scale,
+                              freq);
+  }
+  if (j == 0 && !dd_lag0) {
+    float t = 0.f;
+    for (int c = 0; c < chunks; ++c) t += ddpart[(size_t)h * chunks + c];
+    dD[h] = t;
   }
 }
 
