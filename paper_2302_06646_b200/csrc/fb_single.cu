@@ -94,11 +94,33 @@ __global__ void __launch_bounds__(FftShape<LOG2N>::T, 2)
   // the fp64 regularizer once per element in a rolled loop (its code inlined
   // sixteen times next to the FFT thrashed the instruction cache), staged in smem
   float* kb = reinterpret_cast<float*>(work);
+  if (!freq && (size_t)N * 12 <= (size_t)S::work_len * sizeof(float2)) {
+    // time smoothing: dropout(K) converted to fp64 once per element into
+    // smem, then reg_value's tap sum (same order, same rounding) from there
+    double* kd = reinterpret_cast<double*>(work);
+    kb = reinterpret_cast<float*>(kd + N);
+    for (uint32_t t = j; t < N; t += S::T) kd[t] = dropped(K, keep, keep_scale, base + t);
+    __syncthreads();
+    const double inv_w = 1.0 / (double)(2 * p + 1);
 #pragma unroll 1
-  for (uint32_t t = j; t < N; t += S::T) {
-    const float kv = reg_value(K, keep, keep_scale, base, t, N, p, lambda, freq);
-    kbar[base + t] = kv;
-    kb[t] = kv;
+    for (uint32_t t = j; t < N; t += S::T) {
+      const int64_t lo = (int64_t)t >= p ? (int64_t)t - p : 0;
+      const int64_t hi = ((int64_t)t + p < (int64_t)N - 1) ? (int64_t)t + p : (int64_t)N - 1;
+      double acc = 0.0;
+      for (int64_t q = lo; q <= hi; ++q) acc += kd[q];
+      const double sv = acc * inv_w;
+      const double mag = fabs(sv) - lambda;
+      const float kv = mag > 0.0 ? (float)copysign(mag, sv) : 0.0f;
+      kbar[base + t] = kv;
+      kb[t] = kv;
+    }
+  } else {
+#pragma unroll 1
+    for (uint32_t t = j; t < N; t += S::T) {
+      const float kv = reg_value(K, keep, keep_scale, base, t, N, p, lambda, freq);
+      kbar[base + t] = kv;
+      kb[t] = kv;
+    }
   }
   __syncthreads();
   float2 v[16];
