@@ -117,6 +117,12 @@ __device__ __forceinline__ void dft_reg(float2 (&v)[R]) {
 __device__ __forceinline__ uint32_t pad16(uint32_t e) { return e + (e >> 4); }
 __host__ __device__ constexpr uint32_t padded_len(uint32_t n) { return n + (n >> 4); }
 
+// Division / remainder by a runtime power of two (every transform size,
+// batch and column-tile width here is one): a shift and a mask instead of the
+// integer-division sequence.
+__device__ __forceinline__ uint32_t pdiv(uint32_t a, uint32_t b) { return a >> (__ffs(b) - 1); }
+__device__ __forceinline__ uint32_t pmod(uint32_t a, uint32_t b) { return a & (b - 1); }
+
 // Twiddle lookup exp(SIGN * 2 pi i * t / n) from a table of exp(-2 pi i t/n).
 template <int SIGN>
 __device__ __forceinline__ float2 tw_lookup(const float2* __restrict__ tw, uint32_t t) {
@@ -134,11 +140,11 @@ template <int SIGN, int R>
 __device__ __forceinline__ void stockham_load_twiddle(const float2* s, float2 (&v)[R], uint32_t j,
                                                       uint32_t c, uint32_t n, uint32_t batch,
                                                       uint32_t Ns, const float2* __restrict__ tw) {
-  const uint32_t stride = n / R;
+  const uint32_t stride = pdiv(n, R);
 #pragma unroll
   for (int r = 0; r < R; ++r) v[r] = s[pad16(j + r * stride) * batch + c];
   if (Ns > 1) {
-    const uint32_t base = (j % Ns) * (n / (Ns * R));
+    const uint32_t base = pmod(j, Ns) * pdiv(n, Ns * R);
 #pragma unroll
     for (int r = 1; r < R; ++r) v[r] = cmul(v[r], tw_lookup<SIGN>(tw, r * base));
   }
@@ -147,7 +153,7 @@ __device__ __forceinline__ void stockham_load_twiddle(const float2* s, float2 (&
 template <int R>
 __device__ __forceinline__ void stockham_store(float2* s, const float2 (&v)[R], uint32_t j,
                                                uint32_t c, uint32_t batch, uint32_t Ns) {
-  const uint32_t idxD = (j / Ns) * Ns * R + (j % Ns);
+  const uint32_t idxD = pdiv(j, Ns) * Ns * R + pmod(j, Ns);
 #pragma unroll
   for (int r = 0; r < R; ++r) s[pad16(idxD + r * Ns) * batch + c] = v[r];
 }
@@ -157,7 +163,7 @@ template <int SIGN, int R>
 __device__ __forceinline__ void stockham_twiddle(float2 (&v)[R], uint32_t j, uint32_t n, uint32_t Ns,
                                                  const float2* __restrict__ tw) {
   if (Ns > 1) {
-    const uint32_t base = (j % Ns) * (n / (Ns * R));
+    const uint32_t base = pmod(j, Ns) * pdiv(n, Ns * R);
 #pragma unroll
     for (int r = 1; r < R; ++r) v[r] = cmul(v[r], tw_lookup<SIGN>(tw, r * base));
   }
@@ -181,7 +187,7 @@ __device__ __forceinline__ void smem_passes(float2* s, uint32_t n, uint32_t batc
 #pragma unroll
         for (int g = 0; g < G; ++g) {
           const uint32_t q = tid + g * blockDim.x;
-          const uint32_t c = q % batch, j = q / batch;
+          const uint32_t c = pmod(q, batch), j = pdiv(q, batch);
           stockham_load_twiddle<SIGN, SMALL>(s, v[g], j, c, n, batch, Ns, tw);
           dft_reg<SIGN, SMALL>(v[g]);
         }
@@ -189,14 +195,14 @@ __device__ __forceinline__ void smem_passes(float2* s, uint32_t n, uint32_t batc
 #pragma unroll
         for (int g = 0; g < G; ++g) {
           const uint32_t q = tid + g * blockDim.x;
-          stockham_store<SMALL>(s, v[g], q / batch, q % batch, batch, Ns);
+          stockham_store<SMALL>(s, v[g], pdiv(q, batch), pmod(q, batch), batch, Ns);
         }
         __syncthreads();
       }
       Ns *= SMALL;
     } else {
       float2 v[16];
-      const uint32_t c = tid % batch, j = tid / batch;
+      const uint32_t c = pmod(tid, batch), j = pdiv(tid, batch);
       stockham_load_twiddle<SIGN, 16>(s, v, j, c, n, batch, Ns, tw);
       dft_reg<SIGN, 16>(v);
       __syncthreads();

@@ -685,7 +685,7 @@ __global__ void __launch_bounds__(kBigThreads, 1)
   const uint32_t cmax = causal ? m / 2 : m;
   float dd = 0.f;
   for (uint32_t i = threadIdx.x; i < kBigTile; i += kBigThreads) {
-    const uint32_t e = i / TAU, c = i % TAU;
+    const uint32_t e = pdiv(i, TAU), c = pmod(i, TAU);
     const uint32_t t = e * kL + tau0 + c;
     const bool ok = e < cmax && t < N;
     float2 v = make_float2(0.f, 0.f), w = make_float2(0.f, 0.f);
@@ -710,7 +710,7 @@ __global__ void __launch_bounds__(kBigThreads, 1)
   CxT<ST>* oa = out_a + ((size_t)pr * H + h) * (size_t)m * kL;
   CxT<ST>* ob = SRC == 1 ? out_b + ((size_t)pr * H + h) * (size_t)m * kL : nullptr;
   for (uint32_t i = threadIdx.x; i < kBigTile; i += kBigThreads) {
-    const uint32_t a = i / TAU, c = i % TAU;
+    const uint32_t a = pdiv(i, TAU), c = pmod(i, TAU);
     const float2 w = tw_big<-1>(tb, a * (tau0 + c));
     stc<ST>(&oa[(size_t)a * kL + tau0 + c].x, cmul(sa[pad16(a) * TAU + c], w));
     if constexpr (SRC == 1) stc<ST>(&ob[(size_t)a * kL + tau0 + c].x, cmul(sb[pad16(a) * TAU + c], w));
@@ -741,7 +741,7 @@ __global__ void __launch_bounds__(kBigThreads, 1)
   const int h = blockIdx.y, pr = blockIdx.z;
   const CxT<ST>* src = w_in + ((size_t)pr * H + h) * (size_t)m * kL;
   for (uint32_t i = threadIdx.x; i < kBigTile; i += kBigThreads) {
-    const uint32_t a = i / TAU, c = i % TAU;
+    const uint32_t a = pdiv(i, TAU), c = pmod(i, TAU);
     tsm[pad16(a) * TAU + c] = cmul(cx_load(src + (size_t)a * kL + tau0 + c), tw_big<+1>(tb, a * (tau0 + c)));
   }
   __syncthreads();
@@ -753,7 +753,7 @@ __global__ void __launch_bounds__(kBigThreads, 1)
     const float d = __ldg(D + h);
     const size_t o0 = ((size_t)b0 * H + h) * N, o1 = ((size_t)b1 * H + h) * N;
     for (uint32_t i = threadIdx.x; i < cmax * TAU; i += kBigThreads) {
-      const uint32_t cc = i / TAU, c = i % TAU;
+      const uint32_t cc = pdiv(i, TAU), c = pmod(i, TAU);
       const uint32_t t = cc * kL + tau0 + c;
       if (t < N) {
         const float2 v = tsm[pad16(cc) * TAU + c];
@@ -763,7 +763,7 @@ __global__ void __launch_bounds__(kBigThreads, 1)
     }
   } else {
     for (uint32_t i = threadIdx.x; i < cmax * TAU; i += kBigThreads) {
-      const uint32_t cc = i / TAU, c = i % TAU;
+      const uint32_t cc = pdiv(i, TAU), c = pmod(i, TAU);
       const uint32_t t = cc * kL + tau0 + c;
       if (t < N) dkbar[(size_t)h * N + t] = tsm[pad16(cc) * TAU + c].x * scale;
     }
@@ -851,7 +851,7 @@ __global__ void __launch_bounds__(kBigThreads, SRC == 1 ? 1 : 2)
     const IO* sv = reinterpret_cast<const IO*>(ring + (size_t)sg * stage_bytes);
     float dd = 0.f;
     for (uint32_t i = threadIdx.x; i < kBigTile; i += kBigThreads) {
-      const uint32_t e = i / TAU, c = i % TAU;
+      const uint32_t e = pdiv(i, TAU), c = pmod(i, TAU);
       const bool ok = e < (uint32_t)rows;
       float2 v = make_float2(0.f, 0.f);
       if (ok) {
@@ -874,9 +874,9 @@ __global__ void __launch_bounds__(kBigThreads, SRC == 1 ? 1 : 2)
     if constexpr (SRC == 1) smem_passes<-1, SMALL>(sb, m, TAU, 1, m, tw_m);
     CxT<ST>* oa = out_a + ((size_t)pr * H + h) * (size_t)m * kL;
     CxT<ST>* ob = SRC == 1 ? out_b + ((size_t)pr * H + h) * (size_t)m * kL : nullptr;
-    ColTw<-1> ctw(tb, threadIdx.x / TAU, tau0 + threadIdx.x % TAU, kBigThreads / TAU);
+    ColTw<-1> ctw(tb, pdiv(threadIdx.x, TAU), tau0 + pmod(threadIdx.x, TAU), pdiv(kBigThreads, TAU));
     for (uint32_t i = threadIdx.x; i < kBigTile; i += kBigThreads) {
-      const uint32_t a = i / TAU, c = i % TAU;
+      const uint32_t a = pdiv(i, TAU), c = pmod(i, TAU);
       const float2 w = ctw.next();
       if constexpr (PLANAR) {
         const float2 x = cmul(sa[pad16(a) * TAU + c], w);
@@ -954,9 +954,9 @@ __global__ void __launch_bounds__(kBigThreads, 1)
     ptx::mbar_wait(&full[sg], (uint32_t)(it / kBigStages) & 1);
     const unsigned char* base = ring + (size_t)sg * stage_bytes;
     const CxT<ST>* sw = reinterpret_cast<const CxT<ST>*>(base);
-    ColTw<+1> ctw(tb, threadIdx.x / TAU, tau0 + threadIdx.x % TAU, kBigThreads / TAU);
+    ColTw<+1> ctw(tb, pdiv(threadIdx.x, TAU), tau0 + pmod(threadIdx.x, TAU), pdiv(kBigThreads, TAU));
     for (uint32_t i = threadIdx.x; i < kBigTile; i += kBigThreads) {
-      const uint32_t a = i / TAU, c = i % TAU;
+      const uint32_t a = pdiv(i, TAU), c = pmod(i, TAU);
       tsm[pad16(a) * TAU + c] = cmul(cx_load(sw + a * TAU + c), ctw.next());
     }
     __syncthreads();
@@ -968,7 +968,7 @@ __global__ void __launch_bounds__(kBigThreads, 1)
       const float d = __ldg(D + h);
       const size_t o0 = ((size_t)b0 * H + h) * N, o1 = ((size_t)b1 * H + h) * N;
       for (uint32_t i = threadIdx.x; i < (uint32_t)rows * TAU; i += kBigThreads) {
-        const uint32_t cc = i / TAU, c = i % TAU;
+        const uint32_t cc = pdiv(i, TAU), c = pmod(i, TAU);
         const uint32_t tt = cc * kL + tau0 + c;
         const float2 v = tsm[pad16(cc) * TAU + c];
         st(out + o0 + tt, fmaf(d, tof(sk[cc * TAU + c]), v.x));
@@ -976,7 +976,7 @@ __global__ void __launch_bounds__(kBigThreads, 1)
       }
     } else {
       for (uint32_t i = threadIdx.x; i < (uint32_t)rows * TAU; i += kBigThreads) {
-        const uint32_t cc = i / TAU, c = i % TAU;
+        const uint32_t cc = pdiv(i, TAU), c = pmod(i, TAU);
         dkbar[(size_t)h * N + cc * kL + tau0 + c] = tsm[pad16(cc) * TAU + c].x * scale;
       }
     }
@@ -1002,7 +1002,7 @@ __global__ void __launch_bounds__(kBigThreads, 1)
   const uint32_t c0 = blockIdx.x * TAU;
   const size_t ch = (size_t)blockIdx.y * m * lp;
   for (uint32_t i = threadIdx.x; i < kBigTile; i += kBigThreads) {
-    const uint32_t e = i / TAU, c = i % TAU;
+    const uint32_t e = pdiv(i, TAU), c = pmod(i, TAU);
     float2 v = __ldg(in + ch + (size_t)e * lp + c0 + c);
     if (SIGN > 0) v = cmul(v, tw_big<+1>(tb, e * (tau0 + c0 + c)));
     tsm[pad16(e) * TAU + c] = v;
@@ -1010,7 +1010,7 @@ __global__ void __launch_bounds__(kBigThreads, 1)
   __syncthreads();
   smem_passes<SIGN, SMALL>(tsm, m, TAU, 1, m, tw_m);
   for (uint32_t i = threadIdx.x; i < kBigTile; i += kBigThreads) {
-    const uint32_t a = i / TAU, c = i % TAU;
+    const uint32_t a = pdiv(i, TAU), c = pmod(i, TAU);
     float2 v = tsm[pad16(a) * TAU + c];
     v = SIGN < 0 ? cmul(v, tw_big<-1>(tb, a * (tau0 + c0 + c))) : cscale(v, scale);
     out[ch + (size_t)a * lp + c0 + c] = v;
