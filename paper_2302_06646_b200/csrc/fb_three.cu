@@ -1178,7 +1178,6 @@ uint32_t launch_pass1(const fb_plan* p, const IO* a, const IO* b, CxT<ST>* oa, C
       if (maps) return kL / kTB;
     }
   }
-  if (planar && p->m <= 16) return 0;
   if (p->m <= 16) {
     with_m(p->m, [&](auto mc) {
       constexpr int M = decltype(mc)::value;
