@@ -85,6 +85,29 @@ def test_dropout_training_mode(lc):
     assert_parity(got, want, 1e-5)
 
 
+@pytest.mark.parametrize("dtype,tol", [(torch.float32, 1e-5), (torch.bfloat16, 2e-2)])
+def test_dropout_training_three_pass(lc, dtype, tol):
+    """Three-pass training step with kernel dropout: the prep (mask, Kbar,
+    kernel spectrum) runs on the plan's auxiliary stream and the dK tail
+    (regularizer chain rule through the mask) forks off the backward; two
+    steps back to back on one plan, each against the oracle."""
+    N, H, B = 16384, 3, 3
+    plan = None
+    for seed in (7, 8):
+        inp = layer_inputs(lc, B, H, N, dtype, seeds=(seed, seed + 10, seed + 20))
+        cfg = fb.RegularizationConfig(lambda_=0.003, smooth_width=1, dropout_rate=0.2, seed=seed)
+        if plan is None:
+            plan = fb.LongConvPlan(N, H, fb.ConvMode.CAUSAL, dtype, fb.Engine.THREE_PASS)
+        plan.prep(inp["tK"], inp["tD"], cfg, True)
+        y = plan.forward(inp["tu"])
+        du, dK, dD = plan.backward(inp["tdy"], inp["tu"])
+        torch.cuda.synchronize()
+        got = dict(y=to_np(y), du=to_np(du), dK=to_np(dK), dD=to_np(dD), kbar=to_np(plan.kbar()))
+        want = oracle_layer(lc, inp, cfg, training=True)
+        assert np.array_equal(got["kbar"] == 0, want["kbar"] == 0)
+        assert_parity(got, want, tol, keys=("y", "du", "dK", "dD", "kbar"))
+
+
 def test_smooth_frequency(lc):
     inp = layer_inputs(lc, 2, 2, 256, torch.float32)
     cfg = fb.RegularizationConfig(lambda_=0.01, smooth_width=2,
