@@ -120,40 +120,47 @@ def _traffic(config, direction):
     return json.loads(prof.read_text()).get(f"config{config}", {}).get(direction)
 
 
-def alg_bytes(cfg, s):
-    """Algorithmic HBM bytes per step."""
-    E = cfg["B"] * cfg["H"] * cfg["N"]
-    HN = cfg["H"] * cfg["N"]
-    if cfg["engine"] == "three":
-        return 25 * s * E + 48 * HN
-    return 5 * s * E + 32 * HN
+def alg_bytes(B, H, N, s, three_pass):
+    """Algorithmic HBM bytes per step, for the engine the plan
+    resolved to: single-pass 5sE + 32HN, three-pass 25sE + 48HN."""
+    E, HN = B * H * N, H * N
+    return 25 * s * E + 48 * HN if three_pass else 5 * s * E + 32 * HN
 
 
-def run_ours(args, cfg, rank, world, local_rank):
+def kernel_alg_bytes(B, H, N, s, three_pass):
+    """Algorithmic bytes of one launch of the forward's / backward's main
+    kernel: single-pass fwd reads u, writes y, reads k_f
+    (2sE + 16HN), bwd reads dy and u, writes du, reads k_f (3sE + 16HN);
+    three-pass rows kernels move the complex intermediate (2s bytes per real
+    element per sweep): fwd reads X1, writes W, reads the Kf2 rows
+    (4sE + 16HN); bwd reads dy's rows and U, writes du's rows, reads Kf2,
+    writes the dK rows (6sE + 32HN)."""
+    E, HN = B * H * N, H * N
+    if three_pass:
+        return 4 * s * E + 16 * HN, 6 * s * E + 32 * HN
+    return 2 * s * E + 16 * HN, 3 * s * E + 16 * HN
+
+
+def _timed_layer(args, fb, _lib, cfg, dev, Hloc, head0, clk=None):
+    """Build one plan for Hloc heads (global heads head0 ..) and time
+    args.steps training steps (K1 prep + fwd + bwd) after args.warmup
+    warm-up steps.  Returns a dict of timings and the plan / tensors."""
+    import ctypes as C
+
     import torch
 
-    import paper_2302_06646_b200 as fb
-    from paper_2302_06646_b200 import _lib
-
-    dev = torch.device("cuda", local_rank)
-    torch.cuda.set_device(dev)
-    dist = None
-    if world > 1:
-        import torch.distributed as dist
-
-        dist.init_process_group("nccl", device_id=dev)
     dt = {"f32": torch.float32, "bf16": torch.bfloat16, "f16": torch.float16}[cfg["dtype"]]
-    s = torch.tensor([], dtype=dt).element_size()
-    B, H, N = cfg["B"], cfg["H"], cfg["N"]
+    B, N, H = cfg["B"], cfg["N"], Hloc
     eng = {"auto": fb.Engine.AUTO, "single": fb.Engine.BUTTERFLY,
            "three": fb.Engine.THREE_PASS}[cfg["engine"]]
     g = torch.Generator(device=dev)
-    g.manual_seed(1234 + rank)
+    g.manual_seed(1234 + head0)
     # synthetic data (random-init kernels, geometric decay like init_kernels)
     u = torch.randn(B, H, N, device=dev, generator=g).to(dt)
     dy = torch.randn(B, H, N, device=dev, generator=g).to(dt)
     pos = torch.arange(N, device=dev, dtype=torch.float32) / N
-    decay = (H / 2.0) ** (torch.arange(H, device=dev, dtype=torch.float32) / H)
+    hh = torch.arange(head0, head0 + H, device=dev, dtype=torch.float32)
+    decay = (cfg["H"] / 2.0) ** (hh / cfg["H"])
     K = torch.randn(H, N, device=dev, generator=g) * torch.exp(-pos[None, :] * decay[:, None])
     D = torch.randn(H, device=dev, generator=g)
     rc = fb.RegularizationConfig(lambda_=LAM, smooth_width=P)
@@ -166,23 +173,21 @@ def run_ours(args, cfg, rank, world, local_rank):
     L = _lib.lib()
     stream = torch.cuda.current_stream()
     sp = stream.cuda_stream
-    import ctypes as C
-
     c = rc.to_c()
     P_ = lambda t: C.c_void_p(t.data_ptr())  # noqa: E731
     h = plan._h
-    n_events = []
-
     # training step: the forward keeps its transform of u for the backward
-    # (tensor-core plans; fb_saved_size is 0 otherwise and the calls recompute)
     nsaved = plan.saved_size(B)
     saved = torch.empty(max(nsaved, 1), dtype=torch.uint8, device=dev)
     Ps = P_(saved) if nsaved else C.c_void_p(0)
 
-    def step(rec=None):
+    def step(rec=None, kev=None):
         _lib.check(L.fb_kernel_prep(h, P_(K), P_(D), C.byref(c), 0, C.c_void_p(sp)))
         if rec is not None:
             rec[0].record(stream)
+            # the main kernels alone, bracketed on their launching stream
+            _lib.check(L.fb_plan_profile_events(h, 0, kev[0], kev[1]))
+            _lib.check(L.fb_plan_profile_events(h, 1, kev[2], kev[3]))
         _lib.check(L.fb_fwd_save(h, P_(u), P_(y), Ps, B, P_(ws), C.c_void_p(sp)))
         if rec is not None:
             rec[1].record(stream)
@@ -191,35 +196,85 @@ def run_ours(args, cfg, rank, world, local_rank):
         if rec is not None:
             rec[2].record(stream)
 
-    recs = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(args.steps)]
-    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    # the sampler runs from warm-up through the timed region (nvidia-smi polls
-    # every ~50 ms; a short timed region alone would see one sample)
-    with ClockSampler(local_rank) as clk:
-        for _ in range(args.warmup):
-            step()
-        torch.cuda.synchronize()
-        if dist:
-            dist.barrier()
-        torch.cuda.synchronize()
+    Ev = lambda: torch.cuda.Event(enable_timing=True)  # noqa: E731
+    recs = [[Ev() for _ in range(3)] for _ in range(args.steps)]
+    kevs = [[Ev() for _ in range(4)] for _ in range(args.steps)]
+    for kv in kevs:  # materialise the cudaEvent_t handles
+        for e in kv:
+            e.record(stream)
+    torch.cuda.synchronize()
+    kptr = [[C.c_void_p(e.cuda_event) for e in kv] for kv in kevs]
+    t0, t1 = Ev(), Ev()
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    if torch.distributed.is_initialized():
+        torch.distributed.barrier()
+    torch.cuda.synchronize()
+    if clk is not None:
         clk.mark()
-        t0.record(stream)
-        for i in range(args.steps):
-            step(recs[i])
-        t1.record(stream)
-        torch.cuda.synchronize()
+    t0.record(stream)
+    for i in range(args.steps):
+        step(recs[i], kptr[i])
+    t1.record(stream)
+    torch.cuda.synchronize()
+    K_ = args.steps
+    return dict(
+        ms=t0.elapsed_time(t1), plan=plan, dt=dt, eng=eng, nsaved=nsaved, tensors=(u, dy, K, D),
+        fwd_ms=sum(r[0].elapsed_time(r[1]) for r in recs) / K_,
+        bwd_ms=sum(r[1].elapsed_time(r[2]) for r in recs) / K_,
+        kfwd_ms=sum(k[0].elapsed_time(k[1]) for k in kevs) / K_,
+        kbwd_ms=sum(k[2].elapsed_time(k[3]) for k in kevs) / K_)
+
+
+def run_ours(args, cfg, rank, world, local_rank):
+    import torch
+
+    import paper_2302_06646_b200 as fb
+    from paper_2302_06646_b200 import _lib
+    from paper_2302_06646_b200.seqshard import head_shard
+
+    dev = torch.device("cuda", local_rank)
+    torch.cuda.set_device(dev)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=dev)
+    B, H, N = cfg["B"], cfg["H"], cfg["N"]
+    # strong scaling (default): each rank owns head_shard(H, world, rank) of
+    # the configured job, no communication; weak scaling: every rank runs the
+    # full per-GPU job (second field when world > 1)
+    strong = args.scaling == "strong"
+    hs = head_shard(H, world, rank) if strong else slice(0, H)
+    Hloc = hs.stop - hs.start
+
+    def tmax(x):
+        t = torch.tensor([x], device=dev)
+        if dist:
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    with ClockSampler(local_rank) as clk:
+        r = _timed_layer(args, fb, _lib, cfg, dev, Hloc, hs.start, clk)
     if dist:
         dist.barrier()
-    ms = t0.elapsed_time(t1)
-    fwd_ms = sum(r[0].elapsed_time(r[1]) for r in recs) / args.steps
-    bwd_ms = sum(r[1].elapsed_time(r[2]) for r in recs) / args.steps
-    tmax = torch.tensor([ms], device=dev)
-    if dist:
-        dist.all_reduce(tmax, op=dist.ReduceOp.MAX)
-    ms = float(tmax.item())
-    ms_step = ms / args.steps
-    E = B * H * N
-    value = E * world / (ms_step / 1e3)
+    ms_step = tmax(r["ms"]) / args.steps
+    E_job = B * H * N if strong else B * H * N * world
+    value = E_job / (ms_step / 1e3)
+    other = None
+    if world > 1:  # the other scaling mode, same timing rules
+        r2 = _timed_layer(args, fb, _lib, cfg, dev, H if strong else H // world,
+                          0 if strong else head_shard(H, world, rank).start)
+        ms2 = tmax(r2["ms"]) / args.steps
+        E2 = B * H * N * world if strong else B * H * N
+        other = {"scaling": "weak" if strong else "strong", "value": E2 / (ms2 / 1e3),
+                 "ms_per_step": ms2, "heads_per_gpu": H if strong else H // world}
+        del r2
+    plan, dt = r["plan"], r["dt"]
+    s = torch.tensor([], dtype=dt).element_size()
+    u, dy, K, D = r["tensors"]
+    three = plan.engine == fb.Engine.THREE_PASS
 
     # ---------------- e2e: public API with host buffers, copies timed -------
     # fb_host_runner: heads in chunks, H2D / kernels / D2H overlapped on three
@@ -232,7 +287,10 @@ def run_ours(args, cfg, rank, world, local_rank):
     hdu = torch.empty_like(hu).pin_memory()
     hdK = torch.empty_like(hK).pin_memory()
     hdD = torch.empty_like(hD).pin_memory()
-    runner = fb.HostRunner(N, H, B, dt, engine=eng, heads_per_chunk=max(1, H // 8), device=dev)
+    rc = fb.RegularizationConfig(lambda_=LAM, smooth_width=P)
+    runner = fb.HostRunner(N, Hloc, B, dt, engine=r["eng"], heads_per_chunk=max(1, Hloc // 8),
+                           device=dev)
+    stream = torch.cuda.current_stream()
 
     def e2e_step():
         runner.run(hu, hdy, hK, hD, rc, out=(hy, hdu, hdK, hdD))
@@ -249,10 +307,8 @@ def run_ours(args, cfg, rank, world, local_rank):
         e2e_step()
     e1.record(stream)
     torch.cuda.synchronize()
-    ems = torch.tensor([e0.elapsed_time(e1) / e2e_steps], device=dev)
-    if dist:
-        dist.all_reduce(ems, op=dist.ReduceOp.MAX)
-    e2e_val = E * world / (float(ems.item()) / 1e3)
+    ems = tmax(e0.elapsed_time(e1) / e2e_steps)
+    e2e_val = E_job / (ems / 1e3)
     h2d = (hu.numel() + hdy.numel()) * s + (hK.numel() + hD.numel()) * 4
     d2h = (hy.numel() + hdu.numel()) * s + (hdK.numel() + hdD.numel()) * 4
 
@@ -264,65 +320,64 @@ def run_ours(args, cfg, rank, world, local_rank):
         return None
 
     hbm_peak, tc_peak, peak_kind = load_peaks()
-    # dominant kernel: the backward (K4a sp_bwd / K4b passes)
-    HN = H * N
-    # algorithmic bytes per launch: single-pass reads/writes each
-    # signal once plus k_f (8 B per bin, n = 2N bins per head); three-pass adds
-    # the complex intermediates (2s bytes per real element each, 2N-padded)
-    if plan.engine == fb.Engine.THREE_PASS:
-        bwd_bytes = 16 * s * E + 52 * HN
-        fwd_bytes = 11 * s * E + 16 * HN
+    # dominant kernel: the larger of the forward's / backward's main kernel,
+    # each timed alone by events the plan records around its launch
+    kb_fwd, kb_bwd = kernel_alg_bytes(B, Hloc, N, s, three)
+    if r["kbwd_ms"] >= r["kfwd_ms"]:
+        dom, dom_bytes, dom_ms = "bwd", kb_bwd, r["kbwd_ms"]
     else:
-        bwd_bytes = 3 * s * E + 16 * HN
-        fwd_bytes = 2 * s * E + 16 * HN
-    dom = "bwd" if bwd_ms >= fwd_ms else "fwd"
-    dom_bytes, dom_ms = (bwd_bytes, bwd_ms) if dom == "bwd" else (fwd_bytes, fwd_ms)
+        dom, dom_bytes, dom_ms = "fwd", kb_fwd, r["kfwd_ms"]
+    kname = {(False, True): f"tc_{dom}_kernel (tcgen05)", (False, False): f"sp_{dom}_kernel",
+             (True, True): f"tc_rows_{dom}_kernel (tcgen05)",
+             (True, False): "tp_pass2" + ("_bwd" if dom == "bwd" else "") + "_kernel"}
+    rows_tc = three and dt == torch.bfloat16
+    kern = kname[(three, plan.tensor_cores or rows_tc)]
     achieved = dom_bytes / (dom_ms / 1e3) / 1e9
-    step_bytes = alg_bytes(cfg, s)
-    prof = ROOT / "profiles" / "traffic.json"
-    traffic = None
-    if prof.exists():
-        traffic = json.loads(prof.read_text()).get(f"config{args.config}", {}).get(dom)
+    step_bytes = alg_bytes(B, Hloc, N, s, three)
+    traffic = _traffic(args.config if cfg["dtype"] == CONFIGS[args.config]["dtype"] else -1, dom)
     cpu = None
-    if not args.no_cpu_baseline:
+    if not args.no_cpu_baseline and world == 1:
         cpu = cpu_baseline(cfg, args.cpu_sample_heads)
     # our kernel launches per timed step (prep + fwd + bwd, training-step path):
     # single-pass: K1 spectrum, forward, backward, backward tail;
     # three-pass: regularize, kernel columns, kernel rows | pass 1, rows, pass 3 |
     # pass 1 (dy), rows, pass 3 (du), dK rows, dD, regularizer chain rule
-    launches_per_step = 12 if plan.engine == fb.Engine.THREE_PASS else 4
+    launches_per_step = 12 if three else 4
     out = {
         "metric": "long-conv fwd+bwd elements/sec (E=B*H*N per step: K1 prep + fwd + bwd)",
         "value": value, "unit": "elements/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": cfg["dtype"],
+        "scaling": "strong" if strong else "weak", "vs_baseline": None, "dtype": cfg["dtype"],
         "data": "synthetic (torch.randn signals, random geometric-decay kernels)",
         "config": {"workload": cfg["workload"], "B": B, "H": H, "N": N,
                    "engine": plan.engine.name.lower(), "transform_len": plan.n,
                    "lambda": LAM, "smooth_width": P, "mode": "causal",
-                   "sharding": f"heads, {H} per GPU, no communication",
-                   "saved_activation": ("bwd reuses the fwd transform of u "
-                                        f"({nsaved / 2**20:.0f} MiB, bf16)" if nsaved else None),
+                   "sharding": (f"heads: head_shard(H={H}, {world}, rank) = {Hloc} per GPU, "
+                                "no communication"),
+                   "saved_activation": (f"bwd reuses the fwd transform of u "
+                                        f"({r['nsaved'] / 2**20:.0f} MiB)" if r["nsaved"] else None),
                    "l2": "inputs larger than L2 (u, dy, y, du = "
-                         f"{4 * E * s / 2**20:.0f} MiB per GPU)"},
-        "fwd_ms": fwd_ms, "bwd_ms": bwd_ms,
-        "roofline": {"bound": "hbm",
-                     "kernel": (f"{dom}: tc_{dom}_kernel (tcgen05)" if plan.tensor_cores else
-                                f"{dom}: sp_{dom}_kernel" if plan.engine.name != "THREE_PASS" else
-                                f"{dom}: three-pass launches (pass 1 cols, pass 2 rows on "
-                                "tcgen05, pass 3 cols)"),
+                         f"{4 * B * Hloc * N * s / 2**20:.0f} MiB per GPU)"},
+        "fwd_ms": r["fwd_ms"], "bwd_ms": r["bwd_ms"],
+        "main_kernel_ms": {"fwd": r["kfwd_ms"], "bwd": r["kbwd_ms"]},
+        "roofline": {"bound": "hbm", "kernel": f"{dom}: {kern}",
                      "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
                      "frac": achieved / hbm_peak, "traffic": traffic,
-                     "alg_bytes_per_launch": dom_bytes, "peak_kind": peak_kind},
+                     "traffic_over_alg": (traffic / dom_bytes) if traffic else None,
+                     "alg_bytes_per_launch": dom_bytes, "launch_ms": dom_ms,
+                     "peak_kind": peak_kind},
         "step_roofline": {"alg_bytes": step_bytes,
+                          "formula": "25sE+48HN (three-pass)" if three else "5sE+32HN (single-pass)",
                           "achieved_GBs": step_bytes / (ms_step / 1e3) / 1e9,
                           "frac": step_bytes / (ms_step / 1e3) / 1e9 / hbm_peak},
         "e2e": {"value": e2e_val, "unit": "elements/s", "h2d_bytes_per_step": h2d,
-                "d2h_bytes_per_step": d2h, "ms_per_step": float(ems.item())},
+                "d2h_bytes_per_step": d2h, "ms_per_step": ems},
         "cpu_baseline": cpu,
         "clocks": clk.summary(),
         "gpu_launches": launches_per_step * args.steps,
     }
+    if other:
+        out["other_scaling"] = other
     print(json.dumps(out), flush=True)
     if dist:
         dist.destroy_process_group()
@@ -451,9 +506,13 @@ def run_learned(args, cfg, rank, world, local_rank):
 
 
 def reference_cpu_run(cfg, heads, steps=1, threads=None):
-    """Reference CPU path (oracle/_ref = unmodified reference sources):
-    regularized_long_conv(kButterfly, kCausal, threads=nproc) + the backward
-    composed from conv_butterfly.  Returns (elements, seconds)."""
+    """Reference CPU path (oracle/_ref = unmodified reference sources), one
+    step per call: regularize_bank once (regularize.cpp:93-107), the forward
+    regularized_long_conv(kButterfly, kCausal, threads) on that regularized
+    bank with the identity regularizer (lambda = 0, p = 0: no second
+    smooth/squash pass), the backward composed from conv_butterfly
+     and the regularizer chain rule.  Returns (elements,
+    seconds) over `steps` steps of B x heads x N."""
     import numpy as np
 
     from oracle.oracle import RefOracle, ref_available
@@ -484,14 +543,18 @@ def reference_cpu_run(cfg, heads, steps=1, threads=None):
     t0 = time.perf_counter()
     for _ in range(steps):
         Kbar = ref.regularize_bank(K, LAM, P)
-        ref.regularized_long_conv(u, K, D, LAM, P, engine=engine)
+        ref.regularized_long_conv(u, Kbar, D, 0.0, 0, engine=engine)
         _, dKbar, _ = ref.long_conv_backward(u, dy, Kbar, D)
         ref.regularizer_backward(K, LAM, P, dKbar)
     return B * heads * N * steps, time.perf_counter() - t0
 
 
 def cpu_baseline(cfg, heads):
-    heads = min(cfg["H"], heads)
+    """One reference step on the host cores: the whole configured workload
+    when it is a few seconds of CPU work (configs 1, 2, 4), else `heads`
+    heads of it (configs with N >= 64K; channels are independent)."""
+    full = cfg["B"] * cfg["H"] * cfg["N"] <= 64 * 2**20
+    heads = cfg["H"] if full else min(cfg["H"], heads)
     threads = os.cpu_count() or 1
     try:
         el, sec = reference_cpu_run(cfg, heads, 1, threads)
@@ -500,33 +563,40 @@ def cpu_baseline(cfg, heads):
     if cfg["engine"] == "learned":
         threads = 1  # learned_forward / learned_gradients are single-threaded per row
     return {"value": el / sec, "unit": "elements/s", "cores": threads, "kind": "reference",
-            "sample": f"B={cfg['B']} H={heads} (of {cfg['H']}) N={cfg['N']}, fp64, "
-                      f"{sec:.1f}s: regularize_bank + regularized_long_conv(kButterfly) + "
-                      "composed conv_butterfly backward; channels independent so the rate "
-                      "extrapolates linearly",
+            "sample": f"B={cfg['B']} H={heads} (of {cfg['H']}) N={cfg['N']}, fp64, one step "
+                      f"in {sec:.1f}s: regularize_bank + regularized_long_conv(kButterfly) + "
+                      "composed conv_butterfly backward + regularizer chain rule"
+                      + ("" if heads == cfg["H"] else "; a head sample (channels independent)"),
             "host": platform.processor() or platform.machine()}
 
 
 def run_reference(args, cfg, rank):
+    """--impl reference: the reference's CPU implementation, rank 0 only, all
+    host threads; every step is the WHOLE configured workload (no head
+    sampling or extrapolation) for configs of up to 64M elements (config 2:
+    ~2.5 s per step on 16 cores), a head sample above that."""
     if rank != 0:
         return
-    heads = min(cfg["H"], args.cpu_sample_heads)
+    full = cfg["B"] * cfg["H"] * cfg["N"] <= 64 * 2**20
+    heads = cfg["H"] if full else min(cfg["H"], args.cpu_sample_heads)
     threads = os.cpu_count() or 1
-    for _ in range(args.warmup if args.warmup < 1 else 1):
-        reference_cpu_run(cfg, max(1, heads // 8), 1, threads)
+    if args.warmup > 0:  # one warm-up step (page-in, thread spawn); the rest are timed
+        reference_cpu_run(cfg, heads, 1, threads)
     el, sec = reference_cpu_run(cfg, heads, args.steps, threads)
     val = el / sec
     out = {
         "impl": "reference",
         "metric": "long-conv fwd+bwd elements/sec (E=B*H*N per step: K1 prep + fwd + bwd)",
         "value": val, "unit": "elements/s", "n_gpus": 1, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": sec / args.steps * 1e3 * cfg["H"] / heads,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "warmup": min(args.warmup, 1), "ms_per_step": sec / args.steps * 1e3,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic", "config": {"workload": cfg["workload"], "B": cfg["B"], "H": cfg["H"],
-                                        "N": cfg["N"]},
+                                        "N": cfg["N"], "heads_timed": heads},
         "cpu_baseline": {"value": val, "unit": "elements/s", "cores": threads,
                          "kind": "reference",
-                         "sample": f"each step B={cfg['B']} H={heads} of {cfg['H']} heads"},
+                         "sample": (f"each step the full B={cfg['B']} H={cfg['H']} N={cfg['N']} "
+                                    "workload" if heads == cfg["H"] else
+                                    f"each step B={cfg['B']} H={heads} of {cfg['H']} heads")},
         "e2e": {"value": val, "unit": "elements/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
@@ -619,6 +689,10 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--n", type=int, default=None, help="sequence length (config 5 sweep)")
     ap.add_argument("--bh", type=int, default=None, help="B*H override (config 6, few GPUs)")
+    ap.add_argument("--dtype", default=None, choices=["f32", "bf16", "f16"],
+                    help="I/O dtype override (e.g. the fp32 validation line of config 2)")
+    ap.add_argument("--scaling", default="strong", choices=["strong", "weak"],
+                    help="N>1: strong = head_shard(H) per rank (default), weak = full job per rank")
     args = ap.parse_args()
     rank = int(os.environ.get("RANK", 0))
     world = int(os.environ.get("WORLD_SIZE", 1))
@@ -627,6 +701,11 @@ def main():
     if args.n is not None:
         cfg["N"] = args.n
         cfg["workload"] = cfg["workload"] + f", N={args.n}"
+    if args.dtype is not None and args.dtype != cfg["dtype"]:
+        cfg["dtype"] = args.dtype
+        cfg["workload"] = cfg["workload"] + f", {args.dtype} I/O"
+        if cfg["engine"] == "single" and args.dtype == "f32":
+            cfg["engine"] = "auto"  # fp32 validation mode: the CUDA-core single pass
     if args.config == 4 and args.impl == "ours":
         run_learned(args, cfg, rank, world, local_rank)
         return

@@ -136,6 +136,15 @@ int fb_fwd_save(fb_plan* plan, const void* u, void* y, void* saved, int64_t B, v
 int fb_bwd_saved(fb_plan* plan, const void* dy, const void* u, const void* saved, void* du,
                  float* dK, float* dKbar, float* dD, int64_t B, void* workspace, void* stream);
 
+/* Measurement hook (not part of the reference interface): the plan records
+ * the caller's CUDA events `begin` / `end` (cudaEvent_t as void*) on the
+ * launching stream immediately before / after the NEXT launch of its main
+ * forward kernel (which = 0: tc_fwd_kernel, sp_fwd_kernel, or the three-pass
+ * row kernel) or main backward kernel (which = 1: tc_bwd_kernel,
+ * sp_bwd_kernel, or the three-pass backward row kernel), then forgets them.
+ * bench.py times the dominant kernel alone this way (roofline). */
+int fb_plan_profile_events(fb_plan* plan, int which, void* begin, void* end);
+
 /* Host-buffer layer runner: the whole regularized_long_conv forward +
  * backward (regularize.hpp:67-70 with the SURVEY.md §8c backward) on HOST
  * arrays, pipelined.  The H heads are independent, so the runner walks them

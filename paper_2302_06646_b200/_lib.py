@@ -24,7 +24,7 @@ EXPORTED = [
     "fb_last_error", "fb_version", "fb_host_runner_create", "fb_host_runner_destroy",
     "fb_host_runner_chunk_heads", "fb_host_runner_run", "fb_saved_size", "fb_fwd_save",
     "fb_bwd_saved", "fb_shard_plan_create", "fb_shard_plan_destroy", "fb_shard_plan_dims",
-    "fb_shard_columns", "fb_shard_rows",
+    "fb_shard_columns", "fb_shard_rows", "fb_plan_profile_events",
 ]
 
 
@@ -97,6 +97,7 @@ def lib() -> C.CDLL:
         L.fb_host_runner_chunk_heads.restype = i64
         L.fb_host_runner_run.argtypes = [vp, C.POINTER(RegConfig), C.c_int, vp, vp, vp, vp, vp,
                                          vp, vp, vp, vp]
+        L.fb_plan_profile_events.argtypes = [vp, C.c_int, vp, vp]
         L.fb_last_error.restype = C.c_char_p
         _lib = L
     return _lib

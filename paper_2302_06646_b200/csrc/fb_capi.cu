@@ -288,6 +288,14 @@ static int check_run(const fb_plan* p, int64_t B, const char* who) {
   return cuda_status(cudaSetDevice(p->device), "cudaSetDevice");
 }
 
+int fb_plan_profile_events(fb_plan* p, int which, void* begin, void* end) {
+  if (!p) return fail(FB_ERR_ARG, "fb_plan_profile_events: null plan");
+  if (which != 0 && which != 1) return fail(FB_ERR_ARG, "fb_plan_profile_events: which must be 0 or 1");
+  p->prof[which][0] = (cudaEvent_t)begin;
+  p->prof[which][1] = (cudaEvent_t)end;
+  return FB_OK;
+}
+
 int fb_fwd(fb_plan* p, const void* u, void* y, int64_t B, void* ws, void* stream) {
   int rc = check_run(p, B, "fb_fwd");
   if (rc) return rc;

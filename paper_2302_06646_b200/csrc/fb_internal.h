@@ -40,6 +40,9 @@ struct fb_plan {
   cudaStream_t aux = nullptr;
   cudaEvent_t ev_fork = nullptr, ev_prep = nullptr, ev_join = nullptr;
   bool prep_async = false;  // ev_prep guards kbar / kf / D / keep
+  // one-shot caller events around the next launch of the forward's / the
+  // backward's main kernel (fb_plan_profile_events; bench.py's roofline)
+  cudaEvent_t prof[2][2] = {{nullptr, nullptr}, {nullptr, nullptr}};
 };
 
 struct fb_learned_plan {
@@ -110,6 +113,13 @@ int regularize_bank_dev(fb_plan* p, const float* K, cudaStream_t s);
 int dropout_keep_dev(fb_plan* p, double rate, uint64_t seed, cudaStream_t s);
 // dK = chain(dKbar) through dropout/smooth/squash, per head; dkbar_in [H][N]
 int regularizer_backward_dev(fb_plan* p, const float* dkbar, float* dK, cudaStream_t s);
+// record (and clear) the caller's profiling event `e` (0 begin, 1 end) of main kernel k
+inline void prof_mark(fb_plan* p, int k, int e, cudaStream_t s) {
+  if (p->prof[k][e]) {
+    cudaEventRecord(p->prof[k][e], s);
+    p->prof[k][e] = nullptr;
+  }
+}
 // make `s` wait for an asynchronous kernel prep (no-op otherwise)
 inline void prep_wait(const fb_plan* p, cudaStream_t s) {
   if (p->prep_async) cudaStreamWaitEvent(s, p->ev_prep, 0);

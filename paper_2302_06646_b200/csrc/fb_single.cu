@@ -634,6 +634,7 @@ int sp_fwd(fb_plan* p, const void* u, void* y, int64_t B, cudaStream_t s) {
   const int chunks = chunks_for(p, B);
   const int64_t npairs = (B + 1) / 2;
   const int ppc = (int)((npairs + chunks - 1) / chunks);
+  prof_mark(p, 0, 0, s);
   with_log2n(p->n, [&](auto ks) {
     switch (p->dtype) {
       case FB_F32: ks.template fwd<float>(s, p, u, y, (int)B, chunks, ppc); break;
@@ -641,6 +642,7 @@ int sp_fwd(fb_plan* p, const void* u, void* y, int64_t B, cudaStream_t s) {
       default: ks.template fwd<__half>(s, p, u, y, (int)B, chunks, ppc); break;
     }
   });
+  prof_mark(p, 0, 1, s);
   return cuda_status(cudaGetLastError(), "sp_fwd");
 }
 
@@ -667,11 +669,13 @@ int sp_bwd(fb_plan* p, const void* dy, const void* u, void* du, float* dK, float
   off += (size_t)p->H * chunks * sizeof(float);
   off = (off + 255) & ~size_t(255);
   with_log2n(p->n, [&](auto ks) {
+    prof_mark(p, 1, 0, s);
     switch (p->dtype) {
       case FB_F32: ks.template bwd<float>(s, p, dy, u, du, spart, ddpart, (int)B, chunks, ppc); break;
       case FB_BF16: ks.template bwd<__nv_bfloat16>(s, p, dy, u, du, spart, ddpart, (int)B, chunks, ppc); break;
       default: ks.template bwd<__half>(s, p, dy, u, du, spart, ddpart, (int)B, chunks, ppc); break;
     }
+    prof_mark(p, 1, 1, s);
     ks.finalize(s, p, spart, ddpart, chunks, dKbar, dD, dK, 0, nullptr);
   });
   return cuda_status(cudaGetLastError(), "sp_bwd");

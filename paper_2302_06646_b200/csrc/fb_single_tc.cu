@@ -1476,10 +1476,12 @@ int tc_fwd(fb_plan* p, const void* u, void* y, int64_t B, cudaStream_t s, void* 
     if (rc) return rc;
     auto k = tc_fwd_kernel<T>;
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM_FWD);
+    prof_mark(p, 0, 0, s);
     k<<<(unsigned)gr.ctas, kThreads, SMEM_FWD, s>>>(map, (T*)y, (const __half2*)p->kf_tc,
                                                      p->kf_scale, (const uint4*)p->tc_mats, p->tw2,
                                                      (int)B, (int)p->H, gr.total,
                                                      (uint32_t*)usave);
+    prof_mark(p, 0, 1, s);
     return cuda_status(cudaGetLastError(), "tc_fwd");
   };
   return p->dtype == FB_BF16 ? go(__nv_bfloat16{}) : go(__half{});
@@ -1502,9 +1504,11 @@ int tc_bwd(fb_plan* p, const void* dy, const void* u, void* du, float* dK, float
     if (rc) return rc;
     auto launch = [&](auto kern) {
       cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM_BWD3);
+      prof_mark(p, 1, 0, s);
       kern<<<(unsigned)gr.bctas, kThreads, SMEM_BWD3, s>>>(
           dmap, umap, (T*)du, (const __half2*)p->kf_tc, p->kf_scale, (const uint4*)p->tc_mats,
           p->tw2, spart, (int)B, (int)p->H, gr.total, gr.maxseg, (const uint32_t*)usave);
+      prof_mark(p, 1, 1, s);
     };
     if (usave) launch(tc_bwd_kernel<T, true>);
     else launch(tc_bwd_kernel<T, false>);
@@ -1602,9 +1606,11 @@ int tc_rows_fwd(fb_plan* p, void* x1, void* usave, int64_t npairs, cudaStream_t 
   auto k = tc_rows_fwd_kernel<__nv_bfloat16>;
   cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rows::SMEM);
   const int ctas = std::max(1, std::min(p->num_sms, total));
+  prof_mark(p, 0, 0, s);
   k<<<(unsigned)ctas, kThreads, rows::SMEM, s>>>(map, (uint32_t*)x1, p->kf, (const uint4*)p->tcr_mats,
                                                  p->tw_l, (int)npairs, hm, total, (uint32_t*)usave,
                                                  rows_token());
+  prof_mark(p, 0, 1, s);
   return cuda_status(cudaGetLastError(), "tc_rows_fwd");
 }
 
@@ -1634,9 +1640,11 @@ int tc_rows_bwd(fb_plan* p, void* x1dy, const void* usave, float2* wdk, int64_t 
   auto k = tc_rows_bwd_kernel<__nv_bfloat16>;
   cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rows::SMEM_BWD);
   const int ctas = std::max(1, std::min(p->num_sms, hm));
+  prof_mark(p, 1, 0, s);
   k<<<(unsigned)ctas, kThreads, rows::SMEM_BWD, s>>>(map, (uint32_t*)x1dy, (const uint32_t*)usave,
                                                      p->kf, wdk, (const uint4*)p->tcr_mats, p->tw_l,
                                                      (int)npairs, hm);
+  prof_mark(p, 1, 1, s);
   return cuda_status(cudaGetLastError(), "tc_rows_bwd");
 }
 

@@ -1396,9 +1396,11 @@ int tp_fwd(fb_plan* p, const void* u, void* y, int64_t B, void* ws, cudaStream_t
     cudaFuncSetAttribute(k2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     const int chunks = pass2_chunks(p, npairs);
     const int ppc = (int)((npairs + chunks - 1) / chunks);
+    prof_mark(p, 0, 0, s);
     k2<<<dim3((unsigned)(p->H * p->m), (unsigned)chunks), kL / 16, sm, s>>>(
         x1, p->kf, nullptr, p->tw_l, (int)npairs, (int)p->H, (int)p->m, ppc, 0.f,
         reinterpret_cast<CxT<ST>*>(usave));
+    prof_mark(p, 0, 1, s);
     launch_pass3<ST, IO, 0>(p, x1, (const IO*)u, (IO*)y, nullptr, (int)B, (int)npairs, 1.f, s);
   });
   if (rc) return rc;
@@ -1453,16 +1455,20 @@ int tp_bwd(fb_plan* p, const void* dy, const void* u, void* du, float* dK, float
                               (int)npairs, s);
       auto k2 = tp_pass2_bwd_kernel<ST, true>;
       cudaFuncSetAttribute(k2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+      prof_mark(p, 1, 0, s);
       k2<<<(unsigned)(p->H * p->m), kL / 16, sm, s>>>(
           x1dy, reinterpret_cast<const CxT<ST>*>(usave), p->kf, wdk, p->tw_l, (int)npairs,
           (int)p->H, (int)p->m);
+      prof_mark(p, 1, 1, s);
     } else {
       gx = launch_pass1<IO, ST, 1>(p, (const IO*)dy, (const IO*)u, x1dy, x1u, ddpart, (int)B,
                                    (int)npairs, s);
       auto k2 = tp_pass2_bwd_kernel<ST, false>;
       cudaFuncSetAttribute(k2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+      prof_mark(p, 1, 0, s);
       k2<<<(unsigned)(p->H * p->m), kL / 16, sm, s>>>(x1dy, x1u, p->kf, wdk, p->tw_l, (int)npairs,
                                                        (int)p->H, (int)p->m);
+      prof_mark(p, 1, 1, s);
     }
     // the dK tail (dK rows -> dKbar, dD, regularizer chain rule) on the
     // auxiliary stream, alongside pass 3 of du

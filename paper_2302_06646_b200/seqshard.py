@@ -262,8 +262,8 @@ def sharded_long_conv_backward(dy_cols: torch.Tensor, u_cols: torch.Tensor,
       dD     = dKbar[0]                 (lag 0, held by the rank with tau0 = 0)
     Layouts as in sharded_long_conv; returns (du_cols [B, H, m/2, lp],
     dkbar_cols [H, m/2, lp] fp32, dD [H] fp32).  The chain rule through the
-    regularizers (smooth needs the +-p neighbours across slices) is left to
-    the caller on the gathered dKbar."""
+    regularizers to dK is sharded_regularizer_backward (halo exchange of the
+    +-p smoothing neighbours across slices)."""
     B, H, half, lp = u_cols.shape
     m = shard.m
     dev = u_cols.device
@@ -289,6 +289,65 @@ def sharded_long_conv_backward(dy_cols: torch.Tensor, u_cols: torch.Tensor,
     if shard.world > 1:
         dist.all_reduce(dD, group=group)
     return du.to(dy_cols.dtype), dkbar, dD
+
+
+def _halo(x_cols: torch.Tensor, p: int, shard: SeqShard, group=None) -> torch.Tensor:
+    """[H, rows, lp] slices of t = c l + tau -> [H, rows, lp + 2p] with the p
+    neighbours on either side of every row of the slice: the left halo of row
+    c comes from rank r-1's last p columns of row c (rank 0: rank P-1's row
+    c-1), the right halo from rank r+1's first p columns of row c (rank P-1:
+    rank 0's row c+1); zero beyond t = 0 and t = rows * l (the zero-padded
+    window of regularize.cpp:22-34)."""
+    H, R, lp = x_cols.shape
+    if p == 0:
+        return x_cols
+    if p > lp:
+        raise ValueError(f"smooth width {p} exceeds the slice width {lp}")
+    edges = torch.cat([x_cols[..., :p], x_cols[..., lp - p:]], -1).contiguous()  # [H, R, 2p]
+    P, r = shard.world, shard.rank
+    if P == 1:
+        parts = [edges]
+    else:
+        parts = [torch.empty_like(edges) for _ in range(P)]
+        dist.all_gather(parts, edges, group=group)
+    zrow = torch.zeros_like(edges[:, :1, :p])
+    lft = parts[r - 1][..., p:] if r > 0 else torch.cat([zrow, parts[P - 1][:, :-1, p:]], 1)
+    rgt = parts[r + 1][..., :p] if r < P - 1 else torch.cat([parts[0][:, 1:, :p], zrow], 1)
+    return torch.cat([lft, x_cols, rgt], -1)
+
+
+def _smooth_sharded(x_cols: torch.Tensor, p: int, shard: SeqShard, group=None) -> torch.Tensor:
+    """smooth (regularize.cpp:22-34): zero-padded window mean over |j - i| <= p,
+    on the sharded layout (halo exchange of p columns per slice edge)."""
+    if p == 0:
+        return x_cols.clone()
+    xp = _halo(x_cols, p, shard, group)
+    lp = x_cols.shape[-1]
+    acc = xp[..., 0:lp].clone()
+    for d in range(1, 2 * p + 1):
+        acc += xp[..., d:d + lp]
+    return acc * (1.0 / (2 * p + 1))
+
+
+def sharded_regularize(k_cols: torch.Tensor, lam: float, p: int, shard: SeqShard,
+                       group=None) -> torch.Tensor:
+    """regularize_bank (regularize.cpp:93-107, time-domain smooth, no dropout)
+    on the sharded layout: Kbar = squash(smooth(K)).  k_cols [H, m/2, lp]
+    (raw kernels, any float dtype) -> fp32 Kbar slices; computed in fp64."""
+    s = _smooth_sharded(k_cols.double(), p, shard, group)
+    mag = s.abs() - lam
+    return torch.where(mag > 0, torch.copysign(mag, s), torch.zeros_like(s)).float()
+
+
+def sharded_regularizer_backward(k_cols: torch.Tensor, dkbar_cols: torch.Tensor, lam: float,
+                                 p: int, shard: SeqShard, group=None) -> torch.Tensor:
+    """Chain rule of sharded_regularize: smooth is a symmetric
+    zero-padded band (self-adjoint) and squash' = 1[|smooth(K)| > lam], so
+    dK = smooth(1[|smooth(K)| > lam] * dKbar) — two halo exchanges.  Returns
+    fp32 dK slices [H, m/2, lp] w.r.t. the raw K."""
+    s = _smooth_sharded(k_cols.double(), p, shard, group)
+    g = torch.where(s.abs() > lam, dkbar_cols.double(), torch.zeros_like(s))
+    return _smooth_sharded(g, p, shard, group).float()
 
 
 def head_shard(H: int, world: int, rank: int) -> slice:

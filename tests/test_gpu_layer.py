@@ -481,3 +481,26 @@ def test_sharded_long_conv_backward_single_rank(lc):
     assert rel_l2(to_np(du.reshape(B, H, N)), du_w) < 1e-5
     assert rel_l2(to_np(dkbar.reshape(H, N)), dkbar_w) < 1e-5
     assert rel_l2(to_np(dD), dD_w) < 1e-5
+
+
+@pytest.mark.parametrize("dtype,world", [(torch.bfloat16, 4), (torch.float32, 2)])
+def test_head_sharding_product(lc, dtype, world):
+    """B*H sharding as bench.py --gpus P runs it (seqshard.head_shard, no
+    collective): each 'rank' builds its own plan on its head slice; the
+    concatenated y / du / dK / dD equal the unsharded plan's bit for bit
+    (channels are independent, dK / dD are head-local) and match the oracle."""
+    from paper_2302_06646_b200.seqshard import head_shard
+
+    B, H, N = 6, 8, 4096
+    inp = layer_inputs(lc, B, H, N, dtype)
+    cfg = fb.RegularizationConfig(**CFG)
+    _, want = run_layer(inp, N, H, dtype, cfg, engine=1)
+    parts = []
+    for r in range(world):
+        hs = head_shard(H, world, r)
+        sub = dict(tu=inp["tu"][:, hs].contiguous(), tdy=inp["tdy"][:, hs].contiguous(),
+                   tK=inp["tK"][hs].contiguous(), tD=inp["tD"][hs].contiguous())
+        parts.append(run_layer(sub, N, hs.stop - hs.start, dtype, cfg, engine=1)[1])
+    for k, ax in (("y", 1), ("du", 1), ("dK", 0), ("dD", 0)):
+        assert np.array_equal(np.concatenate([p[k] for p in parts], axis=ax), want[k]), k
+    assert_parity(want, oracle_layer(lc, inp, cfg), TOL[dtype], keys=("y", "du", "dK", "dD"))

@@ -198,3 +198,45 @@ def test_sharded_layer_backward_gloo(world, monkeypatch, lc):
     assert rel(cat("bdk").reshape(H, N), dkbar_w) < 1e-5
     for r in range(world):
         assert rel(np.load(os.path.join(d, f"bdd_{world}_{r}.npy")), dD_w) < 1e-5
+
+
+def _reg_worker(rank, world):
+    """Sharded regularize_bank + chain rule with the +-p halo exchange."""
+    from oracle.oracle import LcOracle
+
+    lc = LcOracle()
+    H, N, p = 3, L_COLS * M_ROWS // 2, int(os.environ["FB_TEST_P"])
+    K, _ = lc.init_kernels(1, H, N, 3)
+    dkbar = lc.signal_batch(4, 1, H, N)[0]
+    sh = ss.SeqShard(L_COLS, M_ROWS, world, rank)
+    cols = lambda a: torch.from_numpy(a.reshape(H, M_ROWS // 2, L_COLS)[..., sh.tau0:sh.tau0 + sh.lp])  # noqa: E731
+    kb = ss.sharded_regularize(cols(K), 0.003, p, sh)
+    dk = ss.sharded_regularizer_backward(cols(K), cols(dkbar), 0.003, p, sh)
+    d = os.environ["FB_TEST_DIR"]
+    np.save(os.path.join(d, f"rkb_{world}_{rank}.npy"), kb.numpy())
+    np.save(os.path.join(d, f"rdk_{world}_{rank}.npy"), dk.numpy())
+
+
+@pytest.mark.parametrize("world,p", [(1, 1), (2, 1), (4, 1), (2, 3), (4, 16)])
+def test_sharded_regularizer_halo_gloo(world, p, monkeypatch, lc):
+    """sharded_regularize / sharded_regularizer_backward (halo of p columns per
+    slice edge, wrapping to the neighbouring row at the first / last rank)
+    reproduce regularize_bank and its chain rule on the gathered bank; p = 16
+    is the whole slice at world 4 (lp = 16)."""
+    d = tempfile.mkdtemp()
+    monkeypatch.setenv("FB_TEST_DIR", d)
+    monkeypatch.setenv("FB_TEST_P", str(p))
+    if world == 1:
+        _reg_worker(0, 1)
+    else:
+        ss.run_ranks(world, _reg_worker, port=29611 + 7 * world + p)
+    H, N = 3, L_COLS * M_ROWS // 2
+    K, _ = lc.init_kernels(1, H, N, 3)
+    dkbar = lc.signal_batch(4, 1, H, N)[0]
+    kb_w = lc.regularize_bank(K, 0.003, p)
+    dk_w = lc.regularizer_backward(K, 0.003, p, dkbar)
+    cat = lambda name: np.concatenate([np.load(os.path.join(d, f"{name}_{world}_{r}.npy"))  # noqa: E731
+                                       for r in range(world)], axis=-1).reshape(H, N)
+    # fp64 in the reference's summation order, rounded once to fp32
+    assert np.array_equal(cat("rkb"), kb_w.astype(np.float32))
+    assert np.array_equal(cat("rdk"), dk_w.astype(np.float32))
