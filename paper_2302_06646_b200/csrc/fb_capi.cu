@@ -97,6 +97,49 @@ constexpr int64_t kMinTransform = 256;
 
 using namespace fb;
 
+namespace fb {
+// ---- zero-padded staging for causal three-pass plans with N % l != 0 ----
+// rows of `w` bytes with pitch `sp` -> rows of pitch `dp`, the tail of each
+// destination row (dp - w bytes) zeroed
+static int pad_rows(void* dst, size_t dp, const void* src, size_t sp, size_t w, size_t rows,
+                    cudaStream_t s) {
+  int rc = cuda_status(cudaMemcpy2DAsync(dst, dp, src, sp, w, rows, cudaMemcpyDeviceToDevice, s),
+                       "pad copy");
+  if (!rc && dp > w) rc = cuda_status(cudaMemset2DAsync((char*)dst + w, dp, 0, dp - w, rows, s),
+                                      "pad zero");
+  return rc;
+}
+static int crop_rows(void* dst, size_t dp, const void* src, size_t sp, size_t w, size_t rows,
+                     cudaStream_t s) {
+  return cuda_status(cudaMemcpy2DAsync(dst, dp, src, sp, w, rows, cudaMemcpyDeviceToDevice, s),
+                     "crop copy");
+}
+static size_t al256(size_t x) { return (x + 255) & ~size_t(255); }
+static size_t es_of(int dtype) { return dtype == FB_F32 ? 4 : 2; }
+
+// workspace of a padded plan: [inner workspace | u' | v' | w' | dK' | dKbar']
+struct PadWs {
+  char *inner, *a, *b, *c;
+  float *dk, *dkbar;
+};
+static size_t pad_ws_bytes(const fb_plan* p, int64_t B, PadWs* w, void* base) {
+  const fb_plan* q = p->inner;
+  const size_t sig = al256((size_t)B * q->H * q->N * es_of(q->dtype));
+  const size_t bank = al256((size_t)q->H * q->N * sizeof(float));
+  const size_t inner = al256(tp_workspace(q, B));
+  if (w) {
+    char* c = (char*)base;
+    w->inner = c;
+    w->a = c + inner;
+    w->b = w->a + sig;
+    w->c = w->b + sig;
+    w->dk = (float*)(w->c + sig);
+    w->dkbar = (float*)((char*)w->dk + bank);
+  }
+  return inner + 3 * sig + 2 * bank + 256;
+}
+}  // namespace fb
+
 extern "C" {
 
 const char* fb_last_error(void) { return g_last_error.c_str(); }
@@ -115,7 +158,8 @@ int fb_plan_create(fb_plan** out, int64_t N, int64_t H, int mode, int dtype, int
   if (mode == FB_MODE_CIRCULAR && !is_pow2(N))
     return fail(FB_ERR_PLAN, "fb_plan_create: circular mode needs a power-of-two N "
                              "(causal mode accepts any N; pad the input)");
-  int rc = cuda_status(cudaSetDevice(device), "cudaSetDevice");
+  DevGuard dg(device);
+  int rc = cuda_status(dg.err, "cudaSetDevice");
   if (rc) return rc;
   fb_plan* p = new fb_plan();
   p->N = N;
@@ -150,6 +194,19 @@ int fb_plan_create(fb_plan** out, int64_t N, int64_t H, int mode, int dtype, int
     p->l = n;
     p->m = 1;
   }
+  if (engine == FB_ENGINE_THREE && mode == FB_MODE_CAUSAL && N % kThreePassRow) {
+    // the column passes tile the data rows c < N / l; pad N to whole rows
+    // (same transform length: N' <= n / 2) and crop the outputs
+    const int64_t Np = (N + kThreePassRow - 1) / kThreePassRow * kThreePassRow;
+    rc = fb_plan_create(&p->inner, Np, H, mode, dtype, FB_ENGINE_THREE, device);
+    if (!rc) rc = cuda_status(cudaMalloc(&p->kraw, sizeof(float) * H * Np), "cudaMalloc(K pad)");
+    if (rc) {
+      fb_plan_destroy(p);
+      return rc;
+    }
+    *out = p;
+    return FB_OK;
+  }
   cudaDeviceGetAttribute(&p->num_sms, cudaDevAttrMultiProcessorCount, device);
   p->use_tc = engine == FB_ENGINE_SINGLE && !simt && tc_eligible(p);
   rc = upload_twiddles2(&p->tw2, n);
@@ -162,7 +219,8 @@ int fb_plan_create(fb_plan** out, int64_t N, int64_t H, int mode, int dtype, int
   if (!rc) rc = cuda_status(cudaMalloc(&p->d, sizeof(float) * H), "cudaMalloc(D)");
   if (!rc && p->use_tc) rc = tc_init(p);
   if (!rc && p->engine == FB_ENGINE_THREE) {
-    rc = cuda_status(cudaStreamCreateWithFlags(&p->aux, cudaStreamNonBlocking), "aux stream");
+    rc = cuda_status(cudaMalloc(&p->kraw, sizeof(float) * H * N), "cudaMalloc(K copy)");
+    if (!rc) rc = cuda_status(cudaStreamCreateWithFlags(&p->aux, cudaStreamNonBlocking), "aux stream");
     for (cudaEvent_t* e : {&p->ev_fork, &p->ev_prep, &p->ev_join})
       if (!rc) rc = cuda_status(cudaEventCreateWithFlags(e, cudaEventDisableTiming), "event");
   }
@@ -176,6 +234,8 @@ int fb_plan_create(fb_plan** out, int64_t N, int64_t H, int mode, int dtype, int
 
 int fb_plan_destroy(fb_plan* p) {
   if (!p) return FB_OK;
+  DevGuard dg(p->device);
+  if (p->inner) fb_plan_destroy(p->inner);
   cudaFree(p->tw_n);
   cudaFree(p->tw2);
   cudaFree(p->tw_l);
@@ -185,6 +245,7 @@ int fb_plan_destroy(fb_plan* p) {
   cudaFree(p->kbar);
   cudaFree(p->keep);
   cudaFree(p->d);
+  cudaFree(p->kraw);
   cudaFree(p->tc_mats);
   cudaFree(p->kf_tc);
   cudaFree(p->tcr_mats);
@@ -199,23 +260,33 @@ int fb_plan_destroy(fb_plan* p) {
 
 int fb_plan_get_info(const fb_plan* p, fb_plan_info* info) {
   if (!p || !info) return fail(FB_ERR_ARG, "fb_plan_get_info: null argument");
+  const fb_plan* q = p->inner ? p->inner : p;
   info->N = p->N;
   info->H = p->H;
-  info->n = p->n;
-  info->l = p->l;
-  info->m = p->m;
-  info->engine = p->engine;
-  info->dtype = p->dtype;
-  info->mode = p->mode;
-  info->tensor_cores = p->use_tc ? 1 : 0;
+  info->n = q->n;
+  info->l = q->l;
+  info->m = q->m;
+  info->engine = q->engine;
+  info->dtype = q->dtype;
+  info->mode = q->mode;
+  info->tensor_cores = q->use_tc ? 1 : 0;
   return FB_OK;
 }
 
 int fb_plan_copy_kbar(const fb_plan* p, float* dst, void* stream) {
   if (!p || !dst) return fail(FB_ERR_ARG, "fb_plan_copy_kbar: null argument");
-  prep_wait(p, (cudaStream_t)stream);
+  DevGuard dg(p->device);
+  cudaStream_t s = (cudaStream_t)stream;
+  if (p->inner) {
+    int rc = prep_wait(p->inner, s);
+    if (rc) return rc;
+    return crop_rows(dst, p->N * sizeof(float), p->inner->kbar, p->inner->N * sizeof(float),
+                     p->N * sizeof(float), p->H, s);
+  }
+  int rc = prep_wait(p, s);
+  if (rc) return rc;
   return cuda_status(cudaMemcpyAsync(dst, p->kbar, sizeof(float) * p->H * p->N,
-                                     cudaMemcpyDeviceToDevice, (cudaStream_t)stream),
+                                     cudaMemcpyDeviceToDevice, s),
                      "fb_plan_copy_kbar");
 }
 
@@ -229,8 +300,25 @@ int fb_kernel_prep(fb_plan* p, const float* K, const float* D, const fb_reg_conf
   if (cfg->smooth_domain != FB_SMOOTH_TIME && cfg->smooth_domain != FB_SMOOTH_FREQUENCY)
     return fail(FB_ERR_ARG, "fb_kernel_prep: bad smooth domain");
   cudaStream_t s = (cudaStream_t)stream;
-  int rc = cuda_status(cudaSetDevice(p->device), "cudaSetDevice");
+  DevGuard dg(p->device);
+  int rc = cuda_status(dg.err, "cudaSetDevice");
   if (rc) return rc;
+  if (p->inner) {
+    // zero-padded kernels: smooth's zero padding beyond N and causal taps >= N
+    // never reach outputs t < N, so y, du, dK[:N] equal the unpadded ones
+    // (the frequency-domain smooth transforms the whole length: not padded)
+    if (cfg->smooth_domain == FB_SMOOTH_FREQUENCY)
+      return fail(FB_ERR_UNSUPPORTED, "fb_kernel_prep: smooth_frequency needs N divisible by " +
+                                          std::to_string(kThreePassRow) + " on three-pass");
+    fb_plan* q = p->inner;
+    q->head0 = p->head0;
+    if ((rc = prep_wait(q, s))) return rc;  // the previous prep still reads kraw
+    rc = pad_rows(p->kraw, q->N * sizeof(float), K, p->N * sizeof(float), p->N * sizeof(float),
+                  p->H, s);
+    if (!rc) rc = fb_kernel_prep(q, p->kraw, D, cfg, training, stream);
+    if (!rc) p->prepared = true;
+    return rc;
+  }
   // three-pass: the prep chain runs on the plan's auxiliary stream (after
   // everything already queued on s), so the next forward's pass 1 overlaps it;
   // consumers of the plan state wait on ev_prep.  Not while s is capturing.
@@ -238,8 +326,21 @@ int fb_kernel_prep(fb_plan* p, const float* K, const float* D, const fb_reg_conf
   cudaStreamIsCapturing(s, &cap);
   const bool async = p->aux && cap == cudaStreamCaptureStatusNone;
   if (p->prep_async) {  // the previous prep must be done before its state is rewritten
-    prep_wait(p, s);
+    if ((rc = prep_wait(p, s))) return rc;
     p->prep_async = false;
+  }
+  // K and D are copied on the caller's stream, so the caller may overwrite
+  // them as soon as this call returns (stream order), even when the rest of
+  // the prep runs on the auxiliary stream
+  rc = cuda_status(cudaMemcpyAsync(p->d, D, sizeof(float) * p->H, cudaMemcpyDeviceToDevice, s),
+                   "copy D");
+  if (rc) return rc;
+  const float* Kin = K;
+  if (p->kraw && K != p->kraw) {
+    rc = cuda_status(cudaMemcpyAsync(p->kraw, K, sizeof(float) * p->H * p->N,
+                                     cudaMemcpyDeviceToDevice, s), "copy K");
+    if (rc) return rc;
+    Kin = p->kraw;
   }
   cudaStream_t ps = s;
   if (async) {
@@ -261,10 +362,7 @@ int fb_kernel_prep(fb_plan* p, const float* K, const float* D, const fb_reg_conf
     rc = dropout_keep_dev(p, cfg->dropout_rate, cfg->seed, ps);
     if (rc) return rc;
   }
-  rc = cuda_status(cudaMemcpyAsync(p->d, D, sizeof(float) * p->H, cudaMemcpyDeviceToDevice, ps),
-                   "copy D");
-  if (rc) return rc;
-  rc = p->engine == FB_ENGINE_SINGLE ? sp_prep(p, K, ps) : tp_prep(p, K, ps);
+  rc = p->engine == FB_ENGINE_SINGLE ? sp_prep(p, Kin, ps) : tp_prep(p, Kin, ps);
   if (rc) return rc;
   if (async) {
     rc = cuda_status(cudaEventRecord(p->ev_prep, p->aux), "prep event");
@@ -277,6 +375,7 @@ int fb_kernel_prep(fb_plan* p, const float* K, const float* D, const fb_reg_conf
 
 size_t fb_workspace_size(const fb_plan* p, int64_t B) {
   if (!p || B < 1) return 0;
+  if (p->inner) return pad_ws_bytes(p, B, nullptr, nullptr);
   return p->engine == FB_ENGINE_SINGLE ? sp_workspace(p, B) : tp_workspace(p, B);
 }
 
@@ -285,15 +384,60 @@ static int check_run(const fb_plan* p, int64_t B, const char* who) {
   if (!p->prepared) return fail(FB_ERR_ARG, std::string(who) + ": call fb_kernel_prep first");
   if (B < 1) return fail(FB_ERR_DIM, std::string(who) + ": batch must be >= 1");
   if (B > 65535 * 2) return fail(FB_ERR_DIM, std::string(who) + ": batch too large");
-  return cuda_status(cudaSetDevice(p->device), "cudaSetDevice");
+  return FB_OK;
 }
 
 int fb_plan_profile_events(fb_plan* p, int which, void* begin, void* end) {
   if (!p) return fail(FB_ERR_ARG, "fb_plan_profile_events: null plan");
   if (which != 0 && which != 1) return fail(FB_ERR_ARG, "fb_plan_profile_events: which must be 0 or 1");
+  if (p->inner) return fb_plan_profile_events(p->inner, which, begin, end);
   p->prof[which][0] = (cudaEvent_t)begin;
   p->prof[which][1] = (cudaEvent_t)end;
   return FB_OK;
+}
+
+size_t fb_saved_size(const fb_plan* p, int64_t B) {
+  if (!p || B < 1) return 0;
+  if (p->inner) return fb_saved_size(p->inner, B);
+  if (p->use_tc) return tc_saved_size(p, B);
+  // three-pass: the saved row spectra are kept in the I/O precision, which
+  // for fp16 cannot hold FFT_l of a long non-zero-mean row (|U[0]| = l |mean|
+  // overflows 65504): fp16 plans recompute U in the backward instead
+  if (p->engine == FB_ENGINE_THREE && !p->periodic && p->dtype != FB_F16)
+    return tp_saved_size(p, B);
+  return 0;
+}
+
+// forward of a padded plan: u -> u' (zero-padded rows), inner forward, y' -> y
+static int pad_fwd(fb_plan* p, const void* u, void* y, void* saved, int64_t B, void* ws,
+                   cudaStream_t s) {
+  fb_plan* q = p->inner;
+  PadWs w;
+  pad_ws_bytes(p, B, &w, ws);
+  const size_t es = es_of(p->dtype), rows = (size_t)B * p->H;
+  int rc = pad_rows(w.a, q->N * es, u, p->N * es, p->N * es, rows, s);
+  if (!rc) rc = saved ? fb_fwd_save(q, w.a, w.b, saved, B, w.inner, s)
+                      : fb_fwd(q, w.a, w.b, B, w.inner, s);
+  if (!rc) rc = crop_rows(y, p->N * es, w.b, q->N * es, p->N * es, rows, s);
+  return rc;
+}
+
+static int pad_bwd(fb_plan* p, const void* dy, const void* u, const void* saved, void* du,
+                   float* dK, float* dKbar, float* dD, int64_t B, void* ws, cudaStream_t s) {
+  fb_plan* q = p->inner;
+  PadWs w;
+  pad_ws_bytes(p, B, &w, ws);
+  const size_t es = es_of(p->dtype), rows = (size_t)B * p->H;
+  int rc = pad_rows(w.a, q->N * es, dy, p->N * es, p->N * es, rows, s);
+  if (!rc && u) rc = pad_rows(w.b, q->N * es, u, p->N * es, p->N * es, rows, s);
+  if (!rc) rc = saved ? fb_bwd_saved(q, w.a, u ? w.b : nullptr, saved, w.c, w.dk,
+                                     dKbar ? w.dkbar : nullptr, dD, B, w.inner, s)
+                      : fb_bwd(q, w.a, w.b, w.c, w.dk, dKbar ? w.dkbar : nullptr, dD, B, w.inner, s);
+  if (!rc) rc = crop_rows(du, p->N * es, w.c, q->N * es, p->N * es, rows, s);
+  const size_t f = sizeof(float);
+  if (!rc) rc = crop_rows(dK, p->N * f, w.dk, q->N * f, p->N * f, p->H, s);
+  if (!rc && dKbar) rc = crop_rows(dKbar, p->N * f, w.dkbar, q->N * f, p->N * f, p->H, s);
+  return rc;
 }
 
 int fb_fwd(fb_plan* p, const void* u, void* y, int64_t B, void* ws, void* stream) {
@@ -301,16 +445,13 @@ int fb_fwd(fb_plan* p, const void* u, void* y, int64_t B, void* ws, void* stream
   if (rc) return rc;
   if (!u || !y) return fail(FB_ERR_ARG, "fb_fwd: null tensor");
   if (p->engine == FB_ENGINE_THREE && !ws) return fail(FB_ERR_ARG, "fb_fwd: workspace required");
+  DevGuard dg(p->device);
+  if ((rc = cuda_status(dg.err, "cudaSetDevice"))) return rc;
   cudaStream_t s = (cudaStream_t)stream;
-  if (p->engine == FB_ENGINE_SINGLE) prep_wait(p, s);  // tp_fwd waits after its pass 1
+  if (p->inner) return pad_fwd(p, u, y, nullptr, B, ws, s);
+  // tp_fwd waits for the prep after its pass 1
+  if (p->engine == FB_ENGINE_SINGLE && (rc = prep_wait(p, s))) return rc;
   return p->engine == FB_ENGINE_SINGLE ? sp_fwd(p, u, y, B, s) : tp_fwd(p, u, y, B, ws, s);
-}
-
-size_t fb_saved_size(const fb_plan* p, int64_t B) {
-  if (!p || B < 1) return 0;
-  if (p->use_tc) return tc_saved_size(p, B);
-  if (p->engine == FB_ENGINE_THREE && !p->periodic) return tp_saved_size(p, B);
-  return 0;
 }
 
 int fb_fwd_save(fb_plan* p, const void* u, void* y, void* saved, int64_t B, void* ws,
@@ -319,12 +460,16 @@ int fb_fwd_save(fb_plan* p, const void* u, void* y, void* saved, int64_t B, void
   int rc = check_run(p, B, "fb_fwd_save");
   if (rc) return rc;
   if (!u || !y) return fail(FB_ERR_ARG, "fb_fwd_save: null tensor");
+  DevGuard dg(p->device);
+  if ((rc = cuda_status(dg.err, "cudaSetDevice"))) return rc;
+  cudaStream_t s = (cudaStream_t)stream;
   if (p->use_tc) {
-    prep_wait(p, (cudaStream_t)stream);
-    return tc_fwd(p, u, y, B, (cudaStream_t)stream, saved);
+    if ((rc = prep_wait(p, s))) return rc;
+    return tc_fwd(p, u, y, B, s, saved);
   }
   if (!ws) return fail(FB_ERR_ARG, "fb_fwd_save: workspace required");
-  return tp_fwd(p, u, y, B, ws, (cudaStream_t)stream, saved);
+  if (p->inner) return pad_fwd(p, u, y, saved, B, ws, s);
+  return tp_fwd(p, u, y, B, ws, s, saved);
 }
 
 int fb_bwd_saved(fb_plan* p, const void* dy, const void* u, const void* saved, void* du,
@@ -334,9 +479,13 @@ int fb_bwd_saved(fb_plan* p, const void* dy, const void* u, const void* saved, v
   int rc = check_run(p, B, "fb_bwd_saved");
   if (rc) return rc;
   if (!dy || !du || !dK || !dD || !ws) return fail(FB_ERR_ARG, "fb_bwd_saved: null argument");
-  prep_wait(p, (cudaStream_t)stream);
-  if (p->use_tc) return tc_bwd(p, dy, u, du, dK, dKbar, dD, B, ws, (cudaStream_t)stream, saved);
-  return tp_bwd(p, dy, u, du, dK, dKbar, dD, B, ws, (cudaStream_t)stream, saved);
+  DevGuard dg(p->device);
+  if ((rc = cuda_status(dg.err, "cudaSetDevice"))) return rc;
+  cudaStream_t s = (cudaStream_t)stream;
+  if (p->inner) return pad_bwd(p, dy, u, saved, du, dK, dKbar, dD, B, ws, s);
+  if ((rc = prep_wait(p, s))) return rc;
+  if (p->use_tc) return tc_bwd(p, dy, u, du, dK, dKbar, dD, B, ws, s, saved);
+  return tp_bwd(p, dy, u, du, dK, dKbar, dD, B, ws, s, saved);
 }
 
 int fb_bwd(fb_plan* p, const void* dy, const void* u, void* du, float* dK, float* dKbar,
@@ -344,8 +493,11 @@ int fb_bwd(fb_plan* p, const void* dy, const void* u, void* du, float* dK, float
   int rc = check_run(p, B, "fb_bwd");
   if (rc) return rc;
   if (!dy || !u || !du || !dK || !dD || !ws) return fail(FB_ERR_ARG, "fb_bwd: null argument");
+  DevGuard dg(p->device);
+  if ((rc = cuda_status(dg.err, "cudaSetDevice"))) return rc;
   cudaStream_t s = (cudaStream_t)stream;
-  prep_wait(p, s);
+  if (p->inner) return pad_bwd(p, dy, u, nullptr, du, dK, dKbar, dD, B, ws, s);
+  if ((rc = prep_wait(p, s))) return rc;
   return p->engine == FB_ENGINE_SINGLE ? sp_bwd(p, dy, u, du, dK, dKbar, dD, B, ws, s)
                                        : tp_bwd(p, dy, u, du, dK, dKbar, dD, B, ws, s);
 }
@@ -372,7 +524,7 @@ extern "C" {
 
 int fb_host_runner_destroy(fb_host_runner* r) {
   if (!r) return FB_OK;
-  if (r->plan) cudaSetDevice(r->plan->device);
+  DevGuard dg(r->plan ? r->plan->device : 0);
   for (auto& b : r->buf) {
     cudaFree(b.u);
     cudaFree(b.dy);
@@ -456,7 +608,8 @@ int fb_host_runner_run(fb_host_runner* r, const fb_reg_config* cfg, int training
   if (!r || !cfg || !u || !dy || !K || !D || !y || !du || !dK || !dD)
     return fail(FB_ERR_ARG, "fb_host_runner_run: null argument");
   fb_plan* p = r->plan;
-  int rc = cuda_status(cudaSetDevice(p->device), "cudaSetDevice");
+  DevGuard dg(p->device);
+  int rc = cuda_status(dg.err, "cudaSetDevice");
   if (rc) return rc;
   cudaStream_t caller = (cudaStream_t)stream;
   const int64_t N = r->N, H = r->H, Hc = r->Hc, B = r->B;

@@ -43,6 +43,13 @@ struct fb_plan {
   // one-shot caller events around the next launch of the forward's / the
   // backward's main kernel (fb_plan_profile_events; bench.py's roofline)
   cudaEvent_t prof[2][2] = {{nullptr, nullptr}, {nullptr, nullptr}};
+  // three-pass: the caller's K, copied on the caller's stream before the prep
+  // forks onto the auxiliary stream ([H][N] f32; the caller may reuse K at once)
+  float* kraw = nullptr;
+  // causal three-pass with N % l != 0: the work runs on `inner`, the same
+  // transform for N' = ceil(N / l) l, through zero-padded staging copies
+  // (signals in the workspace, K in kraw [H][N']); outputs are cropped to N
+  fb_plan* inner = nullptr;
 };
 
 struct fb_learned_plan {
@@ -55,6 +62,21 @@ struct fb_learned_plan {
 };
 
 namespace fb {
+// Restores the calling thread's current device when an entry point returns
+// (entry points run on the plan's device, the caller's context is kept).
+struct DevGuard {
+  int prev = -1;
+  cudaError_t err = cudaSuccess;
+  explicit DevGuard(int dev) {
+    if (cudaGetDevice(&prev) != cudaSuccess) prev = -1;
+    if (prev != dev) err = cudaSetDevice(dev);
+  }
+  ~DevGuard() {
+    int cur = -1;
+    if (prev >= 0 && cudaGetDevice(&cur) == cudaSuccess && cur != prev) cudaSetDevice(prev);
+  }
+};
+
 void set_error(const std::string& msg);
 int cuda_status(cudaError_t e, const char* where);
 
@@ -121,8 +143,9 @@ inline void prof_mark(fb_plan* p, int k, int e, cudaStream_t s) {
   }
 }
 // make `s` wait for an asynchronous kernel prep (no-op otherwise)
-inline void prep_wait(const fb_plan* p, cudaStream_t s) {
-  if (p->prep_async) cudaStreamWaitEvent(s, p->ev_prep, 0);
+inline int prep_wait(const fb_plan* p, cudaStream_t s) {
+  if (p->prep_async) return cuda_status(cudaStreamWaitEvent(s, p->ev_prep, 0), "prep wait");
+  return FB_OK;
 }
 
 // learned (fb_learned.cu)

@@ -824,7 +824,8 @@ int fb_learned_plan_create(fb_learned_plan** out, int64_t n, int64_t r, int64_t 
     set_error("learned: too many stages");
     return FB_ERR_PLAN;
   }
-  int rc = cuda_status(cudaSetDevice(device), "cudaSetDevice");
+  DevGuard dg_(device);
+  int rc = cuda_status(dg_.err, "cudaSetDevice");
   if (rc) return rc;
   auto* p = new fb_learned_plan();
   p->n = n;
@@ -953,7 +954,8 @@ int fb_learned_fwd(fb_learned_plan* p, const float* blocks, const void* x, void*
     set_error("learned_forward: batch must be >= 1");
     return FB_ERR_DIM;
   }
-  int rc = cuda_status(cudaSetDevice(p->device), "cudaSetDevice");
+  DevGuard dg_(p->device);
+  int rc = cuda_status(dg_.err, "cudaSetDevice");
   if (rc) return rc;
   fb_learned_ext* ext = ext_of(p);
   cudaStream_t s = (cudaStream_t)stream;
@@ -1006,7 +1008,8 @@ int fb_learned_bwd(fb_learned_plan* p, const float* blocks, const void* x, const
     set_error("learned_gradients: batch must be >= 1");
     return FB_ERR_DIM;
   }
-  int rc = cuda_status(cudaSetDevice(p->device), "cudaSetDevice");
+  DevGuard dg_(p->device);
+  int rc = cuda_status(dg_.err, "cudaSetDevice");
   if (rc) return rc;
   fb_learned_ext* ext = ext_of(p);
   cudaStream_t s = (cudaStream_t)stream;

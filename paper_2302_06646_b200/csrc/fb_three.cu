@@ -1384,13 +1384,13 @@ int tp_fwd(fb_plan* p, const void* u, void* y, int64_t B, void* ws, cudaStream_t
         rc = FB_ERR_UNSUPPORTED;
         return;
       }
-      prep_wait(p, s);  // pass 1 ran alongside an asynchronous kernel prep
-      if ((rc = tc_rows_fwd(p, x1, usave, npairs, s))) return;
+      // pass 1 ran alongside an asynchronous kernel prep
+      if ((rc = prep_wait(p, s)) || (rc = tc_rows_fwd(p, x1, usave, npairs, s))) return;
       launch_pass3<ST, IO, 0>(p, x1, (const IO*)u, (IO*)y, nullptr, (int)B, (int)npairs, 1.f, s);
       return;
     }
     launch_pass1<IO, ST, 0>(p, (const IO*)u, nullptr, x1, nullptr, nullptr, (int)B, (int)npairs, s);
-    prep_wait(p, s);
+    if ((rc = prep_wait(p, s))) return;
     const size_t sm = pass2_smem<ST>();
     auto k2 = tp_pass2_kernel<ST, 0>;
     cudaFuncSetAttribute(k2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
@@ -1529,7 +1529,8 @@ int fb_shard_plan_create(fb_shard_plan** out, int64_t n, int device) {
     set_error("fb_shard_plan_create: n must be a power of two with 16 <= n / 8192 <= 1024");
     return FB_ERR_PLAN;
   }
-  int rc = cuda_status(cudaSetDevice(device), "cudaSetDevice");
+  DevGuard dg_(device);
+  int rc = cuda_status(dg_.err, "cudaSetDevice");
   if (rc) return rc;
   auto* sp = new fb_shard_plan();
   sp->n = n;
@@ -1567,7 +1568,8 @@ int fb_shard_columns(fb_shard_plan* sp, const void* in, void* out, int64_t C, in
     set_error("fb_shard_columns: bad shard geometry (lp must be a multiple of 8192 / m)");
     return FB_ERR_DIM;
   }
-  int rc = cuda_status(cudaSetDevice(sp->device), "cudaSetDevice");
+  DevGuard dg_(sp->device);
+  int rc = cuda_status(dg_.err, "cudaSetDevice");
   if (rc) return rc;
   cudaStream_t s = (cudaStream_t)stream;
   const size_t sm = padded_len(kBigTile) * sizeof(float2);
@@ -1600,7 +1602,8 @@ int fb_shard_rows(fb_shard_plan* sp, void* rows, const void* kf2, void* kf2_out,
     set_error("fb_shard_rows: bad shard geometry");
     return FB_ERR_DIM;
   }
-  int rc = cuda_status(cudaSetDevice(sp->device), "cudaSetDevice");
+  DevGuard dg_(sp->device);
+  int rc = cuda_status(dg_.err, "cudaSetDevice");
   if (rc) return rc;
   cudaStream_t s = (cudaStream_t)stream;
   const size_t sm = pass2_smem<float>();

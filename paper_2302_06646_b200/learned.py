@@ -88,7 +88,7 @@ class LearnedButterflyPlan:
         blocks = self._blocks(blocks)
         y = torch.empty_like(x)
         check(_lib.lib().fb_learned_fwd(self._h, _ptr(blocks), _ptr(x), _ptr(y), B, C.c_void_p(0),
-                                        _stream()))
+                                        _stream(self.device)))
         return y
 
     def gradients(self, blocks: torch.Tensor, x: torch.Tensor, upstream: torch.Tensor):
@@ -102,7 +102,7 @@ class LearnedButterflyPlan:
         nbytes = _lib.lib().fb_learned_workspace_size(self._h, B)
         ws = torch.empty(max(int(nbytes), 1), dtype=torch.uint8, device=self.device)
         check(_lib.lib().fb_learned_bwd(self._h, _ptr(blocks), _ptr(x), _ptr(upstream), _ptr(dx),
-                                        _ptr(db), B, _ptr(ws), _stream()))
+                                        _ptr(db), B, _ptr(ws), _stream(self.device)))
         return db, dx
 
 

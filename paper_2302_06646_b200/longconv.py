@@ -62,8 +62,13 @@ class RegularizationConfig:  # regularize.hpp:19-25
 _DT = {torch.float32: _lib.FB_F32, torch.bfloat16: _lib.FB_BF16, torch.float16: _lib.FB_F16}
 
 
-def _stream() -> C.c_void_p:
-    return C.c_void_p(torch.cuda.current_stream().cuda_stream)
+def _stream(device: torch.device | None = None) -> C.c_void_p:
+    """The current torch stream of `device` (the plan's device, not whichever
+    device happens to be current)."""
+    return C.c_void_p(torch.cuda.current_stream(device).cuda_stream)
+
+
+_PREP_IDS = iter(range(1, 1 << 62))
 
 
 def _ptr(t: torch.Tensor | None):
@@ -114,14 +119,16 @@ class LongConvPlan:
         D = D.detach().to(self.device, torch.float32).contiguous()
         c = cfg.to_c()
         check(_lib.lib().fb_kernel_prep(self._h, _ptr(K), _ptr(D), C.byref(c), int(training),
-                                        _stream()))
-        self._token = (K.data_ptr(), K._version, cfg, bool(training))
+                                        _stream(self.device)))
+        # every prep gets a fresh id: autograd re-preps in backward whenever the
+        # plan was prepared by anyone else in between (no address-reuse aliasing)
+        self._token = next(_PREP_IDS)
         self._keep = (K, D)
 
     def kbar(self) -> torch.Tensor:
         """Copy of the plan's regularized bank Kbar [H, N] (fp32)."""
         out = torch.empty(self.H, self.N, dtype=torch.float32, device=self.device)
-        check(_lib.lib().fb_plan_copy_kbar(self._h, _ptr(out), _stream()))
+        check(_lib.lib().fb_plan_copy_kbar(self._h, _ptr(out), _stream(self.device)))
         return out
 
     def workspace(self, B: int) -> torch.Tensor:
@@ -148,7 +155,7 @@ class LongConvPlan:
         y = torch.empty_like(u) if out is None else out
         ws = self.workspace(B) if workspace is None else workspace
         if save is False:
-            check(_lib.lib().fb_fwd(self._h, _ptr(u), _ptr(y), B, _ptr(ws), _stream()))
+            check(_lib.lib().fb_fwd(self._h, _ptr(u), _ptr(y), B, _ptr(ws), _stream(self.device)))
             return y
         nbytes = self.saved_size(B)
         saved = None
@@ -156,7 +163,7 @@ class LongConvPlan:
             saved = save if isinstance(save, torch.Tensor) else torch.empty(
                 nbytes, dtype=torch.uint8, device=self.device)
         check(_lib.lib().fb_fwd_save(self._h, _ptr(u), _ptr(y), _ptr(saved), B, _ptr(ws),
-                                     _stream()))
+                                     _stream(self.device)))
         return y, saved
 
     # -- K4 ------------------------------------------------------------------
@@ -180,7 +187,7 @@ class LongConvPlan:
         dKbar = torch.empty_like(dK) if want_dkbar else None
         ws = self.workspace(B) if workspace is None else workspace
         check(_lib.lib().fb_bwd_saved(self._h, _ptr(dy), _ptr(u), _ptr(saved), _ptr(du), _ptr(dK),
-                                      _ptr(dKbar), _ptr(dD), B, _ptr(ws), _stream()))
+                                      _ptr(dKbar), _ptr(dD), B, _ptr(ws), _stream(self.device)))
         return (du, dK, dD, dKbar) if want_dkbar else (du, dK, dD)
 
 
@@ -229,7 +236,7 @@ class HostRunner:
         with torch.cuda.device(self.device):
             check(_lib.lib().fb_host_runner_run(self._h, C.byref(c), int(training), _ptr(u), _ptr(dy),
                                                 _ptr(K), _ptr(D), _ptr(y), _ptr(du), _ptr(dK),
-                                                _ptr(dD), _stream()))
+                                                _ptr(dD), _stream(self.device)))
         return y, du, dK, dD
 
 
