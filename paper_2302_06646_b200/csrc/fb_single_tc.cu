@@ -647,27 +647,136 @@ __device__ __forceinline__ float2 unpack_bf2(uint32_t v) {
 }
 // ------------------------------------------------------------------ forward
 // Persistent: CTA c owns pairs [i0, i1) in head-major order; slot s takes
-// i0 + s, i0 + s + 2, ...  Each slot keeps its head's k_f' (fp16 pairs
-// x scale, from K1) in its own TMEM columns, reloaded when its head changes.
-__device__ __forceinline__ void load_kf_tmem(const Ctx& c, const __half2* __restrict__ kf, float sc) {
-  uint32_t f2, g;
-  coords(f2, g);
+// i0 + s, i0 + s + 2, ...
+// TMEM (512 columns): slot s works in [128 s, 128 s + 128); its head's k_f'
+// sits as raw fp16 pairs (the K1 image, scaled by 2^e, one column per f1) at
+// TKF16 + 64 s; the stage-boundary twiddles w_8192^(f1 t2) are a fp32 table
+// at TTW (re f1 0..63 | im f1 0..63, lane = t2) written once per CTA, so the
+// A and B' exits cost one complex multiply per element (no recurrence, no
+// table arithmetic), and the per-head scale 1/2^e is folded into the store.
+constexpr uint32_t TKF16 = 256, TTW = 384;
+
+// the twiddle table, written by slot 0 (a thread: lane t2, its 32 f1) with
+// exactly the values twiddle_row's recurrence produces (chunks of 16 from a
+// table start), so the backward's recomputed transforms stay bit-identical
+__device__ __forceinline__ void init_tw_tmem(const Ctx& c) {
+  uint32_t t2, g;
+  coords(t2, g);
+  const float2 st = tw2<-1>(c.tab, t2);
 #pragma unroll
   for (uint32_t q = 0; q < kColsPer / 16; ++q) {
     const uint32_t cb = kColsPer * g + 16 * q;
     float re[16], im[16];
+    float2 w = tw2<-1>(c.tab, cb * t2);
 #pragma unroll
     for (int j = 0; j < 16; ++j) {
-      const float2 v = __half22float2(kf[(cb + j) * 128 + f2]);
-      re[j] = v.x * sc;
-      im[j] = v.y * sc;
+      re[j] = w.x;
+      im[j] = w.y;
+      if (j < 15) w = cmul(w, st);
     }
-    tst8(taddr(c, c.aux + cb), re);
-    tst8(taddr(c, c.aux + cb + 8), re + 8);
-    tst8(taddr(c, c.aux + 64 + cb), im);
-    tst8(taddr(c, c.aux + 64 + cb + 8), im + 8);
+    tst8(taddr(c, TTW + cb), re);
+    tst8(taddr(c, TTW + cb + 8), re + 8);
+    tst8(taddr(c, TTW + 64 + cb), im);
+    tst8(taddr(c, TTW + 64 + cb + 8), im + 8);
   }
   tst_wait();
+}
+
+// k_f' of head h as raw fp16 pairs: column f1, lane f2
+__device__ __forceinline__ void load_kf16_tmem(const Ctx& c, const __half2* __restrict__ kf) {
+  uint32_t f2, g;
+  coords(f2, g);
+  const uint32_t* src = reinterpret_cast<const uint32_t*>(kf) + f2;
+#pragma unroll
+  for (uint32_t q = 0; q < kColsPer / 8; ++q) {
+    const uint32_t cb = kColsPer * g + 8 * q;
+    uint32_t v[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) v[j] = __ldg(src + (cb + j) * 128);
+    tst8(taddr(c, c.aux + cb), reinterpret_cast<const float*>(v));
+  }
+  tst_wait();
+}
+
+// A exit from the TMEM twiddles: X[t2][f1] w^(f1 t2) -> planes [-Xi | Xr | Xi]
+template <typename T>
+__device__ __forceinline__ void epi_A_exit_tw(const Ctx& c) {
+  uint32_t t2, g;
+  coords(t2, g);
+  unsigned char* op = c.sm + c.sop;
+#pragma unroll
+  for (uint32_t q = 0; q < kColsPer / 8; ++q) {
+    const uint32_t cb = kColsPer * g + 8 * q;
+    float re[8], im[8], wr[8], wi[8];
+    tld<8>(taddr(c, c.tw + cb), re);
+    tld<8>(taddr(c, c.tw + 64 + cb), im);
+    tld<8>(taddr(c, TTW + cb), wr);
+    tld<8>(taddr(c, TTW + 64 + cb), wi);
+    tc::ld_wait();
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const float a = re[j], b = im[j];
+      re[j] = fmaf(a, wr[j], -b * wi[j]);
+      im[j] = fmaf(a, wi[j], b * wr[j]);
+    }
+    st8n<T>(op + off_bmn(cb, t2), im);
+    st8<T>(op + 16384 + off_bmn(cb, t2), re);
+    st8<T>(op + 32768 + off_bmn(cb, t2), im);
+  }
+}
+
+// B' exit from the TMEM twiddles: w^(-f1 t2) -> stage-A' operand (K-major)
+template <typename T>
+__device__ __forceinline__ void epi_Bp_exit_tw(const Ctx& c) {
+  uint32_t t2, g;
+  coords(t2, g);
+  unsigned char* op = c.sm + c.sop;
+#pragma unroll
+  for (uint32_t q = 0; q < kColsPer / 8; ++q) {
+    const uint32_t cb = kColsPer * g + 8 * q;
+    float re[8], im[8], wr[8], wi[8];
+    tld<8>(taddr(c, c.tw + cb), re);
+    tld<8>(taddr(c, c.tw + 64 + cb), im);
+    tld<8>(taddr(c, TTW + cb), wr);
+    tld<8>(taddr(c, TTW + 64 + cb), wi);
+    tc::ld_wait();
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const float a = re[j], b = im[j];
+      re[j] = fmaf(a, wr[j], b * wi[j]);  // twiddle_row<+1>'s rounding
+      im[j] = fmaf(a, -wi[j], b * wr[j]);
+    }
+    st8<T>(op + off_kmaj(t2, cb, 16384), re);
+    st8<T>(op + off_kmaj(t2, 64 + cb, 16384), im);
+  }
+}
+
+// A' exit with the head's k_f' scale folded in: z[128 t1 + t2], t1 = R g + j
+template <typename T>
+__device__ __forceinline__ void store_rows_sc(const Ctx& c, T* __restrict__ out, int b0, int B,
+                                              int H, int h, float sc) {
+  uint32_t t2, g;
+  coords(t2, g);
+  constexpr int R = 32 / kGroups;
+  float re[R], im[R];
+  tld<R>(taddr(c, c.tw + R * g), re);
+  tld<R>(taddr(c, c.tw + 32 + R * g), im);
+  tc::ld_wait();
+  T* o0 = out + ((size_t)b0 * H + h) * 4096 + 128 * (R * g) + t2;
+#pragma unroll
+  for (int j = 0; j < R; ++j) o0[128 * j] = cvt<T>(re[j] * sc);
+  if (b0 + 1 < B) {
+    T* o1 = out + ((size_t)(b0 + 1) * H + h) * 4096 + 128 * (R * g) + t2;
+#pragma unroll
+    for (int j = 0; j < R; ++j) o1[128 * j] = cvt<T>(im[j] * sc);
+  }
+}
+
+// saved U layout: bf16 pairs [pair][f1 / 4][f2][f1 % 4] — a thread's four
+// consecutive f1 are one 16-byte store / load, a warp's 32 lanes (f2) 512
+// contiguous bytes
+__host__ __device__ __forceinline__ uint32_t usave_idx(uint32_t f1, uint32_t f2) {
+  return ((f1 >> 2) * 128 + f2) * 4 + (f1 & 3);
 }
 
 template <typename T>
@@ -676,6 +785,9 @@ __global__ void __launch_bounds__(kThreads, 1)
                   const __half2* __restrict__ kf16, const float* __restrict__ kscale,
                   const uint4* __restrict__ mats, const float2* __restrict__ tab_g, int B, int H,
                   int total, uint32_t* __restrict__ usave) {
+  // bf16 planes take the scaled product (k_f' x 2^e, e <= ~30) and the
+  // store undoes the scale; fp16 planes need it applied at the B exit
+  constexpr bool kScaleEarly = std::is_same<T, __half>::value;
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   __shared__ uint32_t tmem_slot;
   __shared__ __align__(8) uint64_t bars[4];  // mma[2], in[2]
@@ -686,62 +798,74 @@ __global__ void __launch_bounds__(kThreads, 1)
   setup(sm, &tmem_slot, bars, 4, 0, mats, tab_g, SMAT3, STAB3);
   const uint32_t slot = threadIdx.x / kSlotThreads;
   Ctx c = make_ctx(sm, tmem_slot, slot, &bars[slot], true);
-  c.aux = TKF + 128 * slot;
+  c.aux = TKF16 + 64 * slot;
+  if (slot == 0) init_tw_tmem(c);
+  cta_sync_tc();
   c.on = 4u * (uint32_t)((i1 - i0 + (int)slot) / 2);  // the other slot's pairs x 4 stages
   uint64_t* in_bar = &bars[2 + slot];
   const bool lead = slot_leader();
   int item = i0 + (int)slot;
   if (lead && item < i1) load_pair(sm + c.in_off, &umap, item / npairs, 2 * (item % npairs), in_bar);
   int cur_h = -1;
+  float sc = 1.f;
   for (uint32_t it = 0; item < i1; item += 2, ++it) {
     const int h = item / npairs, pr = item % npairs;
     if (h != cur_h) {
-      { TT_BEGIN load_kf_tmem(c, kf16 + (size_t)h * kN, __ldg(kscale + h)); TT_END(17) }
+      { TT_BEGIN load_kf16_tmem(c, kf16 + (size_t)h * kN); TT_END(17) }
+      sc = __ldg(kscale + h);
       cur_h = h;
     }
     { TT_BEGIN ptx::mbar_wait(in_bar, it & 1); TT_END(16) }
     issue<T, true>(c, 0);
-    { TT_BEGIN epi_A_exit<T, true>(c); TT_END(18) }
+    { TT_BEGIN epi_A_exit_tw<T>(c); TT_END(18) }
     // the input buffer is free since stage A completed: the next pair's TMA
     // goes out from the leader while the stage-B MMAs run
     issue<T, true>(c, 1, [&] {
       if (item + 2 < i1)
         load_pair(sm + c.in_off, &umap, (item + 2) / npairs, 2 * ((item + 2) % npairs), in_bar);
     });
-    // ---- B exit: Z = X * k_f' -> Zr/Zi[k = f2][n = f1]
+    // ---- B exit: Z = X * k_f' (unscaled; the scale is folded into the store)
     {
+      TT_BEGIN
       uint32_t f2, g;
       coords(f2, g);
       unsigned char* op = c.sm + c.sop;
 #pragma unroll
       for (uint32_t q = 0; q < kColsPer / 8; ++q) {
         const uint32_t cb = kColsPer * g + 8 * q;
-        float re[8], im[8], kr[8], ki[8];
+        float re[8], im[8], kk[8];
         tld<8>(taddr(c, c.tw + cb), re);
         tld<8>(taddr(c, c.tw + 64 + cb), im);
-        tld<8>(taddr(c, c.aux + cb), kr);
-        tld<8>(taddr(c, c.aux + 64 + cb), ki);
+        tld<8>(taddr(c, c.aux + cb), kk);
         tc::ld_wait();
-        if (usave) {  // U = F(u) for the backward, bf16 pairs [pair][f1][f2]
-          uint32_t* us = usave + (size_t)item * kN + (size_t)cb * 128 + f2;
-#pragma unroll
-          for (int j = 0; j < 8; ++j) us[j * 128] = pack_bf2(re[j], im[j]);
+        if (usave) {  // U = F(u) for the backward, bf16 pairs (usave_idx layout)
+          uint4* us = reinterpret_cast<uint4*>(usave + (size_t)item * kN + usave_idx(cb, f2));
+          us[0] = make_uint4(pack_bf2(re[0], im[0]), pack_bf2(re[1], im[1]), pack_bf2(re[2], im[2]),
+                             pack_bf2(re[3], im[3]));
+          us[128] = make_uint4(pack_bf2(re[4], im[4]), pack_bf2(re[5], im[5]),
+                               pack_bf2(re[6], im[6]), pack_bf2(re[7], im[7]));
         }
 #pragma unroll
         for (int j = 0; j < 8; ++j) {
+          float2 k = __half22float2(*reinterpret_cast<const __half2*>(&kk[j]));
+          if constexpr (kScaleEarly) {  // fp16 planes: keep Z in the operand range
+            k.x *= sc;
+            k.y *= sc;
+          }
           const float a = re[j], b = im[j];
-          re[j] = fmaf(a, kr[j], -b * ki[j]);
-          im[j] = fmaf(a, ki[j], b * kr[j]);
+          re[j] = fmaf(a, k.x, -b * k.y);
+          im[j] = fmaf(a, k.y, b * k.x);
         }
         st8<T>(op + off_bmn(cb, f2), re);  // planes [Zr | Zi | -Zr]
         st8<T>(op + 16384 + off_bmn(cb, f2), im);
         st8n<T>(op + 32768 + off_bmn(cb, f2), re);
       }
+      TT_END(19)
     }
     issue<T, true>(c, 2);
-    { TT_BEGIN epi_Bp_exit<T>(c); TT_END(20) }
+    { TT_BEGIN epi_Bp_exit_tw<T>(c); TT_END(20) }
     issue<T, true>(c, 3);
-    { TT_BEGIN store_rows<T>(c, y, 2 * pr, B, H, h); TT_END(21) }
+    { TT_BEGIN store_rows_sc<T>(c, y, 2 * pr, B, H, h, kScaleEarly ? 1.f : sc); TT_END(21) }
   }
   teardown(tmem_slot);
 }
@@ -830,10 +954,17 @@ __global__ void __launch_bounds__(kThreads, 1)
         // ---- U from the forward (loads in flight across DY's stage A)
         uint32_t f2, g;
         coords(f2, g);
-        const uint32_t* us = usave + (size_t)(a + j) * kN + (size_t)(kColsPer * g) * 128 + f2;
+        const uint4* us = reinterpret_cast<const uint4*>(usave + (size_t)(a + j) * kN +
+                                                         usave_idx(kColsPer * g, f2));
         TT_BEGIN
 #pragma unroll
-        for (uint32_t jj = 0; jj < kColsPer; ++jj) ur[jj] = __ldg(us + jj * 128);
+        for (uint32_t q = 0; q < kColsPer / 4; ++q) {
+          const uint4 v = __ldg(us + q * 128);
+          ur[4 * q] = v.x;
+          ur[4 * q + 1] = v.y;
+          ur[4 * q + 2] = v.z;
+          ur[4 * q + 3] = v.w;
+        }
         TT_END(26)
       } else {
       // ---- U = F(u), parked as bf16 pairs
