@@ -37,6 +37,7 @@
 #include "fb_internal.h"
 #include "fb_ptx.cuh"
 #include "fb_tc.cuh"
+#include "fb_reg.cuh"
 
 namespace fb {
 namespace tcfft {
@@ -261,6 +262,11 @@ struct Ctx {
   uint32_t seg0;     // nb at the start of the current segment
   uint32_t obase;    // the other slot's batch count at the segment start
   uint32_t on;       // the other slot's batches in the segment
+  // MMA-issue lock (experiment switch FB_TC_SCHED=1): a leader issues its
+  // whole batch while holding it, so the slots' batches reach the tensor pipe
+  // contiguous and first-ready-first-served, without waiting for each
+  // other's completion (the token) or interleaving (free issue)
+  uint32_t* lock;
 };
 
 __device__ __forceinline__ Ctx make_ctx(unsigned char* sm, uint32_t tmem, uint32_t slot,
@@ -281,6 +287,7 @@ __device__ __forceinline__ Ctx make_ctx(unsigned char* sm, uint32_t tmem, uint32
   c.slot = slot;
   c.other_bar = mma_bar + (slot ? -1 : 1);
   c.nb = c.seg0 = c.obase = c.on = 0;
+  c.lock = nullptr;
   return c;
 }
 
@@ -474,6 +481,9 @@ __device__ __forceinline__ void issue(Ctx& c, int stage, const Hook& hook = Hook
     } else if (j < c.on) {
       ptx::mbar_wait(c.other_bar, (c.obase + j) & 1);
     }
+    if (c.lock)
+      while (atomicCAS(c.lock, 0u, 1u) != 0u) {
+      }
     switch (stage) {
       case 0: mma_stage_A<T>(c); break;
       case 1: mma_stage_B<T, false, W3>(c); break;
@@ -483,6 +493,7 @@ __device__ __forceinline__ void issue(Ctx& c, int stage, const Hook& hook = Hook
       default: mma_stage_Ap_full<T>(c); break;
     }
     tc::commit(c.mma_bar);
+    if (c.lock) atomicExch(c.lock, 0u);
     hook();
   }
   ++c.nb;
@@ -701,6 +712,9 @@ __device__ __forceinline__ void load_kf16_tmem(const Ctx& c, const __half2* __re
 // A exit from the TMEM twiddles: X[t2][f1] w^(f1 t2) -> planes [-Xi | Xr | Xi]
 template <typename T>
 __device__ __forceinline__ void epi_A_exit_tw(const Ctx& c) {
+#ifdef FB_TC_NOEPI
+  return;
+#endif
   uint32_t t2, g;
   coords(t2, g);
   unsigned char* op = c.sm + c.sop;
@@ -728,6 +742,9 @@ __device__ __forceinline__ void epi_A_exit_tw(const Ctx& c) {
 // B' exit from the TMEM twiddles: w^(-f1 t2) -> stage-A' operand (K-major)
 template <typename T>
 __device__ __forceinline__ void epi_Bp_exit_tw(const Ctx& c) {
+#ifdef FB_TC_NOEPI
+  return;
+#endif
   uint32_t t2, g;
   coords(t2, g);
   unsigned char* op = c.sm + c.sop;
@@ -755,6 +772,9 @@ __device__ __forceinline__ void epi_Bp_exit_tw(const Ctx& c) {
 template <typename T>
 __device__ __forceinline__ void store_rows_sc(const Ctx& c, T* __restrict__ out, int b0, int B,
                                               int H, int h, float sc) {
+#ifdef FB_TC_NOEPI
+  return;
+#endif
   uint32_t t2, g;
   coords(t2, g);
   constexpr int R = 32 / kGroups;
@@ -784,24 +804,27 @@ __global__ void __launch_bounds__(kThreads, 1)
     tc_fwd_kernel(const __grid_constant__ CUtensorMap umap, T* __restrict__ y,
                   const __half2* __restrict__ kf16, const float* __restrict__ kscale,
                   const uint4* __restrict__ mats, const float2* __restrict__ tab_g, int B, int H,
-                  int total, uint32_t* __restrict__ usave) {
+                  int total, uint32_t* __restrict__ usave, int sched) {
   // bf16 planes take the scaled product (k_f' x 2^e, e <= ~30) and the
   // store undoes the scale; fp16 planes need it applied at the B exit
   constexpr bool kScaleEarly = std::is_same<T, __half>::value;
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   __shared__ uint32_t tmem_slot;
   __shared__ __align__(8) uint64_t bars[4];  // mma[2], in[2]
+  __shared__ uint32_t mma_lock;
   unsigned char* sm = smem_base(smem_raw);
   const int npairs = (B + 1) / 2;
   int i0, i1;
   cta_range(total, i0, i1);
+  if (threadIdx.x == 0) mma_lock = 0;
   setup(sm, &tmem_slot, bars, 4, 0, mats, tab_g, SMAT3, STAB3);
   const uint32_t slot = threadIdx.x / kSlotThreads;
   Ctx c = make_ctx(sm, tmem_slot, slot, &bars[slot], true);
   c.aux = TKF16 + 64 * slot;
   if (slot == 0) init_tw_tmem(c);
   cta_sync_tc();
-  c.on = 4u * (uint32_t)((i1 - i0 + (int)slot) / 2);  // the other slot's pairs x 4 stages
+  if (sched == 1) c.lock = &mma_lock;
+  else c.on = 4u * (uint32_t)((i1 - i0 + (int)slot) / 2);  // token: the other slot's pairs x 4 stages
   uint64_t* in_bar = &bars[2 + slot];
   const bool lead = slot_leader();
   int item = i0 + (int)slot;
@@ -825,6 +848,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         load_pair(sm + c.in_off, &umap, (item + 2) / npairs, 2 * ((item + 2) % npairs), in_bar);
     });
     // ---- B exit: Z = X * k_f' (unscaled; the scale is folded into the store)
+#ifndef FB_TC_NOEPI
     {
       TT_BEGIN
       uint32_t f2, g;
@@ -862,6 +886,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       TT_END(19)
     }
+#endif
     issue<T, true>(c, 2);
     { TT_BEGIN epi_Bp_exit_tw<T>(c); TT_END(20) }
     issue<T, true>(c, 3);
@@ -873,41 +898,71 @@ __global__ void __launch_bounds__(kThreads, 1)
 // ------------------------------------------------------------------ backward
 // Persistent like the forward.  The CTA walks its pairs head segment by head
 // segment; inside a segment slot s takes local pairs s, s+2, ...  Per pair:
-// U = F(u) is parked in TMEM as bf16 pairs, DY = F(dy); then S += conj(U) DY
-// (S = the CTA's dK spectrum, fp32 in TMEM, updated strictly in pair order
-// across the slots through two mbarriers so the sum is deterministic) and
-// du = F^-1(DY conj(k_f')).  At a segment end S goes to spart[cta][seg]
-// (natural order) for the finalize kernel (dKbar = Re F^-1(sum S)/n,
-// dD = dKbar[0]).
+// DY = F(dy); S += conj(U) DY (S = the CTA's dK spectrum, fp32 in TMEM,
+// updated strictly in pair order across the slots through two mbarriers so
+// the sum is deterministic) and du = F^-1(DY conj(k_f')).  U = F(u) comes
+// from the forward's saved transform (SAVED) or is computed here first and
+// parked in the workspace (same layout, same values).  At a segment end slot 0
+// transforms S back on the tensor cores (B', A': the causal lags t < N,
+// real part) into a time-domain partial tpart[cta][seg][t]; tc_dk_tail sums
+// a head's partials in a fixed order and applies the regularizer chain rule.
+// TMEM: slot s works in [128 s, 128 s + 128); S at TS2 (re f1 | im f1); the
+// forward's twiddle table at TTW.
+constexpr uint32_t TS2 = 256;
+
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(ptx::smem_u32(bar)) : "memory");
 }
 
-// SAVED: U comes from the forward's usave (bf16 pairs, exactly what the
-// recompute path parks) instead of F(u): one transform per pair fewer.
+__device__ __forceinline__ void prefetch_l2(const void* p, uint32_t bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
+}
+
+// A' exit of the S inverse: Re of the lags t = 128 t1 + t2 (t1 < 32), scaled
+__device__ __forceinline__ void store_tpart(const Ctx& c, float* __restrict__ dst, float sc) {
+  uint32_t t2, g;
+  coords(t2, g);
+  constexpr int R = 32 / kGroups;
+  float re[R];
+  tld<R>(taddr(c, c.tw + R * g), re);
+  tc::ld_wait();
+  float* o = dst + 128 * (R * g) + t2;
+#pragma unroll
+  for (int j = 0; j < R; ++j) o[128 * j] = re[j] * sc;
+}
+
+// SAVED: U comes from the forward's usave (bf16 pairs, usave_idx layout)
+// instead of F(u): one transform per pair fewer.
 template <typename T, bool SAVED>
 __global__ void __launch_bounds__(kThreads, 1)
     tc_bwd_kernel(const __grid_constant__ CUtensorMap dymap, const __grid_constant__ CUtensorMap umap,
                   T* __restrict__ du, const __half2* __restrict__ kf16,
                   const float* __restrict__ kscale, const uint4* __restrict__ mats,
-                  const float2* __restrict__ tab_g, float2* __restrict__ spart, int B, int H,
-                  int total, int maxseg, const uint32_t* __restrict__ usave) {
+                  const float2* __restrict__ tab_g, float* __restrict__ tpart, int B, int H,
+                  int total, int maxseg, const uint32_t* __restrict__ usave,
+                  uint32_t* __restrict__ uscratch, int sched) {
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   __shared__ uint32_t tmem_slot;
   __shared__ __align__(8) uint64_t bars[6];  // mma[2], in[2], S chain[2] (256 arrivals)
+  __shared__ uint32_t mma_lock;
+  __shared__ float red[8];
   unsigned char* sm = smem_base(smem_raw);
   const int npairs = (B + 1) / 2;
   int i0, i1;
   cta_range_even(total, i0, i1);
+  if (threadIdx.x == 0) mma_lock = 0;
   setup(sm, &tmem_slot, bars, 6, 2, mats, tab_g, SMAT3, STAB3);
   const uint32_t slot = threadIdx.x / kSlotThreads;
   Ctx c = make_ctx(sm, tmem_slot, slot, &bars[slot], true);
-  c.aux = TPK + 64 * slot;
+  if (slot == 0) init_tw_tmem(c);
+  cta_sync_tc();
+  if (sched == 1) c.lock = &mma_lock;
   uint64_t* in_bar = &bars[2 + slot];
   uint64_t* chain_mine = &bars[4 + slot];
   uint64_t* chain_other = &bars[5 - slot];
   const bool lead = slot_leader();
   const uint32_t* kfs = reinterpret_cast<const uint32_t*>(sm + SKF3);
+  const uint32_t* ubase = SAVED ? usave : uscratch;
   uint32_t in_cnt = 0, base0 = 0, base1 = 0;
   int seg = 0;
   for (int a = i0; a < i1; ++seg) {
@@ -932,8 +987,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       float z[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
 #pragma unroll
       for (uint32_t q = 0; q < W / 8; ++q) {
-        tst8(tmem_slot + lane_off + TS + W * g8 + 8 * q, z);
-        tst8(tmem_slot + lane_off + TS + 64 + W * g8 + 8 * q, z);
+        tst8(tmem_slot + lane_off + TS2 + W * g8 + 8 * q, z);
+        tst8(tmem_slot + lane_off + TS2 + 64 + W * g8 + 8 * q, z);
       }
       tst_wait();
       cta_sync_tc();
@@ -949,31 +1004,16 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     for (int j = (int)slot, k = 0; j < L; j += 2, ++k) {
       const int b0 = 2 * (a + j - h * npairs);
-      uint32_t ur[kColsPer];
+      const uint32_t* up = ubase + (size_t)(a + j) * kN;
       if constexpr (SAVED) {
-        // ---- U from the forward (loads in flight across DY's stage A)
-        uint32_t f2, g;
-        coords(f2, g);
-        const uint4* us = reinterpret_cast<const uint4*>(usave + (size_t)(a + j) * kN +
-                                                         usave_idx(kColsPer * g, f2));
-        TT_BEGIN
-#pragma unroll
-        for (uint32_t q = 0; q < kColsPer / 4; ++q) {
-          const uint4 v = __ldg(us + q * 128);
-          ur[4 * q] = v.x;
-          ur[4 * q + 1] = v.y;
-          ur[4 * q + 2] = v.z;
-          ur[4 * q + 3] = v.w;
-        }
-        TT_END(26)
+        if (lead) prefetch_l2(up, kN * sizeof(uint32_t));  // read back in the S epilogue
       } else {
-      // ---- U = F(u), parked as bf16 pairs
-      { TT_BEGIN ptx::mbar_wait(in_bar, in_cnt & 1); TT_END(22) }
-      ++in_cnt;
-      issue<T, true>(c, 0);
-      { TT_BEGIN epi_A_exit<T, true>(c); TT_END(25) }
-      issue<T, true>(c, 1, [&] { load_pair(sm + c.in_off, &dymap, h, b0, in_bar); });
-      {
+        // ---- U = F(u), parked in the workspace (the saved layout)
+        { TT_BEGIN ptx::mbar_wait(in_bar, in_cnt & 1); TT_END(22) }
+        ++in_cnt;
+        issue<T, true>(c, 0);
+        { TT_BEGIN epi_A_exit_tw<T>(c); TT_END(25) }
+        issue<T, true>(c, 1, [&] { load_pair(sm + c.in_off, &dymap, h, b0, in_bar); });
         uint32_t f2, g;
         coords(f2, g);
 #pragma unroll
@@ -983,28 +1023,18 @@ __global__ void __launch_bounds__(kThreads, 1)
           tld<8>(taddr(c, c.tw + cb), re);
           tld<8>(taddr(c, c.tw + 64 + cb), im);
           tc::ld_wait();
-#pragma unroll
-          for (int jj = 0; jj < 8; ++jj) re[jj] = __uint_as_float(pack_bf2(re[jj], im[jj]));
-          tst8(taddr(c, c.aux + cb), re);
+          uint4* us = reinterpret_cast<uint4*>(uscratch + (size_t)(a + j) * kN + usave_idx(cb, f2));
+          us[0] = make_uint4(pack_bf2(re[0], im[0]), pack_bf2(re[1], im[1]), pack_bf2(re[2], im[2]),
+                             pack_bf2(re[3], im[3]));
+          us[128] = make_uint4(pack_bf2(re[4], im[4]), pack_bf2(re[5], im[5]),
+                               pack_bf2(re[6], im[6]), pack_bf2(re[7], im[7]));
         }
-        tst_wait();
-      }
       }
       // ---- DY = F(dy)
       { TT_BEGIN ptx::mbar_wait(in_bar, in_cnt & 1); TT_END(23) }
       ++in_cnt;
       issue<T, true>(c, 0);
-      if constexpr (SAVED) {  // the saved U into this slot's parking columns
-        TT_BEGIN
-        uint32_t f2, g;
-        coords(f2, g);
-#pragma unroll
-        for (uint32_t q = 0; q < kColsPer / 8; ++q)
-          tst8(taddr(c, c.aux + kColsPer * g + 8 * q), reinterpret_cast<const float*>(ur + 8 * q));
-        tst_wait();
-        TT_END(27)
-      }
-      { TT_BEGIN epi_A_exit<T, true>(c); TT_END(25) }
+      { TT_BEGIN epi_A_exit_tw<T>(c); TT_END(25) }
       issue<T, true>(c, 1, [&] {  // next pair's first input, off the critical path
         if (j + 2 < L) load_pair(sm + c.in_off, SAVED ? &dymap : &umap, h, b0 + 4, in_bar);
       });
@@ -1021,32 +1051,35 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll 1
         for (uint32_t q = 0; q < kColsPer / 8; ++q) {
           const uint32_t col = kColsPer * g + 8 * q;
-          float dr[8], di[8], pk[8], sr[8], si[8];
+          float dr[8], di[8], sr[8], si[8];
+          const uint4* us = reinterpret_cast<const uint4*>(up + usave_idx(col, f2));
+          // L2 loads (.cg): the recompute path wrote U moments ago in this kernel
+          const uint4 ua = __ldcg(us), ub = __ldcg(us + 128);
+          const uint32_t pk[8] = {ua.x, ua.y, ua.z, ua.w, ub.x, ub.y, ub.z, ub.w};
           tld<8>(taddr(c, c.tw + col), dr);
           tld<8>(taddr(c, c.tw + 64 + col), di);
-          tld<8>(taddr(c, c.aux + col), pk);
-          tld<8>(taddr(c, TS + col), sr);
-          tld<8>(taddr(c, TS + 64 + col), si);
+          tld<8>(taddr(c, TS2 + col), sr);
+          tld<8>(taddr(c, TS2 + 64 + col), si);
           tc::ld_wait();
 #pragma unroll
           for (int jj = 0; jj < 8; ++jj) {
-            const float2 u = unpack_bf2(__float_as_uint(pk[jj]));
+            const float2 u = unpack_bf2(pk[jj]);
             sr[jj] = fmaf(u.x, dr[jj], fmaf(u.y, di[jj], sr[jj]));
             si[jj] = fmaf(u.x, di[jj], fmaf(-u.y, dr[jj], si[jj]));
             // k_f'[f1 + 64 f2]; upper half (f2 >= 64) by conjugate symmetry
             const uint32_t f1 = col + jj;
-            const bool up = f2 >= 64;
-            const uint32_t idx = !up ? f1 * KFH_ROW + f2
-                                     : (f1 ? (64 - f1) * KFH_ROW + (127 - f2) : 128 - f2);
+            const bool upper = f2 >= 64;
+            const uint32_t idx = !upper ? f1 * KFH_ROW + f2
+                                        : (f1 ? (64 - f1) * KFH_ROW + (127 - f2) : 128 - f2);
             float2 kv = __half22float2(*reinterpret_cast<const __half2*>(&kfs[idx]));
             kv.x *= osc;
-            kv.y *= up ? -osc : osc;
+            kv.y *= upper ? -osc : osc;
             const float a0 = dr[jj], b = di[jj];
             dr[jj] = fmaf(a0, kv.x, b * kv.y);
             di[jj] = fmaf(b, kv.x, -a0 * kv.y);
           }
-          tst8(taddr(c, TS + col), sr);
-          tst8(taddr(c, TS + 64 + col), si);
+          tst8(taddr(c, TS2 + col), sr);
+          tst8(taddr(c, TS2 + 64 + col), si);
           st8<T>(op + off_bmn(col, f2), dr);  // planes [Zr | Zi | -Zr]
           st8<T>(op + 16384 + off_bmn(col, f2), di);
           st8n<T>(op + 32768 + off_bmn(col, f2), dr);
@@ -1056,30 +1089,122 @@ __global__ void __launch_bounds__(kThreads, 1)
         mbar_arrive(chain_mine);
       }
       issue<T, true>(c, 2);
-      { TT_BEGIN epi_Bp_exit<T>(c); TT_END(28) }
+      { TT_BEGIN epi_Bp_exit_tw<T>(c); TT_END(28) }
       issue<T, true>(c, 3);
       { TT_BEGIN store_rows<T>(c, du, b0, B, H, h); TT_END(29) }
     }
     base0 += (uint32_t)(L + 1) / 2;
     base1 += (uint32_t)L / 2;
-    // ---- segment end: flush S (natural order f = f1 + 64 f2)
+    // ---- segment end: slot 0 inverts S on the tensor cores (B', A') into the
+    // time-domain partial tpart[cta][seg] (Re, lags t < N, x 1/n)
     { TT_BEGIN cta_sync_tc(); TT_END(31) }
-    {
-      const uint32_t t = threadIdx.x;
-      constexpr uint32_t W = 64 / (kThreads / 128);
-      const uint32_t f2 = 32 * ((t >> 5) & 3) + (t & 31), g8 = t >> 7;
-      const uint32_t lane_off = (32u * ((t >> 5) & 3)) << 16;
-      float sr[W], si[W];
-      tld<W>(tmem_slot + lane_off + TS + W * g8, sr);
-      tld<W>(tmem_slot + lane_off + TS + 64 + W * g8, si);
-      tc::ld_wait();
-      float2* sp = spart + ((size_t)blockIdx.x * maxseg + seg) * kN + 64 * f2 + W * g8;
+    float ssc = 1.f;
+    if (slot == 0) {
+      uint32_t f2, g;
+      coords(f2, g);
+      // fp16 operands need S brought into range: a power-of-two scale from
+      // the segment's max |S| (bf16 has fp32's exponent range: scale 1)
+      if constexpr (std::is_same<T, __half>::value) {
+        float mx = 0.f;
 #pragma unroll
-      for (uint32_t jj = 0; jj < W; ++jj) sp[jj] = make_float2(sr[jj], si[jj]);
+        for (uint32_t q = 0; q < kColsPer / 8; ++q) {
+          float sr[8], si[8];
+          tld<8>(taddr(c, TS2 + kColsPer * g + 8 * q), sr);
+          tld<8>(taddr(c, TS2 + 64 + kColsPer * g + 8 * q), si);
+          tc::ld_wait();
+#pragma unroll
+          for (int jj = 0; jj < 8; ++jj) mx = fmaxf(mx, fmaxf(fabsf(sr[jj]), fabsf(si[jj])));
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+        if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = mx;
+        slot_sync(c);
+        mx = red[0];
+#pragma unroll
+        for (int w = 1; w < 8; ++w) mx = fmaxf(mx, red[w]);
+        int e = 0;
+        if (mx > 0.f) frexpf(mx, &e);
+        // max |S| -> [2^7, 2^8): the B' exit's 128-term sums stay below 2^15
+        ssc = mx > 0.f ? ldexpf(1.f, 8 - e) : 1.f;
+      }
+      unsigned char* op = c.sm + c.sop;
+#pragma unroll
+      for (uint32_t q = 0; q < kColsPer / 8; ++q) {
+        const uint32_t col = kColsPer * g + 8 * q;
+        float sr[8], si[8];
+        tld<8>(taddr(c, TS2 + col), sr);
+        tld<8>(taddr(c, TS2 + 64 + col), si);
+        tc::ld_wait();
+#pragma unroll
+        for (int jj = 0; jj < 8; ++jj) {
+          sr[jj] *= ssc;
+          si[jj] *= ssc;
+        }
+        st8<T>(op + off_bmn(col, f2), sr);  // planes [Zr | Zi | -Zr]
+        st8<T>(op + 16384 + off_bmn(col, f2), si);
+        st8n<T>(op + 32768 + off_bmn(col, f2), sr);
+      }
+    }
+    // S has been read: slot 1 may start the next segment (k_f' load, S = 0)
+    // while slot 0 finishes the inverse
+    cta_sync_tc();
+    if (slot == 0) {
+      issue<T, true>(c, 2);
+      epi_Bp_exit_tw<T>(c);
+      issue<T, true>(c, 3);
+      store_tpart(c, tpart + ((size_t)blockIdx.x * maxseg + seg) * 4096,
+                  1.f / (ssc * (float)kN));
     }
     a += L;
   }
   teardown(tmem_slot);
+}
+
+// dKbar[h] = sum of the head's time-domain partials (CTA order, fixed), dD =
+// dKbar[0] (lag 0), dK = the regularizer chain rule (fp64 tap sums in the
+// reference order) — the tail of the tensor-core backward
+__global__ void __launch_bounds__(512)
+    tc_dk_tail_kernel(const float* __restrict__ tpart, float* __restrict__ dkbar_out,
+                      float* __restrict__ dD, const float* __restrict__ kbar,
+                      const uint8_t* __restrict__ keep, float* __restrict__ dK, int64_t p,
+                      double keep_scale, int freq, int ctas, int total, int npairs, int maxseg) {
+  constexpr uint32_t N = 4096;
+  __shared__ float row[N];
+  const int h = blockIdx.x;
+  const int64_t G = ctas, T = total, np = npairs;
+  const int64_t U = (T + 1) / 2;
+  // the CTA owning pair i under the backward's even-aligned shares
+  auto owner = [&](int64_t i) { return (int)((((i / 2) + 1) * G - 1) / U); };
+  const int c0 = owner((int64_t)h * np), c1 = owner(((int64_t)h + 1) * np - 1);
+  const size_t base = (size_t)h * N;
+  for (uint32_t t = threadIdx.x; t < N; t += blockDim.x) {
+    float g = 0.f;
+    for (int c = c0; c <= c1; ++c) {
+      const int64_t start = 2 * ((int64_t)c * U / G);
+      const int sg = h - (int)(start / np);
+      g += __ldg(tpart + ((size_t)c * maxseg + sg) * N + t);
+    }
+    if (dkbar_out) dkbar_out[base + t] = g;
+    if (t == 0) dD[h] = g;
+    row[t] = (!freq && __ldg(kbar + base + t) == 0.f) ? 0.f : g;
+  }
+  __syncthreads();
+  if (!freq) {
+    const double w = (double)(2 * p + 1);
+    for (uint32_t t = threadIdx.x; t < N; t += blockDim.x) {
+      const int64_t lo = (int64_t)t >= p ? (int64_t)t - p : 0;
+      const int64_t hi = ((int64_t)t + p < (int64_t)N - 1) ? (int64_t)t + p : (int64_t)N - 1;
+      double acc = 0.0;
+      for (int64_t q = lo; q <= hi; ++q) acc += (double)row[q];
+      double g = acc / w;
+      if (keep) g = keep[base + t] ? g * keep_scale : 0.0;
+      dK[base + t] = (float)g;
+    }
+  } else {
+    for (uint32_t t = threadIdx.x; t < N; t += blockDim.x)
+      dK[base + t] = reg_grad(kbar + base, row, keep ? keep + base : nullptr, t, N, p, keep_scale,
+                              freq);
+  }
 }
 
 // ------------------------------------------------------------------ three-pass rows
@@ -1578,6 +1703,15 @@ TcGrid tc_grid(const fb_plan* p, int64_t B) {
 
 }  // namespace
 
+// experiment switch: 0 = MMA token (forward) / free issue (backward), 1 = issue lock
+static int tc_sched() {
+  static const int v = [] {
+    const char* e = std::getenv("FB_TC_SCHED");
+    return e ? std::atoi(e) : 0;
+  }();
+  return v;
+}
+
 bool tc_eligible(const fb_plan* p) {
   return p->mode == FB_MODE_CAUSAL && p->N == 4096 && p->n == 8192 &&
          (p->dtype == FB_BF16 || p->dtype == FB_F16);
@@ -1611,22 +1745,28 @@ int tc_fwd(fb_plan* p, const void* u, void* y, int64_t B, cudaStream_t s, void* 
     k<<<(unsigned)gr.ctas, kThreads, SMEM_FWD, s>>>(map, (T*)y, (const __half2*)p->kf_tc,
                                                      p->kf_scale, (const uint4*)p->tc_mats, p->tw2,
                                                      (int)B, (int)p->H, gr.total,
-                                                     (uint32_t*)usave);
+                                                     (uint32_t*)usave, tc_sched());
     prof_mark(p, 0, 1, s);
     return cuda_status(cudaGetLastError(), "tc_fwd");
   };
   return p->dtype == FB_BF16 ? go(__nv_bfloat16{}) : go(__half{});
 }
 
+// workspace: time-domain dK partials [ctas][maxseg][4096] f32, then (recompute
+// path) the parked U = F(u) in the saved layout
+static size_t tpart_bytes(const TcGrid& gr) {
+  return ((size_t)gr.bctas * gr.maxseg * 4096 * sizeof(float) + 255) & ~size_t(255);
+}
 size_t tc_workspace(const fb_plan* p, int64_t B) {
   const TcGrid gr = tc_grid(p, B);
-  return (size_t)gr.bctas * gr.maxseg * kN * sizeof(float2) + 256;
+  return tpart_bytes(gr) + tc_saved_size(p, B) + 256;
 }
 
 int tc_bwd(fb_plan* p, const void* dy, const void* u, void* du, float* dK, float* dKbar, float* dD,
            int64_t B, void* ws, cudaStream_t s, const void* usave) {
   const TcGrid gr = tc_grid(p, B);
-  float2* spart = (float2*)ws;
+  float* tpart = (float*)ws;
+  uint32_t* uscratch = (uint32_t*)((char*)ws + tpart_bytes(gr));
   CUtensorMap dmap, umap;
   auto go = [&](auto tv) {
     using T = decltype(tv);
@@ -1638,7 +1778,8 @@ int tc_bwd(fb_plan* p, const void* dy, const void* u, void* du, float* dK, float
       prof_mark(p, 1, 0, s);
       kern<<<(unsigned)gr.bctas, kThreads, SMEM_BWD3, s>>>(
           dmap, umap, (T*)du, (const __half2*)p->kf_tc, p->kf_scale, (const uint4*)p->tc_mats,
-          p->tw2, spart, (int)B, (int)p->H, gr.total, gr.maxseg, (const uint32_t*)usave);
+          p->tw2, tpart, (int)B, (int)p->H, gr.total, gr.maxseg, (const uint32_t*)usave,
+          uscratch, tc_sched());
       prof_mark(p, 1, 1, s);
     };
     if (usave) launch(tc_bwd_kernel<T, true>);
@@ -1647,8 +1788,10 @@ int tc_bwd(fb_plan* p, const void* dy, const void* u, void* du, float* dK, float
   };
   int rc = p->dtype == FB_BF16 ? go(__nv_bfloat16{}) : go(__half{});
   if (rc) return rc;
-  const SpartMap m{gr.bctas, gr.total, gr.npairs, gr.maxseg, 1};
-  return sp_finalize(p, spart, nullptr, 0, dKbar, dD, dK, 1, &m, s);
+  tc_dk_tail_kernel<<<(unsigned)p->H, 512, 0, s>>>(
+      tpart, dKbar, dD, p->kbar, p->use_keep ? p->keep : nullptr, dK, p->p, p->keep_scale,
+      p->smooth_domain == FB_SMOOTH_FREQUENCY, gr.bctas, gr.total, gr.npairs, gr.maxseg);
+  return cuda_status(cudaGetLastError(), "tc_dk_tail");
 }
 
 // ---------------------------------------------------------------- three-pass rows (host)
