@@ -8,7 +8,11 @@ from __future__ import annotations
 import ctypes as C
 from pathlib import Path
 
-LIB_PATH = Path(__file__).resolve().parent / "libflashbutterfly.so"
+import os
+
+# FB_LIB_PATH: experiment builds only (e.g. an instrumented library); the
+# product always loads the in-tree libflashbutterfly.so
+LIB_PATH = Path(os.environ.get("FB_LIB_PATH") or Path(__file__).resolve().parent / "libflashbutterfly.so")
 
 FB_OK, FB_ERR_DIM, FB_ERR_PLAN, FB_ERR_CUDA, FB_ERR_NCCL, FB_ERR_ARG, FB_ERR_UNSUPPORTED = range(7)
 FB_MODE_CIRCULAR, FB_MODE_CAUSAL = 0, 1

@@ -3,6 +3,7 @@
 // every entry point either launches sm_100a kernels or returns an error.
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -209,6 +210,11 @@ int fb_plan_create(fb_plan** out, int64_t N, int64_t H, int mode, int dtype, int
   }
   cudaDeviceGetAttribute(&p->num_sms, cudaDevAttrMultiProcessorCount, device);
   p->use_tc = engine == FB_ENGINE_SINGLE && !simt && tc_eligible(p);
+  {  // experiment switch: FB_TC2=1 selects the 128 x 64 TMEM-resident design
+     // (fb_tc2.cu; measured slower end to end than the 64 x 128 default)
+    const char* e = std::getenv("FB_TC2");
+    p->tc_ver = (e && e[0] == '1') ? 2 : 1;
+  }
   rc = upload_twiddles2(&p->tw2, n);
   if (!rc && engine == FB_ENGINE_THREE && p->m <= 16) rc = upload_twiddles(&p->tw_n, n);
   if (!rc && engine == FB_ENGINE_THREE) rc = upload_twiddles2(&p->tw_l, p->l);

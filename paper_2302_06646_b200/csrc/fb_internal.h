@@ -24,8 +24,10 @@ struct fb_plan {
   uint8_t* keep = nullptr; // [H][N] dropout keep flags (training only)
   float* d = nullptr;      // [H] skip gains
   bool use_tc = false;       // tcgen05 single-pass path (fb_single_tc.cu)
+  int tc_ver = 1;            // 1: 64 x 128 Monarch (fb_single_tc.cu); 2: 128 x 64, TMEM-resident middle stages (fb_tc2.cu)
   void* tc_mats = nullptr;   // DFT blocks in UMMA smem images
-  void* kf_tc = nullptr;     // k_f' = k_f + D/n as fp16 pairs [H][f1 64][f2 128], scaled
+  void* kf_tc = nullptr;     // k_f' = k_f + D/n as fp16 pairs, scaled: v2 [H][f1 128][f2 64]
+                             // (f = f1 + 128 f2), v1 [H][f1 64][f2 128] (f = f1 + 64 f2)
   float* kf_scale = nullptr; // [H] inverse of that per-head power-of-two scale
   void* tcr_mats = nullptr;  // three-pass rows on tcgen05: DFT blocks (fb_single_tc.cu)
   bool prepared = false;
@@ -111,6 +113,12 @@ int tc_rows_spectrum(fb_plan* p, void* x1, int64_t npairs, cudaStream_t s);  // 
 int tc_rows_bwd(fb_plan* p, void* x1dy, const void* usave, float2* wdk, int64_t npairs,
                 cudaStream_t s);
 int tc_init(fb_plan* p);
+// version 2 (fb_tc2.cu)
+int tc2_init(fb_plan* p);
+int tc2_fwd(fb_plan* p, const void* u, void* y, int64_t B, int ctas, int total, cudaStream_t s,
+            void* usave, bool spectrum_only);
+int tc2_bwd(fb_plan* p, const void* dy, void* du, int64_t B, int ctas, int total, int maxseg,
+            float* tpart, const void* usave, cudaStream_t s);
 // usave (optional): the forward writes U = F(u) there (tc_saved_size bytes)
 // and the backward reads it instead of recomputing (u may then be null)
 size_t tc_saved_size(const fb_plan* p, int64_t B);

@@ -82,7 +82,7 @@ __global__ void __launch_bounds__(FftShape<LOG2N>::T, 2)
                        float* __restrict__ kbar, float2* __restrict__ kf, __half2* __restrict__ kf_tc,
                        float* __restrict__ kf_scale, const float* __restrict__ D,
                        const float2* __restrict__ tab_g, uint32_t N, int64_t p, double lambda,
-                       double keep_scale, int freq) {
+                       double keep_scale, int freq, int tc_ver) {
   using S = FftShape<LOG2N>;
   extern __shared__ __align__(128) unsigned char smem_raw[];
   __shared__ float red[32];
@@ -142,7 +142,7 @@ __global__ void __launch_bounds__(FftShape<LOG2N>::T, 2)
     for (int r = 0; r < 16; ++r) out[j + r * S::stride] = cscale(v[r], inv_n);
     return;
   }
-  // f = j + r * stride -> slot (f % 64) * 128 + f / 64, padded by one per 128
+  // f = j + r * stride -> its tensor-core slot (v2 / v1 layouts below), padded by one per 128
   const float dn = __ldg(D + h) * inv_n;
   float mx = 0.f;
 #pragma unroll
@@ -168,7 +168,10 @@ __global__ void __launch_bounds__(FftShape<LOG2N>::T, 2)
   if (j == 0) kf_scale[h] = red[0] > 0.f ? ldexpf(1.f, e - 15) : 1.f;
 #pragma unroll
   for (int r = 0; r < 16; ++r) {
-    const uint32_t f = j + r * S::stride, i = (f & 63u) * 128u + (f >> 6);
+    const uint32_t f = j + r * S::stride;
+    // v2: [f2 / 4][f1][f2 % 4], f1 = f % 128, f2 = f / 128 (coalesced per-lane loads)
+    const uint32_t i = tc_ver == 2 ? (((f >> 9) * 128u + (f & 127u)) * 4u + ((f >> 7) & 3u))
+                                   : (f & 63u) * 128u + (f >> 6);
     work[i + (i >> 7)] = cscale(v[r], sc);
   }
   __syncthreads();
@@ -577,7 +580,7 @@ struct Sp {
     k<<<(unsigned)p->H, FftShape<LOG2N>::T, sm, s>>>(
         K, p->use_keep ? p->keep : nullptr, p->kbar, p->kf,
         p->use_tc ? (__half2*)p->kf_tc : nullptr, p->kf_scale, p->d, p->tw2, (uint32_t)p->N, p->p, p->lambda, p->keep_scale,
-        p->smooth_domain == FB_SMOOTH_FREQUENCY);
+        p->smooth_domain == FB_SMOOTH_FREQUENCY, p->tc_ver);
   }
   static void finalize(cudaStream_t s, const fb_plan* p, const float2* spart, const float* ddpart,
                        int chunks, float* dkbar, float* dD, float* dK, int dd_lag0,

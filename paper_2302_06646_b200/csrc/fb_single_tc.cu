@@ -1718,6 +1718,12 @@ bool tc_eligible(const fb_plan* p) {
 }
 
 int tc_init(fb_plan* p) {
+  if (p->tc_ver == 2) {
+    int rc = tc2_init(p);
+    if (!rc) rc = cuda_status(cudaMalloc(&p->kf_tc, sizeof(__half2) * p->H * kN), "cudaMalloc(kf_tc)");
+    if (!rc) rc = cuda_status(cudaMalloc(&p->kf_scale, sizeof(float) * p->H), "cudaMalloc(kf_scale)");
+    return rc;
+  }
   std::vector<uint8_t> img = p->dtype == FB_BF16 ? build_mats<__nv_bfloat16>() : build_mats<__half>();
   int rc = cuda_status(cudaMalloc(&p->tc_mats, img.size()), "cudaMalloc(tc mats)");
   if (!rc)
@@ -1734,6 +1740,7 @@ size_t tc_saved_size(const fb_plan* p, int64_t B) {
 
 int tc_fwd(fb_plan* p, const void* u, void* y, int64_t B, cudaStream_t s, void* usave) {
   const TcGrid gr = tc_grid(p, B);
+  if (p->tc_ver == 2) return tc2_fwd(p, u, y, B, gr.ctas, gr.total, s, usave, false);
   CUtensorMap map;
   auto go = [&](auto tv) {
     using T = decltype(tv);
@@ -1767,6 +1774,19 @@ int tc_bwd(fb_plan* p, const void* dy, const void* u, void* du, float* dK, float
   const TcGrid gr = tc_grid(p, B);
   float* tpart = (float*)ws;
   uint32_t* uscratch = (uint32_t*)((char*)ws + tpart_bytes(gr));
+  if (p->tc_ver == 2) {
+    int rc = FB_OK;
+    if (!usave) {  // no saved transform: U = F(u) into the workspace first
+      rc = tc2_fwd(p, u, nullptr, B, gr.ctas, gr.total, s, uscratch, true);
+      usave = uscratch;
+    }
+    if (!rc) rc = tc2_bwd(p, dy, du, B, gr.bctas, gr.total, gr.maxseg, tpart, usave, s);
+    if (rc) return rc;
+    tc_dk_tail_kernel<<<(unsigned)p->H, 512, 0, s>>>(
+        tpart, dKbar, dD, p->kbar, p->use_keep ? p->keep : nullptr, dK, p->p, p->keep_scale,
+        p->smooth_domain == FB_SMOOTH_FREQUENCY, gr.bctas, gr.total, gr.npairs, gr.maxseg);
+    return cuda_status(cudaGetLastError(), "tc_dk_tail");
+  }
   CUtensorMap dmap, umap;
   auto go = [&](auto tv) {
     using T = decltype(tv);

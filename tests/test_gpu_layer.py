@@ -212,6 +212,31 @@ def test_tensor_core_persistent_shares(lc, B, H):
     assert_parity(got, oracle_layer(lc, inp, cfg), TOL[dtype], keys=("y", "du", "dK", "dD"))
 
 
+@pytest.mark.parametrize("dtype,B,H", [(torch.bfloat16, 3, 3), (torch.float16, 2, 2),
+                                       (torch.bfloat16, 32, 48), (torch.bfloat16, 9, 37)])
+@pytest.mark.parametrize("saved", [True, False])
+def test_tensor_core_v2_design(lc, monkeypatch, dtype, B, H, saved):
+    """The 128 x 64 TMEM-resident single-pass design (fb_tc2.cu, opt-in via
+    FB_TC2=1 at plan creation): odd batches, multi-segment CTA shares, the
+    training step (saved U) and the recompute path."""
+    monkeypatch.setenv("FB_TC2", "1")
+    N = 4096
+    inp = layer_inputs(lc, B, H, N, dtype)
+    cfg = fb.RegularizationConfig(**CFG)
+    plan = fb.LongConvPlan(N, H, fb.ConvMode.CAUSAL, dtype, fb.Engine.BUTTERFLY)
+    assert plan.tensor_cores
+    plan.prep(inp["tK"], inp["tD"], cfg)
+    if saved:
+        y, sv = plan.forward(inp["tu"], save=True)
+        du, dK, dD = plan.backward(inp["tdy"], inp["tu"], saved=sv)
+    else:
+        y = plan.forward(inp["tu"])
+        du, dK, dD = plan.backward(inp["tdy"], inp["tu"])
+    torch.cuda.synchronize()
+    got = dict(y=to_np(y), du=to_np(du), dK=to_np(dK), dD=to_np(dD))
+    assert_parity(got, oracle_layer(lc, inp, cfg), TOL[dtype], keys=("y", "du", "dK", "dD"))
+
+
 def test_tensor_core_deterministic(lc):
     B, H, N = 32, 20, 4096
     inp = layer_inputs(lc, B, H, N, torch.bfloat16)
