@@ -208,6 +208,34 @@ int fb_learned_fwd(fb_learned_plan* plan, const float* blocks, const void* x, vo
 int fb_learned_bwd(fb_learned_plan* plan, const float* blocks, const void* x, const void* g,
                    void* dx, float* dblocks, int64_t B, void* workspace, void* stream);
 
+/* Complex row transforms / convolutions through the butterfly plan: the
+ * device side of the reference's single-row entry points build_plan +
+ * apply_plan (butterfly.hpp:74-79), conv_butterfly (butterfly.hpp:82-83) and
+ * conv_three_pass's circular convolution with a precomputed spectrum
+ * (three_pass.hpp:119-120).  Rows of complex f32, interleaved (re, im).
+ * fb_dft_plan_create validates n and r like build_plan (FB_ERR_PLAN for
+ * n < 1, r < 2, or a remainder with no factor <= r) and runs the plan's own
+ * greedy stage chain with the exact DFT blocks (butterfly.cpp:13-20), so any
+ * buildable n works (n > 8192 as a four-step composition of two stage chains).
+ *   fb_dft:   y = F_n x (inverse = 0) or conj(F_n conj(x)) / n (inverse = 1)
+ *   fb_conv_rows: y = conv(u, k) per row; mode FB_MODE_CIRCULAR needs n == N,
+ *     FB_MODE_CAUSAL n == 2N (zero-padded, first N outputs); k has k_rows rows
+ *     (1: shared by every row, or rows)
+ *   fb_conv_rows_spectrum: the same with the kernel given as its forward
+ *     spectrum kspec [k_rows][n] (e.g. build_three_pass's K_hat = F_n k).
+ * Workspace: fb_dft_workspace_size(plan, rows, 0) bytes for fb_dft,
+ * fb_dft_workspace_size(plan, rows, k_rows) for the convolutions. */
+typedef struct fb_dft_plan fb_dft_plan;
+int fb_dft_plan_create(fb_dft_plan** plan, int64_t n, int64_t r, int device);
+int fb_dft_plan_destroy(fb_dft_plan* plan);
+int fb_dft_plan_factors(const fb_dft_plan* plan, int64_t* factors, int64_t* count);
+size_t fb_dft_workspace_size(const fb_dft_plan* plan, int64_t rows, int64_t k_rows);
+int fb_dft(fb_dft_plan* plan, const float* x, float* y, int64_t rows, int inverse, void* workspace,
+           void* stream);
+int fb_conv_rows(fb_dft_plan* plan, const float* u, const float* k, float* y, int64_t N, int64_t rows,
+                 int64_t k_rows, int mode, void* workspace, void* stream);
+int fb_conv_rows_spectrum(fb_dft_plan* plan, const float* u, const float* kspec, float* y, int64_t N,
+                          int64_t rows, int64_t k_rows, int mode, void* workspace, void* stream);
 const char* fb_last_error(void);
 int fb_version(void);
 

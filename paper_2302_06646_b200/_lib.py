@@ -28,7 +28,9 @@ EXPORTED = [
     "fb_last_error", "fb_version", "fb_host_runner_create", "fb_host_runner_destroy",
     "fb_host_runner_chunk_heads", "fb_host_runner_run", "fb_saved_size", "fb_fwd_save",
     "fb_bwd_saved", "fb_shard_plan_create", "fb_shard_plan_destroy", "fb_shard_plan_dims",
-    "fb_shard_columns", "fb_shard_rows", "fb_plan_profile_events",
+    "fb_shard_columns", "fb_shard_rows", "fb_plan_profile_events", "fb_dft_plan_create",
+    "fb_dft_plan_destroy", "fb_dft_plan_factors", "fb_dft_workspace_size", "fb_dft", "fb_conv_rows",
+    "fb_conv_rows_spectrum",
 ]
 
 
@@ -102,6 +104,14 @@ def lib() -> C.CDLL:
         L.fb_host_runner_run.argtypes = [vp, C.POINTER(RegConfig), C.c_int, vp, vp, vp, vp, vp,
                                          vp, vp, vp, vp]
         L.fb_plan_profile_events.argtypes = [vp, C.c_int, vp, vp]
+        L.fb_dft_plan_create.argtypes = [C.POINTER(vp), i64, i64, C.c_int]
+        L.fb_dft_plan_destroy.argtypes = [vp]
+        L.fb_dft_plan_factors.argtypes = [vp, C.POINTER(i64), C.POINTER(i64)]
+        L.fb_dft_workspace_size.argtypes = [vp, i64, i64]
+        L.fb_dft_workspace_size.restype = sz
+        L.fb_dft.argtypes = [vp, vp, vp, i64, C.c_int, vp, vp]
+        L.fb_conv_rows.argtypes = [vp, vp, vp, vp, i64, i64, i64, C.c_int, vp, vp]
+        L.fb_conv_rows_spectrum.argtypes = [vp, vp, vp, vp, i64, i64, i64, C.c_int, vp, vp]
         L.fb_last_error.restype = C.c_char_p
         _lib = L
     return _lib
