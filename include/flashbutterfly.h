@@ -101,6 +101,16 @@ int fb_plan_get_info(const fb_plan* plan, fb_plan_info* info);
 int fb_kernel_prep(fb_plan* plan, const float* K, const float* D, const fb_reg_config* cfg,
                    int training, void* stream);
 
+/* InitKind (regularize.hpp:27). */
+enum fb_init_kind { FB_INIT_RANDOM = 0, FB_INIT_GEOMETRIC = 1 };
+/* init_kernels (regularize.hpp:55, regularize.cpp:73-91) on the device:
+ * K[h][i] = draw i of SeededRng(seed).child(h).normal() (times the geometric
+ * envelope exp(-(i/N) (H/2)^(h/H)) for FB_INIT_GEOMETRIC), D[h] = draw h of
+ * child(H) — the reference's streams exactly (xoshiro256++ with GF(2)
+ * jump-ahead so each head's stream splits over many threads).  fp64 values;
+ * K, D receive them rounded to f32, K64, D64 (optional, may be NULL) as f64. */
+int fb_init_kernels(int kind, int64_t H, int64_t N, uint64_t seed, float* K, float* D, double* K64,
+                    double* D64, int device, void* stream);
 /* Copy the plan's regularized kernels Kbar [H][N] f32 into dst (device),
  * stream-ordered after fb_kernel_prep. */
 int fb_plan_copy_kbar(const fb_plan* plan, float* dst, void* stream);

@@ -94,6 +94,18 @@ struct RegularizationConfig {
   std::uint64_t seed = 0;
 };
 
+// regularize.hpp:27-34, 55-59 (init_kernels draws on the device, the
+// reference's streams exactly)
+enum class InitKind { kRandom, kGeometric };
+struct InitConfig {
+  InitKind kind = InitKind::kRandom;
+  std::size_t heads = 1;
+  std::size_t len = 1;
+  std::uint64_t seed = 0;
+};
+KernelBank init_kernels(const InitConfig& cfg);
+double geometric_envelope(std::size_t position, std::size_t len, std::size_t head, std::size_t heads);
+
 enum class Precision { kFp32, kBf16, kFp16 };
 void set_device_precision(Precision p);
 Precision device_precision();

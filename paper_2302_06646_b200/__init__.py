@@ -10,9 +10,11 @@ from .longconv import (  # noqa: F401
     ConvMode,
     Engine,
     HostRunner,
+    InitKind,
     LongConvPlan,
     RegularizationConfig,
     SmoothDomain,
+    init_kernels,
     long_conv,
     regularized_long_conv,
     regularized_long_conv_backward,
@@ -21,7 +23,7 @@ from ._lib import DimensionError, FBError, PlanError  # noqa: F401
 from .learned import LearnedButterflyPlan, learned_butterfly  # noqa: F401
 
 __all__ = [
-    "ConvMode", "Engine", "HostRunner", "LongConvPlan", "RegularizationConfig", "SmoothDomain", "long_conv",
+    "ConvMode", "Engine", "HostRunner", "InitKind", "LongConvPlan", "init_kernels", "RegularizationConfig", "SmoothDomain", "long_conv",
     "regularized_long_conv", "regularized_long_conv_backward", "DimensionError", "FBError",
     "PlanError", "LearnedButterflyPlan", "learned_butterfly",
 ]

@@ -272,6 +272,25 @@ LearnedBatchGradients learned_gradients_batched(std::size_t n, std::size_t r, st
   return g;
 }
 
+KernelBank init_kernels(const InitConfig& cfg) {
+  if (cfg.heads == 0 || cfg.len == 0) throw DimensionError("init_kernels: heads and len must be >= 1");
+  KernelBank bank(cfg.heads, cfg.len);
+  DevBuf K(bank.kernels.size() * 8), D(bank.heads * 8);
+  check(fb_init_kernels(cfg.kind == InitKind::kGeometric ? FB_INIT_GEOMETRIC : FB_INIT_RANDOM,
+                        (int64_t)cfg.heads, (int64_t)cfg.len, cfg.seed, nullptr, nullptr, (double*)K.p,
+                        (double*)D.p, g_device, nullptr),
+        "init_kernels");
+  cuda(cudaDeviceSynchronize(), "sync");
+  cuda(cudaMemcpy(bank.kernels.data(), K.p, bank.kernels.size() * 8, cudaMemcpyDeviceToHost), "download");
+  cuda(cudaMemcpy(bank.skip_gain.data(), D.p, bank.heads * 8, cudaMemcpyDeviceToHost), "download");
+  return bank;
+}
+
+double geometric_envelope(std::size_t position, std::size_t len, std::size_t head, std::size_t heads) {
+  const double decay = std::pow((double)heads / 2.0, (double)head / (double)heads);
+  return std::exp(-((double)position / (double)len) * decay);
+}
+
 // ------------------------------------------------------------------ single rows
 // The reference's single-row entry points (butterfly.hpp:74-108,
 // three_pass.hpp:113-131) on the device: fp64 host spans in, f32 complex rows

@@ -296,6 +296,16 @@ int fb_plan_copy_kbar(const fb_plan* p, float* dst, void* stream) {
                      "fb_plan_copy_kbar");
 }
 
+int fb_init_kernels(int kind, int64_t H, int64_t N, uint64_t seed, float* K, float* D, double* K64,
+                    double* D64, int device, void* stream) {
+  if (H < 1 || N < 1) return fail(FB_ERR_DIM, "init_kernels: heads and len must be >= 1");
+  if (kind != FB_INIT_RANDOM && kind != FB_INIT_GEOMETRIC) return fail(FB_ERR_ARG, "init_kernels: bad kind");
+  DevGuard dg(device);
+  int rc = cuda_status(dg.err, "cudaSetDevice");
+  if (rc) return rc;
+  return init_kernels_dev(kind, H, N, seed, K, D, K64, D64, device, (cudaStream_t)stream);
+}
+
 int fb_kernel_prep(fb_plan* p, const float* K, const float* D, const fb_reg_config* cfg,
                    int training, void* stream) {
   if (!p || !K || !D || !cfg) return fail(FB_ERR_ARG, "fb_kernel_prep: null argument");

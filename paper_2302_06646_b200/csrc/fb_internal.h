@@ -141,6 +141,9 @@ int tp_bwd(fb_plan* p, const void* dy, const void* u, void* du, float* dK, float
 // shared K1 pieces (fb_prep.cu)
 int regularize_bank_dev(fb_plan* p, const float* K, cudaStream_t s);
 int dropout_keep_dev(fb_plan* p, double rate, uint64_t seed, cudaStream_t s);
+// init_kernels (regularize.cpp:73-91) on the device; any output may be null
+int init_kernels_dev(int kind, int64_t H, int64_t N, uint64_t seed, float* K, float* D, double* K64,
+                     double* D64, int device, cudaStream_t s);
 // dK = chain(dKbar) through dropout/smooth/squash, per head; dkbar_in [H][N]
 int regularizer_backward_dev(fb_plan* p, const float* dkbar, float* dK, cudaStream_t s);
 // record (and clear) the caller's profiling event `e` (0 begin, 1 end) of main kernel k

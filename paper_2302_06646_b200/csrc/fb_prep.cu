@@ -14,6 +14,9 @@
 //   w[t] = (2p+1)^-1 sum_{d=-p..p} exp(-2 pi i d t / N)
 //        = (2p+1)^-1 (1 + 2 sum_{d=1..p} cos(2 pi d t / N)),
 // which is real, so smooth_frequency(k) = k * w (and is self-adjoint).
+#include <mutex>
+#include <vector>
+
 #include "fb_common.cuh"
 #include "fb_internal.h"
 #include "fb_reg.cuh"
@@ -56,16 +59,83 @@ struct DevRng {
   __device__ double uniform01() { return (double)(next() >> 11) * 0x1.0p-53; }
 };
 
-// keep[h][i] = !(uniform01() < rate), drawn in order from child stream h.
-// The stream is sequential by construction, so one thread walks one head.
+// Jump-ahead: the xoshiro256 state update is linear over GF(2)^256, so s_k =
+// M^k s_0.  jump_mats() holds P_j = M^(2^j), j < 32, as 256 rows x 4 words
+// (row i: the state bits that feed output bit i); a thread reaches draw k of a
+// stream with popcount(k) matrix-vector products, then walks its chunk
+// sequentially — every head's stream splits over many threads with results
+// bit-identical to the sequential reference walk.
+constexpr int kJumpBits = 32;
+__device__ __forceinline__ void rng_jump(uint64_t s[4], uint64_t steps, const uint64_t* __restrict__ P) {
+  for (int j = 0; steps; ++j, steps >>= 1) {
+    if (!(steps & 1)) continue;
+    const uint64_t* rows = P + (size_t)j * 256 * 4;
+    uint64_t o[4] = {0, 0, 0, 0};
+    for (int i = 0; i < 256; ++i) {
+      const uint64_t* r = rows + 4 * i;
+      const uint64_t v = (__ldg(r) & s[0]) ^ (__ldg(r + 1) & s[1]) ^ (__ldg(r + 2) & s[2]) ^ (__ldg(r + 3) & s[3]);
+      o[i >> 6] |= (uint64_t)(__popcll(v) & 1) << (i & 63);
+    }
+    for (int w = 0; w < 4; ++w) s[w] = o[w];
+  }
+}
+constexpr int64_t kRngChunk = 512;  // draws per thread
+
+// keep[h][i] = !(uniform01() < rate), draw i of child stream h; thread (h, c)
+// jumps to draw c kRngChunk and walks its chunk.
 __global__ void dropout_keep_kernel(uint8_t* __restrict__ keep, int H, int64_t N, double rate,
-                                    uint64_t seed, int64_t head0) {
-  const int h = blockIdx.x * blockDim.x + threadIdx.x;
-  if (h >= H) return;
+                                    uint64_t seed, int64_t head0, const uint64_t* __restrict__ P) {
+  const int64_t chunks = (N + kRngChunk - 1) / kRngChunk;
+  const int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (g >= H * chunks) return;
+  const int h = (int)(g / chunks);
+  const int64_t i0 = (g % chunks) * kRngChunk, i1 = min(N, i0 + kRngChunk);
   DevRng r;
   r.child_of(seed, (uint64_t)(head0 + h));
+  rng_jump(r.s, (uint64_t)i0, P);
   uint8_t* k = keep + (size_t)h * N;
-  for (int64_t i = 0; i < N; ++i) k[i] = (r.uniform01() < rate) ? 0 : 1;
+  for (int64_t i = i0; i < i1; ++i) k[i] = (r.uniform01() < rate) ? 0 : 1;
+}
+
+// init_kernels (regularize.cpp:66-91): K[h][i] = normal draw i of child
+// stream h (Box-Muller pairs, rng.cpp:57-69: cos then the cached sin), times
+// the geometric envelope exp(-(i / N) (H / 2)^(h / H)) for kind 1; D[h] = draw
+// h of child stream H.  fp64 like the reference, stored f32 and/or f64.
+__global__ void init_kernels_kernel(int kind, int H, int64_t N, uint64_t seed, float* __restrict__ K,
+                                    double* __restrict__ K64, const uint64_t* __restrict__ P) {
+  const int64_t chunks = (N + kRngChunk - 1) / kRngChunk;
+  const int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (g >= H * chunks) return;
+  const int h = (int)(g / chunks);
+  const int64_t i0 = (g % chunks) * kRngChunk, i1 = min(N, i0 + kRngChunk);
+  DevRng r;
+  r.child_of(seed, (uint64_t)h);
+  rng_jump(r.s, (uint64_t)i0, P);  // kRngChunk is even: chunks start on a pair
+  const double decay = pow((double)H / 2.0, (double)h / (double)H);
+  for (int64_t i = i0; i < i1; i += 2) {
+    const double u1 = 1.0 - r.uniform01(), u2 = r.uniform01();
+    const double rad = sqrt(-2.0 * log(u1)), ang = 2.0 * M_PI * u2;
+    double v[2] = {rad * cos(ang), rad * sin(ang)};
+    for (int e = 0; e < 2 && i + e < i1; ++e) {
+      double x = v[e];
+      if (kind) x *= exp(-((double)(i + e) / (double)N) * decay);
+      if (K) K[(size_t)h * N + i + e] = (float)x;
+      if (K64) K64[(size_t)h * N + i + e] = x;
+    }
+  }
+}
+__global__ void init_skip_kernel(int H, uint64_t seed, float* __restrict__ D, double* __restrict__ D64) {
+  DevRng r;
+  r.child_of(seed, (uint64_t)H);
+  for (int h = 0; h < H; h += 2) {
+    const double u1 = 1.0 - r.uniform01(), u2 = r.uniform01();
+    const double rad = sqrt(-2.0 * log(u1)), ang = 2.0 * M_PI * u2;
+    const double v[2] = {rad * cos(ang), rad * sin(ang)};
+    for (int e = 0; e < 2 && h + e < H; ++e) {
+      if (D) D[h + e] = (float)v[e];
+      if (D64) D64[h + e] = v[e];
+    }
+  }
 }
 
 // kbar[h][t] = squash(smooth(dropout(K))[t], lambda)
@@ -150,10 +220,73 @@ __global__ void __launch_bounds__(kRegThreads)
   }
 }
 
+namespace {
+// P_j = M^(2^j) of the xoshiro256 state update, built once per device
+void xo_step(uint64_t s[4]) {
+  const uint64_t t = s[1] << 17;
+  s[2] ^= s[0];
+  s[3] ^= s[1];
+  s[1] ^= s[2];
+  s[0] ^= s[3];
+  s[2] ^= t;
+  s[3] = (s[3] << 45) | (s[3] >> 19);
+}
+const uint64_t* jump_mats(int device, int& rc) {
+  static const uint64_t* dev[64] = {nullptr};
+  static std::mutex mu;
+  std::lock_guard<std::mutex> lock(mu);
+  rc = FB_OK;
+  if (device < 0 || device >= 64) {
+    rc = FB_ERR_ARG;
+    return nullptr;
+  }
+  if (dev[device]) return dev[device];
+  std::vector<uint64_t> P((size_t)kJumpBits * 256 * 4, 0);
+  for (int j = 0; j < 256; ++j) {  // M: column j = one step of the unit state e_j
+    uint64_t e[4] = {0, 0, 0, 0};
+    e[j >> 6] = uint64_t(1) << (j & 63);
+    xo_step(e);
+    for (int i = 0; i < 256; ++i)
+      if ((e[i >> 6] >> (i & 63)) & 1) P[(size_t)4 * i + (j >> 6)] |= uint64_t(1) << (j & 63);
+  }
+  for (int k = 1; k < kJumpBits; ++k) {  // P_k = P_{k-1}^2 (rows: XOR of the rows they select)
+    const uint64_t* A = &P[(size_t)(k - 1) * 1024];
+    uint64_t* R = &P[(size_t)k * 1024];
+    for (int i = 0; i < 256; ++i)
+      for (int j = 0; j < 256; ++j)
+        if ((A[4 * i + (j >> 6)] >> (j & 63)) & 1)
+          for (int w = 0; w < 4; ++w) R[4 * i + w] ^= A[4 * j + w];
+  }
+  uint64_t* d = nullptr;
+  rc = cuda_status(cudaMalloc(&d, P.size() * 8), "cudaMalloc(rng jump)");
+  if (!rc) rc = cuda_status(cudaMemcpy(d, P.data(), P.size() * 8, cudaMemcpyHostToDevice), "copy rng jump");
+  if (rc) return nullptr;
+  dev[device] = d;
+  return d;
+}
+unsigned rng_blocks(int64_t H, int64_t N) {
+  return (unsigned)((H * ((N + kRngChunk - 1) / kRngChunk) + 127) / 128);
+}
+}  // namespace
+
 int dropout_keep_dev(fb_plan* p, double rate, uint64_t seed, cudaStream_t s) {
-  dropout_keep_kernel<<<(unsigned)((p->H + 127) / 128), 128, 0, s>>>(p->keep, (int)p->H, p->N,
-                                                                       rate, seed, p->head0);
+  int rc = FB_OK;
+  const uint64_t* P = jump_mats(p->device, rc);
+  if (rc) return rc;
+  dropout_keep_kernel<<<rng_blocks(p->H, p->N), 128, 0, s>>>(p->keep, (int)p->H, p->N, rate, seed,
+                                                             p->head0, P);
   return cuda_status(cudaGetLastError(), "dropout_keep");
+}
+
+int init_kernels_dev(int kind, int64_t H, int64_t N, uint64_t seed, float* K, float* D, double* K64,
+                     double* D64, int device, cudaStream_t s) {
+  int rc = FB_OK;
+  const uint64_t* P = jump_mats(device, rc);
+  if (rc) return rc;
+  if (K || K64)
+    init_kernels_kernel<<<rng_blocks(H, N), 128, 0, s>>>(kind, (int)H, N, seed, K, K64, P);
+  if (D || D64) init_skip_kernel<<<1, 1, 0, s>>>((int)H, seed, D, D64);
+  return cuda_status(cudaGetLastError(), "init_kernels");
 }
 
 int regularize_bank_dev(fb_plan* p, const float* K, cudaStream_t s) {

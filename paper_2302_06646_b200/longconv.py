@@ -240,6 +240,30 @@ class HostRunner:
         return y, du, dK, dD
 
 
+class InitKind(enum.IntEnum):  # regularize.hpp:27
+    RANDOM = 0
+    GEOMETRIC = 1
+
+
+def init_kernels(kind: InitKind, H: int, N: int, seed: int, device=None,
+                 dtype: torch.dtype = torch.float32) -> tuple[torch.Tensor, torch.Tensor]:
+    """init_kernels (regularize.hpp:55, regularize.cpp:73-91) on the device:
+    the reference's RNG streams exactly (K[h] from child stream h, D from child
+    stream H).  Returns (K [H, N], D [H]) in fp32 or fp64."""
+    if H < 1 or N < 1:
+        raise DimensionError(_lib.FB_ERR_DIM, "init_kernels: heads and len must be >= 1")
+    dev = torch.device("cuda", torch.cuda.current_device()) if device is None else torch.device(device)
+    K = torch.empty(H, N, dtype=dtype, device=dev)
+    D = torch.empty(H, dtype=dtype, device=dev)
+    f64 = dtype == torch.float64
+    with torch.cuda.device(dev):
+        check(_lib.lib().fb_init_kernels(int(kind), int(H), int(N), int(seed) & (2**64 - 1),
+                                         _ptr(None if f64 else K), _ptr(None if f64 else D),
+                                         _ptr(K if f64 else None), _ptr(D if f64 else None),
+                                         dev.index or 0, _stream(dev)))
+    return K, D
+
+
 _PLANS: dict = {}
 
 

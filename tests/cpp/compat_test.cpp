@@ -124,6 +124,20 @@ int main() {
       lco_apply_plan(n, r, x.data() + row * 2 * n, 0, want.data() + row * 2 * n);
     expect(rel_l2(y, want) < 1e-5, "learned_forward (DFT init) == apply_plan", rel_l2(y, want));
   }
+  {  // init_kernels on the device vs the oracle (reference streams)
+    InitConfig ic;
+    ic.kind = InitKind::kGeometric;
+    ic.heads = 4;
+    ic.len = 3000;
+    ic.seed = 3;
+    KernelBank kb = init_kernels(ic);
+    std::vector<double> K(ic.heads * ic.len), D(ic.heads);
+    lco_init_kernels(1, ic.heads, ic.len, 3, K.data(), D.data());
+    const double e = rel_l2(kb.kernels, K), ed = rel_l2(kb.skip_gain, D);
+    expect(e < 1e-13 && ed < 1e-13, "init_kernels (geometric) vs oracle", std::max(e, ed));
+    expect(std::abs(geometric_envelope(5, 100, 2, 8) - std::exp(-0.05 * std::pow(4.0, 0.25))) < 1e-15,
+           "geometric_envelope");
+  }
   // ---- single-row entry points (butterfly.hpp:74-108, three_pass.hpp:113-131)
   auto cplx = [](uint64_t seed, size_t n) {
     std::vector<double> d(2 * n);

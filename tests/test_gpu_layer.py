@@ -85,6 +85,38 @@ def test_dropout_training_mode(lc):
     assert_parity(got, want, 1e-5)
 
 
+@pytest.mark.parametrize("kind,H,N,seed", [(1, 3, 4096, 3), (0, 5, 20001, 11), (1, 2, 1, 0),
+                                           (1, 7, 131072, 42)])
+def test_init_kernels_on_device(lc, kind, H, N, seed):
+    """init_kernels (regularize.cpp:73-91) on the device: the reference's
+    xoshiro256++ streams, split over threads by GF(2) jump-ahead (chunks of
+    512 draws; odd N ends on a cached-sine-free pair), fp64 Box-Muller."""
+    K64, D64 = fb.init_kernels(fb.InitKind(kind), H, N, seed, dtype=torch.float64)
+    K32, D32 = fb.init_kernels(fb.InitKind(kind), H, N, seed)
+    Kw, Dw = lc.init_kernels(kind, H, N, seed)
+    K64, D64 = to_np(K64), to_np(D64)
+    # device fp64 libm vs glibc: a last-ulp difference at most
+    assert np.max(np.abs(K64 - Kw) / np.maximum(np.abs(Kw), 1e-300)) < 1e-13
+    assert np.max(np.abs(D64 - Dw) / np.maximum(np.abs(Dw), 1e-300)) < 1e-13
+    assert np.mean(to_np(K32) == Kw.astype(np.float32)) > 0.9999
+    assert np.array_equal(to_np(D32), Dw.astype(np.float32))
+
+
+def test_dropout_mask_long_streams(lc):
+    """Dropout keep flags over many jump-ahead chunks per head (N = 20000, not
+    a multiple of the 512-draw chunk) equal the reference's sequential walk."""
+    H, N = 3, 20000
+    K = torch.randn(H, N, device="cuda")
+    D = torch.zeros(H, device="cuda")
+    cfg = fb.RegularizationConfig(dropout_rate=0.3, seed=123)
+    plan = fb.LongConvPlan(N, H, fb.ConvMode.CAUSAL, torch.float32, fb.Engine.AUTO)
+    plan.prep(K, D, cfg, True)
+    kbar = to_np(plan.kbar())
+    want = lc.regularize_bank(to_np(K), 0.0, 0, 0.3, 0, 123, True)
+    assert np.array_equal(kbar == 0, want == 0)
+    assert rel_l2(kbar, want) < 1e-6
+
+
 @pytest.mark.parametrize("dtype,tol", [(torch.float32, 1e-5), (torch.bfloat16, 2e-2)])
 def test_dropout_training_three_pass(lc, dtype, tol):
     """Three-pass training step with kernel dropout: the prep (mask, Kbar,
