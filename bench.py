@@ -636,9 +636,11 @@ def run_seqshard(args, cfg, rank, world, local_rank):
     D = torch.randn(H, device=dev, generator=g)
     passes = ss.GpuPasses(n, device=dev)
 
+    wire, chunks = args.wire, args.chunks
+
     def step():
-        y = ss.sharded_long_conv(u, kbar, D, sh, passes)
-        du, dk, dD = ss.sharded_long_conv_backward(dy, u, kbar, D, sh, passes)
+        y = ss.sharded_long_conv(u, kbar, D, sh, passes, wire=wire, chunks=chunks)
+        du, dk, dD = ss.sharded_long_conv_backward(dy, u, kbar, D, sh, passes, wire=wire)
         return y, du, dk, dD
 
     for _ in range(args.warmup):
@@ -671,6 +673,7 @@ def run_seqshard(args, cfg, rank, world, local_rank):
             "config": {"workload": cfg["workload"], "B": B, "H": H, "N": N, "transform_len": n,
                        "l": l, "m": m, "sharding": f"sequence over {world} rank(s), tau-slices of "
                        f"{sh.lp} columns; 4 all-to-alls fwd, 6 bwd",
+                       "all_to_all_wire": wire, "fwd_channel_chunks": chunks,
                        "bh_reduced": bool(args.bh), "report_only": True},
             "roofline": None, "cpu_baseline": None, "clocks": clk.summary(),
             "gpu_launches": None, "e2e": None}))
@@ -688,6 +691,10 @@ def main():
     ap.add_argument("--cpu-sample-heads", type=int, default=32)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--n", type=int, default=None, help="sequence length (config 5 sweep)")
+    ap.add_argument("--wire", default="f32", choices=["f32", "bf16"],
+                    help="config 6: all-to-all payload type")
+    ap.add_argument("--chunks", type=int, default=1,
+                    help="config 6: channel-pair chunks of the pipelined forward exchange")
     ap.add_argument("--bh", type=int, default=None, help="B*H override (config 6, few GPUs)")
     ap.add_argument("--dtype", default=None, choices=["f32", "bf16", "f16"],
                     help="I/O dtype override (e.g. the fp32 validation line of config 2)")

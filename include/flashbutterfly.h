@@ -197,6 +197,29 @@ int fb_shard_columns(fb_shard_plan* plan, const void* in, void* out, int64_t C, 
 int fb_shard_rows(fb_shard_plan* plan, void* rows, const void* kf2, void* kf2_out, int64_t C,
                   int64_t mp, int mode, float scale, void* stream);
 
+/* The sharded layer's row passes over channel pairs and its glue (seqshard.py):
+ *   fb_shard_rows_pairs: rows [P][H][mp][l] in place, rows = IFFT_l(FFT_l(rows)
+ *     kf2[h][a]) with the kernel rows kf2 [H][mp][l] shared by the P pairs
+ *   fb_shard_rows_bwd: per (h, a) over the P pairs: dy row <- IFFT_l(DY conj(kf2)),
+ *     wdk[h][a] = IFFT_l(sum_p conj(U) DY) (fixed order; unnormalised transforms)
+ *   fb_shard_stage: out[b][a][x] = in[a][b][x] on complex elements (f32 or bf16
+ *     pairs each side): the all-to-all send / receive layouts */
+int fb_shard_rows_pairs(fb_shard_plan* plan, void* rows, const void* kf2, int64_t P, int64_t H, int64_t mp,
+                        void* stream);
+/* Column passes fused with the layer's pair (un)packing: pass 1 of the
+ * channel pairs read straight from the real signals sig [B][H][half][lp]
+ * (dtype; rows >= half are the causal zero pad) into complex [P][H][m][lp];
+ * pass 3 of complex [P][H][m][lp] written straight back as real signals
+ * [B][H][half][lp] (dtype) plus D[h] skip (skip optional). */
+int fb_shard_columns_from_signals(fb_shard_plan* plan, const void* sig, int dtype, void* out, int64_t B,
+                                  int64_t H, int64_t half, int64_t tau0, int64_t lp, void* stream);
+int fb_shard_columns_to_signals(fb_shard_plan* plan, const void* in, void* sig_out, int dtype,
+                                const void* skip, const float* D, int64_t B, int64_t H, int64_t half,
+                                int64_t tau0, int64_t lp, void* stream);
+int fb_shard_rows_bwd(fb_shard_plan* plan, void* dy_rows, const void* u_rows, const void* kf2, void* wdk,
+                      int64_t P, int64_t H, int64_t mp, void* stream);
+int fb_shard_stage(const void* in, void* out, int64_t A, int64_t Bd, int64_t X, int in_dtype, int out_dtype,
+                   void* stream);
 /* Learned butterfly (K5).  Replaces learned_forward / learned_gradients
  * (butterfly.hpp:88-108, butterfly.cpp:221-307) batched over rows: rows
  * [B][H] of complex length n, with per-head block parameters (one factor x

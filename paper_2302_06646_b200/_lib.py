@@ -30,7 +30,9 @@ EXPORTED = [
     "fb_bwd_saved", "fb_shard_plan_create", "fb_shard_plan_destroy", "fb_shard_plan_dims",
     "fb_shard_columns", "fb_shard_rows", "fb_plan_profile_events", "fb_dft_plan_create",
     "fb_dft_plan_destroy", "fb_dft_plan_factors", "fb_dft_workspace_size", "fb_dft", "fb_conv_rows",
-    "fb_conv_rows_spectrum", "fb_init_kernels",
+    "fb_conv_rows_spectrum", "fb_init_kernels", "fb_shard_rows_pairs", "fb_shard_rows_bwd",
+    "fb_shard_stage",
+    "fb_shard_columns_from_signals", "fb_shard_columns_to_signals",
 ]
 
 
@@ -112,6 +114,11 @@ def lib() -> C.CDLL:
         L.fb_dft.argtypes = [vp, vp, vp, i64, C.c_int, vp, vp]
         L.fb_conv_rows.argtypes = [vp, vp, vp, vp, i64, i64, i64, C.c_int, vp, vp]
         L.fb_conv_rows_spectrum.argtypes = [vp, vp, vp, vp, i64, i64, i64, C.c_int, vp, vp]
+        L.fb_shard_rows_pairs.argtypes = [vp, vp, vp, i64, i64, i64, vp]
+        L.fb_shard_rows_bwd.argtypes = [vp, vp, vp, vp, vp, i64, i64, i64, vp]
+        L.fb_shard_columns_from_signals.argtypes = [vp, vp, C.c_int, vp, i64, i64, i64, i64, i64, vp]
+        L.fb_shard_columns_to_signals.argtypes = [vp, vp, vp, C.c_int, vp, vp, i64, i64, i64, i64, i64, vp]
+        L.fb_shard_stage.argtypes = [vp, vp, i64, i64, i64, C.c_int, C.c_int, vp]
         L.fb_init_kernels.argtypes = [C.c_int, i64, i64, C.c_uint64, vp, vp, vp, vp, C.c_int, vp]
         L.fb_last_error.restype = C.c_char_p
         _lib = L

@@ -992,18 +992,45 @@ __global__ void __launch_bounds__(kBigThreads, 1)
 // with the global column index in the twiddle:
 //   SIGN -1:  out[a][tau] = w_n^(-a tau) sum_c w_m^(-a c) in[c][tau]
 //   SIGN +1:  out[c][tau] = scale sum_a w_m^(+a c) w_n^(+a tau) in[a][tau]
-template <int SIGN, int SMALL>
+// Signal-side variants (the layer's pair packing fused into the passes):
+// IO = the signal type; pass 1 (SIGN -1) reads channel (p, h) straight from
+// the real signals sig[B][H][half][lp] (channels 2p / 2p+1 as re / im, rows
+// >= half the causal zero pad) and pass 3 (SIGN +1) writes re / im of its
+// rows < half back as channels 2p / 2p+1 of out[B][H][half][lp], plus
+// D[h] skip (optional).  IO = void: complex f32 in / out ([C][m][lp]).
+struct ShardSig {
+  const void* sig = nullptr;   // pass 1 input signals
+  void* out = nullptr;         // pass 3 output signals
+  const void* skip = nullptr;  // pass 3: + D[h] skip[b][h][c][tau]
+  const float* D = nullptr;
+  int B = 0, H = 0, half = 0;
+};
+template <int SIGN, int SMALL, typename IO = void>
 __global__ void __launch_bounds__(kBigThreads, 1)
     tp_shard_cols_kernel(const float2* __restrict__ in, float2* __restrict__ out,
                          const float2* __restrict__ tw_m, const float2* __restrict__ tb, uint32_t m,
-                         uint32_t lp, uint32_t tau0, float scale) {
+                         uint32_t lp, uint32_t tau0, float scale, ShardSig sg) {
+  constexpr bool kSig = !std::is_same<IO, void>::value;
+  using T = typename std::conditional<kSig, IO, float>::type;
   extern __shared__ __align__(16) float2 tsm[];
   const uint32_t TAU = kBigTile / m;
   const uint32_t c0 = blockIdx.x * TAU;
   const size_t ch = (size_t)blockIdx.y * m * lp;
+  const int pr = kSig ? (int)blockIdx.y / sg.H : 0, hh = kSig ? (int)blockIdx.y % sg.H : 0;
   for (uint32_t i = threadIdx.x; i < kBigTile; i += kBigThreads) {
     const uint32_t e = pdiv(i, TAU), c = pmod(i, TAU);
-    float2 v = __ldg(in + ch + (size_t)e * lp + c0 + c);
+    float2 v;
+    if constexpr (kSig && SIGN < 0) {
+      v = make_float2(0.f, 0.f);
+      if ((int)e < sg.half) {
+        const T* sg0 = reinterpret_cast<const T*>(sg.sig);
+        const size_t o = ((size_t)(2 * pr) * sg.H + hh) * sg.half * lp + (size_t)e * lp + c0 + c;
+        v.x = tof(sg0[o]);
+        if (2 * pr + 1 < sg.B) v.y = tof(sg0[o + (size_t)sg.H * sg.half * lp]);
+      }
+    } else {
+      v = __ldg(in + ch + (size_t)e * lp + c0 + c);
+    }
     if (SIGN > 0) v = cmul(v, tw_big<+1>(tb, e * (tau0 + c0 + c)));
     tsm[pad16(e) * TAU + c] = v;
   }
@@ -1013,7 +1040,22 @@ __global__ void __launch_bounds__(kBigThreads, 1)
     const uint32_t a = pdiv(i, TAU), c = pmod(i, TAU);
     float2 v = tsm[pad16(a) * TAU + c];
     v = SIGN < 0 ? cmul(v, tw_big<-1>(tb, a * (tau0 + c0 + c))) : cscale(v, scale);
-    out[ch + (size_t)a * lp + c0 + c] = v;
+    if constexpr (kSig && SIGN > 0) {
+      if ((int)a >= sg.half) continue;
+      T* so = reinterpret_cast<T*>(sg.out);
+      const T* sk = reinterpret_cast<const T*>(sg.skip);
+      const float d = sk ? __ldg(sg.D + hh) : 0.f;
+      for (int q = 0; q < 2; ++q) {
+        const int b = 2 * pr + q;
+        if (b >= sg.B) break;
+        const size_t o = ((size_t)b * sg.H + hh) * sg.half * lp + (size_t)a * lp + c0 + c;
+        float r = q ? v.y : v.x;
+        if (sk) r += d * tof(sk[o]);
+        so[o] = cvt<T>(r);
+      }
+    } else {
+      out[ch + (size_t)a * lp + c0 + c] = v;
+    }
   }
 }
 
@@ -1581,15 +1623,86 @@ int fb_shard_columns(fb_shard_plan* sp, const void* in, void* out, int64_t C, in
       auto k = tp_shard_cols_kernel<+1, SM>;
       cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
       k<<<g, kBigThreads, sm, s>>>((const float2*)in, (float2*)out, sp->tw_m, sp->tw_big,
-                                   (uint32_t)sp->m, (uint32_t)lp, (uint32_t)tau0, scale);
+                                   (uint32_t)sp->m, (uint32_t)lp, (uint32_t)tau0, scale, ShardSig());
     } else {
       auto k = tp_shard_cols_kernel<-1, SM>;
       cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
       k<<<g, kBigThreads, sm, s>>>((const float2*)in, (float2*)out, sp->tw_m, sp->tw_big,
-                                   (uint32_t)sp->m, (uint32_t)lp, (uint32_t)tau0, scale);
+                                   (uint32_t)sp->m, (uint32_t)lp, (uint32_t)tau0, scale, ShardSig());
     }
   });
   return cuda_status(cudaGetLastError(), "fb_shard_columns");
+}
+
+// Pass 1 straight from the real signals (pairs packed on the fly) / pass 3
+// straight into them (unpacked, + D skip): the layer's glue fused into the
+// column passes (see ShardSig).
+static int shard_cols_sig(fb_shard_plan* sp, const void* x_in, void* x_out, int dtype, ShardSig sg,
+                          int64_t tau0, int64_t lp, int inverse, cudaStream_t s, const char* name) {
+  const uint32_t TAU = (uint32_t)(kBigTile / sp->m);
+  const int64_t C = ((int64_t)(sg.B + 1) / 2) * sg.H;
+  if (sg.B < 1 || sg.H < 1 || sg.half < 1 || sg.half > sp->m || lp < TAU || lp % TAU || tau0 < 0 ||
+      tau0 + lp > sp->l || C > 65535) {
+    set_error(std::string(name) + ": bad shard geometry");
+    return FB_ERR_DIM;
+  }
+  DevGuard dg_(sp->device);
+  int rc = cuda_status(dg_.err, "cudaSetDevice");
+  if (rc) return rc;
+  const size_t sm = padded_len(kBigTile) * sizeof(float2);
+  const dim3 g((unsigned)(lp / TAU), (unsigned)C);
+  const float scale = 1.0f / (float)sp->n;
+  with_io(dtype, [&](auto io) {
+    using IO = decltype(io);
+    with_small(sp->m, [&](auto sc) {
+      constexpr int SM = decltype(sc)::value;
+      if (inverse) {
+        auto k = tp_shard_cols_kernel<+1, SM, IO>;
+        cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+        k<<<g, kBigThreads, sm, s>>>((const float2*)x_in, nullptr, sp->tw_m, sp->tw_big, (uint32_t)sp->m,
+                                     (uint32_t)lp, (uint32_t)tau0, scale, sg);
+      } else {
+        auto k = tp_shard_cols_kernel<-1, SM, IO>;
+        cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+        k<<<g, kBigThreads, sm, s>>>(nullptr, (float2*)x_out, sp->tw_m, sp->tw_big, (uint32_t)sp->m,
+                                     (uint32_t)lp, (uint32_t)tau0, scale, sg);
+      }
+    });
+  });
+  return cuda_status(cudaGetLastError(), name);
+}
+
+int fb_shard_columns_from_signals(fb_shard_plan* sp, const void* sig, int dtype, void* out, int64_t B,
+                                  int64_t H, int64_t half, int64_t tau0, int64_t lp, void* stream) {
+  if (!sp || !sig || !out) {
+    set_error("fb_shard_columns_from_signals: null argument");
+    return FB_ERR_ARG;
+  }
+  ShardSig sg;
+  sg.sig = sig;
+  sg.B = (int)B;
+  sg.H = (int)H;
+  sg.half = (int)half;
+  return shard_cols_sig(sp, nullptr, out, dtype, sg, tau0, lp, 0, (cudaStream_t)stream,
+                        "fb_shard_columns_from_signals");
+}
+
+int fb_shard_columns_to_signals(fb_shard_plan* sp, const void* in, void* sig_out, int dtype,
+                                const void* skip, const float* D, int64_t B, int64_t H, int64_t half,
+                                int64_t tau0, int64_t lp, void* stream) {
+  if (!sp || !in || !sig_out || (skip && !D)) {
+    set_error("fb_shard_columns_to_signals: null argument");
+    return FB_ERR_ARG;
+  }
+  ShardSig sg;
+  sg.out = sig_out;
+  sg.skip = skip;
+  sg.D = D;
+  sg.B = (int)B;
+  sg.H = (int)H;
+  sg.half = (int)half;
+  return shard_cols_sig(sp, in, nullptr, dtype, sg, tau0, lp, 1, (cudaStream_t)stream,
+                        "fb_shard_columns_to_signals");
 }
 
 int fb_shard_rows(fb_shard_plan* sp, void* rows, const void* kf2, void* kf2_out, int64_t C,
@@ -1620,6 +1733,60 @@ int fb_shard_rows(fb_shard_plan* sp, void* rows, const void* kf2, void* kf2_out,
                                                        1, (int)C, (int)mp, 1, scale, nullptr);
   }
   return cuda_status(cudaGetLastError(), "fb_shard_rows");
+}
+
+// rows [P][H][mp][l] in place: rows = IFFT_l(FFT_l(rows) kf2[h][a]) (unnormalised),
+// the kernel rows [H][mp][l] shared by the P channel pairs of each head
+int fb_shard_rows_pairs(fb_shard_plan* sp, void* rows, const void* kf2, int64_t P, int64_t H, int64_t mp,
+                        void* stream) {
+  if (!sp || !rows || !kf2) {
+    set_error("fb_shard_rows_pairs: null argument");
+    return FB_ERR_ARG;
+  }
+  if (P < 1 || H < 1 || mp < 1 || P * H * mp > (int64_t)1 << 31) {
+    set_error("fb_shard_rows_pairs: bad shard geometry");
+    return FB_ERR_DIM;
+  }
+  DevGuard dg_(sp->device);
+  int rc = cuda_status(dg_.err, "cudaSetDevice");
+  if (rc) return rc;
+  const size_t sm = pass2_smem<float>();
+  auto k = tp_pass2_kernel<float, 0>;
+  cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+  int sms = 148;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, sp->device);
+  const int64_t chunks = std::max<int64_t>(1, std::min<int64_t>(P, (2 * sms + H * mp - 1) / (H * mp)));
+  const int ppc = (int)((P + chunks - 1) / chunks);
+  k<<<dim3((unsigned)(H * mp), (unsigned)chunks), kL / 16, sm, (cudaStream_t)stream>>>(
+      reinterpret_cast<CxT<float>*>(rows), (const float2*)kf2, nullptr, sp->tw_l, (int)P, (int)H, (int)mp,
+      ppc, 0.f, nullptr);
+  return cuda_status(cudaGetLastError(), "fb_shard_rows_pairs");
+}
+
+// The sharded backward's row pass, CTA per (h, a) over all P pairs (fixed
+// order, deterministic): DY = FFT_l(dy row), U = FFT_l(u row),
+// S += conj(U) DY, dy row <- IFFT_l(DY conj(kf2)); finally wdk[h][a] =
+// IFFT_l(S) (unnormalised, complex f32 [H][mp][l]).
+int fb_shard_rows_bwd(fb_shard_plan* sp, void* dy_rows, const void* u_rows, const void* kf2, void* wdk,
+                      int64_t P, int64_t H, int64_t mp, void* stream) {
+  if (!sp || !dy_rows || !u_rows || !kf2 || !wdk) {
+    set_error("fb_shard_rows_bwd: null argument");
+    return FB_ERR_ARG;
+  }
+  if (P < 1 || H < 1 || mp < 1 || P * H * mp > (int64_t)1 << 31) {
+    set_error("fb_shard_rows_bwd: bad shard geometry");
+    return FB_ERR_DIM;
+  }
+  DevGuard dg_(sp->device);
+  int rc = cuda_status(dg_.err, "cudaSetDevice");
+  if (rc) return rc;
+  const size_t sm = pass2_bwd_smem<float>();
+  auto k = tp_pass2_bwd_kernel<float, false>;
+  cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+  k<<<(unsigned)(H * mp), kL / 16, sm, (cudaStream_t)stream>>>(
+      reinterpret_cast<CxT<float>*>(dy_rows), reinterpret_cast<const CxT<float>*>(u_rows), (const float2*)kf2,
+      (float2*)wdk, sp->tw_l, (int)P, (int)H, (int)mp);
+  return cuda_status(cudaGetLastError(), "fb_shard_rows_bwd");
 }
 
 }  // extern "C"

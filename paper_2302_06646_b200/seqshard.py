@@ -70,56 +70,115 @@ def gather_tau(parts: list[torch.Tensor], shard: SeqShard) -> torch.Tensor:
     return v.reshape(*v.shape[:-2], shard.m * shard.l)
 
 
-def _a2a(x: torch.Tensor, group=None, world: int = 2) -> torch.Tensor:
+def _a2a(x: torch.Tensor, group=None, world: int = 2, async_op: bool = False):
+    """Equal-split all-to-all of a flat staging buffer (rank-major blocks)."""
     if world == 1:  # one rank: the transpose moves nothing (no process group needed)
-        return x
+        return (x, None) if async_op else x
     out = torch.empty_like(x)
-    dist.all_to_all_single(out, x, group=group)
-    return out
+    work = dist.all_to_all_single(out, x, group=group, async_op=async_op)
+    return (out, work) if async_op else out
 
 
-def columns_to_rows(x1: torch.Tensor, shard: SeqShard, group=None) -> torch.Tensor:
+# The all-to-all transposes.  The local re-layouts around the exchange are
+# `passes.stage` calls (GpuPasses: the fb_shard_stage kernel, which also
+# converts to the wire type — "bf16" halves the NVLink bytes of each exchange).
+# (one rank: both layouts are the identity, nothing is staged or exchanged)
+def _c2r_send(x1, shard, passes, wire):
+    if shard.world == 1:
+        return x1
+    C = x1.shape[0]
+    return passes.stage(x1, C, shard.world, shard.mp * shard.lp, wire)   # [dest][C][mp lp]
+
+
+def _c2r_recv(recv, C, shard, passes):
+    P, mp, lp = shard.world, shard.mp, shard.lp
+    if P == 1:
+        return recv.reshape(C, mp, lp)
+    return passes.stage(recv, P, C * mp, lp, "f32").reshape(C, mp, P * lp)  # [C][mp][src lp]
+
+
+def _r2c_send(rows, shard, passes, wire):
+    if shard.world == 1:
+        return rows
+    C = rows.shape[0]
+    return passes.stage(rows, C * shard.mp, shard.world, shard.lp, wire)  # [dest][C mp][lp]
+
+
+def _r2c_recv(recv, C, shard, passes):
+    P, mp, lp = shard.world, shard.mp, shard.lp
+    if P == 1:
+        return recv.reshape(C, mp, lp)
+    return passes.stage(recv, P, C, mp * lp, "f32").reshape(C, P * mp, lp)  # [C][src mp][lp]
+
+
+def columns_to_rows(x1: torch.Tensor, shard: SeqShard, group=None, passes=None,
+                    wire: str = "f32") -> torch.Tensor:
     """[C, m, lp] complex (all rows, my columns) -> [C, mp, l] (my rows, all columns)."""
     C = x1.shape[0]
-    P, mp, lp = shard.world, shard.mp, shard.lp
-    send = x1.reshape(C, P, mp, lp).permute(1, 0, 2, 3).contiguous()  # [dest][C][mp][lp]
-    recv = _a2a(torch.view_as_real(send), group, P)                     # [src][C][mp][lp][2]
-    recv = torch.view_as_complex(recv)
-    return recv.permute(1, 2, 0, 3).reshape(C, mp, P * lp).contiguous()
+    return _c2r_recv(_a2a(_c2r_send(x1, shard, passes, wire), group, shard.world), C, shard, passes)
 
 
-def rows_to_columns(rows: torch.Tensor, shard: SeqShard, group=None) -> torch.Tensor:
+def rows_to_columns(rows: torch.Tensor, shard: SeqShard, group=None, passes=None,
+                    wire: str = "f32") -> torch.Tensor:
     """[C, mp, l] (my rows, all columns) -> [C, m, lp] (all rows, my columns)."""
     C = rows.shape[0]
-    P, mp, lp = shard.world, shard.mp, shard.lp
-    send = rows.reshape(C, mp, P, lp).permute(2, 0, 1, 3).contiguous()  # [dest][C][mp][lp]
-    recv = torch.view_as_complex(_a2a(torch.view_as_real(send), group, P))  # [src][C][mp][lp]
-    return recv.permute(1, 0, 2, 3).reshape(C, P * mp, lp).contiguous()
+    return _r2c_recv(_a2a(_r2c_send(rows, shard, passes, wire), group, shard.world), C, shard, passes)
 
 
 class LocalPasses(Protocol):
     def pass1(self, x_cols: torch.Tensor, shard: SeqShard) -> torch.Tensor: ...
     def pass2(self, rows: torch.Tensor, shard: SeqShard) -> torch.Tensor: ...
     def pass3(self, w_cols: torch.Tensor, shard: SeqShard) -> torch.Tensor: ...
+    def stage(self, t: torch.Tensor, A: int, Bd: int, X: int, wire: str) -> torch.Tensor: ...
 
 
-def four_step_conv(x_cols: torch.Tensor, shard: SeqShard, passes: LocalPasses,
-                   group=None) -> torch.Tensor:
+def four_step_conv(x_cols: torch.Tensor | None, shard: SeqShard, passes: LocalPasses,
+                   group=None, wire: str = "f32", chunks: int = 1, C: int | None = None,
+                   first=None, last=None):
     """Circular convolution of length n = l m of the sharded signals
     x_cols [C, m, lp] (complex; two real channels per complex as elsewhere)
-    with the kernel held by `passes`; returns this rank's output columns."""
-    x1 = passes.pass1(x_cols, shard)
-    rows = columns_to_rows(x1, shard, group)
-    rows = passes.pass2(rows, shard)
-    w = rows_to_columns(rows, shard, group)
-    return passes.pass3(w, shard)
+    with the kernel held by `passes`; returns this rank's output columns.
+    `chunks` > 1 splits the channels (whole pairs) so that chunk i's
+    all-to-alls (NCCL, asynchronous) overlap the local passes of its
+    neighbours.  `first(a, b)` / `last(w, a, b)` replace pass 1 / pass 3 of
+    channels [a, b) (the layer's fused signal-side passes); the outputs of
+    `last` are concatenated along dim 0."""
+    C = x_cols.shape[0] if C is None else C
+    first = first or (lambda a, b: passes.pass1(x_cols[a:b], shard))
+    last = last or (lambda w, a, b: passes.pass3(w, shard))
+    # chunks of whole channel pairs (the kernel rows are shared per head)
+    H = passes.kf2.shape[0] if getattr(passes, "kf2", None) is not None else C
+    units = max(1, C // H)
+    chunks = max(1, min(chunks, units))
+    bounds = [H * (units * i // chunks) for i in range(chunks)] + [C]
+    parts = [(a, b) for a, b in zip(bounds[:-1], bounds[1:]) if b > a]
+    P = shard.world
+    sent = []
+    for a, b in parts:  # pass 1 + the outbound exchange, issued back to back
+        sent.append(_a2a(_c2r_send(first(a, b), shard, passes, wire), group, P, True))
+    back = []
+    for (a, b), (recv, work) in zip(parts, sent):
+        if work is not None:
+            work.wait()
+        rows = passes.pass2(_c2r_recv(recv, b - a, shard, passes), shard)
+        back.append(_a2a(_r2c_send(rows, shard, passes, wire), group, P, True))
+    out = []
+    for (a, b), (recv, work) in zip(parts, back):
+        if work is not None:
+            work.wait()
+        out.append(last(_r2c_recv(recv, b - a, shard, passes), a, b))
+    return out[0] if len(out) == 1 else torch.cat(out, 0)
 
 
 class GpuPasses:
-    """The three local passes on this rank's GPU with this package's kernels
-    (fb_shard_columns / fb_shard_rows in libflashbutterfly.so): complex64
-    [C, m, lp] column slices and [C, mp, l] row slices, l = 8192.  `kf2` holds
-    this rank's rows of the kernel spectrum, kf2[c][a - a0][s] = K_hat[a + m s]."""
+    """The local passes and the glue on this rank's GPU with this package's
+    kernels (libflashbutterfly.so: fb_shard_columns(_from_signals /
+    _to_signals: pair packing and the D u skip fused) / fb_shard_rows_pairs /
+    fb_shard_rows_bwd for the passes, fb_shard_stage for the all-to-all
+    layouts): complex64 [C, m, lp] column slices and [C, mp, l]
+    row slices, l = 8192, C = P * H channels (pair-major).  `kf2` holds this
+    rank's rows of the kernel spectrum, kf2[h][a - a0][s] = K_hat[a + m s],
+    shared by the P channel pairs of head h."""
 
     def __init__(self, n: int, kf2: torch.Tensor | None = None, device=None):
         import ctypes as C
@@ -153,13 +212,16 @@ class GpuPasses:
     def _stream(self):
         return self._C.c_void_p(torch.cuda.current_stream(self.device).cuda_stream)
 
+    def _call(self, name, *args):
+        self._lib.check(getattr(self._lib.lib(), name)(*args))
+
     def _cols(self, x: torch.Tensor, sh: SeqShard, inverse: int) -> torch.Tensor:
         x = x.contiguous()
         if x.dtype != torch.complex64 or tuple(x.shape[1:]) != (sh.m, sh.lp):
             raise ValueError(f"expected complex64 [C, {sh.m}, {sh.lp}], got {x.dtype} {list(x.shape)}")
         out = torch.empty_like(x)
-        self._lib.check(self._lib.lib().fb_shard_columns(self._h, self._p(x), self._p(out), x.shape[0],
-                                                         sh.tau0, sh.lp, inverse, self._stream()))
+        self._call("fb_shard_columns", self._h, self._p(x), self._p(out), x.shape[0], sh.tau0, sh.lp,
+                   inverse, self._stream())
         return out
 
     def pass1(self, x_cols: torch.Tensor, sh: SeqShard) -> torch.Tensor:
@@ -168,41 +230,86 @@ class GpuPasses:
     def pass3(self, w_cols: torch.Tensor, sh: SeqShard) -> torch.Tensor:
         return self._cols(w_cols, sh, 1)
 
+    def pass1_signals(self, sig: torch.Tensor, sh: SeqShard) -> torch.Tensor:
+        """Pass 1 of the channel pairs straight from real signals [B, H, m/2, lp]
+        (pairs packed on the fly, causal zero rows implied) -> [P*H, m, lp]."""
+        sig = sig.contiguous()
+        B, H, half, lp = sig.shape
+        out = torch.empty(((B + 1) // 2) * H, sh.m, lp, dtype=torch.complex64, device=self.device)
+        self._call("fb_shard_columns_from_signals", self._h, self._p(sig), self._DT[sig.dtype], self._p(out),
+                   B, H, half, sh.tau0, lp, self._stream())
+        return out
+
+    def pass3_signals(self, w: torch.Tensor, sh: SeqShard, B: int, H: int, half: int, skip=None, D=None,
+                      dtype=torch.float32) -> torch.Tensor:
+        """Pass 3 of [P*H, m, lp] straight into real signals [B, H, m/2, lp]
+        (+ D[h] skip), in `dtype`."""
+        w = w.contiguous()
+        out = torch.empty(B, H, half, sh.lp, dtype=dtype, device=self.device)
+        if skip is not None:
+            skip = skip.to(dtype).contiguous()
+            D = D.float().contiguous()
+        self._call("fb_shard_columns_to_signals", self._h, self._p(w), self._p(out), self._DT[dtype],
+                   self._p(skip), self._p(D), B, H, half, sh.tau0, sh.lp, self._stream())
+        return out
+
     def pass2(self, rows: torch.Tensor, sh: SeqShard) -> torch.Tensor:
+        """Rows [P*H, mp, l] in place against the heads' kernel rows (no copies per pair)."""
         rows = rows.contiguous()
-        kf2 = self.kf2.contiguous()
-        self._lib.check(self._lib.lib().fb_shard_rows(self._h, self._p(rows), self._p(kf2), None,
-                                                      rows.shape[0], sh.mp, 0, 1.0, self._stream()))
+        H = self.kf2.shape[0]
+        self._call("fb_shard_rows_pairs", self._h, self._p(rows), self._p(self.kf2.contiguous()),
+                   rows.shape[0] // H, H, sh.mp, self._stream())
         return rows
+
+    def rows_bwd(self, dy_rows: torch.Tensor, u_rows: torch.Tensor, sh: SeqShard):
+        """du rows = IFFT(DY conj(kf2)) in place, and the heads' dK spectrum rows
+        IFFT(sum_pairs conj(U) DY) [H, mp, l] (fused, fixed order)."""
+        H = self.kf2.shape[0]
+        dy_rows, u_rows = dy_rows.contiguous(), u_rows.contiguous()
+        wdk = torch.empty(H, sh.mp, sh.l, dtype=torch.complex64, device=self.device)
+        self._call("fb_shard_rows_bwd", self._h, self._p(dy_rows), self._p(u_rows),
+                   self._p(self.kf2.contiguous()), self._p(wdk), dy_rows.shape[0] // H, H, sh.mp,
+                   self._stream())
+        return dy_rows, wdk
 
     def rows_fft(self, rows: torch.Tensor, sh: SeqShard) -> torch.Tensor:
         """FFT_l of each row [C, mp, l] (fb_shard_rows, spectrum mode)."""
         rows = rows.contiguous()
         out = torch.empty_like(rows)
-        self._lib.check(self._lib.lib().fb_shard_rows(self._h, self._p(rows), None, self._p(out),
-                                                      rows.shape[0], sh.mp, 1, 1.0, self._stream()))
+        self._call("fb_shard_rows", self._h, self._p(rows), None, self._p(out), rows.shape[0], sh.mp, 1,
+                   self._C.c_float(1.0), self._stream())
         return out
 
-    def rows_ifft(self, rows: torch.Tensor, sh: SeqShard) -> torch.Tensor:
-        """Unnormalised inverse FFT_l of each row: conj(FFT_l(conj(rows)))."""
-        return torch.conj(self.rows_fft(torch.conj(rows).resolve_conj(), sh)).resolve_conj()
+    def stage(self, t: torch.Tensor, A: int, Bd: int, X: int, wire: str) -> torch.Tensor:
+        """out[b][a][x] = t[a][b][x] (complex elements) as a flat wire buffer."""
+        t = t.contiguous()
+        in_dt = self._lib.FB_F32 if t.dtype == torch.complex64 else self._lib.FB_BF16
+        if wire == "f32":
+            out = torch.empty(A * Bd * X, dtype=torch.complex64, device=self.device)
+            out_dt = self._lib.FB_F32
+        else:
+            out = torch.empty(2 * A * Bd * X, dtype=torch.bfloat16, device=self.device)
+            out_dt = self._lib.FB_BF16
+        self._call("fb_shard_stage", self._p(t), self._p(out), A, Bd, X, in_dt, out_dt, self._stream())
+        return out
 
-    def spectrum_rows(self, kbar_cols: torch.Tensor, sh: SeqShard, group=None) -> torch.Tensor:
+    _DT = {torch.float32: 0, torch.bfloat16: 1, torch.float16: 2}
+
+    def spectrum_rows(self, kbar_cols: torch.Tensor, sh: SeqShard, group=None,
+                      wire: str = "f32") -> torch.Tensor:
         """This rank's kernel-spectrum rows from its real kernel columns
-        kbar_cols [C, m, lp] (float32; zero-padded causal kernels): pass 1,
-        the transpose, then the row FFTs — the sharded build_three_pass
-        (three_pass.cpp:197-203).  Sets and returns self.kf2."""
-        x = torch.complex(kbar_cols.float(), torch.zeros_like(kbar_cols, dtype=torch.float32))
-        rows = columns_to_rows(self.pass1(x, sh), sh, group)
-        kf2 = torch.empty_like(rows)
-        self._lib.check(self._lib.lib().fb_shard_rows(self._h, self._p(rows), None, self._p(kf2),
-                                                      rows.shape[0], sh.mp, 1, 1.0, self._stream()))
-        self.kf2 = kf2
-        return kf2
+        kbar_cols [H, m/2, lp] (regularized, the causal zero rows implied):
+        pass 1, the transpose, then the row FFTs — the sharded build_three_pass
+        (three_pass.cpp:197-203).  Sets and returns self.kf2 [H, mp, l]."""
+        x = self.pass1_signals(kbar_cols.float().unsqueeze(0), sh)  # one "batch": re = Kbar, im = 0
+        rows = columns_to_rows(x, sh, group, self, wire)
+        self.kf2 = self.rows_fft(rows, sh)
+        return self.kf2
 
 
 def sharded_long_conv(u_cols: torch.Tensor, kbar_cols: torch.Tensor, D: torch.Tensor,
-                      shard: SeqShard, passes: "GpuPasses", group=None) -> torch.Tensor:
+                      shard: SeqShard, passes: "GpuPasses", group=None, wire: str = "f32",
+                      chunks: int = 1) -> torch.Tensor:
     """The layer forward y = conv_causal(u, Kbar) + D u (regularize.cpp:185-187)
     with the sequence sharded: rank r holds the tau-slice [tau0, tau0 + lp) of
     every data row c < m/2 of t = c l + tau (N = n / 2 causal; rows c >= m/2
@@ -211,84 +318,50 @@ def sharded_long_conv(u_cols: torch.Tensor, kbar_cols: torch.Tensor, D: torch.Te
       D [H]  ->  y_cols [B, H, m/2, lp] (u's dtype).
     Two real channels ride as re / im of one complex transform (batch-pair
     packing, as on a single GPU); the kernel spectrum is built sharded with the
-    same passes (two all-to-alls), the convolution costs two more."""
+    same passes (two all-to-alls), the convolution costs two more.  All glue
+    (packing, staging, unpack with D u) runs in the passes' kernels."""
     B, H, half, lp = u_cols.shape
-    m = shard.m
-    if half * 2 != m or lp != shard.lp or kbar_cols.shape != (H, half, lp):
+    if half * 2 != shard.m or lp != shard.lp or kbar_cols.shape != (H, half, lp):
         raise ValueError("sharded_long_conv: expected u [B, H, m/2, lp] and Kbar [H, m/2, lp]")
-    dev = u_cols.device
-    kpad = torch.zeros(H, m, lp, dtype=torch.float32, device=dev)
-    kpad[:, :half] = kbar_cols.float()
-    kf2 = passes.spectrum_rows(kpad, shard, group)  # [H, mp, l]
-    P = (B + 1) // 2
-    uf = u_cols.float()
-    if B % 2:
-        uf = torch.cat([uf, torch.zeros_like(uf[:1])], 0)
-    x = torch.zeros(P, H, m, lp, dtype=torch.complex64, device=dev)
-    x[:, :, :half] = torch.complex(uf[0::2], uf[1::2])
-    passes.kf2 = kf2.repeat(P, 1, 1)  # channel (p, h) uses head h's rows
-    y = four_step_conv(x.reshape(P * H, m, lp), shard, passes, group).reshape(P, H, m, lp)
-    y = y[:, :, :half]
-    out = torch.stack([y.real, y.imag], 1).reshape(2 * P, H, half, lp)[:B]
-    out = out + D.float().view(1, H, 1, 1) * u_cols.float()
-    return out.to(u_cols.dtype)
+    passes.spectrum_rows(kbar_cols, shard, group, wire)  # [H, mp, l]
 
+    def first(a, b):  # channels [a, b) = pairs [a/H, b/H) = batches [2a/H, 2b/H)
+        return passes.pass1_signals(u_cols[2 * a // H:min(B, 2 * b // H)], shard)
 
-def _pack_pairs(sig_cols: torch.Tensor, m: int) -> torch.Tensor:
-    """[B, H, m/2, lp] real -> [P*H, m, lp] complex (channels 2p, 2p+1 -> re, im;
-    rows c >= m/2 are the causal zero pad)."""
-    B, H, half, lp = sig_cols.shape
-    P = (B + 1) // 2
-    f = sig_cols.float()
-    if B % 2:
-        f = torch.cat([f, torch.zeros_like(f[:1])], 0)
-    x = torch.zeros(P, H, m, lp, dtype=torch.complex64, device=sig_cols.device)
-    x[:, :, :half] = torch.complex(f[0::2], f[1::2])
-    return x.reshape(P * H, m, lp)
+    def last(w, a, b):
+        b0, b1 = 2 * a // H, min(B, 2 * b // H)
+        return passes.pass3_signals(w, shard, b1 - b0, H, half, skip=u_cols[b0:b1], D=D, dtype=u_cols.dtype)
 
-
-def _unpack_pairs(y: torch.Tensor, B: int, H: int, half: int) -> torch.Tensor:
-    P = (B + 1) // 2
-    y = y.reshape(P, H, -1, y.shape[-1])[:, :, :half]
-    return torch.stack([y.real, y.imag], 1).reshape(2 * P, H, half, y.shape[-1])[:B]
+    return four_step_conv(None, shard, passes, group, wire, chunks, C=((B + 1) // 2) * H, first=first,
+                          last=last)
 
 
 def sharded_long_conv_backward(dy_cols: torch.Tensor, u_cols: torch.Tensor,
                                kbar_cols: torch.Tensor, D: torch.Tensor, shard: SeqShard,
-                               passes: "GpuPasses", group=None):
+                               passes: "GpuPasses", group=None, wire: str = "f32"):
     """Backward of sharded_long_conv (SURVEY.md §8c formulas, sequence sharded):
       du     = corr(dy, Kbar) + D dy   -> IFFT(DY conj(K_hat)), causal crop
       dKbar  = sum_b corr(dy_b, u_b)   -> Re IFFT(sum_pairs conj(U) DY), lag < N
       dD     = dKbar[0]                 (lag 0, held by the rank with tau0 = 0)
     Layouts as in sharded_long_conv; returns (du_cols [B, H, m/2, lp],
-    dkbar_cols [H, m/2, lp] fp32, dD [H] fp32).  The chain rule through the
-    regularizers to dK is sharded_regularizer_backward (halo exchange of the
-    +-p smoothing neighbours across slices)."""
+    dkbar_cols [H, m/2, lp] fp32, dD [H] fp32).  The row pass (both spectra,
+    du rows, the dK spectrum summed over pairs in a fixed order, its inverse)
+    is one fused kernel (fb_shard_rows_bwd).  The chain rule through the
+    regularizers to dK is sharded_regularizer_backward (halo exchange)."""
     B, H, half, lp = u_cols.shape
-    m = shard.m
     dev = u_cols.device
-    kpad = torch.zeros(H, m, lp, dtype=torch.float32, device=dev)
-    kpad[:, :half] = kbar_cols.float()
-    kf2 = passes.spectrum_rows(kpad, shard, group)  # [H, mp, l] (K_hat rows)
-    P = (B + 1) // 2
-    xdy = _pack_pairs(dy_cols, m)
-    xu = _pack_pairs(u_cols, m)
-    # row spectra of dy and u (pass 1, transpose, row FFT)
-    DY = passes.rows_fft(columns_to_rows(passes.pass1(xdy, shard), shard, group), shard)
-    U = passes.rows_fft(columns_to_rows(passes.pass1(xu, shard), shard, group), shard)
-    # du: DY conj(K_hat), inverse rows, transpose back, pass 3
-    kc = torch.conj(kf2).resolve_conj().repeat(P, 1, 1)
-    du_rows = passes.rows_ifft(DY * kc, shard)
-    du = _unpack_pairs(passes.pass3(rows_to_columns(du_rows, shard, group), shard), B, H, half)
-    du = du + D.float().view(1, H, 1, 1) * dy_cols.float()
-    # dKbar: sum over the pairs of each head, then the inverse transform
-    S = (torch.conj(U) * DY).reshape(P, H, shard.mp, shard.l).sum(0)
-    dk = passes.pass3(rows_to_columns(passes.rows_ifft(S, shard), shard, group), shard)
-    dkbar = dk.real[:, :half].contiguous()
+    passes.spectrum_rows(kbar_cols, shard, group, wire)  # [H, mp, l] (K_hat rows)
+    rdy = columns_to_rows(passes.pass1_signals(dy_cols, shard), shard, group, passes, wire)
+    ru = columns_to_rows(passes.pass1_signals(u_cols, shard), shard, group, passes, wire)
+    du_rows, wdk = passes.rows_bwd(rdy, ru, shard)
+    du = passes.pass3_signals(rows_to_columns(du_rows, shard, group, passes, wire), shard, B, H, half,
+                              skip=dy_cols, D=D, dtype=dy_cols.dtype)
+    # the dK rows: one "batch" per head, the real part is dKbar
+    dkbar = passes.pass3_signals(rows_to_columns(wdk, shard, group, passes, wire), shard, 1, H, half)[0]
     dD = dkbar[:, 0, 0].clone() if shard.tau0 == 0 else torch.zeros(H, device=dev)
     if shard.world > 1:
         dist.all_reduce(dD, group=group)
-    return du.to(dy_cols.dtype), dkbar, dD
+    return du, dkbar, dD
 
 
 def _halo(x_cols: torch.Tensor, p: int, shard: SeqShard, group=None) -> torch.Tensor:

@@ -466,16 +466,34 @@ def test_four_step_gpu_passes_single_rank(m):
     want = np.fft.ifft(np.fft.fft(x.astype(np.complex128), axis=1) * np.fft.fft(k, axis=1), axis=1)
     sh = ss.SeqShard(l=l, m=m, world=1, rank=0)
     gp = ss.GpuPasses(n)
-    kcols = ss.scatter_tau(torch.from_numpy(k).cuda(), sh)
+    kcols = ss.scatter_tau(torch.from_numpy(k).cuda(), sh)[:, : m // 2]  # the causal half
     kf2 = gp.spectrum_rows(kcols, sh)
     khat = np.fft.fft(k.astype(np.float64), axis=1)
     s_idx, a_idx = np.arange(l), np.arange(m)
     kf2_want = khat[:, a_idx[:, None] + m * s_idx[None, :]]
     assert rel_l2(kf2.cpu().numpy(), kf2_want) < 1e-5
     xc = ss.scatter_tau(torch.from_numpy(x).cuda(), sh)
-    y = ss.four_step_conv(xc, sh, gp)
-    got = ss.gather_tau([y.cpu()], sh).numpy()
-    assert rel_l2(got, want) < 1e-5
+    for chunks in (1, 2):
+        y = ss.four_step_conv(xc, sh, gp, chunks=chunks)
+        got = ss.gather_tau([y.cpu()], sh).numpy()
+        assert rel_l2(got, want) < 1e-5, chunks
+
+
+def test_shard_stage_layouts():
+    """fb_shard_stage (the all-to-all send / receive layouts): out[b][a][x] =
+    in[a][b][x], exact in f32, bf16-rounded on a bf16 wire and back."""
+    from paper_2302_06646_b200 import seqshard as ss
+
+    gp = ss.GpuPasses(8192 * 16)
+    A, Bd, X = 6, 4, 96
+    t = torch.randn(A, Bd, X, dtype=torch.complex64, device="cuda")
+    want = t.permute(1, 0, 2).contiguous().reshape(-1)
+    assert torch.equal(gp.stage(t, A, Bd, X, "f32"), want)
+    wire = gp.stage(t, A, Bd, X, "bf16")
+    assert wire.dtype == torch.bfloat16 and wire.numel() == 2 * A * Bd * X
+    back = gp.stage(wire, Bd, A, X, "f32")  # [A][Bd][X] again, f32
+    ref = torch.view_as_complex(torch.view_as_real(t).bfloat16().float()).reshape(-1)
+    assert torch.equal(back, ref)
 
 
 @pytest.mark.parametrize("dtype,N", [(torch.float32, 16384), (torch.bfloat16, 32768)])

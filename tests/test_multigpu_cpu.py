@@ -20,10 +20,16 @@ L_COLS, M_ROWS = 64, 16  # n = l * m = 1024
 
 
 class NumpyPasses:
-    """numpy restatement of three_pass.cpp:225-254 on a rank's slice."""
+    """numpy / torch restatement of the local passes (three_pass.cpp:225-254)
+    and of the glue kernels (fb_shard_pack / _unpack / _stage / _real_rows,
+    fb_shard_rows_bwd) on a rank's slice: test infrastructure standing in for
+    seqshard.GpuPasses on CPU ranks."""
 
-    def __init__(self, kf2_full: np.ndarray):
-        self.kf2 = kf2_full  # [C][m][l] = K_hat[a + m s] (per channel)
+    def __init__(self, kf2_full):
+        self.kf2 = kf2_full  # [C][m][l] = K_hat[a + m s] (per channel), or set by spectrum_rows
+
+    def _kf2(self):
+        return self.kf2.numpy() if isinstance(self.kf2, torch.Tensor) else self.kf2
 
     def pass1(self, x, sh):
         n = sh.l * sh.m
@@ -32,11 +38,15 @@ class NumpyPasses:
         a = np.arange(sh.m)[:, None]
         return torch.from_numpy(X * np.exp(-2j * np.pi * a * tau[None, :] / n)).to(torch.complex64)
 
+    def _rows_kf2(self, sh):
+        kf2 = self._kf2()
+        # full-height kf2 (unsharded problem) or this rank's rows
+        return kf2[:, sh.a0:sh.a0 + sh.mp, :] if kf2.shape[1] == sh.m else kf2
+
     def pass2(self, rows, sh):
-        Z = np.fft.fft(rows.numpy(), axis=2)
-        kf2 = self.kf2.numpy() if isinstance(self.kf2, torch.Tensor) else self.kf2
-        # full-height kf2 (unsharded problem) or this rank's rows (sharded_long_conv)
-        Z = Z * (kf2[:, sh.a0:sh.a0 + sh.mp, :] if kf2.shape[1] == sh.m else kf2)
+        kf2 = self._rows_kf2(sh)
+        P = rows.shape[0] // kf2.shape[0]  # kernel rows shared by the channel pairs of a head
+        Z = np.fft.fft(rows.numpy(), axis=2) * np.tile(kf2, (P, 1, 1))
         return torch.from_numpy(np.fft.ifft(Z, axis=2) * sh.l).to(torch.complex64)
 
     def pass3(self, w, sh):
@@ -49,13 +59,55 @@ class NumpyPasses:
     def rows_fft(self, rows, sh):
         return torch.from_numpy(np.fft.fft(rows.numpy(), axis=2)).to(torch.complex64)
 
-    def rows_ifft(self, rows, sh):
-        return torch.from_numpy(np.fft.ifft(rows.numpy(), axis=2) * sh.l).to(torch.complex64)
+    def rows_bwd(self, dy_rows, u_rows, sh):
+        kf2 = self._rows_kf2(sh)
+        H = kf2.shape[0]
+        P = dy_rows.shape[0] // H
+        DY = np.fft.fft(dy_rows.numpy(), axis=2)
+        U = np.fft.fft(u_rows.numpy(), axis=2)
+        du = np.fft.ifft(DY * np.conj(np.tile(kf2, (P, 1, 1))), axis=2) * sh.l
+        S = (np.conj(U) * DY).reshape(P, H, sh.mp, sh.l).sum(0)
+        wdk = np.fft.ifft(S, axis=2) * sh.l
+        return torch.from_numpy(du).to(torch.complex64), torch.from_numpy(wdk).to(torch.complex64)
 
-    def spectrum_rows(self, kbar_cols, sh, group=None):
+    def stage(self, t, A, Bd, X, wire):
+        t = t.reshape(-1)
+        if t.dtype == torch.bfloat16:
+            t = torch.view_as_complex(t.float().reshape(-1, 2).contiguous())
+        v = t.reshape(A, Bd, X).permute(1, 0, 2).contiguous().reshape(-1)
+        return torch.view_as_real(v).to(torch.bfloat16).reshape(-1) if wire == "bf16" else v
+
+    def pack(self, sig, m):
+        B, H, half, lp = sig.shape
+        P = (B + 1) // 2
+        f = sig.float()
+        if B % 2:
+            f = torch.cat([f, torch.zeros_like(f[:1])], 0)
+        x = torch.zeros(P, H, m, lp, dtype=torch.complex64)
+        x[:, :, :half] = torch.complex(f[0::2], f[1::2])
+        return x.reshape(P * H, m, lp)
+
+    def unpack(self, y, B, H, half, skip=None, D=None, dtype=torch.float32):
+        P = (B + 1) // 2
+        y = y.reshape(P, H, -1, y.shape[-1])[:, :, :half]
+        out = torch.stack([y.real, y.imag], 1).reshape(2 * P, H, half, y.shape[-1])[:B]
+        if skip is not None:
+            out = out + D.float().view(1, H, 1, 1) * skip.float()
+        return out.to(dtype)
+
+    def pass1_signals(self, sig, sh):
+        return self.pass1(self.pack(sig, sh.m), sh)
+
+    def pass3_signals(self, w, sh, B, H, half, skip=None, D=None, dtype=torch.float32):
+        return self.unpack(self.pass3(w, sh), B, H, half, skip, D, dtype)
+
+    def real_rows(self, y, half):
+        return y.real[:, :half].contiguous().float()
+
+    def spectrum_rows(self, kbar_cols, sh, group=None, wire="f32"):
         """The sharded kernel spectrum, as GpuPasses.spectrum_rows does it."""
-        x = torch.complex(kbar_cols.float(), torch.zeros_like(kbar_cols.float()))
-        rows = ss.columns_to_rows(self.pass1(x, sh), sh, group)
+        rows = ss.columns_to_rows(self.pass1(self.pack(kbar_cols.float().unsqueeze(0), sh.m), sh), sh, group,
+                                  self, wire)
         self.kf2 = np.fft.fft(rows.numpy(), axis=2)
         return torch.from_numpy(self.kf2).to(torch.complex64)
 
@@ -73,20 +125,39 @@ def _problem(C=3, seed=0):
     return x, kf2, want
 
 
+def _problem_pairs(P=3, H=2, seed=1):
+    """P channel pairs per head, H heads (pair-major channels), per-head kernels."""
+    rng = np.random.default_rng(seed)
+    n = L_COLS * M_ROWS
+    x = (rng.standard_normal((P * H, n)) + 1j * rng.standard_normal((P * H, n))).astype(np.complex64)
+    k = rng.standard_normal((H, n)).astype(np.float32)
+    khat = np.fft.fft(k, axis=1)
+    s = np.arange(L_COLS)
+    a = np.arange(M_ROWS)
+    kf2 = khat[:, a[:, None] + M_ROWS * s[None, :]]
+    want = np.fft.ifft(np.fft.fft(x, axis=1) * np.tile(khat, (P, 1)), axis=1)
+    return x, kf2, want
+
+
 def _seq_worker(rank, world):
-    x, kf2, _ = _problem()
+    chunks = int(os.environ.get("FB_TEST_CHUNKS", "1"))
+    x, kf2, _ = _problem() if chunks == 1 else _problem_pairs()
     sh = ss.SeqShard(L_COLS, M_ROWS, world, rank)
     cols = ss.scatter_tau(torch.from_numpy(x), sh)
-    y = ss.four_step_conv(cols, sh, NumpyPasses(kf2))
+    y = ss.four_step_conv(cols, sh, NumpyPasses(kf2), chunks=chunks)
     np.save(os.path.join(os.environ["FB_TEST_DIR"], f"seq_{world}_{rank}.npy"), y.numpy())
 
 
-@pytest.mark.parametrize("world", [2, 4])
-def test_seq_sharded_four_step_gloo(world, monkeypatch):
+@pytest.mark.parametrize("world,chunks", [(2, 1), (4, 1), (2, 3)])
+def test_seq_sharded_four_step_gloo(world, chunks, monkeypatch):
+    """The two all-to-all transposes (and, chunks > 1, the pipelined exchange:
+    per-channel-chunk asynchronous all-to-alls) move the data so that the
+    sharded circular convolution equals the single-process one."""
     d = tempfile.mkdtemp()
     monkeypatch.setenv("FB_TEST_DIR", d)
-    ss.run_ranks(world, _seq_worker, port=29571 + world)
-    x, _, want = _problem()
+    monkeypatch.setenv("FB_TEST_CHUNKS", str(chunks))
+    ss.run_ranks(world, _seq_worker, port=29571 + world + 10 * chunks)
+    x, _, want = _problem() if chunks == 1 else _problem_pairs()
     sh = ss.SeqShard(L_COLS, M_ROWS, world, 0)
     parts = [torch.from_numpy(np.load(os.path.join(d, f"seq_{world}_{r}.npy"))) for r in range(world)]
     got = ss.gather_tau(parts, sh).numpy()
