@@ -269,6 +269,25 @@ int fb_conv_rows(fb_dft_plan* plan, const float* u, const float* k, float* y, in
                  int64_t k_rows, int mode, void* workspace, void* stream);
 int fb_conv_rows_spectrum(fb_dft_plan* plan, const float* u, const float* kspec, float* y, int64_t N,
                           int64_t rows, int64_t k_rows, int mode, void* workspace, void* stream);
+/* Learned-butterfly long convolution: the paper's extension
+ * with the Butterfly matrices of the FlashButterfly transform learned.  Per
+ * head h, with L(W, .) = learned_forward (butterfly.cpp:235-246) over the
+ * build_plan(n, r) scaffolding and IL(W, z) = conj(L(W, conj z)) / n:
+ *   y[b,h] = Re IL(Wi[h], L(Wf[h], pad u[b,h]) * L(Wf[h], pad Kbar[h]))[:N] + D[h] u[b,h]
+ * n = 2N (causal) or N (circular); f32 I/O; Wf, Wi, dWf, dWi: [H][P] complex f32
+ * (fb_lconv_plan_dims: P per head).  With Wf = Wi = the DFT blocks
+ * (LearnedButterfly::from_plan) this equals regularized_long_conv.  The
+ * backward returns du, dKbar (w.r.t. the regularized bank), dD, dWf, dWi. */
+typedef struct fb_lconv_plan fb_lconv_plan;
+int fb_lconv_plan_create(fb_lconv_plan** plan, int64_t N, int64_t H, int64_t r, int mode, int device);
+int fb_lconv_plan_destroy(fb_lconv_plan* plan);
+int fb_lconv_plan_dims(const fb_lconv_plan* plan, int64_t* n, int64_t* param_count);
+size_t fb_lconv_workspace_size(const fb_lconv_plan* plan, int64_t B);
+int fb_lconv_fwd(fb_lconv_plan* plan, const float* u, const float* kbar, const float* D, const float* Wf,
+                 const float* Wi, float* y, int64_t B, void* workspace, void* stream);
+int fb_lconv_bwd(fb_lconv_plan* plan, const float* dy, const float* u, const float* kbar, const float* D,
+                 const float* Wf, const float* Wi, float* du, float* dkbar, float* dD, float* dWf,
+                 float* dWi, int64_t B, void* workspace, void* stream);
 const char* fb_last_error(void);
 int fb_version(void);
 

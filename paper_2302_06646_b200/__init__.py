@@ -20,10 +20,15 @@ from .longconv import (  # noqa: F401
     regularized_long_conv_backward,
 )
 from ._lib import DimensionError, FBError, PlanError  # noqa: F401
-from .learned import LearnedButterflyPlan, learned_butterfly  # noqa: F401
+from .learned import (  # noqa: F401
+    LearnedButterflyPlan,
+    LearnedLongConvPlan,
+    learned_butterfly,
+    learned_long_conv,
+)
 
 __all__ = [
     "ConvMode", "Engine", "HostRunner", "InitKind", "LongConvPlan", "init_kernels", "RegularizationConfig", "SmoothDomain", "long_conv",
     "regularized_long_conv", "regularized_long_conv_backward", "DimensionError", "FBError",
-    "PlanError", "LearnedButterflyPlan", "learned_butterfly",
+    "PlanError", "LearnedButterflyPlan", "learned_butterfly", "LearnedLongConvPlan", "learned_long_conv",
 ]

@@ -32,7 +32,8 @@ EXPORTED = [
     "fb_dft_plan_destroy", "fb_dft_plan_factors", "fb_dft_workspace_size", "fb_dft", "fb_conv_rows",
     "fb_conv_rows_spectrum", "fb_init_kernels", "fb_shard_rows_pairs", "fb_shard_rows_bwd",
     "fb_shard_stage",
-    "fb_shard_columns_from_signals", "fb_shard_columns_to_signals",
+    "fb_shard_columns_from_signals", "fb_shard_columns_to_signals", "fb_lconv_plan_create",
+    "fb_lconv_plan_destroy", "fb_lconv_plan_dims", "fb_lconv_workspace_size", "fb_lconv_fwd", "fb_lconv_bwd",
 ]
 
 
@@ -119,6 +120,13 @@ def lib() -> C.CDLL:
         L.fb_shard_columns_from_signals.argtypes = [vp, vp, C.c_int, vp, i64, i64, i64, i64, i64, vp]
         L.fb_shard_columns_to_signals.argtypes = [vp, vp, vp, C.c_int, vp, vp, i64, i64, i64, i64, i64, vp]
         L.fb_shard_stage.argtypes = [vp, vp, i64, i64, i64, C.c_int, C.c_int, vp]
+        L.fb_lconv_plan_create.argtypes = [C.POINTER(vp), i64, i64, i64, C.c_int, C.c_int]
+        L.fb_lconv_plan_destroy.argtypes = [vp]
+        L.fb_lconv_plan_dims.argtypes = [vp, C.POINTER(i64), C.POINTER(i64)]
+        L.fb_lconv_workspace_size.argtypes = [vp, i64]
+        L.fb_lconv_workspace_size.restype = sz
+        L.fb_lconv_fwd.argtypes = [vp] * 7 + [i64, vp, vp]
+        L.fb_lconv_bwd.argtypes = [vp] * 12 + [i64, vp, vp]
         L.fb_init_kernels.argtypes = [C.c_int, i64, i64, C.c_uint64, vp, vp, vp, vp, C.c_int, vp]
         L.fb_last_error.restype = C.c_char_p
         _lib = L

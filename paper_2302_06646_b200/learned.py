@@ -135,3 +135,93 @@ class _LearnedFn(torch.autograd.Function):
 def learned_butterfly(x: torch.Tensor, blocks: torch.Tensor, r: int = 16) -> torch.Tensor:
     """y[b, h] = LearnedButterfly_h(x[b, h]) with trainable blocks [H, P]."""
     return _LearnedFn.apply(x, blocks, r)
+
+
+class LearnedLongConvPlan:
+    """The learned-butterfly long convolution: FlashButterfly
+    with the Butterfly matrices of its transform learned (fb_lconv_* in
+    libflashbutterfly.so).  Per head h:
+        y = Re IL(Wi[h], L(Wf[h], pad u) * L(Wf[h], pad Kbar[h]))[:N] + D[h] u
+    with L = learned_forward over build_plan(n, r) and IL(W, z) =
+    conj(L(W, conj z)) / n; n = 2N causal, N circular.  fp32 signals
+    [B, H, N]; blocks Wf, Wi [H, P] complex64.  dft_blocks() initialises both
+    to the DFT, where the operator equals regularized_long_conv."""
+
+    def __init__(self, N: int, H: int, r: int = 16, mode=1, device=None):
+        dev = torch.device("cuda", torch.cuda.current_device()) if device is None else torch.device(device)
+        self.N, self.H, self.r, self.mode, self.device = int(N), int(H), int(r), int(mode), dev
+        h = C.c_void_p()
+        check(_lib.lib().fb_lconv_plan_create(C.byref(h), self.N, self.H, self.r, self.mode, dev.index or 0))
+        self._h = h
+        n, pc = C.c_int64(), C.c_int64()
+        check(_lib.lib().fb_lconv_plan_dims(h, C.byref(n), C.byref(pc)))
+        self.n, self.param_count = int(n.value), int(pc.value)
+        self._lb = LearnedButterflyPlan(self.n, self.r, self.H, torch.complex64, dev)
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h is not None and h.value:
+            try:
+                _lib.lib().fb_lconv_plan_destroy(h)
+            except Exception:
+                pass
+            self._h = None
+
+    def dft_blocks(self) -> torch.Tensor:
+        return self._lb.dft_blocks()
+
+    def _ws(self, B):
+        return torch.empty(max(int(_lib.lib().fb_lconv_workspace_size(self._h, B)), 1), dtype=torch.uint8,
+                           device=self.device)
+
+    def _check(self, u):
+        if u.dim() != 3 or u.shape[1:] != (self.H, self.N):
+            raise DimensionError(_lib.FB_ERR_DIM, f"learned conv: expected [B, {self.H}, {self.N}]")
+        return u.shape[0]
+
+    @staticmethod
+    def _f(t, dt=torch.float32):
+        return t.detach().to(dtype=dt).contiguous()
+
+    def forward(self, u, kbar, D, Wf, Wi):
+        B = self._check(u)
+        u, kbar, D = self._f(u), self._f(kbar), self._f(D)
+        Wf, Wi = self._f(Wf, torch.complex64), self._f(Wi, torch.complex64)
+        y = torch.empty_like(u)
+        check(_lib.lib().fb_lconv_fwd(self._h, _ptr(u), _ptr(kbar), _ptr(D), _ptr(Wf), _ptr(Wi), _ptr(y), B,
+                                      _ptr(self._ws(B)), _stream(self.device)))
+        return y
+
+    def backward(self, dy, u, kbar, D, Wf, Wi):
+        """-> (du, dKbar, dD, dWf, dWi)."""
+        B = self._check(u)
+        dy, u, kbar, D = self._f(dy), self._f(u), self._f(kbar), self._f(D)
+        Wf, Wi = self._f(Wf, torch.complex64), self._f(Wi, torch.complex64)
+        du, dk, dD = torch.empty_like(u), torch.empty_like(kbar), torch.empty_like(D)
+        dWf, dWi = torch.empty_like(Wf), torch.empty_like(Wi)
+        check(_lib.lib().fb_lconv_bwd(self._h, _ptr(dy), _ptr(u), _ptr(kbar), _ptr(D), _ptr(Wf), _ptr(Wi),
+                                      _ptr(du), _ptr(dk), _ptr(dD), _ptr(dWf), _ptr(dWi), B, _ptr(self._ws(B)),
+                                      _stream(self.device)))
+        return du, dk, dD, dWf, dWi
+
+
+class _LearnedConvFn(torch.autograd.Function):
+    @staticmethod
+    def forward(ctx, u, kbar, D, Wf, Wi, plan):
+        ctx.save_for_backward(u, kbar, D, Wf, Wi)
+        ctx.plan = plan
+        return plan.forward(u, kbar, D, Wf, Wi)
+
+    @staticmethod
+    def backward(ctx, dy):
+        u, kbar, D, Wf, Wi = ctx.saved_tensors
+        du, dk, dD, dWf, dWi = ctx.plan.backward(dy, u, kbar, D, Wf, Wi)
+        return du, dk, dD, dWf.to(Wf.dtype), dWi.to(Wi.dtype), None
+
+
+def learned_long_conv(u, kbar, D, Wf, Wi, r: int = 16, mode: int = 1):
+    """Differentiable learned-butterfly long convolution (see LearnedLongConvPlan)."""
+    key = ("lconv", u.shape[2], u.shape[1], r, mode, str(u.device))
+    if key not in _PLANS:
+        _PLANS[key] = LearnedLongConvPlan(u.shape[2], u.shape[1], r, mode, u.device)
+    return _LearnedConvFn.apply(u, kbar, D, Wf, Wi, _PLANS[key])

@@ -126,3 +126,105 @@ def test_autograd():
     y.backward(up)
     db, dx = plan.gradients(blocks.detach(), x.detach(), up)
     assert torch.allclose(x.grad, dx) and torch.allclose(blocks.grad, db)
+
+
+# ------------------------------------------------------------ learned-butterfly long convolution
+def _lconv_oracle(lc, u, kbar, D, Wf, Wi, r, causal):
+    """fp64 composition of the reference's learned_forward / learned_gradients
+    (oracle rows): y = Re IL(Wi, L(Wf, pad u) L(Wf, pad k))[:N] + D u and its
+    backward for dy (IL(W, z) = conj(L(W, conj z)) / n)."""
+    B, H, N = u.shape
+    n = 2 * N if causal else N
+
+    def pad(x):
+        z = np.zeros(n, np.complex128)
+        z[:N] = x
+        return z
+    out = {}
+
+    def fwd(dy=None):
+        y = np.zeros((B, H, N))
+        du = np.zeros((B, H, N))
+        dk = np.zeros((H, N))
+        dD = np.zeros(H)
+        dWf = np.zeros_like(Wf)
+        dWi = np.zeros_like(Wi)
+        for h in range(H):
+            Kf = lc.learned_forward(Wf[h], pad(kbar[h]), r)
+            gK = np.zeros(n, np.complex128)
+            for b in range(B):
+                U = lc.learned_forward(Wf[h], pad(u[b, h]), r)
+                Zc = np.conj(U * Kf)
+                V = lc.learned_forward(Wi[h], Zc, r)
+                y[b, h] = V.real[:N] / n + D[h] * u[b, h]
+                if dy is None:
+                    continue
+                g = pad(dy[b, h]) / n
+                db, G = lc.learned_gradients(Wi[h], Zc, g, r)
+                dWi[h] += db
+                gZ = np.conj(G)
+                db, dX = lc.learned_gradients(Wf[h], pad(u[b, h]), gZ * np.conj(Kf), r)
+                dWf[h] += db
+                du[b, h] = dX.real[:N] + D[h] * dy[b, h]
+                gK += gZ * np.conj(U)
+                dD[h] += np.dot(dy[b, h], u[b, h])
+            if dy is not None:
+                db, dXk = lc.learned_gradients(Wf[h], pad(kbar[h]), gK, r)
+                dWf[h] += db
+                dk[h] = dXk.real[:N]
+        return y, du, dk, dD, dWf, dWi
+    return fwd
+
+
+@pytest.mark.parametrize("B,H,N,r,causal", [(2, 2, 64, 4, True), (3, 1, 96, 16, False), (2, 3, 512, 16, True)])
+def test_learned_long_conv(lc, B, H, N, r, causal):
+    """The learned-butterfly long convolution on the device
+    vs the fp64 composition of the reference's learned operator: y, du, dKbar,
+    dD and both block gradients, with perturbed (non-DFT) blocks; and at the DFT
+    initialisation it is the regular layer."""
+    rng = np.random.default_rng(B * 100 + N)
+    plan = fb.LearnedLongConvPlan(N, H, r, 1 if causal else 0)
+    W0 = plan.dft_blocks().cpu().numpy().astype(np.complex128)
+    P = W0.shape[1]
+    Wf = W0 + 0.1 * (rng.standard_normal((H, P)) + 1j * rng.standard_normal((H, P)))
+    Wi = W0 + 0.1 * (rng.standard_normal((H, P)) + 1j * rng.standard_normal((H, P)))
+    u = rng.standard_normal((B, H, N)).astype(np.float32).astype(np.float64)
+    dy = rng.standard_normal((B, H, N)).astype(np.float32).astype(np.float64)
+    kbar = (rng.standard_normal((H, N)) * np.exp(-np.arange(N) / 30.0)).astype(np.float32).astype(np.float64)
+    D = rng.standard_normal(H).astype(np.float32).astype(np.float64)
+    Wf = Wf.astype(np.complex64).astype(np.complex128)
+    Wi = Wi.astype(np.complex64).astype(np.complex128)
+    t = lambda a, dt=torch.float32: torch.tensor(a, dtype=dt).cuda()  # noqa: E731
+    y = plan.forward(t(u), t(kbar), t(D), t(Wf, torch.complex64), t(Wi, torch.complex64))
+    du, dk, dD, dWf, dWi = plan.backward(t(dy), t(u), t(kbar), t(D), t(Wf, torch.complex64),
+                                         t(Wi, torch.complex64))
+    torch.cuda.synchronize()
+    yw, duw, dkw, dDw, dWfw, dWiw = _lconv_oracle(lc, u, kbar, D, Wf, Wi, r, causal)(dy)
+    got = dict(y=y, du=du, dk=dk, dD=dD, dWf=dWf, dWi=dWi)
+    want = dict(y=yw, du=duw, dk=dkw, dD=dDw, dWf=dWfw, dWi=dWiw)
+    errs = {k: rel_l2(got[k].cpu().numpy().astype(np.complex128 if k.startswith("dW") else np.float64), want[k])
+            for k in got}
+    assert all(e < 1e-5 for e in errs.values()), errs
+    # DFT blocks: the layer itself (regularized_long_conv with Kbar, D)
+    y0 = plan.forward(t(u), t(kbar), t(D), t(W0, torch.complex64), t(W0, torch.complex64))
+    want0 = lc.long_conv_forward(u, kbar, D, causal)
+    assert rel_l2(y0.cpu().numpy(), want0) < 1e-5
+
+
+def test_learned_long_conv_autograd():
+    """torch.autograd through fb.learned_long_conv matches the plan's backward."""
+    B, H, N, r = 2, 2, 64, 4
+    plan = fb.LearnedLongConvPlan(N, H, r)
+    W0 = plan.dft_blocks()
+    g = torch.Generator(device="cuda").manual_seed(3)
+    u = torch.randn(B, H, N, device="cuda", generator=g, requires_grad=True)
+    kb = torch.randn(H, N, device="cuda", generator=g, requires_grad=True)
+    D = torch.randn(H, device="cuda", generator=g, requires_grad=True)
+    Wf = (W0 + 0.05 * torch.randn(W0.shape, dtype=torch.complex64, device="cuda", generator=g)).requires_grad_()
+    Wi = (W0 + 0.05 * torch.randn(W0.shape, dtype=torch.complex64, device="cuda", generator=g)).requires_grad_()
+    y = fb.learned_long_conv(u, kb, D, Wf, Wi, r)
+    dy = torch.randn_like(y)
+    (y * dy).sum().backward()
+    du, dk, dD, dWf, dWi = plan.backward(dy, u, kb, D, Wf, Wi)
+    for a, b in ((u.grad, du), (kb.grad, dk), (D.grad, dD), (Wf.grad, dWf), (Wi.grad, dWi)):
+        assert torch.allclose(a, b, rtol=1e-5, atol=1e-6)
