@@ -102,12 +102,14 @@ __global__ void __launch_bounds__(FftShape<LOG2N>::T, 2)
     for (uint32_t t = j; t < N; t += S::T) kd[t] = dropped(K, keep, keep_scale, base + t);
     __syncthreads();
     const double inv_w = 1.0 / (double)(2 * p + 1);
+    const int pp = (int)p, Ni = (int)N;  // N <= 4096 here: 32-bit index math
 #pragma unroll 1
     for (uint32_t t = j; t < N; t += S::T) {
-      const int64_t lo = (int64_t)t >= p ? (int64_t)t - p : 0;
-      const int64_t hi = ((int64_t)t + p < (int64_t)N - 1) ? (int64_t)t + p : (int64_t)N - 1;
+      const int ti = (int)t;
+      const int lo = ti >= pp ? ti - pp : 0;
+      const int hi = (ti + pp < Ni - 1) ? ti + pp : Ni - 1;
       double acc = 0.0;
-      for (int64_t q = lo; q <= hi; ++q) acc += kd[q];
+      for (int q = lo; q <= hi; ++q) acc += kd[q];
       const double sv = acc * inv_w;
       const double mag = fabs(sv) - lambda;
       const float kv = mag > 0.0 ? (float)copysign(mag, sv) : 0.0f;

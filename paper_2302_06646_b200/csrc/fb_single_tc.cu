@@ -1168,38 +1168,63 @@ __global__ void __launch_bounds__(512)
                       float* __restrict__ dD, const float* __restrict__ kbar,
                       const uint8_t* __restrict__ keep, float* __restrict__ dK, int64_t p,
                       double keep_scale, int freq, int ctas, int total, int npairs, int maxseg) {
-  constexpr uint32_t N = 4096;
+  constexpr uint32_t N = 4096, kPer = 8;  // 512 threads x 8 consecutive lags
   __shared__ float row[N];
+  __shared__ const float* src[8];
   const int h = blockIdx.x;
   const int64_t G = ctas, T = total, np = npairs;
   const int64_t U = (T + 1) / 2;
   // the CTA owning pair i under the backward's even-aligned shares
   auto owner = [&](int64_t i) { return (int)((((i / 2) + 1) * G - 1) / U); };
   const int c0 = owner((int64_t)h * np), c1 = owner(((int64_t)h + 1) * np - 1);
+  const int nc = c1 - c0 + 1;
+  auto part = [&](int c) {  // CTA c's partial row of head h (segment h - its first head)
+    const int64_t start = 2 * ((int64_t)c * U / G);
+    return tpart + ((size_t)c * maxseg + (h - (int)(start / np))) * N;
+  };
+  if (threadIdx.x < (unsigned)min(nc, 8)) src[threadIdx.x] = part(c0 + (int)threadIdx.x);
+  __syncthreads();
   const size_t base = (size_t)h * N;
-  for (uint32_t t = threadIdx.x; t < N; t += blockDim.x) {
-    float g = 0.f;
-    for (int c = c0; c <= c1; ++c) {
-      const int64_t start = 2 * ((int64_t)c * U / G);
-      const int sg = h - (int)(start / np);
-      g += __ldg(tpart + ((size_t)c * maxseg + sg) * N + t);
-    }
-    if (dkbar_out) dkbar_out[base + t] = g;
-    if (t == 0) dD[h] = g;
-    row[t] = (!freq && __ldg(kbar + base + t) == 0.f) ? 0.f : g;
+  const uint32_t t0 = threadIdx.x * kPer;
+  // sum the partials in CTA order (deterministic), 16-byte loads
+  float4 g0 = make_float4(0.f, 0.f, 0.f, 0.f), g1 = g0;
+  for (int c = 0; c < nc; ++c) {
+    const float4* sp = reinterpret_cast<const float4*>((c < 8 ? src[c] : part(c0 + c)) + t0);
+    const float4 a = __ldg(sp), b = __ldg(sp + 1);
+    g0.x += a.x; g0.y += a.y; g0.z += a.z; g0.w += a.w;
+    g1.x += b.x; g1.y += b.y; g1.z += b.z; g1.w += b.w;
+  }
+  if (dkbar_out) {
+    reinterpret_cast<float4*>(dkbar_out + base + t0)[0] = g0;
+    reinterpret_cast<float4*>(dkbar_out + base + t0)[1] = g1;
+  }
+  if (threadIdx.x == 0) dD[h] = g0.x;
+  const float g[kPer] = {g0.x, g0.y, g0.z, g0.w, g1.x, g1.y, g1.z, g1.w};
+  {
+    const float4 k0 = __ldg(reinterpret_cast<const float4*>(kbar + base + t0));
+    const float4 k1 = __ldg(reinterpret_cast<const float4*>(kbar + base + t0) + 1);
+    const float kb[kPer] = {k0.x, k0.y, k0.z, k0.w, k1.x, k1.y, k1.z, k1.w};
+#pragma unroll
+    for (uint32_t j = 0; j < kPer; ++j) row[t0 + j] = (!freq && kb[j] == 0.f) ? 0.f : g[j];
   }
   __syncthreads();
   if (!freq) {
     const double w = (double)(2 * p + 1);
-    for (uint32_t t = threadIdx.x; t < N; t += blockDim.x) {
-      const int64_t lo = (int64_t)t >= p ? (int64_t)t - p : 0;
-      const int64_t hi = ((int64_t)t + p < (int64_t)N - 1) ? (int64_t)t + p : (int64_t)N - 1;
+    const int pp = (int)p;
+    float o[kPer];
+#pragma unroll
+    for (uint32_t j = 0; j < kPer; ++j) {
+      const int t = (int)(t0 + j);
+      const int lo = t >= pp ? t - pp : 0;
+      const int hi = (t + pp < (int)N - 1) ? t + pp : (int)N - 1;
       double acc = 0.0;
-      for (int64_t q = lo; q <= hi; ++q) acc += (double)row[q];
-      double g = acc / w;
-      if (keep) g = keep[base + t] ? g * keep_scale : 0.0;
-      dK[base + t] = (float)g;
+      for (int q = lo; q <= hi; ++q) acc += (double)row[q];
+      double gg = acc / w;
+      if (keep) gg = keep[base + t] ? gg * keep_scale : 0.0;
+      o[j] = (float)gg;
     }
+    reinterpret_cast<float4*>(dK + base + t0)[0] = make_float4(o[0], o[1], o[2], o[3]);
+    reinterpret_cast<float4*>(dK + base + t0)[1] = make_float4(o[4], o[5], o[6], o[7]);
   } else {
     for (uint32_t t = threadIdx.x; t < N; t += blockDim.x)
       dK[base + t] = reg_grad(kbar + base, row, keep ? keep + base : nullptr, t, N, p, keep_scale,
