@@ -220,6 +220,12 @@ template <> struct Lg2<8> { static constexpr int v = 3; };
 template <> struct Lg2<16> { static constexpr int v = 4; };
 
 // column `col` of R rows under stage geometry (lgL, F): element offset of p = 0
+// Stage buffers are padded by one float2 per 32 (element e at px(e)): the
+// butterfly's power-of-two strides would otherwise put a warp's accesses in
+// a few banks (measured 7x bank conflicts on the config-4 forward).
+__host__ __device__ __forceinline__ int px(int e) { return e + (e >> 5); }
+// a padded buffer of e elements, rounded to 16 bytes (cp.async destinations)
+__host__ __device__ __forceinline__ int pxbuf(int e) { return (px(e) + 2) & ~1; }
 __device__ __forceinline__ int lx_base(int col, int lgcpr, int lgrest, int lgL, int lgn) {
   const int r = col >> lgcpr, cc = col & ((1 << lgcpr) - 1);
   return (r << lgn) + ((cc >> lgrest) << lgL) + (cc & ((1 << lgrest) - 1));
@@ -258,7 +264,7 @@ __device__ __forceinline__ void lx_fwd_stage(const float2* __restrict__ src, flo
     const int ts = (col & ((1 << lgrest) - 1)) << (lgn - lgL);  // q n / L
     float2 x[F];
 #pragma unroll
-    for (int p = 0; p < F; ++p) x[p] = src[base + (p << lgrest)];
+    for (int p = 0; p < F; ++p) x[p] = src[px(base + (p << lgrest))];
     // one output row at a time: the W row is a broadcast load (all lanes read
     // the same entry), so a full unroll would only hoist F^2 registers
 #pragma unroll 1
@@ -273,7 +279,7 @@ __device__ __forceinline__ void lx_fwd_stage(const float2* __restrict__ src, flo
         ar = fmaf(w2.z, x[p + 1].x, fmaf(-w2.w, x[p + 1].y, ar));
         ai = fmaf(w2.z, x[p + 1].y, fmaf(w2.w, x[p + 1].x, ai));
       }
-      dst[base + (a << lgrest)] = cmul(make_float2(ar, ai), tw[a * ts]);
+      dst[px(base + (a << lgrest))] = cmul(make_float2(ar, ai), tw[px(a * ts)]);
     }
   }
 }
@@ -296,7 +302,7 @@ __device__ __forceinline__ void lx_adj_stage(const float2* __restrict__ w, float
     const int base = lx_base(col, lgcpr, lgrest, lgL, lgn);
     float2 v[F];
 #pragma unroll
-    for (int a = 0; a < F; ++a) v[a] = w[base + (a << lgrest)];
+    for (int a = 0; a < F; ++a) v[a] = w[px(base + (a << lgrest))];
 #pragma unroll 1
     for (int p = part * per; p < (part + 1) * per; ++p) {
       float ar = 0.f, ai = 0.f;
@@ -314,9 +320,9 @@ __device__ __forceinline__ void lx_adj_stage(const float2* __restrict__ w, float
       if (plgL >= 0) {
         const int loc = idx & ((1 << plgL) - 1);
         const int pa = loc >> plgrest, pq = loc & ((1 << plgrest) - 1);
-        o = cmulc(o, tw[(pa * pq) << (lgn - plgL)]);
+        o = cmulc(o, tw[px((pa * pq) << (lgn - plgL))]);
       }
-      gout[idx] = o;
+      gout[px(idx)] = o;
     }
   }
 }
@@ -343,8 +349,8 @@ __device__ __forceinline__ void lx_grad(const float2* __restrict__ w, const floa
     float2 wv[TS], vv[TS];
 #pragma unroll
     for (int i = 0; i < TS; ++i) {
-      wv[i] = w[base + ((a0 + i) << lgrest)];
-      vv[i] = v[base + ((p0 + i) << lgrest)];
+      wv[i] = w[px(base + ((a0 + i) << lgrest))];
+      vv[i] = v[px(base + ((p0 + i) << lgrest))];
     }
 #pragma unroll
     for (int i = 0; i < TS; ++i)
@@ -444,8 +450,8 @@ __device__ __forceinline__ void lx_stage_mma16(const float2* __restrict__ src, f
   const int plgrest = plgL - plgf;
   for (int nt = warp; nt * 8 < C; nt += kLxThreads / 32) {
     const int base = lx_base(nt * 8 + g, lgcpr, lgrest, lgL, lgn);
-    const float2 x0 = src[base + ((2 * tig) << lgrest)], x1 = src[base + ((2 * tig + 1) << lgrest)];
-    const float2 x2 = src[base + ((2 * tig + 8) << lgrest)], x3 = src[base + ((2 * tig + 9) << lgrest)];
+    const float2 x0 = src[px(base + ((2 * tig) << lgrest))], x1 = src[px(base + ((2 * tig + 1) << lgrest))];
+    const float2 x2 = src[px(base + ((2 * tig + 8) << lgrest))], x3 = src[px(base + ((2 * tig + 9) << lgrest))];
     const uint32_t br0 = pk_bf16(x0.x, x1.x), br1 = pk_bf16(x2.x, x3.x);
     const uint32_t bi0 = pk_bf16(x0.y, x1.y), bi1 = pk_bf16(x2.y, x3.y);
     float d[2][4] = {{0.f, 0.f, 0.f, 0.f}, {0.f, 0.f, 0.f, 0.f}};
@@ -464,11 +470,11 @@ __device__ __forceinline__ void lx_stage_mma16(const float2* __restrict__ src, f
       idx[e] = lx_base(cn, lgcpr, lgrest, lgL, lgn) + (o << lgrest);
       if (!ADJ) {
         const int q = cn & ((1 << lgrest) - 1);
-        t[e] = tw[o * (q << (lgn - lgL))];
+        t[e] = tw[px(o * (q << (lgn - lgL)))];
       } else if (plgL >= 0) {
         const int loc = idx[e] & ((1 << plgL) - 1);
         const int pa = loc >> plgrest, pq = loc & ((1 << plgrest) - 1);
-        t[e] = tw[(pa * pq) << (lgn - plgL)];
+        t[e] = tw[px((pa * pq) << (lgn - plgL))];
       } else {
         t[e] = make_float2(1.f, 0.f);
       }
@@ -476,7 +482,7 @@ __device__ __forceinline__ void lx_stage_mma16(const float2* __restrict__ src, f
 #pragma unroll
     for (int e = 0; e < 4; ++e) {
       const float2 y = make_float2(d[0][e], d[1][e]);
-      dst[idx[e]] = ADJ ? cmulc(y, t[e]) : cmul(y, t[e]);
+      dst[px(idx[e])] = ADJ ? cmulc(y, t[e]) : cmul(y, t[e]);
     }
   }
 }
@@ -507,8 +513,8 @@ __device__ __forceinline__ void lx_grad_mma16(const float2* __restrict__ w, cons
     for (int h8 = 0; h8 < 2; ++h8)
 #pragma unroll
       for (int r = 0; r < 4; ++r) {
-        wv[h8][r] = w[cb[r] + ((g + 8 * h8) << lgrest)];
-        vv[h8][r] = v[cb[r] + ((g + 8 * h8) << lgrest)];
+        wv[h8][r] = w[px(cb[r] + ((g + 8 * h8) << lgrest))];
+        vv[h8][r] = v[px(cb[r] + ((g + 8 * h8) << lgrest))];
       }
     uint32_t a[2][4];  // [re/im][reg]: reg = (row g / g+8) x (k lo / hi)
 #pragma unroll
@@ -568,15 +574,15 @@ __global__ void __launch_bounds__(kLxThreads)
   const int n = 1 << geo.lgn;
   float2* W = lsm;
   float2* tw = W + P;
-  float2* bufA = tw + n;
-  float2* bufB = bufA + (size_t)R * n;
+  float2* bufA = tw + pxbuf(n);
+  float2* bufB = bufA + pxbuf(R * n);
   const int h = blockIdx.x;
   const float2* wg = reinterpret_cast<const float2*>(blocks) + (size_t)h * P;
   const int b0 = blockIdx.y * R, rows = min(R, B - b0);
   // blocks, twiddles and the raw rows (staged in bufB) all in flight at once
   IO* raw = reinterpret_cast<IO*>(bufB);
   cp_async_bytes(W, wg, (size_t)P * sizeof(float2));
-  cp_async_bytes(tw, tw_g, (size_t)n * sizeof(float2));
+  for (int i = threadIdx.x; i < n; i += kLxThreads) tw[px(i)] = __ldg(tw_g + i);  // padded twiddle table
   for (int r = 0; r < rows; ++r)
     cp_async_bytes(raw + (size_t)r * 2 * n, x + ((size_t)(b0 + r) * H + h) * 2 * n,
                    2 * (size_t)n * sizeof(IO));
@@ -584,7 +590,7 @@ __global__ void __launch_bounds__(kLxThreads)
   __syncthreads();
   for (int i = threadIdx.x; i < R * n; i += kLxThreads) {
     const int r = i >> geo.lgn;
-    bufA[i] = r < rows ? ldc_any<IO>(raw + 2 * (size_t)i) : make_float2(0.f, 0.f);
+    bufA[px(i)] = r < rows ? ldc_any<IO>(raw + 2 * (size_t)i) : make_float2(0.f, 0.f);
   }
   __syncthreads();
   float2 *s = bufA, *d = bufB;
@@ -600,7 +606,7 @@ __global__ void __launch_bounds__(kLxThreads)
   }
   for (int i = threadIdx.x; i < rows * n; i += kLxThreads) {
     const int r = i >> geo.lgn, e = i & (n - 1);
-    stc<IO>(y + ((size_t)(b0 + r) * H + h) * 2 * n + 2 * e, s[(r << geo.lgn) + __ldg(omap + e)]);
+    stc<IO>(y + ((size_t)(b0 + r) * H + h) * 2 * n + 2 * e, s[px((r << geo.lgn) + (int)__ldg(omap + e))]);
   }
 }
 
@@ -619,13 +625,14 @@ __global__ void __launch_bounds__(kLxThreads)
   float2* WT = W + P;  // per stage block transposed (the adjoint's rows)
   float2* G = WT + P;
   float2* tw = G + P;
-  float2* v = tw + n;  // [S][R n] stage inputs
-  float2* ga = v + (size_t)S * R * n;
-  float2* gb = ga + (size_t)R * n;
+  const int RNP = pxbuf(R * n);  // one padded stage buffer
+  float2* v = tw + pxbuf(n);  // [S][RNP] stage inputs
+  float2* ga = v + (size_t)S * RNP;
+  float2* gb = ga + RNP;
   const int h = blockIdx.x;
   const float2* wg = reinterpret_cast<const float2*>(blocks) + (size_t)h * P;
   cp_async_bytes(W, wg, (size_t)P * sizeof(float2));
-  cp_async_bytes(tw, tw_g, (size_t)n * sizeof(float2));
+  for (int i = threadIdx.x; i < n; i += kLxThreads) tw[px(i)] = __ldg(tw_g + i);  // padded twiddle table
   cp_async_wait_all();
   __syncthreads();
   for (int i = threadIdx.x; i < P; i += kLxThreads) G[i] = make_float2(0.f, 0.f);
@@ -652,23 +659,23 @@ __global__ void __launch_bounds__(kLxThreads)
         const int r = i >> geo.lgn, e = i & (n - 1);
         const float2 val = r < rows ? ldc_any<IO>(raw + 2 * (size_t)i) : make_float2(0.f, 0.f);
         if (phase == 0) {
-          v[i] = val;
+          v[px(i)] = val;
         } else {
           // adjoint of the output permutation, then the top stage's conj twiddle
           const int idx = __ldg(omap + e);
           const int loc = idx & ((1 << lgLt) - 1), lgr = lgLt - lgft;
           const int pa = loc >> lgr, pq = loc & ((1 << lgr) - 1);
-          ga[(r << geo.lgn) + idx] = cmulc(val, tw[(pa * pq) << (geo.lgn - lgLt)]);
+          ga[px((r << geo.lgn) + idx)] = cmulc(val, tw[px((pa * pq) << (geo.lgn - lgLt))]);
         }
       }
       __syncthreads();
     }
     for (int k = 0; k + 1 < S; ++k) {
       if (kTc<IO> && geo.lgf[k] == 4)
-        lx_stage_mma16<false>(v + (size_t)k * R * n, v + (size_t)(k + 1) * R * n, W + geo.off[k],
+        lx_stage_mma16<false>(v + (size_t)k * RNP, v + (size_t)(k + 1) * RNP, W + geo.off[k],
                               geo.lgL[k], geo.lgn, R, tw, -1, 0);
       else
-      LX_DISPATCH(geo.lgf[k], (lx_fwd_stage<F>(v + (size_t)k * R * n, v + (size_t)(k + 1) * R * n,
+      LX_DISPATCH(geo.lgf[k], (lx_fwd_stage<F>(v + (size_t)k * RNP, v + (size_t)(k + 1) * RNP,
                                                W + geo.off[k], geo.lgL[k], geo.lgn, R, tw)));
       __syncthreads();
     }
@@ -676,9 +683,9 @@ __global__ void __launch_bounds__(kLxThreads)
       // gb is free until the adjoint pass: it holds the gradient pass's
       // per-warp partials (R n >= 8 f^2 is a condition of the fast path)
       if (kTc<IO> && geo.lgf[k] == 4)
-        lx_grad_mma16(ga, v + (size_t)k * R * n, G + geo.off[k], gb, geo.lgL[k], geo.lgn, R);
+        lx_grad_mma16(ga, v + (size_t)k * RNP, G + geo.off[k], gb, geo.lgL[k], geo.lgn, R);
       else
-      LX_DISPATCH(geo.lgf[k], (lx_grad<F>(ga, v + (size_t)k * R * n, G + geo.off[k], gb, geo.lgL[k],
+      LX_DISPATCH(geo.lgf[k], (lx_grad<F>(ga, v + (size_t)k * RNP, G + geo.off[k], gb, geo.lgL[k],
                                           geo.lgn, R)));
       const int plgL = k > 0 ? geo.lgL[k - 1] : -1, plgf = k > 0 ? geo.lgf[k - 1] : 0;
       if (kTc<IO> && geo.lgf[k] == 4)
@@ -693,7 +700,7 @@ __global__ void __launch_bounds__(kLxThreads)
     }
     for (int i = threadIdx.x; i < rows * n; i += kLxThreads) {
       const int r = i >> geo.lgn, e = i & (n - 1);
-      stc<IO>(dx + ((size_t)(b0 + r) * H + h) * 2 * n + 2 * e, ga[i]);
+      stc<IO>(dx + ((size_t)(b0 + r) * H + h) * 2 * n + 2 * e, ga[px(i)]);
     }
   }
   __syncthreads();
@@ -731,12 +738,17 @@ inline int64_t lx_maxf(const fb_learned_plan* p) {
   for (int i = 0; i < p->nstages; ++i) m = std::max(m, p->factors[i]);
   return m;
 }
-inline size_t lx_fwd_fixed(const fb_learned_plan* p) { return (p->param_count + p->n) * sizeof(float2); }
+// (stage buffers padded to pxbuf(R n) float2: n + n / 32 per row plus up to
+// two float2 per buffer, the latter counted in the fixed part)
+inline size_t lx_fwd_fixed(const fb_learned_plan* p) {
+  return (p->param_count + p->n + p->n / 32 + 6) * sizeof(float2);
+}
+inline size_t lx_fwd_per_row(const fb_learned_plan* p) { return 2 * (size_t)(p->n + p->n / 32) * sizeof(float2); }
 inline size_t lx_bwd_fixed(const fb_learned_plan* p) {
-  return (3 * p->param_count + p->n) * sizeof(float2);
+  return (3 * p->param_count + p->n + p->n / 32 + 2 + 2 * (p->nstages + 2)) * sizeof(float2);
 }
 inline size_t lx_bwd_per_row(const fb_learned_plan* p) {
-  return (size_t)(p->nstages + 2) * p->n * sizeof(float2);
+  return (size_t)(p->nstages + 2) * (p->n + p->n / 32) * sizeof(float2);
 }
 
 }  // namespace fb
@@ -962,11 +974,11 @@ int fb_learned_fwd(fb_learned_plan* p, const float* blocks, const void* x, void*
   if (ext->dev.fast) {
     // small CTAs (four per SM): the stage chain is latency-bound, so more
     // independent CTAs per SM beat wider ones
-    const int R = lx_rows(lx_fwd_fixed(p), 2 * p->n * sizeof(float2), 56 * 1024) > 0
-                      ? lx_rows(lx_fwd_fixed(p), 2 * p->n * sizeof(float2), 56 * 1024)
-                      : lx_rows(lx_fwd_fixed(p), 2 * p->n * sizeof(float2), 227 * 1024);
+    const int R = lx_rows(lx_fwd_fixed(p), lx_fwd_per_row(p), 56 * 1024) > 0
+                      ? lx_rows(lx_fwd_fixed(p), lx_fwd_per_row(p), 56 * 1024)
+                      : lx_rows(lx_fwd_fixed(p), lx_fwd_per_row(p), 227 * 1024);
     if (R > 0) {
-      const size_t sm = lx_fwd_fixed(p) + 2 * (size_t)R * p->n * sizeof(float2);
+      const size_t sm = lx_fwd_fixed(p) + lx_fwd_per_row(p) * R;
       const dim3 g((unsigned)p->H, (unsigned)((B + R - 1) / R));
       auto go = [&](auto io) {
         using IO = decltype(io);
