@@ -1039,6 +1039,18 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (j + 2 < L) load_pair(sm + c.in_off, SAVED ? &dymap : &umap, h, b0 + 4, in_bar);
       });
       // ---- S += conj(U) DY (in pair order), Z = DY conj(k_f') -> B' operand
+      // this thread's U values (L2: prefetched at the pair start), software-
+      // pipelined one column chunk ahead: the first chunk's loads are in
+      // flight across the chain wait, each later one across the previous
+      // chunk's math, instead of one exposed L2 round trip per chunk
+      uint4 ua_n, ub_n;
+      {
+        uint32_t f2u, gu;
+        coords(f2u, gu);
+        const uint4* us = reinterpret_cast<const uint4*>(up + usave_idx(kColsPer * gu, f2u));
+        ua_n = __ldcg(us);
+        ub_n = __ldcg(us + 128);
+      }
       if (j > 0) {
         const uint32_t idx = slot ? base0 + (uint32_t)k : base1 + (uint32_t)k - 1;
         TT_BEGIN ptx::mbar_wait(chain_other, idx & 1); TT_END(24)
@@ -1052,9 +1064,13 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (uint32_t q = 0; q < kColsPer / 8; ++q) {
           const uint32_t col = kColsPer * g + 8 * q;
           float dr[8], di[8], sr[8], si[8];
-          const uint4* us = reinterpret_cast<const uint4*>(up + usave_idx(col, f2));
-          // L2 loads (.cg): the recompute path wrote U moments ago in this kernel
-          const uint4 ua = __ldcg(us), ub = __ldcg(us + 128);
+          // (L2 loads, .cg: the recompute path wrote U moments ago in this kernel)
+          const uint4 ua = ua_n, ub = ub_n;
+          if (q + 1 < kColsPer / 8) {
+            const uint4* us = reinterpret_cast<const uint4*>(up + usave_idx(col + 8, f2));
+            ua_n = __ldcg(us);
+            ub_n = __ldcg(us + 128);
+          }
           const uint32_t pk[8] = {ua.x, ua.y, ua.z, ua.w, ub.x, ub.y, ub.z, ub.w};
           tld<8>(taddr(c, c.tw + col), dr);
           tld<8>(taddr(c, c.tw + 64 + col), di);
