@@ -21,7 +21,7 @@ CUDA_HOME = Path(os.environ.get("CUDA_HOME", "/usr/local/cuda"))
 INCLUDE = PKG.parent / "include"
 
 SOURCES = ["fb_capi.cu", "fb_prep.cu", "fb_single.cu", "fb_single_tc.cu", "fb_tc2.cu",
-           "fb_three.cu", "fb_learned.cu", "fb_dft.cu", "fb_shard.cu", "fb_lconv.cu"]
+           "fb_three.cu", "fb_learned.cu", "fb_learned_tc.cu", "fb_dft.cu", "fb_shard.cu", "fb_lconv.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVCC_FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "--expt-relaxed-constexpr",
               "-Xptxas", "-warn-spills"]

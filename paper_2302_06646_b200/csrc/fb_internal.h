@@ -165,4 +165,12 @@ int lb_fwd(fb_learned_plan* p, const float* blocks, const void* x, void* y, int6
            cudaStream_t s);
 int lb_bwd(fb_learned_plan* p, const float* blocks, const void* x, const void* g, void* dx,
            float* dblocks, int64_t B, void* ws, cudaStream_t s);
+// learned butterfly on tcgen05 (fb_learned_tc.cu): chains [16] * stc + [2^lgfl]
+bool lt_config(int64_t n, const int64_t* f, int nst, int dtype, int* stc, int* lgfl);
+int lt_rows(int64_t n);
+cudaError_t lt_fwd(int stc, int lgfl, int dtype, const float* blocks, const void* x, void* y,
+                   const uint32_t* omap, const float2* tw, int B, int H, int P, cudaStream_t s);
+cudaError_t lt_bwd(int stc, int lgfl, int dtype, const float* blocks, const void* x, const void* g,
+                   void* dx, float2* gpart, const uint32_t* omap, const float2* tw, int B, int H,
+                   int P, cudaStream_t s);
 }  // namespace fb

@@ -723,6 +723,8 @@ struct LbDevice {
   LbStages st{};
   bool fast = false;  // power-of-two factors <= 16: the lx_* kernels
   LxGeo geo{};
+  bool tc = false;    // 16-bit modes, [16] * stc + [2^lgfl]: the tcgen05 lt_* kernels
+  int stc = 0, lgfl = 0;
 };
 
 // rows per pass for the fast kernels: the largest R in {4, 2, 1} whose smem
@@ -877,6 +879,7 @@ int fb_learned_plan_create(fb_learned_plan** out, int64_t n, int64_t r, int64_t 
       gg.off[i] = st.off[i];
     }
     ext->dev.fast = fast && n >= 2;
+    ext->dev.tc = lt_config(n, f.data(), (int)f.size(), dtype, &ext->dev.stc, &ext->dev.lgfl);
   }
   std::vector<uint32_t> om = output_map(n, f);
   std::vector<float2> tw((size_t)n);
@@ -940,6 +943,7 @@ static int lx_bwd_R(const fb_learned_plan* p) {
 // Row splits per head for the backward: enough CTAs to fill the SMs (a few
 // waves), each split a whole number of the fast kernel's R-row passes.
 static int lb_splits(const fb_learned_plan* p, int64_t B) {
+  if (ext_of(p)->dev.tc) return (int)((B + lt_rows(p->n) - 1) / lt_rows(p->n));
   int dev_sms = 148;
   cudaDeviceGetAttribute(&dev_sms, cudaDevAttrMultiProcessorCount, p->device);
   if (lx_fast_bwd(p)) {
@@ -971,6 +975,10 @@ int fb_learned_fwd(fb_learned_plan* p, const float* blocks, const void* x, void*
   if (rc) return rc;
   fb_learned_ext* ext = ext_of(p);
   cudaStream_t s = (cudaStream_t)stream;
+  if (ext->dev.tc)
+    return cuda_status(lt_fwd(ext->dev.stc, ext->dev.lgfl, p->dtype, blocks, x, y, ext->dev.omap,
+                              ext->dev.tw, (int)B, (int)p->H, (int)p->param_count, s),
+                       "fb_learned_fwd (tcgen05)");
   if (ext->dev.fast) {
     // small CTAs (four per SM): the stage chain is latency-bound, so more
     // independent CTAs per SM beat wider ones
@@ -1030,6 +1038,16 @@ int fb_learned_bwd(fb_learned_plan* p, const float* blocks, const void* x, const
     return FB_ERR_ARG;
   }
   const int splits = lb_splits(p, B);
+  if (ext->dev.tc) {
+    rc = cuda_status(lt_bwd(ext->dev.stc, ext->dev.lgfl, p->dtype, blocks, x, g, dx, (float2*)ws,
+                            ext->dev.omap, ext->dev.tw, (int)B, (int)p->H, (int)p->param_count, s),
+                     "fb_learned_bwd (tcgen05)");
+    if (rc) return rc;
+    const size_t HP = (size_t)p->H * p->param_count;
+    lb_reduce_kernel<<<(unsigned)((HP + 255) / 256), 256, 0, s>>>((const float2*)ws,
+                                                                 (float2*)dblocks, splits, HP);
+    return cuda_status(cudaGetLastError(), "fb_learned_bwd");
+  }
   if (lx_fast_bwd(p)) {
     const int R = lx_bwd_R(p);
     const int64_t passes = (B + R - 1) / R;

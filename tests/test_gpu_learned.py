@@ -115,6 +115,31 @@ def test_config4_shape_16bit(lc, dtype):
     assert rel_l2(db.cpu().numpy()[heads], rdb) < 2e-2
 
 
+@pytest.mark.parametrize("n,B", [(32, 5), (64, 3), (128, 2), (512, 9), (1024, 6), (2048, 3)])
+@pytest.mark.parametrize("dtype", [torch.bfloat16, torch.float16])
+def test_tensor_core_chains_16bit(lc, n, B, dtype):
+    """The tcgen05 kernels (fb_learned_tc.cu) own the 16-bit chains
+    [16] * S + [FL] (n = 32 .. 2048); B not a multiple of the CTA's
+    4096 / n rows, so the last row group is partial."""
+    H, r = 3, 16
+    blocks, x, g = batch_case(lc, B, H, n, r, seed=n + B)
+    plan = fb.LearnedButterflyPlan(n, r, H, dtype)
+    tb = cplx(blocks, blocks.shape)
+    tx = to16(cplx(x, x.shape), dtype)
+    tg = to16(cplx(g, g.shape), dtype)
+    y = from16(plan.forward(tb, tx))
+    db, dx = plan.gradients(tb, tx, tg)
+    dx = from16(dx)
+    heads = list(range(H))
+    ry, rdx, rdb = oracle_batch(lc, blocks, from16(tx), from16(tg), r, heads)
+    order = [(b, h) for h in heads for b in range(B)]
+    ey = rel_l2(np.array([y[b, h] for b, h in order]), ry)
+    edx = rel_l2(np.array([dx[b, h] for b, h in order]), rdx)
+    edb = rel_l2(db.cpu().numpy(), rdb)
+    print(f"n={n} B={B} {dtype}: y {ey:.2e} dx {edx:.2e} dblocks {edb:.2e}")
+    assert ey < 2e-2 and edx < 2e-2 and edb < 2e-2
+
+
 def test_autograd():
     n, H, B = 256, 2, 3
     plan = fb.LearnedButterflyPlan(n, 16, H)
