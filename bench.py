@@ -480,10 +480,12 @@ def run_learned(args, cfg, rank, world, local_rank):
         "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
         "data": "synthetic (randn rows, DFT-initialised blocks + 0.1 randn)",
         "config": {"workload": cfg["workload"], "B": B, "H": H, "n": n, "r": r,
-                   "factors": plan.factors, "params_per_head": plan.param_count,
+                   "factors": plan.factors, "params_per_head": plan.param_count, "engine": plan.engine,
                    "l2": "rows 100 MiB per tensor"},
         "fwd_ms": fwd_ms, "bwd_ms": bwd_ms,
-        "roofline": {"bound": "hbm", "kernel": "bwd: lx_bwd_kernel + lb_reduce_kernel",
+        "roofline": {"bound": "hbm", "kernel": ("bwd: lt_bwd_kernel (tcgen05) + lb_reduce_kernel"
+                                                if plan.engine == "tcgen05" else
+                                                "bwd: lx_bwd_kernel + lb_reduce_kernel"),
                      "achieved": 12 * E / (bwd_ms / 1e3) / 1e9,
                      "peak": hbm_peak, "unit": "GB/s",
                      "frac": 12 * E / (bwd_ms / 1e3) / 1e9 / hbm_peak,
@@ -564,8 +566,10 @@ def cpu_baseline(cfg, heads):
         threads = 1  # learned_forward / learned_gradients are single-threaded per row
     return {"value": el / sec, "unit": "elements/s", "cores": threads, "kind": "reference",
             "sample": f"B={cfg['B']} H={heads} (of {cfg['H']}) N={cfg['N']}, fp64, one step "
-                      f"in {sec:.1f}s: regularize_bank + regularized_long_conv(kButterfly) + "
-                      "composed conv_butterfly backward + regularizer chain rule"
+                      f"in {sec:.1f}s: "
+                      + ("learned_forward + learned_gradients per row" if cfg["engine"] == "learned"
+                         else "regularize_bank + regularized_long_conv(kButterfly) + "
+                              "composed conv_butterfly backward + regularizer chain rule")
                       + ("" if heads == cfg["H"] else "; a head sample (channels independent)"),
             "host": platform.processor() or platform.machine()}
 
@@ -586,7 +590,9 @@ def run_reference(args, cfg, rank):
     val = el / sec
     out = {
         "impl": "reference",
-        "metric": "long-conv fwd+bwd elements/sec (E=B*H*N per step: K1 prep + fwd + bwd)",
+        "metric": ("learned-butterfly fwd+bwd rows*n elements/sec (incl. block gradients)"
+                   if cfg["engine"] == "learned" else
+                   "long-conv fwd+bwd elements/sec (E=B*H*N per step: K1 prep + fwd + bwd)"),
         "value": val, "unit": "elements/s", "n_gpus": 1, "steps": args.steps,
         "warmup": min(args.warmup, 1), "ms_per_step": sec / args.steps * 1e3,
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",

@@ -24,7 +24,7 @@ FB_SMOOTH_TIME, FB_SMOOTH_FREQUENCY = 0, 1
 EXPORTED = [
     "fb_plan_create", "fb_plan_destroy", "fb_plan_get_info", "fb_kernel_prep", "fb_plan_copy_kbar",
     "fb_workspace_size", "fb_fwd", "fb_bwd", "fb_learned_plan_create", "fb_learned_plan_destroy",
-    "fb_learned_plan_factors", "fb_learned_workspace_size", "fb_learned_fwd", "fb_learned_bwd",
+    "fb_learned_plan_factors", "fb_learned_plan_engine", "fb_learned_workspace_size", "fb_learned_fwd", "fb_learned_bwd",
     "fb_last_error", "fb_version", "fb_host_runner_create", "fb_host_runner_destroy",
     "fb_host_runner_chunk_heads", "fb_host_runner_run", "fb_saved_size", "fb_fwd_save",
     "fb_bwd_saved", "fb_shard_plan_create", "fb_shard_plan_destroy", "fb_shard_plan_dims",
@@ -86,6 +86,7 @@ def lib() -> C.CDLL:
         L.fb_learned_plan_create.argtypes = [C.POINTER(vp), i64, i64, i64, C.c_int, C.c_int]
         L.fb_learned_plan_destroy.argtypes = [vp]
         L.fb_learned_plan_factors.argtypes = [vp, C.POINTER(i64), C.POINTER(i64), C.POINTER(i64)]
+        L.fb_learned_plan_engine.argtypes = [vp, C.POINTER(C.c_int)]
         L.fb_learned_workspace_size.argtypes = [vp, i64]
         L.fb_learned_workspace_size.restype = sz
         L.fb_learned_fwd.argtypes = [vp, vp, vp, vp, i64, vp, vp]

@@ -929,6 +929,15 @@ int fb_learned_plan_factors(const fb_learned_plan* p, int64_t* factors, int64_t*
   return FB_OK;
 }
 
+int fb_learned_plan_engine(const fb_learned_plan* p, int* engine) {
+  if (!p || !engine) {
+    set_error("fb_learned_plan_engine: null argument");
+    return FB_ERR_ARG;
+  }
+  *engine = ext_of(p)->dev.tc ? 2 : ext_of(p)->dev.fast ? 1 : 0;
+  return FB_OK;
+}
+
 static int lx_bwd_R(const fb_learned_plan* p);
 static bool lx_fast_bwd(const fb_learned_plan* p) {
   return ext_of(p)->dev.fast && lx_bwd_R(p) > 0;

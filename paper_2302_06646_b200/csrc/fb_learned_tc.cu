@@ -24,7 +24,9 @@
 // Every stage boundary: tcgen05.mma (M = 128 x 2 tiles, N = 32, K = 32) into
 // TMEM, tcgen05.ld by the column's thread, twiddle (power chain from one
 // table value), bf16 store scattered into the next stage's operand rows.
-// The last stage (factor FL <= 8) runs on the CUDA cores.  The backward
+// The last stage (factor FL <= 8) runs as the same GEMM with 16 / FL of its
+// columns per operand row against a block-diagonal table (its rows are then
+// simply 16 consecutive natural-order values).  The backward
 // recomputes the forward stage inputs, keeps them in shared memory, and
 // accumulates each stage's block gradient over the CTA's columns in TMEM
 // (fixed MMA order; CTAs of one head reduced by lb_reduce_kernel in a fixed
@@ -49,31 +51,15 @@ namespace ltc {
 constexpr int kThreads = 256;
 constexpr int kNB = 4096;                    // complex values per CTA (R rows x n)
 constexpr uint32_t kOp = kNB * 4;            // bf16 operand buffer: 256 rows x 64 B (SW64)
-constexpr uint32_t kNat = (kNB + kNB / 16) * 4;  // padded natural buffer (4-byte complex)
 constexpr uint32_t kTab = 2048;              // one N = 32 x K = 32 block table (SW64)
 
-// natural-order buffers padded FL words per 16 FL: the last tc stage's
-// epilogue writes (segment, q) lanes at stride 16 FL, the last stage reads FL
-// consecutive values per thread; both conflict-free with this padding
-template <int LGFL>
-__device__ __forceinline__ int pn(int e) {
-  return e + ((e >> (4 + LGFL)) << LGFL);
-}
-
-// acc + a b, acc + a conj(b)
-__device__ __forceinline__ float2 cfma(float2 a, float2 b, float2 acc) {
-  return make_float2(fmaf(a.x, b.x, fmaf(-a.y, b.y, acc.x)), fmaf(a.x, b.y, fmaf(a.y, b.x, acc.y)));
-}
-__device__ __forceinline__ float2 cfmac(float2 a, float2 b, float2 acc) {
-  return make_float2(fmaf(a.x, b.x, fmaf(a.y, b.y, acc.x)), fmaf(a.y, b.x, fmaf(-a.x, b.y, acc.y)));
-}
+// the forward's last-stage output, element e = 16 J + o of the CTA at word
+// o * 256 + J: thread J's 16 stores are conflict-free across the warp
+__device__ __forceinline__ int out_word(int e) { return ((e & 15) << 8) | (e >> 4); }
 
 __device__ __forceinline__ uint32_t pack_bf16(float2 v) {
   __nv_bfloat162 h = __floats2bfloat162_rn(v.x, v.y);
   return *reinterpret_cast<uint32_t*>(&h);
-}
-__device__ __forceinline__ float2 unpack_bf16(uint32_t u) {
-  return __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&u));
 }
 template <typename IO>
 __device__ __forceinline__ float2 io_f2(uint32_t u) {
@@ -102,15 +88,24 @@ __device__ __forceinline__ uint32_t op_off(uint32_t row, uint32_t slot) {
   return tc::kmajor_off<tc::kSw64>(row, 2 * slot);  // complex slot = k pair (2 slot, 2 slot + 1)
 }
 
-// [[Mr, -Mi], [Mi, Mr]] as the N x K = 32 x 32 K-major SW64 operand, with
-// M(o, i) = W[o][i] (forward) or conj(W[i][o]) (adjoint)
-template <bool ADJ>
+// [[Mr, -Mi], [Mi, Mr]] as the N x K = 32 x 32 K-major SW64 operand of the
+// 16 x 16 complex M made of 16 / FB diagonal FB x FB blocks of W:
+// M(o, i) = W[o % FB][i % FB] when o / FB == i / FB, else 0 (FB = 16: the
+// plain stage block); the adjoint reads it transposed (issue_stage_adj)
+template <int FB>
 __device__ __forceinline__ void build_table(unsigned char* tab, const float2* __restrict__ W) {
-  for (int i = threadIdx.x; i < 32 * 32; i += kThreads) {
-    const int nn = i >> 5, k = i & 31;
-    const int o = nn >> 1, co = nn & 1, in = k >> 1, ci = k & 1;
-    const float2 w = __ldg(ADJ ? W + in * 16 + o : W + o * 16 + in);
-    const float mr = w.x, mi = ADJ ? -w.y : w.y;
+  constexpr int PER = 32 * 32 / kThreads;
+  float2 w[PER];
+#pragma unroll
+  for (int j = 0; j < PER; ++j) {  // all loads in flight first
+    const int i = threadIdx.x + j * kThreads, o = (i >> 5) >> 1, in = (i & 31) >> 1;
+    const int wo = o % FB, wi = in % FB;
+    w[j] = (o / FB == in / FB) ? __ldg(W + wo * FB + wi) : make_float2(0.f, 0.f);
+  }
+#pragma unroll
+  for (int j = 0; j < PER; ++j) {
+    const int i = threadIdx.x + j * kThreads, nn = i >> 5, k = i & 31, co = nn & 1, ci = k & 1;
+    const float mr = w[j].x, mi = w[j].y;
     const float val = co == 0 ? (ci == 0 ? mr : -mi) : (ci == 0 ? mi : mr);
     *reinterpret_cast<__nv_bfloat16*>(tab + tc::kmajor_off<tc::kSw64>(nn, k)) = __float2bfloat16_rn(val);
   }
@@ -126,15 +121,26 @@ __device__ __forceinline__ void issue_stage(uint32_t tmem_d, uint32_t op, uint32
       tc::mma_bf16(tmem_d + 32 * t, tc::smem_desc(op + t * 8192 + k * 32, 512, tc::kSw64),
                    tc::smem_desc(tab + k * 32, 512, tc::kSw64), id, k);
 }
-// G[m][n] (+)= sum_col w[col][m] v[col][n] over the 256 columns: both operands
+// the adjoint: the same table read MN-major, i.e. transposed, which is the
+// real-stacked conj(M)^T ([[Wr, -Wi], [Wi, Wr]]^T = [[Wr^T, Wi^T], [-Wi^T, Wr^T]])
+__device__ __forceinline__ void issue_stage_adj(uint32_t tmem_d, uint32_t op, uint32_t tab) {
+  const uint32_t id = tc::idesc_bf16(128, 32) | (1u << 16);
+#pragma unroll
+  for (uint32_t t = 0; t < 2; ++t)
+#pragma unroll
+    for (uint32_t k = 0; k < 2; ++k)
+      tc::mma_bf16(tmem_d + 32 * t, tc::smem_desc(op + t * 8192 + k * 32, 512, tc::kSw64),
+                   tc::smem_desc(tab + k * 1024, 512, tc::kSw64, 0), id, k);
+}
+// G[m][n] = sum_col w[col][m] v[col][n] over the 256 columns: both operands
 // MN-major SW64 (8-column groups 512 B apart); M = 128 with the MN atoms
 // aliased (LBO = 0: lanes 32-127 repeat lanes 0-31 and are not read)
-__device__ __forceinline__ void issue_grad(uint32_t tmem_g, uint32_t wop, uint32_t vop, bool acc) {
+__device__ __forceinline__ void issue_grad(uint32_t tmem_g, uint32_t wop, uint32_t vop) {
   const uint32_t id = tc::idesc_bf16(128, 32) | (1u << 15) | (1u << 16);
 #pragma unroll
   for (uint32_t kk = 0; kk < 16; ++kk)
     tc::mma_bf16(tmem_g, tc::smem_desc(wop + kk * 1024, 512, tc::kSw64, 0),
-                 tc::smem_desc(vop + kk * 1024, 512, tc::kSw64, 0), id, (acc || kk) ? 1u : 0u);
+                 tc::smem_desc(vop + kk * 1024, 512, tc::kSw64, 0), id, kk ? 1u : 0u);
 }
 
 __device__ __forceinline__ void sync_for_mma() {
@@ -162,9 +168,15 @@ __device__ __forceinline__ void tw_chain(float2 (&t)[16], float2 b, float2 s) {
   for (int a = 1; a < 16; ++a) t[a] = cmul(t[a - 1], s);
 }
 
-// forward epilogue of tc stage S: column c = tid, out[a] = w_L^(a q) D[a] to
-// the next stage's operand (tc) or the natural buffer (last stage)
-template <int LGN, int LGFL, int S, bool NEXT_TC>
+// Stage geometry (n = 2^LGN, STC factor-16 stages, then the last factor FL):
+// factor-16 stage s < STC, segment L = n / 16^s, rest = L / 16: column
+// c = (r, seg, q) = r n/16 + seg rest + q holds in[p] = x_r[seg L + p rest + q].
+// The last stage (s = STC) runs as 16 / FL of its columns per GEMM row:
+// row J holds the CTA's natural elements 16 J .. 16 J + 15 (slot = e % 16),
+// its block-diagonal product leaves outputs in the same natural order.
+
+// forward epilogue of factor-16 stage S: out[a] = w_L^(a q) D[a] into stage S + 1's operand
+template <int LGN, int LGFL, int STC, int S>
 __device__ __forceinline__ void fwd_epilogue(uint32_t tmem_d, unsigned char* next,
                                              const float2* __restrict__ tw_g) {
   constexpr int LGL = LGN - 4 * S, LGR = LGL - 4, LGC = LGN - 4;
@@ -173,35 +185,32 @@ __device__ __forceinline__ void fwd_epilogue(uint32_t tmem_d, unsigned char* nex
   float v[32];
   load_col(tmem_d, v);
   float2 t[16];
-  const float2 t1 = __ldg(tw_g + (q << (LGN - LGL)));
-  tw_chain(t, make_float2(1.f, 0.f), t1);
+  tw_chain(t, make_float2(1.f, 0.f), __ldg(tw_g + (q << (LGN - LGL))));
 #pragma unroll
   for (int a = 0; a < 16; ++a) {
-    const float2 o = cmul(make_float2(v[2 * a], v[2 * a + 1]), t[a]);
-    if constexpr (NEXT_TC) {
-      constexpr int LGR2 = LGR - 4;
+    const uint32_t o = pack_bf16(cmul(make_float2(v[2 * a], v[2 * a + 1]), t[a]));
+    if constexpr (S + 1 < STC) {
+      constexpr int LGR2 = LGR - 4 > 0 ? LGR - 4 : 0;
       const int c2 = (r << LGC) + ((seg * 16 + a) << LGR2) + (q & ((1 << LGR2) - 1));
-      *reinterpret_cast<uint32_t*>(next + op_off(c2, q >> LGR2)) = pack_bf16(o);
+      *reinterpret_cast<uint32_t*>(next + op_off(c2, q >> LGR2)) = o;
     } else {
-      const int e = (r << LGN) + (seg << LGL) + (a << LGR) + q;
-      reinterpret_cast<uint32_t*>(next)[pn<LGFL>(e)] = pack_bf16(o);
+      const int e = (r << LGN) + (seg << LGL) + (a << LGR) + q;  // natural order
+      *reinterpret_cast<uint32_t*>(next + op_off(e >> 4, e & 15)) = o;
     }
   }
 }
 
-// one forward tc stage: MMA batch, wait, epilogue to stage S + 1 (or the last stage)
+// one forward factor-16 stage: MMA batch, wait, epilogue
 template <int LGN, int LGFL, int STC, int S>
-__device__ __forceinline__ void run_fwd_stage(uint32_t tm, uint32_t op, uint32_t tab,
-                                              unsigned char* X0, unsigned char* V2,
-                                              const float2* __restrict__ tw_g, uint64_t* bar,
-                                              uint32_t& phase) {
+__device__ __forceinline__ void run_fwd_stage(uint32_t tm, uint32_t sbase, uint32_t tab,
+                                              unsigned char* X0, const float2* __restrict__ tw_g,
+                                              uint64_t* bar, uint32_t& phase) {
   if (threadIdx.x == 0) {
-    issue_stage(tm, op, tab);
+    issue_stage(tm, sbase + S * kOp, tab);
     tc::commit(bar);
   }
   wait_mma(bar, phase);
-  if constexpr (S + 1 < STC) fwd_epilogue<LGN, LGFL, S, true>(tm, X0 + (S + 1) * kOp, tw_g);
-  else fwd_epilogue<LGN, LGFL, S, false>(tm, V2, tw_g);
+  fwd_epilogue<LGN, LGFL, STC, S>(tm, X0 + (S + 1) * kOp, tw_g);
   sync_for_mma();
 }
 
@@ -216,7 +225,7 @@ __device__ __forceinline__ void load_x(unsigned char* x0, const IO* __restrict__
   if (b < B) {
     const uint32_t* src = reinterpret_cast<const uint32_t*>(x) + ((size_t)b * H + h) * ((size_t)1 << LGN);
 #pragma unroll
-    for (int p = 0; p < 16; ++p) u[p] = io_op<IO>(__ldg(src + (p << LGC) + q));
+    for (int p = 0; p < 16; ++p) u[p] = __ldg(src + (p << LGC) + q);
   } else {
 #pragma unroll
     for (int p = 0; p < 16; ++p) u[p] = 0u;
@@ -224,13 +233,65 @@ __device__ __forceinline__ void load_x(unsigned char* x0, const IO* __restrict__
 #pragma unroll
   for (int j = 0; j < 4; ++j)
     *reinterpret_cast<uint4*>(x0 + tc::kmajor_off<tc::kSw64>(c, 8 * j)) =
-        make_uint4(u[4 * j], u[4 * j + 1], u[4 * j + 2], u[4 * j + 3]);
+        make_uint4(io_op<IO>(u[4 * j]), io_op<IO>(u[4 * j + 1]), io_op<IO>(u[4 * j + 2]),
+                   io_op<IO>(u[4 * j + 3]));
+}
+
+// one stage's block gradient from its TMEM slot into dg (called by one warp):
+// P's rows m = 2A + c sit in lanes 0-31 and, the M = 128 operand's atoms being
+// aliased, again in every other lane quarter, so any warp reads them through
+// its own quarter.  Complex entry (A, B) = (P[2A][2B] + P[2A+1][2B+1],
+// P[2A+1][2B] - P[2A][2B+1]); FB < 16 (the last stage): G[a][p] = sum over
+// the diagonal blocks i of entry (FB i + a, FB i + p).
+template <int LGFL, int FB>
+__device__ __forceinline__ void store_grad(uint32_t slot, float2* __restrict__ dg) {
+  const int lane = threadIdx.x & 31;
+  float pv[32];
+  tc::ld32(slot + ((32 * ((threadIdx.x >> 5) & 3)) << 16), pv);
+  tc::ld_wait();
+  float qv[32];
+#pragma unroll
+  for (int i = 0; i < 32; ++i) qv[i] = __shfl_down_sync(0xffffffffu, pv[i], 1);
+  float2 G[16];
+#pragma unroll
+  for (int b = 0; b < 16; ++b) G[b] = make_float2(pv[2 * b] + qv[2 * b + 1], qv[2 * b] - pv[2 * b + 1]);
+  const int A = lane >> 1;
+  if constexpr (FB == 16) {
+    if ((lane & 1) == 0)
+#pragma unroll
+      for (int b = 0; b < 16; ++b) dg[A * 16 + b] = G[b];
+  } else {
+    constexpr int FL = 1 << LGFL;
+    const int blk = A >> LGFL, a = A & (FL - 1);
+    float2 d[FL];
+#pragma unroll
+    for (int p = 0; p < FL; ++p) {
+      d[p] = make_float2(0.f, 0.f);
+#pragma unroll
+      for (int i = 0; i < 16 / FL; ++i)
+        if (blk == i) d[p] = G[FL * i + p];
+    }
+#pragma unroll
+    for (int off = 2 * FL; off < 32; off <<= 1)
+#pragma unroll
+      for (int p = 0; p < FL; ++p) {
+        d[p].x += __shfl_xor_sync(0xffffffffu, d[p].x, off);
+        d[p].y += __shfl_xor_sync(0xffffffffu, d[p].y, off);
+      }
+    if ((lane & 1) == 0 && blk == 0)
+#pragma unroll
+      for (int p = 0; p < FL; ++p) dg[a * FL + p] = d[p];
+  }
 }
 
 struct Smem {
   uint64_t bar;
   uint32_t tmem;
 };
+
+__device__ __forceinline__ unsigned char* align1k(unsigned char* p) {
+  return reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(p) + 1023) & ~uintptr_t(1023));
+}
 
 template <typename IO, int STC, int LGFL>
 __global__ void __launch_bounds__(kThreads)
@@ -239,14 +300,11 @@ __global__ void __launch_bounds__(kThreads)
                   int P) {
   constexpr int FL = 1 << LGFL, LGN = 4 * STC + LGFL, N = 1 << LGN, R = kNB / N;
   extern __shared__ __align__(1024) unsigned char lt_raw[];
-  unsigned char* sm = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(lt_raw) + 1023) &
-                                                       ~uintptr_t(1023));
-  unsigned char* X0 = sm;                       // stage operands
-  unsigned char* V2 = sm + STC * kOp;           // last-stage input (bf16, natural padded)
-  unsigned char* OUT = V2 + kNat;               // last-stage output (IO, natural padded)
-  unsigned char* TAB = OUT + kNat;              // STC forward tables
-  float2* WL = reinterpret_cast<float2*>(TAB + STC * kTab);
-  Smem* ss = reinterpret_cast<Smem*>(WL + FL * FL);
+  unsigned char* sm = align1k(lt_raw);
+  unsigned char* X0 = sm;                          // operands of stages 0 .. STC
+  unsigned char* OUT = sm;                         // last-stage output (IO, out_word order), over X0
+  unsigned char* TAB = sm + (STC + 1) * kOp;       // forward tables, stages 0 .. STC
+  Smem* ss = reinterpret_cast<Smem*>(TAB + (STC + 1) * kTab);
   const int h = blockIdx.x, b0 = blockIdx.y * R;
   const float2* W = reinterpret_cast<const float2*>(blocks) + (size_t)h * P;
   if (threadIdx.x == 0) {
@@ -254,40 +312,38 @@ __global__ void __launch_bounds__(kThreads)
     ptx::fence_barrier_init();
   }
   if (threadIdx.x < 32) tc::alloc<64>(&ss->tmem);
-#pragma unroll
-  for (int s = 0; s < STC; ++s) build_table<false>(TAB + s * kTab, W + 256 * s);
-  if (threadIdx.x < FL * FL) WL[threadIdx.x] = __ldg(W + 256 * STC + threadIdx.x);
   load_x<IO, LGN>(X0, x, B, H, h, b0);
+#pragma unroll
+  for (int s = 0; s < STC; ++s) build_table<16>(TAB + s * kTab, W + 256 * s);
+  build_table<FL>(TAB + STC * kTab, W + 256 * STC);
   sync_for_mma();
   const uint32_t tm = ss->tmem, sbase = ptx::smem_u32(sm), tab = ptx::smem_u32(TAB);
   uint32_t phase = 0;
-  run_fwd_stage<LGN, LGFL, STC, 0>(tm, sbase, tab, X0, V2, tw_g, &ss->bar, phase);
-  if constexpr (STC == 2) run_fwd_stage<LGN, LGFL, STC, 1>(tm, sbase + kOp, tab + kTab, X0, V2, tw_g, &ss->bar, phase);
-  // last stage (factor FL, no twiddle): out[a] = sum_p WL[a][p] in[p]
-  const uint32_t* v2 = reinterpret_cast<const uint32_t*>(V2);
-  uint32_t* out = reinterpret_cast<uint32_t*>(OUT);
-  for (int j = threadIdx.x; j < kNB / FL; j += kThreads) {
-    float2 in[FL];
-#pragma unroll
-    for (int p = 0; p < FL; ++p) in[p] = unpack_bf16(v2[pn<LGFL>(j * FL + p)]);
-#pragma unroll
-    for (int a = 0; a < FL; ++a) {
-      float2 acc = make_float2(0.f, 0.f);
-#pragma unroll
-      for (int p = 0; p < FL; ++p) acc = cfma(WL[a * FL + p], in[p], acc);
-      out[pn<LGFL>(j * FL + a)] = f2_io<IO>(acc);
-    }
+  run_fwd_stage<LGN, LGFL, STC, 0>(tm, sbase, tab, X0, tw_g, &ss->bar, phase);
+  if constexpr (STC == 2) run_fwd_stage<LGN, LGFL, STC, 1>(tm, sbase, tab + kTab, X0, tw_g, &ss->bar, phase);
+  // last stage (block-diagonal, no twiddle): row J -> natural elements 16 J + o
+  if (threadIdx.x == 0) {
+    issue_stage(tm, sbase + STC * kOp, tab + STC * kTab);
+    tc::commit(&ss->bar);
   }
+  wait_mma(&ss->bar, phase);
+  {
+    float v[32];
+    load_col(tm, v);
+    uint32_t* out = reinterpret_cast<uint32_t*>(OUT);  // X0 is free: stage 0 is long done
+#pragma unroll
+    for (int o = 0; o < 16; ++o) out[out_word(16 * threadIdx.x + o)] = f2_io<IO>(make_float2(v[2 * o], v[2 * o + 1]));
+  }
+  tc::fence_before();
   __syncthreads();
   // y[i] = cur[output_map[i]] (butterfly.cpp:161)
+  const uint32_t* out = reinterpret_cast<const uint32_t*>(OUT);
   for (int i = threadIdx.x; i < kNB; i += kThreads) {
     const int r = i >> LGN, e = i & (N - 1);
     if (b0 + r < B)
       reinterpret_cast<uint32_t*>(y)[((size_t)(b0 + r) * H + h) * N + e] =
-          out[pn<LGFL>((r << LGN) + (int)__ldg(omap + e))];
+          out[out_word((r << LGN) + (int)__ldg(omap + e))];
   }
-  tc::fence_before();
-  __syncthreads();
   if (threadIdx.x < 32) tc::dealloc<64>(tm);
 }
 
@@ -300,16 +356,11 @@ __global__ void __launch_bounds__(kThreads)
   constexpr int FL = 1 << LGFL, LGN = 4 * STC + LGFL, N = 1 << LGN, R = kNB / N;
   constexpr int LGC = LGN - 4;
   extern __shared__ __align__(1024) unsigned char lt_raw[];
-  unsigned char* sm = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(lt_raw) + 1023) &
-                                                       ~uintptr_t(1023));
-  unsigned char* X0 = sm;                        // stage inputs v_s (operands), s < STC
-  unsigned char* WB = sm + STC * kOp;            // w of the top tc stage (w of stage 0 reuses X1)
-  unsigned char* V2 = WB + kOp;                  // last-stage input (bf16, natural padded)
-  unsigned char* GA = V2 + kNat;                 // upstream in stage order (IO, natural padded)
-  unsigned char* TAB = GA + kNat;                // [s][fwd, adj] tables
-  float2* WL = reinterpret_cast<float2*>(TAB + 2 * STC * kTab);
-  float2* RED = WL + FL * FL;                    // [8 warps][<= 32] last-stage gradient partials
-  Smem* ss = reinterpret_cast<Smem*>(RED + kThreads);
+  unsigned char* sm = align1k(lt_raw);
+  unsigned char* X0 = sm;                          // stage inputs v_0 .. v_STC (operands)
+  unsigned char* GA = sm + (STC + 1) * kOp;        // w of the last stage: upstream in stage order
+  unsigned char* TAB = GA + kOp;                   // forward tables, s = 0 .. STC (adjoints: transposed)
+  Smem* ss = reinterpret_cast<Smem*>(TAB + (STC + 1) * kTab);
   const int h = blockIdx.x, b0 = blockIdx.y * R;
   const float2* W = reinterpret_cast<const float2*>(blocks) + (size_t)h * P;
   if (threadIdx.x == 0) {
@@ -317,95 +368,86 @@ __global__ void __launch_bounds__(kThreads)
     ptx::fence_barrier_init();
   }
   if (threadIdx.x < 32) tc::alloc<128>(&ss->tmem);
-#pragma unroll
-  for (int s = 0; s < STC; ++s) {
-    build_table<false>(TAB + (2 * s) * kTab, W + 256 * s);
-    build_table<true>(TAB + (2 * s + 1) * kTab, W + 256 * s);
-  }
-  if (threadIdx.x < FL * FL) WL[threadIdx.x] = __ldg(W + 256 * STC + threadIdx.x);
   load_x<IO, LGN>(X0, x, B, H, h, b0);
-  // upstream, adjoint of y[i] = cur[omap[i]]: GA[omap[i]] = g[i]
+  // upstream, adjoint of y[i] = cur[omap[i]]: w_last[omap[i]] = g[i], all loads first
   {
-    uint32_t* ga = reinterpret_cast<uint32_t*>(GA);
-    for (int i = threadIdx.x; i < kNB; i += kThreads) {
-      const int r = i >> LGN, e = i & (N - 1);
-      const uint32_t val = b0 + r < B ? __ldg(reinterpret_cast<const uint32_t*>(g) +
-                                              ((size_t)(b0 + r) * H + h) * N + e)
-                                      : 0u;
-      ga[pn<LGFL>((r << LGN) + (int)__ldg(omap + e))] = val;
+    constexpr int PER = kNB / kThreads;
+    uint32_t gv[PER];
+    int dst[PER];
+#pragma unroll
+    for (int j = 0; j < PER; ++j) {
+      const int i = threadIdx.x + j * kThreads, r = i >> LGN, e = i & (N - 1);
+      gv[j] = b0 + r < B ? __ldg(reinterpret_cast<const uint32_t*>(g) + ((size_t)(b0 + r) * H + h) * N + e) : 0u;
+      dst[j] = (r << LGN) + (int)__ldg(omap + e);
     }
+#pragma unroll
+    for (int j = 0; j < PER; ++j)
+      *reinterpret_cast<uint32_t*>(GA + op_off(dst[j] >> 4, dst[j] & 15)) = io_op<IO>(gv[j]);
   }
+#pragma unroll
+  for (int s = 0; s < STC; ++s) build_table<16>(TAB + s * kTab, W + 256 * s);
+  build_table<FL>(TAB + STC * kTab, W + 256 * STC);
   sync_for_mma();
   const uint32_t tm = ss->tmem, sbase = ptx::smem_u32(sm), tab = ptx::smem_u32(TAB);
-  const uint32_t tmg = tm + 64;  // per-stage gradient accumulators, 32 columns each
+  // block-gradient accumulators: two 32-column slots, stage s in slot (STC - s) & 1
+  // (a slot is read out in the epilogue right after its batch, before reuse)
+  auto gslot = [&](int s) { return tm + 64 + 32 * ((STC - s) & 1); };
+  float2* dg = gpart + ((size_t)blockIdx.y * H + h) * P;
   uint32_t phase = 0;
-  // forward recompute: v_1 .. v_STC (the last stage's input)
-  run_fwd_stage<LGN, LGFL, STC, 0>(tm, sbase, tab, X0, V2, tw_g, &ss->bar, phase);
-  if constexpr (STC == 2)
-    run_fwd_stage<LGN, LGFL, STC, 1>(tm, sbase + kOp, tab + 2 * kTab, X0, V2, tw_g, &ss->bar, phase);
-  // last stage (CUDA cores).  Block gradient: thread = one entry (a, p),
-  // columns strided; lanes of one entry reduced by shuffles, warps in order.
-  const uint32_t* v2 = reinterpret_cast<const uint32_t*>(V2);
-  const uint32_t* ga = reinterpret_cast<const uint32_t*>(GA);
-  {
-    constexpr int E = FL * FL, GROUPS = kThreads / E;
-    const int ent = threadIdx.x % E, grp = threadIdx.x / E, a = ent / FL, p = ent % FL;
-    float2 acc = make_float2(0.f, 0.f);
-    for (int j = grp; j < kNB / FL; j += GROUPS) {
-      const float2 w = io_f2<IO>(ga[pn<LGFL>(j * FL + a)]);
-      const float2 vv = unpack_bf16(v2[pn<LGFL>(j * FL + p)]);
-      acc = cfmac(w, vv, acc);  // w conj(v)
-    }
-#pragma unroll
-    for (int o = E; o < 32; o <<= 1) {
-      acc.x += __shfl_xor_sync(0xffffffffu, acc.x, o);
-      acc.y += __shfl_xor_sync(0xffffffffu, acc.y, o);
-    }
-    constexpr int PER = E < 32 ? E : 32;  // lanes of a warp holding distinct entries
-    if ((threadIdx.x & 31) < PER) RED[(threadIdx.x >> 5) * PER + (threadIdx.x & 31)] = acc;
+  // forward recompute: v_1 .. v_STC
+  run_fwd_stage<LGN, LGFL, STC, 0>(tm, sbase, tab, X0, tw_g, &ss->bar, phase);
+  if constexpr (STC == 2) run_fwd_stage<LGN, LGFL, STC, 1>(tm, sbase, tab + kTab, X0, tw_g, &ss->bar, phase);
+  // last stage: block gradient + adjoint (block-diagonal), then times conj of
+  // stage STC - 1's twiddle into that stage's w (over v_STC, consumed here):
+  // natural element e = 16 J + o of a row lies in column (r, e / 16 FL, e % FL),
+  // slot (e / FL) % 16 of stage STC - 1 (L = 16 FL, rest = FL)
+  if (threadIdx.x == 0) {
+    issue_grad(gslot(STC), ptx::smem_u32(GA), sbase + STC * kOp);
+    issue_stage_adj(tm, ptx::smem_u32(GA), tab + STC * kTab);
+    tc::commit(&ss->bar);
   }
-  // adjoint of the last stage, times conj of the top tc stage's twiddle, to
-  // that stage's w operand: element e = seg2 FL + p of a row sits at column
-  // (r, seg2 / 16, q = p), slot seg2 % 16 of tc stage STC - 1 (L = 16 FL)
-  for (int j = threadIdx.x; j < kNB / FL; j += kThreads) {
-    float2 w[FL];
+  wait_mma(&ss->bar, phase);
+  if ((threadIdx.x >> 5) == 1) store_grad<LGFL, FL>(gslot(STC), dg + 256 * STC);
+  {
+    float v[32];
+    load_col(tm, v);
+    unsigned char* wdst = X0 + STC * kOp;
+    const int J = threadIdx.x, r = J >> (LGN - 4), el0 = (J << 4) & (N - 1);
 #pragma unroll
-    for (int a = 0; a < FL; ++a) w[a] = io_f2<IO>(ga[pn<LGFL>(j * FL + a)]);
-    const int r = j >> (LGN - LGFL), seg2 = j & ((1 << (LGN - LGFL)) - 1), a2 = seg2 & 15;
-#pragma unroll
-    for (int p = 0; p < FL; ++p) {
-      float2 o = make_float2(0.f, 0.f);
-#pragma unroll
-      for (int a = 0; a < FL; ++a) o = cfmac(w[a], WL[a * FL + p], o);  // conj(WL[a][p]) w[a]
-      o = cmulc(o, __ldg(tw_g + ((a2 * p) << (LGN - LGFL - 4))));
-      const int c2 = (r << LGC) + ((seg2 >> 4) << LGFL) + p;
-      *reinterpret_cast<uint32_t*>(WB + op_off(c2, a2)) = pack_bf16(o);
+    for (int o = 0; o < 16; ++o) {
+      const int el = el0 + o, a2 = (el >> LGFL) & 15, q2 = el & (FL - 1);
+      const float2 t = __ldg(tw_g + ((a2 * q2) << (LGN - LGFL - 4)));
+      const float2 w = cmulc(make_float2(v[2 * o], v[2 * o + 1]), t);
+      const int c2 = (r << LGC) + ((el >> (LGFL + 4)) << LGFL) + q2;
+      *reinterpret_cast<uint32_t*>(wdst + op_off(c2, a2)) = pack_bf16(w);
     }
   }
   sync_for_mma();
-  // tc stages, top down: block gradient + adjoint GEMMs in one batch
+  // factor-16 stages, top down: block gradient + adjoint GEMMs in one batch;
+  // w_s sits over v_(s+1)
   auto adjoint_stage = [&](auto s_c) {
     constexpr int s = decltype(s_c)::value;
-    const uint32_t wop = s == STC - 1 ? ptx::smem_u32(WB) : sbase + (s + 1) * kOp;
+    const uint32_t wop = sbase + (s + 1) * kOp;
     if (threadIdx.x == 0) {
-      issue_grad(tmg + 32 * s, wop, sbase + s * kOp, false);
-      issue_stage(tm, wop, tab + (2 * s + 1) * kTab);
+      issue_grad(gslot(s), wop, sbase + s * kOp);
+      issue_stage_adj(tm, wop, tab + s * kTab);
       tc::commit(&ss->bar);
     }
     wait_mma(&ss->bar, phase);
+    if ((threadIdx.x >> 5) == 1) store_grad<LGFL, 16>(gslot(s), dg + 256 * s);
     if constexpr (s > 0) {
-      // column (r, seg, q) of stage s (L = n / 16^s): g'[p] at e = seg L + p rest + q;
-      // stage s - 1 (L' = 16 L): a' = seg % 16, q' = p rest + q, column (r, seg / 16, q')
-      constexpr int LGL = LGN - 4, LGR = STC == 2 ? LGL - 4 : 0;  // s == 1 (STC == 2)
+      // column (r, seg, q) of stage 1 (L = n / 16): g'[p] at e = seg L + p rest + q;
+      // stage 0 (L' = n): a' = seg, q' = p rest + q, column (r, q')
+      constexpr int LGL = LGN - 4, LGR = STC == 2 ? LGL - 4 : 0;
       const int c = threadIdx.x;
       const int r = c >> LGC, cc = c & ((1 << LGC) - 1), seg = cc >> LGR, q = cc & ((1 << LGR) - 1);
       const int a2 = seg & 15;
       float v[32];
       load_col(tm, v);
       float2 t[16];
-      // conj(w_{16L}^(a2 (p rest + q))) = conj(b s^p), b = w^(a2 q), s = w^(a2 rest)
+      // conj(w_n^(a2 (p rest + q))) = conj(b s^p), b = w^(a2 q), s = w^(a2 rest)
       tw_chain(t, __ldg(tw_g + ((a2 * q) & (N - 1))), __ldg(tw_g + ((a2 << LGR) & (N - 1))));
-      unsigned char* wdst = X0 + kOp;  // w of stage 0 over v_1 (consumed above)
+      unsigned char* wdst = X0 + kOp;  // w_0 over v_1 (consumed above)
 #pragma unroll
       for (int p = 0; p < 16; ++p) {
         const float2 o = cmulc(make_float2(v[2 * p], v[2 * p + 1]), t[p]);
@@ -427,39 +469,6 @@ __global__ void __launch_bounds__(kThreads)
   };
   if constexpr (STC == 2) adjoint_stage(std::integral_constant<int, 1>());
   adjoint_stage(std::integral_constant<int, 0>());
-  // block gradients -> gpart[split][h]: tc stages from TMEM (warp 0: lanes
-  // m = 2a + c), the last stage from the warp partials
-  float2* dg = gpart + ((size_t)blockIdx.y * H + h) * P;
-  if (threadIdx.x < 32) {
-    const int lane = threadIdx.x;
-#pragma unroll 1
-    for (int s = 0; s < STC; ++s) {
-      float pv[32];
-      tc::ld32(tmg + 32 * s, pv);
-      tc::ld_wait();
-      float qv[32];
-#pragma unroll
-      for (int i = 0; i < 32; ++i) qv[i] = __shfl_down_sync(0xffffffffu, pv[i], 1);
-      if ((lane & 1) == 0) {
-        const int a = lane >> 1;
-#pragma unroll
-        for (int p = 0; p < 16; ++p)
-          dg[256 * s + a * 16 + p] = make_float2(pv[2 * p] + qv[2 * p + 1], qv[2 * p] - pv[2 * p + 1]);
-      }
-    }
-  }
-  {
-    // entry e sits in lane l = e % 32 of every warp whose lanes start at an
-    // entry == e - l (mod E); warps summed in order
-    constexpr int E = FL * FL, PER = E < 32 ? E : 32;
-    for (int e = threadIdx.x; e < E; e += kThreads) {
-      const int l = e % PER;
-      float2 s = make_float2(0.f, 0.f);
-      for (int wq = 0; wq < kThreads / 32; ++wq)
-        if ((wq * 32 + l) % E == e) s = cadd(s, RED[wq * PER + l]);
-      dg[256 * STC + e] = s;
-    }
-  }
   tc::fence_before();
   __syncthreads();
   if (threadIdx.x < 32) tc::dealloc<128>(tm);
@@ -467,12 +476,11 @@ __global__ void __launch_bounds__(kThreads)
 
 template <int STC, int LGFL>
 constexpr size_t fwd_smem() {
-  return 1024 + STC * kOp + 2 * kNat + STC * kTab + (1 << (2 * LGFL)) * 8 + 64;
+  return 1024 + (STC + 1) * kOp + (STC + 1) * kTab + 64;
 }
 template <int STC, int LGFL>
 constexpr size_t bwd_smem() {
-  return 1024 + (STC + 1) * kOp + 2 * kNat + 2 * STC * kTab + (1 << (2 * LGFL)) * 8 +
-         kThreads * 8 + 64;
+  return 1024 + (STC + 2) * kOp + (STC + 1) * kTab + 64;
 }
 
 template <typename IO, int STC, int LGFL>

@@ -44,6 +44,10 @@ class LearnedButterflyPlan:
         check(_lib.lib().fb_learned_plan_factors(h, f, C.byref(cnt), C.byref(pc)))
         self.factors = [int(f[i]) for i in range(cnt.value)]
         self.param_count = int(pc.value)
+        eng = C.c_int()
+        check(_lib.lib().fb_learned_plan_engine(h, C.byref(eng)))
+        # kernel family: generic stage walk, CUDA-core fast path, or tcgen05
+        self.engine = ("generic", "cuda-core", "tcgen05")[eng.value]
 
     def __del__(self):
         h = getattr(self, "_h", None)

@@ -80,6 +80,7 @@ def test_batched_fp32(lc, n, r):
     B, H = 3, 4
     blocks, x, g = batch_case(lc, B, H, n, r)
     plan = fb.LearnedButterflyPlan(n, r, H)
+    assert plan.engine != "tcgen05"  # fp32 stays on the CUDA cores (1e-5 bar)
     tb, tx, tg = cplx(blocks, blocks.shape), cplx(x, x.shape), cplx(g, g.shape)
     y = plan.forward(tb, tx).cpu().numpy()
     db, dx = plan.gradients(tb, tx, tg)
@@ -124,6 +125,7 @@ def test_tensor_core_chains_16bit(lc, n, B, dtype):
     H, r = 3, 16
     blocks, x, g = batch_case(lc, B, H, n, r, seed=n + B)
     plan = fb.LearnedButterflyPlan(n, r, H, dtype)
+    assert plan.engine == "tcgen05"
     tb = cplx(blocks, blocks.shape)
     tx = to16(cplx(x, x.shape), dtype)
     tg = to16(cplx(g, g.shape), dtype)
