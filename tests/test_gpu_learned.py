@@ -140,6 +140,9 @@ def test_tensor_core_chains_16bit(lc, n, B, dtype):
     edb = rel_l2(db.cpu().numpy(), rdb)
     print(f"n={n} B={B} {dtype}: y {ey:.2e} dx {edx:.2e} dblocks {edb:.2e}")
     assert ey < 2e-2 and edx < 2e-2 and edb < 2e-2
+    # again: bit-identical (fixed-order in-kernel reduction, counters reset)
+    db2, dx2 = plan.gradients(tb, tx, tg)
+    assert torch.equal(db2, db) and np.array_equal(from16(dx2), dx)
 
 
 def test_autograd():
