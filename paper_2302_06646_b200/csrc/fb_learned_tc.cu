@@ -53,9 +53,16 @@ constexpr int kNB = 4096;                    // complex values per CTA (R rows x
 constexpr uint32_t kOp = kNB * 4;            // bf16 operand buffer: 256 rows x 64 B (SW64)
 constexpr uint32_t kTab = 2048;              // one N = 32 x K = 32 block table (SW64)
 
-// the forward's last-stage output, element e = 16 J + o of the CTA at word
-// o * 256 + J: thread J's 16 stores are conflict-free across the warp
-__device__ __forceinline__ int out_word(int e) { return ((e & 15) << 8) | (e >> 4); }
+// output_map (butterfly.cpp:103-116) of the chain [16] * STC + [FL] is the
+// mixed-radix digit reversal: y[i] = cur[output_map[i]] puts the CTA row's
+// element e = e0 16 FL + e1 FL + e2 (STC = 2) at i = e0 + 16 e1 + 256 e2
+// (STC = 1: e = e0 FL + e2 -> i = e0 + 16 e2)
+template <int STC, int LGFL>
+__device__ __forceinline__ int out_index(int e) {
+  constexpr int FL = 1 << LGFL;
+  if constexpr (STC == 2) return (e >> (LGFL + 4)) | (((e >> LGFL) & 15) << 4) | ((e & (FL - 1)) << 8);
+  else return (e >> LGFL) | ((e & (FL - 1)) << 4);
+}
 
 __device__ __forceinline__ uint32_t pack_bf16(float2 v) {
   __nv_bfloat162 h = __floats2bfloat162_rn(v.x, v.y);
@@ -296,13 +303,12 @@ __device__ __forceinline__ unsigned char* align1k(unsigned char* p) {
 template <typename IO, int STC, int LGFL>
 __global__ void __launch_bounds__(kThreads)
     lt_fwd_kernel(const float* __restrict__ blocks, const IO* __restrict__ x, IO* __restrict__ y,
-                  const uint32_t* __restrict__ omap, const float2* __restrict__ tw_g, int B, int H,
+                  const uint32_t* __restrict__ /* omap: out_index */, const float2* __restrict__ tw_g, int B, int H,
                   int P) {
   constexpr int FL = 1 << LGFL, LGN = 4 * STC + LGFL, N = 1 << LGN, R = kNB / N;
   extern __shared__ __align__(1024) unsigned char lt_raw[];
   unsigned char* sm = align1k(lt_raw);
   unsigned char* X0 = sm;                          // operands of stages 0 .. STC
-  unsigned char* OUT = sm;                         // last-stage output (IO, out_word order), over X0
   unsigned char* TAB = sm + (STC + 1) * kOp;       // forward tables, stages 0 .. STC
   Smem* ss = reinterpret_cast<Smem*>(TAB + (STC + 1) * kTab);
   const int h = blockIdx.x, b0 = blockIdx.y * R;
@@ -328,30 +334,28 @@ __global__ void __launch_bounds__(kThreads)
   }
   wait_mma(&ss->bar, phase);
   {
+    // y[out_index(e)] = cur[e] for the thread's 16 natural elements: a warp's
+    // stores cover whole 32-byte sectors (8 consecutive i per sector)
     float v[32];
     load_col(tm, v);
-    uint32_t* out = reinterpret_cast<uint32_t*>(OUT);  // X0 is free: stage 0 is long done
+    const int J = threadIdx.x, r = J >> (LGN - 4), el0 = (J << 4) & (N - 1);
+    if (b0 + r < B) {
+      uint32_t* dst = reinterpret_cast<uint32_t*>(y) + ((size_t)(b0 + r) * H + h) * N;
 #pragma unroll
-    for (int o = 0; o < 16; ++o) out[out_word(16 * threadIdx.x + o)] = f2_io<IO>(make_float2(v[2 * o], v[2 * o + 1]));
+      for (int o = 0; o < 16; ++o)
+        dst[out_index<STC, LGFL>(el0 + o)] = f2_io<IO>(make_float2(v[2 * o], v[2 * o + 1]));
+    }
   }
   tc::fence_before();
   __syncthreads();
-  // y[i] = cur[output_map[i]] (butterfly.cpp:161)
-  const uint32_t* out = reinterpret_cast<const uint32_t*>(OUT);
-  for (int i = threadIdx.x; i < kNB; i += kThreads) {
-    const int r = i >> LGN, e = i & (N - 1);
-    if (b0 + r < B)
-      reinterpret_cast<uint32_t*>(y)[((size_t)(b0 + r) * H + h) * N + e] =
-          out[out_word((r << LGN) + (int)__ldg(omap + e))];
-  }
   if (threadIdx.x < 32) tc::dealloc<64>(tm);
 }
 
 template <typename IO, int STC, int LGFL>
-__global__ void __launch_bounds__(kThreads)
+__global__ void __launch_bounds__(kThreads, 3)
     lt_bwd_kernel(const float* __restrict__ blocks, const IO* __restrict__ x,
                   const IO* __restrict__ g, IO* __restrict__ dx, float2* __restrict__ gpart,
-                  const uint32_t* __restrict__ omap, const float2* __restrict__ tw_g, int B, int H,
+                  const uint32_t* __restrict__ /* omap: out_index */, const float2* __restrict__ tw_g, int B, int H,
                   int P) {
   constexpr int FL = 1 << LGFL, LGN = 4 * STC + LGFL, N = 1 << LGN, R = kNB / N;
   constexpr int LGC = LGN - 4;
@@ -369,20 +373,24 @@ __global__ void __launch_bounds__(kThreads)
   }
   if (threadIdx.x < 32) tc::alloc<128>(&ss->tmem);
   load_x<IO, LGN>(X0, x, B, H, h, b0);
-  // upstream, adjoint of y[i] = cur[omap[i]]: w_last[omap[i]] = g[i], all loads first
+  // upstream in stage order, the adjoint of y[i] = cur[output_map[i]]:
+  // row J of the last stage's w operand = g[out_index(16 J + o)], o < 16
   {
-    constexpr int PER = kNB / kThreads;
-    uint32_t gv[PER];
-    int dst[PER];
+    const int J = threadIdx.x, r = J >> (LGN - 4), el0 = (J << 4) & (N - 1);
+    uint32_t u[16];
+    if (b0 + r < B) {
+      const uint32_t* src = reinterpret_cast<const uint32_t*>(g) + ((size_t)(b0 + r) * H + h) * N;
 #pragma unroll
-    for (int j = 0; j < PER; ++j) {
-      const int i = threadIdx.x + j * kThreads, r = i >> LGN, e = i & (N - 1);
-      gv[j] = b0 + r < B ? __ldg(reinterpret_cast<const uint32_t*>(g) + ((size_t)(b0 + r) * H + h) * N + e) : 0u;
-      dst[j] = (r << LGN) + (int)__ldg(omap + e);
+      for (int o = 0; o < 16; ++o) u[o] = __ldg(src + out_index<STC, LGFL>(el0 + o));
+    } else {
+#pragma unroll
+      for (int o = 0; o < 16; ++o) u[o] = 0u;
     }
 #pragma unroll
-    for (int j = 0; j < PER; ++j)
-      *reinterpret_cast<uint32_t*>(GA + op_off(dst[j] >> 4, dst[j] & 15)) = io_op<IO>(gv[j]);
+    for (int j4 = 0; j4 < 4; ++j4)
+      *reinterpret_cast<uint4*>(GA + tc::kmajor_off<tc::kSw64>(J, 8 * j4)) =
+          make_uint4(io_op<IO>(u[4 * j4]), io_op<IO>(u[4 * j4 + 1]), io_op<IO>(u[4 * j4 + 2]),
+                     io_op<IO>(u[4 * j4 + 3]));
   }
 #pragma unroll
   for (int s = 0; s < STC; ++s) build_table<16>(TAB + s * kTab, W + 256 * s);
