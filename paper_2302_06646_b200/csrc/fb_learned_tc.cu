@@ -98,24 +98,17 @@ __device__ __forceinline__ uint32_t op_off(uint32_t row, uint32_t slot) {
 // [[Mr, -Mi], [Mi, Mr]] as the N x K = 32 x 32 K-major SW64 operand of the
 // 16 x 16 complex M made of 16 / FB diagonal FB x FB blocks of W:
 // M(o, i) = W[o % FB][i % FB] when o / FB == i / FB, else 0 (FB = 16: the
-// plain stage block); the adjoint reads it transposed (issue_stage_adj)
+// plain stage block); the adjoint reads it transposed (issue_stage_adj).
+// Thread t owns entry (o, i) = (t / 16, t % 16): one load, two 4-byte stores.
 template <int FB>
-__device__ __forceinline__ void build_table(unsigned char* tab, const float2* __restrict__ W) {
-  constexpr int PER = 32 * 32 / kThreads;
-  float2 w[PER];
-#pragma unroll
-  for (int j = 0; j < PER; ++j) {  // all loads in flight first
-    const int i = threadIdx.x + j * kThreads, o = (i >> 5) >> 1, in = (i & 31) >> 1;
-    const int wo = o % FB, wi = in % FB;
-    w[j] = (o / FB == in / FB) ? __ldg(W + wo * FB + wi) : make_float2(0.f, 0.f);
-  }
-#pragma unroll
-  for (int j = 0; j < PER; ++j) {
-    const int i = threadIdx.x + j * kThreads, nn = i >> 5, k = i & 31, co = nn & 1, ci = k & 1;
-    const float mr = w[j].x, mi = w[j].y;
-    const float val = co == 0 ? (ci == 0 ? mr : -mi) : (ci == 0 ? mi : mr);
-    *reinterpret_cast<__nv_bfloat16*>(tab + tc::kmajor_off<tc::kSw64>(nn, k)) = __float2bfloat16_rn(val);
-  }
+__device__ __forceinline__ float2 table_entry(const float2* __restrict__ W) {
+  const int o = threadIdx.x >> 4, in = threadIdx.x & 15;
+  return (o / FB == in / FB) ? __ldg(W + (o % FB) * FB + in % FB) : make_float2(0.f, 0.f);
+}
+__device__ __forceinline__ void store_table(unsigned char* tab, float2 m) {
+  const int o = threadIdx.x >> 4, in = threadIdx.x & 15;
+  *reinterpret_cast<uint32_t*>(tab + tc::kmajor_off<tc::kSw64>(2 * o, 2 * in)) = pack_bf16(make_float2(m.x, -m.y));
+  *reinterpret_cast<uint32_t*>(tab + tc::kmajor_off<tc::kSw64>(2 * o + 1, 2 * in)) = pack_bf16(make_float2(m.y, m.x));
 }
 
 // D[tile t][col][2a + c] = sum_k op[col][k] tab[2a + c][k], two M = 128 tiles
@@ -222,13 +215,13 @@ __device__ __forceinline__ void run_fwd_stage(uint32_t tm, uint32_t sbase, uint3
 }
 
 // x rows (IO) -> stage-0 operand: column c = (r, q), slot p = x[r][p rest0 + q]
-template <typename IO, int LGN>
-__device__ __forceinline__ void load_x(unsigned char* x0, const IO* __restrict__ x, int B, int H,
+// (loads and stores split so the prologue's loads are all in flight at once)
+template <int LGN>
+__device__ __forceinline__ void load_x(uint32_t (&u)[16], const void* __restrict__ x, int B, int H,
                                        int h, int b0) {
   constexpr int LGC = LGN - 4;
   const int c = threadIdx.x, r = c >> LGC, q = c & ((1 << LGC) - 1);
   const int b = b0 + r;
-  uint32_t u[16];
   if (b < B) {
     const uint32_t* src = reinterpret_cast<const uint32_t*>(x) + ((size_t)b * H + h) * ((size_t)1 << LGN);
 #pragma unroll
@@ -237,9 +230,13 @@ __device__ __forceinline__ void load_x(unsigned char* x0, const IO* __restrict__
 #pragma unroll
     for (int p = 0; p < 16; ++p) u[p] = 0u;
   }
+}
+// this thread's operand row (64 bytes) from 16 IO complex values
+template <typename IO>
+__device__ __forceinline__ void store_row(unsigned char* op, int row, const uint32_t (&u)[16]) {
 #pragma unroll
   for (int j = 0; j < 4; ++j)
-    *reinterpret_cast<uint4*>(x0 + tc::kmajor_off<tc::kSw64>(c, 8 * j)) =
+    *reinterpret_cast<uint4*>(op + tc::kmajor_off<tc::kSw64>(row, 8 * j)) =
         make_uint4(io_op<IO>(u[4 * j]), io_op<IO>(u[4 * j + 1]), io_op<IO>(u[4 * j + 2]),
                    io_op<IO>(u[4 * j + 3]));
 }
@@ -318,10 +315,17 @@ __global__ void __launch_bounds__(kThreads)
     ptx::fence_barrier_init();
   }
   if (threadIdx.x < 32) tc::alloc<64>(&ss->tmem);
-  load_x<IO, LGN>(X0, x, B, H, h, b0);
+  {
+    uint32_t u[16];
+    float2 wt[STC + 1];
+    load_x<LGN>(u, x, B, H, h, b0);
 #pragma unroll
-  for (int s = 0; s < STC; ++s) build_table<16>(TAB + s * kTab, W + 256 * s);
-  build_table<FL>(TAB + STC * kTab, W + 256 * STC);
+    for (int s = 0; s < STC; ++s) wt[s] = table_entry<16>(W + 256 * s);
+    wt[STC] = table_entry<FL>(W + 256 * STC);
+    store_row<IO>(X0, threadIdx.x, u);
+#pragma unroll
+    for (int s = 0; s <= STC; ++s) store_table(TAB + s * kTab, wt[s]);
+  }
   sync_for_mma();
   const uint32_t tm = ss->tmem, sbase = ptx::smem_u32(sm), tab = ptx::smem_u32(TAB);
   uint32_t phase = 0;
@@ -372,29 +376,30 @@ __global__ void __launch_bounds__(kThreads, 3)
     ptx::fence_barrier_init();
   }
   if (threadIdx.x < 32) tc::alloc<128>(&ss->tmem);
-  load_x<IO, LGN>(X0, x, B, H, h, b0);
-  // upstream in stage order, the adjoint of y[i] = cur[output_map[i]]:
-  // row J of the last stage's w operand = g[out_index(16 J + o)], o < 16
   {
+    // x, the upstream in stage order (the adjoint of y[i] = cur[output_map[i]]:
+    // row J of the last stage's w operand = g[out_index(16 J + o)], o < 16)
+    // and the block tables: all loads in flight, then the stores
+    uint32_t u[16], gu[16];
+    float2 wt[STC + 1];
+    load_x<LGN>(u, x, B, H, h, b0);
     const int J = threadIdx.x, r = J >> (LGN - 4), el0 = (J << 4) & (N - 1);
-    uint32_t u[16];
     if (b0 + r < B) {
       const uint32_t* src = reinterpret_cast<const uint32_t*>(g) + ((size_t)(b0 + r) * H + h) * N;
 #pragma unroll
-      for (int o = 0; o < 16; ++o) u[o] = __ldg(src + out_index<STC, LGFL>(el0 + o));
+      for (int o = 0; o < 16; ++o) gu[o] = __ldg(src + out_index<STC, LGFL>(el0 + o));
     } else {
 #pragma unroll
-      for (int o = 0; o < 16; ++o) u[o] = 0u;
+      for (int o = 0; o < 16; ++o) gu[o] = 0u;
     }
 #pragma unroll
-    for (int j4 = 0; j4 < 4; ++j4)
-      *reinterpret_cast<uint4*>(GA + tc::kmajor_off<tc::kSw64>(J, 8 * j4)) =
-          make_uint4(io_op<IO>(u[4 * j4]), io_op<IO>(u[4 * j4 + 1]), io_op<IO>(u[4 * j4 + 2]),
-                     io_op<IO>(u[4 * j4 + 3]));
-  }
+    for (int s = 0; s < STC; ++s) wt[s] = table_entry<16>(W + 256 * s);
+    wt[STC] = table_entry<FL>(W + 256 * STC);
+    store_row<IO>(X0, threadIdx.x, u);
+    store_row<IO>(GA, J, gu);
 #pragma unroll
-  for (int s = 0; s < STC; ++s) build_table<16>(TAB + s * kTab, W + 256 * s);
-  build_table<FL>(TAB + STC * kTab, W + 256 * STC);
+    for (int s = 0; s <= STC; ++s) store_table(TAB + s * kTab, wt[s]);
+  }
   sync_for_mma();
   const uint32_t tm = ss->tmem, sbase = ptx::smem_u32(sm), tab = ptx::smem_u32(TAB);
   // block-gradient accumulators: two 32-column slots, stage s in slot (STC - s) & 1
