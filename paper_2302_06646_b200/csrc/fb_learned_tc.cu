@@ -175,12 +175,44 @@ __device__ __forceinline__ void tw_chain(float2 (&t)[16], float2 b, float2 s) {
 // row J holds the CTA's natural elements 16 J .. 16 J + 15 (slot = e % 16),
 // its block-diagonal product leaves outputs in the same natural order.
 
+// Operand row of stage S's column c: a permutation of the low 6 bits (bit i
+// -> bit perm[i]), free since the GEMMs only see rows and the stage's w / v
+// share it; chosen for config 4's chain so that the epilogues' 4-byte
+// scatters hit distinct banks (modelled: 2/1/4/1-way for the 0->1 / 1->2 /
+// last-adjoint / 1-adjoint scatters, 2/4/8/2-way unpermuted).  Epilogue
+// threads own D row tid, i.e. column col_of(tid).
+template <int STC, int LGFL, int S>
+__host__ __device__ constexpr int row_perm(int i) {
+  if constexpr (STC == 2 && LGFL == 2) {
+    constexpr int p0[6] = {0, 2, 1, 3, 4, 5}, p1[6] = {1, 2, 0, 3, 4, 5}, p2[6] = {3, 4, 2, 1, 0, 5};
+    return S == 0 ? p0[i] : S == 1 ? p1[i] : p2[i];
+  } else {
+    return i;
+  }
+}
+// (a bit permutation: row_of(x | y) = row_of(x) | row_of(y) for disjoint bit
+// sets, so the scatters split a row into a per-thread part and a constant)
+template <int STC, int LGFL, int S>
+__host__ __device__ constexpr int row_of(int c) {
+  int y = c & ~63;
+#pragma unroll
+  for (int i = 0; i < 6; ++i) y |= ((c >> i) & 1) << row_perm<STC, LGFL, S>(i);
+  return y;
+}
+template <int STC, int LGFL, int S>
+__device__ __forceinline__ int col_of(int row) {
+  int y = row & ~63;
+#pragma unroll
+  for (int i = 0; i < 6; ++i) y |= ((row >> row_perm<STC, LGFL, S>(i)) & 1) << i;
+  return y;
+}
+
 // forward epilogue of factor-16 stage S: out[a] = w_L^(a q) D[a] into stage S + 1's operand
 template <int LGN, int LGFL, int STC, int S>
 __device__ __forceinline__ void fwd_epilogue(uint32_t tmem_d, unsigned char* next,
                                              const float2* __restrict__ tw_g) {
   constexpr int LGL = LGN - 4 * S, LGR = LGL - 4, LGC = LGN - 4;
-  const int c = threadIdx.x;
+  const int c = col_of<STC, LGFL, S>(threadIdx.x);
   const int r = c >> LGC, cc = c & ((1 << LGC) - 1), seg = cc >> LGR, q = cc & ((1 << LGR) - 1);
   float v[32];
   load_col(tmem_d, v);
@@ -191,11 +223,18 @@ __device__ __forceinline__ void fwd_epilogue(uint32_t tmem_d, unsigned char* nex
     const uint32_t o = pack_bf16(cmul(make_float2(v[2 * a], v[2 * a + 1]), t[a]));
     if constexpr (S + 1 < STC) {
       constexpr int LGR2 = LGR - 4 > 0 ? LGR - 4 : 0;
-      const int c2 = (r << LGC) + ((seg * 16 + a) << LGR2) + (q & ((1 << LGR2) - 1));
-      *reinterpret_cast<uint32_t*>(next + op_off(c2, q >> LGR2)) = o;
+      static_assert(S == 0, "one factor-16 stage feeds another only from stage 0");
+      // column (r, a, q % rest2) of stage 1: row_of(r, q % rest2) | row_of(a rest2)
+      const int c2b = row_of<STC, LGFL, S + 1>((r << LGC) + (q & ((1 << LGR2) - 1)));
+      const int row = c2b | row_of<STC, LGFL, S + 1>(a << LGR2);
+      *reinterpret_cast<uint32_t*>(next + op_off(row, q >> LGR2)) = o;
     } else {
       const int e = (r << LGN) + (seg << LGL) + (a << LGR) + q;  // natural order
-      *reinterpret_cast<uint32_t*>(next + op_off(e >> 4, e & 15)) = o;
+      // row e >> 4 = ((r << LGN) + (seg << LGL)) >> 4 | (a << LGR) >> 4 (q < 2^LGR <= 16)
+      static_assert(LGR <= 4, "the last factor-16 stage has rest = FL <= 8");
+      const int rowb = row_of<STC, LGFL, STC>(((r << LGN) + (seg << LGL)) >> 4);
+      const int row = rowb | row_of<STC, LGFL, STC>((a << LGR) >> 4);
+      *reinterpret_cast<uint32_t*>(next + op_off(row, e & 15)) = o;
     }
   }
 }
@@ -322,7 +361,7 @@ __global__ void __launch_bounds__(kThreads)
 #pragma unroll
     for (int s = 0; s < STC; ++s) wt[s] = table_entry<16>(W + 256 * s);
     wt[STC] = table_entry<FL>(W + 256 * STC);
-    store_row<IO>(X0, threadIdx.x, u);
+    store_row<IO>(X0, row_of<STC, LGFL, 0>(threadIdx.x), u);
 #pragma unroll
     for (int s = 0; s <= STC; ++s) store_table(TAB + s * kTab, wt[s]);
   }
@@ -342,7 +381,7 @@ __global__ void __launch_bounds__(kThreads)
     // stores cover whole 32-byte sectors (8 consecutive i per sector)
     float v[32];
     load_col(tm, v);
-    const int J = threadIdx.x, r = J >> (LGN - 4), el0 = (J << 4) & (N - 1);
+    const int J = col_of<STC, LGFL, STC>(threadIdx.x), r = J >> (LGN - 4), el0 = (J << 4) & (N - 1);
     if (b0 + r < B) {
       uint32_t* dst = reinterpret_cast<uint32_t*>(y) + ((size_t)(b0 + r) * H + h) * N;
 #pragma unroll
@@ -395,8 +434,8 @@ __global__ void __launch_bounds__(kThreads, 3)
 #pragma unroll
     for (int s = 0; s < STC; ++s) wt[s] = table_entry<16>(W + 256 * s);
     wt[STC] = table_entry<FL>(W + 256 * STC);
-    store_row<IO>(X0, threadIdx.x, u);
-    store_row<IO>(GA, J, gu);
+    store_row<IO>(X0, row_of<STC, LGFL, 0>(threadIdx.x), u);
+    store_row<IO>(GA, row_of<STC, LGFL, STC>(J), gu);
 #pragma unroll
     for (int s = 0; s <= STC; ++s) store_table(TAB + s * kTab, wt[s]);
   }
@@ -425,14 +464,16 @@ __global__ void __launch_bounds__(kThreads, 3)
     float v[32];
     load_col(tm, v);
     unsigned char* wdst = X0 + STC * kOp;
-    const int J = threadIdx.x, r = J >> (LGN - 4), el0 = (J << 4) & (N - 1);
+    const int J = col_of<STC, LGFL, STC>(threadIdx.x), r = J >> (LGN - 4), el0 = (J << 4) & (N - 1);
 #pragma unroll
     for (int o = 0; o < 16; ++o) {
       const int el = el0 + o, a2 = (el >> LGFL) & 15, q2 = el & (FL - 1);
       const float2 t = __ldg(tw_g + ((a2 * q2) << (LGN - LGFL - 4)));
       const float2 w = cmulc(make_float2(v[2 * o], v[2 * o + 1]), t);
-      const int c2 = (r << LGC) + ((el >> (LGFL + 4)) << LGFL) + q2;
-      *reinterpret_cast<uint32_t*>(wdst + op_off(c2, a2)) = pack_bf16(w);
+      // column (r, el / 16 FL, q2): el / 16 FL = J / FL for every o
+      const int row = row_of<STC, LGFL, STC - 1>((r << LGC) + ((el0 >> (LGFL + 4)) << LGFL)) |
+                      row_of<STC, LGFL, STC - 1>(o & (FL - 1));
+      *reinterpret_cast<uint32_t*>(wdst + op_off(row, a2)) = pack_bf16(w);
     }
   }
   sync_for_mma();
@@ -452,7 +493,7 @@ __global__ void __launch_bounds__(kThreads, 3)
       // column (r, seg, q) of stage 1 (L = n / 16): g'[p] at e = seg L + p rest + q;
       // stage 0 (L' = n): a' = seg, q' = p rest + q, column (r, q')
       constexpr int LGL = LGN - 4, LGR = STC == 2 ? LGL - 4 : 0;
-      const int c = threadIdx.x;
+      const int c = col_of<STC, LGFL, 1>(threadIdx.x);
       const int r = c >> LGC, cc = c & ((1 << LGC) - 1), seg = cc >> LGR, q = cc & ((1 << LGR) - 1);
       const int a2 = seg & 15;
       float v[32];
@@ -464,12 +505,13 @@ __global__ void __launch_bounds__(kThreads, 3)
 #pragma unroll
       for (int p = 0; p < 16; ++p) {
         const float2 o = cmulc(make_float2(v[2 * p], v[2 * p + 1]), t[p]);
-        const int c2 = (r << LGC) + ((seg >> 4) << LGL) + (p << LGR) + q;
-        *reinterpret_cast<uint32_t*>(wdst + op_off(c2, a2)) = pack_bf16(o);
+        // column (r, p rest + q) of stage 0 (seg < 16)
+        const int row = row_of<STC, LGFL, 0>((r << LGC) + q) | row_of<STC, LGFL, 0>(p << LGR);
+        *reinterpret_cast<uint32_t*>(wdst + op_off(row, a2)) = pack_bf16(o);
       }
     } else {
       // stage 0: dx[r][p rest0 + q] = g'[p]
-      const int c = threadIdx.x, r = c >> LGC, q = c & ((1 << LGC) - 1);
+      const int c = col_of<STC, LGFL, 0>(threadIdx.x), r = c >> LGC, q = c & ((1 << LGC) - 1);
       float v[32];
       load_col(tm, v);
       if (b0 + r < B) {
