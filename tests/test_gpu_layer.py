@@ -517,14 +517,16 @@ def test_three_pass_saved_transform(lc, dtype, N):
                   keys=("y", "du", "dK", "dD"))
 
 
-def test_sharded_long_conv_layer_single_rank(lc):
+@pytest.mark.parametrize("dtype,tol", [(torch.float32, 1e-5), (torch.bfloat16, 2e-2)])
+def test_sharded_long_conv_layer_single_rank(lc, dtype, tol):
     """seqshard.sharded_long_conv (pairs of real channels, causal crop, D u)
-    at one rank against the fp64 layer oracle (N = 65536: l = 8192, m = 16)."""
+    at one rank against the fp64 layer oracle (N = 65536: l = 8192, m = 16);
+    bf16 signals in and out (fp32 complex intermediates)."""
     from paper_2302_06646_b200 import seqshard as ss
 
     B, H, N = 3, 2, 65536
     l, m = 8192, 16
-    inp = layer_inputs(lc, B, H, N, torch.float32)
+    inp = layer_inputs(lc, B, H, N, dtype)
     cfg = fb.RegularizationConfig(**CFG)
     kbar = lc.regularize_bank(inp["K"], cfg.lambda_, cfg.smooth_width)
     want = lc.long_conv_forward(inp["u"], kbar, inp["D"])
@@ -533,17 +535,19 @@ def test_sharded_long_conv_layer_single_rank(lc):
     k_cols = torch.tensor(kbar, dtype=torch.float32, device="cuda").reshape(H, m // 2, l)
     y = ss.sharded_long_conv(u_cols, k_cols, inp["tD"], sh, ss.GpuPasses(2 * N))
     torch.cuda.synchronize()
-    assert rel_l2(to_np(y.reshape(B, H, N)), want) < 1e-5
+    assert y.dtype == dtype
+    assert rel_l2(to_np(y.reshape(B, H, N)), want) < tol
 
 
-def test_sharded_long_conv_backward_single_rank(lc):
+@pytest.mark.parametrize("dtype,tol", [(torch.float32, 1e-5), (torch.bfloat16, 2e-2)])
+def test_sharded_long_conv_backward_single_rank(lc, dtype, tol):
     """seqshard.sharded_long_conv_backward on the GPU passes at one rank vs the
-    fp64 backward oracle (du, dKbar, dD)."""
+    fp64 backward oracle (du, dKbar, dD); bf16 signals in the 16-bit case."""
     from paper_2302_06646_b200 import seqshard as ss
 
     B, H, N = 3, 2, 65536
     l, m = 8192, 16
-    inp = layer_inputs(lc, B, H, N, torch.float32)
+    inp = layer_inputs(lc, B, H, N, dtype)
     cfg = fb.RegularizationConfig(**CFG)
     kbar = lc.regularize_bank(inp["K"], cfg.lambda_, cfg.smooth_width)
     du_w, dkbar_w, dD_w = lc.long_conv_backward(inp["u"], inp["dy"], kbar, inp["D"])
@@ -553,9 +557,9 @@ def test_sharded_long_conv_backward_single_rank(lc):
     du, dkbar, dD = ss.sharded_long_conv_backward(cols(inp["tdy"]), cols(inp["tu"]), cols(kt),
                                                   inp["tD"], sh, ss.GpuPasses(2 * N))
     torch.cuda.synchronize()
-    assert rel_l2(to_np(du.reshape(B, H, N)), du_w) < 1e-5
-    assert rel_l2(to_np(dkbar.reshape(H, N)), dkbar_w) < 1e-5
-    assert rel_l2(to_np(dD), dD_w) < 1e-5
+    assert rel_l2(to_np(du.reshape(B, H, N)), du_w) < tol
+    assert rel_l2(to_np(dkbar.reshape(H, N)), dkbar_w) < tol
+    assert rel_l2(to_np(dD), dD_w) < tol
 
 
 @pytest.mark.parametrize("dtype,world", [(torch.bfloat16, 4), (torch.float32, 2)])
