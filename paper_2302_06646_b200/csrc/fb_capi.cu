@@ -521,8 +521,12 @@ int fb_bwd(fb_plan* p, const void* dy, const void* u, void* du, float* dK, float
 }  // extern "C"
 
 // ---------------------------------------------------------------- host runner
+constexpr int kRunnerBufs = 3;  // device buffer sets: copies of chunks c-1, c, c+1 in flight
 struct fb_host_runner {
   fb_plan* plan = nullptr;  // Hc heads, reused chunk after chunk on the compute stream
+  // Hc / 2 and Hc / 4 heads: the first and last chunks are smaller, so the
+  // pipeline fills and drains in a fraction of a full chunk's copy time
+  fb_plan* small[2] = {nullptr, nullptr};
   int64_t N = 0, H = 0, Hc = 0, B = 0;
   size_t es = 2;
   cudaStream_t s_in = nullptr, s_comp = nullptr, s_out = nullptr;
@@ -533,7 +537,7 @@ struct fb_host_runner {
     float *K = nullptr, *D = nullptr, *dK = nullptr, *dD = nullptr;
     cudaEvent_t in_ready = nullptr, comp_done = nullptr, out_done = nullptr;
     bool used = false;
-  } buf[2];
+  } buf[kRunnerBufs];
 };
 
 extern "C" {
@@ -561,6 +565,8 @@ int fb_host_runner_destroy(fb_host_runner* r) {
   if (r->s_comp) cudaStreamDestroy(r->s_comp);
   if (r->s_out) cudaStreamDestroy(r->s_out);
   fb_plan_destroy(r->plan);
+  fb_plan_destroy(r->small[0]);
+  fb_plan_destroy(r->small[1]);
   delete r;
   return FB_OK;
 }
@@ -583,6 +589,14 @@ int fb_host_runner_create(fb_host_runner** out, int64_t N, int64_t H, int mode, 
   if (rc) {
     delete r;
     return rc;
+  }
+  if (H / hc >= 4 && hc % 4 == 0) {
+    rc = fb_plan_create(&r->small[0], N, hc / 2, mode, dtype, engine, device);
+    if (!rc) rc = fb_plan_create(&r->small[1], N, hc / 4, mode, dtype, engine, device);
+    if (rc) {
+      fb_host_runner_destroy(r);
+      return rc;
+    }
   }
   const size_t sig = (size_t)B * hc * N * r->es, bank = (size_t)hc * N * sizeof(float);
   const size_t wsb = fb_workspace_size(r->plan, B);
@@ -630,41 +644,54 @@ int fb_host_runner_run(fb_host_runner* r, const fb_reg_config* cfg, int training
   cudaStream_t caller = (cudaStream_t)stream;
   const int64_t N = r->N, H = r->H, Hc = r->Hc, B = r->B;
   const size_t es = r->es;
-  const size_t row = (size_t)Hc * N * es, pitch = (size_t)H * N * es;  // one batch row of a chunk
+  const size_t pitch = (size_t)H * N * es;  // host row pitch (one batch row of all heads)
   rc = cuda_status(cudaEventRecord(r->start, caller), "event record");
   for (cudaStream_t s : {r->s_in, r->s_comp, r->s_out})
     if (!rc) rc = cuda_status(cudaStreamWaitEvent(s, r->start, 0), "stream wait");
-  const int64_t chunks = H / Hc;
-  for (int64_t c = 0; c < chunks && !rc; ++c) {
-    auto& b = r->buf[c & 1];
-    const int64_t h0 = c * Hc;
+  // chunk schedule: Hc heads each, or (small plans present) Hc/4, Hc/4, Hc/2,
+  // Hc ..., Hc/2, Hc/4, Hc/4
+  std::vector<fb_plan*> sched;
+  if (r->small[0]) {
+    sched = {r->small[1], r->small[1], r->small[0]};
+    for (int64_t i = 0; i < H / Hc - 2; ++i) sched.push_back(p);
+    for (fb_plan* q : {r->small[0], r->small[1], r->small[1]}) sched.push_back(q);
+  } else {
+    sched.assign((size_t)(H / Hc), p);
+  }
+  int64_t h0 = 0;
+  for (size_t c = 0; c < sched.size() && !rc; ++c) {
+    auto& b = r->buf[c % kRunnerBufs];
+    fb_plan* q = sched[c];
+    const int64_t Hk = q->H;
+    const size_t row = (size_t)Hk * N * es;
     const char* hu = (const char*)u + h0 * N * es;
     const char* hdy = (const char*)dy + h0 * N * es;
     // inputs: the previous user of this buffer must be done reading u / dy
     if (b.used) rc = cuda_status(cudaStreamWaitEvent(r->s_in, b.comp_done, 0), "wait");
     if (!rc) rc = cuda_status(cudaMemcpy2DAsync(b.u, row, hu, pitch, row, B, cudaMemcpyHostToDevice, r->s_in), "h2d u");
     if (!rc) rc = cuda_status(cudaMemcpy2DAsync(b.dy, row, hdy, pitch, row, B, cudaMemcpyHostToDevice, r->s_in), "h2d dy");
-    if (!rc) rc = cuda_status(cudaMemcpyAsync(b.K, K + h0 * N, Hc * N * sizeof(float), cudaMemcpyHostToDevice, r->s_in), "h2d K");
-    if (!rc) rc = cuda_status(cudaMemcpyAsync(b.D, D + h0, Hc * sizeof(float), cudaMemcpyHostToDevice, r->s_in), "h2d D");
+    if (!rc) rc = cuda_status(cudaMemcpyAsync(b.K, K + h0 * N, Hk * N * sizeof(float), cudaMemcpyHostToDevice, r->s_in), "h2d K");
+    if (!rc) rc = cuda_status(cudaMemcpyAsync(b.D, D + h0, Hk * sizeof(float), cudaMemcpyHostToDevice, r->s_in), "h2d D");
     if (!rc) rc = cuda_status(cudaEventRecord(b.in_ready, r->s_in), "event record");
     // compute: inputs landed, and the previous results of this buffer copied out
     if (!rc) rc = cuda_status(cudaStreamWaitEvent(r->s_comp, b.in_ready, 0), "wait");
     if (!rc && b.used) rc = cuda_status(cudaStreamWaitEvent(r->s_comp, b.out_done, 0), "wait");
-    p->head0 = h0;
-    if (!rc) rc = fb_kernel_prep(p, b.K, b.D, cfg, training, r->s_comp);
-    if (!rc) rc = fb_fwd_save(p, b.u, b.y, b.saved, B, b.ws, r->s_comp);
-    if (!rc) rc = fb_bwd_saved(p, b.dy, b.u, b.saved, b.du, b.dK, nullptr, b.dD, B, b.ws, r->s_comp);
+    q->head0 = h0;
+    if (!rc) rc = fb_kernel_prep(q, b.K, b.D, cfg, training, r->s_comp);
+    if (!rc) rc = fb_fwd_save(q, b.u, b.y, b.saved, B, b.ws, r->s_comp);
+    if (!rc) rc = fb_bwd_saved(q, b.dy, b.u, b.saved, b.du, b.dK, nullptr, b.dD, B, b.ws, r->s_comp);
     if (!rc) rc = cuda_status(cudaEventRecord(b.comp_done, r->s_comp), "event record");
     // outputs
     if (!rc) rc = cuda_status(cudaStreamWaitEvent(r->s_out, b.comp_done, 0), "wait");
     if (!rc) rc = cuda_status(cudaMemcpy2DAsync((char*)y + h0 * N * es, pitch, b.y, row, row, B, cudaMemcpyDeviceToHost, r->s_out), "d2h y");
     if (!rc) rc = cuda_status(cudaMemcpy2DAsync((char*)du + h0 * N * es, pitch, b.du, row, row, B, cudaMemcpyDeviceToHost, r->s_out), "d2h du");
-    if (!rc) rc = cuda_status(cudaMemcpyAsync(dK + h0 * N, b.dK, Hc * N * sizeof(float), cudaMemcpyDeviceToHost, r->s_out), "d2h dK");
-    if (!rc) rc = cuda_status(cudaMemcpyAsync(dD + h0, b.dD, Hc * sizeof(float), cudaMemcpyDeviceToHost, r->s_out), "d2h dD");
+    if (!rc) rc = cuda_status(cudaMemcpyAsync(dK + h0 * N, b.dK, Hk * N * sizeof(float), cudaMemcpyDeviceToHost, r->s_out), "d2h dK");
+    if (!rc) rc = cuda_status(cudaMemcpyAsync(dD + h0, b.dD, Hk * sizeof(float), cudaMemcpyDeviceToHost, r->s_out), "d2h dD");
     if (!rc) rc = cuda_status(cudaEventRecord(b.out_done, r->s_out), "event record");
     b.used = true;
+    q->head0 = 0;
+    h0 += Hk;
   }
-  p->head0 = 0;
   // the caller's stream resumes after everything
   for (auto& b : r->buf)
     if (!rc && b.used) rc = cuda_status(cudaStreamWaitEvent(caller, b.out_done, 0), "wait");

@@ -407,7 +407,10 @@ def test_config3_heads_sample(lc):
 # ------------------------------------------------------------ host-buffer runner
 @pytest.mark.parametrize("dtype,H,hc,training,N", [(torch.bfloat16, 12, 4, False, 4096),
                                                    (torch.float32, 6, 2, True, 4096),
-                                                   (torch.bfloat16, 4, 2, False, 16384)])
+                                                   (torch.bfloat16, 4, 2, False, 16384),
+                                                   # H / hc >= 4: small first / last chunks
+                                                   (torch.bfloat16, 32, 8, True, 4096),
+                                                   (torch.float32, 16, 4, False, 4096)])
 def test_host_runner_matches_device_path(lc, dtype, H, hc, training, N):
     """fb_host_runner (pinned host buffers, heads in pipelined chunks) gives
     the device path's results: y / du per channel bit-identical, dK / dD up to
