@@ -170,6 +170,11 @@ int fb_plan_create(fb_plan** out, int64_t N, int64_t H, int mode, int dtype, int
   p->device = device;
   int64_t n = mode == FB_MODE_CAUSAL ? next_pow2(2 * N) : N;
   if (n < kMinTransform) n = kMinTransform;
+  // the tensor-core single pass also serves N = 2048 on its n = 8192 transform
+  const bool tc_pad = mode == FB_MODE_CAUSAL && N == 2048 && dtype != FB_F32 &&
+                      (engine == FB_ENGINE_AUTO || engine == FB_ENGINE_SINGLE) && tc_length_ok(N) &&
+                      !(std::getenv("FB_TC2") && std::getenv("FB_TC2")[0] == '1');
+  if (tc_pad) n = 8192;
   p->n = n;
   p->periodic = (mode == FB_MODE_CIRCULAR) && n > N;
   const bool simt = engine == FB_ENGINE_SINGLE_SIMT;

@@ -115,6 +115,7 @@ int tc_rows_bwd(fb_plan* p, void* x1dy, const void* usave, float2* wdk, int64_t 
 int tc_init(fb_plan* p);
 // version 2 (fb_tc2.cu)
 int tc2_init(fb_plan* p);
+bool tc_length_ok(int64_t N);
 int tc2_fwd(fb_plan* p, const void* u, void* y, int64_t B, int ctas, int total, cudaStream_t s,
             void* usave, bool spectrum_only);
 int tc2_bwd(fb_plan* p, const void* dy, void* du, int64_t B, int ctas, int total, int maxseg,

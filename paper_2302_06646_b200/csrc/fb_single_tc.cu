@@ -208,12 +208,17 @@ __device__ __forceinline__ void tma_load_4d(void* dst, const CUtensorMap* map, i
       : "memory");
 }
 
-// Channel pair (b0, b0+1) of head h: 4 boxes [64 t2][32 t1] (4 KB each),
+// Data rows t1 of a channel: N / 128 = 32 (N = 4096) or 16 (N = 2048, the
+// same n = 8192 transform with u zero beyond 2048: stage A skips the K steps
+// of rows 16..31, the A' exit stores rows < 16).  Set once per CTA.
+__shared__ uint32_t g_rows;
+
+// Channel pair (b0, b0+1) of head h: 4 boxes [64 t2][g_rows t1] (4 KB / 2 KB),
 // channel c of 64-row block mb at dst + mb * 8 KB + c * 4 KB.  An odd batch's
 // missing partner is out of bounds and arrives as zeros.
 __device__ __forceinline__ void load_pair(unsigned char* dst, const CUtensorMap* map, int h, int b0,
                                           uint64_t* bar) {
-  ptx::mbar_arrive_expect_tx(bar, 4 * 4096);
+  ptx::mbar_arrive_expect_tx(bar, 4 * 128 * g_rows);
 #pragma unroll
   for (int mb = 0; mb < 2; ++mb)
 #pragma unroll
@@ -321,8 +326,11 @@ __device__ __forceinline__ void cta_sync_tc() {
 template <typename T>
 __device__ __forceinline__ void mma_stage_A(const Ctx& c) {
   const uint32_t id = idesc<T>(128, 128, true, false);
-#pragma unroll
-  for (uint32_t s = 0; s < 4; ++s) {
+  // K steps s: channel s / 2, rows t1 16 (s % 2) .. +15; with 16 data rows the
+  // odd steps would only multiply zero padding
+  const uint32_t step = g_rows == 32 ? 1 : 2;
+#pragma unroll 1
+  for (uint32_t s = 0; s < 4; s += step) {
     const uint64_t ad = tc::smem_desc(c.smb + c.in_off + s * 2048, 1024, tc::kSw128, 8192);
     const uint64_t bd = tc::smem_desc(c.smb + c.smat + MAT_FA + s * 32, 1024, tc::kSw128);
     tc::mma_bf16(c.tmem + c.tw, ad, bd, id, s);
@@ -602,11 +610,13 @@ __device__ __forceinline__ void store_rows(const Ctx& c, T* __restrict__ out, in
   tld<R>(taddr(c, c.tw + R * g), re);
   tld<R>(taddr(c, c.tw + 32 + R * g), im);
   tc::ld_wait();
-  T* o0 = out + ((size_t)b0 * H + h) * 4096 + 128 * (R * g) + t2;
+  const uint32_t rows = g_rows, N = 128 * rows;
+  if (R * g >= rows) return;  // beyond the data rows (N = 2048)
+  T* o0 = out + ((size_t)b0 * H + h) * N + 128 * (R * g) + t2;
 #pragma unroll
   for (int j = 0; j < R; ++j) o0[128 * j] = cvt<T>(re[j]);
   if (b0 + 1 < B) {
-    T* o1 = out + ((size_t)(b0 + 1) * H + h) * 4096 + 128 * (R * g) + t2;
+    T* o1 = out + ((size_t)(b0 + 1) * H + h) * N + 128 * (R * g) + t2;
 #pragma unroll
     for (int j = 0; j < R; ++j) o1[128 * j] = cvt<T>(im[j]);
   }
@@ -782,11 +792,13 @@ __device__ __forceinline__ void store_rows_sc(const Ctx& c, T* __restrict__ out,
   tld<R>(taddr(c, c.tw + R * g), re);
   tld<R>(taddr(c, c.tw + 32 + R * g), im);
   tc::ld_wait();
-  T* o0 = out + ((size_t)b0 * H + h) * 4096 + 128 * (R * g) + t2;
+  const uint32_t rows = g_rows, N = 128 * rows;
+  if (R * g >= rows) return;  // beyond the data rows (N = 2048)
+  T* o0 = out + ((size_t)b0 * H + h) * N + 128 * (R * g) + t2;
 #pragma unroll
   for (int j = 0; j < R; ++j) o0[128 * j] = cvt<T>(re[j] * sc);
   if (b0 + 1 < B) {
-    T* o1 = out + ((size_t)(b0 + 1) * H + h) * 4096 + 128 * (R * g) + t2;
+    T* o1 = out + ((size_t)(b0 + 1) * H + h) * N + 128 * (R * g) + t2;
 #pragma unroll
     for (int j = 0; j < R; ++j) o1[128 * j] = cvt<T>(im[j] * sc);
   }
@@ -804,7 +816,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     tc_fwd_kernel(const __grid_constant__ CUtensorMap umap, T* __restrict__ y,
                   const __half2* __restrict__ kf16, const float* __restrict__ kscale,
                   const uint4* __restrict__ mats, const float2* __restrict__ tab_g, int B, int H,
-                  int total, uint32_t* __restrict__ usave, int sched) {
+                  int total, uint32_t* __restrict__ usave, int sched, int rows) {
   // bf16 planes take the scaled product (k_f' x 2^e, e <= ~30) and the
   // store undoes the scale; fp16 planes need it applied at the B exit
   constexpr bool kScaleEarly = std::is_same<T, __half>::value;
@@ -816,7 +828,10 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int npairs = (B + 1) / 2;
   int i0, i1;
   cta_range(total, i0, i1);
-  if (threadIdx.x == 0) mma_lock = 0;
+  if (threadIdx.x == 0) {
+    mma_lock = 0;
+    g_rows = (uint32_t)rows;
+  }
   setup(sm, &tmem_slot, bars, 4, 0, mats, tab_g, SMAT3, STAB3);
   const uint32_t slot = threadIdx.x / kSlotThreads;
   Ctx c = make_ctx(sm, tmem_slot, slot, &bars[slot], true);
@@ -940,7 +955,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                   const float* __restrict__ kscale, const uint4* __restrict__ mats,
                   const float2* __restrict__ tab_g, float* __restrict__ tpart, int B, int H,
                   int total, int maxseg, const uint32_t* __restrict__ usave,
-                  uint32_t* __restrict__ uscratch, int sched) {
+                  uint32_t* __restrict__ uscratch, int sched, int rows) {
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   __shared__ uint32_t tmem_slot;
   __shared__ __align__(8) uint64_t bars[6];  // mma[2], in[2], S chain[2] (256 arrivals)
@@ -950,7 +965,10 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int npairs = (B + 1) / 2;
   int i0, i1;
   cta_range_even(total, i0, i1);
-  if (threadIdx.x == 0) mma_lock = 0;
+  if (threadIdx.x == 0) {
+    mma_lock = 0;
+    g_rows = (uint32_t)rows;
+  }
   setup(sm, &tmem_slot, bars, 6, 2, mats, tab_g, SMAT3, STAB3);
   const uint32_t slot = threadIdx.x / kSlotThreads;
   Ctx c = make_ctx(sm, tmem_slot, slot, &bars[slot], true);
@@ -1179,12 +1197,15 @@ __global__ void __launch_bounds__(kThreads, 1)
 // dKbar[h] = sum of the head's time-domain partials (CTA order, fixed), dD =
 // dKbar[0] (lag 0), dK = the regularizer chain rule (fp64 tap sums in the
 // reference order) — the tail of the tensor-core backward
+template <uint32_t N>
 __global__ void __launch_bounds__(512)
     tc_dk_tail_kernel(const float* __restrict__ tpart, float* __restrict__ dkbar_out,
                       float* __restrict__ dD, const float* __restrict__ kbar,
                       const uint8_t* __restrict__ keep, float* __restrict__ dK, int64_t p,
                       double keep_scale, int freq, int ctas, int total, int npairs, int maxseg) {
-  constexpr uint32_t N = 4096, kPer = 8;  // 512 threads x 8 consecutive lags
+  // 512 threads x kPer consecutive lags; partial rows hold lags 0..4095
+  constexpr uint32_t kPer = N / 512, kPitch = 4096;
+  static_assert(kPer == 8 || kPer == 4, "N = 4096 or 2048");
   __shared__ float row[N];
   __shared__ const float* src[8];
   const int h = blockIdx.x;
@@ -1196,32 +1217,37 @@ __global__ void __launch_bounds__(512)
   const int nc = c1 - c0 + 1;
   auto part = [&](int c) {  // CTA c's partial row of head h (segment h - its first head)
     const int64_t start = 2 * ((int64_t)c * U / G);
-    return tpart + ((size_t)c * maxseg + (h - (int)(start / np))) * N;
+    return tpart + ((size_t)c * maxseg + (h - (int)(start / np))) * kPitch;
   };
   if (threadIdx.x < (unsigned)min(nc, 8)) src[threadIdx.x] = part(c0 + (int)threadIdx.x);
   __syncthreads();
   const size_t base = (size_t)h * N;
   const uint32_t t0 = threadIdx.x * kPer;
   // sum the partials in CTA order (deterministic), 16-byte loads
-  float4 g0 = make_float4(0.f, 0.f, 0.f, 0.f), g1 = g0;
+  constexpr uint32_t V = kPer / 4;
+  float4 gv[V];
+#pragma unroll
+  for (uint32_t v = 0; v < V; ++v) gv[v] = make_float4(0.f, 0.f, 0.f, 0.f);
   for (int c = 0; c < nc; ++c) {
     const float4* sp = reinterpret_cast<const float4*>((c < 8 ? src[c] : part(c0 + c)) + t0);
-    const float4 a = __ldg(sp), b = __ldg(sp + 1);
-    g0.x += a.x; g0.y += a.y; g0.z += a.z; g0.w += a.w;
-    g1.x += b.x; g1.y += b.y; g1.z += b.z; g1.w += b.w;
-  }
-  if (dkbar_out) {
-    reinterpret_cast<float4*>(dkbar_out + base + t0)[0] = g0;
-    reinterpret_cast<float4*>(dkbar_out + base + t0)[1] = g1;
-  }
-  if (threadIdx.x == 0) dD[h] = g0.x;
-  const float g[kPer] = {g0.x, g0.y, g0.z, g0.w, g1.x, g1.y, g1.z, g1.w};
-  {
-    const float4 k0 = __ldg(reinterpret_cast<const float4*>(kbar + base + t0));
-    const float4 k1 = __ldg(reinterpret_cast<const float4*>(kbar + base + t0) + 1);
-    const float kb[kPer] = {k0.x, k0.y, k0.z, k0.w, k1.x, k1.y, k1.z, k1.w};
 #pragma unroll
-    for (uint32_t j = 0; j < kPer; ++j) row[t0 + j] = (!freq && kb[j] == 0.f) ? 0.f : g[j];
+    for (uint32_t v = 0; v < V; ++v) {
+      const float4 a = __ldg(sp + v);
+      gv[v].x += a.x; gv[v].y += a.y; gv[v].z += a.z; gv[v].w += a.w;
+    }
+  }
+  if (dkbar_out)
+#pragma unroll
+    for (uint32_t v = 0; v < V; ++v) reinterpret_cast<float4*>(dkbar_out + base + t0)[v] = gv[v];
+  if (threadIdx.x == 0) dD[h] = gv[0].x;
+  {
+#pragma unroll
+    for (uint32_t v = 0; v < V; ++v) {
+      const float4 k4 = __ldg(reinterpret_cast<const float4*>(kbar + base + t0) + v);
+      const float kb[4] = {k4.x, k4.y, k4.z, k4.w}, g[4] = {gv[v].x, gv[v].y, gv[v].z, gv[v].w};
+#pragma unroll
+      for (uint32_t j = 0; j < 4; ++j) row[t0 + 4 * v + j] = (!freq && kb[j] == 0.f) ? 0.f : g[j];
+    }
   }
   __syncthreads();
   if (!freq) {
@@ -1239,8 +1265,9 @@ __global__ void __launch_bounds__(512)
       if (keep) gg = keep[base + t] ? gg * keep_scale : 0.0;
       o[j] = (float)gg;
     }
-    reinterpret_cast<float4*>(dK + base + t0)[0] = make_float4(o[0], o[1], o[2], o[3]);
-    reinterpret_cast<float4*>(dK + base + t0)[1] = make_float4(o[4], o[5], o[6], o[7]);
+#pragma unroll
+    for (uint32_t v = 0; v < kPer / 4; ++v)
+      reinterpret_cast<float4*>(dK + base + t0)[v] = make_float4(o[4 * v], o[4 * v + 1], o[4 * v + 2], o[4 * v + 3]);
   } else {
     for (uint32_t t = threadIdx.x; t < N; t += blockDim.x)
       dK[base + t] = reg_grad(kbar + base, row, keep ? keep + base : nullptr, t, N, p, keep_scale,
@@ -1702,17 +1729,17 @@ int encode_map_3d(CUtensorMap* map, CUtensorMapDataType type, const void* ptr, c
 
 namespace {
 
-// signal [B][H][4096] viewed as [B][H][32 t1][128 t2]; box [64 t2][32 t1][1][1]
+// signal [B][H][N] viewed as [B][H][N/128 t1][128 t2]; box [64 t2][N/128 t1][1][1]
 template <typename T>
-int make_map(CUtensorMap* map, const void* ptr, int64_t B, int64_t H) {
+int make_map(CUtensorMap* map, const void* ptr, int64_t B, int64_t H, int64_t N) {
   EncodeFn enc = encode_fn();
   if (!enc) {
     set_error("tcgen05 path: cuTensorMapEncodeTiled unavailable");
     return FB_ERR_CUDA;
   }
-  const cuuint64_t dims[4] = {128, 32, (cuuint64_t)H, (cuuint64_t)B};
-  const cuuint64_t strides[3] = {128 * 2, 4096 * 2, (cuuint64_t)H * 4096 * 2};
-  const cuuint32_t box[4] = {64, 32, 1, 1};
+  const cuuint64_t dims[4] = {128, (cuuint64_t)(N / 128), (cuuint64_t)H, (cuuint64_t)B};
+  const cuuint64_t strides[3] = {128 * 2, (cuuint64_t)N * 2, (cuuint64_t)H * N * 2};
+  const cuuint32_t box[4] = {64, (cuuint32_t)(N / 128), 1, 1};
   const cuuint32_t es[4] = {1, 1, 1, 1};
   CUresult r = enc(map, Fmt<T>::tma, 4, const_cast<void*>(ptr), dims, strides, box, es,
                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
@@ -1753,9 +1780,13 @@ static int tc_sched() {
   return v;
 }
 
+// N = 4096, and N = 2048 run on the same n = 8192 transform (fb_plan_create
+// picks n = 8192 for it): the extra zero padding costs transform work but the
+// tensor-core path still beats the CUDA-core one there
+bool tc_length_ok(int64_t N) { return N == 4096 || N == 2048; }
 bool tc_eligible(const fb_plan* p) {
-  return p->mode == FB_MODE_CAUSAL && p->N == 4096 && p->n == 8192 &&
-         (p->dtype == FB_BF16 || p->dtype == FB_F16);
+  return p->mode == FB_MODE_CAUSAL && tc_length_ok(p->N) && p->n == 8192 &&
+         (p->dtype == FB_BF16 || p->dtype == FB_F16) && (p->tc_ver == 1 || p->N == 4096);
 }
 
 int tc_init(fb_plan* p) {
@@ -1785,7 +1816,7 @@ int tc_fwd(fb_plan* p, const void* u, void* y, int64_t B, cudaStream_t s, void* 
   CUtensorMap map;
   auto go = [&](auto tv) {
     using T = decltype(tv);
-    int rc = make_map<T>(&map, u, B, p->H);
+    int rc = make_map<T>(&map, u, B, p->H, p->N);
     if (rc) return rc;
     auto k = tc_fwd_kernel<T>;
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM_FWD);
@@ -1793,7 +1824,7 @@ int tc_fwd(fb_plan* p, const void* u, void* y, int64_t B, cudaStream_t s, void* 
     k<<<(unsigned)gr.ctas, kThreads, SMEM_FWD, s>>>(map, (T*)y, (const __half2*)p->kf_tc,
                                                      p->kf_scale, (const uint4*)p->tc_mats, p->tw2,
                                                      (int)B, (int)p->H, gr.total,
-                                                     (uint32_t*)usave, tc_sched());
+                                                     (uint32_t*)usave, tc_sched(), (int)(p->N / 128));
     prof_mark(p, 0, 1, s);
     return cuda_status(cudaGetLastError(), "tc_fwd");
   };
@@ -1810,6 +1841,15 @@ size_t tc_workspace(const fb_plan* p, int64_t B) {
   return tpart_bytes(gr) + tc_saved_size(p, B) + 256;
 }
 
+static int dk_tail(const fb_plan* p, const TcGrid& gr, const float* tpart, float* dKbar, float* dD,
+                   float* dK, cudaStream_t s) {
+  auto k = p->N == 4096 ? tc_dk_tail_kernel<4096> : tc_dk_tail_kernel<2048>;
+  k<<<(unsigned)p->H, 512, 0, s>>>(tpart, dKbar, dD, p->kbar, p->use_keep ? p->keep : nullptr, dK,
+                                   p->p, p->keep_scale, p->smooth_domain == FB_SMOOTH_FREQUENCY,
+                                   gr.bctas, gr.total, gr.npairs, gr.maxseg);
+  return cuda_status(cudaGetLastError(), "tc_dk_tail");
+}
+
 int tc_bwd(fb_plan* p, const void* dy, const void* u, void* du, float* dK, float* dKbar, float* dD,
            int64_t B, void* ws, cudaStream_t s, const void* usave) {
   const TcGrid gr = tc_grid(p, B);
@@ -1823,16 +1863,13 @@ int tc_bwd(fb_plan* p, const void* dy, const void* u, void* du, float* dK, float
     }
     if (!rc) rc = tc2_bwd(p, dy, du, B, gr.bctas, gr.total, gr.maxseg, tpart, usave, s);
     if (rc) return rc;
-    tc_dk_tail_kernel<<<(unsigned)p->H, 512, 0, s>>>(
-        tpart, dKbar, dD, p->kbar, p->use_keep ? p->keep : nullptr, dK, p->p, p->keep_scale,
-        p->smooth_domain == FB_SMOOTH_FREQUENCY, gr.bctas, gr.total, gr.npairs, gr.maxseg);
-    return cuda_status(cudaGetLastError(), "tc_dk_tail");
+    return dk_tail(p, gr, tpart, dKbar, dD, dK, s);
   }
   CUtensorMap dmap, umap;
   auto go = [&](auto tv) {
     using T = decltype(tv);
-    int rc = make_map<T>(&dmap, dy, B, p->H);
-    if (!rc) rc = make_map<T>(&umap, usave ? dy : u, B, p->H);
+    int rc = make_map<T>(&dmap, dy, B, p->H, p->N);
+    if (!rc) rc = make_map<T>(&umap, usave ? dy : u, B, p->H, p->N);
     if (rc) return rc;
     auto launch = [&](auto kern) {
       cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM_BWD3);
@@ -1840,7 +1877,7 @@ int tc_bwd(fb_plan* p, const void* dy, const void* u, void* du, float* dK, float
       kern<<<(unsigned)gr.bctas, kThreads, SMEM_BWD3, s>>>(
           dmap, umap, (T*)du, (const __half2*)p->kf_tc, p->kf_scale, (const uint4*)p->tc_mats,
           p->tw2, tpart, (int)B, (int)p->H, gr.total, gr.maxseg, (const uint32_t*)usave,
-          uscratch, tc_sched());
+          uscratch, tc_sched(), (int)(p->N / 128));
       prof_mark(p, 1, 1, s);
     };
     if (usave) launch(tc_bwd_kernel<T, true>);
@@ -1849,10 +1886,7 @@ int tc_bwd(fb_plan* p, const void* dy, const void* u, void* du, float* dK, float
   };
   int rc = p->dtype == FB_BF16 ? go(__nv_bfloat16{}) : go(__half{});
   if (rc) return rc;
-  tc_dk_tail_kernel<<<(unsigned)p->H, 512, 0, s>>>(
-      tpart, dKbar, dD, p->kbar, p->use_keep ? p->keep : nullptr, dK, p->p, p->keep_scale,
-      p->smooth_domain == FB_SMOOTH_FREQUENCY, gr.bctas, gr.total, gr.npairs, gr.maxseg);
-  return cuda_status(cudaGetLastError(), "tc_dk_tail");
+  return dk_tail(p, gr, tpart, dKbar, dD, dK, s);
 }
 
 // ---------------------------------------------------------------- three-pass rows (host)

@@ -219,23 +219,23 @@ def test_dimension_errors():
 
 
 # ------------------------------------------------------------ tcgen05 single-pass
+@pytest.mark.parametrize("N", [4096, 2048])
 @pytest.mark.parametrize("dtype", [torch.bfloat16, torch.float16])
 @pytest.mark.parametrize("B,H", [(2, 2), (3, 3), (5, 1)])
-def test_tensor_core_single_pass(lc, dtype, B, H):
-    N = 4096
+def test_tensor_core_single_pass(lc, dtype, B, H, N):
+    """N = 4096, and N = 2048 on the same n = 8192 transform (16 data rows)."""
     inp = layer_inputs(lc, B, H, N, dtype)
     cfg = fb.RegularizationConfig(**CFG)
     plan, got = run_layer(inp, N, H, dtype, cfg, engine=1)
-    assert plan.tensor_cores, "16-bit causal N=4096 must run on tcgen05"
+    assert plan.tensor_cores, "16-bit causal N=4096 / 2048 must run on tcgen05"
     assert_parity(got, oracle_layer(lc, inp, cfg), TOL[dtype])
 
 
-@pytest.mark.parametrize("B,H", [(32, 20), (9, 37), (64, 6)])
-def test_tensor_core_persistent_shares(lc, B, H):
+@pytest.mark.parametrize("B,H,N", [(32, 20, 4096), (9, 37, 4096), (64, 6, 4096), (9, 37, 2048)])
+def test_tensor_core_persistent_shares(lc, B, H, N):
     """Pair counts above the SM count: the persistent CTAs' shares straddle
     head boundaries (several head segments per CTA, several CTAs per head),
     which exercises the k_f' reloads and the dK-partial bookkeeping."""
-    N = 4096
     dtype = torch.bfloat16
     inp = layer_inputs(lc, B, H, N, dtype)
     cfg = fb.RegularizationConfig(**CFG)
@@ -434,13 +434,12 @@ def test_host_runner_matches_device_path(lc, dtype, H, hc, training, N):
     assert rel_l2(to_np(dD), want["dD"]) < tol
 
 
-@pytest.mark.parametrize("B,H,dtype", [(32, 20, torch.bfloat16), (7, 3, torch.bfloat16),
-                                       (6, 4, torch.float16)])
-def test_tensor_core_saved_transform(lc, B, H, dtype):
+@pytest.mark.parametrize("B,H,dtype,N", [(32, 20, torch.bfloat16, 4096), (7, 3, torch.bfloat16, 4096),
+                                         (6, 4, torch.float16, 4096), (7, 3, torch.bfloat16, 2048)])
+def test_tensor_core_saved_transform(lc, B, H, dtype, N):
     """fb_fwd_save / fb_bwd_saved (the backward reads the forward's transform
     of u) gives bit-identical results to the recompute path: it parks exactly
     the same bf16 values."""
-    N = 4096
     inp = layer_inputs(lc, B, H, N, dtype)
     cfg = fb.RegularizationConfig(**CFG)
     plan, want = run_layer(inp, N, H, dtype, cfg, engine=1)
