@@ -212,6 +212,8 @@ __device__ __forceinline__ void tma_load_4d(void* dst, const CUtensorMap* map, i
 // same n = 8192 transform with u zero beyond 2048: stage A skips the K steps
 // of rows 16..31, the A' exit stores rows < 16).  Set once per CTA.
 __shared__ uint32_t g_rows;
+// the CTA's one-time bulk load of its DFT blocks (setup)
+__shared__ __align__(8) uint64_t g_setup_bar;
 
 // Channel pair (b0, b0+1) of head h: 4 boxes [64 t2][g_rows t1] (4 KB / 2 KB),
 // channel c of 64-row block mb at dst + mb * 8 KB + c * 4 KB.  An odd batch's
@@ -629,14 +631,21 @@ __device__ __forceinline__ void setup(unsigned char* sm, uint32_t* tmem_slot, ui
   if (threadIdx.x < 32) tc::alloc<512>(tmem_slot);
   if (threadIdx.x == 0) {
     for (int i = 0; i < nbars; ++i) ptx::mbar_init(&bars[i], i < nbars - nbars_slot ? 1 : kSlotThreads);
+    ptx::mbar_init(&g_setup_bar, 1);
     ptx::fence_barrier_init();
+    // the DFT blocks (80-96 KB) as a few bulk copies: one L2 round trip
+    // instead of a dependent load/store loop per thread (measured ~6 % of
+    // the forward's samples there)
+    ptx::mbar_arrive_expect_tx(&g_setup_bar, mat_bytes);
+    for (uint32_t off = 0; off < mat_bytes; off += 16384)
+      ptx::bulk_g2s(sm + smat + off, reinterpret_cast<const char*>(mats) + off,
+                    mat_bytes - off < 16384 ? mat_bytes - off : 16384, &g_setup_bar);
   }
-  uint4* dm = reinterpret_cast<uint4*>(sm + smat);
-  for (uint32_t i = threadIdx.x; i < mat_bytes / 16; i += kThreads) dm[i] = __ldg(mats + i);
   float2* tab = reinterpret_cast<float2*>(sm + stab);
   for (uint32_t i = threadIdx.x; i < 192; i += kThreads) tab[i] = __ldg(tab_g + i);
   ptx::fence_proxy_async_smem();
   cta_sync_tc();
+  ptx::mbar_wait(&g_setup_bar, 0);
 }
 
 __device__ __forceinline__ void teardown(uint32_t tmem) {
