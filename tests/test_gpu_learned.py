@@ -116,7 +116,7 @@ def test_config4_shape_16bit(lc, dtype):
     assert rel_l2(db.cpu().numpy()[heads], rdb) < 2e-2
 
 
-@pytest.mark.parametrize("n,B", [(32, 5), (64, 3), (128, 2), (512, 9), (1024, 6), (1024, 10), (2048, 3), (2048, 19)])
+@pytest.mark.parametrize("n,B", [(32, 5), (64, 3), (128, 2), (512, 9), (1024, 1), (1024, 6), (1024, 10), (2048, 3), (2048, 19)])
 @pytest.mark.parametrize("dtype", [torch.bfloat16, torch.float16])
 def test_tensor_core_chains_16bit(lc, n, B, dtype):
     """The tcgen05 kernels (fb_learned_tc.cu) own the 16-bit chains
