@@ -206,7 +206,7 @@ __global__ void __launch_bounds__(kRegThreads)
     sg[i] = g;
   }
   __syncthreads();
-  const double w = (double)(2 * p + 1);
+  const double inv_w = 1.0 / (double)(2 * p + 1);
   for (int i = threadIdx.x; i < kRegTile; i += kRegThreads) {
     const int t = t0 + i;
     if (t >= N) break;
@@ -214,7 +214,7 @@ __global__ void __launch_bounds__(kRegThreads)
     const int hi = (t + p < N - 1) ? p : N - 1 - t;
     double acc = 0.0;
     for (int d = lo; d <= hi; ++d) acc += sg[i + p + d];
-    double g = acc / w;
+    double g = acc * inv_w;
     if (keep) g = keep[base + t] ? g * keep_scale : 0.0;
     dK[base + t] = (float)g;
   }

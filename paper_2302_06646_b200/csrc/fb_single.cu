@@ -493,13 +493,13 @@ __global__ void __launch_bounds__(FftShape<LOG2N>::T, 2)
   }
   __syncthreads();
   if (tsm) {
-    const double w = (double)(2 * p + 1);
+    const double inv_w = 1.0 / (double)(2 * p + 1);
     for (uint32_t t = j; t < N; t += S::T) {
       const int64_t lo = (int64_t)t >= p ? (int64_t)t - p : 0;
       const int64_t hi = ((int64_t)t + p < (int64_t)N - 1) ? (int64_t)t + p : (int64_t)N - 1;
       double acc = 0.0;
       for (int64_t q = lo; q <= hi; ++q) acc += (double)row[q];
-      double g = acc / w;
+      double g = acc * inv_w;
       if (keep) g = keep[base + t] ? g * keep_scale : 0.0;
       dK[base + t] = (float)g;
     }

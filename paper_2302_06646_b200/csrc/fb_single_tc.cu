@@ -1217,17 +1217,23 @@ __global__ void __launch_bounds__(512)
   static_assert(kPer == 8 || kPer == 4, "N = 4096 or 2048");
   __shared__ float row[N];
   __shared__ const float* src[8];
+  __shared__ int s_c0, s_nc;
   const int h = blockIdx.x;
   const int64_t G = ctas, T = total, np = npairs;
   const int64_t U = (T + 1) / 2;
-  // the CTA owning pair i under the backward's even-aligned shares
+  // the CTA owning pair i under the backward's even-aligned shares (64-bit
+  // divisions: once per CTA, not per thread)
   auto owner = [&](int64_t i) { return (int)((((i / 2) + 1) * G - 1) / U); };
-  const int c0 = owner((int64_t)h * np), c1 = owner(((int64_t)h + 1) * np - 1);
-  const int nc = c1 - c0 + 1;
   auto part = [&](int c) {  // CTA c's partial row of head h (segment h - its first head)
     const int64_t start = 2 * ((int64_t)c * U / G);
     return tpart + ((size_t)c * maxseg + (h - (int)(start / np))) * kPitch;
   };
+  if (threadIdx.x == 0) {
+    s_c0 = owner((int64_t)h * np);
+    s_nc = owner(((int64_t)h + 1) * np - 1) - s_c0 + 1;
+  }
+  __syncthreads();
+  const int c0 = s_c0, nc = s_nc;
   if (threadIdx.x < (unsigned)min(nc, 8)) src[threadIdx.x] = part(c0 + (int)threadIdx.x);
   __syncthreads();
   const size_t base = (size_t)h * N;
@@ -1260,7 +1266,7 @@ __global__ void __launch_bounds__(512)
   }
   __syncthreads();
   if (!freq) {
-    const double w = (double)(2 * p + 1);
+    const double inv_w = 1.0 / (double)(2 * p + 1);
     const int pp = (int)p;
     float o[kPer];
 #pragma unroll
@@ -1270,7 +1276,7 @@ __global__ void __launch_bounds__(512)
       const int hi = (t + pp < (int)N - 1) ? t + pp : (int)N - 1;
       double acc = 0.0;
       for (int q = lo; q <= hi; ++q) acc += (double)row[q];
-      double gg = acc / w;
+      double gg = acc * inv_w;
       if (keep) gg = keep[base + t] ? gg * keep_scale : 0.0;
       o[j] = (float)gg;
     }
