@@ -99,6 +99,8 @@ __global__ void __launch_bounds__(FftShape<LOG2N>::T, 2)
     // smem, then reg_value's tap sum (same order, same rounding) from there
     double* kd = reinterpret_cast<double*>(work);
     kb = reinterpret_cast<float*>(kd + N);
+    // (unrolled: the K loads of all of a thread's elements in flight at once)
+#pragma unroll 8
     for (uint32_t t = j; t < N; t += S::T) kd[t] = dropped(K, keep, keep_scale, base + t);
     __syncthreads();
     const double inv_w = 1.0 / (double)(2 * p + 1);
