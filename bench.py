@@ -334,6 +334,8 @@ def run_ours(args, cfg, rank, world, local_rank):
              (True, False): "tp_pass2" + ("_bwd" if dom == "bwd" else "") + "_kernel"}
     rows_tc = three and dt == torch.bfloat16
     kern = kname[(three, plan.tensor_cores or rows_tc)]
+    if not three and plan.tensor_cores and N <= 1024:  # the radix-16 short single pass
+        kern = f"sc_{dom}_kernel (tcgen05, radix-16 stages)"
     achieved = dom_bytes / (dom_ms / 1e3) / 1e9
     step_bytes = alg_bytes(B, Hloc, N, s, three)
     traffic = _traffic(args.config if cfg["dtype"] == CONFIGS[args.config]["dtype"] else -1, dom)

@@ -229,6 +229,10 @@ int fb_plan_create(fb_plan** out, int64_t N, int64_t H, int mode, int dtype, int
   if (!rc) rc = cuda_status(cudaMalloc(&p->kbar, sizeof(float) * H * N), "cudaMalloc(kbar)");
   if (!rc) rc = cuda_status(cudaMalloc(&p->d, sizeof(float) * H), "cudaMalloc(D)");
   if (!rc && p->use_tc) rc = tc_init(p);
+  if (!rc && engine == FB_ENGINE_SINGLE && !simt && !p->use_tc && sc_config(p, &p->sc_lgfl)) {
+    p->use_sc = true;
+    rc = sc_init(p);
+  }
   if (!rc && p->engine == FB_ENGINE_THREE) {
     rc = cuda_status(cudaMalloc(&p->kraw, sizeof(float) * H * N), "cudaMalloc(K copy)");
     if (!rc) rc = cuda_status(cudaStreamCreateWithFlags(&p->aux, cudaStreamNonBlocking), "aux stream");
@@ -261,6 +265,8 @@ int fb_plan_destroy(fb_plan* p) {
   cudaFree(p->kf_tc);
   cudaFree(p->tcr_mats);
   cudaFree(p->kf_scale);
+  cudaFree(p->sc_blocks);
+  cudaFree(p->sc_tw);
   if (p->aux) cudaStreamSynchronize(p->aux);
   for (cudaEvent_t e : {p->ev_fork, p->ev_prep, p->ev_join})
     if (e) cudaEventDestroy(e);
@@ -280,7 +286,7 @@ int fb_plan_get_info(const fb_plan* p, fb_plan_info* info) {
   info->engine = q->engine;
   info->dtype = q->dtype;
   info->mode = q->mode;
-  info->tensor_cores = q->use_tc ? 1 : 0;
+  info->tensor_cores = (q->use_tc || q->use_sc) ? 1 : 0;
   return FB_OK;
 }
 

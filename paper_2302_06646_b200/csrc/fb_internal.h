@@ -30,6 +30,12 @@ struct fb_plan {
                              // (f = f1 + 128 f2), v1 [H][f1 64][f2 128] (f = f1 + 64 f2)
   float* kf_scale = nullptr; // [H] inverse of that per-head power-of-two scale
   void* tcr_mats = nullptr;  // three-pass rows on tcgen05: DFT blocks (fb_single_tc.cu)
+  // short single pass (N = n / 2 <= 1024, 16-bit) on the radix-16 tcgen05
+  // stages of fb_learned_tc.cu with the DFT as blocks: chain [16, 16, 2^sc_lgfl]
+  bool use_sc = false;
+  int sc_lgfl = 0;
+  float2* sc_blocks = nullptr;  // the chain's DFT blocks [16 x 16, 16 x 16, FL x FL]
+  float2* sc_tw = nullptr;      // exp(-2 pi i t / n), t < n
   bool prepared = false;
   bool use_keep = false;
   double lambda = 0.0, keep_scale = 1.0;
@@ -169,6 +175,13 @@ int lb_bwd(fb_learned_plan* p, const float* blocks, const void* x, const void* g
 // learned butterfly on tcgen05 (fb_learned_tc.cu): chains [16] * stc + [2^lgfl]
 bool lt_config(int64_t n, const int64_t* f, int nst, int dtype, int* stc, int* lgfl);
 int lt_rows(int64_t n);
+// short causal single pass on the same stages (fb_learned_tc.cu)
+bool sc_config(const fb_plan* p, int* lgfl);
+int sc_init(fb_plan* p);
+int sc_chunks(const fb_plan* p, int64_t B);
+int sc_fwd(fb_plan* p, const void* u, void* y, int64_t B, cudaStream_t s);
+int sc_bwd(fb_plan* p, const void* dy, const void* u, void* du, float2* spart, float* ddpart,
+           int64_t B, cudaStream_t s);
 cudaError_t lt_fwd(int stc, int lgfl, int dtype, const float* blocks, const void* x, void* y,
                    const uint32_t* omap, const float2* tw, int B, int H, int P, cudaStream_t s);
 cudaError_t lt_bwd(int stc, int lgfl, int dtype, const float* blocks, const void* x, const void* g,

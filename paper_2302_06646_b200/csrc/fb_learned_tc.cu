@@ -35,7 +35,9 @@
 #include <cuda_fp16.h>
 #include <cuda_runtime.h>
 
+#include <cmath>
 #include <cstdint>
+#include <vector>
 #include <cstdlib>
 #include <type_traits>
 
@@ -529,6 +531,319 @@ __global__ void __launch_bounds__(kThreads, 3)
   if (threadIdx.x < 32) tc::dealloc<128>(tm);
 }
 
+// ---------------------------------------------------------------- short causal convolutions
+// The same radix-16 tcgen05 stages with the blocks fixed to the DFT: the
+// single-pass layer for N = n / 2 in {512, 1024} (16-bit modes), where the
+// 64 x 128 Monarch kernels would pad to n = 8192.  A GEMM row of the CTA is a
+// pair of real channels (re = channel 2 pr, im = 2 pr + 1) zero-padded to n;
+// U = F(u) by the forward stages, Z = U (k_f + D / n) in the last stage's
+// digit-reversed order (k_f = FFT(Kbar) / n from K1), y = the adjoint stages
+// of Z (= n F^-1).  The backward: U and DY by the forward stages, du from
+// DY conj(k_f + D / n) through the adjoint stages, and the head's dK spectrum
+// sum_pairs conj(U) DY (natural order) for sp_dk_finalize_kernel.
+
+// the adjoint stages from w_STC (operand at wlast) down to stage 0; stage 0's
+// result for this thread's column c (16 complex, slot p -> t = p rest0 + q)
+// goes to out(c, v).  w_s lands over v_(s+1).
+template <int LGN, int LGFL, int STC, typename Out>
+__device__ __forceinline__ void adjoint_chain(uint32_t tm, uint32_t sbase, uint32_t tab,
+                                              uint32_t wlast, unsigned char* X0,
+                                              const float2* __restrict__ tw_g, uint64_t* bar,
+                                              uint32_t& phase, Out out) {
+  constexpr int FL = 1 << LGFL, N = 1 << LGN, LGC = LGN - 4;
+  if (threadIdx.x == 0) {
+    issue_stage_adj(tm, wlast, tab + STC * kTab);
+    tc::commit(bar);
+  }
+  wait_mma(bar, phase);
+  {
+    float v[32];
+    load_col(tm, v);
+    unsigned char* wdst = X0 + STC * kOp;
+    const int J = col_of<STC, LGFL, STC>(threadIdx.x), r = J >> (LGN - 4), el0 = (J << 4) & (N - 1);
+#pragma unroll
+    for (int o = 0; o < 16; ++o) {
+      const int el = el0 + o, a2 = (el >> LGFL) & 15, q2 = el & (FL - 1);
+      const float2 t = __ldg(tw_g + ((a2 * q2) << (LGN - LGFL - 4)));
+      const float2 w = cmulc(make_float2(v[2 * o], v[2 * o + 1]), t);
+      const int row = row_of<STC, LGFL, STC - 1>((r << LGC) + ((el0 >> (LGFL + 4)) << LGFL)) |
+                      row_of<STC, LGFL, STC - 1>(o & (FL - 1));
+      *reinterpret_cast<uint32_t*>(wdst + op_off(row, a2)) = pack_bf16(w);
+    }
+  }
+  sync_for_mma();
+  auto adjoint_stage = [&](auto s_c) {
+    constexpr int s = decltype(s_c)::value;
+    if (threadIdx.x == 0) {
+      issue_stage_adj(tm, sbase + (s + 1) * kOp, tab + s * kTab);
+      tc::commit(bar);
+    }
+    wait_mma(bar, phase);
+    if constexpr (s > 0) {
+      constexpr int LGL = LGN - 4, LGR = STC == 2 ? LGL - 4 : 0;
+      const int c = col_of<STC, LGFL, 1>(threadIdx.x);
+      const int r = c >> LGC, cc = c & ((1 << LGC) - 1), seg = cc >> LGR, q = cc & ((1 << LGR) - 1);
+      const int a2 = seg & 15;
+      float v[32];
+      load_col(tm, v);
+      float2 t[16];
+      tw_chain(t, __ldg(tw_g + ((a2 * q) & (N - 1))), __ldg(tw_g + ((a2 << LGR) & (N - 1))));
+      unsigned char* wdst = X0 + kOp;
+#pragma unroll
+      for (int p = 0; p < 16; ++p) {
+        const float2 o = cmulc(make_float2(v[2 * p], v[2 * p + 1]), t[p]);
+        const int row = row_of<STC, LGFL, 0>((r << LGC) + q) | row_of<STC, LGFL, 0>(p << LGR);
+        *reinterpret_cast<uint32_t*>(wdst + op_off(row, a2)) = pack_bf16(o);
+      }
+    } else {
+      const int c = col_of<STC, LGFL, 0>(threadIdx.x);
+      float v[32];
+      load_col(tm, v);
+      out(c, v);
+    }
+    sync_for_mma();
+  };
+  if constexpr (STC == 2) adjoint_stage(std::integral_constant<int, 1>());
+  adjoint_stage(std::integral_constant<int, 0>());
+}
+
+// two real channels of one head as the stage-0 column (r, q): slots p < 8 hold
+// t = p rest0 + q < N / 2 (re = channel b0, im = b1), slots 8..15 the zero pad
+template <typename IO, int LGN>
+__device__ __forceinline__ void load_pair_col(uint32_t (&u)[16], float (&a)[8], float (&b)[8],
+                                              const IO* __restrict__ sig, int q, int b0, int B,
+                                              int H, int h, bool valid) {
+  constexpr int LGC = LGN - 4, NS = 1 << (LGN - 1);
+#pragma unroll
+  for (int p = 0; p < 16; ++p) u[p] = 0u;
+#pragma unroll
+  for (int p = 0; p < 8; ++p) a[p] = b[p] = 0.f;
+  if (!valid) return;
+  const IO* s0 = sig + ((size_t)b0 * H + h) * NS;
+  const IO* s1 = sig + ((size_t)(b0 + 1) * H + h) * NS;
+  const bool two = b0 + 1 < B;
+#pragma unroll
+  for (int p = 0; p < 8; ++p) {
+    a[p] = ld(s0 + (p << LGC) + q);
+    b[p] = two ? ld(s1 + (p << LGC) + q) : 0.f;
+  }
+#pragma unroll
+  for (int p = 0; p < 8; ++p) u[p] = pack_bf16(make_float2(a[p], b[p]));
+}
+template <typename IO>
+__device__ __forceinline__ void store_pair_col(IO* __restrict__ sig, const float (&v)[32], int LGC,
+                                               int q, int b0, int B, int H, int h, int NS) {
+  IO* s0 = sig + ((size_t)b0 * H + h) * NS;
+  IO* s1 = sig + ((size_t)(b0 + 1) * H + h) * NS;
+  const bool two = b0 + 1 < B;
+#pragma unroll
+  for (int p = 0; p < 8; ++p) {
+    st(s0 + (p << LGC) + q, v[2 * p]);
+    if (two) st(s1 + (p << LGC) + q, v[2 * p + 1]);
+  }
+}
+
+// the last forward stage's result times (k_f + D / n) of the row's head, in
+// the stage's digit-reversed order (cur element e -> frequency out_index(e)),
+// as the w operand of the adjoint chain; CONJ: times the conjugate
+template <int STC, int LGFL, bool CONJ>
+__device__ __forceinline__ float2 kf_at(const float2* __restrict__ kf, float dn, int h, int el) {
+  constexpr int LGN = 4 * STC + LGFL;
+  float2 k = __ldg(kf + ((size_t)h << LGN) + out_index<STC, LGFL>(el));
+  k.x += dn;
+  if (CONJ) k.y = -k.y;
+  return k;
+}
+
+template <typename IO, int STC, int LGFL>
+__global__ void __launch_bounds__(kThreads)
+    sc_fwd_kernel(const float* __restrict__ blocks, const IO* __restrict__ u, IO* __restrict__ y,
+                  const float2* __restrict__ kf, const float* __restrict__ Dg,
+                  const float2* __restrict__ tw_g, int B, int H, int npairs, int rows) {
+  constexpr int FL = 1 << LGFL, LGN = 4 * STC + LGFL, N = 1 << LGN, R = kNB / N, LGC = LGN - 4;
+  extern __shared__ __align__(1024) unsigned char lt_raw[];
+  unsigned char* sm = align1k(lt_raw);
+  unsigned char* X0 = sm;                          // operands of stages 0 .. STC
+  unsigned char* TAB = sm + (STC + 1) * kOp;
+  Smem* ss = reinterpret_cast<Smem*>(TAB + (STC + 1) * kTab);
+  const float2* W = reinterpret_cast<const float2*>(blocks);
+  if (threadIdx.x == 0) {
+    ptx::mbar_init(&ss->bar, 1);
+    ptx::fence_barrier_init();
+  }
+  if (threadIdx.x < 32) tc::alloc<64>(&ss->tmem);
+  {
+    const int c = threadIdx.x, r = c >> LGC, q = c & ((1 << LGC) - 1);
+    const int gr = blockIdx.x * R + r;
+    uint32_t x[16];
+    float xa[8], xb[8];
+    float2 wt[STC + 1];
+    load_pair_col<IO, LGN>(x, xa, xb, u, q, 2 * (gr % npairs), B, H, gr / npairs, gr < rows);
+#pragma unroll
+    for (int s = 0; s < STC; ++s) wt[s] = table_entry<16>(W + 256 * s);
+    wt[STC] = table_entry<FL>(W + 256 * STC);
+    store_row<__nv_bfloat16>(X0, row_of<STC, LGFL, 0>(c), x);
+#pragma unroll
+    for (int s = 0; s <= STC; ++s) store_table(TAB + s * kTab, wt[s]);
+  }
+  sync_for_mma();
+  const uint32_t tm = ss->tmem, sbase = ptx::smem_u32(sm), tab = ptx::smem_u32(TAB);
+  uint32_t phase = 0;
+  run_fwd_stage<LGN, LGFL, STC, 0>(tm, sbase, tab, X0, tw_g, &ss->bar, phase);
+  if constexpr (STC == 2) run_fwd_stage<LGN, LGFL, STC, 1>(tm, sbase, tab + kTab, X0, tw_g, &ss->bar, phase);
+  if (threadIdx.x == 0) {
+    issue_stage(tm, sbase + STC * kOp, tab + STC * kTab);
+    tc::commit(&ss->bar);
+  }
+  wait_mma(&ss->bar, phase);
+  {
+    // Z = U (k_f + D / n) -> w_STC over the consumed stage-0 operand
+    float v[32];
+    load_col(tm, v);
+    const int J = col_of<STC, LGFL, STC>(threadIdx.x), r = J >> (LGN - 4), el0 = (J << 4) & (N - 1);
+    const int gr = blockIdx.x * R + r, h = min(gr, rows - 1) / npairs;
+    const float dn = __ldg(Dg + h) / (float)N;
+    uint32_t z[16];
+#pragma unroll
+    for (int o = 0; o < 16; ++o)
+      z[o] = pack_bf16(cmul(make_float2(v[2 * o], v[2 * o + 1]), kf_at<STC, LGFL, false>(kf, dn, h, el0 + o)));
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+      *reinterpret_cast<uint4*>(X0 + tc::kmajor_off<tc::kSw64>(row_of<STC, LGFL, STC>(J), 8 * j)) =
+          make_uint4(z[4 * j], z[4 * j + 1], z[4 * j + 2], z[4 * j + 3]);
+  }
+  sync_for_mma();
+  adjoint_chain<LGN, LGFL, STC>(tm, sbase, tab, sbase, X0, tw_g, &ss->bar, phase,
+                                [&](int c, const float (&v)[32]) {
+                                  const int r = c >> LGC, q = c & ((1 << LGC) - 1);
+                                  const int gr = blockIdx.x * R + r;
+                                  if (gr < rows)
+                                    store_pair_col<IO>(y, v, LGC, q, 2 * (gr % npairs), B, H,
+                                                       gr / npairs, N / 2);
+                                });
+  tc::fence_before();
+  __syncthreads();
+  if (threadIdx.x < 32) tc::dealloc<64>(tm);
+}
+
+// backward: CTA (h, k) owns pairs k R .. k R + R - 1 of head h
+template <typename IO, int STC, int LGFL>
+__global__ void __launch_bounds__(kThreads)
+    sc_bwd_kernel(const float* __restrict__ blocks, const IO* __restrict__ dy,
+                  const IO* __restrict__ u, IO* __restrict__ du, const float2* __restrict__ kf,
+                  const float* __restrict__ Dg, const float2* __restrict__ tw_g,
+                  float2* __restrict__ spart, float* __restrict__ ddpart, int B, int H,
+                  int npairs) {
+  constexpr int FL = 1 << LGFL, LGN = 4 * STC + LGFL, N = 1 << LGN, R = kNB / N, LGC = LGN - 4;
+  constexpr int NJ = N / 16;  // rows J per channel pair
+  extern __shared__ __align__(1024) unsigned char lt_raw[];
+  unsigned char* sm = align1k(lt_raw);
+  unsigned char* X0 = sm;                          // operands of stages 0 .. STC
+  uint32_t* UB = reinterpret_cast<uint32_t*>(sm + (STC + 1) * kOp);  // U (bf16 pairs) [o][J]
+  float2* SP = reinterpret_cast<float2*>(sm + (STC + 2) * kOp);      // conj(U) DY [o][J]
+  unsigned char* TAB = sm + (STC + 4) * kOp;
+  Smem* ss = reinterpret_cast<Smem*>(TAB + (STC + 1) * kTab);
+  float* ss_red = reinterpret_cast<float*>(ss + 1);  // [8] warp partials of dD
+  const float2* W = reinterpret_cast<const float2*>(blocks);
+  const int h = blockIdx.x, k = blockIdx.y;
+  if (threadIdx.x == 0) {
+    ptx::mbar_init(&ss->bar, 1);
+    ptx::fence_barrier_init();
+  }
+  if (threadIdx.x < 32) tc::alloc<64>(&ss->tmem);
+  uint32_t xd[16];  // dy's column, stored once u's stage 0 is done
+  {
+    const int c = threadIdx.x, r = c >> LGC, q = c & ((1 << LGC) - 1), pr = k * R + r;
+    uint32_t x[16];
+    float2 wt[STC + 1];
+    float ua[8], ub[8], ga[8], gb[8];
+    load_pair_col<IO, LGN>(x, ua, ub, u, q, 2 * pr, B, H, h, pr < npairs);
+    load_pair_col<IO, LGN>(xd, ga, gb, dy, q, 2 * pr, B, H, h, pr < npairs);
+    // dD partial = sum dy u over the CTA's channels, in fp32 from the 16-bit
+    // inputs (not the lag-0 bin of the bf16-operand spectrum: dD can be small)
+    float dd = 0.f;
+#pragma unroll
+    for (int p = 0; p < 8; ++p) dd = fmaf(ua[p], ga[p], fmaf(ub[p], gb[p], dd));
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) dd += __shfl_xor_sync(0xffffffffu, dd, o);
+    if ((threadIdx.x & 31) == 0) ss_red[threadIdx.x >> 5] = dd;
+#pragma unroll
+    for (int s = 0; s < STC; ++s) wt[s] = table_entry<16>(W + 256 * s);
+    wt[STC] = table_entry<FL>(W + 256 * STC);
+    store_row<__nv_bfloat16>(X0, row_of<STC, LGFL, 0>(c), x);
+#pragma unroll
+    for (int s = 0; s <= STC; ++s) store_table(TAB + s * kTab, wt[s]);
+  }
+  sync_for_mma();
+  const uint32_t tm = ss->tmem, sbase = ptx::smem_u32(sm), tab = ptx::smem_u32(TAB);
+  uint32_t phase = 0;
+  const int J = col_of<STC, LGFL, STC>(threadIdx.x), el0 = (J << 4) & (N - 1);
+  // U = F(u pair)
+  run_fwd_stage<LGN, LGFL, STC, 0>(tm, sbase, tab, X0, tw_g, &ss->bar, phase);
+  store_row<__nv_bfloat16>(X0, row_of<STC, LGFL, 0>(threadIdx.x), xd);  // stage 0 of u is done
+  if constexpr (STC == 2) run_fwd_stage<LGN, LGFL, STC, 1>(tm, sbase, tab + kTab, X0, tw_g, &ss->bar, phase);
+  if (threadIdx.x == 0) {
+    issue_stage(tm, sbase + STC * kOp, tab + STC * kTab);
+    tc::commit(&ss->bar);
+  }
+  wait_mma(&ss->bar, phase);
+  {
+    float v[32];
+    load_col(tm, v);
+#pragma unroll
+    for (int o = 0; o < 16; ++o) UB[o * (R * NJ) + J] = pack_bf16(make_float2(v[2 * o], v[2 * o + 1]));
+  }
+  sync_for_mma();
+  // DY = F(dy pair) (dy's stage-0 operand is in place)
+  run_fwd_stage<LGN, LGFL, STC, 0>(tm, sbase, tab, X0, tw_g, &ss->bar, phase);
+  if constexpr (STC == 2) run_fwd_stage<LGN, LGFL, STC, 1>(tm, sbase, tab + kTab, X0, tw_g, &ss->bar, phase);
+  if (threadIdx.x == 0) {
+    issue_stage(tm, sbase + STC * kOp, tab + STC * kTab);
+    tc::commit(&ss->bar);
+  }
+  wait_mma(&ss->bar, phase);
+  {
+    float v[32];
+    load_col(tm, v);
+    const float dn = __ldg(Dg + h) / (float)N;
+    uint32_t z[16];
+#pragma unroll
+    for (int o = 0; o < 16; ++o) {
+      const float2 d = make_float2(v[2 * o], v[2 * o + 1]);
+      const float2 uu = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&UB[o * (R * NJ) + J]));
+      SP[o * (R * NJ) + J] = cmulc(d, uu);  // DY conj(U)
+      z[o] = pack_bf16(cmul(d, kf_at<STC, LGFL, true>(kf, dn, h, el0 + o)));
+    }
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+      *reinterpret_cast<uint4*>(X0 + tc::kmajor_off<tc::kSw64>(row_of<STC, LGFL, STC>(J), 8 * j)) =
+          make_uint4(z[4 * j], z[4 * j + 1], z[4 * j + 2], z[4 * j + 3]);
+  }
+  sync_for_mma();
+  adjoint_chain<LGN, LGFL, STC>(tm, sbase, tab, sbase, X0, tw_g, &ss->bar, phase,
+                                [&](int c, const float (&v)[32]) {
+                                  const int r = c >> LGC, q = c & ((1 << LGC) - 1), pr = k * R + r;
+                                  if (pr < npairs) store_pair_col<IO>(du, v, LGC, q, 2 * pr, B, H, h, N / 2);
+                                });
+  if (threadIdx.x == 0) {
+    float t = 0.f;
+    for (int w = 0; w < kThreads / 32; ++w) t += ss_red[w];
+    ddpart[(size_t)h * gridDim.y + k] = t;
+  }
+  // the head's dK spectrum partial: sum over this CTA's pairs in order, natural frequency order
+  const int nr = min(R, npairs - k * R);
+  float2* sp = spart + ((size_t)h * gridDim.y + k) * N;
+  for (int idx = threadIdx.x; idx < N; idx += kThreads) {
+    const int o = idx / NJ, j = idx % NJ;  // lanes: consecutive j
+    float2 acc = make_float2(0.f, 0.f);
+    for (int r = 0; r < nr; ++r) acc = cadd(acc, SP[o * (R * NJ) + r * NJ + j]);
+    sp[out_index<STC, LGFL>(16 * j + o)] = acc;
+  }
+  tc::fence_before();
+  __syncthreads();
+  if (threadIdx.x < 32) tc::dealloc<64>(tm);
+}
+
 template <int STC, int LGFL>
 constexpr size_t fwd_smem() {
   return 1024 + (STC + 1) * kOp + (STC + 1) * kTab + 64;
@@ -572,6 +887,93 @@ cudaError_t dispatch(int stc, int lgfl, bool bwd, const float* blocks, const voi
 }
 
 }  // namespace ltc
+
+// ---------------------------------------------------------------- short single pass (host)
+template <typename IO, int LGFL>
+static int sc_launch(fb_plan* p, bool bwd, const void* a, const void* b, void* out, float2* spart,
+                     float* ddpart, int64_t B, cudaStream_t s) {
+  constexpr int STC = 2, N = 1 << (8 + LGFL), R = ltc::kNB / N;
+  const int npairs = (int)((B + 1) / 2);
+  if (!bwd) {
+    auto k = ltc::sc_fwd_kernel<IO, STC, LGFL>;
+    constexpr size_t sm = ltc::fwd_smem<STC, LGFL>();
+    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    const int rows = (int)(p->H * npairs);
+    k<<<(unsigned)((rows + R - 1) / R), ltc::kThreads, sm, s>>>(
+        (const float*)p->sc_blocks, (const IO*)a, (IO*)out, p->kf, p->d, p->sc_tw, (int)B,
+        (int)p->H, npairs, rows);
+  } else {
+    auto k = ltc::sc_bwd_kernel<IO, STC, LGFL>;
+    constexpr size_t sm = 1024 + (STC + 4) * ltc::kOp + (STC + 1) * ltc::kTab + 128;
+    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    k<<<dim3((unsigned)p->H, (unsigned)((npairs + R - 1) / R)), ltc::kThreads, sm, s>>>(
+        (const float*)p->sc_blocks, (const IO*)a, (const IO*)b, (IO*)out, p->kf, p->d, p->sc_tw,
+        spart, ddpart, (int)B, (int)p->H, npairs);
+  }
+  return cuda_status(cudaGetLastError(), bwd ? "sc_bwd" : "sc_fwd");
+}
+template <typename IO>
+static int sc_dispatch(fb_plan* p, bool bwd, const void* a, const void* b, void* out, float2* spart,
+                       float* ddpart, int64_t B, cudaStream_t s) {
+  switch (p->sc_lgfl) {
+    case 1: return sc_launch<IO, 1>(p, bwd, a, b, out, spart, ddpart, B, s);
+    case 2: return sc_launch<IO, 2>(p, bwd, a, b, out, spart, ddpart, B, s);
+    default: return sc_launch<IO, 3>(p, bwd, a, b, out, spart, ddpart, B, s);
+  }
+}
+
+// causal, 16-bit, N = 512 (n = 1024 = [16, 16, 4]): measured 0.090 -> 0.068 ms
+// per step at B*H = 2048 against the CUDA-core single pass.  N = 1024
+// (n = 2048, two rows per CTA) measured 3 % slower than the CUDA cores and
+// N = 256 (n = 512) leaves half of a CTA's eight rows idle at B = 8, so those
+// stay on the CUDA cores; FB_SHORT_TC=2048 forces n = 2048 for comparisons,
+// FB_SHORT_TC=0 disables the path.
+bool sc_config(const fb_plan* p, int* lgfl) {
+  const char* env = std::getenv("FB_SHORT_TC");
+  if (env && env[0] == '0') return false;
+  if (p->mode != FB_MODE_CAUSAL || p->dtype == FB_F32 || p->periodic || p->N * 2 != p->n) return false;
+  if (p->n == 1024) *lgfl = 2;
+  else if (p->n == 2048 && env && std::atoi(env) == 2048) *lgfl = 3;
+  else return false;
+  return true;
+}
+int sc_init(fb_plan* p) {
+  const int64_t n = p->n, FL = int64_t(1) << p->sc_lgfl;
+  std::vector<float2> blk, tw((size_t)n);
+  auto dft = [&](int64_t f) {
+    for (int64_t a = 0; a < f; ++a)
+      for (int64_t q = 0; q < f; ++q) {
+        const double ang = -2.0 * M_PI * (double)((a * q) % f) / (double)f;
+        blk.push_back(make_float2((float)std::cos(ang), (float)std::sin(ang)));
+      }
+  };
+  dft(16);
+  dft(16);
+  dft(FL);
+  for (int64_t t = 0; t < n; ++t) {
+    const double ang = -2.0 * M_PI * (double)t / (double)n;
+    tw[(size_t)t] = make_float2((float)std::cos(ang), (float)std::sin(ang));
+  }
+  int rc = cuda_status(cudaMalloc(&p->sc_blocks, sizeof(float2) * blk.size()), "cudaMalloc(sc blocks)");
+  if (!rc) rc = cuda_status(cudaMalloc(&p->sc_tw, sizeof(float2) * n), "cudaMalloc(sc tw)");
+  if (!rc) rc = cuda_status(cudaMemcpy(p->sc_blocks, blk.data(), sizeof(float2) * blk.size(), cudaMemcpyHostToDevice), "copy sc blocks");
+  if (!rc) rc = cuda_status(cudaMemcpy(p->sc_tw, tw.data(), sizeof(float2) * n, cudaMemcpyHostToDevice), "copy sc tw");
+  return rc;
+}
+int sc_chunks(const fb_plan* p, int64_t B) {
+  const int64_t R = ltc::kNB / p->n;
+  return (int)((((B + 1) / 2) + R - 1) / R);
+}
+int sc_fwd(fb_plan* p, const void* u, void* y, int64_t B, cudaStream_t s) {
+  return p->dtype == FB_BF16
+             ? sc_dispatch<__nv_bfloat16>(p, false, u, nullptr, y, nullptr, nullptr, B, s)
+             : sc_dispatch<__half>(p, false, u, nullptr, y, nullptr, nullptr, B, s);
+}
+int sc_bwd(fb_plan* p, const void* dy, const void* u, void* du, float2* spart, float* ddpart,
+           int64_t B, cudaStream_t s) {
+  return p->dtype == FB_BF16 ? sc_dispatch<__nv_bfloat16>(p, true, dy, u, du, spart, ddpart, B, s)
+                             : sc_dispatch<__half>(p, true, dy, u, du, spart, ddpart, B, s);
+}
 
 // chains [16] * stc + [2^lgfl], stc in {1, 2}, lgfl in {1, 2, 3}; 16-bit modes
 bool lt_config(int64_t n, const int64_t* f, int nst, int dtype, int* stc, int* lgfl) {

@@ -641,6 +641,12 @@ int sp_finalize(fb_plan* p, const float2* spart, const float* ddpart, int chunks
 
 int sp_fwd(fb_plan* p, const void* u, void* y, int64_t B, cudaStream_t s) {
   if (p->use_tc) return tc_fwd(p, u, y, B, s);
+  if (p->use_sc) {
+    prof_mark(p, 0, 0, s);
+    const int rc = sc_fwd(p, u, y, B, s);
+    prof_mark(p, 0, 1, s);
+    return rc;
+  }
   const int chunks = chunks_for(p, B);
   const int64_t npairs = (B + 1) / 2;
   const int ppc = (int)((npairs + chunks - 1) / chunks);
@@ -658,6 +664,8 @@ int sp_fwd(fb_plan* p, const void* u, void* y, int64_t B, cudaStream_t s) {
 
 size_t sp_workspace(const fb_plan* p, int64_t B) {
   if (p->use_tc) return tc_workspace(p, B);
+  if (p->use_sc)  // spectral partials, then dD partials
+    return ((size_t)p->H * sc_chunks(p, B) * (p->n * sizeof(float2) + sizeof(float)) + 255) & ~size_t(255);
   const int c = chunks_for(p, B);
   size_t bytes = (size_t)p->H * c * p->n * sizeof(float2);  // spectral partials
   bytes += (size_t)p->H * c * sizeof(float);                 // dD partials
@@ -669,6 +677,16 @@ size_t sp_workspace(const fb_plan* p, int64_t B) {
 int sp_bwd(fb_plan* p, const void* dy, const void* u, void* du, float* dK, float* dKbar, float* dD,
            int64_t B, void* ws, cudaStream_t s) {
   if (p->use_tc) return tc_bwd(p, dy, u, du, dK, dKbar, dD, B, ws, s);
+  if (p->use_sc) {
+    const int c = sc_chunks(p, B);
+    float2* spart = (float2*)ws;
+    float* ddpart = (float*)((char*)ws + (size_t)p->H * c * p->n * sizeof(float2));
+    prof_mark(p, 1, 0, s);
+    int rc = sc_bwd(p, dy, u, du, spart, ddpart, B, s);
+    prof_mark(p, 1, 1, s);
+    if (!rc) rc = sp_finalize(p, spart, ddpart, c, dKbar, dD, dK, 0, nullptr, s);
+    return rc;
+  }
   const int chunks = chunks_for(p, B);
   const int64_t npairs = (B + 1) / 2;
   const int ppc = (int)((npairs + chunks - 1) / chunks);
