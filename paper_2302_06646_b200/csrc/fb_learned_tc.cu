@@ -733,7 +733,7 @@ __global__ void __launch_bounds__(kThreads)
                   const IO* __restrict__ u, IO* __restrict__ du, const float2* __restrict__ kf,
                   const float* __restrict__ Dg, const float2* __restrict__ tw_g,
                   float2* __restrict__ spart, float* __restrict__ ddpart, int B, int H,
-                  int npairs) {
+                  int npairs, int hpc) {
   constexpr int FL = 1 << LGFL, LGN = 4 * STC + LGFL, N = 1 << LGN, R = kNB / N, LGC = LGN - 4;
   constexpr int NJ = N / 16;  // rows J per channel pair
   extern __shared__ __align__(1024) unsigned char lt_raw[];
@@ -745,7 +745,12 @@ __global__ void __launch_bounds__(kThreads)
   Smem* ss = reinterpret_cast<Smem*>(TAB + (STC + 1) * kTab);
   float* ss_red = reinterpret_cast<float*>(ss + 1);  // [8] warp partials of dD
   const float2* W = reinterpret_cast<const float2*>(blocks);
-  const int h = blockIdx.x, k = blockIdx.y;
+  // rows: hpc > 1 -> hpc whole heads per CTA (npairs divides R), else CTA
+  // (h, k) owns pairs k R .. k R + R - 1 of head h
+  const int k = blockIdx.y;
+  auto row_head = [&](int r) { return hpc > 1 ? (int)blockIdx.x * hpc + r / npairs : (int)blockIdx.x; };
+  auto row_pair = [&](int r) { return hpc > 1 ? r % npairs : k * R + r; };
+  auto row_ok = [&](int r) { return hpc > 1 ? row_head(r) < H : row_pair(r) < npairs; };
   if (threadIdx.x == 0) {
     ptx::mbar_init(&ss->bar, 1);
     ptx::fence_barrier_init();
@@ -753,12 +758,13 @@ __global__ void __launch_bounds__(kThreads)
   if (threadIdx.x < 32) tc::alloc<64>(&ss->tmem);
   uint32_t xd[16];  // dy's column, stored once u's stage 0 is done
   {
-    const int c = threadIdx.x, r = c >> LGC, q = c & ((1 << LGC) - 1), pr = k * R + r;
+    const int c = threadIdx.x, r = c >> LGC, q = c & ((1 << LGC) - 1), pr = row_pair(r);
+    const int hr = row_head(r);
     uint32_t x[16];
     float2 wt[STC + 1];
     float ua[8], ub[8], ga[8], gb[8];
-    load_pair_col<IO, LGN>(x, ua, ub, u, q, 2 * pr, B, H, h, pr < npairs);
-    load_pair_col<IO, LGN>(xd, ga, gb, dy, q, 2 * pr, B, H, h, pr < npairs);
+    load_pair_col<IO, LGN>(x, ua, ub, u, q, 2 * pr, B, H, hr, row_ok(r));
+    load_pair_col<IO, LGN>(xd, ga, gb, dy, q, 2 * pr, B, H, hr, row_ok(r));
     // dD partial = sum dy u over the CTA's channels, in fp32 from the 16-bit
     // inputs (not the lag-0 bin of the bf16-operand spectrum: dD can be small)
     float dd = 0.f;
@@ -805,14 +811,15 @@ __global__ void __launch_bounds__(kThreads)
   {
     float v[32];
     load_col(tm, v);
-    const float dn = __ldg(Dg + h) / (float)N;
+    const int hr = min(row_head(J >> (LGN - 4)), H - 1);
+    const float dn = __ldg(Dg + hr) / (float)N;
     uint32_t z[16];
 #pragma unroll
     for (int o = 0; o < 16; ++o) {
       const float2 d = make_float2(v[2 * o], v[2 * o + 1]);
       const float2 uu = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&UB[o * (R * NJ) + J]));
       SP[o * (R * NJ) + J] = cmulc(d, uu);  // DY conj(U)
-      z[o] = pack_bf16(cmul(d, kf_at<STC, LGFL, true>(kf, dn, h, el0 + o)));
+      z[o] = pack_bf16(cmul(d, kf_at<STC, LGFL, true>(kf, dn, hr, el0 + o)));
     }
 #pragma unroll
     for (int j = 0; j < 4; ++j)
@@ -822,22 +829,34 @@ __global__ void __launch_bounds__(kThreads)
   sync_for_mma();
   adjoint_chain<LGN, LGFL, STC>(tm, sbase, tab, sbase, X0, tw_g, &ss->bar, phase,
                                 [&](int c, const float (&v)[32]) {
-                                  const int r = c >> LGC, q = c & ((1 << LGC) - 1), pr = k * R + r;
-                                  if (pr < npairs) store_pair_col<IO>(du, v, LGC, q, 2 * pr, B, H, h, N / 2);
+                                  const int r = c >> LGC, q = c & ((1 << LGC) - 1);
+                                  if (row_ok(r))
+                                    store_pair_col<IO>(du, v, LGC, q, 2 * row_pair(r), B, H,
+                                                       row_head(r), N / 2);
                                 });
-  if (threadIdx.x == 0) {
-    float t = 0.f;
-    for (int w = 0; w < kThreads / 32; ++w) t += ss_red[w];
-    ddpart[(size_t)h * gridDim.y + k] = t;
-  }
-  // the head's dK spectrum partial: sum over this CTA's pairs in order, natural frequency order
-  const int nr = min(R, npairs - k * R);
-  float2* sp = spart + ((size_t)h * gridDim.y + k) * N;
-  for (int idx = threadIdx.x; idx < N; idx += kThreads) {
-    const int o = idx / NJ, j = idx % NJ;  // lanes: consecutive j
-    float2 acc = make_float2(0.f, 0.f);
-    for (int r = 0; r < nr; ++r) acc = cadd(acc, SP[o * (R * NJ) + r * NJ + j]);
-    sp[out_index<STC, LGFL>(16 * j + o)] = acc;
+  // per head of the CTA: the dD partial (warps in order; a warp's columns are
+  // one row) and the dK spectrum partial (rows in order, natural frequency order)
+  const int heads = hpc > 1 ? hpc : 1, chunks = gridDim.y;
+  for (int hh = 0; hh < heads; ++hh) {
+    const int r0 = hpc > 1 ? hh * npairs : 0;
+    const int nr = hpc > 1 ? npairs : min(R, npairs - k * R);
+    const int head = row_head(r0);
+    if (head >= H) break;
+    if (threadIdx.x == 0) {
+      float t = 0.f;
+      for (int w = 0; w < kThreads / 32; ++w) {
+        const int rw = (32 * w) >> LGC;
+        if (rw >= r0 && rw < r0 + nr) t += ss_red[w];
+      }
+      ddpart[(size_t)head * chunks + k] = t;
+    }
+    float2* sp = spart + ((size_t)head * chunks + k) * N;
+    for (int idx = threadIdx.x; idx < N; idx += kThreads) {
+      const int o = idx / NJ, j = idx % NJ;  // lanes: consecutive j
+      float2 acc = make_float2(0.f, 0.f);
+      for (int r = r0; r < r0 + nr; ++r) acc = cadd(acc, SP[o * (R * NJ) + r * NJ + j]);
+      sp[out_index<STC, LGFL>(16 * j + o)] = acc;
+    }
   }
   tc::fence_before();
   __syncthreads();
@@ -889,6 +908,11 @@ cudaError_t dispatch(int stc, int lgfl, bool bwd, const float* blocks, const voi
 }  // namespace ltc
 
 // ---------------------------------------------------------------- short single pass (host)
+// backward CTAs: whole heads when a head's pairs divide the CTA's rows
+static int sc_heads_per_cta(const fb_plan* p, int64_t B) {
+  const int64_t R = ltc::kNB / p->n, np = (B + 1) / 2;
+  return (np < R && R % np == 0) ? (int)(R / np) : 1;
+}
 template <typename IO, int LGFL>
 static int sc_launch(fb_plan* p, bool bwd, const void* a, const void* b, void* out, float2* spart,
                      float* ddpart, int64_t B, cudaStream_t s) {
@@ -906,9 +930,12 @@ static int sc_launch(fb_plan* p, bool bwd, const void* a, const void* b, void* o
     auto k = ltc::sc_bwd_kernel<IO, STC, LGFL>;
     constexpr size_t sm = 1024 + (STC + 4) * ltc::kOp + (STC + 1) * ltc::kTab + 128;
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-    k<<<dim3((unsigned)p->H, (unsigned)((npairs + R - 1) / R)), ltc::kThreads, sm, s>>>(
-        (const float*)p->sc_blocks, (const IO*)a, (const IO*)b, (IO*)out, p->kf, p->d, p->sc_tw,
-        spart, ddpart, (int)B, (int)p->H, npairs);
+    const int hpc = sc_heads_per_cta(p, B);
+    const dim3 grid = hpc > 1 ? dim3((unsigned)((p->H + hpc - 1) / hpc), 1)
+                              : dim3((unsigned)p->H, (unsigned)((npairs + R - 1) / R));
+    k<<<grid, ltc::kThreads, sm, s>>>((const float*)p->sc_blocks, (const IO*)a, (const IO*)b,
+                                      (IO*)out, p->kf, p->d, p->sc_tw, spart, ddpart, (int)B,
+                                      (int)p->H, npairs, hpc);
   }
   return cuda_status(cudaGetLastError(), bwd ? "sc_bwd" : "sc_fwd");
 }
@@ -933,6 +960,7 @@ bool sc_config(const fb_plan* p, int* lgfl) {
   if (env && env[0] == '0') return false;
   if (p->mode != FB_MODE_CAUSAL || p->dtype == FB_F32 || p->periodic || p->N * 2 != p->n) return false;
   if (p->n == 1024) *lgfl = 2;
+  else if (p->n == 512) *lgfl = 1;
   else if (p->n == 2048 && env && std::atoi(env) == 2048) *lgfl = 3;
   else return false;
   return true;
@@ -962,6 +990,7 @@ int sc_init(fb_plan* p) {
 }
 int sc_chunks(const fb_plan* p, int64_t B) {
   const int64_t R = ltc::kNB / p->n;
+  if (sc_heads_per_cta(p, B) > 1) return 1;
   return (int)((((B + 1) / 2) + R - 1) / R);
 }
 int sc_fwd(fb_plan* p, const void* u, void* y, int64_t B, cudaStream_t s) {

@@ -219,9 +219,9 @@ def test_dimension_errors():
 
 
 # ------------------------------------------------------------ tcgen05 single-pass
-@pytest.mark.parametrize("N", [4096, 2048, 1024, 512])
+@pytest.mark.parametrize("N", [4096, 2048, 1024, 512, 256])
 @pytest.mark.parametrize("dtype", [torch.bfloat16, torch.float16])
-@pytest.mark.parametrize("B,H", [(2, 2), (3, 3), (5, 1), (16, 3)])
+@pytest.mark.parametrize("B,H", [(2, 2), (3, 3), (5, 1), (16, 3), (8, 5)])
 def test_tensor_core_single_pass(lc, monkeypatch, dtype, B, H, N):
     """N = 4096, and N = 2048 on the same n = 8192 transform (16 data rows);
     N = 512 on the radix-16 stages (fb_learned_tc.cu short single pass);
