@@ -1,7 +1,9 @@
-// FlashButterfly-B200 learned butterfly (K5) on the tcgen05 tensor cores, for
-// the 16-bit modes and the chains build_plan(n, 16) gives for
-// n = 16^S x FL (S in {1, 2} stages of factor 16, a last factor FL in
-// {2, 4, 8}: n = 32 .. 2048, config 4's n = 1024 = [16, 16, 4]).
+// FlashButterfly-B200 radix-16 stages on the tcgen05 tensor cores: the
+// learned butterfly (K5) for the 16-bit modes and the chains build_plan(n, 16)
+// gives for n = 16^S x FL (S in {1, 2} stages of factor 16, a last factor FL
+// in {2, 4, 8}: n = 32 .. 2048, config 4's n = 1024 = [16, 16, 4]); and, with
+// the blocks fixed to the DFT, the short causal single pass (N = 256, 512;
+// sc_fwd_kernel / sc_bwd_kernel at the end of this file).
 //
 // Reference: learned_forward / learned_gradients (proj/src/butterfly.cpp:
 // 235-307) over apply_stages (:124-163).  In the matrix form of
