@@ -332,7 +332,7 @@ def run_ours(args, cfg, rank, world, local_rank):
     kname = {(False, True): f"tc_{dom}_kernel (tcgen05)", (False, False): f"sp_{dom}_kernel",
              (True, True): f"tc_rows_{dom}_kernel (tcgen05)",
              (True, False): "tp_pass2" + ("_bwd" if dom == "bwd" else "") + "_kernel"}
-    rows_tc = three and dt == torch.bfloat16
+    rows_tc = three and dt in (torch.bfloat16, torch.float16)
     kern = kname[(three, plan.tensor_cores or rows_tc)]
     if not three and plan.tensor_cores and N <= 1024:  # the radix-16 short single pass
         kern = f"sc_{dom}_kernel (tcgen05, radix-16 stages)"

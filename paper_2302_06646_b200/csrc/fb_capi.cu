@@ -427,10 +427,11 @@ size_t fb_saved_size(const fb_plan* p, int64_t B) {
   if (!p || B < 1) return 0;
   if (p->inner) return fb_saved_size(p->inner, B);
   if (p->use_tc) return tc_saved_size(p, B);
-  // three-pass: the saved row spectra are kept in the I/O precision, which
-  // for fp16 cannot hold FFT_l of a long non-zero-mean row (|U[0]| = l |mean|
-  // overflows 65504): fp16 plans recompute U in the backward instead
-  if (p->engine == FB_ENGINE_THREE && !p->periodic && p->dtype != FB_F16)
+  // three-pass: the saved row spectra are kept in the intermediate precision,
+  // which for fp16 on the CUDA-core rows cannot hold FFT_l of a long
+  // non-zero-mean row (|U[0]| = l |mean| overflows 65504): those plans
+  // recompute U in the backward; fp16 on the tcgen05 rows keeps bf16 rows
+  if (p->engine == FB_ENGINE_THREE && !p->periodic && (p->dtype != FB_F16 || tp_uses_tc_rows(p)))
     return tp_saved_size(p, B);
   return 0;
 }

@@ -122,6 +122,7 @@ int tc_init(fb_plan* p);
 // version 2 (fb_tc2.cu)
 int tc2_init(fb_plan* p);
 bool tc_length_ok(int64_t N);
+bool tp_uses_tc_rows(const fb_plan* p);  // fb_three.cu: pass 2 on the tcgen05 rows
 int tc2_fwd(fb_plan* p, const void* u, void* y, int64_t B, int ctas, int total, cudaStream_t s,
             void* usave, bool spectrum_only);
 int tc2_bwd(fb_plan* p, const void* dy, void* du, int64_t B, int ctas, int total, int maxseg,

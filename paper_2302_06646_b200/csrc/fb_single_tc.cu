@@ -1958,7 +1958,8 @@ bool tc_rows_eligible(const fb_plan* p) {
     const char* e = std::getenv("FB_ROWS_TC");
     return e && e[0] == '0';
   }();
-  return !off && p->dtype == FB_BF16 && p->l == 8192;
+  // fp16 I/O runs the same bf16 rows (fb_three.cu keeps its intermediates in bf16 then)
+  return !off && (p->dtype == FB_BF16 || p->dtype == FB_F16) && p->l == 8192;
 }
 
 // x1: npairs x H x m planar bf16 rows in, interleaved (re, im) rows out

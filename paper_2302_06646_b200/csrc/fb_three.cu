@@ -1409,6 +1409,8 @@ static bool use_tc_rows(const fb_plan* p) {
   return bigs_smem((uint32_t)p->m, 1, stage) <= 227 * 1024 && (bigs_mask() & 1);
 }
 
+bool tp_uses_tc_rows(const fb_plan* p) { return use_tc_rows(p); }
+
 int tp_fwd(fb_plan* p, const void* u, void* y, int64_t B, void* ws, cudaStream_t s, void* usave) {
   const int64_t npairs = (B + 1) / 2;
   if (p->periodic) {
@@ -1416,11 +1418,14 @@ int tp_fwd(fb_plan* p, const void* u, void* y, int64_t B, void* ws, cudaStream_t
     return FB_ERR_UNSUPPORTED;
   }
   int rc = FB_OK;
-  with_io(p->dtype, [&](auto io) {
+  const bool tcr = use_tc_rows(p);
+  // intermediates in the I/O precision, except fp16 on the tcgen05 rows:
+  // bf16 there (the rows kernels' operand type; no fp16 range limit)
+  auto body = [&](auto io, auto st) {
     using IO = decltype(io);
-    using ST = IO;
+    using ST = decltype(st);
     auto* x1 = reinterpret_cast<CxT<ST>*>(ws);
-    if (use_tc_rows(p)) {  // pass 2 on tcgen05 (planar rows in, interleaved out)
+    if (tcr) {  // pass 2 on tcgen05 (planar rows in, interleaved out)
       if (!launch_pass1<IO, ST, 0>(p, (const IO*)u, nullptr, x1, nullptr, nullptr, (int)B,
                                    (int)npairs, s, true)) {
         rc = FB_ERR_UNSUPPORTED;
@@ -1444,6 +1449,15 @@ int tp_fwd(fb_plan* p, const void* u, void* y, int64_t B, void* ws, cudaStream_t
         reinterpret_cast<CxT<ST>*>(usave));
     prof_mark(p, 0, 1, s);
     launch_pass3<ST, IO, 0>(p, x1, (const IO*)u, (IO*)y, nullptr, (int)B, (int)npairs, 1.f, s);
+  };
+  with_io(p->dtype, [&](auto io) {
+    using IO = decltype(io);
+    if constexpr (std::is_same<IO, __half>::value) {
+      if (tcr) body(io, __nv_bfloat16{});
+      else body(io, io);
+    } else {
+      body(io, io);
+    }
   });
   if (rc) return rc;
   return cuda_status(cudaGetLastError(), "tp_fwd");
@@ -1469,9 +1483,9 @@ int tp_bwd(fb_plan* p, const void* dy, const void* u, void* du, float* dK, float
   float* dkbar = dKbar ? dKbar : dkbar_s;
   int rc = FB_OK;
   const bool tcr = use_tc_rows(p);
-  with_io(p->dtype, [&](auto io) {
+  auto body = [&](auto io, auto st) {
     using IO = decltype(io);
-    using ST = IO;
+    using ST = decltype(st);
     auto* x1dy = reinterpret_cast<CxT<ST>*>(x1dy_raw);
     auto* x1u = reinterpret_cast<CxT<ST>*>(x1u_raw);
     const size_t sm = pass2_bwd_smem<ST>();
@@ -1528,6 +1542,15 @@ int tp_bwd(fb_plan* p, const void* dy, const void* u, void* du, float* dK, float
     if (ts != s) {  // join
       cudaEventRecord(p->ev_join, ts);
       cudaStreamWaitEvent(s, p->ev_join, 0);
+    }
+  };
+  with_io(p->dtype, [&](auto io) {
+    using IO = decltype(io);
+    if constexpr (std::is_same<IO, __half>::value) {
+      if (tcr) body(io, __nv_bfloat16{});
+      else body(io, io);
+    } else {
+      body(io, io);
     }
   });
   if (rc) return rc;

@@ -361,14 +361,20 @@ def test_three_pass_16bit(lc, dtype):
     assert_parity(got, oracle_layer(lc, inp, cfg), 2e-2)
 
 
-@pytest.mark.parametrize("B,H,N,mode", [(2, 2, 8192, 1), (1, 3, 16384, 0), (5, 2, 65536, 1),
-                                        (4, 3, 16384, 1), (3, 1, 131072, 1), (2, 1, 262144, 1)])
-def test_three_pass_bf16_tc_rows(lc, B, H, N, mode):
-    """bf16 three-pass with pass 2 on tcgen05 (m = 2 .. 64: register and
+@pytest.mark.parametrize("B,H,N,mode,dtype", [(2, 2, 8192, 1, torch.bfloat16),
+                                              (1, 3, 16384, 0, torch.bfloat16),
+                                              (5, 2, 65536, 1, torch.bfloat16),
+                                              (4, 3, 16384, 1, torch.bfloat16),
+                                              (3, 1, 131072, 1, torch.bfloat16),
+                                              (2, 1, 262144, 1, torch.bfloat16),
+                                              (3, 2, 16384, 1, torch.float16),
+                                              (2, 2, 65536, 0, torch.float16),
+                                              (3, 1, 131072, 1, torch.float16)])
+def test_three_pass_bf16_tc_rows(lc, B, H, N, mode, dtype):
+    """16-bit three-pass with pass 2 on tcgen05 (m = 2 .. 64: register and
     big-column pass 1 writing planar rows; causal and circular; odd B = a
-    zero partner channel): recompute and saved-U backward agree bit for bit,
-    both within the 16-bit bar of the oracle."""
-    dtype = torch.bfloat16
+    zero partner channel; fp16 I/O with bf16 rows): recompute and saved-U
+    backward agree bit for bit, both within the 16-bit bar of the oracle."""
     inp = layer_inputs(lc, B, H, N, dtype)
     cfg = fb.RegularizationConfig(**CFG)
     plan, got = run_layer(inp, N, H, dtype, cfg, mode=mode, engine=2)
@@ -502,7 +508,8 @@ def test_shard_stage_layouts():
     assert torch.equal(back, ref)
 
 
-@pytest.mark.parametrize("dtype,N", [(torch.float32, 16384), (torch.bfloat16, 32768)])
+@pytest.mark.parametrize("dtype,N", [(torch.float32, 16384), (torch.bfloat16, 32768),
+                                     (torch.float16, 32768)])
 def test_three_pass_saved_transform(lc, dtype, N):
     """Three-pass training step: the forward keeps its pass-2 row spectra of u
     and the backward runs passes 1/2 on dy only (dD from the lag-0 dKbar).
