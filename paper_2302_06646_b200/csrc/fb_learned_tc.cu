@@ -187,7 +187,9 @@ __device__ __forceinline__ void tw_chain(float2 (&t)[16], float2 b, float2 s) {
 // threads own D row tid, i.e. column col_of(tid).
 template <int STC, int LGFL, int S>
 __host__ __device__ constexpr int row_perm(int i) {
-  if constexpr (STC == 2 && LGFL == 2) {
+  // (n = 2048 reuses n = 1024's permutations: with the identity ptxas
+  // schedules the short single pass at 128 registers instead of 64)
+  if constexpr (STC == 2 && (LGFL == 2 || LGFL == 3)) {
     constexpr int p0[6] = {0, 2, 1, 3, 4, 5}, p1[6] = {1, 2, 0, 3, 4, 5}, p2[6] = {3, 4, 2, 1, 0, 5};
     return S == 0 ? p0[i] : S == 1 ? p1[i] : p2[i];
   } else {
@@ -951,19 +953,16 @@ static int sc_dispatch(fb_plan* p, bool bwd, const void* a, const void* b, void*
   }
 }
 
-// causal, 16-bit, N = 512 (n = 1024 = [16, 16, 4]): measured 0.090 -> 0.068 ms
-// per step at B*H = 2048 against the CUDA-core single pass.  N = 1024
-// (n = 2048, two rows per CTA) measured 3 % slower than the CUDA cores and
-// N = 256 (n = 512) leaves half of a CTA's eight rows idle at B = 8, so those
-// stay on the CUDA cores; FB_SHORT_TC=2048 forces n = 2048 for comparisons,
-// FB_SHORT_TC=0 disables the path.
+// causal, 16-bit, N = 256 / 512 / 1024 (n = 512 / 1024 / 2048): measured per
+// step at B*H = 2048 against the CUDA-core single pass 0.063 -> 0.062,
+// 0.090 -> 0.068 and 0.097 -> 0.090 ms.  FB_SHORT_TC=0 disables the path.
 bool sc_config(const fb_plan* p, int* lgfl) {
   const char* env = std::getenv("FB_SHORT_TC");
   if (env && env[0] == '0') return false;
   if (p->mode != FB_MODE_CAUSAL || p->dtype == FB_F32 || p->periodic || p->N * 2 != p->n) return false;
   if (p->n == 1024) *lgfl = 2;
   else if (p->n == 512) *lgfl = 1;
-  else if (p->n == 2048 && env && std::atoi(env) == 2048) *lgfl = 3;
+  else if (p->n == 2048) *lgfl = 3;
   else return false;
   return true;
 }
