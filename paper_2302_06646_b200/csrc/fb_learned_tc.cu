@@ -187,9 +187,9 @@ __device__ __forceinline__ void tw_chain(float2 (&t)[16], float2 b, float2 s) {
 // threads own D row tid, i.e. column col_of(tid).
 template <int STC, int LGFL, int S>
 __host__ __device__ constexpr int row_perm(int i) {
-  // (n = 2048 reuses n = 1024's permutations: with the identity ptxas
-  // schedules the short single pass at 128 registers instead of 64)
-  if constexpr (STC == 2 && (LGFL == 2 || LGFL == 3)) {
+  // (n = 512 / 2048 reuse n = 1024's permutations: with the identity ptxas
+  // schedules the short single pass at 100-128 registers instead of 64)
+  if constexpr (STC == 2) {
     constexpr int p0[6] = {0, 2, 1, 3, 4, 5}, p1[6] = {1, 2, 0, 3, 4, 5}, p2[6] = {3, 4, 2, 1, 0, 5};
     return S == 0 ? p0[i] : S == 1 ? p1[i] : p2[i];
   } else {
