@@ -237,7 +237,7 @@ int fb_learned_plan_factors(const fb_learned_plan* plan, int64_t* factors, int64
                             int64_t* param_count);
 /* Kernel family the plan runs: 0 = generic stage walk (any chain), 1 = the
  * factor-specialised CUDA-core kernels (power-of-two factors <= 16), 2 =
- * tcgen05 (16-bit modes, chains [16] * S + [2|4|8], n = 32 .. 2048). */
+ * tcgen05 (16-bit modes, chains [16] * S + [2|4|8|16], n = 32 .. 4096). */
 int fb_learned_plan_engine(const fb_learned_plan* plan, int* engine);
 size_t fb_learned_workspace_size(const fb_learned_plan* plan, int64_t B);
 int fb_learned_fwd(fb_learned_plan* plan, const float* blocks, const void* x, void* y, int64_t B,

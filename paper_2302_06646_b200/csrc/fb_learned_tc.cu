@@ -1,7 +1,7 @@
 // FlashButterfly-B200 radix-16 stages on the tcgen05 tensor cores: the
 // learned butterfly (K5) for the 16-bit modes and the chains build_plan(n, 16)
 // gives for n = 16^S x FL (S in {1, 2} stages of factor 16, a last factor FL
-// in {2, 4, 8}: n = 32 .. 2048, config 4's n = 1024 = [16, 16, 4]); and, with
+// in {2, 4, 8, 16}: n = 32 .. 4096, config 4's n = 1024 = [16, 16, 4]); and, with
 // the blocks fixed to the DFT, the short causal single pass (N = 256, 512;
 // sc_fwd_kernel / sc_bwd_kernel at the end of this file).
 //
@@ -26,7 +26,7 @@
 // Every stage boundary: tcgen05.mma (M = 128 x 2 tiles, N = 32, K = 32) into
 // TMEM, tcgen05.ld by the column's thread, twiddle (power chain from one
 // table value), bf16 store scattered into the next stage's operand rows.
-// The last stage (factor FL <= 8) runs as the same GEMM with 16 / FL of its
+// The last stage (factor FL <= 16) runs as the same GEMM with 16 / FL of its
 // columns per operand row against a block-diagonal table (its rows are then
 // simply 16 consecutive natural-order values).  The backward
 // recomputes the forward stage inputs, keeps them in shared memory, and
@@ -237,7 +237,7 @@ __device__ __forceinline__ void fwd_epilogue(uint32_t tmem_d, unsigned char* nex
     } else {
       const int e = (r << LGN) + (seg << LGL) + (a << LGR) + q;  // natural order
       // row e >> 4 = ((r << LGN) + (seg << LGL)) >> 4 | (a << LGR) >> 4 (q < 2^LGR <= 16)
-      static_assert(LGR <= 4, "the last factor-16 stage has rest = FL <= 8");
+      static_assert(LGR <= 4, "the last factor-16 stage has rest = FL <= 16");
       const int rowb = row_of<STC, LGFL, STC>(((r << LGN) + (seg << LGL)) >> 4);
       const int row = rowb | row_of<STC, LGFL, STC>((a << LGR) >> 4);
       *reinterpret_cast<uint32_t*>(next + op_off(row, e & 15)) = o;
@@ -904,7 +904,8 @@ cudaError_t dispatch(int stc, int lgfl, bool bwd, const float* blocks, const voi
 #define LT_CASE(S_, F_)                                                                        \
   if (stc == S_ && lgfl == F_)                                                                 \
     return launch<IO, S_, F_>(bwd, blocks, x, g, out, gpart, omap, tw, B, H, P, s);
-  LT_CASE(1, 1) LT_CASE(1, 2) LT_CASE(1, 3) LT_CASE(2, 1) LT_CASE(2, 2) LT_CASE(2, 3)
+  LT_CASE(1, 1) LT_CASE(1, 2) LT_CASE(1, 3) LT_CASE(1, 4)
+  LT_CASE(2, 1) LT_CASE(2, 2) LT_CASE(2, 3) LT_CASE(2, 4)
 #undef LT_CASE
   return cudaErrorInvalidValue;
 }
@@ -1005,13 +1006,13 @@ int sc_bwd(fb_plan* p, const void* dy, const void* u, void* du, float2* spart, f
                              : sc_dispatch<__half>(p, true, dy, u, du, spart, ddpart, B, s);
 }
 
-// chains [16] * stc + [2^lgfl], stc in {1, 2}, lgfl in {1, 2, 3}; 16-bit modes
+// chains [16] * stc + [2^lgfl], stc in {1, 2}, lgfl in {1, 2, 3, 4}; 16-bit modes
 bool lt_config(int64_t n, const int64_t* f, int nst, int dtype, int* stc, int* lgfl) {
   if (dtype == FB_F32 || nst < 2 || nst > 3) return false;
   for (int i = 0; i + 1 < nst; ++i)
     if (f[i] != 16) return false;
   const int64_t fl = f[nst - 1];
-  if (fl != 2 && fl != 4 && fl != 8) return false;
+  if (fl != 2 && fl != 4 && fl != 8 && fl != 16) return false;
   int lg = 0;
   while ((int64_t(1) << lg) < fl) ++lg;
   if ((int64_t(1) << (4 * (nst - 1) + lg)) != n) return false;

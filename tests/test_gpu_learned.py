@@ -116,11 +116,12 @@ def test_config4_shape_16bit(lc, dtype):
     assert rel_l2(db.cpu().numpy()[heads], rdb) < 2e-2
 
 
-@pytest.mark.parametrize("n,B", [(32, 5), (64, 3), (128, 2), (512, 9), (1024, 1), (1024, 6), (1024, 10), (2048, 3), (2048, 19)])
+@pytest.mark.parametrize("n,B", [(32, 5), (64, 3), (128, 2), (256, 7), (512, 9), (1024, 1), (1024, 6),
+                                 (1024, 10), (2048, 3), (2048, 19), (4096, 3)])
 @pytest.mark.parametrize("dtype", [torch.bfloat16, torch.float16])
 def test_tensor_core_chains_16bit(lc, n, B, dtype):
     """The tcgen05 kernels (fb_learned_tc.cu) own the 16-bit chains
-    [16] * S + [FL] (n = 32 .. 2048); B not a multiple of the CTA's
+    [16] * S + [FL] (n = 32 .. 4096); B not a multiple of the CTA's
     4096 / n rows, so the last row group is partial."""
     H, r = 3, 16
     blocks, x, g = batch_case(lc, B, H, n, r, seed=n + B)
