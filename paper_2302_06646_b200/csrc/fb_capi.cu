@@ -229,7 +229,7 @@ int fb_plan_create(fb_plan** out, int64_t N, int64_t H, int mode, int dtype, int
   if (!rc) rc = cuda_status(cudaMalloc(&p->kbar, sizeof(float) * H * N), "cudaMalloc(kbar)");
   if (!rc) rc = cuda_status(cudaMalloc(&p->d, sizeof(float) * H), "cudaMalloc(D)");
   if (!rc && p->use_tc) rc = tc_init(p);
-  if (!rc && engine == FB_ENGINE_SINGLE && !simt && !p->use_tc && sc_config(p, &p->sc_lgfl)) {
+  if (!rc && engine == FB_ENGINE_SINGLE && !simt && !p->use_tc && sc_config(p, &p->sc_stc, &p->sc_lgfl)) {
     p->use_sc = true;
     rc = sc_init(p);
   }

@@ -31,9 +31,9 @@ struct fb_plan {
   float* kf_scale = nullptr; // [H] inverse of that per-head power-of-two scale
   void* tcr_mats = nullptr;  // three-pass rows on tcgen05: DFT blocks (fb_single_tc.cu)
   // short single pass (N = n / 2 <= 1024, 16-bit) on the radix-16 tcgen05
-  // stages of fb_learned_tc.cu with the DFT as blocks: chain [16, 16, 2^sc_lgfl]
+  // stages of fb_learned_tc.cu with the DFT as blocks: chain [16] * sc_stc + [2^sc_lgfl]
   bool use_sc = false;
-  int sc_lgfl = 0;
+  int sc_stc = 0, sc_lgfl = 0;
   float2* sc_blocks = nullptr;  // the chain's DFT blocks [16 x 16, 16 x 16, FL x FL]
   float2* sc_tw = nullptr;      // exp(-2 pi i t / n), t < n
   bool prepared = false;
@@ -177,7 +177,7 @@ int lb_bwd(fb_learned_plan* p, const float* blocks, const void* x, const void* g
 bool lt_config(int64_t n, const int64_t* f, int nst, int dtype, int* stc, int* lgfl);
 int lt_rows(int64_t n);
 // short causal single pass on the same stages (fb_learned_tc.cu)
-bool sc_config(const fb_plan* p, int* lgfl);
+bool sc_config(const fb_plan* p, int* stc, int* lgfl);
 int sc_init(fb_plan* p);
 int sc_chunks(const fb_plan* p, int64_t B);
 int sc_fwd(fb_plan* p, const void* u, void* y, int64_t B, cudaStream_t s);

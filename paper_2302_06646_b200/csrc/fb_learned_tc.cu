@@ -747,7 +747,9 @@ __global__ void __launch_bounds__(kThreads)
   float2* SP = reinterpret_cast<float2*>(sm + (STC + 2) * kOp);      // conj(U) DY [o][J]
   unsigned char* TAB = sm + (STC + 4) * kOp;
   Smem* ss = reinterpret_cast<Smem*>(TAB + (STC + 1) * kTab);
-  float* ss_red = reinterpret_cast<float*>(ss + 1);  // [8] warp partials of dD
+  // dD partials: per warp (n >= 512: a warp's columns are one row), or per
+  // row (n < 512: a warp holds 32 / (n / 16) rows)
+  float* ss_red = reinterpret_cast<float*>(ss + 1);  // [max(8, R)]
   const float2* W = reinterpret_cast<const float2*>(blocks);
   // rows: hpc > 1 -> hpc whole heads per CTA (npairs divides R), else CTA
   // (h, k) owns pairs k R .. k R + R - 1 of head h
@@ -774,9 +776,14 @@ __global__ void __launch_bounds__(kThreads)
     float dd = 0.f;
 #pragma unroll
     for (int p = 0; p < 8; ++p) dd = fmaf(ua[p], ga[p], fmaf(ub[p], gb[p], dd));
+    constexpr int CW = (1 << LGC) < 32 ? (1 << LGC) : 32;  // a row's lanes in one warp
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) dd += __shfl_xor_sync(0xffffffffu, dd, o);
-    if ((threadIdx.x & 31) == 0) ss_red[threadIdx.x >> 5] = dd;
+    for (int o = CW / 2; o > 0; o >>= 1) dd += __shfl_xor_sync(0xffffffffu, dd, o);
+    if constexpr (CW == 32) {
+      if ((threadIdx.x & 31) == 0) ss_red[threadIdx.x >> 5] = dd;
+    } else {
+      if ((threadIdx.x & (CW - 1)) == 0) ss_red[threadIdx.x >> LGC] = dd;
+    }
 #pragma unroll
     for (int s = 0; s < STC; ++s) wt[s] = table_entry<16>(W + 256 * s);
     wt[STC] = table_entry<FL>(W + 256 * STC);
@@ -848,9 +855,13 @@ __global__ void __launch_bounds__(kThreads)
     if (head >= H) break;
     if (threadIdx.x == 0) {
       float t = 0.f;
-      for (int w = 0; w < kThreads / 32; ++w) {
-        const int rw = (32 * w) >> LGC;
-        if (rw >= r0 && rw < r0 + nr) t += ss_red[w];
+      if constexpr ((1 << LGC) >= 32) {
+        for (int w = 0; w < kThreads / 32; ++w) {
+          const int rw = (32 * w) >> LGC;
+          if (rw >= r0 && rw < r0 + nr) t += ss_red[w];
+        }
+      } else {
+        for (int r = r0; r < r0 + nr; ++r) t += ss_red[r];
       }
       ddpart[(size_t)head * chunks + k] = t;
     }
@@ -918,10 +929,10 @@ static int sc_heads_per_cta(const fb_plan* p, int64_t B) {
   const int64_t R = ltc::kNB / p->n, np = (B + 1) / 2;
   return (np < R && R % np == 0) ? (int)(R / np) : 1;
 }
-template <typename IO, int LGFL>
+template <typename IO, int STC, int LGFL>
 static int sc_launch(fb_plan* p, bool bwd, const void* a, const void* b, void* out, float2* spart,
                      float* ddpart, int64_t B, cudaStream_t s) {
-  constexpr int STC = 2, N = 1 << (8 + LGFL), R = ltc::kNB / N;
+  constexpr int N = 1 << (4 * STC + LGFL), R = ltc::kNB / N;
   const int npairs = (int)((B + 1) / 2);
   if (!bwd) {
     auto k = ltc::sc_fwd_kernel<IO, STC, LGFL>;
@@ -933,7 +944,7 @@ static int sc_launch(fb_plan* p, bool bwd, const void* a, const void* b, void* o
         (int)p->H, npairs, rows);
   } else {
     auto k = ltc::sc_bwd_kernel<IO, STC, LGFL>;
-    constexpr size_t sm = 1024 + (STC + 4) * ltc::kOp + (STC + 1) * ltc::kTab + 128;
+    constexpr size_t sm = 1024 + (STC + 4) * ltc::kOp + (STC + 1) * ltc::kTab + 64 + 4 * (R > 8 ? R : 8);
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     const int hpc = sc_heads_per_cta(p, B);
     const dim3 grid = hpc > 1 ? dim3((unsigned)((p->H + hpc - 1) / hpc), 1)
@@ -947,29 +958,33 @@ static int sc_launch(fb_plan* p, bool bwd, const void* a, const void* b, void* o
 template <typename IO>
 static int sc_dispatch(fb_plan* p, bool bwd, const void* a, const void* b, void* out, float2* spart,
                        float* ddpart, int64_t B, cudaStream_t s) {
-  switch (p->sc_lgfl) {
-    case 1: return sc_launch<IO, 1>(p, bwd, a, b, out, spart, ddpart, B, s);
-    case 2: return sc_launch<IO, 2>(p, bwd, a, b, out, spart, ddpart, B, s);
-    default: return sc_launch<IO, 3>(p, bwd, a, b, out, spart, ddpart, B, s);
-  }
+#define SC_CASE(S_, F_)                  \
+  if (p->sc_stc == S_ && p->sc_lgfl == F_) \
+    return sc_launch<IO, S_, F_>(p, bwd, a, b, out, spart, ddpart, B, s);
+  SC_CASE(1, 1) SC_CASE(1, 2) SC_CASE(1, 3) SC_CASE(1, 4) SC_CASE(2, 1) SC_CASE(2, 2) SC_CASE(2, 3)
+#undef SC_CASE
+  return FB_ERR_UNSUPPORTED;
 }
 
-// causal, 16-bit, N = 256 / 512 / 1024 (n = 512 / 1024 / 2048): measured per
-// step at B*H = 2048 against the CUDA-core single pass 0.063 -> 0.062,
-// 0.090 -> 0.068 and 0.097 -> 0.090 ms.  FB_SHORT_TC=0 disables the path.
-bool sc_config(const fb_plan* p, int* lgfl) {
+// causal, 16-bit, n = 2N = [16] * stc + [2^lgfl] (N = 128 .. 1024; plans
+// pad shorter N to n = 256): measured per step at B*H = 2048 against the
+// CUDA-core single pass 0.0585 -> 0.0565 (N = 128), 0.063 -> 0.062 (256),
+// 0.090 -> 0.068 (512) and 0.097 -> 0.090 ms (1024).  FB_SHORT_TC=0
+// disables the path.
+bool sc_config(const fb_plan* p, int* stc, int* lgfl) {
   const char* env = std::getenv("FB_SHORT_TC");
   if (env && env[0] == '0') return false;
   if (p->mode != FB_MODE_CAUSAL || p->dtype == FB_F32 || p->periodic || p->N * 2 != p->n) return false;
-  if (p->n == 1024) *lgfl = 2;
-  else if (p->n == 512) *lgfl = 1;
-  else if (p->n == 2048) *lgfl = 3;
-  else return false;
+  int lg = 0;
+  while ((int64_t(1) << lg) < p->n) ++lg;
+  if ((int64_t(1) << lg) != p->n || lg < 5 || lg > 11) return false;
+  *stc = lg > 8 ? 2 : 1;  // n = 32 .. 256: [16, FL]; 512 .. 2048: [16, 16, FL]
+  *lgfl = lg - 4 * *stc;
   return true;
 }
 int sc_init(fb_plan* p) {
   const int64_t n = p->n, FL = int64_t(1) << p->sc_lgfl;
-  std::vector<float2> blk, tw((size_t)n);
+  std::vector<float2> blk, tw((size_t)n);  // blocks: [16 x 16] * stc, [FL x FL]
   auto dft = [&](int64_t f) {
     for (int64_t a = 0; a < f; ++a)
       for (int64_t q = 0; q < f; ++q) {
@@ -977,8 +992,7 @@ int sc_init(fb_plan* p) {
         blk.push_back(make_float2((float)std::cos(ang), (float)std::sin(ang)));
       }
   };
-  dft(16);
-  dft(16);
+  for (int i = 0; i < p->sc_stc; ++i) dft(16);
   dft(FL);
   for (int64_t t = 0; t < n; ++t) {
     const double ang = -2.0 * M_PI * (double)t / (double)n;

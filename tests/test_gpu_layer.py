@@ -219,12 +219,12 @@ def test_dimension_errors():
 
 
 # ------------------------------------------------------------ tcgen05 single-pass
-@pytest.mark.parametrize("N", [4096, 2048, 1024, 512, 256])
+@pytest.mark.parametrize("N", [4096, 2048, 1024, 512, 256, 128])
 @pytest.mark.parametrize("dtype", [torch.bfloat16, torch.float16])
 @pytest.mark.parametrize("B,H", [(2, 2), (3, 3), (5, 1), (16, 3), (8, 5)])
 def test_tensor_core_single_pass(lc, dtype, B, H, N):
     """N = 4096, and N = 2048 on the same n = 8192 transform (16 data rows);
-    N = 256 / 512 / 1024 on the radix-16 stages (fb_learned_tc.cu short single pass)."""
+    N = 128 / 256 / 512 / 1024 on the radix-16 stages (fb_learned_tc.cu short single pass)."""
     inp = layer_inputs(lc, B, H, N, dtype)
     cfg = fb.RegularizationConfig(**CFG)
     plan, got = run_layer(inp, N, H, dtype, cfg, engine=1)
