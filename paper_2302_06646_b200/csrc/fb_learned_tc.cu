@@ -611,37 +611,38 @@ __device__ __forceinline__ void adjoint_chain(uint32_t tm, uint32_t sbase, uint3
   adjoint_stage(std::integral_constant<int, 0>());
 }
 
-// two real channels of one head as the stage-0 column (r, q): slots p < 8 hold
-// t = p rest0 + q < N / 2 (re = channel b0, im = b1), slots 8..15 the zero pad
-template <typename IO, int LGN>
-__device__ __forceinline__ void load_pair_col(uint32_t (&u)[16], float (&a)[8], float (&b)[8],
+// two real channels of one head as the stage-0 column (r, q): slots p < PS
+// hold t = p rest0 + q (re = channel b0, im = b1): PS = 8 causal (t < n / 2,
+// slots 8..15 the zero pad), PS = 16 circular (t < n = N)
+template <typename IO, int LGN, int PS>
+__device__ __forceinline__ void load_pair_col(uint32_t (&u)[16], float (&a)[PS], float (&b)[PS],
                                               const IO* __restrict__ sig, int q, int b0, int B,
                                               int H, int h, bool valid) {
-  constexpr int LGC = LGN - 4, NS = 1 << (LGN - 1);
+  constexpr int LGC = LGN - 4, NS = PS == 16 ? 1 << LGN : 1 << (LGN - 1);
 #pragma unroll
   for (int p = 0; p < 16; ++p) u[p] = 0u;
 #pragma unroll
-  for (int p = 0; p < 8; ++p) a[p] = b[p] = 0.f;
+  for (int p = 0; p < PS; ++p) a[p] = b[p] = 0.f;
   if (!valid) return;
   const IO* s0 = sig + ((size_t)b0 * H + h) * NS;
   const IO* s1 = sig + ((size_t)(b0 + 1) * H + h) * NS;
   const bool two = b0 + 1 < B;
 #pragma unroll
-  for (int p = 0; p < 8; ++p) {
+  for (int p = 0; p < PS; ++p) {
     a[p] = ld(s0 + (p << LGC) + q);
     b[p] = two ? ld(s1 + (p << LGC) + q) : 0.f;
   }
 #pragma unroll
-  for (int p = 0; p < 8; ++p) u[p] = pack_bf16(make_float2(a[p], b[p]));
+  for (int p = 0; p < PS; ++p) u[p] = pack_bf16(make_float2(a[p], b[p]));
 }
-template <typename IO>
+template <typename IO, int PS>
 __device__ __forceinline__ void store_pair_col(IO* __restrict__ sig, const float (&v)[32], int LGC,
                                                int q, int b0, int B, int H, int h, int NS) {
   IO* s0 = sig + ((size_t)b0 * H + h) * NS;
   IO* s1 = sig + ((size_t)(b0 + 1) * H + h) * NS;
   const bool two = b0 + 1 < B;
 #pragma unroll
-  for (int p = 0; p < 8; ++p) {
+  for (int p = 0; p < PS; ++p) {
     st(s0 + (p << LGC) + q, v[2 * p]);
     if (two) st(s1 + (p << LGC) + q, v[2 * p + 1]);
   }
@@ -659,7 +660,7 @@ __device__ __forceinline__ float2 kf_at(const float2* __restrict__ kf, float dn,
   return k;
 }
 
-template <typename IO, int STC, int LGFL>
+template <typename IO, int STC, int LGFL, bool CIRC>
 __global__ void __launch_bounds__(kThreads)
     sc_fwd_kernel(const float* __restrict__ blocks, const IO* __restrict__ u, IO* __restrict__ y,
                   const float2* __restrict__ kf, const float* __restrict__ Dg,
@@ -679,10 +680,11 @@ __global__ void __launch_bounds__(kThreads)
   {
     const int c = threadIdx.x, r = c >> LGC, q = c & ((1 << LGC) - 1);
     const int gr = blockIdx.x * R + r;
+    constexpr int PS = CIRC ? 16 : 8;
     uint32_t x[16];
-    float xa[8], xb[8];
+    float xa[PS], xb[PS];
     float2 wt[STC + 1];
-    load_pair_col<IO, LGN>(x, xa, xb, u, q, 2 * (gr % npairs), B, H, gr / npairs, gr < rows);
+    load_pair_col<IO, LGN, PS>(x, xa, xb, u, q, 2 * (gr % npairs), B, H, gr / npairs, gr < rows);
 #pragma unroll
     for (int s = 0; s < STC; ++s) wt[s] = table_entry<16>(W + 256 * s);
     wt[STC] = table_entry<FL>(W + 256 * STC);
@@ -722,8 +724,9 @@ __global__ void __launch_bounds__(kThreads)
                                   const int r = c >> LGC, q = c & ((1 << LGC) - 1);
                                   const int gr = blockIdx.x * R + r;
                                   if (gr < rows)
-                                    store_pair_col<IO>(y, v, LGC, q, 2 * (gr % npairs), B, H,
-                                                       gr / npairs, N / 2);
+                                    store_pair_col<IO, CIRC ? 16 : 8>(y, v, LGC, q, 2 * (gr % npairs),
+                                                                      B, H, gr / npairs,
+                                                                      CIRC ? N : N / 2);
                                 });
   tc::fence_before();
   __syncthreads();
@@ -731,7 +734,7 @@ __global__ void __launch_bounds__(kThreads)
 }
 
 // backward: CTA (h, k) owns pairs k R .. k R + R - 1 of head h
-template <typename IO, int STC, int LGFL>
+template <typename IO, int STC, int LGFL, bool CIRC>
 __global__ void __launch_bounds__(kThreads)
     sc_bwd_kernel(const float* __restrict__ blocks, const IO* __restrict__ dy,
                   const IO* __restrict__ u, IO* __restrict__ du, const float2* __restrict__ kf,
@@ -768,14 +771,15 @@ __global__ void __launch_bounds__(kThreads)
     const int hr = row_head(r);
     uint32_t x[16];
     float2 wt[STC + 1];
-    float ua[8], ub[8], ga[8], gb[8];
-    load_pair_col<IO, LGN>(x, ua, ub, u, q, 2 * pr, B, H, hr, row_ok(r));
-    load_pair_col<IO, LGN>(xd, ga, gb, dy, q, 2 * pr, B, H, hr, row_ok(r));
+    constexpr int PS = CIRC ? 16 : 8;
+    float ua[PS], ub[PS], ga[PS], gb[PS];
+    load_pair_col<IO, LGN, PS>(x, ua, ub, u, q, 2 * pr, B, H, hr, row_ok(r));
+    load_pair_col<IO, LGN, PS>(xd, ga, gb, dy, q, 2 * pr, B, H, hr, row_ok(r));
     // dD partial = sum dy u over the CTA's channels, in fp32 from the 16-bit
     // inputs (not the lag-0 bin of the bf16-operand spectrum: dD can be small)
     float dd = 0.f;
 #pragma unroll
-    for (int p = 0; p < 8; ++p) dd = fmaf(ua[p], ga[p], fmaf(ub[p], gb[p], dd));
+    for (int p = 0; p < PS; ++p) dd = fmaf(ua[p], ga[p], fmaf(ub[p], gb[p], dd));
     constexpr int CW = (1 << LGC) < 32 ? (1 << LGC) : 32;  // a row's lanes in one warp
 #pragma unroll
     for (int o = CW / 2; o > 0; o >>= 1) dd += __shfl_xor_sync(0xffffffffu, dd, o);
@@ -842,8 +846,9 @@ __global__ void __launch_bounds__(kThreads)
                                 [&](int c, const float (&v)[32]) {
                                   const int r = c >> LGC, q = c & ((1 << LGC) - 1);
                                   if (row_ok(r))
-                                    store_pair_col<IO>(du, v, LGC, q, 2 * row_pair(r), B, H,
-                                                       row_head(r), N / 2);
+                                    store_pair_col<IO, CIRC ? 16 : 8>(du, v, LGC, q, 2 * row_pair(r),
+                                                                      B, H, row_head(r),
+                                                                      CIRC ? N : N / 2);
                                 });
   // per head of the CTA: the dD partial (warps in order; a warp's columns are
   // one row) and the dK spectrum partial (rows in order, natural frequency order)
@@ -929,13 +934,13 @@ static int sc_heads_per_cta(const fb_plan* p, int64_t B) {
   const int64_t R = ltc::kNB / p->n, np = (B + 1) / 2;
   return (np < R && R % np == 0) ? (int)(R / np) : 1;
 }
-template <typename IO, int STC, int LGFL>
+template <typename IO, int STC, int LGFL, bool CIRC>
 static int sc_launch(fb_plan* p, bool bwd, const void* a, const void* b, void* out, float2* spart,
                      float* ddpart, int64_t B, cudaStream_t s) {
   constexpr int N = 1 << (4 * STC + LGFL), R = ltc::kNB / N;
   const int npairs = (int)((B + 1) / 2);
   if (!bwd) {
-    auto k = ltc::sc_fwd_kernel<IO, STC, LGFL>;
+    auto k = ltc::sc_fwd_kernel<IO, STC, LGFL, CIRC>;
     constexpr size_t sm = ltc::fwd_smem<STC, LGFL>();
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     const int rows = (int)(p->H * npairs);
@@ -943,7 +948,7 @@ static int sc_launch(fb_plan* p, bool bwd, const void* a, const void* b, void* o
         (const float*)p->sc_blocks, (const IO*)a, (IO*)out, p->kf, p->d, p->sc_tw, (int)B,
         (int)p->H, npairs, rows);
   } else {
-    auto k = ltc::sc_bwd_kernel<IO, STC, LGFL>;
+    auto k = ltc::sc_bwd_kernel<IO, STC, LGFL, CIRC>;
     constexpr size_t sm = 1024 + (STC + 4) * ltc::kOp + (STC + 1) * ltc::kTab + 64 + 4 * (R > 8 ? R : 8);
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     const int hpc = sc_heads_per_cta(p, B);
@@ -958,23 +963,27 @@ static int sc_launch(fb_plan* p, bool bwd, const void* a, const void* b, void* o
 template <typename IO>
 static int sc_dispatch(fb_plan* p, bool bwd, const void* a, const void* b, void* out, float2* spart,
                        float* ddpart, int64_t B, cudaStream_t s) {
-#define SC_CASE(S_, F_)                  \
-  if (p->sc_stc == S_ && p->sc_lgfl == F_) \
-    return sc_launch<IO, S_, F_>(p, bwd, a, b, out, spart, ddpart, B, s);
+#define SC_CASE(S_, F_)                                                          \
+  if (p->sc_stc == S_ && p->sc_lgfl == F_)                                         \
+    return p->mode == FB_MODE_CIRCULAR                                             \
+               ? sc_launch<IO, S_, F_, true>(p, bwd, a, b, out, spart, ddpart, B, s) \
+               : sc_launch<IO, S_, F_, false>(p, bwd, a, b, out, spart, ddpart, B, s);
   SC_CASE(1, 1) SC_CASE(1, 2) SC_CASE(1, 3) SC_CASE(1, 4) SC_CASE(2, 1) SC_CASE(2, 2) SC_CASE(2, 3)
 #undef SC_CASE
   return FB_ERR_UNSUPPORTED;
 }
 
-// causal, 16-bit, n = 2N = [16] * stc + [2^lgfl] (N = 128 .. 1024; plans
-// pad shorter N to n = 256): measured per step at B*H = 2048 against the
+// 16-bit, n = [16] * stc + [2^lgfl] = 2N causal (N = 128 .. 1024; plans pad
+// shorter N to n = 256) or N circular (N = 256 .. 2048): measured per step at B*H = 2048 against the
 // CUDA-core single pass 0.0585 -> 0.0565 (N = 128), 0.063 -> 0.062 (256),
 // 0.090 -> 0.068 (512) and 0.097 -> 0.090 ms (1024).  FB_SHORT_TC=0
 // disables the path.
 bool sc_config(const fb_plan* p, int* stc, int* lgfl) {
   const char* env = std::getenv("FB_SHORT_TC");
   if (env && env[0] == '0') return false;
-  if (p->mode != FB_MODE_CAUSAL || p->dtype == FB_F32 || p->periodic || p->N * 2 != p->n) return false;
+  if (p->dtype == FB_F32 || p->periodic) return false;
+  // causal: n = 2N (zero half); circular: n = N
+  if (p->mode == FB_MODE_CAUSAL ? p->N * 2 != p->n : p->N != p->n) return false;
   int lg = 0;
   while ((int64_t(1) << lg) < p->n) ++lg;
   if ((int64_t(1) << lg) != p->n || lg < 5 || lg > 11) return false;

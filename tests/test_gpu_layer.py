@@ -75,6 +75,19 @@ def test_circular_mode_fp32(lc, N):
     assert_parity(got, oracle_layer(lc, inp, cfg, causal=False), 1e-5)
 
 
+@pytest.mark.parametrize("N", [256, 512, 1024, 2048])
+@pytest.mark.parametrize("dtype", [torch.bfloat16, torch.float16])
+@pytest.mark.parametrize("B,H", [(3, 2), (8, 3)])
+def test_circular_mode_tensor_cores(lc, dtype, B, H, N):
+    """16-bit circular mode (n = N, no zero padding) on the radix-16 tcgen05
+    single pass."""
+    inp = layer_inputs(lc, B, H, N, dtype)
+    cfg = fb.RegularizationConfig(**CFG)
+    plan, got = run_layer(inp, N, H, dtype, cfg, mode=0)
+    assert plan.tensor_cores
+    assert_parity(got, oracle_layer(lc, inp, cfg, causal=False), TOL[dtype])
+
+
 def test_dropout_training_mode(lc):
     # on-device xoshiro256++ stream must reproduce the reference mask exactly
     inp = layer_inputs(lc, 2, 3, 512, torch.float32)
