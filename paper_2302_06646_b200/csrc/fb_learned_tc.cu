@@ -969,12 +969,13 @@ static int sc_dispatch(fb_plan* p, bool bwd, const void* a, const void* b, void*
                ? sc_launch<IO, S_, F_, true>(p, bwd, a, b, out, spart, ddpart, B, s) \
                : sc_launch<IO, S_, F_, false>(p, bwd, a, b, out, spart, ddpart, B, s);
   SC_CASE(1, 1) SC_CASE(1, 2) SC_CASE(1, 3) SC_CASE(1, 4) SC_CASE(2, 1) SC_CASE(2, 2) SC_CASE(2, 3)
+  SC_CASE(2, 4)
 #undef SC_CASE
   return FB_ERR_UNSUPPORTED;
 }
 
 // 16-bit, n = [16] * stc + [2^lgfl] = 2N causal (N = 128 .. 1024; plans pad
-// shorter N to n = 256) or N circular (N = 256 .. 2048): measured per step at B*H = 2048 against the
+// shorter N to n = 256) or N circular (N = 256 .. 4096): measured per step at B*H = 2048 against the
 // CUDA-core single pass 0.0585 -> 0.0565 (N = 128), 0.063 -> 0.062 (256),
 // 0.090 -> 0.068 (512) and 0.097 -> 0.090 ms (1024).  FB_SHORT_TC=0
 // disables the path.
@@ -986,7 +987,10 @@ bool sc_config(const fb_plan* p, int* stc, int* lgfl) {
   if (p->mode == FB_MODE_CAUSAL ? p->N * 2 != p->n : p->N != p->n) return false;
   int lg = 0;
   while ((int64_t(1) << lg) < p->n) ++lg;
-  if ((int64_t(1) << lg) != p->n || lg < 5 || lg > 11) return false;
+  // n = 4096 ([16, 16, 16]) only for circular N = 4096: causal N = 2048 runs
+  // on the 64 x 128 kernels (n = 8192)
+  if ((int64_t(1) << lg) != p->n || lg < 5 || lg > 12 || (lg == 12 && p->mode == FB_MODE_CAUSAL))
+    return false;
   *stc = lg > 8 ? 2 : 1;  // n = 32 .. 256: [16, FL]; 512 .. 2048: [16, 16, FL]
   *lgfl = lg - 4 * *stc;
   return true;

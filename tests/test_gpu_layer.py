@@ -75,7 +75,7 @@ def test_circular_mode_fp32(lc, N):
     assert_parity(got, oracle_layer(lc, inp, cfg, causal=False), 1e-5)
 
 
-@pytest.mark.parametrize("N", [256, 512, 1024, 2048])
+@pytest.mark.parametrize("N", [256, 512, 1024, 2048, 4096])
 @pytest.mark.parametrize("dtype", [torch.bfloat16, torch.float16])
 @pytest.mark.parametrize("B,H", [(3, 2), (8, 3)])
 def test_circular_mode_tensor_cores(lc, dtype, B, H, N):
