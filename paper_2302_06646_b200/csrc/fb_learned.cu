@@ -708,13 +708,30 @@ __global__ void __launch_bounds__(kLxThreads)
   for (int i = threadIdx.x; i < P; i += kLxThreads) dg[i] = G[i];
 }
 
+// dblocks[i] = sum over the splits in order; two complex entries per thread
+// (16-byte accesses when HP is even), the splits' loads in flight together
 __global__ void lb_reduce_kernel(const float2* __restrict__ gpart, float2* __restrict__ dblocks,
                                  int splits, size_t HP) {
-  const size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const size_t i = 2 * ((size_t)blockIdx.x * blockDim.x + threadIdx.x);
   if (i >= HP) return;
-  float2 acc = make_float2(0.f, 0.f);
-  for (int sp = 0; sp < splits; ++sp) acc = cadd(acc, gpart[(size_t)sp * HP + i]);
-  dblocks[i] = acc;
+  if ((HP & 1) == 0) {
+    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll 4
+    for (int sp = 0; sp < splits; ++sp) {
+      const float4 v = __ldg(reinterpret_cast<const float4*>(gpart + (size_t)sp * HP + i));
+      acc.x += v.x;
+      acc.y += v.y;
+      acc.z += v.z;
+      acc.w += v.w;
+    }
+    *reinterpret_cast<float4*>(dblocks + i) = acc;
+    return;
+  }
+  for (size_t e = i; e < i + 2 && e < HP; ++e) {
+    float2 acc = make_float2(0.f, 0.f);
+    for (int sp = 0; sp < splits; ++sp) acc = cadd(acc, __ldg(gpart + (size_t)sp * HP + e));
+    dblocks[e] = acc;
+  }
 }
 
 struct LbDevice {
@@ -1053,7 +1070,7 @@ int fb_learned_bwd(fb_learned_plan* p, const float* blocks, const void* x, const
                      "fb_learned_bwd (tcgen05)");
     if (rc) return rc;
     const size_t HP = (size_t)p->H * p->param_count;
-    lb_reduce_kernel<<<(unsigned)((HP + 255) / 256), 256, 0, s>>>((const float2*)ws,
+    lb_reduce_kernel<<<(unsigned)((HP + 511) / 512), 256, 0, s>>>((const float2*)ws,
                                                                  (float2*)dblocks, splits, HP);
     return cuda_status(cudaGetLastError(), "fb_learned_bwd");
   }
@@ -1074,7 +1091,7 @@ int fb_learned_bwd(fb_learned_plan* p, const float* blocks, const void* x, const
     else if (p->dtype == FB_BF16) go(__nv_bfloat16{});
     else go(__half{});
     const size_t HP = (size_t)p->H * p->param_count;
-    lb_reduce_kernel<<<(unsigned)((HP + 255) / 256), 256, 0, s>>>((const float2*)ws,
+    lb_reduce_kernel<<<(unsigned)((HP + 511) / 512), 256, 0, s>>>((const float2*)ws,
                                                                  (float2*)dblocks, splits, HP);
     return cuda_status(cudaGetLastError(), "fb_learned_bwd");
   }
@@ -1096,7 +1113,7 @@ int fb_learned_bwd(fb_learned_plan* p, const float* blocks, const void* x, const
   else if (p->dtype == FB_BF16) go(__nv_bfloat16{});
   else go(__half{});
   const size_t HP = (size_t)p->H * p->param_count;
-  lb_reduce_kernel<<<(unsigned)((HP + 255) / 256), 256, 0, s>>>((const float2*)ws, (float2*)dblocks,
+  lb_reduce_kernel<<<(unsigned)((HP + 511) / 512), 256, 0, s>>>((const float2*)ws, (float2*)dblocks,
                                                                splits, HP);
   return cuda_status(cudaGetLastError(), "fb_learned_bwd");
 }
