@@ -1951,7 +1951,216 @@ int make_rows_map(CUtensorMap* map, const void* ptr, int64_t R) {
   }
   return FB_OK;
 }
+
+// ---------------------------------------------------------------- three-pass pass 1, m = 32 .. 128
+// The m-point column DFTs of pass 1 (three_pass.cpp:82-122 as applied by
+// conv_three_pass_ordered :225-254) for the causal 16-bit three-pass plans
+// with m = 32 / 64 / 128 (N = 128K / 256K / 512K) as one GEMM per tile of 128
+// columns tau of a channel pair (b0, b0 + 1) of head h:
+//   D[tau][c' m + a] = sum_{c, e < m/2} X[tau][c rows + e] T[c' m + a][c rows + e]
+// X = the two channels' data rows (e < m/2; the causal zero half is skipped),
+// straight from TMA as an MN-major SW128 A operand (M = 128 tau, K = m);
+// T = the real-stacked DFT_m (re / im of sum_e w_m^(-a e) (x0 + i x1)[e]),
+// a K-major B operand built once per CTA (N = 2m).  The epilogue applies
+// the column twiddle w_n^(-a tau) and stores the planar rows [re l | im l]
+// the tcgen05 row pass reads.  Warp-specialised: warp 8 issues the TMA ring,
+// warp 9 the MMAs (two TMEM accumulators), warps 0-7 drain TMEM
+// (lane quarter = tau, warp half = rows a).
+namespace colc {
+constexpr int kStages = 3;
+constexpr uint32_t kEpi = 256, kThreads = kEpi + 64;
+constexpr uint32_t kRowL = 8192;  // l: the row length of the three-pass split
+// CTAs per SM: TMEM holds 2 x 2m accumulator columns per CTA; at most 3 (registers)
+constexpr int per_sm(int M) { return 512 / (4 * M) < 3 ? 512 / (4 * M) : 3; }
+}  // namespace colc
+
+__device__ __forceinline__ void tma_load_3d_sw(void* dst, const CUtensorMap* map, int c0, int c1, int c2,
+                                               uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, "
+      "%3, %4}], [%5];" ::"r"(ptx::smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(ptx::smem_u32(bar))
+      : "memory");
+}
+
+// w_n^(-t) from the two-level table [w^t, t < 4096 | w^(4096 i)]
+__device__ __forceinline__ float2 tw_two(const float2* __restrict__ tb, uint32_t t) {
+  const float2 lo = __ldg(tb + (t & 4095u)), hi = __ldg(tb + 4096u + (t >> 12));
+  return make_float2(lo.x * hi.x - lo.y * hi.y, lo.x * hi.y + lo.y * hi.x);
+}
+
+template <typename T, int M>
+__global__ void __launch_bounds__(colc::kThreads, colc::per_sm(M))
+    tc_col1_kernel(const __grid_constant__ CUtensorMap smap, __nv_bfloat16* __restrict__ x1,
+                   const float2* __restrict__ tb, int H, int ntiles) {
+  constexpr uint32_t ROWS = M / 2, K = 2 * ROWS, NN = 2 * M;
+  constexpr uint32_t ABYTES = 4 * ROWS * 128;       // 2 tau blocks x 2 channels x ROWS x 128 B
+  constexpr uint32_t KBLK = NN * 128;               // one 64-wide K block of the table
+  constexpr uint32_t TCOLS = 2 * NN;                // two accumulators
+  constexpr uint32_t NTB = colc::kRowL / 128;       // tau tiles per row
+  extern __shared__ __align__(1024) unsigned char raw[];
+  unsigned char* sm = smem_base(raw);
+  unsigned char* tabl = sm + colc::kStages * ABYTES;
+  __shared__ __align__(8) uint64_t full[colc::kStages], sfree[colc::kStages], tfull[2], tempty[2];
+  __shared__ uint32_t tmem_base;
+  const uint32_t tid = threadIdx.x, warp = tid >> 5;
+
+  // the real-stacked DFT_m table, (n' = c' M + a, k = c ROWS + e)
+  for (uint32_t i = tid; i < NN * K; i += colc::kThreads) {
+    const uint32_t np = i / K, k = i % K;
+    const uint32_t cp = np / M, a = np % M, c = k / ROWS, e = k % ROWS;
+    float sn, cs;
+    sincospif(2.f * (float)((a * e) % M) / (float)M, &sn, &cs);
+    const float v = cp == 0 ? (c == 0 ? cs : sn) : (c == 0 ? -sn : cs);
+    *reinterpret_cast<T*>(tabl + off_kmaj(np, k, KBLK)) = cvt<T>(v);
+  }
+  if (tid == 0) {
+    for (int s = 0; s < colc::kStages; ++s) {
+      ptx::mbar_init(&full[s], 1);
+      ptx::mbar_init(&sfree[s], 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      ptx::mbar_init(&tfull[b], 1);
+      ptx::mbar_init(&tempty[b], colc::kEpi);
+    }
+    ptx::fence_barrier_init();
+  }
+  if (warp == 0) tc::alloc<TCOLS>(&tmem_base);
+  ptx::fence_proxy_async_smem();
+  tc::fence_before();
+  __syncthreads();
+  tc::fence_after();
+  const uint32_t tmem = tmem_base;
+  const int first = blockIdx.x, step = gridDim.x;
+
+  if (warp == 8) {  // TMA producer
+    if ((tid & 31) == 0) {
+      int i = 0;
+      for (int t = first; t < ntiles; t += step, ++i) {
+        const int s = i % colc::kStages;
+        if (i >= colc::kStages) ptx::mbar_wait(&sfree[s], (uint32_t)(i / colc::kStages + 1) & 1);
+        const int tbk = t % NTB, h = (t / NTB) % H, pr = t / (NTB * H);
+        unsigned char* dst = sm + s * ABYTES;
+        ptx::mbar_arrive_expect_tx(&full[s], ABYTES);
+#pragma unroll
+        for (int mb = 0; mb < 2; ++mb)
+#pragma unroll
+          for (int c = 0; c < 2; ++c)
+            tma_load_3d_sw(dst + mb * (2 * ROWS * 128) + c * (ROWS * 128), &smap, tbk * 128 + mb * 64, 0,
+                           (2 * pr + c) * H + h, &full[s]);
+      }
+    }
+  } else if (warp == 9) {  // MMA issuer
+    if ((tid & 31) == 0) {
+      const uint32_t id = idesc<T>(128, NN, true, false);
+      const uint32_t sa = ptx::smem_u32(sm), st = ptx::smem_u32(tabl);
+      int i = 0;
+      for (int t = first; t < ntiles; t += step, ++i) {
+        const int s = i % colc::kStages, b = i & 1;
+        ptx::mbar_wait(&full[s], (uint32_t)(i / colc::kStages) & 1);
+        if (i >= 2) ptx::mbar_wait(&tempty[b], (uint32_t)(i / 2 + 1) & 1);
+        tc::fence_after();
+#pragma unroll
+        for (uint32_t ks = 0; ks < K / 16; ++ks) {
+          const uint64_t ad = tc::smem_desc(sa + s * ABYTES + ks * 2048, 1024, tc::kSw128, 2 * ROWS * 128);
+          const uint64_t bd = tc::smem_desc(st + (ks * 16 / 64) * KBLK + (ks * 16 % 64) * 2, 1024, tc::kSw128);
+          tc::mma_bf16(tmem + b * NN, ad, bd, id, ks);
+        }
+        tc::commit(&sfree[s]);
+        tc::commit(&tfull[b]);
+      }
+    }
+  } else {  // epilogue: tau = 32 (warp % 4) + lane, rows a in [half M/2, (half + 1) M/2)
+    const uint32_t q = warp & 3, half = warp >> 2, lane = tid & 31;
+    int i = 0;
+    for (int t = first; t < ntiles; t += step, ++i) {
+      const int b = i & 1;
+      const int tbk = t % NTB, h = (t / NTB) % H, pr = t / (NTB * H);
+      const uint32_t tau = tbk * 128 + 32 * q + lane;
+      ptx::mbar_wait(&tfull[b], (uint32_t)(i / 2) & 1);
+      tc::fence_after();
+      __nv_bfloat16* rows = x1 + (((size_t)pr * H + h) * M) * (2 * colc::kRowL) + tau;
+      const uint32_t ta = tmem + ((32u * q) << 16) + b * NN;
+      const float2 stp = tw_two(tb, tau);
+#pragma unroll 1
+      for (uint32_t a0 = half * (M / 2); a0 < (half + 1) * (M / 2); a0 += 16) {
+        float re[16], im[16];
+        tld<16>(ta + a0, re);
+        tld<16>(ta + M + a0, im);
+        tc::ld_wait();
+        float2 w = tw_two(tb, a0 * tau);
+#pragma unroll
+        for (int j = 0; j < 16; ++j) {
+          const float xr = re[j] * w.x - im[j] * w.y, xi = re[j] * w.y + im[j] * w.x;
+          __nv_bfloat16* r = rows + (size_t)(a0 + j) * (2 * colc::kRowL);
+          r[0] = __float2bfloat16_rn(xr);
+          r[colc::kRowL] = __float2bfloat16_rn(xi);
+          w = make_float2(w.x * stp.x - w.y * stp.y, w.x * stp.y + w.y * stp.x);
+        }
+      }
+      tc::fence_before();
+      mbar_arrive(&tempty[b]);
+    }
+  }
+  tc::fence_before();
+  __syncthreads();
+  tc::fence_after();
+  if (warp == 0) tc::dealloc<TCOLS>(tmem);
+}
+
+template <typename T, int M>
+int col1_launch(const fb_plan* p, const void* sig, void* x1, int64_t B, int64_t npairs, cudaStream_t s) {
+  EncodeFn enc = encode_fn();
+  if (!enc) {
+    set_error("tcgen05 pass 1: cuTensorMapEncodeTiled unavailable");
+    return FB_ERR_CUDA;
+  }
+  constexpr uint32_t ROWS = M / 2;
+  const cuuint64_t dims[3] = {colc::kRowL, ROWS, (cuuint64_t)(B * p->H)};
+  const cuuint64_t strides[2] = {colc::kRowL * 2, (cuuint64_t)p->N * 2};
+  const cuuint32_t box[3] = {64, ROWS, 1};
+  const cuuint32_t es[3] = {1, 1, 1};
+  CUtensorMap map;
+  CUresult r = enc(&map, Fmt<T>::tma, 3, const_cast<void*>(sig), dims, strides, box, es,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) {
+    set_error("cuTensorMapEncodeTiled (pass 1) failed (" + std::to_string((int)r) + ")");
+    return FB_ERR_CUDA;
+  }
+  constexpr uint32_t smem = colc::kStages * 4 * ROWS * 128 + (2 * M) * 128 * ((M + 63) / 64) + 1024;
+  constexpr int per_sm = colc::per_sm(M);
+  const int ntiles = (int)(npairs * p->H * (colc::kRowL / 128));
+  auto k = tc_col1_kernel<T, M>;
+  cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  const int grid = std::max(1, std::min(ntiles, per_sm * p->num_sms));
+  k<<<(unsigned)grid, colc::kThreads, smem, s>>>(map, (__nv_bfloat16*)x1, p->tw_big, (int)p->H, ntiles);
+  return cuda_status(cudaGetLastError(), "tc_col1_kernel");
+}
 }  // namespace
+
+// pass 1 of the causal 16-bit three-pass plans with m = 32 / 64 / 128 on the
+// tensor cores (planar bf16 rows for the tcgen05 row pass); FB_ERR_UNSUPPORTED
+// when the plan is outside that range (the caller runs the CUDA-core kernel)
+int tc_col1(const fb_plan* p, const void* sig, void* x1, int64_t B, int64_t npairs, cudaStream_t s) {
+  static const int off = [] {
+    const char* e = std::getenv("FB_COL1_TC");
+    return e && e[0] == '0';
+  }();
+  if (off || p->mode != FB_MODE_CAUSAL || p->l != colc::kRowL || p->N % colc::kRowL ||
+      p->m != 2 * (p->N / colc::kRowL) || (p->dtype != FB_BF16 && p->dtype != FB_F16))
+    return FB_ERR_UNSUPPORTED;
+  const bool bf = p->dtype == FB_BF16;
+  switch (p->m) {
+    case 32: return bf ? col1_launch<__nv_bfloat16, 32>(p, sig, x1, B, npairs, s)
+                       : col1_launch<__half, 32>(p, sig, x1, B, npairs, s);
+    case 64: return bf ? col1_launch<__nv_bfloat16, 64>(p, sig, x1, B, npairs, s)
+                       : col1_launch<__half, 64>(p, sig, x1, B, npairs, s);
+    case 128: return bf ? col1_launch<__nv_bfloat16, 128>(p, sig, x1, B, npairs, s)
+                        : col1_launch<__half, 128>(p, sig, x1, B, npairs, s);
+    default: return FB_ERR_UNSUPPORTED;
+  }
+}
 
 bool tc_rows_eligible(const fb_plan* p) {
   static const int off = [] {

@@ -1200,6 +1200,11 @@ uint32_t launch_pass1(const fb_plan* p, const IO* a, const IO* b, CxT<ST>* oa, C
       });
       return kL / kTB;
     }
+    if (planar && p->m > 16) {  // m = 32 .. 128: the column DFTs as tcgen05 GEMMs
+      const int rc = tc_col1(p, a, oa, B, npairs, s);
+      if (rc == FB_OK) return kL / 128;
+      if (rc != FB_ERR_UNSUPPORTED) return 0;
+    }
   }
   if constexpr (SRC != 2) {
     if (p->m <= 16) {

@@ -379,10 +379,14 @@ def test_three_pass_16bit(lc, dtype):
                                               (2, 1, 262144, 1, torch.bfloat16),
                                               (3, 2, 16384, 1, torch.float16),
                                               (2, 2, 65536, 0, torch.float16),
-                                              (3, 1, 131072, 1, torch.float16)])
+                                              (3, 1, 131072, 1, torch.float16),
+                                              (4, 2, 131072, 1, torch.bfloat16),
+                                              (1, 2, 262144, 1, torch.float16),
+                                              (2, 1, 524288, 1, torch.bfloat16)])
 def test_three_pass_bf16_tc_rows(lc, B, H, N, mode, dtype):
-    """16-bit three-pass with pass 2 on tcgen05 (m = 2 .. 64: register and
-    big-column pass 1 writing planar rows; causal and circular; odd B = a
+    """16-bit three-pass with pass 2 on tcgen05 (m = 2 .. 128: register
+    column pass 1 for m <= 16, the tcgen05 column GEMM for causal m = 32 ..
+    128, writing planar rows; causal and circular; odd B = a
     zero partner channel; fp16 I/O with bf16 rows): recompute and saved-U
     backward agree bit for bit, both within the 16-bit bar of the oracle."""
     inp = layer_inputs(lc, B, H, N, dtype)
