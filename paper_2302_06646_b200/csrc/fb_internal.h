@@ -116,6 +116,9 @@ bool tc_rows_eligible(const fb_plan* p);
 int tc_rows_fwd(fb_plan* p, void* x1, void* usave, int64_t npairs, cudaStream_t s);
 // three-pass pass 1 on tcgen05 (causal, 16-bit, m = 32 / 64 / 128): planar bf16 rows
 int tc_col1(const fb_plan* p, const void* sig, void* x1, int64_t B, int64_t npairs, cudaStream_t s);
+// pass 3 (y / du) of the same plans for m = 32 / 64 (W = interleaved complex bf16 rows)
+int tc_col3(const fb_plan* p, const void* w, const void* skip, void* out, int64_t B, int64_t npairs,
+            cudaStream_t s);
 // backward rows (saved U): planar dy rows in, du rows out in place, wdk = IFFT_l(dK spectrum)
 int tc_rows_spectrum(fb_plan* p, void* x1, int64_t npairs, cudaStream_t s);  // U in place
 int tc_rows_bwd(fb_plan* p, void* x1dy, const void* usave, float2* wdk, int64_t npairs,

@@ -2137,7 +2137,228 @@ int col1_launch(const fb_plan* p, const void* sig, void* x1, int64_t B, int64_t 
   k<<<(unsigned)grid, colc::kThreads, smem, s>>>(map, (__nv_bfloat16*)x1, p->tw_big, (int)p->H, ntiles);
   return cuda_status(cudaGetLastError(), "tc_col1_kernel");
 }
+
+// ---------------------------------------------------------------- three-pass pass 3, m = 32 / 64
+// Pass 3 of the causal 16-bit three-pass forward / du (three_pass.cpp:225-254,
+// the B^-1 factor :101-122):  y[c l + tau] = sum_a w_m^(+a c) w_n^(+a tau) W[a][tau]
+// for the data rows c < m/2, channel b0 = Re, b1 = Im, plus D u.  The
+// twiddle sits on the contraction index, so the A operand is built by the
+// eight worker warps (TMA'd W tile [a][128 tau] -> x w_n^(+a tau) -> bf16
+// MN-major SW128, K = [re a | im a]); the inverse DFT_m is a K-major B
+// operand (N = m: [Re c | Im c]); the same warps then drain the previous
+// tile's accumulator (skip added, 16-bit stores).  Warp 8: TMA, warp 9: MMA.
+namespace colc3 {
+constexpr int kStages = 2;
+constexpr int per_sm(int M) { return M == 32 ? 3 : 1; }
+}  // namespace colc3
+
+template <typename IO, int M>
+__global__ void __launch_bounds__(colc::kThreads, colc3::per_sm(M))
+    tc_col3_kernel(const __grid_constant__ CUtensorMap wmap, const IO* __restrict__ skip,
+                   IO* __restrict__ out, const float* __restrict__ D, const float2* __restrict__ tb,
+                   int B, int H, int ntiles) {
+  constexpr uint32_t ROWS = M / 2, K = 2 * M, NN = M;
+  constexpr uint32_t WBYTES = M * 128 * 4;        // W tile [a][128 tau] complex bf16
+  constexpr uint32_t ABYTES = 128 * K * 2;        // A [tau / 64][k][64 tau]
+  constexpr uint32_t KBLK = NN * 128;
+  constexpr uint32_t TCOLS = 2 * NN < 32 ? 32 : 2 * NN;
+  constexpr uint32_t NTB = colc::kRowL / 128;
+  extern __shared__ __align__(1024) unsigned char raw[];
+  unsigned char* sm = smem_base(raw);
+  unsigned char* abuf = sm;                                   // 2 x ABYTES
+  unsigned char* tabl = sm + 2 * ABYTES;                      // K / 64 x KBLK
+  unsigned char* wring = tabl + (K / 64) * KBLK;              // kStages x WBYTES
+  __shared__ __align__(8) uint64_t wfull[colc3::kStages], wempty[colc3::kStages], afull[2], afree[2],
+      tfull[2], tempty[2];
+  __shared__ uint32_t tmem_base;
+  const uint32_t tid = threadIdx.x, warp = tid >> 5;
+
+  // inverse DFT_m, (n' = c' ROWS + c, k = [re a | im a])
+  for (uint32_t i = tid; i < NN * K; i += colc::kThreads) {
+    const uint32_t np = i / K, k = i % K;
+    const uint32_t cp = np / ROWS, c = np % ROWS, a = k % M, im = k / M;
+    float sn, cs;
+    sincospif(2.f * (float)((a * c) % M) / (float)M, &sn, &cs);
+    const float v = cp == 0 ? (im ? -sn : cs) : (im ? cs : sn);
+    *reinterpret_cast<__nv_bfloat16*>(tabl + off_kmaj(np, k, KBLK)) = __float2bfloat16_rn(v);
+  }
+  if (tid == 0) {
+    for (int s = 0; s < colc3::kStages; ++s) {
+      ptx::mbar_init(&wfull[s], 1);
+      ptx::mbar_init(&wempty[s], colc::kEpi);
+    }
+    for (int b = 0; b < 2; ++b) {
+      ptx::mbar_init(&afull[b], colc::kEpi);
+      ptx::mbar_init(&afree[b], 1);
+      ptx::mbar_init(&tfull[b], 1);
+      ptx::mbar_init(&tempty[b], colc::kEpi);
+    }
+    ptx::fence_barrier_init();
+  }
+  if (warp == 0) tc::alloc<TCOLS>(&tmem_base);
+  ptx::fence_proxy_async_smem();
+  tc::fence_before();
+  __syncthreads();
+  tc::fence_after();
+  const uint32_t tmem = tmem_base;
+  const int first = blockIdx.x, step = gridDim.x;
+
+  if (warp == 8) {  // TMA producer: W tiles
+    if ((tid & 31) == 0) {
+      int i = 0;
+      for (int t = first; t < ntiles; t += step, ++i) {
+        const int s = i % colc3::kStages;
+        if (i >= colc3::kStages) ptx::mbar_wait(&wempty[s], (uint32_t)(i / colc3::kStages + 1) & 1);
+        const int tbk = t % NTB, hp = t / NTB;  // hp = pr * H + h
+        ptx::mbar_arrive_expect_tx(&wfull[s], WBYTES);
+        tma_load_3d_sw(wring + s * WBYTES, &wmap, tbk * 128, 0, hp, &wfull[s]);
+      }
+    }
+  } else if (warp == 9) {  // MMA issuer
+    if ((tid & 31) == 0) {
+      const uint32_t id = idesc<__nv_bfloat16>(128, NN, true, false);
+      const uint32_t sa = ptx::smem_u32(abuf), st = ptx::smem_u32(tabl);
+      int i = 0;
+      for (int t = first; t < ntiles; t += step, ++i) {
+        const int b = i & 1;
+        ptx::mbar_wait(&afull[b], (uint32_t)(i / 2) & 1);
+        if (i >= 2) ptx::mbar_wait(&tempty[b], (uint32_t)(i / 2 + 1) & 1);
+        tc::fence_after();
+#pragma unroll
+        for (uint32_t ks = 0; ks < K / 16; ++ks) {
+          const uint64_t ad = tc::smem_desc(sa + b * ABYTES + ks * 2048, 1024, tc::kSw128, K * 128);
+          const uint64_t bd = tc::smem_desc(st + (ks * 16 / 64) * KBLK + (ks * 16 % 64) * 2, 1024, tc::kSw128);
+          tc::mma_bf16(tmem + b * NN, ad, bd, id, ks);
+        }
+        tc::commit(&afree[b]);
+        tc::commit(&tfull[b]);
+      }
+    }
+  } else {  // workers
+    const uint32_t q = warp & 3, half = warp >> 2, lane = tid & 31;
+    int i = 0, tprev = -1;
+    for (int t = first;; t += step, ++i) {
+      const bool have = t < ntiles;
+      if (have) {  // A operand of tile i
+        const int s = i % colc3::kStages, b = i & 1;
+        const uint32_t tau0 = (uint32_t)(t % NTB) * 128;
+        ptx::mbar_wait(&wfull[s], (uint32_t)(i / colc3::kStages) & 1);
+        if (i >= 2) ptx::mbar_wait(&afree[b], (uint32_t)(i / 2 + 1) & 1);
+        const unsigned char* ws = wring + s * WBYTES;
+        unsigned char* ab = abuf + b * ABYTES;
+#pragma unroll 1
+        for (uint32_t j = tid; j < M * 16; j += colc::kEpi) {
+          const uint32_t a = j >> 4, tc8 = (j & 15) * 8;
+          const uint4 v0 = *reinterpret_cast<const uint4*>(ws + a * 512 + tc8 * 4);
+          const uint4 v1 = *reinterpret_cast<const uint4*>(ws + a * 512 + tc8 * 4 + 16);
+          const uint32_t vv[8] = {v0.x, v0.y, v0.z, v0.w, v1.x, v1.y, v1.z, v1.w};
+          float2 w = tw_two(tb, a * (tau0 + tc8));
+          const float2 sp = tw_two(tb, a);
+          w.y = -w.y;  // w_n^(+a tau)
+          float re[8], im[8];
+#pragma unroll
+          for (int e = 0; e < 8; ++e) {
+            const float2 z = unpack2<__nv_bfloat16>(vv[e]);
+            re[e] = z.x * w.x - z.y * w.y;
+            im[e] = z.x * w.y + z.y * w.x;
+            w = make_float2(w.x * sp.x + w.y * sp.y, w.y * sp.x - w.x * sp.y);  // x conj(sp)
+          }
+          const uint32_t base = (tc8 >> 6) * (K * 128) + (tc8 & 63) * 2;
+          st8<__nv_bfloat16>(ab + sw128(base + a * 128), re);
+          st8<__nv_bfloat16>(ab + sw128(base + (M + a) * 128), im);
+        }
+        ptx::fence_proxy_async_smem();
+        mbar_arrive(&wempty[s]);
+        mbar_arrive(&afull[b]);
+      }
+      if (tprev >= 0) {  // drain tile i - 1: warps 0-3 channel b0 (Re), 4-7 b1 (Im)
+        const int ip = i - 1, b = ip & 1;
+        const int tbk = tprev % NTB, h = (tprev / NTB) % H, pr = tprev / (NTB * H);
+        const uint32_t tau = tbk * 128 + 32 * q + lane;
+        ptx::mbar_wait(&tfull[b], (uint32_t)(ip / 2) & 1);
+        tc::fence_after();
+        const int bc = 2 * pr + (int)half;
+        const uint32_t ta = tmem + ((32u * q) << 16) + b * NN + half * ROWS;
+        const float d = __ldg(D + h);
+        const size_t o = ((size_t)bc * H + h) * (size_t)(ROWS * colc::kRowL) + tau;
+#pragma unroll 1
+        for (uint32_t c0 = 0; c0 < ROWS; c0 += 16) {
+          float v[16];
+          tld<16>(ta + c0, v);
+          tc::ld_wait();
+          if (bc < B) {
+#pragma unroll
+            for (int j = 0; j < 16; ++j) {
+              const size_t off = o + (size_t)(c0 + j) * colc::kRowL;
+              out[off] = cvt<IO>(fmaf(d, tof(skip[off]), v[j]));
+            }
+          }
+        }
+        tc::fence_before();
+        mbar_arrive(&tempty[b]);
+      }
+      if (!have) break;
+      tprev = t;
+    }
+  }
+  tc::fence_before();
+  __syncthreads();
+  tc::fence_after();
+  if (warp == 0) tc::dealloc<TCOLS>(tmem);
+}
+
+template <typename IO, int M>
+int col3_launch(const fb_plan* p, const void* w, const void* skip, void* out, int64_t B, int64_t npairs,
+                cudaStream_t s) {
+  EncodeFn enc = encode_fn();
+  if (!enc) {
+    set_error("tcgen05 pass 3: cuTensorMapEncodeTiled unavailable");
+    return FB_ERR_CUDA;
+  }
+  // W = x1 [npairs H][m][l] complex bf16 as 32-bit elements; box [128 tau][m a][1]
+  const cuuint64_t dims[3] = {colc::kRowL, (cuuint64_t)M, (cuuint64_t)(npairs * p->H)};
+  const cuuint64_t strides[2] = {colc::kRowL * 4, (cuuint64_t)M * colc::kRowL * 4};
+  const cuuint32_t box[3] = {128, (cuuint32_t)M, 1};
+  const cuuint32_t es[3] = {1, 1, 1};
+  CUtensorMap map;
+  CUresult r = enc(&map, CU_TENSOR_MAP_DATA_TYPE_UINT32, 3, const_cast<void*>(w), dims, strides, box, es,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) {
+    set_error("cuTensorMapEncodeTiled (pass 3) failed (" + std::to_string((int)r) + ")");
+    return FB_ERR_CUDA;
+  }
+  constexpr uint32_t smem = 2 * (128 * 2 * M * 2) + (2 * M / 64) * (M * 128) + colc3::kStages * M * 512 + 1024;
+  const int ntiles = (int)(npairs * p->H * (colc::kRowL / 128));
+  auto k = tc_col3_kernel<IO, M>;
+  cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  const int grid = std::max(1, std::min(ntiles, colc3::per_sm(M) * p->num_sms));
+  k<<<(unsigned)grid, colc::kThreads, smem, s>>>(map, (const IO*)skip, (IO*)out, p->d, p->tw_big, (int)B,
+                                                 (int)p->H, ntiles);
+  return cuda_status(cudaGetLastError(), "tc_col3_kernel");
+}
 }  // namespace
+
+// pass 3 (forward y / backward du) of the same plans for m = 32 / 64 on the
+// tensor cores; FB_ERR_UNSUPPORTED outside that range
+int tc_col3(const fb_plan* p, const void* w, const void* skip, void* out, int64_t B, int64_t npairs,
+            cudaStream_t s) {
+  static const int off = [] {
+    const char* e = std::getenv("FB_COL3_TC");
+    return e && e[0] == '0';
+  }();
+  if (off || p->mode != FB_MODE_CAUSAL || p->l != colc::kRowL || p->N % colc::kRowL ||
+      p->m != 2 * (p->N / colc::kRowL) || (p->dtype != FB_BF16 && p->dtype != FB_F16))
+    return FB_ERR_UNSUPPORTED;
+  const bool bf = p->dtype == FB_BF16;
+  switch (p->m) {
+    case 32: return bf ? col3_launch<__nv_bfloat16, 32>(p, w, skip, out, B, npairs, s)
+                       : col3_launch<__half, 32>(p, w, skip, out, B, npairs, s);
+    case 64: return bf ? col3_launch<__nv_bfloat16, 64>(p, w, skip, out, B, npairs, s)
+                       : col3_launch<__half, 64>(p, w, skip, out, B, npairs, s);
+    default: return FB_ERR_UNSUPPORTED;
+  }
+}
 
 // pass 1 of the causal 16-bit three-pass plans with m = 32 / 64 / 128 on the
 // tensor cores (planar bf16 rows for the tcgen05 row pass); FB_ERR_UNSUPPORTED

@@ -1307,6 +1307,12 @@ void launch_pass3(const fb_plan* p, const CxT<ST>* w, const IO* skip, IO* out, f
       });
       if (maps) return;  // else: the register column kernel below
     }
+    if constexpr (std::is_same_v<ST, __nv_bfloat16>) {
+      if (p->m > 16) {  // m = 32 / 64: the inverse column DFTs as tcgen05 GEMMs
+        const int rc = tc_col3(p, w, skip, out, B, npairs, s);
+        if (rc != FB_ERR_UNSUPPORTED) return;
+      }
+    }
   }
   if (p->m <= 16) {
     with_m(p->m, [&](auto mc) {
