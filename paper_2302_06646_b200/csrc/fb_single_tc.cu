@@ -2138,7 +2138,7 @@ int col1_launch(const fb_plan* p, const void* sig, void* x1, int64_t B, int64_t 
   return cuda_status(cudaGetLastError(), "tc_col1_kernel");
 }
 
-// ---------------------------------------------------------------- three-pass pass 3, m = 32 / 64
+// ---------------------------------------------------------------- three-pass pass 3, m = 32 .. 128
 // Pass 3 of the causal 16-bit three-pass forward / du (three_pass.cpp:225-254,
 // the B^-1 factor :101-122):  y[c l + tau] = sum_a w_m^(+a c) w_n^(+a tau) W[a][tau]
 // for the data rows c < m/2, channel b0 = Re, b1 = Im, plus D u.  The
@@ -2150,6 +2150,9 @@ int col1_launch(const fb_plan* p, const void* sig, void* x1, int64_t B, int64_t 
 namespace colc3 {
 constexpr int kStages = 2;
 constexpr int per_sm(int M) { return M == 32 ? 3 : 1; }
+// rows a per sub-tile: m = 128 runs each tile as two a-halves (W and A
+// buffers of 32 KB), accumulating into one TMEM tile
+constexpr int half_a(int M) { return M > 64 ? 64 : M; }
 }  // namespace colc3
 
 template <typename IO, int M>
@@ -2158,8 +2161,9 @@ __global__ void __launch_bounds__(colc::kThreads, colc3::per_sm(M))
                    IO* __restrict__ out, const float* __restrict__ D, const float2* __restrict__ tb,
                    int B, int H, int ntiles) {
   constexpr uint32_t ROWS = M / 2, K = 2 * M, NN = M;
-  constexpr uint32_t WBYTES = M * 128 * 4;        // W tile [a][128 tau] complex bf16
-  constexpr uint32_t ABYTES = 128 * K * 2;        // A [tau / 64][k][64 tau]
+  constexpr uint32_t MH = colc3::half_a(M), SPLIT = M / MH, KC = 2 * MH;  // sub-tile: a-rows, K
+  constexpr uint32_t WBYTES = MH * 128 * 4;       // W sub-tile [a][128 tau] complex bf16
+  constexpr uint32_t ABYTES = 128 * KC * 2;       // A [tau / 64][k][64 tau], k = [re a | im a]
   constexpr uint32_t KBLK = NN * 128;
   constexpr uint32_t TCOLS = 2 * NN < 32 ? 32 : 2 * NN;
   constexpr uint32_t NTB = colc::kRowL / 128;
@@ -2205,52 +2209,57 @@ __global__ void __launch_bounds__(colc::kThreads, colc3::per_sm(M))
 
   if (warp == 8) {  // TMA producer: W tiles
     if ((tid & 31) == 0) {
-      int i = 0;
-      for (int t = first; t < ntiles; t += step, ++i) {
-        const int s = i % colc3::kStages;
-        if (i >= colc3::kStages) ptx::mbar_wait(&wempty[s], (uint32_t)(i / colc3::kStages + 1) & 1);
-        const int tbk = t % NTB, hp = t / NTB;  // hp = pr * H + h
-        ptx::mbar_arrive_expect_tx(&wfull[s], WBYTES);
-        tma_load_3d_sw(wring + s * WBYTES, &wmap, tbk * 128, 0, hp, &wfull[s]);
-      }
+      int g = 0;
+      for (int t = first; t < ntiles; t += step)
+        for (uint32_t part = 0; part < SPLIT; ++part, ++g) {
+          const int s = g % colc3::kStages;
+          if (g >= colc3::kStages) ptx::mbar_wait(&wempty[s], (uint32_t)(g / colc3::kStages + 1) & 1);
+          const int tbk = t % NTB, hp = t / NTB;  // hp = pr * H + h
+          ptx::mbar_arrive_expect_tx(&wfull[s], WBYTES);
+          tma_load_3d_sw(wring + s * WBYTES, &wmap, tbk * 128, (int)(part * MH), hp, &wfull[s]);
+        }
     }
   } else if (warp == 9) {  // MMA issuer
     if ((tid & 31) == 0) {
       const uint32_t id = idesc<__nv_bfloat16>(128, NN, true, false);
       const uint32_t sa = ptx::smem_u32(abuf), st = ptx::smem_u32(tabl);
-      int i = 0;
+      int i = 0, g = 0;
       for (int t = first; t < ntiles; t += step, ++i) {
-        const int b = i & 1;
-        ptx::mbar_wait(&afull[b], (uint32_t)(i / 2) & 1);
-        if (i >= 2) ptx::mbar_wait(&tempty[b], (uint32_t)(i / 2 + 1) & 1);
-        tc::fence_after();
+        const int tb2 = i & 1;
+        for (uint32_t part = 0; part < SPLIT; ++part, ++g) {
+          const int b = g & 1;
+          ptx::mbar_wait(&afull[b], (uint32_t)(g / 2) & 1);
+          if (part == 0 && i >= 2) ptx::mbar_wait(&tempty[tb2], (uint32_t)(i / 2 + 1) & 1);
+          tc::fence_after();
 #pragma unroll
-        for (uint32_t ks = 0; ks < K / 16; ++ks) {
-          const uint64_t ad = tc::smem_desc(sa + b * ABYTES + ks * 2048, 1024, tc::kSw128, K * 128);
-          const uint64_t bd = tc::smem_desc(st + (ks * 16 / 64) * KBLK + (ks * 16 % 64) * 2, 1024, tc::kSw128);
-          tc::mma_bf16(tmem + b * NN, ad, bd, id, ks);
+          for (uint32_t ks = 0; ks < KC / 16; ++ks) {
+            const uint32_t kk = ks * 16, k = kk < MH ? part * MH + kk : M + part * MH + (kk - MH);
+            const uint64_t ad = tc::smem_desc(sa + b * ABYTES + ks * 2048, 1024, tc::kSw128, KC * 128);
+            const uint64_t bd = tc::smem_desc(st + (k / 64) * KBLK + (k % 64) * 2, 1024, tc::kSw128);
+            tc::mma_bf16(tmem + tb2 * NN, ad, bd, id, (part | ks) ? 1u : 0u);
+          }
+          tc::commit(&afree[b]);
         }
-        tc::commit(&afree[b]);
-        tc::commit(&tfull[b]);
+        tc::commit(&tfull[tb2]);
       }
     }
   } else {  // workers
     const uint32_t q = warp & 3, half = warp >> 2, lane = tid & 31;
-    int i = 0, tprev = -1;
+    int i = 0, g = 0, tprev = -1;
     for (int t = first;; t += step, ++i) {
       const bool have = t < ntiles;
-      if (have) {  // A operand of tile i
-        const int s = i % colc3::kStages, b = i & 1;
+      for (uint32_t part = 0; have && part < SPLIT; ++part, ++g) {  // A operand of tile i
+        const int s = g % colc3::kStages, b = g & 1;
         const uint32_t tau0 = (uint32_t)(t % NTB) * 128;
-        ptx::mbar_wait(&wfull[s], (uint32_t)(i / colc3::kStages) & 1);
-        if (i >= 2) ptx::mbar_wait(&afree[b], (uint32_t)(i / 2 + 1) & 1);
+        ptx::mbar_wait(&wfull[s], (uint32_t)(g / colc3::kStages) & 1);
+        if (g >= 2) ptx::mbar_wait(&afree[b], (uint32_t)(g / 2 + 1) & 1);
         const unsigned char* ws = wring + s * WBYTES;
         unsigned char* ab = abuf + b * ABYTES;
 #pragma unroll 1
-        for (uint32_t j = tid; j < M * 16; j += colc::kEpi) {
-          const uint32_t a = j >> 4, tc8 = (j & 15) * 8;
-          const uint4 v0 = *reinterpret_cast<const uint4*>(ws + a * 512 + tc8 * 4);
-          const uint4 v1 = *reinterpret_cast<const uint4*>(ws + a * 512 + tc8 * 4 + 16);
+        for (uint32_t j = tid; j < MH * 16; j += colc::kEpi) {
+          const uint32_t al = j >> 4, a = part * MH + al, tc8 = (j & 15) * 8;
+          const uint4 v0 = *reinterpret_cast<const uint4*>(ws + al * 512 + tc8 * 4);
+          const uint4 v1 = *reinterpret_cast<const uint4*>(ws + al * 512 + tc8 * 4 + 16);
           const uint32_t vv[8] = {v0.x, v0.y, v0.z, v0.w, v1.x, v1.y, v1.z, v1.w};
           float2 w = tw_two(tb, a * (tau0 + tc8));
           const float2 sp = tw_two(tb, a);
@@ -2263,9 +2272,9 @@ __global__ void __launch_bounds__(colc::kThreads, colc3::per_sm(M))
             im[e] = z.x * w.y + z.y * w.x;
             w = make_float2(w.x * sp.x + w.y * sp.y, w.y * sp.x - w.x * sp.y);  // x conj(sp)
           }
-          const uint32_t base = (tc8 >> 6) * (K * 128) + (tc8 & 63) * 2;
-          st8<__nv_bfloat16>(ab + sw128(base + a * 128), re);
-          st8<__nv_bfloat16>(ab + sw128(base + (M + a) * 128), im);
+          const uint32_t base = (tc8 >> 6) * (KC * 128) + (tc8 & 63) * 2;
+          st8<__nv_bfloat16>(ab + sw128(base + al * 128), re);
+          st8<__nv_bfloat16>(ab + sw128(base + (MH + al) * 128), im);
         }
         ptx::fence_proxy_async_smem();
         mbar_arrive(&wempty[s]);
@@ -2318,7 +2327,7 @@ int col3_launch(const fb_plan* p, const void* w, const void* skip, void* out, in
   // W = x1 [npairs H][m][l] complex bf16 as 32-bit elements; box [128 tau][m a][1]
   const cuuint64_t dims[3] = {colc::kRowL, (cuuint64_t)M, (cuuint64_t)(npairs * p->H)};
   const cuuint64_t strides[2] = {colc::kRowL * 4, (cuuint64_t)M * colc::kRowL * 4};
-  const cuuint32_t box[3] = {128, (cuuint32_t)M, 1};
+  const cuuint32_t box[3] = {128, (cuuint32_t)colc3::half_a(M), 1};
   const cuuint32_t es[3] = {1, 1, 1};
   CUtensorMap map;
   CUresult r = enc(&map, CU_TENSOR_MAP_DATA_TYPE_UINT32, 3, const_cast<void*>(w), dims, strides, box, es,
@@ -2328,7 +2337,8 @@ int col3_launch(const fb_plan* p, const void* w, const void* skip, void* out, in
     set_error("cuTensorMapEncodeTiled (pass 3) failed (" + std::to_string((int)r) + ")");
     return FB_ERR_CUDA;
   }
-  constexpr uint32_t smem = 2 * (128 * 2 * M * 2) + (2 * M / 64) * (M * 128) + colc3::kStages * M * 512 + 1024;
+  constexpr uint32_t MH = colc3::half_a(M);
+  constexpr uint32_t smem = 2 * (128 * 2 * MH * 2) + (2 * M / 64) * (M * 128) + colc3::kStages * MH * 512 + 1024;
   const int ntiles = (int)(npairs * p->H * (colc::kRowL / 128));
   auto k = tc_col3_kernel<IO, M>;
   cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -2339,7 +2349,7 @@ int col3_launch(const fb_plan* p, const void* w, const void* skip, void* out, in
 }
 }  // namespace
 
-// pass 3 (forward y / backward du) of the same plans for m = 32 / 64 on the
+// pass 3 (forward y / backward du) of the same plans for m = 32 / 64 / 128 on the
 // tensor cores; FB_ERR_UNSUPPORTED outside that range
 int tc_col3(const fb_plan* p, const void* w, const void* skip, void* out, int64_t B, int64_t npairs,
             cudaStream_t s) {
@@ -2356,6 +2366,8 @@ int tc_col3(const fb_plan* p, const void* w, const void* skip, void* out, int64_
                        : col3_launch<__half, 32>(p, w, skip, out, B, npairs, s);
     case 64: return bf ? col3_launch<__nv_bfloat16, 64>(p, w, skip, out, B, npairs, s)
                        : col3_launch<__half, 64>(p, w, skip, out, B, npairs, s);
+    case 128: return bf ? col3_launch<__nv_bfloat16, 128>(p, w, skip, out, B, npairs, s)
+                        : col3_launch<__half, 128>(p, w, skip, out, B, npairs, s);
     default: return FB_ERR_UNSUPPORTED;
   }
 }

@@ -382,7 +382,8 @@ def test_three_pass_16bit(lc, dtype):
                                               (3, 1, 131072, 1, torch.float16),
                                               (4, 2, 131072, 1, torch.bfloat16),
                                               (1, 2, 262144, 1, torch.float16),
-                                              (2, 1, 524288, 1, torch.bfloat16)])
+                                              (2, 1, 524288, 1, torch.bfloat16),
+                                              (3, 1, 524288, 1, torch.float16)])
 def test_three_pass_bf16_tc_rows(lc, B, H, N, mode, dtype):
     """16-bit three-pass with pass 2 on tcgen05 (m = 2 .. 128: register
     column pass 1 for m <= 16, the tcgen05 column GEMM for causal m = 32 ..
