@@ -2149,10 +2149,11 @@ int col1_launch(const fb_plan* p, const void* sig, void* x1, int64_t B, int64_t 
 // tile's accumulator (skip added, 16-bit stores).  Warp 8: TMA, warp 9: MMA.
 namespace colc3 {
 constexpr int kStages = 2;
-constexpr int per_sm(int M) { return M == 32 ? 3 : 1; }
-// rows a per sub-tile: m = 128 runs each tile as two a-halves (W and A
-// buffers of 32 KB), accumulating into one TMEM tile
-constexpr int half_a(int M) { return M > 64 ? 64 : M; }
+constexpr int per_sm(int M) { return M == 32 ? 3 : (M == 64 ? 2 : 1); }
+// rows a per sub-tile: m = 64 / 128 run each tile as two a-halves (W and A
+// buffers of 16 / 32 KB) accumulating into one TMEM tile, so the double
+// buffers fit (two CTAs per SM at m = 64)
+constexpr int half_a(int M) { return M == 32 ? 32 : M / 2; }
 }  // namespace colc3
 
 template <typename IO, int M>
