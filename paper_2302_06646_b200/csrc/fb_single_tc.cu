@@ -2285,23 +2285,34 @@ __global__ void __launch_bounds__(colc::kThreads, colc3::per_sm(M))
         const int ip = i - 1, b = ip & 1;
         const int tbk = tprev % NTB, h = (tprev / NTB) % H, pr = tprev / (NTB * H);
         const uint32_t tau = tbk * 128 + 32 * q + lane;
+        const int bc = 2 * pr + (int)half;
+        const bool live = bc < B;
+        const size_t o = ((size_t)bc * H + h) * (size_t)(ROWS * colc::kRowL) + tau;
+        // skip rows of the next chunk in flight while this one drains (the
+        // first chunk's before the accumulator wait)
+        IO sk[16];
+#pragma unroll
+        for (int j = 0; j < 16; ++j) sk[j] = live ? skip[o + (size_t)j * colc::kRowL] : IO{};
+        const float d = __ldg(D + h);
         ptx::mbar_wait(&tfull[b], (uint32_t)(ip / 2) & 1);
         tc::fence_after();
-        const int bc = 2 * pr + (int)half;
         const uint32_t ta = tmem + ((32u * q) << 16) + b * NN + half * ROWS;
-        const float d = __ldg(D + h);
-        const size_t o = ((size_t)bc * H + h) * (size_t)(ROWS * colc::kRowL) + tau;
 #pragma unroll 1
         for (uint32_t c0 = 0; c0 < ROWS; c0 += 16) {
           float v[16];
           tld<16>(ta + c0, v);
           tc::ld_wait();
-          if (bc < B) {
+          float y[16];
 #pragma unroll
-            for (int j = 0; j < 16; ++j) {
-              const size_t off = o + (size_t)(c0 + j) * colc::kRowL;
-              out[off] = cvt<IO>(fmaf(d, tof(skip[off]), v[j]));
-            }
+          for (int j = 0; j < 16; ++j) y[j] = fmaf(d, tof(sk[j]), v[j]);
+          if (c0 + 16 < ROWS) {
+#pragma unroll
+            for (int j = 0; j < 16; ++j)
+              sk[j] = live ? skip[o + (size_t)(c0 + 16 + j) * colc::kRowL] : IO{};
+          }
+          if (live) {
+#pragma unroll
+            for (int j = 0; j < 16; ++j) out[o + (size_t)(c0 + j) * colc::kRowL] = cvt<IO>(y[j]);
           }
         }
         tc::fence_before();
