@@ -173,12 +173,34 @@ __global__ void __launch_bounds__(kRegThreads)
   __shared__ double sk[kRegTile + 2 * kRegHalo];
   const size_t base = (size_t)blockIdx.y * N;
   const int t0 = blockIdx.x * kRegTile;
-  for (int i = threadIdx.x; i < kRegTile + 2 * p; i += kRegThreads) {
-    const int t = t0 - p + i;
-    sk[i] = (t >= 0 && t < N) ? dropped(K, keep, keep_scale, base + t) : 0.0;
+  if (!keep && (N & 3) == 0 && t0 + kRegTile <= N) {
+    // whole tile: both 16-byte loads per thread in flight at once, halo apart
+    const float4* src = reinterpret_cast<const float4*>(K + base + t0);
+    float4 v[kRegTile / (4 * kRegThreads)];
+#pragma unroll
+    for (int j = 0; j < kRegTile / (4 * kRegThreads); ++j) v[j] = __ldg(src + threadIdx.x + j * kRegThreads);
+#pragma unroll
+    for (int j = 0; j < kRegTile / (4 * kRegThreads); ++j) {
+      double* d = sk + p + 4 * (threadIdx.x + j * kRegThreads);
+      d[0] = v[j].x;
+      d[1] = v[j].y;
+      d[2] = v[j].z;
+      d[3] = v[j].w;
+    }
+    if ((int)threadIdx.x < 2 * p) {
+      const int i = threadIdx.x < (unsigned)p ? (int)threadIdx.x : kRegTile + (int)threadIdx.x;
+      const int t = t0 - p + i;
+      sk[i] = (t >= 0 && t < N) ? (double)__ldg(K + base + t) : 0.0;
+    }
+  } else {
+    for (int i = threadIdx.x; i < kRegTile + 2 * p; i += kRegThreads) {
+      const int t = t0 - p + i;
+      sk[i] = (t >= 0 && t < N) ? dropped(K, keep, keep_scale, base + t) : 0.0;
+    }
   }
   __syncthreads();
   const double inv_w = 1.0 / (double)(2 * p + 1);
+#pragma unroll 4
   for (int i = threadIdx.x; i < kRegTile; i += kRegThreads) {
     const int t = t0 + i;
     if (t >= N) break;
@@ -199,14 +221,42 @@ __global__ void __launch_bounds__(kRegThreads)
   __shared__ double sg[kRegTile + 2 * kRegHalo];  // 1[kbar != 0] dkbar
   const size_t base = (size_t)blockIdx.y * N;
   const int t0 = blockIdx.x * kRegTile;
-  for (int i = threadIdx.x; i < kRegTile + 2 * p; i += kRegThreads) {
-    const int t = t0 - p + i;
-    double g = 0.0;
-    if (t >= 0 && t < N && __ldg(kbar + base + t) != 0.f) g = (double)__ldg(dkbar + base + t);
-    sg[i] = g;
+  if ((N & 3) == 0 && t0 + kRegTile <= N) {
+    constexpr int V = kRegTile / (4 * kRegThreads);
+    const float4* kb = reinterpret_cast<const float4*>(kbar + base + t0);
+    const float4* dk = reinterpret_cast<const float4*>(dkbar + base + t0);
+    float4 a[V], g[V];
+#pragma unroll
+    for (int j = 0; j < V; ++j) {
+      a[j] = __ldg(kb + threadIdx.x + j * kRegThreads);
+      g[j] = __ldg(dk + threadIdx.x + j * kRegThreads);
+    }
+#pragma unroll
+    for (int j = 0; j < V; ++j) {
+      double* d = sg + p + 4 * (threadIdx.x + j * kRegThreads);
+      d[0] = a[j].x != 0.f ? (double)g[j].x : 0.0;
+      d[1] = a[j].y != 0.f ? (double)g[j].y : 0.0;
+      d[2] = a[j].z != 0.f ? (double)g[j].z : 0.0;
+      d[3] = a[j].w != 0.f ? (double)g[j].w : 0.0;
+    }
+    if ((int)threadIdx.x < 2 * p) {
+      const int i = threadIdx.x < (unsigned)p ? (int)threadIdx.x : kRegTile + (int)threadIdx.x;
+      const int t = t0 - p + i;
+      double gv = 0.0;
+      if (t >= 0 && t < N && __ldg(kbar + base + t) != 0.f) gv = (double)__ldg(dkbar + base + t);
+      sg[i] = gv;
+    }
+  } else {
+    for (int i = threadIdx.x; i < kRegTile + 2 * p; i += kRegThreads) {
+      const int t = t0 - p + i;
+      double gv = 0.0;
+      if (t >= 0 && t < N && __ldg(kbar + base + t) != 0.f) gv = (double)__ldg(dkbar + base + t);
+      sg[i] = gv;
+    }
   }
   __syncthreads();
   const double inv_w = 1.0 / (double)(2 * p + 1);
+#pragma unroll 4
   for (int i = threadIdx.x; i < kRegTile; i += kRegThreads) {
     const int t = t0 + i;
     if (t >= N) break;
