@@ -2259,8 +2259,13 @@ __global__ void __launch_bounds__(colc::kThreads, colc3::per_sm(M))
 #pragma unroll 1
         for (uint32_t j = tid; j < MH * 16; j += colc::kEpi) {
           const uint32_t al = j >> 4, a = part * MH + al, tc8 = (j & 15) * 8;
-          const uint4 v0 = *reinterpret_cast<const uint4*>(ws + al * 512 + tc8 * 4);
-          const uint4 v1 = *reinterpret_cast<const uint4*>(ws + al * 512 + tc8 * 4 + 16);
+          // half-chunk order alternates every 4 chunks so one load instruction
+          // covers all 8 16-byte bank groups (conflict-free 512 B per warp)
+          const uint32_t sel = (j >> 2) & 1;
+          const unsigned char* rp = ws + al * 512 + tc8 * 4;
+          const uint4 x0 = *reinterpret_cast<const uint4*>(rp + 16 * sel);
+          const uint4 x1 = *reinterpret_cast<const uint4*>(rp + 16 * (sel ^ 1));
+          const uint4 v0 = sel ? x1 : x0, v1 = sel ? x0 : x1;
           const uint32_t vv[8] = {v0.x, v0.y, v0.z, v0.w, v1.x, v1.y, v1.z, v1.w};
           float2 w = tw_two(tb, a * (tau0 + tc8));
           const float2 sp = tw_two(tb, a);
