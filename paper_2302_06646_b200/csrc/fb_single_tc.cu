@@ -2143,10 +2143,11 @@ int col1_launch(const fb_plan* p, const void* sig, void* x1, int64_t B, int64_t 
 // the B^-1 factor :101-122):  y[c l + tau] = sum_a w_m^(+a c) w_n^(+a tau) W[a][tau]
 // for the data rows c < m/2, channel b0 = Re, b1 = Im, plus D u.  The
 // twiddle sits on the contraction index, so the A operand is built by the
-// eight worker warps (TMA'd W tile [a][128 tau] -> x w_n^(+a tau) -> bf16
+// worker warps (TMA'd W tile [a][128 tau] -> x w_n^(+a tau) -> bf16
 // MN-major SW128, K = [re a | im a]); the inverse DFT_m is a K-major B
 // operand (N = m: [Re c | Im c]); the same warps then drain the previous
-// tile's accumulator (skip added, 16-bit stores).  Warp 8: TMA, warp 9: MMA.
+// tile's accumulator (skip added, 16-bit stores).  Warps 8 / 9 (16 / 17 with the
+// sixteen worker warps at m = 128) issue the TMA loads / the MMAs.
 namespace colc3 {
 constexpr int kStages = 2;
 constexpr int per_sm(int M) { return M == 32 ? 3 : (M == 64 ? 2 : 1); }
@@ -2154,15 +2155,19 @@ constexpr int per_sm(int M) { return M == 32 ? 3 : (M == 64 ? 2 : 1); }
 // buffers of 16 / 32 KB) accumulating into one TMEM tile, so the double
 // buffers fit (two CTAs per SM at m = 64)
 constexpr int half_a(int M) { return M == 32 ? 32 : M / 2; }
+// worker warps: 16 at m = 128 (one CTA per SM; the drain splits the rows c)
+constexpr uint32_t workers(int M) { return M == 128 ? 512 : 256; }
+constexpr uint32_t threads(int M) { return workers(M) + 64; }
 }  // namespace colc3
 
 template <typename IO, int M>
-__global__ void __launch_bounds__(colc::kThreads, colc3::per_sm(M))
+__global__ void __launch_bounds__(colc3::threads(M), colc3::per_sm(M))
     tc_col3_kernel(const __grid_constant__ CUtensorMap wmap, const IO* __restrict__ skip,
                    IO* __restrict__ out, const float* __restrict__ D, const float2* __restrict__ tb,
                    int B, int H, int ntiles) {
   constexpr uint32_t ROWS = M / 2, K = 2 * M, NN = M;
   constexpr uint32_t MH = colc3::half_a(M), SPLIT = M / MH, KC = 2 * MH;  // sub-tile: a-rows, K
+  constexpr uint32_t EPI = colc3::workers(M), RW = ROWS / (EPI / 256);     // drain rows per warp
   constexpr uint32_t WBYTES = MH * 128 * 4;       // W sub-tile [a][128 tau] complex bf16
   constexpr uint32_t ABYTES = 128 * KC * 2;       // A [tau / 64][k][64 tau], k = [re a | im a]
   constexpr uint32_t KBLK = NN * 128;
@@ -2179,7 +2184,7 @@ __global__ void __launch_bounds__(colc::kThreads, colc3::per_sm(M))
   const uint32_t tid = threadIdx.x, warp = tid >> 5;
 
   // inverse DFT_m, (n' = c' ROWS + c, k = [re a | im a])
-  for (uint32_t i = tid; i < NN * K; i += colc::kThreads) {
+  for (uint32_t i = tid; i < NN * K; i += EPI + 64) {
     const uint32_t np = i / K, k = i % K;
     const uint32_t cp = np / ROWS, c = np % ROWS, a = k % M, im = k / M;
     float sn, cs;
@@ -2190,13 +2195,13 @@ __global__ void __launch_bounds__(colc::kThreads, colc3::per_sm(M))
   if (tid == 0) {
     for (int s = 0; s < colc3::kStages; ++s) {
       ptx::mbar_init(&wfull[s], 1);
-      ptx::mbar_init(&wempty[s], colc::kEpi);
+      ptx::mbar_init(&wempty[s], EPI);
     }
     for (int b = 0; b < 2; ++b) {
-      ptx::mbar_init(&afull[b], colc::kEpi);
+      ptx::mbar_init(&afull[b], EPI);
       ptx::mbar_init(&afree[b], 1);
       ptx::mbar_init(&tfull[b], 1);
-      ptx::mbar_init(&tempty[b], colc::kEpi);
+      ptx::mbar_init(&tempty[b], EPI);
     }
     ptx::fence_barrier_init();
   }
@@ -2208,7 +2213,7 @@ __global__ void __launch_bounds__(colc::kThreads, colc3::per_sm(M))
   const uint32_t tmem = tmem_base;
   const int first = blockIdx.x, step = gridDim.x;
 
-  if (warp == 8) {  // TMA producer: W tiles
+  if (warp == EPI / 32) {  // TMA producer: W tiles
     if ((tid & 31) == 0) {
       int g = 0;
       for (int t = first; t < ntiles; t += step)
@@ -2220,7 +2225,7 @@ __global__ void __launch_bounds__(colc::kThreads, colc3::per_sm(M))
           tma_load_3d_sw(wring + s * WBYTES, &wmap, tbk * 128, (int)(part * MH), hp, &wfull[s]);
         }
     }
-  } else if (warp == 9) {  // MMA issuer
+  } else if (warp == EPI / 32 + 1) {  // MMA issuer
     if ((tid & 31) == 0) {
       const uint32_t id = idesc<__nv_bfloat16>(128, NN, true, false);
       const uint32_t sa = ptx::smem_u32(abuf), st = ptx::smem_u32(tabl);
@@ -2245,7 +2250,7 @@ __global__ void __launch_bounds__(colc::kThreads, colc3::per_sm(M))
       }
     }
   } else {  // workers
-    const uint32_t q = warp & 3, half = warp >> 2, lane = tid & 31;
+    const uint32_t q = warp & 3, half = (warp >> 2) & 1, c_lo = (warp >> 3) * RW, lane = tid & 31;
     int i = 0, g = 0, tprev = -1;
     for (int t = first;; t += step, ++i) {
       const bool have = t < ntiles;
@@ -2257,7 +2262,7 @@ __global__ void __launch_bounds__(colc::kThreads, colc3::per_sm(M))
         const unsigned char* ws = wring + s * WBYTES;
         unsigned char* ab = abuf + b * ABYTES;
 #pragma unroll 1
-        for (uint32_t j = tid; j < MH * 16; j += colc::kEpi) {
+        for (uint32_t j = tid; j < MH * 16; j += EPI) {
           const uint32_t al = j >> 4, a = part * MH + al, tc8 = (j & 15) * 8;
           // half-chunk order alternates every 4 chunks so one load instruction
           // covers all 8 16-byte bank groups (conflict-free 512 B per warp)
@@ -2286,13 +2291,14 @@ __global__ void __launch_bounds__(colc::kThreads, colc3::per_sm(M))
         mbar_arrive(&wempty[s]);
         mbar_arrive(&afull[b]);
       }
-      if (tprev >= 0) {  // drain tile i - 1: warps 0-3 channel b0 (Re), 4-7 b1 (Im)
+      if (tprev >= 0) {  // drain tile i - 1: warps w % 8 < 4 channel b0 (Re), else b1 (Im); w / 8 picks the rows
         const int ip = i - 1, b = ip & 1;
         const int tbk = tprev % NTB, h = (tprev / NTB) % H, pr = tprev / (NTB * H);
         const uint32_t tau = tbk * 128 + 32 * q + lane;
         const int bc = 2 * pr + (int)half;
         const bool live = bc < B;
-        const size_t o = ((size_t)bc * H + h) * (size_t)(ROWS * colc::kRowL) + tau;
+        const size_t o =
+            ((size_t)bc * H + h) * (size_t)(ROWS * colc::kRowL) + tau + (size_t)c_lo * colc::kRowL;
         // skip rows of the next chunk in flight while this one drains (the
         // first chunk's before the accumulator wait)
         IO sk[16];
@@ -2301,16 +2307,16 @@ __global__ void __launch_bounds__(colc::kThreads, colc3::per_sm(M))
         const float d = __ldg(D + h);
         ptx::mbar_wait(&tfull[b], (uint32_t)(ip / 2) & 1);
         tc::fence_after();
-        const uint32_t ta = tmem + ((32u * q) << 16) + b * NN + half * ROWS;
+        const uint32_t ta = tmem + ((32u * q) << 16) + b * NN + half * ROWS + c_lo;
 #pragma unroll 1
-        for (uint32_t c0 = 0; c0 < ROWS; c0 += 16) {
+        for (uint32_t c0 = 0; c0 < RW; c0 += 16) {
           float v[16];
           tld<16>(ta + c0, v);
           tc::ld_wait();
           float y[16];
 #pragma unroll
           for (int j = 0; j < 16; ++j) y[j] = fmaf(d, tof(sk[j]), v[j]);
-          if (c0 + 16 < ROWS) {
+          if (c0 + 16 < RW) {
 #pragma unroll
             for (int j = 0; j < 16; ++j)
               sk[j] = live ? skip[o + (size_t)(c0 + 16 + j) * colc::kRowL] : IO{};
@@ -2360,7 +2366,7 @@ int col3_launch(const fb_plan* p, const void* w, const void* skip, void* out, in
   auto k = tc_col3_kernel<IO, M>;
   cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   const int grid = std::max(1, std::min(ntiles, colc3::per_sm(M) * p->num_sms));
-  k<<<(unsigned)grid, colc::kThreads, smem, s>>>(map, (const IO*)skip, (IO*)out, p->d, p->tw_big, (int)B,
+  k<<<(unsigned)grid, colc3::threads(M), smem, s>>>(map, (const IO*)skip, (IO*)out, p->d, p->tw_big, (int)B,
                                                  (int)p->H, ntiles);
   return cuda_status(cudaGetLastError(), "tc_col3_kernel");
 }
