@@ -22,7 +22,8 @@ fb = pytest.importorskip("paper_2302_06646_b200")
 
 @pytest.mark.parametrize("N,dtype", [(12288, torch.float32), (10000, torch.bfloat16),
                                      (5000, torch.bfloat16), (20000, torch.float16),
-                                     (12288, torch.bfloat16)])
+                                     (12288, torch.bfloat16), (100000, torch.bfloat16),
+                                     (98304, torch.float16)])
 def test_three_pass_ragged_N(lc, N, dtype):
     B, H = 3, 2
     inp = layer_inputs(lc, B, H, N, dtype)
