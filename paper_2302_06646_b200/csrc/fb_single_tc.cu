@@ -2115,8 +2115,8 @@ int col1_launch(const fb_plan* p, const void* sig, void* x1, int64_t B, int64_t 
     set_error("tcgen05 pass 1: cuTensorMapEncodeTiled unavailable");
     return FB_ERR_CUDA;
   }
-  constexpr uint32_t ROWS = M / 2;
-  const cuuint64_t dims[3] = {colc::kRowL, ROWS, (cuuint64_t)(B * p->H)};
+  constexpr uint32_t ROWS = M / 2;  // box rows; data rows N / l <= ROWS (the rest zero-filled)
+  const cuuint64_t dims[3] = {colc::kRowL, (cuuint64_t)(p->N / colc::kRowL), (cuuint64_t)(B * p->H)};
   const cuuint64_t strides[2] = {colc::kRowL * 2, (cuuint64_t)p->N * 2};
   const cuuint32_t box[3] = {64, ROWS, 1};
   const cuuint32_t es[3] = {1, 1, 1};
@@ -2164,7 +2164,7 @@ template <typename IO, int M>
 __global__ void __launch_bounds__(colc3::threads(M), colc3::per_sm(M))
     tc_col3_kernel(const __grid_constant__ CUtensorMap wmap, const IO* __restrict__ skip,
                    IO* __restrict__ out, const float* __restrict__ D, const float2* __restrict__ tb,
-                   int B, int H, int ntiles) {
+                   int B, int H, int rows, int ntiles) {
   constexpr uint32_t ROWS = M / 2, K = 2 * M, NN = M;
   constexpr uint32_t MH = colc3::half_a(M), SPLIT = M / MH, KC = 2 * MH;  // sub-tile: a-rows, K
   constexpr uint32_t EPI = colc3::workers(M), RW = ROWS / (EPI / 256);     // drain rows per warp
@@ -2298,12 +2298,13 @@ __global__ void __launch_bounds__(colc3::threads(M), colc3::per_sm(M))
         const int bc = 2 * pr + (int)half;
         const bool live = bc < B;
         const size_t o =
-            ((size_t)bc * H + h) * (size_t)(ROWS * colc::kRowL) + tau + (size_t)c_lo * colc::kRowL;
+            ((size_t)bc * H + h) * ((size_t)rows * colc::kRowL) + tau + (size_t)c_lo * colc::kRowL;
+        const int nr = rows - (int)c_lo;  // data rows c < rows of this warp's range
         // skip rows of the next chunk in flight while this one drains (the
         // first chunk's before the accumulator wait)
         IO sk[16];
 #pragma unroll
-        for (int j = 0; j < 16; ++j) sk[j] = live ? skip[o + (size_t)j * colc::kRowL] : IO{};
+        for (int j = 0; j < 16; ++j) sk[j] = (live && j < nr) ? skip[o + (size_t)j * colc::kRowL] : IO{};
         const float d = __ldg(D + h);
         ptx::mbar_wait(&tfull[b], (uint32_t)(ip / 2) & 1);
         tc::fence_after();
@@ -2319,11 +2320,12 @@ __global__ void __launch_bounds__(colc3::threads(M), colc3::per_sm(M))
           if (c0 + 16 < RW) {
 #pragma unroll
             for (int j = 0; j < 16; ++j)
-              sk[j] = live ? skip[o + (size_t)(c0 + 16 + j) * colc::kRowL] : IO{};
+              sk[j] = (live && (int)(c0 + 16) + j < nr) ? skip[o + (size_t)(c0 + 16 + j) * colc::kRowL] : IO{};
           }
           if (live) {
 #pragma unroll
-            for (int j = 0; j < 16; ++j) out[o + (size_t)(c0 + j) * colc::kRowL] = cvt<IO>(y[j]);
+            for (int j = 0; j < 16; ++j)
+              if ((int)c0 + j < nr) out[o + (size_t)(c0 + j) * colc::kRowL] = cvt<IO>(y[j]);
           }
         }
         tc::fence_before();
@@ -2367,7 +2369,7 @@ int col3_launch(const fb_plan* p, const void* w, const void* skip, void* out, in
   cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   const int grid = std::max(1, std::min(ntiles, colc3::per_sm(M) * p->num_sms));
   k<<<(unsigned)grid, colc3::threads(M), smem, s>>>(map, (const IO*)skip, (IO*)out, p->d, p->tw_big, (int)B,
-                                                 (int)p->H, ntiles);
+                                                    (int)p->H, (int)(p->N / colc::kRowL), ntiles);
   return cuda_status(cudaGetLastError(), "tc_col3_kernel");
 }
 }  // namespace
@@ -2381,7 +2383,7 @@ int tc_col3(const fb_plan* p, const void* w, const void* skip, void* out, int64_
     return e && e[0] == '0';
   }();
   if (off || p->mode != FB_MODE_CAUSAL || p->l != colc::kRowL || p->N % colc::kRowL ||
-      p->m != 2 * (p->N / colc::kRowL) || (p->dtype != FB_BF16 && p->dtype != FB_F16))
+      p->N / colc::kRowL > p->m / 2 || (p->dtype != FB_BF16 && p->dtype != FB_F16))
     return FB_ERR_UNSUPPORTED;
   const bool bf = p->dtype == FB_BF16;
   switch (p->m) {
@@ -2404,7 +2406,7 @@ int tc_col1(const fb_plan* p, const void* sig, void* x1, int64_t B, int64_t npai
     return e && e[0] == '0';
   }();
   if (off || p->mode != FB_MODE_CAUSAL || p->l != colc::kRowL || p->N % colc::kRowL ||
-      p->m != 2 * (p->N / colc::kRowL) || (p->dtype != FB_BF16 && p->dtype != FB_F16))
+      p->N / colc::kRowL > p->m / 2 || (p->dtype != FB_BF16 && p->dtype != FB_F16))
     return FB_ERR_UNSUPPORTED;
   const bool bf = p->dtype == FB_BF16;
   switch (p->m) {
