@@ -102,8 +102,26 @@ namespace fb {
 // ---- zero-padded staging for causal three-pass plans with N % l != 0 ----
 // rows of `w` bytes with pitch `sp` -> rows of pitch `dp`, the tail of each
 // destination row (dp - w bytes) zeroed
+// 16-byte row copy: dst[r][j] = j < w16 ? src[r][j] : 0 for j < dw16 (one
+// streaming pass at HBM rate; the 2-D copy engine path ran at a fraction)
+__global__ void row_copy_kernel(uint4* __restrict__ dst, size_t dp16, const uint4* __restrict__ src,
+                                size_t sp16, size_t w16, size_t dw16) {
+  const size_t r = blockIdx.y;
+  const size_t j = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (j < dw16) dst[r * dp16 + j] = j < w16 ? __ldg(src + r * sp16 + j) : make_uint4(0, 0, 0, 0);
+}
+static bool row_copy(void* dst, size_t dp, const void* src, size_t sp, size_t w, size_t dw,
+                     size_t rows, cudaStream_t s) {
+  const bool ok = ((reinterpret_cast<uintptr_t>(dst) | reinterpret_cast<uintptr_t>(src) | dp | sp | w |
+                    dw) & 15) == 0 && rows > 0 && rows <= 65535;
+  if (!ok) return false;
+  const dim3 g((unsigned)((dw / 16 + 255) / 256), (unsigned)rows);
+  row_copy_kernel<<<g, 256, 0, s>>>((uint4*)dst, dp / 16, (const uint4*)src, sp / 16, w / 16, dw / 16);
+  return true;
+}
 static int pad_rows(void* dst, size_t dp, const void* src, size_t sp, size_t w, size_t rows,
                     cudaStream_t s) {
+  if (row_copy(dst, dp, src, sp, w, dp, rows, s)) return cuda_status(cudaGetLastError(), "pad copy");
   int rc = cuda_status(cudaMemcpy2DAsync(dst, dp, src, sp, w, rows, cudaMemcpyDeviceToDevice, s),
                        "pad copy");
   if (!rc && dp > w) rc = cuda_status(cudaMemset2DAsync((char*)dst + w, dp, 0, dp - w, rows, s),
@@ -112,6 +130,7 @@ static int pad_rows(void* dst, size_t dp, const void* src, size_t sp, size_t w, 
 }
 static int crop_rows(void* dst, size_t dp, const void* src, size_t sp, size_t w, size_t rows,
                      cudaStream_t s) {
+  if (row_copy(dst, dp, src, sp, w, w, rows, s)) return cuda_status(cudaGetLastError(), "crop copy");
   return cuda_status(cudaMemcpy2DAsync(dst, dp, src, sp, w, rows, cudaMemcpyDeviceToDevice, s),
                      "crop copy");
 }
